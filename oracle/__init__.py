@@ -1,0 +1,196 @@
+"""CPU oracle for the HybridServe cascade router -- TEST INFRASTRUCTURE ONLY.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s ``cpu_baseline``
+/ ``--impl reference`` legs may import this package.  The product package
+``paper_2505_12566_b200`` never imports it; the two share no code.
+
+The arithmetic lives in ``hs_oracle.c`` (plain C, fp64, Neumaier sums); this
+module only marshals numpy arrays into it and derives the per-stage lists of
+the cascade statement with ``numpy.flatnonzero``.  Citations are
+PAPER.md line numbers (``P:<n>``); readings are listed in DESIGN.md.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+import threading
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "hs_oracle.c")
+_LIB = os.path.join(_HERE, "libhs_oracle.so")
+_lock = threading.Lock()
+_lib = None
+
+F32, BF16 = 0, 1
+MAXPROB, MAXPROB_SQ, ENTROPY = 0, 1, 2
+SEQ_NONE, SEQ_MIN, SEQ_MEAN = 0, 1, 2
+
+_P = ctypes.c_void_p
+_I64 = ctypes.c_int64
+
+
+def build(force: bool = False) -> str:
+    """Compile hs_oracle.c with gcc (plain -O2, IEEE semantics, no fast-math)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = _LIB + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", "-O2", "-std=c11", "-fPIC", "-shared", "-o", tmp, _SRC,
+                               "-lm", "-lpthread"])
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+def lib():
+    global _lib
+    with _lock:
+        if _lib is None:
+            L = ctypes.CDLL(build())
+            L.hso_row_stats.argtypes = [_P, _I64, ctypes.c_double, _P, _P, _P]
+            L.hso_row_stats.restype = ctypes.c_int
+            L.hso_confidence.argtypes = [_P, ctypes.c_int, _I64, ctypes.c_int, _I64, _I64, _P,
+                                         ctypes.c_double, ctypes.c_int, ctypes.c_int,
+                                         _P, _P, _P, _P, _P, ctypes.c_int]
+            L.hso_confidence.restype = ctypes.c_int
+            L.hso_route.argtypes = [_P, _I64, ctypes.c_double, ctypes.c_int, _P, _P, _P, _P]
+            L.hso_route.restype = None
+            L.hso_cascade.argtypes = [ctypes.c_int, _I64, _P, _P, _P]
+            L.hso_cascade.restype = None
+            L.hso_calibrate.argtypes = [ctypes.c_int, _I64, _P, _P, ctypes.c_int, _I64,
+                                        ctypes.c_int, _P, _P, _P, _P, _P]
+            L.hso_calibrate.restype = ctypes.c_int
+            _lib = L
+    return _lib
+
+
+def _ptr(a):
+    return None if a is None else a.ctypes.data_as(ctypes.c_void_p)
+
+
+def default_threads() -> int:
+    return max(1, os.cpu_count() or 1)
+
+
+# --------------------------------------------------------------------------
+# D1: one row.  P:373-391 (temperature-scaled softmax).
+# --------------------------------------------------------------------------
+def row_stats(x, T: float = 1.0):
+    """(p_max, H [nats], argmax) of one logits row in fp64; None if invalid."""
+    x = np.ascontiguousarray(np.asarray(x, dtype=np.float64))
+    p = ctypes.c_double()
+    h = ctypes.c_double()
+    a = ctypes.c_int64()
+    rc = lib().hso_row_stats(_ptr(x), x.size, float(T), ctypes.byref(p), ctypes.byref(h),
+                             ctypes.byref(a))
+    if rc != 0:
+        return None
+    return p.value, h.value, a.value
+
+
+# --------------------------------------------------------------------------
+# D1 + D2 batched.  P:413-430.
+# --------------------------------------------------------------------------
+def confidence(logits: np.ndarray, n_seq: int, seq_len: int, n_classes: int, row_stride: int,
+               temperature: float, kind: int = MAXPROB, reduce: int = SEQ_NONE,
+               row_index=None, labels=None, nthreads: int | None = None):
+    """Per-item confidence of a batch of logits rows.
+
+    ``logits``: a flat float32 array, or a uint16 array of raw bf16 bits.
+    Returns dict(conf f64[n], argmax i32[n*L], correct u8[n] or None, bad u8[n]).
+    """
+    flat = np.ascontiguousarray(logits).reshape(-1)
+    if flat.dtype == np.float32:
+        dtype = F32
+    elif flat.dtype == np.uint16:
+        dtype = BF16
+    else:
+        raise TypeError("oracle takes float32 or raw-bf16 (uint16) logits")
+    n_seq = int(n_seq)
+    conf = np.empty(n_seq, np.float64)
+    argmax = np.empty(n_seq * seq_len, np.int32)
+    bad = np.empty(n_seq, np.uint8)
+    ri = None if row_index is None else np.ascontiguousarray(row_index, dtype=np.int64)
+    lab = None if labels is None else np.ascontiguousarray(labels, dtype=np.int32)
+    correct = np.empty(n_seq, np.uint8) if lab is not None else None
+    rc = lib().hso_confidence(_ptr(flat), dtype, n_seq, int(seq_len), int(n_classes),
+                              int(row_stride), _ptr(ri), float(temperature), int(kind),
+                              int(reduce), _ptr(conf), _ptr(argmax), _ptr(lab), _ptr(correct),
+                              _ptr(bad), int(nthreads or default_threads()))
+    if rc != 0:
+        raise ValueError("oracle: invalid argument")
+    return {"conf": conf, "argmax": argmax, "correct": correct, "bad": bad}
+
+
+# --------------------------------------------------------------------------
+# D3/D4.  P:443-444.
+# --------------------------------------------------------------------------
+def route(conf: np.ndarray, threshold: float, is_last: bool):
+    """Stable split of one stage's batch: (accepted positions, deferred positions)."""
+    c = np.ascontiguousarray(conf, dtype=np.float64)
+    n = c.size
+    acc = np.empty(n, np.int64)
+    dfr = np.empty(n, np.int64)
+    na = ctypes.c_int64()
+    nd = ctypes.c_int64()
+    lib().hso_route(_ptr(c), n, float(threshold), int(bool(is_last)), _ptr(acc),
+                    ctypes.byref(na), _ptr(dfr), ctypes.byref(nd))
+    return acc[: na.value].copy(), dfr[: nd.value].copy()
+
+
+def cascade(conf_by_stage: np.ndarray, thresholds) -> np.ndarray:
+    """stage(r) for every request: conf_by_stage[k, r]; thresholds t[0..K-1]."""
+    c = np.ascontiguousarray(conf_by_stage, dtype=np.float64)
+    K, n = c.shape
+    t = np.ascontiguousarray(np.asarray(thresholds, dtype=np.float64).reshape(-1)[:K])
+    if t.size < K:
+        t = np.concatenate([t, np.zeros(K - t.size)])
+    out = np.empty(n, np.int32)
+    lib().hso_cascade(int(K), int(n), _ptr(c), _ptr(t), _ptr(out))
+    return out
+
+
+def stage_lists(stage_of: np.ndarray, K: int):
+    """Per-stage (batch, accepted, deferred) request lists, increasing order (D4)."""
+    out = []
+    for k in range(K):
+        out.append((np.flatnonzero(stage_of >= k), np.flatnonzero(stage_of == k),
+                    np.flatnonzero(stage_of > k)))
+    return out
+
+
+# --------------------------------------------------------------------------
+# D5 calibration.  P:457-489 (Alg. 1, AP mode); exact sweep of SURVEY 8(c).
+# --------------------------------------------------------------------------
+def calibrate(conf: np.ndarray, correct: np.ndarray, log2_bins: int = 12, target: int = -1,
+              refine_passes: int = 0):
+    """conf[K-1, N] (fp64 or fp32), correct[K, N] (0/1) -> dict of b, t, reach, ..."""
+    c = np.ascontiguousarray(conf, dtype=np.float64)
+    ok = np.ascontiguousarray(correct, dtype=np.uint8)
+    K = ok.shape[0]
+    N = ok.shape[1]
+    assert c.shape == (K - 1, N)
+    b = np.empty(K - 1, np.int32)
+    reach = np.empty(K, np.int64)
+    handled = np.empty(K, np.int64)
+    A = ctypes.c_int64()
+    tau = ctypes.c_int64()
+    rc = lib().hso_calibrate(int(K), int(N), _ptr(c), _ptr(ok), int(log2_bins), int(target),
+                             int(refine_passes), _ptr(b), _ptr(reach), _ptr(handled),
+                             ctypes.byref(A), ctypes.byref(tau))
+    if rc != 0:
+        raise ValueError("oracle: invalid calibration argument")
+    B = 1 << log2_bins
+    t = [float("inf") if int(x) == B + 1 else int(x) / B for x in b] + [0.0]
+    return {"b": b, "t": np.array(t, np.float64), "reach": reach, "handled": handled,
+            "correct_total": A.value, "tau": tau.value}
+
+
+def bin_index(c, log2_bins: int):
+    """bin(c) = min(B, floor(c * B)); NaN -> -1.  (D5 grid, reading G10.)"""
+    B = 1 << log2_bins
+    c = np.asarray(c, dtype=np.float64)
+    out = np.floor(c * B)
+    out = np.clip(out, 0, B)
+    out = np.where(np.isnan(c), -1, out)
+    return out.astype(np.int64)

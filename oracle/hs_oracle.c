@@ -1,0 +1,331 @@
+/*
+ * oracle/hs_oracle.c -- the CPU ORACLE for the HybridServe cascade router.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and the
+ * cpu_baseline / --impl reference legs of bench.py may load this library.
+ * The product path (paper_2505_12566_b200/) never links, imports or calls it,
+ * and this file shares no code, header, table or constant with csrc/.
+ *
+ * Plain, slow, obviously-correct C: fp64 arithmetic, plain loops, Neumaier
+ * (compensated) summation, qsort as the only library primitive.  Each
+ * function cites the passage of /root/reference/PAPER.md ("P:<line>") it
+ * follows, and the reading taken where the paper is garbled (DESIGN.md
+ * "Readings", mirrored from SURVEY.md 8(c) G1..G18).
+ *
+ * Parity status: every function below is pinned by tests/test_oracle_*.py
+ * (closed forms, library special cases, hand-worked cascades, brute force).
+ * Nothing here is "parity unpinned".
+ */
+#include <math.h>
+#include <pthread.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+/* ------------------------------------------------------------------------- */
+/* enums: the oracle's own numbering (tests pass plain ints)                 */
+/* ------------------------------------------------------------------------- */
+enum { ORC_F32 = 0, ORC_BF16 = 1 };
+enum { ORC_MAXPROB = 0, ORC_MAXPROB_SQ = 1, ORC_ENTROPY = 2 };
+enum { ORC_SEQ_NONE = 0, ORC_SEQ_MIN = 1, ORC_SEQ_MEAN = 2 };
+
+/* Exact widening of one stored logit to double (bf16 = top 16 bits of an
+ * IEEE binary32; every bf16 and every fp32 value is exactly a double). */
+static double load_logit(const void* base, int dtype, int64_t idx) {
+    float f;
+    if (dtype == ORC_BF16) {
+        uint32_t u = ((uint32_t)((const uint16_t*)base)[idx]) << 16;
+        memcpy(&f, &u, sizeof f);
+    } else {
+        f = ((const float*)base)[idx];
+    }
+    return (double)f;
+}
+
+/* Neumaier compensated summation (plain definition of a sum, with the
+ * rounding error carried so that the fp64 result is ~exact). */
+typedef struct { double s, c; } nsum_t;
+static void nsum_add(nsum_t* a, double v) {
+    double t = a->s + v;
+    if (fabs(a->s) >= fabs(v)) a->c += (a->s - t) + v;
+    else                       a->c += (v - t) + a->s;
+    a->s = t;
+}
+static double nsum_get(const nsum_t* a) { return a->s + a->c; }
+
+/* ------------------------------------------------------------------------- */
+/* D1. Row confidence statistics.                                            */
+/*   P:384-391 (f_theta maps a prediction vector of logits to a score),      */
+/*   P:373-375 (Temperature Scaling: theta is a temperature, z = x / T),     */
+/*   P:413-416 (classification: max of the softmax, squared -- reading G1).  */
+/* Returns 0 on success, 1 if the row is not a valid prediction vector      */
+/* (a NaN or +inf entry, or every entry -inf; S:122 requires finite input;  */
+/* -inf is accepted as a masked class with p = 0 and entropy term 0).       */
+/* ------------------------------------------------------------------------- */
+int hso_row_stats(const double* x, int64_t C, double T,
+                  double* p_max, double* entropy, int64_t* argmax) {
+    /* step 2: reject non-finite rows */
+    int64_t n_finite = 0;
+    for (int64_t j = 0; j < C; ++j) {
+        if (isnan(x[j]) || (isinf(x[j]) && x[j] > 0)) return 1;
+        if (!isinf(x[j])) ++n_finite;
+    }
+    if (n_finite == 0) return 1;
+    /* step 3: mx = max_j x_j, j* = lowest index attaining it (reading G12) */
+    double mx = x[0];
+    int64_t jstar = 0;
+    for (int64_t j = 1; j < C; ++j)
+        if (x[j] > mx) { mx = x[j]; jstar = j; }
+    /* step 4-5: a_j = (x_j - mx) / T; s = sum exp(a_j); w = sum exp(a_j) a_j */
+    nsum_t s = {0, 0}, w = {0, 0};
+    for (int64_t j = 0; j < C; ++j) {
+        if (isinf(x[j])) continue;                 /* masked class: p_j = 0 */
+        double a = (x[j] - mx) / T;
+        double e = exp(a);
+        nsum_add(&s, e);
+        nsum_add(&w, e * a);
+    }
+    double S = nsum_get(&s), W = nsum_get(&w);
+    /* step 6: p_max = exp(0)/s = 1/s ; H = -sum p_j ln p_j = ln s - w/s */
+    *p_max = 1.0 / S;
+    *entropy = log(S) - W / S;
+    *argmax = jstar;
+    return 0;
+}
+
+/* step 7: the confidence of one row from its statistics.
+ *   MAXPROB    : p_max                      (north_star; reading G1)
+ *   MAXPROB_SQ : p_max^2                    (P:415 taken literally, G1)
+ *   ENTROPY    : exp(-H) = 1/perplexity     (north_star; reading G3)      */
+static double conf_of(int kind, double p_max, double H) {
+    if (kind == ORC_MAXPROB_SQ) return p_max * p_max;
+    if (kind == ORC_ENTROPY) return exp(-H);
+    return p_max;
+}
+
+/* ------------------------------------------------------------------------- */
+/* D1 + D2 batched: per-sequence confidence.                                 */
+/*   P:420-424 (generation: "the minimal confidence is the confidence of     */
+/*   complete output" -> MIN over the L token confidences; MEAN is the       */
+/*   north_star's alternative), P:427-430 (QA = MIN with L = 2).             */
+/* Batch item i reads sequence r = row_index ? row_index[i] : i; its token  */
+/* t is the logits row r*L + t at element offset (r*L + t) * stride.        */
+/* Outputs per item: conf, argmax[i*L + t], correct (all L tokens equal     */
+/* their labels[r*L + t]; reading G13), bad (1 = invalid row seen).         */
+/* ------------------------------------------------------------------------- */
+typedef struct {
+    const void* logits; int dtype; int64_t n_seq; int L; int64_t C; int64_t stride;
+    const int64_t* row_index; double T; int kind; int reduce;
+    double* conf; int32_t* argmax; const int32_t* labels; uint8_t* correct; uint8_t* bad;
+    int64_t lo, hi;
+} conf_job_t;
+
+static void* conf_worker(void* arg) {
+    conf_job_t* J = (conf_job_t*)arg;
+    double* row = (double*)malloc(sizeof(double) * (size_t)J->C);
+    for (int64_t i = J->lo; i < J->hi; ++i) {
+        int64_t r = J->row_index ? J->row_index[i] : i;
+        double cmin = INFINITY;
+        nsum_t csum = {0, 0};
+        int all_correct = 1, any_bad = 0;
+        for (int t = 0; t < J->L; ++t) {
+            int64_t tok = r * J->L + t;
+            for (int64_t j = 0; j < J->C; ++j)
+                row[j] = load_logit(J->logits, J->dtype, tok * J->stride + j);
+            double p, H; int64_t am;
+            if (hso_row_stats(row, J->C, J->T, &p, &H, &am) != 0) {
+                any_bad = 1; am = -1; p = NAN; H = NAN;
+            }
+            double c = conf_of(J->kind, p, H);
+            if (c < cmin || isnan(c)) cmin = c;
+            nsum_add(&csum, c);
+            if (J->argmax) J->argmax[i * J->L + t] = (int32_t)am;
+            if (J->labels && am != (int64_t)J->labels[tok]) all_correct = 0;
+        }
+        double cs;
+        if (any_bad)                          cs = NAN;
+        else if (J->reduce == ORC_SEQ_MEAN)   cs = nsum_get(&csum) / (double)J->L;
+        else                                  cs = cmin;   /* MIN, or NONE with L == 1 */
+        J->conf[i] = cs;
+        if (J->correct) J->correct[i] = (uint8_t)(J->labels ? all_correct : 0);
+        if (J->bad) J->bad[i] = (uint8_t)any_bad;
+    }
+    free(row);
+    return NULL;
+}
+
+/* Returns 0, or -1 on an argument error (C < 2, T <= 0 or non-finite,
+ * L < 1, NONE with L > 1, stride < C). */
+int hso_confidence(const void* logits, int dtype, int64_t n_seq, int L, int64_t C,
+                   int64_t stride, const int64_t* row_index, double T, int kind, int reduce,
+                   double* conf, int32_t* argmax, const int32_t* labels, uint8_t* correct,
+                   uint8_t* bad, int nthreads) {
+    if (C < 2 || !(T > 0) || isinf(T) || L < 1 || stride < C || n_seq < 0) return -1;
+    if (reduce == ORC_SEQ_NONE && L != 1) return -1;
+    if (nthreads < 1) nthreads = 1;
+    if (n_seq < nthreads) nthreads = n_seq > 0 ? (int)n_seq : 1;
+    conf_job_t* jobs = (conf_job_t*)calloc((size_t)nthreads, sizeof(conf_job_t));
+    pthread_t* th = (pthread_t*)calloc((size_t)nthreads, sizeof(pthread_t));
+    for (int w = 0; w < nthreads; ++w) {
+        conf_job_t J = {logits, dtype, n_seq, L, C, stride, row_index, T, kind, reduce,
+                        conf, argmax, labels, correct, bad,
+                        n_seq * w / nthreads, n_seq * (w + 1) / nthreads};
+        jobs[w] = J;
+        pthread_create(&th[w], NULL, conf_worker, &jobs[w]);
+    }
+    for (int w = 0; w < nthreads; ++w) pthread_join(th[w], NULL);
+    free(jobs); free(th);
+    return 0;
+}
+
+/* ------------------------------------------------------------------------- */
+/* D3 + D4. Threshold test and stable split of one stage's batch.            */
+/*   "requests with scores below a threshold at a model in the    */
+/*   dataflow are passed to larger models" -> defer iff c < t, accept iff    */
+/*   c >= t (tie accepts, G5); the last model accepts everything (t_K = 0,   */
+/*   Table III P:816/826/835, G6).  Lists hold batch positions in            */
+/*   increasing order (stable).                                              */
+/* ------------------------------------------------------------------------- */
+void hso_route(const double* conf, int64_t n, double t, int is_last,
+               int64_t* acc, int64_t* n_acc, int64_t* dfr, int64_t* n_dfr) {
+    int64_t na = 0, nd = 0;
+    for (int64_t i = 0; i < n; ++i) {
+        int accept = is_last ? 1 : (conf[i] >= t);
+        if (accept) acc[na++] = i;
+        else        dfr[nd++] = i;
+    }
+    *n_acc = na;
+    *n_dfr = nd;
+}
+
+/* D4 per request: stage(r) = first k with c_k(r) >= t_k, else the last.
+ * conf[k * n + r] is stage k's confidence for request r (k = 0..K-1). */
+void hso_cascade(int K, int64_t n, const double* conf, const double* t, int32_t* stage_of) {
+    for (int64_t r = 0; r < n; ++r) {
+        int k = 0;
+        while (k < K - 1 && !(conf[(int64_t)k * n + r] >= t[k])) ++k;
+        stage_of[r] = k;
+    }
+}
+
+/* ------------------------------------------------------------------------- */
+/* D5. Offline threshold calibration (Accuracy-Preserving mode).             */
+/*   P:457-479 Alg. 1 (threshold search; replaced by the north_star's exact  */
+/*   deterministic sweep, reading G8), P:483-484 (AP: accuracy of the        */
+/*   cascade equal to Acc(m_n), read as ">= tau" in integer counts, G9),     */
+/*   P:441 ("exhaustively find the most energy-saving thresholds").          */
+/* Grid: B = 2^q bins, bin(c) = min(B, floor(c * B)), NaN -> -1 (never        */
+/* accepted).  Threshold index b in 0..B+1: t = b/B, b = B+1 = defer all     */
+/* (G10, G11).  This implementation sorts the alive samples by bin and takes */
+/* suffix sums ("by sort"); tests/ pins it against a simulation brute force. */
+/* ------------------------------------------------------------------------- */
+static int64_t bin_of(double c, int64_t B) {
+    if (isnan(c)) return -1;
+    double f = floor(c * (double)B);
+    if (f < 0) f = 0;
+    if (f > (double)B) f = (double)B;
+    return (int64_t)f;
+}
+
+typedef struct { int64_t bin; int64_t d; int64_t ck; } cal_item_t;
+static int cmp_bin(const void* a, const void* b) {
+    int64_t x = ((const cal_item_t*)a)->bin, y = ((const cal_item_t*)b)->bin;
+    return (x > y) - (x < y);
+}
+
+/* Among `m` alive items with weight d (the gain of answering here instead of
+ * deeper), return the smallest b in 0..B+1 with base + S(b) >= tau where
+ * S(b) = sum of d over items with bin >= b.  S is not monotone in b, so
+ * every b is examined in increasing order. */
+static int64_t select_min_b(cal_item_t* it, int64_t m, int64_t B, int64_t base, int64_t tau) {
+    qsort(it, (size_t)m, sizeof(cal_item_t), cmp_bin);
+    int64_t total = 0;
+    for (int64_t i = 0; i < m; ++i) if (it[i].bin >= 0) total += it[i].d;
+    int64_t below = 0;   /* sum of d over items with 0 <= bin < b */
+    int64_t p = 0;
+    while (p < m && it[p].bin < 0) ++p;
+    for (int64_t b = 0; b <= B + 1; ++b) {
+        while (p < m && it[p].bin < b) { below += it[p].d; ++p; }
+        int64_t S = total - below;
+        if (base + S >= tau) return b;
+    }
+    return B + 1;   /* unreachable when base >= tau (S(B+1) = 0) */
+}
+
+/* conf[k*N + r], k = 0..K-2 (stage K has no threshold); correct[k*N + r],
+ * k = 0..K-1.  tau < 0 selects AP: tau = sum_r correct[K-1][r].
+ * Outputs: b[K-1], reach[K], handled[K], *A_out (cascade correct count),
+ * *tau_out.  Returns 0, or -1 on argument error. */
+int hso_calibrate(int K, int64_t N, const double* conf, const uint8_t* correct, int q,
+                  int64_t tau, int refine_passes, int32_t* b_out, int64_t* reach,
+                  int64_t* handled, int64_t* A_out, int64_t* tau_out) {
+    if (K < 2 || N <= 0 || q < 1 || q > 20) return -1;
+    const int64_t B = (int64_t)1 << q;
+    const uint8_t* cK = correct + (int64_t)(K - 1) * N;
+    if (tau < 0) { tau = 0; for (int64_t r = 0; r < N; ++r) tau += cK[r]; }
+    *tau_out = tau;
+
+    int64_t* bins = (int64_t*)malloc(sizeof(int64_t) * (size_t)(K - 1) * (size_t)N);
+    for (int64_t k = 0; k < K - 1; ++k)
+        for (int64_t r = 0; r < N; ++r) bins[k * N + r] = bin_of(conf[k * N + r], B);
+    uint8_t* alive = (uint8_t*)malloc((size_t)N);
+    cal_item_t* it = (cal_item_t*)malloc(sizeof(cal_item_t) * (size_t)N);
+
+    /* forward greedy pass */
+    for (int64_t r = 0; r < N; ++r) alive[r] = 1;
+    int64_t A = 0;
+    for (int k = 0; k < K - 1; ++k) {
+        const uint8_t* ck = correct + (int64_t)k * N;
+        int64_t m = 0, G = 0;
+        for (int64_t r = 0; r < N; ++r) {
+            if (!alive[r]) continue;
+            G += cK[r];
+            cal_item_t x = {bins[k * N + r], (int64_t)ck[r] - (int64_t)cK[r], ck[r]};
+            it[m++] = x;
+        }
+        int64_t b = select_min_b(it, m, B, A + G, tau);
+        b_out[k] = (int32_t)b;
+        for (int64_t r = 0; r < N; ++r)
+            if (alive[r] && bins[k * N + r] >= b) { A += ck[r]; alive[r] = 0; }
+    }
+
+    /* optional refinement passes: re-pick each b_k given the
+     * current downstream thresholds; never raises b_k. */
+    for (int pass = 0; pass < refine_passes; ++pass) {
+        int changed = 0;
+        for (int k = 0; k < K - 1; ++k) {
+            const uint8_t* ck = correct + (int64_t)k * N;
+            int64_t Ak = 0, m = 0, Cdown = 0;
+            for (int64_t r = 0; r < N; ++r) {
+                /* replay stages < k under the current thresholds */
+                int j = 0;
+                while (j < k && bins[(int64_t)j * N + r] < b_out[j]) ++j;
+                if (j < k) { Ak += correct[(int64_t)j * N + r]; continue; }
+                /* downstream correctness C_{k+1}(r) */
+                int d = k + 1;
+                while (d < K - 1 && bins[(int64_t)d * N + r] < b_out[d]) ++d;
+                int64_t Cd = correct[(int64_t)d * N + r];
+                Cdown += Cd;
+                cal_item_t x = {bins[k * N + r], (int64_t)ck[r] - Cd, ck[r]};
+                it[m++] = x;
+            }
+            int64_t b = select_min_b(it, m, B, Ak + Cdown, tau);
+            if (b != b_out[k]) { b_out[k] = (int32_t)b; changed = 1; }
+        }
+        if (!changed) break;
+    }
+
+    /* final replay under the chosen thresholds: reach, handled, A */
+    for (int k = 0; k < K; ++k) { reach[k] = 0; handled[k] = 0; }
+    A = 0;
+    for (int64_t r = 0; r < N; ++r) {
+        int j = 0;
+        reach[0] += 1;
+        while (j < K - 1 && bins[(int64_t)j * N + r] < b_out[j]) { ++j; reach[j] += 1; }
+        handled[j] += 1;
+        A += correct[(int64_t)j * N + r];
+    }
+    *A_out = A;
+    free(bins); free(alive); free(it);
+    return 0;
+}
