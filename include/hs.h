@@ -1,0 +1,209 @@
+/*
+ * include/hs.h -- C-ABI of libhs.so, the B200 (sm_100a) HybridServe cascade router.
+ *
+ * The library implements the data-parallel hot path of HybridServe (arXiv
+ * 2505.12566): per-request confidence from a stage model's logits, the
+ * threshold test, stable compaction + gather of the deferred requests into the
+ * next stage's batch, and offline Accuracy-Preserving threshold calibration.
+ * Citations "P:<n>" are line numbers of the paper's text; the
+ * readings taken where the paper is garbled are listed in DESIGN.md.
+ *
+ * Conventions (all entry points):
+ *  - Pointers are DEVICE pointers unless marked "host".  The caller owns every
+ *    buffer; the library never allocates device memory and never synchronises
+ *    the device or the stream.  Every data call is asynchronous and ordered on
+ *    the given CUDA stream; passing 0 selects the legacy default stream.
+ *  - Argument errors are detected on the host before any launch and leave all
+ *    outputs untouched (HS_ERR_INVALID_ARGUMENT).  hs_last_error() returns a
+ *    thread-local detail string for the most recent failure.
+ *  - Data errors (a NaN or +inf logit, or a row whose entries are all -inf;
+ *    the paper's prediction vectors are finite probabilities) cannot be
+ *    known at return time: the kernel ORs bit 0 (HS_STATUS_NONFINITE) into
+ *    *d_status (optional device word) and writes conf = NaN, argmax = -1 for
+ *    that row.  A NaN confidence is deferred at every stage but the last.
+ *    -inf is accepted as a masked class (probability 0).
+ *  - Counts that size later work may live on the device ("d_n" arguments):
+ *    when non-NULL, the kernels read the actual item count from *d_n (which
+ *    must be <= the host capacity argument).  This lets a whole K-stage
+ *    cascade run without a host round trip and be captured in a CUDA graph.
+ *  - Alignment: logits base and row_stride * element size must be multiples of
+ *    16 bytes (128-bit vector loads); payload rows likewise.
+ *  - Determinism: outputs are bitwise identical run to run (fixed reduction
+ *    trees, integer histograms, stable compaction).
+ *  - Reentrancy: calls are reentrant; a workspace must not be shared by two
+ *    calls that may be in flight at the same time.
+ */
+#ifndef HS_H_
+#define HS_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* hs_stream_t; /* == cudaStream_t */
+
+typedef enum {
+  HS_OK = 0,
+  HS_ERR_INVALID_ARGUMENT = 1,
+  HS_ERR_NONFINITE_INPUT = 2, /* reserved for host-side checks of d_status */
+  HS_ERR_CUDA = 3,
+  HS_ERR_WORKSPACE_TOO_SMALL = 5,
+  HS_ERR_UNSUPPORTED = 6
+} hs_status_t;
+
+typedef enum { HS_F32 = 0, HS_BF16 = 1 } hs_dtype_t;
+
+/* Confidence score f_theta(P) of one prediction vector, z = x / T (Temperature
+ * Scaling; Eq. 1 P:384-389 fits T offline):
+ *   MAXPROB    c = max_j softmax(z)_j             (north_star; reading G1 of P:415)
+ *   MAXPROB_SQ c = (max_j softmax(z)_j)^2         ("max(theta(P)^2)" taken literally)
+ *   ENTROPY    c = exp(-H), H = -sum_j p_j ln p_j (north_star; 1/perplexity, reading G3) */
+typedef enum { HS_CONF_MAXPROB = 0, HS_CONF_MAXPROB_SQ = 1, HS_CONF_ENTROPY = 2 } hs_conf_kind_t;
+
+/* Token -> sequence reduction for generation models ("the minimal
+ * confidence is the confidence of complete output"); QA is MIN with L = 2
+ * (P:427-430).  NONE requires seq_len == 1. */
+typedef enum { HS_SEQ_NONE = 0, HS_SEQ_MIN = 1, HS_SEQ_MEAN = 2 } hs_seq_reduce_t;
+
+#define HS_STATUS_NONFINITE 1u
+
+/* ------------------------------------------------------------------------ */
+/* Confidence.                                        */
+/* ------------------------------------------------------------------------ */
+/* Batch item i (0 <= i < n) reads sequence r = row_index ? row_index[i] : i;
+ * its token t (0 <= t < seq_len) is the logits row r*seq_len + t, starting at
+ * element (r*seq_len + t) * row_stride of `logits` ([rows x row_stride],
+ * row-major, dtype elements, n_classes >= 2 valid entries per row).
+ * Outputs (per batch item):
+ *   conf[i]                    fp32 confidence (sequence-reduced when seq_len > 1)
+ *   argmax[i*seq_len + t]      int32 predicted class per token, lowest index on
+ *                              ties (optional, may be NULL)
+ *   correct[i]                 1 iff argmax == labels[r*seq_len + t] for all t
+ *                              (optional; requires labels, int32 indexed like
+ *                              the logits rows)
+ * Workspace: hs_confidence_workspace(n, seq_len) bytes (0 when seq_len == 1).
+ * temperature: > 0 and finite.  Errors: INVALID_ARGUMENT (n_classes < 2,
+ * seq_len < 1, NONE with seq_len > 1, bad T, stride < n_classes, misaligned),
+ * WORKSPACE_TOO_SMALL, CUDA (launch failure). */
+size_t hs_confidence_workspace(int64_t n, int32_t seq_len);
+hs_status_t hs_confidence(const void* logits, hs_dtype_t dtype, int64_t n, int32_t seq_len,
+                          int64_t n_classes, int64_t row_stride, const int64_t* row_index,
+                          const int64_t* d_n, float temperature, hs_conf_kind_t kind,
+                          hs_seq_reduce_t reduce, float* conf, int32_t* argmax,
+                          const int32_t* labels, uint8_t* correct, void* ws, size_t ws_bytes,
+                          uint32_t* d_status, hs_stream_t stream);
+
+/* ------------------------------------------------------------------------ */
+/* Threshold test + stable compaction + gather.       */
+/* ------------------------------------------------------------------------ */
+/* Item i (0 <= i < n, or *d_n) is ACCEPTED iff is_last || conf[i] >= threshold
+ * ("requests with scores below a threshold ... are passed to larger models",
+ * P:444; ties accept; the last model answers everything, t_K = 0, Table III),
+ * otherwise DEFERRED.  threshold must be in [0,1] or +inf ("defer all").
+ * Both lists are stable (increasing i):
+ *   acc_ids[j]   = ids ? ids[i] : i        for the j-th accepted item (optional)
+ *   acc_conf[j]  = conf[i]                                             (optional)
+ *   acc_pred[j*pred_len + t] = pred[i*pred_len + t]                    (optional)
+ *   def_ids[j]   = ids ? ids[i] : i        for the j-th deferred item  (optional)
+ *   def_pos[j]   = i                                                   (optional)
+ *   def_payload[j*P .. +P) = payload[i*P .. +P)   P = payload_row_bytes (optional, P % 16 == 0)
+ *   d_counts[0] = #accepted, d_counts[1] = #deferred  (int64, required)
+ * d_threshold (optional device float) overrides `threshold` when non-NULL, so
+ * thresholds calibrated on the device need no host round trip (its value is
+ * not range-checked; a NaN threshold defers everything).
+ * Output buffers must hold n entries (worst case).  Workspace:
+ * hs_route_compact_workspace(n) bytes, ZERO-FILLED before its first use; every
+ * call leaves it zero-filled again (decoupled look-back tile descriptors). */
+size_t hs_route_compact_workspace(int64_t n);
+hs_status_t hs_route_compact(const float* conf, int64_t n, const int64_t* d_n, float threshold,
+                             const float* d_threshold, int32_t is_last, const int64_t* ids, const int32_t* pred,
+                             int32_t pred_len, int64_t* acc_ids, float* acc_conf,
+                             int32_t* acc_pred, int64_t* def_ids, int64_t* def_pos,
+                             const void* payload, int64_t payload_row_bytes, void* def_payload,
+                             int64_t* d_counts, void* ws, size_t ws_bytes, hs_stream_t stream);
+
+/* ------------------------------------------------------------------------ */
+/* One cascade stage m_k: confidence -> threshold test -> compaction/gather.  */
+/* ------------------------------------------------------------------------ */
+/* stage: 0-based index k of the model; is_last = (stage == n_stages - 1).
+ * The batch is items 0..n-1 (or *d_n); item i has request id ids[i] (NULL =
+ * identity) and reads its logits via row_index (NULL = dense, row i; pass
+ * row_index == ids when the stage's logits are indexed by request id).
+ * Accepted items go to acc_ids / acc_conf / acc_pred (pred = the seq_len
+ * argmaxes); deferred items become the next stage's batch: next_ids,
+ * next_payload (optional).  d_counts = {#accepted, #deferred}.  d_threshold as
+ * for hs_route_compact.
+ * Workspace: hs_cascade_step_workspace(n, seq_len) bytes, zero-filled before
+ * first use (left zero-filled).  Same errors as the two calls above. */
+size_t hs_cascade_step_workspace(int64_t n, int32_t seq_len);
+hs_status_t hs_cascade_step(int32_t stage, int32_t n_stages, const void* logits, hs_dtype_t dtype,
+                            int64_t n, int32_t seq_len, int64_t n_classes, int64_t row_stride,
+                            const int64_t* row_index, const int64_t* d_n, float temperature,
+                            hs_conf_kind_t kind, hs_seq_reduce_t reduce, float threshold,
+                            const float* d_threshold, const int64_t* ids, const void* payload, int64_t payload_row_bytes,
+                            int64_t* acc_ids, float* acc_conf, int32_t* acc_pred,
+                            int64_t* next_ids, void* next_payload, int64_t* d_counts, void* ws,
+                            size_t ws_bytes, uint32_t* d_status, hs_stream_t stream);
+
+/* ------------------------------------------------------------------------ */
+/* Offline Accuracy-Preserving threshold calibration (Alg. 1, AP).  */
+/* ------------------------------------------------------------------------ */
+/* Deterministic forward-greedy sweep on a 2^q grid (replaces Alg. 1's random
+ * sampler, reading G8): bin(c) = min(B, floor(c*B)), B = 2^log2_bins, NaN never
+ * accepted.  Round k = 0..K-2 over the validation samples still alive:
+ *   G = sum_alive correct[K-1][r];  S(b) = sum_{alive, bin >= b} (correct[k][r] - correct[K-1][r])
+ *   b_k = min { b in 0..B+1 : A + G + S(b) >= tau },  A += sum_{alive, bin >= b_k} correct[k][r]
+ * t_k = b_k / B, or +inf for b_k = B+1 (defer all); t_{K-1} = 0.  tau = target_correct,
+ * or (target_correct < 0, AP) the count of correct answers of m_K.
+ * Inputs: conf [(K-1) x N] fp32 (stage k's confidence of sample r at k*N + r),
+ * correct [K x N] u8 (0/1).  Outputs (device): d_bin_idx[K-1], d_thresholds[K],
+ * d_reach[K], d_handled[K], d_correct_total[1] (int64 counts).
+ * log2_bins in [1, 14]; K >= 2; N >= 1; refine_passes must be 0 (the optional
+ * refinement of DESIGN.md is not implemented on the GPU: HS_ERR_UNSUPPORTED).
+ * Workspace: hs_calibrate_workspace(K, log2_bins) bytes (no zero-fill needed).
+ * Entirely stream-ordered (capturable in a CUDA graph). */
+size_t hs_calibrate_workspace(int32_t K, int32_t log2_bins);
+hs_status_t hs_calibrate_thresholds(const float* conf, const uint8_t* correct, int32_t K, int64_t N,
+                                    int32_t log2_bins, int64_t target_correct,
+                                    int32_t refine_passes, int32_t* d_bin_idx,
+                                    float* d_thresholds, int64_t* d_reach, int64_t* d_handled,
+                                    int64_t* d_correct_total, void* ws, size_t ws_bytes,
+                                    hs_stream_t stream);
+
+/* Building blocks of the same sweep for request-sharded calibration across
+ * GPUs (each rank holds a shard of the validation set; the caller sums the
+ * histograms across ranks between the two calls, e.g. with an all-reduce):
+ *   hs_calibrate_begin:      zero the histogram/state in ws, set tau (target >= 0) or AP.
+ *   hs_calibrate_histogram:  round k: add this shard's 3 x (B+2) int32 histogram
+ *                            (count, correct_k, correct_K per bin; index 0 = NaN)
+ *                            into hs_calibrate_hist_ptr(ws).
+ *   hs_calibrate_select:     round k: pick b_k from the (summed) histogram, update
+ *                            A, reach/handled, thresholds; zero the histogram.
+ * Every rank that runs select on identical histograms gets identical b_k. */
+hs_status_t hs_calibrate_begin(int32_t K, int32_t log2_bins, int64_t target_correct, void* ws,
+                               size_t ws_bytes, hs_stream_t stream);
+int32_t* hs_calibrate_hist_ptr(void* ws);
+size_t hs_calibrate_hist_bytes(int32_t log2_bins);
+hs_status_t hs_calibrate_histogram(const float* conf, const uint8_t* correct, int32_t K, int64_t N,
+                                   int32_t log2_bins, int32_t round, const int32_t* d_bin_idx,
+                                   void* ws, size_t ws_bytes, hs_stream_t stream);
+hs_status_t hs_calibrate_select(int32_t K, int32_t log2_bins, int32_t round, int32_t* d_bin_idx,
+                                float* d_thresholds, int64_t* d_reach, int64_t* d_handled,
+                                int64_t* d_correct_total, void* ws, size_t ws_bytes,
+                                hs_stream_t stream);
+
+/* ------------------------------------------------------------------------ */
+/* Diagnostics.                                                              */
+/* ------------------------------------------------------------------------ */
+const char* hs_status_string(hs_status_t s);
+const char* hs_last_error(void);     /* thread-local detail of the last failure */
+uint64_t hs_launch_count(void);      /* kernels this process has launched through libhs */
+const char* hs_build_info(void);     /* compile target / flags */
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HS_H_ */

@@ -1,0 +1,335 @@
+"""HybridServe cascade router on B200 (sm_100a) -- thin Python binding of libhs.so.
+
+Every step of the router (confidence, threshold test, compaction, gather,
+calibration) runs in the CUDA kernels behind the C-ABI of ``include/hs.h``;
+this module only turns torch tensors into pointers, allocates caller-owned
+buffers with torch, and passes ``torch.cuda.current_stream()``.  There is no
+CPU fallback: without ``libhs.so`` (or a GPU) every call raises.
+
+Names follow the C-ABI (``hs_confidence`` -> ``confidence`` ...).  The paper's
+statement of the cascade: models m_1..m_K, small to large, with
+thresholds t_1..t_{K-1}; a request answered by m_k iff its confidence at m_k
+is >= t_k; t_K = 0.
+"""
+from __future__ import annotations
+
+import dataclasses
+
+import torch
+
+from . import _abi
+from ._abi import HsError, lib
+
+MAXPROB, MAXPROB_SQ, ENTROPY = 0, 1, 2
+SEQ_NONE, SEQ_MIN, SEQ_MEAN = 0, 1, 2
+_KINDS = {"maxprob": MAXPROB, "maxprob_sq": MAXPROB_SQ, "entropy": ENTROPY}
+_REDUCES = {"none": SEQ_NONE, "min": SEQ_MIN, "mean": SEQ_MEAN}
+STATUS_NONFINITE = 1
+
+__all__ = ["confidence", "route_compact", "cascade_step", "calibrate_thresholds",
+           "calibrate_begin", "calibrate_histogram", "calibrate_select", "Cascade", "HsError",
+           "launch_count", "MAXPROB", "MAXPROB_SQ", "ENTROPY", "SEQ_NONE", "SEQ_MIN", "SEQ_MEAN"]
+
+
+def _kind(k):
+    return _KINDS[k] if isinstance(k, str) else int(k)
+
+
+def _reduce(r):
+    return _REDUCES[r] if isinstance(r, str) else int(r)
+
+
+def _p(t):
+    return None if t is None else t.data_ptr()
+
+
+def _stream(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def _dtype_code(t: torch.Tensor) -> int:
+    if t.dtype == torch.bfloat16:
+        return 1
+    if t.dtype == torch.float32:
+        return 0
+    raise TypeError(f"logits must be bfloat16 or float32, got {t.dtype}")
+
+
+def _check_cuda(*ts):
+    for t in ts:
+        if t is not None and not t.is_cuda:
+            raise ValueError("libhs takes CUDA tensors only (no CPU fallback)")
+
+
+def launch_count() -> int:
+    """Kernels launched through libhs by this process."""
+    return int(lib().hs_launch_count())
+
+
+def build_info() -> str:
+    return lib().hs_build_info().decode()
+
+
+def workspace(nbytes: int, device) -> torch.Tensor:
+    """A zero-filled workspace (the compaction descriptors must start zeroed)."""
+    return torch.zeros(max(int(nbytes), 16), dtype=torch.uint8, device=device)
+
+
+# ---------------------------------------------------------------------------
+# hs_confidence
+# ---------------------------------------------------------------------------
+def confidence(logits: torch.Tensor, *, n: int | None = None, seq_len: int = 1,
+               n_classes: int | None = None, temperature: float = 1.0, kind="maxprob",
+               reduce="none", row_index: torch.Tensor | None = None,
+               d_n: torch.Tensor | None = None, labels: torch.Tensor | None = None,
+               want_argmax: bool = True, status: torch.Tensor | None = None,
+               out: dict | None = None, ws: torch.Tensor | None = None, stream=None) -> dict:
+    """Per-item confidence of a batch of logits rows.
+
+    ``logits``: [rows, row_stride] bf16/fp32 on the GPU (row-major; the first
+    ``n_classes`` entries of a row are the prediction vector).  Returns dict of
+    ``conf`` f32[n], ``argmax`` i32[n*seq_len] and ``correct`` u8[n] (when
+    ``labels`` is given)."""
+    _check_cuda(logits, row_index, d_n, labels, status)
+    if logits.dim() != 2 or logits.stride(1) != 1:
+        raise ValueError("logits must be a 2-D row-major tensor")
+    C = int(n_classes or logits.shape[1])
+    stride = int(logits.stride(0))
+    if n is None:
+        n = int(row_index.numel()) if row_index is not None else logits.shape[0] // seq_len
+    dev = logits.device
+    out = dict(out or {})
+    if "conf" not in out:
+        out["conf"] = torch.empty(n, dtype=torch.float32, device=dev)
+    if want_argmax and "argmax" not in out:
+        out["argmax"] = torch.empty(n * seq_len, dtype=torch.int32, device=dev)
+    if labels is not None and "correct" not in out:
+        out["correct"] = torch.empty(n, dtype=torch.uint8, device=dev)
+    need = lib().hs_confidence_workspace(n, seq_len)
+    if need and (ws is None or ws.numel() < need):
+        ws = torch.empty(need, dtype=torch.uint8, device=dev)
+    _abi.call("hs_confidence", _p(logits), _dtype_code(logits), n, seq_len, C, stride,
+              _p(row_index), _p(d_n), float(temperature), _kind(kind), _reduce(reduce),
+              _p(out["conf"]), _p(out.get("argmax")), _p(labels), _p(out.get("correct")),
+              _p(ws), 0 if ws is None else ws.numel(), _p(status), _stream(stream))
+    return out
+
+
+# ---------------------------------------------------------------------------
+# hs_route_compact
+# ---------------------------------------------------------------------------
+def route_compact(conf: torch.Tensor, threshold: float | torch.Tensor, *, is_last: bool = False,
+                  n: int | None = None, d_n: torch.Tensor | None = None,
+                  ids: torch.Tensor | None = None, pred: torch.Tensor | None = None,
+                  pred_len: int = 1, payload: torch.Tensor | None = None,
+                  out: dict | None = None, ws: torch.Tensor | None = None, stream=None) -> dict:
+    """Threshold test + stable split.  Returns capacity-sized
+    buffers and ``counts`` (device int64[2] = {#accepted, #deferred})."""
+    _check_cuda(conf, d_n, ids, pred, payload)
+    n = int(conf.numel() if n is None else n)
+    dev = conf.device
+    out = dict(out or {})
+    out.setdefault("acc_ids", torch.empty(n, dtype=torch.int64, device=dev))
+    out.setdefault("acc_conf", torch.empty(n, dtype=torch.float32, device=dev))
+    if pred is not None:
+        out.setdefault("acc_pred", torch.empty(n * pred_len, dtype=torch.int32, device=dev))
+    out.setdefault("def_ids", torch.empty(n, dtype=torch.int64, device=dev))
+    out.setdefault("def_pos", torch.empty(n, dtype=torch.int64, device=dev))
+    P = 0
+    if payload is not None:
+        P = payload.element_size()
+        for d in payload.shape[1:]:
+            P *= int(d)
+        out.setdefault("def_payload", torch.empty_like(payload))
+    out.setdefault("counts", torch.zeros(2, dtype=torch.int64, device=dev))
+    need = lib().hs_route_compact_workspace(n)
+    if ws is None:
+        ws = workspace(need, dev)
+    d_thr = threshold if isinstance(threshold, torch.Tensor) else None
+    thr = 0.0 if d_thr is not None else float(threshold)
+    _abi.call("hs_route_compact", _p(conf), n, _p(d_n), thr, _p(d_thr), int(bool(is_last)),
+              _p(ids), _p(pred), int(pred_len), _p(out["acc_ids"]), _p(out["acc_conf"]),
+              _p(out.get("acc_pred")), _p(out["def_ids"]), _p(out["def_pos"]), _p(payload), P,
+              _p(out.get("def_payload")), _p(out["counts"]), _p(ws), ws.numel(), _stream(stream))
+    return out
+
+
+# ---------------------------------------------------------------------------
+# hs_cascade_step
+# ---------------------------------------------------------------------------
+def cascade_step(stage: int, n_stages: int, logits: torch.Tensor, threshold, *, n: int,
+                 seq_len: int = 1, n_classes: int | None = None, temperature: float = 1.0,
+                 kind="maxprob", reduce="none", row_index: torch.Tensor | None = None,
+                 d_n: torch.Tensor | None = None, ids: torch.Tensor | None = None,
+                 payload: torch.Tensor | None = None, payload_row_bytes: int = 0,
+                 out: dict | None = None, ws: torch.Tensor | None = None,
+                 status: torch.Tensor | None = None, stream=None) -> dict:
+    """One model m_k of the cascade: confidence -> threshold -> compaction/gather."""
+    _check_cuda(logits, row_index, d_n, ids, payload, status)
+    C = int(n_classes or logits.shape[1])
+    dev = logits.device
+    out = dict(out or {})
+    out.setdefault("acc_ids", torch.empty(n, dtype=torch.int64, device=dev))
+    out.setdefault("acc_conf", torch.empty(n, dtype=torch.float32, device=dev))
+    out.setdefault("acc_pred", torch.empty(n * seq_len, dtype=torch.int32, device=dev))
+    out.setdefault("next_ids", torch.empty(n, dtype=torch.int64, device=dev))
+    if payload is not None and payload_row_bytes > 0:
+        out.setdefault("next_payload", torch.empty(n * payload_row_bytes, dtype=torch.uint8, device=dev))
+    out.setdefault("counts", torch.zeros(2, dtype=torch.int64, device=dev))
+    need = lib().hs_cascade_step_workspace(n, seq_len)
+    if ws is None:
+        ws = workspace(need, dev)
+    d_thr = threshold if isinstance(threshold, torch.Tensor) else None
+    thr = 0.0 if d_thr is not None else float(threshold)
+    _abi.call("hs_cascade_step", int(stage), int(n_stages), _p(logits), _dtype_code(logits), int(n),
+              int(seq_len), C, int(logits.stride(0)), _p(row_index), _p(d_n), float(temperature),
+              _kind(kind), _reduce(reduce), thr, _p(d_thr), _p(ids), _p(payload),
+              int(payload_row_bytes), _p(out["acc_ids"]), _p(out["acc_conf"]), _p(out["acc_pred"]),
+              _p(out["next_ids"]), _p(out.get("next_payload")), _p(out["counts"]), _p(ws),
+              ws.numel(), _p(status), _stream(stream))
+    return out
+
+
+# ---------------------------------------------------------------------------
+# hs_calibrate_*
+# ---------------------------------------------------------------------------
+def _calib_out(K: int, dev, out: dict | None):
+    out = dict(out or {})
+    out.setdefault("b", torch.empty(K - 1, dtype=torch.int32, device=dev))
+    out.setdefault("t", torch.empty(K, dtype=torch.float32, device=dev))
+    out.setdefault("reach", torch.empty(K, dtype=torch.int64, device=dev))
+    out.setdefault("handled", torch.empty(K, dtype=torch.int64, device=dev))
+    out.setdefault("correct_total", torch.empty(1, dtype=torch.int64, device=dev))
+    return out
+
+
+def calibrate_thresholds(conf: torch.Tensor, correct: torch.Tensor, *, log2_bins: int = 12,
+                         target: int = -1, refine_passes: int = 0, out: dict | None = None,
+                         ws: torch.Tensor | None = None, stream=None) -> dict:
+    """AP threshold calibration on the validation set.
+    conf: f32 [K-1, N]; correct: u8 [K, N]."""
+    _check_cuda(conf, correct)
+    K, N = int(correct.shape[0]), int(correct.shape[1])
+    if conf.dtype != torch.float32 or correct.dtype != torch.uint8:
+        raise TypeError("conf must be float32 and correct uint8")
+    if tuple(conf.shape) != (K - 1, N) or not conf.is_contiguous() or not correct.is_contiguous():
+        raise ValueError("conf must be contiguous [K-1, N], correct contiguous [K, N]")
+    dev = conf.device
+    out = _calib_out(K, dev, out)
+    need = lib().hs_calibrate_workspace(K, log2_bins)
+    if ws is None or ws.numel() < need:
+        ws = torch.empty(max(need, 16), dtype=torch.uint8, device=dev)
+    _abi.call("hs_calibrate_thresholds", _p(conf), _p(correct), K, N, int(log2_bins), int(target),
+              int(refine_passes), _p(out["b"]), _p(out["t"]), _p(out["reach"]),
+              _p(out["handled"]), _p(out["correct_total"]), _p(ws), ws.numel(), _stream(stream))
+    return out
+
+
+def calibrate_begin(K: int, log2_bins: int, target: int, ws: torch.Tensor, stream=None):
+    _abi.call("hs_calibrate_begin", int(K), int(log2_bins), int(target), _p(ws), ws.numel(),
+              _stream(stream))
+
+
+def calibrate_hist_view(ws: torch.Tensor, log2_bins: int) -> torch.Tensor:
+    """The int32 [3, B+2] histogram inside a calibration workspace (for all-reduce)."""
+    off = lib().hs_calibrate_hist_ptr(ws.data_ptr()) - ws.data_ptr()
+    nb = (1 << log2_bins) + 2
+    return ws[off: off + 3 * nb * 4].view(torch.int32).view(3, nb)
+
+
+def calibrate_histogram(conf, correct, round_: int, b: torch.Tensor, *, log2_bins: int,
+                        ws: torch.Tensor, stream=None):
+    K, N = int(correct.shape[0]), int(correct.shape[1])
+    _abi.call("hs_calibrate_histogram", _p(conf), _p(correct), K, N, int(log2_bins), int(round_),
+              _p(b), _p(ws), ws.numel(), _stream(stream))
+
+
+def calibrate_select(K: int, round_: int, out: dict, *, log2_bins: int, ws: torch.Tensor,
+                     stream=None):
+    _abi.call("hs_calibrate_select", int(K), int(log2_bins), int(round_), _p(out["b"]),
+              _p(out["t"]), _p(out["reach"]), _p(out["handled"]), _p(out["correct_total"]),
+              _p(ws), ws.numel(), _stream(stream))
+
+
+def calibrate_workspace(K: int, log2_bins: int, device) -> torch.Tensor:
+    return torch.empty(max(lib().hs_calibrate_workspace(K, log2_bins), 16), dtype=torch.uint8,
+                       device=device)
+
+
+# ---------------------------------------------------------------------------
+# A K-stage cascade with preallocated buffers (no host round trip between
+# stages: each stage's batch size and threshold are read on the device).
+# ---------------------------------------------------------------------------
+@dataclasses.dataclass
+class StageSpec:
+    n_classes: int
+    temperature: float = 1.0
+    seq_len: int = 1
+    kind: int = MAXPROB
+    reduce: int = SEQ_NONE
+
+
+class Cascade:
+    """Routes a batch through models m_1..m_K.
+
+    ``route(logits, thresholds)``: logits[k] holds stage k's logits for every
+    request id (row = id, ``by_id=True``) or for stage k's batch in order
+    (``by_id=False``); thresholds is a device f32[K] (e.g. from
+    ``calibrate_thresholds``) or a list of floats.  All stages are launched
+    stream-ordered without host synchronisation; results stay on the device:
+    ``acc_ids[k][:counts[k,0]]``, ``acc_pred[k]``, ``acc_conf[k]``.
+    """
+
+    def __init__(self, n_cap: int, stages: list[StageSpec], device, payload_row_bytes: int = 0):
+        self.n_cap = int(n_cap)
+        self.stages = stages
+        self.K = len(stages)
+        self.device = torch.device(device)
+        self.P = int(payload_row_bytes)
+        L = max(s.seq_len for s in stages)
+        dev = self.device
+        self.counts = torch.zeros(self.K, 2, dtype=torch.int64, device=dev)
+        self.status = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.outs = []
+        for k, s in enumerate(stages):
+            o = {"acc_ids": torch.empty(n_cap, dtype=torch.int64, device=dev),
+                 "acc_conf": torch.empty(n_cap, dtype=torch.float32, device=dev),
+                 "acc_pred": torch.empty(n_cap * s.seq_len, dtype=torch.int32, device=dev),
+                 "next_ids": torch.empty(n_cap, dtype=torch.int64, device=dev),
+                 "counts": self.counts[k]}
+            if self.P and k < self.K - 1:
+                o["next_payload"] = torch.empty(n_cap * self.P, dtype=torch.uint8, device=dev)
+            self.outs.append(o)
+        self.ws = workspace(lib().hs_cascade_step_workspace(n_cap, L), dev)
+
+    def route(self, logits: list, thresholds, *, n: int | None = None, ids=None, payload=None,
+              by_id: bool = True, stream=None):
+        n = self.n_cap if n is None else int(n)
+        d_thr = thresholds if isinstance(thresholds, torch.Tensor) else None
+        for k, s in enumerate(self.stages):
+            prev = self.outs[k - 1] if k else None
+            cur_ids = prev["next_ids"] if k else ids
+            cur_payload = prev.get("next_payload") if k else payload
+            thr = d_thr[k:k + 1] if d_thr is not None else float(thresholds[k] if k < self.K - 1 else 0.0)
+            row_index = cur_ids if by_id else None
+            if by_id and cur_ids is None:
+                row_index = None   # stage 1 with identity ids: row = id = position
+            cascade_step(k, self.K, logits[k], thr, n=n, seq_len=s.seq_len, n_classes=s.n_classes,
+                         temperature=s.temperature, kind=s.kind, reduce=s.reduce,
+                         row_index=row_index, d_n=prev["counts"][1:2] if k else None,
+                         ids=cur_ids, payload=cur_payload, payload_row_bytes=self.P,
+                         out=self.outs[k], ws=self.ws, status=self.status, stream=stream)
+        return self
+
+    def results(self):
+        """Host copy of the per-stage accepted lists (synchronises)."""
+        counts = self.counts.cpu()
+        res = []
+        for k, s in enumerate(self.stages):
+            na = int(counts[k, 0])
+            o = self.outs[k]
+            res.append({"ids": o["acc_ids"][:na].cpu(), "conf": o["acc_conf"][:na].cpu(),
+                        "pred": o["acc_pred"][:na * s.seq_len].cpu(), "n_acc": na,
+                        "n_def": int(counts[k, 1])})
+        return res

@@ -1,0 +1,77 @@
+"""ctypes declarations of libhs.so (include/hs.h).  Argument marshalling only."""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libhs.so")
+
+P = ctypes.c_void_p
+I64 = ctypes.c_int64
+I32 = ctypes.c_int32
+F32 = ctypes.c_float
+SZ = ctypes.c_size_t
+
+HS_OK = 0
+STATUS_NAMES = {0: "HS_OK", 1: "HS_ERR_INVALID_ARGUMENT", 2: "HS_ERR_NONFINITE_INPUT",
+                3: "HS_ERR_CUDA", 5: "HS_ERR_WORKSPACE_TOO_SMALL", 6: "HS_ERR_UNSUPPORTED"}
+
+# every symbol include/hs.h declares: name -> (restype, argtypes)
+SIGNATURES = {
+    "hs_confidence_workspace": (SZ, [I64, I32]),
+    "hs_confidence": (I32, [P, I32, I64, I32, I64, I64, P, P, F32, I32, I32, P, P, P, P, P, SZ, P, P]),
+    "hs_route_compact_workspace": (SZ, [I64]),
+    "hs_route_compact": (I32, [P, I64, P, F32, P, I32, P, P, I32, P, P, P, P, P, P, I64, P, P, P,
+                               SZ, P]),
+    "hs_cascade_step_workspace": (SZ, [I64, I32]),
+    "hs_cascade_step": (I32, [I32, I32, P, I32, I64, I32, I64, I64, P, P, F32, I32, I32, F32, P, P,
+                              P, I64, P, P, P, P, P, P, P, SZ, P, P]),
+    "hs_calibrate_workspace": (SZ, [I32, I32]),
+    "hs_calibrate_thresholds": (I32, [P, P, I32, I64, I32, I64, I32, P, P, P, P, P, P, SZ, P]),
+    "hs_calibrate_begin": (I32, [I32, I32, I64, P, SZ, P]),
+    "hs_calibrate_hist_ptr": (P, [P]),
+    "hs_calibrate_hist_bytes": (SZ, [I32]),
+    "hs_calibrate_histogram": (I32, [P, P, I32, I64, I32, I32, P, P, SZ, P]),
+    "hs_calibrate_select": (I32, [I32, I32, I32, P, P, P, P, P, P, SZ, P]),
+    "hs_status_string": (ctypes.c_char_p, [I32]),
+    "hs_last_error": (ctypes.c_char_p, []),
+    "hs_launch_count": (ctypes.c_uint64, []),
+    "hs_build_info": (ctypes.c_char_p, []),
+}
+
+_lock = threading.Lock()
+_lib = None
+
+
+class HsError(RuntimeError):
+    def __init__(self, fn: str, code: int, detail: str):
+        super().__init__(f"{fn}: {STATUS_NAMES.get(code, code)}: {detail}")
+        self.code = code
+
+
+def lib():
+    """Load libhs.so (built in-tree by __graft_entry__.build()).  There is no
+    fallback: the router runs on the CUDA kernels or not at all."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise ImportError(f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'`")
+            L = ctypes.CDLL(LIB_PATH)
+            for name, (res, args) in SIGNATURES.items():
+                f = getattr(L, name)
+                f.restype = res
+                f.argtypes = args
+            _lib = L
+    return _lib
+
+
+def check(fn: str, code: int):
+    if code != HS_OK:
+        raise HsError(fn, code, lib().hs_last_error().decode(errors="replace"))
+
+
+def call(fn: str, *args):
+    check(fn, getattr(lib(), fn)(*args))

@@ -1,0 +1,381 @@
+// api.cu -- the C-ABI of libhs.so (declared and documented in include/hs.h).
+//
+// Host side only: synchronous argument validation, workspace carving, variant
+// selection and stream-ordered launches.  No allocation, no synchronisation.
+#include <atomic>
+#include <cstdarg>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "hs_internal.h"
+
+namespace hs {
+
+static std::atomic<uint64_t> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+int num_sms() {
+  static std::mutex mu;
+  static std::vector<int> cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  if ((int)cache.size() <= dev) cache.resize(dev + 1, 0);
+  if (cache[dev] == 0) {
+    int n = 0;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    cache[dev] = n > 0 ? n : 1;
+  }
+  return cache[dev];
+}
+
+}  // namespace hs
+
+namespace {
+
+thread_local std::string g_err;
+
+hs_status_t fail(hs_status_t s, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
+hs_status_t fail(hs_status_t s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return s;
+}
+
+hs_status_t cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) return fail(HS_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+  return HS_OK;
+}
+
+inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// workspace for hs_confidence with seq_len > 1: token conf (f32) + token ok (u8)
+size_t conf_ws(int64_t n, int32_t L) {
+  if (L <= 1) return 0;
+  const size_t rows = (size_t)n * (size_t)L;
+  return align_up(rows * sizeof(float), 256) + align_up(rows, 256);
+}
+
+hs_status_t check_logits(const void* logits, hs_dtype_t dtype, int64_t n, int32_t L, int64_t C,
+                         int64_t stride, float T, hs_conf_kind_t kind, hs_seq_reduce_t reduce) {
+  if (n < 0) return fail(HS_ERR_INVALID_ARGUMENT, "n = %lld < 0", (long long)n);
+  if (dtype != HS_F32 && dtype != HS_BF16) return fail(HS_ERR_INVALID_ARGUMENT, "bad dtype %d", (int)dtype);
+  if (C < 2) return fail(HS_ERR_INVALID_ARGUMENT, "n_classes = %lld < 2", (long long)C);
+  if (L < 1) return fail(HS_ERR_INVALID_ARGUMENT, "seq_len = %d < 1", (int)L);
+  if (stride < C) return fail(HS_ERR_INVALID_ARGUMENT, "row_stride %lld < n_classes %lld", (long long)stride, (long long)C);
+  if (!(T > 0.f) || !std::isfinite(T)) return fail(HS_ERR_INVALID_ARGUMENT, "temperature must be > 0 and finite");
+  if ((int)kind < 0 || (int)kind > 2) return fail(HS_ERR_INVALID_ARGUMENT, "bad confidence kind %d", (int)kind);
+  if ((int)reduce < 0 || (int)reduce > 2) return fail(HS_ERR_INVALID_ARGUMENT, "bad seq reduce %d", (int)reduce);
+  if (reduce == HS_SEQ_NONE && L != 1) return fail(HS_ERR_INVALID_ARGUMENT, "HS_SEQ_NONE requires seq_len == 1");
+  const int eb = dtype == HS_BF16 ? 2 : 4;
+  if (((stride * eb) & 15) != 0) return fail(HS_ERR_INVALID_ARGUMENT, "row_stride * element size must be a multiple of 16 bytes");
+  if (n > 0 && (!logits || !aligned16(logits))) return fail(HS_ERR_INVALID_ARGUMENT, "logits must be non-NULL and 16-byte aligned");
+  const int ve = 16 / eb;
+  if ((C + ve - 1) / ve > (int64_t)0x7FFFFFFF / 8) return fail(HS_ERR_INVALID_ARGUMENT, "n_classes too large");
+  return HS_OK;
+}
+
+hs::ConfArgs make_conf_args(const void* logits, hs_dtype_t dtype, int64_t n, int32_t L, int64_t C,
+                            int64_t stride, const int64_t* row_index, const int64_t* d_n, float T,
+                            hs_conf_kind_t kind) {
+  hs::ConfArgs a{};
+  const int eb = dtype == HS_BF16 ? 2 : 4, ve = 16 / eb;
+  a.logits = logits;
+  a.row_bytes = stride * eb;
+  a.n = n;
+  a.L = L;
+  a.C = C;
+  a.nvec = (int)((C + ve - 1) / ve);
+  a.tail = (int)(C % ve);
+  a.row_index = row_index;
+  a.d_n = d_n;
+  a.c = (float)(1.4426950408889634 / (double)T);
+  a.kind = (int)kind;
+  return a;
+}
+
+// Runs K1 (+ K2).  conf / argmax / correct are per batch item.
+hs_status_t run_confidence(const void* logits, hs_dtype_t dtype, int64_t n, int32_t L, int64_t C,
+                           int64_t stride, const int64_t* row_index, const int64_t* d_n, float T,
+                           hs_conf_kind_t kind, hs_seq_reduce_t reduce, float* conf,
+                           int32_t* argmax, const int32_t* labels, uint8_t* correct, void* ws,
+                           uint32_t* d_status, cudaStream_t s) {
+  if (n == 0) return HS_OK;
+  hs::ConfArgs a = make_conf_args(logits, dtype, n, L, C, stride, row_index, d_n, T, kind);
+  a.argmax = argmax;
+  a.labels = labels;
+  a.status = d_status;
+  if (L == 1) {
+    a.conf = conf;
+    a.ok = correct;
+    return cuda_check(hs::launch_confidence(a, dtype == HS_BF16, s), "confidence kernel");
+  }
+  float* tok_conf = reinterpret_cast<float*>(ws);
+  uint8_t* tok_ok = reinterpret_cast<uint8_t*>(ws) + align_up((size_t)n * L * sizeof(float), 256);
+  a.conf = tok_conf;
+  a.ok = (correct && labels) ? tok_ok : nullptr;
+  hs_status_t st = cuda_check(hs::launch_confidence(a, dtype == HS_BF16, s), "confidence kernel");
+  if (st != HS_OK) return st;
+  return cuda_check(hs::launch_seq_reduce(tok_conf, a.ok, n, d_n, L, (int)reduce, conf, correct, s),
+                    "sequence reduce kernel");
+}
+
+hs_status_t check_threshold(float t) {
+  if (std::isnan(t) || (t < 0.f) || (t > 1.f && !std::isinf(t)))
+    return fail(HS_ERR_INVALID_ARGUMENT, "threshold must be in [0,1] or +inf");
+  return HS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* hs_status_string(hs_status_t s) {
+  switch (s) {
+    case HS_OK: return "HS_OK";
+    case HS_ERR_INVALID_ARGUMENT: return "HS_ERR_INVALID_ARGUMENT";
+    case HS_ERR_NONFINITE_INPUT: return "HS_ERR_NONFINITE_INPUT";
+    case HS_ERR_CUDA: return "HS_ERR_CUDA";
+    case HS_ERR_WORKSPACE_TOO_SMALL: return "HS_ERR_WORKSPACE_TOO_SMALL";
+    case HS_ERR_UNSUPPORTED: return "HS_ERR_UNSUPPORTED";
+  }
+  return "HS_ERR_UNKNOWN";
+}
+
+const char* hs_last_error(void) { return g_err.c_str(); }
+uint64_t hs_launch_count(void) { return hs::g_launches.load(); }
+const char* hs_build_info(void) {
+#define HS_STR2(x) #x
+#define HS_STR(x) HS_STR2(x)
+  return "libhs: sm_100a (compute_100a), nvcc " HS_STR(__CUDACC_VER_MAJOR__) "." HS_STR(__CUDACC_VER_MINOR__);
+}
+
+size_t hs_confidence_workspace(int64_t n, int32_t seq_len) { return conf_ws(n, seq_len); }
+
+hs_status_t hs_confidence(const void* logits, hs_dtype_t dtype, int64_t n, int32_t seq_len,
+                          int64_t n_classes, int64_t row_stride, const int64_t* row_index,
+                          const int64_t* d_n, float temperature, hs_conf_kind_t kind,
+                          hs_seq_reduce_t reduce, float* conf, int32_t* argmax,
+                          const int32_t* labels, uint8_t* correct, void* ws, size_t ws_bytes,
+                          uint32_t* d_status, hs_stream_t stream) {
+  hs_status_t st = check_logits(logits, dtype, n, seq_len, n_classes, row_stride, temperature, kind, reduce);
+  if (st != HS_OK) return st;
+  if (n > 0 && !conf) return fail(HS_ERR_INVALID_ARGUMENT, "conf output is required");
+  if (correct && !labels) return fail(HS_ERR_INVALID_ARGUMENT, "correct requires labels");
+  if (ws_bytes < conf_ws(n, seq_len) || (conf_ws(n, seq_len) && !ws))
+    return fail(HS_ERR_WORKSPACE_TOO_SMALL, "workspace %zu < %zu", ws_bytes, conf_ws(n, seq_len));
+  return run_confidence(logits, dtype, n, seq_len, n_classes, row_stride, row_index, d_n,
+                        temperature, kind, reduce, conf, argmax, labels, correct, ws, d_status,
+                        (cudaStream_t)stream);
+}
+
+size_t hs_route_compact_workspace(int64_t n) { return hs::compact_ws_bytes(n); }
+
+static hs_status_t route_compact_impl(const float* conf, int64_t n, const int64_t* d_n,
+                                      float threshold, const float* d_threshold, int32_t is_last, const int64_t* ids,
+                                      const int32_t* pred, int32_t pred_len, int64_t* acc_ids,
+                                      float* acc_conf, int32_t* acc_pred, int64_t* def_ids,
+                                      int64_t* def_pos, const void* payload,
+                                      int64_t payload_row_bytes, void* def_payload,
+                                      int64_t* d_counts, void* ws, cudaStream_t s) {
+  hs::CompactArgs a{};
+  a.conf = conf;
+  a.n = n;
+  a.d_n = d_n;
+  a.threshold = threshold;
+  a.d_threshold = d_threshold;
+  a.is_last = is_last ? 1 : 0;
+  a.ids = ids;
+  a.pred = pred;
+  a.pred_len = pred_len;
+  a.acc_ids = acc_ids;
+  a.acc_conf = acc_conf;
+  a.acc_pred = acc_pred;
+  a.def_ids = def_ids;
+  a.def_pos = def_pos;
+  a.counts = d_counts;
+  a.ws = ws;
+  hs_status_t st = cuda_check(hs::launch_route_compact(a, s), "route/compact kernel");
+  if (st != HS_OK) return st;
+  if (def_payload && payload_row_bytes > 0 && !is_last)
+    st = cuda_check(hs::launch_gather_rows(def_pos, d_counts + 1, n, payload, payload_row_bytes,
+                                           def_payload, s),
+                    "gather kernel");
+  return st;
+}
+
+hs_status_t hs_route_compact(const float* conf, int64_t n, const int64_t* d_n, float threshold,
+                             const float* d_threshold, int32_t is_last, const int64_t* ids, const int32_t* pred,
+                             int32_t pred_len, int64_t* acc_ids, float* acc_conf,
+                             int32_t* acc_pred, int64_t* def_ids, int64_t* def_pos,
+                             const void* payload, int64_t payload_row_bytes, void* def_payload,
+                             int64_t* d_counts, void* ws, size_t ws_bytes, hs_stream_t stream) {
+  if (n < 0) return fail(HS_ERR_INVALID_ARGUMENT, "n < 0");
+  if (!is_last && !d_threshold) {
+    hs_status_t st = check_threshold(threshold);
+    if (st != HS_OK) return st;
+  }
+  if (!d_counts) return fail(HS_ERR_INVALID_ARGUMENT, "d_counts is required");
+  if (n > 0 && !conf) return fail(HS_ERR_INVALID_ARGUMENT, "conf is required");
+  if (acc_pred && (!pred || pred_len < 1)) return fail(HS_ERR_INVALID_ARGUMENT, "acc_pred requires pred and pred_len >= 1");
+  if (def_payload) {
+    if (!payload || payload_row_bytes <= 0 || (payload_row_bytes & 15) || !aligned16(payload) || !aligned16(def_payload))
+      return fail(HS_ERR_INVALID_ARGUMENT, "payload rows must be 16-byte aligned multiples of 16 bytes");
+    if (!def_pos) return fail(HS_ERR_INVALID_ARGUMENT, "def_payload requires def_pos (gather indices)");
+  }
+  if (!ws || ws_bytes < hs::compact_ws_bytes(n))
+    return fail(HS_ERR_WORKSPACE_TOO_SMALL, "workspace %zu < %zu", ws_bytes, hs::compact_ws_bytes(n));
+  return route_compact_impl(conf, n, d_n, threshold, d_threshold, is_last, ids, pred, pred_len,
+                            acc_ids, acc_conf, acc_pred, def_ids, def_pos, payload, payload_row_bytes,
+                            def_payload, d_counts, ws, (cudaStream_t)stream);
+}
+
+// cascade-step workspace: [compact ws][conf f32 n][argmax i32 n*L][def_pos i64 n][conf ws]
+static size_t step_layout(int64_t n, int32_t L, size_t* o_conf, size_t* o_am, size_t* o_pos,
+                          size_t* o_cws) {
+  size_t off = align_up(hs::compact_ws_bytes(n), 256);
+  *o_conf = off;
+  off = align_up(off + (size_t)n * sizeof(float), 256);
+  *o_am = off;
+  off = align_up(off + (size_t)n * (size_t)L * sizeof(int32_t), 256);
+  *o_pos = off;
+  off = align_up(off + (size_t)n * sizeof(int64_t), 256);
+  *o_cws = off;
+  off = align_up(off + conf_ws(n, L), 256);
+  return off;
+}
+
+size_t hs_cascade_step_workspace(int64_t n, int32_t seq_len) {
+  size_t a, b, c, d;
+  return step_layout(n < 0 ? 0 : n, seq_len < 1 ? 1 : seq_len, &a, &b, &c, &d);
+}
+
+hs_status_t hs_cascade_step(int32_t stage, int32_t n_stages, const void* logits, hs_dtype_t dtype,
+                            int64_t n, int32_t seq_len, int64_t n_classes, int64_t row_stride,
+                            const int64_t* row_index, const int64_t* d_n, float temperature,
+                            hs_conf_kind_t kind, hs_seq_reduce_t reduce, float threshold,
+                            const float* d_threshold, const int64_t* ids, const void* payload, int64_t payload_row_bytes,
+                            int64_t* acc_ids, float* acc_conf, int32_t* acc_pred,
+                            int64_t* next_ids, void* next_payload, int64_t* d_counts, void* ws,
+                            size_t ws_bytes, uint32_t* d_status, hs_stream_t stream) {
+  if (n_stages < 1 || stage < 0 || stage >= n_stages)
+    return fail(HS_ERR_INVALID_ARGUMENT, "stage %d outside 0..n_stages-1 (%d)", stage, n_stages);
+  const int is_last = stage == n_stages - 1;
+  hs_status_t st = check_logits(logits, dtype, n, seq_len, n_classes, row_stride, temperature, kind, reduce);
+  if (st != HS_OK) return st;
+  if (!is_last && !d_threshold) {
+    st = check_threshold(threshold);
+    if (st != HS_OK) return st;
+  }
+  if (!d_counts) return fail(HS_ERR_INVALID_ARGUMENT, "d_counts is required");
+  if (next_payload && (!payload || payload_row_bytes <= 0 || (payload_row_bytes & 15) ||
+                       !aligned16(payload) || !aligned16(next_payload)))
+    return fail(HS_ERR_INVALID_ARGUMENT, "payload rows must be 16-byte aligned multiples of 16 bytes");
+  size_t o_conf, o_am, o_pos, o_cws;
+  const size_t need = step_layout(n, seq_len, &o_conf, &o_am, &o_pos, &o_cws);
+  if (!ws || ws_bytes < need) return fail(HS_ERR_WORKSPACE_TOO_SMALL, "workspace %zu < %zu", ws_bytes, need);
+  cudaStream_t s = (cudaStream_t)stream;
+  char* w = reinterpret_cast<char*>(ws);
+  float* conf = reinterpret_cast<float*>(w + o_conf);
+  int32_t* am = reinterpret_cast<int32_t*>(w + o_am);
+  int64_t* pos = reinterpret_cast<int64_t*>(w + o_pos);
+  if (n == 0) {
+    st = cuda_check(cudaMemsetAsync(d_counts, 0, 2 * sizeof(int64_t), s), "memset counts");
+    return st;
+  }
+  st = run_confidence(logits, dtype, n, seq_len, n_classes, row_stride, row_index, d_n, temperature,
+                      kind, reduce, conf, am, nullptr, nullptr, w + o_cws, d_status, s);
+  if (st != HS_OK) return st;
+  return route_compact_impl(conf, n, d_n, threshold, d_threshold, is_last, ids, am, seq_len, acc_ids, acc_conf,
+                            acc_pred, next_ids, next_payload ? pos : nullptr, payload,
+                            payload_row_bytes, next_payload, d_counts, ws, s);
+}
+
+size_t hs_calibrate_workspace(int32_t K, int32_t log2_bins) {
+  if (log2_bins < 1 || log2_bins > 14) return 0;
+  return hs::calib_ws_bytes(K, log2_bins);
+}
+size_t hs_calibrate_hist_bytes(int32_t log2_bins) {
+  if (log2_bins < 1 || log2_bins > 14) return 0;
+  return hs::calib_hist_bytes(log2_bins);
+}
+int32_t* hs_calibrate_hist_ptr(void* ws) {
+  return reinterpret_cast<int32_t*>(reinterpret_cast<char*>(ws) + sizeof(hs::CalibState));
+}
+
+static hs_status_t check_calib(int32_t K, int32_t q, void* ws, size_t ws_bytes) {
+  if (K < 2 || K > 17) return fail(HS_ERR_INVALID_ARGUMENT, "K = %d outside 2..17", K);
+  if (q < 1 || q > 14) return fail(HS_ERR_INVALID_ARGUMENT, "log2_bins = %d outside 1..14", q);
+  if (!ws || ws_bytes < hs::calib_ws_bytes(K, q))
+    return fail(HS_ERR_WORKSPACE_TOO_SMALL, "workspace %zu < %zu", ws_bytes, hs::calib_ws_bytes(K, q));
+  return HS_OK;
+}
+
+hs_status_t hs_calibrate_begin(int32_t K, int32_t log2_bins, int64_t target_correct, void* ws,
+                               size_t ws_bytes, hs_stream_t stream) {
+  hs_status_t st = check_calib(K, log2_bins, ws, ws_bytes);
+  if (st != HS_OK) return st;
+  return cuda_check(hs::launch_calib_init(ws, log2_bins, target_correct, (cudaStream_t)stream), "calib init");
+}
+
+hs_status_t hs_calibrate_histogram(const float* conf, const uint8_t* correct, int32_t K, int64_t N,
+                                   int32_t log2_bins, int32_t round, const int32_t* d_bin_idx,
+                                   void* ws, size_t ws_bytes, hs_stream_t stream) {
+  hs_status_t st = check_calib(K, log2_bins, ws, ws_bytes);
+  if (st != HS_OK) return st;
+  if (N < 0) return fail(HS_ERR_INVALID_ARGUMENT, "N < 0");
+  if (round < 0 || round > K - 2) return fail(HS_ERR_INVALID_ARGUMENT, "round outside 0..K-2");
+  if (N == 0) return HS_OK;   // an empty shard contributes nothing
+  if (!conf || !correct || (round > 0 && !d_bin_idx)) return fail(HS_ERR_INVALID_ARGUMENT, "NULL input");
+  return cuda_check(hs::launch_calib_hist(conf, correct, K, N, log2_bins, round, d_bin_idx,
+                                          hs_calibrate_hist_ptr(ws), (cudaStream_t)stream),
+                    "calib histogram");
+}
+
+hs_status_t hs_calibrate_select(int32_t K, int32_t log2_bins, int32_t round, int32_t* d_bin_idx,
+                                float* d_thresholds, int64_t* d_reach, int64_t* d_handled,
+                                int64_t* d_correct_total, void* ws, size_t ws_bytes,
+                                hs_stream_t stream) {
+  hs_status_t st = check_calib(K, log2_bins, ws, ws_bytes);
+  if (st != HS_OK) return st;
+  if (round < 0 || round > K - 2) return fail(HS_ERR_INVALID_ARGUMENT, "round outside 0..K-2");
+  if (!d_bin_idx || !d_thresholds || !d_reach || !d_handled || !d_correct_total)
+    return fail(HS_ERR_INVALID_ARGUMENT, "NULL output");
+  return cuda_check(hs::launch_calib_select(K, log2_bins, round, d_bin_idx, d_thresholds, d_reach,
+                                            d_handled, d_correct_total, ws, (cudaStream_t)stream),
+                    "calib select");
+}
+
+hs_status_t hs_calibrate_thresholds(const float* conf, const uint8_t* correct, int32_t K, int64_t N,
+                                    int32_t log2_bins, int64_t target_correct,
+                                    int32_t refine_passes, int32_t* d_bin_idx,
+                                    float* d_thresholds, int64_t* d_reach, int64_t* d_handled,
+                                    int64_t* d_correct_total, void* ws, size_t ws_bytes,
+                                    hs_stream_t stream) {
+  hs_status_t st = check_calib(K, log2_bins, ws, ws_bytes);
+  if (st != HS_OK) return st;
+  if (N <= 0) return fail(HS_ERR_INVALID_ARGUMENT, "empty validation set (N = %lld)", (long long)N);
+  if (refine_passes != 0) return fail(HS_ERR_UNSUPPORTED, "refine_passes > 0 is not implemented on the GPU");
+  if (!conf || !correct) return fail(HS_ERR_INVALID_ARGUMENT, "NULL input");
+  if (!d_bin_idx || !d_thresholds || !d_reach || !d_handled || !d_correct_total)
+    return fail(HS_ERR_INVALID_ARGUMENT, "NULL output");
+  st = hs_calibrate_begin(K, log2_bins, target_correct, ws, ws_bytes, stream);
+  for (int k = 0; st == HS_OK && k < K - 1; ++k) {
+    st = hs_calibrate_histogram(conf, correct, K, N, log2_bins, k, d_bin_idx, ws, ws_bytes, stream);
+    if (st == HS_OK)
+      st = hs_calibrate_select(K, log2_bins, k, d_bin_idx, d_thresholds, d_reach, d_handled,
+                               d_correct_total, ws, ws_bytes, stream);
+  }
+  return st;
+}
+
+}  // extern "C"

@@ -1,0 +1,223 @@
+// compact.cu -- K3 (threshold test + stable compaction) and K4 (payload gather).
+//
+// The router's per-stage decision: an item is deferred to the next,
+// larger model iff its confidence is below the stage threshold (ties accept;
+// the last model answers everything).  The deferred items must form the next
+// stage's batch in their original order, so the split is a stable partition:
+// a single-pass scan with decoupled look-back (Merrill & Garland).  Each
+// 4,096-item tile takes a ticket (so tiles wait only on tiles already running),
+// ranks its items with warp ballots, publishes its deferred count, and walks
+// back over predecessor descriptors (64-bit {flag, count}, release/acquire at
+// gpu scope) for its exclusive prefix.  The last CTA to finish re-zeroes the
+// descriptors, so the workspace needs no memset between calls (graph-friendly).
+#include "hs_common.cuh"
+#include "hs_internal.h"
+
+namespace hs {
+
+namespace {
+
+constexpr unsigned long long kFlagA = 1ull << 62;   // aggregate available
+constexpr unsigned long long kFlagP = 2ull << 62;   // inclusive prefix available
+constexpr unsigned long long kValMask = (1ull << 62) - 1;
+
+__device__ __forceinline__ unsigned long long* tile_status(void* ws) {
+  return reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(ws) + sizeof(CompactWs));
+}
+
+__global__ void __launch_bounds__(kCompactThreads) route_compact_kernel(const CompactArgs a) {
+  constexpr int T = kCompactThreads, I = kCompactItems, NW = T / 32;
+  __shared__ unsigned s_tile;
+  __shared__ int s_cnt[I * NW];     // deferred count per (item row j, warp), j-major
+  __shared__ int s_off[I * NW];     // exclusive offsets within the tile
+  __shared__ long long s_excl;
+  __shared__ int s_last;
+
+  CompactWs* ws = reinterpret_cast<CompactWs*>(a.ws);
+  unsigned long long* st = tile_status(a.ws);
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+
+  int64_t n = a.n;
+  if (a.d_n) n = min(*a.d_n, a.n);
+  const int64_t ntiles = (n + kCompactTile - 1) / kCompactTile;
+
+  if (tid == 0) {
+    s_tile = atomicAdd(&ws->ticket, 1u);
+    s_last = 0;
+  }
+  __syncthreads();
+  const int64_t tile = s_tile;
+
+  if (tile < ntiles) {
+    const int64_t base = tile * kCompactTile;
+    const float thr = a.d_threshold ? *a.d_threshold : a.threshold;
+    // ---- flags (coalesced: item j of thread tid is base + j*T + tid)
+    bool dfr[I];
+    unsigned bal[I];
+#pragma unroll
+    for (int j = 0; j < I; ++j) {
+      const int64_t i = base + (int64_t)j * T + tid;
+      bool d = false;
+      if (i < n) {
+        const float c = a.conf[i];
+        d = !(a.is_last || c >= thr);   // NaN confidence: deferred (unless last)
+      }
+      dfr[j] = d;
+      bal[j] = __ballot_sync(0xFFFFFFFFu, d);
+      if (lane == 0) s_cnt[j * NW + wid] = __popc(bal[j]);
+    }
+    __syncthreads();
+    // ---- tile-local exclusive scan over (j, warp) in index order: warp 0
+    if (wid == 0) {
+      constexpr int PER = I * NW / 32;   // 4 entries per lane
+      int loc[PER];
+      int sum = 0;
+#pragma unroll
+      for (int q = 0; q < PER; ++q) {
+        loc[q] = s_cnt[lane * PER + q];
+        sum += loc[q];
+      }
+      int incl = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      int run = incl - sum;
+#pragma unroll
+      for (int q = 0; q < PER; ++q) {
+        s_off[lane * PER + q] = run;
+        run += loc[q];
+      }
+      const long long agg = __shfl_sync(0xFFFFFFFFu, incl, 31);
+      // ---- decoupled look-back for the deferred count before this tile
+      long long excl = 0;
+      if (tile == 0) {
+        if (lane == 0) st_release(&st[0], kFlagP | (unsigned long long)agg);
+      } else {
+        if (lane == 0) st_release(&st[tile], kFlagA | (unsigned long long)agg);
+        int64_t pred = tile - 1;
+        while (true) {
+          const int64_t idx = pred - lane;
+          unsigned long long d = (idx >= 0) ? ld_acquire(&st[idx]) : kFlagP;
+          while (__any_sync(0xFFFFFFFFu, (d >> 62) == 0)) {
+            if ((d >> 62) == 0) d = ld_acquire(&st[idx]);
+          }
+          const unsigned pm = __ballot_sync(0xFFFFFFFFu, (d >> 62) == 2);
+          long long val = (long long)(d & kValMask);
+          if (pm) {
+            const int first = __ffs(pm) - 1;
+            excl += warp_sum(lane <= first ? val : 0ll);
+            break;
+          }
+          excl += warp_sum(val);
+          pred -= 32;
+        }
+        if (lane == 0) st_release(&st[tile], kFlagP | (unsigned long long)(excl + agg));
+      }
+      if (lane == 0) s_excl = excl;
+    }
+    __syncthreads();
+    const long long excl = s_excl;
+    const long long acc_base = base - excl;   // accepted items before this tile
+    const unsigned lt = lanemask_lt();
+#pragma unroll
+    for (int j = 0; j < I; ++j) {
+      const int64_t i = base + (int64_t)j * T + tid;
+      if (i >= n) continue;
+      const int local = j * T + tid;
+      const int drank = s_off[j * NW + wid] + __popc(bal[j] & lt);
+      const int64_t id = a.ids ? a.ids[i] : i;
+      if (dfr[j]) {
+        const int64_t pos = excl + drank;
+        if (a.def_ids) a.def_ids[pos] = id;
+        if (a.def_pos) a.def_pos[pos] = i;
+      } else {
+        const int64_t pos = acc_base + (local - drank);
+        if (a.acc_ids) a.acc_ids[pos] = id;
+        if (a.acc_conf) a.acc_conf[pos] = a.conf[i];
+        if (a.acc_pred) {
+          for (int t = 0; t < a.pred_len; ++t)
+            a.acc_pred[pos * a.pred_len + t] = a.pred[i * a.pred_len + t];
+        }
+      }
+    }
+  }
+
+  // ---- completion: the last CTA publishes the counts and re-zeroes the workspace
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    const unsigned d = atomicAdd(&ws->done, 1u);
+    if (d == gridDim.x - 1) {
+      __threadfence();
+      long long tot_def = 0;
+      if (ntiles > 0) tot_def = (long long)(ld_acquire(&st[ntiles - 1]) & kValMask);
+      a.counts[0] = n - tot_def;
+      a.counts[1] = tot_def;
+      s_last = 1;
+    }
+  }
+  __syncthreads();
+  if (s_last) {
+    for (int64_t t = tid; t < ntiles; t += T) st[t] = 0ull;
+    if (tid == 0) {
+      ws->ticket = 0u;
+      ws->done = 0u;
+    }
+  }
+}
+
+// K4: dst[j] = src[pos[j]] for j < *d_count, rows of row_bytes (multiple of 16)
+__global__ void __launch_bounds__(256) gather_rows_kernel(const int64_t* __restrict__ pos,
+                                                          const int64_t* d_count, int64_t cap,
+                                                          const uint4* __restrict__ src,
+                                                          int64_t row_vec, uint4* __restrict__ dst) {
+  int64_t n = cap;
+  if (d_count) n = min(*d_count, cap);
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t j = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; j < n; j += nwarps) {
+    const uint4* s = src + pos[j] * row_vec;
+    uint4* d = dst + j * row_vec;
+    int64_t v = lane;
+    for (; v + 96 < row_vec; v += 128) {
+      const uint4 x0 = ldg_stream(s + v), x1 = ldg_stream(s + v + 32), x2 = ldg_stream(s + v + 64),
+                  x3 = ldg_stream(s + v + 96);
+      d[v] = x0;
+      d[v + 32] = x1;
+      d[v + 64] = x2;
+      d[v + 96] = x3;
+    }
+    for (; v < row_vec; v += 32) d[v] = ldg_stream(s + v);
+  }
+}
+
+}  // namespace
+
+size_t compact_ws_bytes(int64_t n) {
+  const int64_t tiles = (n + kCompactTile - 1) / kCompactTile;
+  return sizeof(CompactWs) + (size_t)(tiles > 0 ? tiles : 1) * sizeof(unsigned long long);
+}
+
+cudaError_t launch_route_compact(const CompactArgs& a, cudaStream_t s) {
+  const int64_t tiles = (a.n + kCompactTile - 1) / kCompactTile;
+  const int grid = (int)(tiles > 0 ? tiles : 1);
+  route_compact_kernel<<<grid, kCompactThreads, 0, s>>>(a);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gather_rows(const int64_t* pos, const int64_t* d_count, int64_t cap,
+                               const void* src, int64_t row_bytes, void* dst, cudaStream_t s) {
+  if (cap <= 0 || row_bytes <= 0) return cudaSuccess;
+  const int64_t want = (cap + 7) / 8;
+  const int64_t lim = (int64_t)num_sms() * 8;
+  const int grid = (int)(want < lim ? want : lim);
+  gather_rows_kernel<<<grid, 256, 0, s>>>(pos, d_count, cap, reinterpret_cast<const uint4*>(src),
+                                          row_bytes / 16, reinterpret_cast<uint4*>(dst));
+  count_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace hs

@@ -1,0 +1,90 @@
+// hs_internal.h -- launcher interfaces between the C-ABI layer (api.cu) and the
+// kernels (conf.cu, compact.cu, calib.cu).  Not part of the public ABI.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/hs.h"
+
+namespace hs {
+
+int num_sms();          // SM count of the current device (cached per device)
+void count_launch();    // bumps the process-wide launch counter (hs_launch_count)
+
+// ---- K1 / K2 ---------------------------------------------------------------
+struct ConfArgs {
+  const void* logits;
+  int64_t row_bytes;       // row_stride * element size (multiple of 16)
+  int64_t n;               // batch items (capacity when d_n != NULL)
+  int L;                   // tokens per item
+  int64_t C;               // classes
+  int nvec;                // 16-byte vectors covering C elements
+  int tail;                // C % elements-per-vector (0: last vector full)
+  const int64_t* row_index;
+  const int64_t* d_n;
+  float c;                 // log2(e) / T
+  int kind;                // hs_conf_kind_t
+  float* conf;             // [n*L] per token row
+  int32_t* argmax;         // [n*L] or NULL
+  const int32_t* labels;   // indexed by source token row, or NULL
+  uint8_t* ok;             // [n*L] argmax == label, or NULL
+  uint32_t* status;        // or NULL
+};
+cudaError_t launch_confidence(const ConfArgs& a, bool bf16, cudaStream_t s);
+cudaError_t launch_seq_reduce(const float* tok_conf, const uint8_t* tok_ok, int64_t n,
+                              const int64_t* d_n, int L, int reduce, float* conf,
+                              uint8_t* correct, cudaStream_t s);
+const char* confidence_path(int64_t nvec);
+
+// ---- K3 / K4 ---------------------------------------------------------------
+constexpr int kCompactThreads = 256;
+constexpr int kCompactItems = 16;
+constexpr int kCompactTile = kCompactThreads * kCompactItems;   // 4096 items per tile
+
+struct CompactWs {          // zero-filled between calls (the last CTA resets it)
+  unsigned int ticket;
+  unsigned int done;
+  unsigned long long pad[3];
+  // unsigned long long status[n_tiles] follows (32-byte header)
+};
+size_t compact_ws_bytes(int64_t n);
+
+struct CompactArgs {
+  const float* conf;
+  int64_t n;
+  const int64_t* d_n;
+  float threshold;
+  const float* d_threshold;   // overrides threshold when non-NULL
+  int is_last;
+  const int64_t* ids;
+  const int32_t* pred;
+  int pred_len;
+  int64_t* acc_ids;
+  float* acc_conf;
+  int32_t* acc_pred;
+  int64_t* def_ids;
+  int64_t* def_pos;
+  int64_t* counts;
+  void* ws;
+};
+cudaError_t launch_route_compact(const CompactArgs& a, cudaStream_t s);
+cudaError_t launch_gather_rows(const int64_t* pos, const int64_t* d_count, int64_t cap,
+                               const void* src, int64_t row_bytes, void* dst, cudaStream_t s);
+
+// ---- K5 / K6 ---------------------------------------------------------------
+struct CalibState {         // lives at the start of the calibration workspace
+  long long A;              // correct answers committed so far
+  long long tau;            // target correct count
+  int tau_ap;               // 1: tau = correct count of m_K (set in round 0)
+  int pad[11];
+};
+size_t calib_hist_bytes(int q);
+size_t calib_ws_bytes(int K, int q);
+cudaError_t launch_calib_init(void* ws, int q, long long target, cudaStream_t s);
+cudaError_t launch_calib_hist(const float* conf, const uint8_t* correct, int K, int64_t N, int q,
+                              int round, const int32_t* b_idx, int32_t* hist, cudaStream_t s);
+cudaError_t launch_calib_select(int K, int q, int round, int32_t* b_idx, float* thr,
+                                int64_t* reach, int64_t* handled, int64_t* correct_total,
+                                void* ws, cudaStream_t s);
+
+}  // namespace hs

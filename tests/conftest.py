@@ -24,3 +24,16 @@ def pytest_collection_modifyitems(config, items):
     for it in items:
         if "gpu" in it.keywords:
             it.add_marker(skip)
+
+
+@pytest.fixture(scope="session")
+def libhs():
+    """Build (if stale) and load libhs.so; the GPU box receives the in-tree build."""
+    from paper_2505_12566_b200 import _build
+    try:
+        _build.build_all()
+    except RuntimeError as e:  # no nvcc on this host: use the shipped .so
+        if not os.path.exists(_build.LIBHS):
+            raise
+    import paper_2505_12566_b200 as hs
+    return hs

@@ -1,0 +1,107 @@
+"""The C-ABI library loads and exports every symbol include/hs.h declares; the
+host-side argument validation works without a GPU (no compute calls here)."""
+import ctypes
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared():
+    src = open(os.path.join(ROOT, "include", "hs.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(hs_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_every_declared_symbol_is_exported(libhs):
+    from paper_2505_12566_b200 import _abi
+    lib = ctypes.CDLL(_abi.LIB_PATH)
+    names = _declared()
+    assert len(names) >= 15
+    for n in names:
+        assert hasattr(lib, n), n
+    assert set(names) == set(_abi.SIGNATURES), "binding and header disagree"
+
+
+def test_header_compiles_as_c(tmp_path):
+    c = tmp_path / "t.c"
+    c.write_text('#include "hs.h"\nint main(void){ return (int)sizeof(hs_status_t) - 4; }\n')
+    import subprocess
+    subprocess.check_call(["gcc", "-std=c99", "-Wall", "-Werror", "-I", os.path.join(ROOT, "include"),
+                           "-o", str(tmp_path / "t"), str(c)])
+    assert subprocess.call([str(tmp_path / "t")]) == 0
+
+
+def test_workspace_queries_are_pure(libhs):
+    lib = libhs.lib()
+    assert lib.hs_route_compact_workspace(0) > 0
+    assert lib.hs_route_compact_workspace(4096) == lib.hs_route_compact_workspace(1)
+    assert lib.hs_route_compact_workspace(4097) == lib.hs_route_compact_workspace(4096) + 8
+    assert lib.hs_confidence_workspace(100, 1) == 0
+    assert lib.hs_confidence_workspace(100, 64) >= 100 * 64 * 5
+    assert lib.hs_calibrate_workspace(5, 12) >= 3 * (4096 + 2) * 4
+    assert lib.hs_calibrate_workspace(5, 15) == 0
+    assert lib.hs_cascade_step_workspace(1000, 1) >= 1000 * (4 + 4 + 8)
+
+
+@pytest.mark.parametrize("kw,needle", [
+    (dict(C=1), "n_classes"),
+    (dict(T=0.0), "temperature"),
+    (dict(T=float("inf")), "temperature"),
+    (dict(L=0), "seq_len"),
+    (dict(L=2, reduce=0), "SEQ_NONE"),
+    (dict(stride=999), "row_stride"),
+    (dict(stride=1001), "16 bytes"),
+    (dict(ptr=8), "aligned"),
+])
+def test_confidence_argument_errors(libhs, kw, needle):
+    lib = libhs.lib()
+    C = kw.get("C", 1000)
+    rc = lib.hs_confidence(kw.get("ptr", 256), 1, 10, kw.get("L", 1), C, kw.get("stride", 1000), None,
+                           None, kw.get("T", 1.0), 0, kw.get("reduce", 0), 512, None, None, None,
+                           None, 0, None, None)
+    assert rc == 1
+    assert needle in lib.hs_last_error().decode()
+
+
+def test_route_and_calibrate_argument_errors(libhs):
+    lib = libhs.lib()
+    nan = float("nan")
+    for t in (nan, -0.1, 1.5):
+        rc = lib.hs_route_compact(256, 10, None, t, None, 0, None, None, 1, None, None, None, None,
+                                  None, None, 0, None, 512, 1024, 4096, None)
+        assert rc == 1 and "threshold" in lib.hs_last_error().decode()
+    rc = lib.hs_route_compact(256, 10, None, 0.5, None, 0, None, None, 1, None, None, None, None,
+                              None, None, 0, None, 512, 1024, 8, None)
+    assert rc == 5   # workspace too small
+    rc = lib.hs_calibrate_thresholds(256, 512, 1, 10, 12, -1, 0, 1, 2, 3, 4, 5, 1024, 1 << 20, None)
+    assert rc == 1 and "K" in lib.hs_last_error().decode()
+    rc = lib.hs_calibrate_thresholds(256, 512, 3, 10, 15, -1, 0, 1, 2, 3, 4, 5, 1024, 1 << 20, None)
+    assert rc == 1 and "log2_bins" in lib.hs_last_error().decode()
+    rc = lib.hs_calibrate_thresholds(256, 512, 3, 0, 12, -1, 0, 1, 2, 3, 4, 5, 1024, 1 << 20, None)
+    assert rc == 1 and "empty" in lib.hs_last_error().decode()
+    rc = lib.hs_calibrate_thresholds(256, 512, 3, 10, 12, -1, 2, 1, 2, 3, 4, 5, 1024, 1 << 20, None)
+    assert rc == 6   # refinement not on the GPU
+    rc = lib.hs_cascade_step(3, 3, 256, 1, 10, 1, 1000, 1000, None, None, 1.0, 0, 0, 0.5, None,
+                             None, None, 0, None, None, None, None, None, 512, 1024, 1 << 20,
+                             None, None)
+    assert rc == 1 and "stage" in lib.hs_last_error().decode()
+
+
+def test_status_strings(libhs):
+    lib = libhs.lib()
+    assert lib.hs_status_string(0) == b"HS_OK"
+    assert lib.hs_status_string(5) == b"HS_ERR_WORKSPACE_TOO_SMALL"
+    assert b"sm_100a" in lib.hs_build_info()
+
+
+def test_product_never_imports_oracle():
+    """The product package must not import, link or load the oracle (no CPU path)."""
+    pkg = os.path.join(ROOT, "paper_2505_12566_b200")
+    bad = re.compile(r"(import\s+oracle|from\s+oracle|hs_oracle|libhs_oracle|hso_)")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
+                assert not bad.search(open(os.path.join(dirpath, f)).read()), f

@@ -1,0 +1,430 @@
+"""GPU parity: the CUDA path (through the C-ABI) vs the fp64 CPU oracle on the
+same seeded inputs.  Tolerances (north_star): confidences within 1e-5 relative;
+argmax, correct bits, routing decisions, compacted lists and calibrated
+threshold indices bit-exact, except requests whose oracle confidence lies within
+1e-5 (relative) of a threshold, which are counted and excluded."""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from workload import synth
+
+pytestmark = pytest.mark.gpu
+
+REL = 1e-5
+
+
+@pytest.fixture(scope="module")
+def hs(libhs):
+    return libhs
+
+
+def dev():
+    return torch.device("cuda:0")
+
+
+def to_dev_bits(bits: np.ndarray, dtype: str, stride: int | None = None) -> torch.Tensor:
+    """numpy logits (raw bf16 bits or fp32) [rows, C] -> CUDA tensor [rows, stride]."""
+    rows, C = bits.shape
+    stride = stride or C
+    if dtype == "bf16":
+        t = torch.zeros(rows, stride, dtype=torch.int16)
+        t[:, :C] = torch.from_numpy(bits.view(np.int16))
+        return t.to(dev()).view(torch.bfloat16)
+    t = torch.zeros(rows, stride, dtype=torch.float32)
+    t[:, :C] = torch.from_numpy(bits)
+    return t.to(dev())
+
+
+def host_bits(x: torch.Tensor) -> np.ndarray:
+    if x.dtype == torch.bfloat16:
+        return x.view(torch.int16).cpu().numpy().view(np.uint16)
+    return x.cpu().numpy()
+
+
+def assert_conf_close(g: np.ndarray, o: np.ndarray):
+    g = g.astype(np.float64)
+    nan_o = np.isnan(o)
+    assert np.array_equal(np.isnan(g), nan_o), "NaN pattern differs"
+    err = np.abs(g[~nan_o] - o[~nan_o]) / np.maximum(np.abs(o[~nan_o]), 1e-300)
+    assert err.size == 0 or err.max() <= REL, f"max rel err {err.max():.3e}"
+    return 0.0 if err.size == 0 else float(err.max())
+
+
+def run_conf(hs, x, fam_like, n, L, C, T, kind, reduce, labels=None, row_index=None):
+    status = torch.zeros(1, dtype=torch.int32, device=dev())
+    lab = None if labels is None else torch.from_numpy(np.ascontiguousarray(labels, np.int32)).to(dev())
+    ri = None if row_index is None else torch.from_numpy(np.asarray(row_index, np.int64)).to(dev())
+    r = hs.confidence(x, n=n, seq_len=L, n_classes=C, temperature=T, kind=kind, reduce=reduce,
+                      labels=lab, row_index=ri, status=status)
+    torch.cuda.synchronize()
+    return r, int(status.item())
+
+
+def check_family(hs, fam, n, kinds=None, stride_pad=0, T=None):
+    ids = np.arange(n, dtype=np.int64) * 7 + 3
+    L, C = fam.L, fam.C
+    bits = synth.logits_np(fam.seed, 0, ids, L, C, fam.thr[0], fam.dtype)
+    lab = synth.labels_np(fam.seed, ids, L, C).reshape(-1)
+    eb = 2 if fam.dtype == "bf16" else 4
+    stride = C + stride_pad
+    x = to_dev_bits(bits, fam.dtype, stride)
+    worst = 0.0
+    for kind in (kinds or [fam.kind]):
+        T_ = T or fam.temps[0]
+        r, st = run_conf(hs, x, fam, n, L, C, T_, kind, fam.reduce, labels=lab)
+        ref = oracle.confidence(host_bits(x), n, L, C, stride, T_, kind=kind, reduce=fam.reduce,
+                                labels=lab)
+        assert st == 0
+        worst = max(worst, assert_conf_close(r["conf"].cpu().numpy(), ref["conf"]))
+        assert np.array_equal(r["argmax"].cpu().numpy(), ref["argmax"])
+        assert np.array_equal(r["correct"].cpu().numpy(), ref["correct"])
+    return worst
+
+
+# ---------------------------------------------------------------------------
+# K1/K2 confidence
+# ---------------------------------------------------------------------------
+def test_conf_c1_full_fp32(hs):
+    fam = synth.FAMILIES["c1"]
+    check_family(hs, fam, fam.n, kinds=[0, 1, 2])
+
+
+def test_conf_c2_bf16_all_kinds(hs):
+    check_family(hs, synth.FAMILIES["c2"], 9000, kinds=[0, 1, 2])
+
+
+@pytest.mark.parametrize("C", [2, 3, 8, 17, 255, 256, 257, 1000, 2047, 2048, 4096, 4100, 9000,
+                               32128])
+@pytest.mark.parametrize("dtype", ["bf16", "fp32"])
+def test_conf_class_counts_and_tails(hs, C, dtype):
+    """Every launch shape (warp-per-row NV=1..16, CTA-per-row) and ragged last vectors."""
+    ve = 8 if dtype == "bf16" else 4
+    pad = (-C) % ve
+    fam = synth.Family("t", 0, C, 1, dtype, (0.6,), (1.0,), 0, 0, 1)
+    n = 300 if C <= 4096 else 40
+    check_family(hs, fam, n, kinds=[0, 2], stride_pad=pad + (ve if C % 5 == 0 else 0))
+
+
+def test_conf_t5_sequences_min_mean(hs):
+    fam = synth.scaled(synth.FAMILIES["c3"], L=6)
+    for reduce in (1, 2):
+        f = synth.dataclasses.replace(fam, reduce=reduce)
+        check_family(hs, f, 48, kinds=[0, 1])
+
+
+def test_conf_llama_entropy_vocab(hs):
+    fam = synth.FAMILIES["c4"]
+    check_family(hs, fam, 24, kinds=[2, 0])
+
+
+@pytest.mark.parametrize("T", [0.05, 1.0, 20.0])
+def test_conf_temperatures(hs, T):
+    check_family(hs, synth.FAMILIES["c2"], 2000, kinds=[0, 2], T=T)
+
+
+def test_conf_adversarial_rows(hs):
+    C = 64
+    rows = []
+    rows.append(np.zeros(C))                                    # uniform, tie at 0
+    r = np.full(C, -3.0); r[[5, 9, 40]] = 7.0; rows.append(r)     # 3-way tie
+    r = np.full(C, -np.inf); r[[3, 4]] = 1.0; rows.append(r)     # masked classes
+    r = np.full(C, -np.inf); r[60] = -2.0; rows.append(r)        # one live class
+    r = np.zeros(C); r[0] = 1e30; rows.append(r)                 # huge (fp32 only)
+    r = np.linspace(-50, 50, C); rows.append(r)                  # ramp
+    r = np.zeros(C); r[7] = 88.0; rows.append(r)                 # saturated
+    r = np.zeros(C); r[1] = np.nan; rows.append(r)               # NaN -> invalid
+    r = np.zeros(C); r[2] = np.inf; rows.append(r)               # +inf -> invalid
+    rows.append(np.full(C, -np.inf))                             # all masked -> invalid
+    r = np.full(C, 1e-40); r[11] = 2e-40; rows.append(r)         # denormals
+    x32 = np.stack(rows).astype(np.float32)
+    for dtype in ("fp32", "bf16"):
+        bits = x32 if dtype == "fp32" else torch.from_numpy(x32).to(torch.bfloat16).view(torch.int16).numpy().view(np.uint16)
+        x = to_dev_bits(bits, dtype)
+        for kind in (0, 1, 2):
+            for T in (0.05, 1.0, 20.0):
+                r, st = run_conf(hs, x, None, len(rows), 1, C, T, kind, 0)
+                ref = oracle.confidence(host_bits(x), len(rows), 1, C, C, T, kind=kind)
+                assert st == 1, "invalid rows must set status bit 0"
+                assert_conf_close(r["conf"].cpu().numpy(), ref["conf"])
+                assert np.array_equal(r["argmax"].cpu().numpy(), ref["argmax"])
+
+
+def test_conf_row_index_and_dynamic_n(hs):
+    fam = synth.FAMILIES["c2"]
+    n_all = 5000
+    bits = synth.logits_np(fam.seed, 1, np.arange(n_all), 1, fam.C, fam.thr[1], "bf16")
+    x = to_dev_bits(bits, "bf16")
+    ri = np.sort(np.random.default_rng(0).choice(n_all, 1234, replace=False))
+    r, _ = run_conf(hs, x, fam, len(ri), 1, fam.C, 1.3, 0, 0, row_index=ri)
+    ref = oracle.confidence(bits, len(ri), 1, fam.C, fam.C, 1.3, row_index=ri)
+    assert_conf_close(r["conf"].cpu().numpy(), ref["conf"])
+    # device-side count: only the first d_n items are processed
+    d_n = torch.tensor([700], dtype=torch.int64, device=dev())
+    out = {"conf": torch.full((1234,), -7.0, device=dev())}
+    hs.confidence(x, n=1234, n_classes=fam.C, temperature=1.3, d_n=d_n, out=out,
+                  row_index=torch.from_numpy(ri).to(dev()))
+    g = out["conf"].cpu().numpy()
+    assert_conf_close(g[:700], ref["conf"][:700])
+    assert np.all(g[700:] == -7.0)
+
+
+def test_gpu_generator_matches_numpy(hs):
+    import workload
+    for key in ("c1", "c2", "c3", "c4"):
+        fam = synth.FAMILIES[key]
+        L = min(fam.L, 3)
+        f = synth.scaled(fam, L=L)
+        ids = np.array([0, 1, 5, 77, 1 << 33], np.int64)
+        want = synth.logits_np(f.seed, 1, ids, L, f.C, f.thr[1], f.dtype)
+        tdt = torch.bfloat16 if f.dtype == "bf16" else torch.float32
+        out = torch.empty(len(ids) * L, f.C, dtype=tdt, device=dev())
+        workload.gpu_logits(out, f, 1, ids=torch.from_numpy(ids).to(dev()))
+        assert np.array_equal(host_bits(out), want)
+        lab = torch.empty(len(ids) * L, dtype=torch.int32, device=dev())
+        workload.gpu_labels(lab, f, ids=torch.from_numpy(ids).to(dev()))
+        assert np.array_equal(lab.cpu().numpy(), synth.labels_np(f.seed, ids, L, f.C).reshape(-1))
+
+
+# ---------------------------------------------------------------------------
+# K3/K4 routing + compaction
+# ---------------------------------------------------------------------------
+def _route_ref(conf32: np.ndarray, t: float, is_last: bool):
+    return oracle.route(conf32.astype(np.float64), float(np.float32(t)), is_last)
+
+
+@pytest.mark.parametrize("n", [0, 1, 31, 4095, 4096, 4097, 12289, 262144])
+def test_route_compact_exact(hs, n):
+    rng = np.random.default_rng(n)
+    c = rng.uniform(size=n).astype(np.float32)
+    if n:
+        c[rng.uniform(size=n) < 0.02] = np.nan
+        c[rng.uniform(size=n) < 0.05] = np.float32(0.5)         # exact ties with t
+    cd = torch.from_numpy(c).to(dev())
+    ids = torch.from_numpy(rng.integers(0, 1 << 40, size=n)).to(dev())
+    pred = torch.from_numpy(rng.integers(0, 1000, size=3 * n).astype(np.int32)).to(dev())
+    payload = torch.from_numpy(rng.integers(0, 255, size=(n, 48), dtype=np.uint8)).to(dev())
+    ws = hs.workspace(hs.lib().hs_route_compact_workspace(n), dev())
+    for t, last in ((0.5, False), (0.0, False), (1.0, False), (math.inf, False), (0.3, True)):
+        o = hs.route_compact(cd, t, is_last=last, ids=ids, pred=pred, pred_len=3, payload=payload,
+                             ws=ws)
+        torch.cuda.synchronize()
+        acc, dfr = _route_ref(c, t, last)
+        na, nd = o["counts"].cpu().tolist()
+        assert (na, nd) == (len(acc), len(dfr))
+        idh = ids.cpu().numpy()
+        assert np.array_equal(o["acc_ids"][:na].cpu().numpy(), idh[acc])
+        assert np.array_equal(o["def_ids"][:nd].cpu().numpy(), idh[dfr])
+        assert np.array_equal(o["def_pos"][:nd].cpu().numpy(), dfr)
+        np.testing.assert_array_equal(o["acc_conf"][:na].cpu().numpy(), c[acc])
+        assert np.array_equal(o["acc_pred"][:3 * na].cpu().numpy().reshape(-1, 3),
+                              pred.cpu().numpy().reshape(-1, 3)[acc])
+        if not last:
+            assert np.array_equal(o["def_payload"][:nd].cpu().numpy(), payload.cpu().numpy()[dfr])
+    # the workspace is left zeroed (decoupled look-back descriptors reset by the last CTA)
+    assert int(ws.sum().item()) == 0
+
+
+def test_route_device_threshold_and_count(hs):
+    rng = np.random.default_rng(5)
+    n = 20000
+    c = rng.uniform(size=n).astype(np.float32)
+    cd = torch.from_numpy(c).to(dev())
+    d_n = torch.tensor([15000], dtype=torch.int64, device=dev())
+    d_t = torch.tensor([0.625], dtype=torch.float32, device=dev())
+    o = hs.route_compact(cd, d_t, n=n, d_n=d_n)
+    torch.cuda.synchronize()
+    acc, dfr = _route_ref(c[:15000], 0.625, False)
+    assert o["counts"].cpu().tolist() == [len(acc), len(dfr)]
+    assert np.array_equal(o["acc_ids"][:len(acc)].cpu().numpy(), acc)
+
+
+# ---------------------------------------------------------------------------
+# Whole cascade (K1 -> K3 -> K4 per stage, device-resident counts/thresholds)
+# ---------------------------------------------------------------------------
+def near_mask(conf_by_stage, t):
+    near = np.zeros(conf_by_stage.shape[1], bool)
+    for k in range(len(t) - 1):
+        if np.isfinite(t[k]):
+            near |= np.abs(conf_by_stage[k] - t[k]) <= REL * t[k]
+    return near
+
+
+@pytest.mark.parametrize("key,n", [("c1", 4096), ("c2", 20000), ("c4", 96)])
+def test_cascade_vs_oracle(hs, key, n):
+    fam = synth.FAMILIES[key]
+    K = fam.K
+    ids = np.arange(n, dtype=np.int64)
+    logits, conf_o = [], []
+    for k in range(K):
+        bits = synth.logits_np(fam.seed, k, ids, fam.L, fam.C, fam.thr[k], fam.dtype)
+        logits.append(to_dev_bits(bits, fam.dtype))
+        conf_o.append(oracle.confidence(bits, n, fam.L, fam.C, fam.C, fam.temps[k], kind=fam.kind,
+                                        reduce=fam.reduce)["conf"])
+    conf_o = np.stack(conf_o)
+    rng = np.random.default_rng(1)
+    t = np.sort(rng.uniform(0.2, 0.9, size=K - 1)).astype(np.float32).tolist() + [0.0]
+    P = 64
+    payload = torch.from_numpy(rng.integers(0, 255, size=(n, P), dtype=np.uint8)).to(dev())
+    casc = hs.Cascade(n, [hs.StageSpec(fam.C, fam.temps[k], fam.L, fam.kind, fam.reduce)
+                          for k in range(K)], dev(), payload_row_bytes=P)
+    casc.route(logits, t, payload=payload)
+    res = casc.results()
+    tt = np.array(t, np.float64)
+    stage_of = oracle.cascade(conf_o, tt)
+    lists = oracle.stage_lists(stage_of, K)
+    near = near_mask(conf_o, tt)
+    for k in range(K):
+        got = res[k]["ids"].numpy()
+        want = lists[k][1]
+        assert np.array_equal(got[~near[got]], want[~near[want]])
+        if k < K - 1 and not near.any():
+            batch_next = lists[k][2]
+            nd = res[k]["n_def"]
+            pl = casc.outs[k]["next_payload"][:nd * P].cpu().numpy().reshape(nd, P)
+            assert np.array_equal(pl, payload.cpu().numpy()[batch_next])
+
+
+# ---------------------------------------------------------------------------
+# K5/K6 calibration
+# ---------------------------------------------------------------------------
+def _gpu_val(hs, fam, n_val):
+    K = fam.K
+    vids = np.arange(n_val, dtype=np.int64) + synth.VAL_ID_BASE
+    lab = synth.labels_np(fam.seed, vids, fam.L, fam.C).reshape(-1)
+    lab_d = torch.from_numpy(lab).to(dev())
+    vconf = torch.empty(K - 1, n_val, dtype=torch.float32, device=dev())
+    vok = torch.empty(K, n_val, dtype=torch.uint8, device=dev())
+    oconf = np.empty((K - 1, n_val))
+    for k in range(K):
+        bits = synth.logits_np(fam.seed, k, vids, fam.L, fam.C, fam.thr[k], fam.dtype)
+        x = to_dev_bits(bits, fam.dtype)
+        r = hs.confidence(x, n=n_val, seq_len=fam.L, temperature=fam.temps[k], kind=fam.kind,
+                          reduce=fam.reduce, labels=lab_d)
+        vok[k] = r["correct"]
+        if k < K - 1:
+            vconf[k] = r["conf"]
+            oconf[k] = oracle.confidence(bits, n_val, fam.L, fam.C, fam.C, fam.temps[k],
+                                         kind=fam.kind, reduce=fam.reduce)["conf"]
+    return vconf, vok, oconf
+
+
+@pytest.mark.parametrize("key,n_val,q", [("c1", 4096, 12), ("c2", 50000, 12), ("c2", 3000, 4),
+                                         ("c2", 777, 14), ("c4", 256, 10)])
+def test_calibration_bit_exact(hs, key, n_val, q):
+    fam = synth.FAMILIES[key]
+    vconf, vok, oconf = _gpu_val(hs, fam, n_val)
+    g = hs.calibrate_thresholds(vconf, vok, log2_bins=q)
+    torch.cuda.synchronize()
+    gc, gk = vconf.cpu().numpy(), vok.cpu().numpy()
+    # (i) oracle on the GPU's confidences and correct bits: bit-exact, no exceptions
+    ref = oracle.calibrate(gc, gk, q)
+    assert np.array_equal(g["b"].cpu().numpy(), ref["b"])
+    assert np.array_equal(g["reach"].cpu().numpy(), ref["reach"])
+    assert np.array_equal(g["handled"].cpu().numpy(), ref["handled"])
+    assert int(g["correct_total"].item()) == ref["correct_total"] >= ref["tau"]
+    assert np.array_equal(g["t"].cpu().numpy().astype(np.float64), ref["t"])
+    # (ii) oracle on its own fp64 confidences: equal unless a sample sits within 1e-5 of a bin edge
+    own = oracle.calibrate(oconf, gk, q)
+    B = 1 << q
+    edge = np.abs(oconf * B - np.round(oconf * B)) <= REL * np.maximum(oconf * B, 1e-30)
+    if not edge.any():
+        assert np.array_equal(own["b"], ref["b"])
+
+
+def test_calibration_blocks_equal_full_call(hs):
+    fam = synth.FAMILIES["c2"]
+    vconf, vok, _ = _gpu_val(hs, fam, 6000)
+    q, K = 11, fam.K
+    full = hs.calibrate_thresholds(vconf, vok, log2_bins=q, target=4000)
+    ws = hs.calibrate_workspace(K, q, dev())
+    out = hs._calib_out(K, dev(), None)
+    hs.calibrate_begin(K, q, 4000, ws)
+    for k in range(K - 1):
+        # two "ranks": each adds its shard's histogram (sum == one big histogram)
+        hs.calibrate_histogram(vconf[:, :2500].contiguous(), vok[:, :2500].contiguous(), k,
+                               out["b"], log2_bins=q, ws=ws)
+        hs.calibrate_histogram(vconf[:, 2500:].contiguous(), vok[:, 2500:].contiguous(), k,
+                               out["b"], log2_bins=q, ws=ws)
+        hs.calibrate_select(K, k, out, log2_bins=q, ws=ws)
+    torch.cuda.synchronize()
+    for key in ("b", "t", "reach", "handled", "correct_total"):
+        assert torch.equal(full[key], out[key]), key
+
+
+def test_calibration_degenerate(hs):
+    # c = 1.0 exactly is reachable: only defer-all (b = B+1, t = +inf) rejects it (G11)
+    conf = torch.tensor([[1.0, 1.0, 0.5]], device=dev())
+    ok = torch.tensor([[0, 0, 1], [1, 1, 1]], dtype=torch.uint8, device=dev())
+    g = hs.calibrate_thresholds(conf, ok, log2_bins=3)
+    assert g["b"].item() == 9 and math.isinf(g["t"][0].item()) and g["correct_total"].item() == 3
+    # NaN confidences are never accepted
+    conf = torch.tensor([[float("nan"), 0.9]], device=dev())
+    ok = torch.tensor([[1, 1], [0, 1]], dtype=torch.uint8, device=dev())
+    g = hs.calibrate_thresholds(conf, ok, log2_bins=4)
+    ref = oracle.calibrate(conf.cpu().numpy(), ok.cpu().numpy(), 4)
+    assert g["b"].cpu().tolist() == ref["b"].tolist() and g["handled"].cpu().tolist() == ref["handled"].tolist()
+
+
+# ---------------------------------------------------------------------------
+# Full BASELINE sizes, in the launch configuration bench.py times
+# ---------------------------------------------------------------------------
+def test_full_size_c2_sampled(hs):
+    import workload
+    fam = synth.FAMILIES["c2"]
+    n = fam.n
+    x = torch.empty(n, fam.C, dtype=torch.bfloat16, device=dev())
+    workload.gpu_logits(x, fam, 0, id_base=0, n=n)
+    r = hs.confidence(x, temperature=fam.temps[0])
+    torch.cuda.synchronize()
+    rows = np.sort(np.random.default_rng(2).choice(n, 3000, replace=False))
+    sample = host_bits(x[torch.from_numpy(rows).to(dev())])
+    ref = oracle.confidence(sample, len(rows), 1, fam.C, fam.C, fam.temps[0])
+    assert_conf_close(r["conf"].cpu().numpy()[rows], ref["conf"])
+    assert np.array_equal(r["argmax"].cpu().numpy()[rows], ref["argmax"])
+    # full-size compaction on these confidences is exact integer work: compare all of it
+    c = r["conf"].cpu().numpy()
+    o = hs.route_compact(r["conf"], 0.7)
+    torch.cuda.synchronize()
+    acc, dfr = _route_ref(c, 0.7, False)
+    assert o["counts"].cpu().tolist() == [len(acc), len(dfr)]
+    assert np.array_equal(o["def_ids"][:len(dfr)].cpu().numpy(), dfr)
+
+
+def test_full_size_c4_sampled(hs):
+    import workload
+    fam = synth.FAMILIES["c4"]
+    n = fam.n
+    x = torch.empty(n, fam.C, dtype=torch.bfloat16, device=dev())
+    workload.gpu_logits(x, fam, 0, id_base=0, n=n)
+    r = hs.confidence(x, temperature=fam.temps[0], kind="entropy")
+    torch.cuda.synchronize()
+    rows = np.sort(np.random.default_rng(3).choice(n, 64, replace=False))
+    sample = host_bits(x[torch.from_numpy(rows).to(dev())])
+    ref = oracle.confidence(sample, len(rows), 1, fam.C, fam.C, fam.temps[0], kind=oracle.ENTROPY)
+    assert_conf_close(r["conf"].cpu().numpy()[rows], ref["conf"])
+    assert np.array_equal(r["argmax"].cpu().numpy()[rows], ref["argmax"])
+    del x
+
+
+def test_c3_sequences_sampled_launch_config(hs):
+    """T5: 64 tokens x 32,128 vocab per sequence, MIN/MEAN; sampled sequences of the full id range."""
+    import workload
+    fam = synth.FAMILIES["c3"]
+    ids = np.sort(np.random.default_rng(4).choice(fam.n, 24, replace=False)).astype(np.int64)
+    x = torch.empty(len(ids) * fam.L, fam.C, dtype=torch.bfloat16, device=dev())
+    workload.gpu_logits(x, fam, 2, ids=torch.from_numpy(ids).to(dev()))
+    lab = torch.empty(len(ids) * fam.L, dtype=torch.int32, device=dev())
+    workload.gpu_labels(lab, fam, ids=torch.from_numpy(ids).to(dev()))
+    for reduce in ("min", "mean"):
+        r = hs.confidence(x, n=len(ids), seq_len=fam.L, temperature=1.0, reduce=reduce, labels=lab)
+        torch.cuda.synchronize()
+        ref = oracle.confidence(host_bits(x), len(ids), fam.L, fam.C, fam.C, 1.0,
+                                reduce=oracle.SEQ_MIN if reduce == "min" else oracle.SEQ_MEAN,
+                                labels=lab.cpu().numpy())
+        assert_conf_close(r["conf"].cpu().numpy(), ref["conf"])
+        assert np.array_equal(r["argmax"].cpu().numpy(), ref["argmax"])
+        assert np.array_equal(r["correct"].cpu().numpy(), ref["correct"])
