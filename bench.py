@@ -1,0 +1,482 @@
+"""bench.py -- HybridServe cascade router on B200: requests routed/s and logits HBM GB/s.
+
+One step = one pass of the whole hot path over one batch:
+  (1) confidence of every stage model on the validation shard (K launches),
+  (2) AP threshold calibration (histogram + select per round; NCCL all-reduce of
+      the integer histograms when N > 1),
+  (3) routing of the request batch through the K-stage cascade with the
+      device-resident thresholds: per stage confidence -> threshold test ->
+      stable compaction (+ gather).
+Inputs are resident in HBM (per-stage logits indexed by request id, generated
+by the seeded keyed generator before timing); the working set (~3 GB at C2) is
+far larger than the 126 MB L2, so no flush is needed between steps.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl reference]
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "requests routed/sec and logits HBM GB/s (% of peak) at 1/2/4/8 B200"
+CONFIG_TEXT = {
+    "c1": "2-stage ViT-S->ViT-L cascade, 4,096 requests x 1,000 classes fp32, calibrated on 4,096 validation samples",
+    "c2": "5-stage ViT family cascade, 262,144 requests x 1,000 classes bf16 per GPU, thresholds calibrated on 50,000 validation samples",
+    "c4": "3-stage Llama-like next-token cascade, 8,192 requests x 128,256 vocab bf16 per GPU, entropy confidence, 8 KB hidden-state payload gathered",
+    "c5": "5-stage ViT streaming cascade, 1,048,576 requests x 1,000 classes bf16 per GPU (8M over 8 GPUs), validation 131,072 per GPU",
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIG_TEXT))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy burst)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region (NVML sampled every ~5 ms in a thread)
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+               0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown", 0x1: "gpu_idle"}
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and bit != 0x1:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.nv:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                    "samples": 0}
+        s = sorted(self.samples)
+        return {"sm_mhz": s[len(s) // 2], "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(s)}
+
+
+# ---------------------------------------------------------------------------
+# distributed plumbing
+# ---------------------------------------------------------------------------
+def init_dist(args):
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sum_over_ranks(x, world: int):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor(x, dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return t.tolist()
+
+
+# ---------------------------------------------------------------------------
+# workload (per rank): weak scaling -- every rank routes its own shard
+# ---------------------------------------------------------------------------
+def family(config: str):
+    from workload import synth
+    f = synth.FAMILIES[config]
+    if config == "c5":
+        f = synth.scaled(f, n=1 << 20, n_val=1 << 17)
+    return f
+
+
+def build_inputs(fam, rank: int, dev):
+    import torch
+    import workload
+    from workload import synth
+    tdt = torch.bfloat16 if fam.dtype == "bf16" else torch.float32
+    K = fam.K
+    id0 = rank * fam.n
+    vid0 = synth.VAL_ID_BASE + rank * fam.n_val
+    # route logits: stage k's model output for every request id of this shard (row = id - id0)
+    route = []
+    for k in range(K):
+        x = torch.empty(fam.n * fam.L, fam.C, dtype=tdt, device=dev)
+        workload.gpu_logits(x, fam, k, id_base=id0, n=fam.n)
+        route.append(x)
+    val = []
+    for k in range(K):
+        x = torch.empty(fam.n_val * fam.L, fam.C, dtype=tdt, device=dev)
+        workload.gpu_logits(x, fam, k, id_base=vid0, n=fam.n_val)
+        val.append(x)
+    labels = torch.empty(fam.n_val * fam.L, dtype=torch.int32, device=dev)
+    workload.gpu_labels(labels, fam, id_base=vid0, n=fam.n_val)
+    payload = None
+    if fam.payload_bytes:
+        payload = torch.randint(0, 255, (fam.n, fam.payload_bytes), dtype=torch.uint8, device=dev)
+    torch.cuda.synchronize()
+    return route, val, labels, payload
+
+
+def make_router(fam, dev, group):
+    import paper_2505_12566_b200 as hs
+    from paper_2505_12566_b200.router import Router
+    stages = [hs.StageSpec(fam.C, fam.temps[k], fam.L, fam.kind, fam.reduce) for k in range(fam.K)]
+    return Router(stages, fam.n, fam.n_val, dev, log2_bins=fam.log2_bins,
+                  payload_row_bytes=fam.payload_bytes, group=group)
+
+
+def timing_event():
+    """A timing event usable inside a captured CUDA graph (recorded as an
+    external event node), so the dominant kernel is timed inside the step."""
+    import torch
+    try:
+        return torch.cuda.Event(enable_timing=True, external=True)
+    except TypeError:
+        return torch.cuda.Event(enable_timing=True)
+
+
+def run_ours(args, world, rank, local):
+    import torch
+    import torch.distributed as dist
+    import paper_2505_12566_b200 as hs
+
+    dev = torch.device("cuda", local)
+    fam = family(args.config)
+    group = dist.group.WORLD if world > 1 else None
+    route, val, labels, payload = build_inputs(fam, rank, dev)
+    router = make_router(fam, dev, group)
+    ev = (timing_event(), timing_event())
+
+    def step():
+        router.calibrate(val, labels)
+        router.route(route, payload=payload, time_stage0=ev)
+
+    stream = torch.cuda.Stream(device=dev)
+    torch.cuda.synchronize()
+    with torch.cuda.stream(stream):
+        for _ in range(max(args.warmup, 3)):
+            step()
+    torch.cuda.synchronize()
+    use_graph = not args.no_graph
+    graph = None
+    launches_per_step = None
+    if use_graph:
+        try:
+            l0 = hs.launch_count()
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph, stream=stream):
+                step()
+            launches_per_step = hs.launch_count() - l0
+            graph.replay()
+            torch.cuda.synchronize()
+        except Exception as e:  # collectives that cannot be captured: eager timing
+            print(f"[bench] graph capture failed ({e}); timing eagerly", file=sys.stderr)
+            graph = None
+            torch.cuda.synchronize()
+    l_before = hs.launch_count()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    k_ms = []
+    barrier(world)
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        with torch.cuda.stream(stream):
+            t0.record(stream)
+            for _ in range(args.steps):
+                if graph is not None:
+                    graph.replay()
+                else:
+                    step()
+            t1.record(stream)
+        torch.cuda.synchronize()
+    barrier(world)
+    total_ms = t0.elapsed_time(t1)
+    clocks = clk.summary()
+    gpu_launches = (launches_per_step * args.steps) if graph is not None else (hs.launch_count() - l_before)
+    # per-launch duration of the dominant kernel: one more timed pass, recording each step's events
+    k_ms = []
+    with torch.cuda.stream(stream):
+        for _ in range(min(args.steps, 50)):
+            if graph is not None:
+                graph.replay()
+            else:
+                step()
+            stream.synchronize()
+            k_ms.append(ev[0].elapsed_time(ev[1]))
+    kernel_ms = sum(k_ms) / len(k_ms)
+    ms = max_over_ranks(total_ms, world) / args.steps
+    # cascade statistics (identical every step): reach per stage
+    counts = router.cascade.counts.cpu().tolist()
+    reach = [fam.n] + [c[1] for c in counts[:-1]]
+    st = int(router.status.item())
+    # algorithmic bytes of one step (logits dominate): validation sweep + reach-weighted routing
+    row_b = fam.row_bytes
+    val_bytes = fam.K * fam.n_val * row_b
+    route_bytes = sum(reach) * row_b
+    step_bytes = val_bytes + route_bytes
+    step_bytes_all = sum_over_ranks([float(step_bytes)], world)[0]
+    n_all = fam.n * world
+    value = n_all / (ms / 1e3)
+    peak, peak_src = peaks()
+    # dominant kernel: stage-1 confidence over this rank's batch: n rows x (row bytes + 8 B out)
+    k_bytes = fam.n * (row_b + 8)
+    achieved = k_bytes / (kernel_ms / 1e3) / 1e9
+    e2e = run_e2e(args, fam, router, route, val, labels, payload, stream, world)
+    line = {
+        "metric": METRIC, "value": value, "unit": "requests/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": fam.name, "description": CONFIG_TEXT[args.config],
+                   "requests_per_gpu": fam.n, "validation_per_gpu": fam.n_val, "K": fam.K,
+                   "classes": fam.C, "seq_len": fam.L, "logits_dtype": fam.dtype,
+                   "confidence": ["maxprob", "maxprob_sq", "entropy"][fam.kind],
+                   "log2_bins": fam.log2_bins, "parallelism": f"request-sharded dp{world}",
+                   "l2": "inputs larger than L2 (per-step logits working set >> 126 MB)",
+                   "cuda_graph": graph is not None},
+        "logits_GBps": step_bytes_all / (ms / 1e3) / 1e9,
+        "logits_frac_of_peak": step_bytes_all / world / (ms / 1e3) / 1e9 / peak,
+        "reach": reach, "thresholds": router.cal["t"].cpu().tolist(), "status": st,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": None,
+                     "kernel": "conf_warp_kernel (stage-1 confidence, K1)",
+                     "bytes_per_launch": k_bytes, "avg_launch_ms": kernel_ms,
+                     "peak_source": peak_src},
+        "e2e": e2e, "gpu_launches": gpu_launches, "clocks": clocks,
+        "gpu_launches_per_step": gpu_launches / args.steps,
+    }
+    return line, fam, route, val, labels
+
+
+def run_e2e(args, fam, router, route, val, labels, payload, stream, world):
+    """Same metric through the public API from pinned HOST buffers: every step copies
+    its inputs host->device and reads the per-request results back."""
+    import torch
+    steps = max(1, args.e2e_steps)
+    host_route = [x.cpu().pin_memory() for x in route]
+    host_val = [x.cpu().pin_memory() for x in val]
+    host_lab = labels.cpu().pin_memory()
+    host_pay = payload.cpu().pin_memory() if payload is not None else None
+    outs = router.cascade.outs
+    res_host = [torch.empty(fam.n * 8, dtype=torch.uint8).pin_memory() for _ in outs]
+    cnt_host = torch.empty(fam.K, 2, dtype=torch.int64).pin_memory()
+    h2d = sum(x.numel() * x.element_size() for x in host_route + host_val) + \
+        host_lab.numel() * 4 + (host_pay.numel() if host_pay is not None else 0)
+    d2h = 0
+
+    def once():
+        nonlocal d2h
+        for d, h in zip(route, host_route):
+            d.copy_(h, non_blocking=True)
+        for d, h in zip(val, host_val):
+            d.copy_(h, non_blocking=True)
+        labels.copy_(host_lab, non_blocking=True)
+        if payload is not None:
+            payload.copy_(host_pay, non_blocking=True)
+        router.calibrate(val, labels)
+        router.route(route, payload=payload)
+        cnt_host.copy_(router.cascade.counts, non_blocking=True)
+        # accepted ids of every stage (the answers' request ids)
+        for o, h in zip(outs, res_host):
+            h.view(torch.int64).copy_(o["acc_ids"], non_blocking=True)
+        d2h = cnt_host.numel() * 8 + sum(h.numel() for h in res_host)
+
+    with torch.cuda.stream(stream):
+        once()
+    torch.cuda.synchronize()
+    barrier(world)
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        t0.record(stream)
+        for _ in range(steps):
+            once()
+        t1.record(stream)
+    torch.cuda.synchronize()
+    ms = max_over_ranks(t0.elapsed_time(t1), world) / steps
+    return {"value": fam.n * world / (ms / 1e3), "unit": "requests/s",
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": ms,
+            "steps": steps}
+
+
+# ---------------------------------------------------------------------------
+# the oracle on the host cores (cpu_baseline leg and --impl reference)
+# ---------------------------------------------------------------------------
+def oracle_step(fam, frac_n: int, frac_val: int, seed_off: int = 0):
+    """One bounded oracle step on host-generated bytes of the same workload:
+    validation confidences of every stage -> calibration -> cascade routing.
+    Returns (seconds of oracle work, requests routed)."""
+    import numpy as np
+    import oracle
+    from workload import synth
+    K = fam.K
+    ids = np.arange(frac_n, dtype=np.int64) + seed_off
+    vids = np.arange(frac_val, dtype=np.int64) + synth.VAL_ID_BASE
+    lab = synth.labels_np(fam.seed, vids, fam.L, fam.C).reshape(-1)
+    vl = [synth.logits_np(fam.seed, k, vids, fam.L, fam.C, fam.thr[k], fam.dtype) for k in range(K)]
+    rl = [synth.logits_np(fam.seed, k, ids, fam.L, fam.C, fam.thr[k], fam.dtype) for k in range(K)]
+    t = time.perf_counter()
+    conf = np.empty((K - 1, frac_val))
+    ok = np.empty((K, frac_val), np.uint8)
+    for k in range(K):
+        r = oracle.confidence(vl[k], frac_val, fam.L, fam.C, fam.C, fam.temps[k], kind=fam.kind,
+                              reduce=fam.reduce, labels=lab)
+        ok[k] = r["correct"]
+        if k < K - 1:
+            conf[k] = r["conf"]
+    cal = oracle.calibrate(conf, ok, fam.log2_bins)
+    batch = np.arange(frac_n, dtype=np.int64)
+    for k in range(K):
+        r = oracle.confidence(rl[k], len(batch), fam.L, fam.C, fam.C, fam.temps[k], kind=fam.kind,
+                              reduce=fam.reduce, row_index=batch)
+        acc, dfr = oracle.route(r["conf"], float(np.float32(cal["t"][k])), k == K - 1)
+        batch = batch[dfr]
+    return time.perf_counter() - t, frac_n
+
+
+def cpu_sample_sizes(fam, seconds: float):
+    """Scale the oracle sample so one step takes ~`seconds` on this host."""
+    n0 = min(fam.n, 2048)
+    v0 = max(64, int(n0 * fam.n_val / fam.n))
+    dt, _ = oracle_step(fam, n0, v0)
+    scale = max(1.0, seconds / max(dt, 1e-3))
+    n = int(min(fam.n, n0 * scale))
+    v = int(min(fam.n_val, max(64, n * fam.n_val / fam.n)))
+    return n, v
+
+
+def cpu_baseline(fam, seconds: float):
+    n, v = cpu_sample_sizes(fam, seconds)
+    dt, routed = oracle_step(fam, n, v)
+    return {"value": routed / dt, "unit": "requests/s", "cores": os.cpu_count(), "kind": "oracle",
+            "sample": f"{n} of {fam.n} requests + {v} of {fam.n_val} validation samples of "
+                      f"{fam.name} (same generator), fp64 C oracle, {dt:.1f} s"}
+
+
+def run_reference(args, world, rank):
+    """--impl reference: the oracle as it stands, on host cores, K bounded steps."""
+    if rank != 0:
+        return None
+    fam = family(args.config)
+    budget = 150.0 / max(1, args.steps + args.warmup)
+    n, v = cpu_sample_sizes(fam, min(budget, 20.0))
+    for _ in range(args.warmup):
+        oracle_step(fam, n, v)
+    tot = 0.0
+    routed = 0
+    for _ in range(args.steps):
+        dt, r = oracle_step(fam, n, v)
+        tot += dt
+        routed += r
+    value = routed / tot
+    ms = tot / args.steps * 1e3
+    sample = f"{n} of {fam.n} requests + {v} of {fam.n_val} validation samples of {fam.name} per step"
+    return {"impl": "reference", "metric": METRIC, "value": value, "unit": "requests/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": fam.name, "description": CONFIG_TEXT[args.config],
+                       "requests_per_gpu": fam.n, "validation_per_gpu": fam.n_val, "K": fam.K,
+                       "classes": fam.C, "logits_dtype": fam.dtype,
+                       "parallelism": "host cores (oracle)"},
+            "cpu_baseline": {"value": value, "unit": "requests/s", "cores": os.cpu_count(),
+                             "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": "requests/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if args.impl == "reference":
+        line = run_reference(args, world, rank)
+        if line is not None:
+            print(json.dumps(line), flush=True)
+        return
+    world, rank, local = init_dist(args)
+    line, fam, *_ = run_ours(args, world, rank, local)
+    if rank == 0:
+        if world == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline(fam, args.cpu_seconds)
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -130,19 +130,26 @@ def route_compact(conf: torch.Tensor, threshold: float | torch.Tensor, *, is_las
     n = int(conf.numel() if n is None else n)
     dev = conf.device
     out = dict(out or {})
-    out.setdefault("acc_ids", torch.empty(n, dtype=torch.int64, device=dev))
-    out.setdefault("acc_conf", torch.empty(n, dtype=torch.float32, device=dev))
+    if "acc_ids" not in out:
+        out["acc_ids"] = torch.empty(n, dtype=torch.int64, device=dev)
+    if "acc_conf" not in out:
+        out["acc_conf"] = torch.empty(n, dtype=torch.float32, device=dev)
     if pred is not None:
-        out.setdefault("acc_pred", torch.empty(n * pred_len, dtype=torch.int32, device=dev))
-    out.setdefault("def_ids", torch.empty(n, dtype=torch.int64, device=dev))
-    out.setdefault("def_pos", torch.empty(n, dtype=torch.int64, device=dev))
+        if "acc_pred" not in out:
+            out["acc_pred"] = torch.empty(n * pred_len, dtype=torch.int32, device=dev)
+    if "def_ids" not in out:
+        out["def_ids"] = torch.empty(n, dtype=torch.int64, device=dev)
+    if "def_pos" not in out:
+        out["def_pos"] = torch.empty(n, dtype=torch.int64, device=dev)
     P = 0
     if payload is not None:
         P = payload.element_size()
         for d in payload.shape[1:]:
             P *= int(d)
-        out.setdefault("def_payload", torch.empty_like(payload))
-    out.setdefault("counts", torch.zeros(2, dtype=torch.int64, device=dev))
+        if "def_payload" not in out:
+            out["def_payload"] = torch.empty_like(payload)
+    if "counts" not in out:
+        out["counts"] = torch.zeros(2, dtype=torch.int64, device=dev)
     need = lib().hs_route_compact_workspace(n)
     if ws is None:
         ws = workspace(need, dev)
@@ -170,13 +177,19 @@ def cascade_step(stage: int, n_stages: int, logits: torch.Tensor, threshold, *, 
     C = int(n_classes or logits.shape[1])
     dev = logits.device
     out = dict(out or {})
-    out.setdefault("acc_ids", torch.empty(n, dtype=torch.int64, device=dev))
-    out.setdefault("acc_conf", torch.empty(n, dtype=torch.float32, device=dev))
-    out.setdefault("acc_pred", torch.empty(n * seq_len, dtype=torch.int32, device=dev))
-    out.setdefault("next_ids", torch.empty(n, dtype=torch.int64, device=dev))
+    if "acc_ids" not in out:
+        out["acc_ids"] = torch.empty(n, dtype=torch.int64, device=dev)
+    if "acc_conf" not in out:
+        out["acc_conf"] = torch.empty(n, dtype=torch.float32, device=dev)
+    if "acc_pred" not in out:
+        out["acc_pred"] = torch.empty(n * seq_len, dtype=torch.int32, device=dev)
+    if "next_ids" not in out:
+        out["next_ids"] = torch.empty(n, dtype=torch.int64, device=dev)
     if payload is not None and payload_row_bytes > 0:
-        out.setdefault("next_payload", torch.empty(n * payload_row_bytes, dtype=torch.uint8, device=dev))
-    out.setdefault("counts", torch.zeros(2, dtype=torch.int64, device=dev))
+        if "next_payload" not in out:
+            out["next_payload"] = torch.empty(n * payload_row_bytes, dtype=torch.uint8, device=dev)
+    if "counts" not in out:
+        out["counts"] = torch.zeros(2, dtype=torch.int64, device=dev)
     need = lib().hs_cascade_step_workspace(n, seq_len)
     if ws is None:
         ws = workspace(need, dev)
@@ -196,11 +209,16 @@ def cascade_step(stage: int, n_stages: int, logits: torch.Tensor, threshold, *, 
 # ---------------------------------------------------------------------------
 def _calib_out(K: int, dev, out: dict | None):
     out = dict(out or {})
-    out.setdefault("b", torch.empty(K - 1, dtype=torch.int32, device=dev))
-    out.setdefault("t", torch.empty(K, dtype=torch.float32, device=dev))
-    out.setdefault("reach", torch.empty(K, dtype=torch.int64, device=dev))
-    out.setdefault("handled", torch.empty(K, dtype=torch.int64, device=dev))
-    out.setdefault("correct_total", torch.empty(1, dtype=torch.int64, device=dev))
+    if "b" not in out:
+        out["b"] = torch.empty(K - 1, dtype=torch.int32, device=dev)
+    if "t" not in out:
+        out["t"] = torch.empty(K, dtype=torch.float32, device=dev)
+    if "reach" not in out:
+        out["reach"] = torch.empty(K, dtype=torch.int64, device=dev)
+    if "handled" not in out:
+        out["handled"] = torch.empty(K, dtype=torch.int64, device=dev)
+    if "correct_total" not in out:
+        out["correct_total"] = torch.empty(1, dtype=torch.int64, device=dev)
     return out
 
 

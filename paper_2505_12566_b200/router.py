@@ -1,0 +1,120 @@
+"""The user-facing router: calibrate thresholds on a validation set, then route
+batches through the cascade -- a sequence of C-ABI calls, nothing else.
+
+One ``Router`` per GPU.  With a ``torch.distributed`` process group the
+validation set and the request stream are sharded over the ranks: the only
+exchange is the integer calibration histogram, summed with an all-reduce
+between ``hs_calibrate_histogram`` and ``hs_calibrate_select`` (order-independent
+count merging), so every rank selects identical thresholds.  Forwarding
+deferred requests to other ranks is in ``dist.py``.
+"""
+from __future__ import annotations
+
+import torch
+
+from . import (Cascade, StageSpec, _calib_out, calibrate_begin, calibrate_hist_view,
+               calibrate_histogram, calibrate_select, calibrate_thresholds,
+               calibrate_workspace, confidence, cascade_step, route_compact)
+
+
+class Router:
+    def __init__(self, stages: list[StageSpec], n_cap: int, n_val: int, device, *,
+                 log2_bins: int = 12, payload_row_bytes: int = 0, group=None):
+        self.stages = stages
+        self.K = len(stages)
+        self.n_cap = int(n_cap)
+        self.n_val = int(n_val)
+        self.q = int(log2_bins)
+        self.device = torch.device(device)
+        self.group = group
+        dev = self.device
+        K = self.K
+        self.vconf = torch.empty(K - 1, self.n_val, dtype=torch.float32, device=dev)
+        self.vok = torch.empty(K, self.n_val, dtype=torch.uint8, device=dev)
+        self.vconf_last = torch.empty(self.n_val, dtype=torch.float32, device=dev)
+        L = max(s.seq_len for s in stages)
+        self.vargmax = torch.empty(self.n_val * L, dtype=torch.int32, device=dev)
+        self.conf_ws = torch.empty(max(1, self.n_val * L * 5 + 1024), dtype=torch.uint8, device=dev)
+        self.cal = _calib_out(K, dev, None)
+        self.cal_ws = calibrate_workspace(K, self.q, dev)
+        self.status = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.cascade = Cascade(self.n_cap, stages, dev, payload_row_bytes)
+        self.cascade.status = self.status
+
+    # ---- offline: Alg. 1 / AP thresholds -----------------------
+    def calibrate(self, val_logits: list, labels: torch.Tensor, *, target: int = -1,
+                  stream=None) -> dict:
+        """val_logits[k]: stage k's logits of the validation shard ([n_val*L, stride]);
+        labels: int32 [n_val*L].  Thresholds stay on the device (self.cal['t'])."""
+        for k, s in enumerate(self.stages):
+            out = {"conf": self.vconf[k] if k < self.K - 1 else self.vconf_last,
+                   "argmax": self.vargmax[: self.n_val * s.seq_len], "correct": self.vok[k]}
+            confidence(val_logits[k], n=self.n_val, seq_len=s.seq_len, n_classes=s.n_classes,
+                       temperature=s.temperature, kind=s.kind, reduce=s.reduce, labels=labels,
+                       out=out, ws=self.conf_ws, status=self.status, stream=stream)
+        if self.group is None:
+            calibrate_thresholds(self.vconf, self.vok, log2_bins=self.q, target=target,
+                                 out=self.cal, ws=self.cal_ws, stream=stream)
+        else:
+            import torch.distributed as dist
+            hist = calibrate_hist_view(self.cal_ws, self.q)
+            calibrate_begin(self.K, self.q, target, self.cal_ws, stream=stream)
+            for k in range(self.K - 1):
+                calibrate_histogram(self.vconf, self.vok, k, self.cal["b"], log2_bins=self.q,
+                                    ws=self.cal_ws, stream=stream)
+                dist.all_reduce(hist, op=dist.ReduceOp.SUM, group=self.group)
+                calibrate_select(self.K, k, self.cal, log2_bins=self.q, ws=self.cal_ws,
+                                 stream=stream)
+        return self.cal
+
+    # ---- online: the cascade ------------------------------------
+    def route(self, logits: list, *, n: int | None = None, ids=None, payload=None,
+              by_id: bool = True, thresholds=None, time_stage0=None, stream=None):
+        """Route a batch; thresholds default to the calibrated device vector."""
+        thr = self.cal["t"] if thresholds is None else thresholds
+        if time_stage0 is None:
+            self.cascade.route(logits, thr, n=n, ids=ids, payload=payload, by_id=by_id,
+                               stream=stream)
+        else:
+            self._route_timed(logits, thr, n, ids, payload, by_id, time_stage0, stream)
+        return self.cascade
+
+    def _route_timed(self, logits, thr, n, ids, payload, by_id, events, stream):
+        """Same kernels as Cascade.route, with stage 0 split into hs_confidence +
+        hs_route_compact so CUDA events can bracket the confidence kernel alone."""
+        c = self.cascade
+        n = c.n_cap if n is None else int(n)
+        s0 = self.stages[0]
+        o0 = c.outs[0]
+        d_thr = thr if isinstance(thr, torch.Tensor) else None
+        t0 = d_thr[0:1] if d_thr is not None else float(thr[0])
+        if not hasattr(self, "_s0"):
+            self._s0 = {"conf": torch.empty(n, dtype=torch.float32, device=self.device),
+                        "argmax": torch.empty(n * s0.seq_len, dtype=torch.int32, device=self.device)}
+            self._s0_ws = torch.empty(max(16, n * s0.seq_len * 5 + 1024), dtype=torch.uint8,
+                                      device=self.device)
+            self._s0_cws = torch.zeros(1 << 20, dtype=torch.uint8, device=self.device)
+        events[0].record()
+        confidence(logits[0], n=n, seq_len=s0.seq_len, n_classes=s0.n_classes,
+                   temperature=s0.temperature, kind=s0.kind, reduce=s0.reduce,
+                   row_index=ids if by_id else None, out=self._s0, ws=self._s0_ws,
+                   status=self.status, stream=stream)
+        events[1].record()
+        route_compact(self._s0["conf"], t0, is_last=self.K == 1, n=n, ids=ids,
+                      pred=self._s0["argmax"], pred_len=s0.seq_len, payload=payload,
+                      out={"acc_ids": o0["acc_ids"], "acc_conf": o0["acc_conf"],
+                           "acc_pred": o0["acc_pred"], "def_ids": o0["next_ids"],
+                           "def_pos": self._s0.setdefault("pos", torch.empty(n, dtype=torch.int64, device=self.device)),
+                           "counts": o0["counts"],
+                           **({"def_payload": o0["next_payload"].view(n, -1)} if payload is not None and "next_payload" in o0 else {})},
+                      ws=self._s0_cws, stream=stream)
+        for k in range(1, self.K):
+            s = self.stages[k]
+            prev = c.outs[k - 1]
+            thr_k = d_thr[k:k + 1] if d_thr is not None else float(thr[k] if k < self.K - 1 else 0.0)
+            cascade_step(k, self.K, logits[k], thr_k, n=n, seq_len=s.seq_len,
+                         n_classes=s.n_classes, temperature=s.temperature, kind=s.kind,
+                         reduce=s.reduce, row_index=prev["next_ids"] if by_id else None,
+                         d_n=prev["counts"][1:2], ids=prev["next_ids"],
+                         payload=prev.get("next_payload"), payload_row_bytes=c.P,
+                         out=c.outs[k], ws=c.ws, status=self.status, stream=stream)
