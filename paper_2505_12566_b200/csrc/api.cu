@@ -6,6 +6,7 @@
 #include <cstdarg>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -368,6 +369,11 @@ hs_status_t hs_calibrate_thresholds(const float* conf, const uint8_t* correct, i
   if (!conf || !correct) return fail(HS_ERR_INVALID_ARGUMENT, "NULL input");
   if (!d_bin_idx || !d_thresholds || !d_reach || !d_handled || !d_correct_total)
     return fail(HS_ERR_INVALID_ARGUMENT, "NULL output");
+  if (!getenv("HS_CALIB_SPLIT"))   // one cooperative launch for all rounds
+    return cuda_check(hs::launch_calib_fused(conf, correct, K, N, log2_bins, target_correct,
+                                             d_bin_idx, d_thresholds, d_reach, d_handled,
+                                             d_correct_total, ws, (cudaStream_t)stream),
+                      "calib fused (cooperative) kernel");
   st = hs_calibrate_begin(K, log2_bins, target_correct, ws, ws_bytes, stream);
   for (int k = 0; st == HS_OK && k < K - 1; ++k) {
     st = hs_calibrate_histogram(conf, correct, K, N, log2_bins, k, d_bin_idx, ws, ws_bytes, stream);

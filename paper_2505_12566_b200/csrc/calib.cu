@@ -14,10 +14,14 @@
 //       examined), then A += committed correct answers; reach/handled counts.
 // Histograms are integers, so a request-sharded calibration sums them across
 // GPUs (all-reduce) and every rank selects the same b_k.
+#include <cooperative_groups.h>
+
 #include "hs_common.cuh"
 #include "hs_internal.h"
 
 namespace hs {
+
+namespace cg = cooperative_groups;
 
 namespace {
 
@@ -39,12 +43,11 @@ __global__ void calib_init_kernel(CalibState* st, int32_t* hist, int nwords, lon
 }
 
 // hist layout: int32 [3][B+2]; index 0 = NaN bin (never accepted), index b+1 = bin b.
-__global__ void __launch_bounds__(512) calib_hist_kernel(const float* __restrict__ conf,
-                                                         const uint8_t* __restrict__ correct,
-                                                         int K, int64_t N, int q, int round,
-                                                         const int32_t* __restrict__ b_idx,
-                                                         int32_t* __restrict__ hist) {
-  extern __shared__ unsigned long long sh[];
+// One CTA's share (grid-stride) of round `round`, added into the global histogram.
+__device__ __forceinline__ void hist_body(const float* __restrict__ conf,
+                                          const uint8_t* __restrict__ correct, int K, int64_t N,
+                                          int q, int round, const int32_t* b_idx,
+                                          int32_t* __restrict__ hist, unsigned long long* sh) {
   const int nb = (1 << q) + 2;
   for (int i = threadIdx.x; i < nb; i += blockDim.x) sh[i] = 0ull;
   int bprev[16];
@@ -95,14 +98,23 @@ __global__ void __launch_bounds__(512) calib_hist_kernel(const float* __restrict
   }
 }
 
-// One CTA of 1024 threads.  Each thread owns a contiguous segment of bins
+__global__ void __launch_bounds__(512) calib_hist_kernel(const float* __restrict__ conf,
+                                                         const uint8_t* __restrict__ correct,
+                                                         int K, int64_t N, int q, int round,
+                                                         const int32_t* __restrict__ b_idx,
+                                                         int32_t* __restrict__ hist) {
+  extern __shared__ unsigned long long sh[];
+  hist_body(conf, correct, K, N, q, round, b_idx, hist, sh);
+}
+
+// One CTA of NT threads.  Each thread owns a contiguous segment of bins
 // 0..B (hist index b+1); suffix sums come from a block scan of segment totals.
-__global__ void __launch_bounds__(1024) calib_select_kernel(int K, int q, int round,
-                                                            int32_t* b_idx, float* thr,
-                                                            int64_t* reach, int64_t* handled,
-                                                            int64_t* correct_total,
-                                                            CalibState* st, int32_t* hist) {
-  constexpr int NT = 1024, NW = NT / 32;
+template <int NT>
+__device__ __forceinline__ void select_body(int K, int q, int round, int32_t* b_idx, float* thr,
+                                            int64_t* reach, int64_t* handled,
+                                            int64_t* correct_total, CalibState* st,
+                                            int32_t* hist) {
+  constexpr int NW = NT / 32;
   __shared__ long long sh_w[NW];
   __shared__ long long sh_tot[3];
   __shared__ int sh_b;
@@ -214,6 +226,43 @@ __global__ void __launch_bounds__(1024) calib_select_kernel(int K, int q, int ro
   for (int i = tid; i < 3 * nb; i += NT) hist[i] = 0;
 }
 
+__global__ void __launch_bounds__(1024) calib_select_kernel(int K, int q, int round,
+                                                            int32_t* b_idx, float* thr,
+                                                            int64_t* reach, int64_t* handled,
+                                                            int64_t* correct_total,
+                                                            CalibState* st, int32_t* hist) {
+  select_body<1024>(K, q, round, b_idx, thr, reach, handled, correct_total, st, hist);
+}
+
+// All K-1 rounds in one cooperative launch (single GPU): histogram by every
+// CTA -> grid barrier -> select by CTA 0 -> grid barrier -> next round.
+__global__ void __launch_bounds__(1024) calib_fused_kernel(const float* __restrict__ conf,
+                                                           const uint8_t* __restrict__ correct,
+                                                           int K, int64_t N, int q, long long target,
+                                                           int32_t* b_idx, float* thr,
+                                                           int64_t* reach, int64_t* handled,
+                                                           int64_t* correct_total, CalibState* st,
+                                                           int32_t* hist) {
+  extern __shared__ unsigned long long sh[];
+  cg::grid_group grid = cg::this_grid();
+  if (blockIdx.x == 0) {
+    const int nw = 3 * ((1 << q) + 2);
+    for (int i = threadIdx.x; i < nw; i += blockDim.x) hist[i] = 0;
+    if (threadIdx.x == 0) {
+      st->A = 0;
+      st->tau = target < 0 ? 0 : target;
+      st->tau_ap = target < 0 ? 1 : 0;
+    }
+  }
+  grid.sync();
+  for (int k = 0; k < K - 1; ++k) {
+    hist_body(conf, correct, K, N, q, k, b_idx, hist, sh);
+    grid.sync();
+    if (blockIdx.x == 0) select_body<1024>(K, q, k, b_idx, thr, reach, handled, correct_total, st, hist);
+    grid.sync();
+  }
+}
+
 }  // namespace
 
 size_t calib_hist_bytes(int q) { return (size_t)3 * ((1u << q) + 2) * sizeof(int32_t); }
@@ -252,6 +301,35 @@ cudaError_t launch_calib_hist(const float* conf, const uint8_t* correct, int K, 
   calib_hist_kernel<<<(int)grid, 512, smem, s>>>(conf, correct, K, N, q, round, b_idx, hist);
   count_launch();
   return cudaGetLastError();
+}
+
+cudaError_t launch_calib_fused(const float* conf, const uint8_t* correct, int K, int64_t N, int q,
+                               long long target, int32_t* b_idx, float* thr, int64_t* reach,
+                               int64_t* handled, int64_t* correct_total, void* ws,
+                               cudaStream_t s) {
+  const size_t smem = (size_t)((1 << q) + 2) * sizeof(unsigned long long);
+  static int max_blocks = -1;
+  if (max_blocks < 0) {
+    cudaFuncSetAttribute(calib_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(((1 << 14) + 2) * sizeof(unsigned long long)));
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, calib_fused_kernel, 1024,
+                                                  ((1 << 14) + 2) * sizeof(unsigned long long));
+    max_blocks = per_sm > 0 ? per_sm * num_sms() : 0;
+  }
+  int grid = (int)((N + 1023) / 1024);
+  if (grid > num_sms()) grid = num_sms();
+  if (grid > max_blocks) grid = max_blocks;
+  if (grid < 1) grid = 1;
+  CalibState* st = reinterpret_cast<CalibState*>(ws);
+  int32_t* hist = hist_of(ws);
+  void* args[] = {(void*)&conf, (void*)&correct, (void*)&K, (void*)&N, (void*)&q, (void*)&target,
+                  (void*)&b_idx, (void*)&thr, (void*)&reach, (void*)&handled,
+                  (void*)&correct_total, (void*)&st, (void*)&hist};
+  cudaError_t e = cudaLaunchCooperativeKernel((void*)calib_fused_kernel, dim3(grid), dim3(1024),
+                                              args, smem, s);
+  count_launch();
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 cudaError_t launch_calib_select(int K, int q, int round, int32_t* b_idx, float* thr,

@@ -23,6 +23,8 @@
 //     online (max, sum, weighted sum) over 8-vector chunks, block merge
 //     (vocabulary-sized rows: T5 32,128, Llama 128,256).
 #include <cuda_bf16.h>
+#include <cstdlib>
+#include <cstring>
 
 #include "hs_common.cuh"
 #include "hs_internal.h"
@@ -36,6 +38,7 @@ struct RowOut {
   float s;     // sum 2^a
   float w;     // sum 2^a * a
   uint32_t am; // argmax
+  float e0;    // 2^a of the max element (1 when a is formed as (x - m) * c)
 };
 
 __device__ __forceinline__ void write_row(const ConfArgs& a, int64_t row, int64_t src_row,
@@ -48,11 +51,12 @@ __device__ __forceinline__ void write_row(const ConfArgs& a, int64_t row, int64_
     am = -1;
     if (a.status) atomicOr(a.status, HS_STATUS_NONFINITE);
   } else {
-    const float p = 1.0f / r.s;
+    const float p = r.e0 / r.s;
     if (a.kind == HS_CONF_MAXPROB_SQ) {
       c = p * p;
     } else if (a.kind == HS_CONF_ENTROPY) {
-      // exp(-H) = (1/s) * 2^{w/s} = 2^{w/s - log2 s}; full-precision exp2f/log2f
+      // exp(-H) = 2^{w/s - log2 s} (invariant to a common shift of every a);
+      // full-precision exp2f/log2f
       c = exp2f(r.w / r.s - log2f(r.s));
     } else {
       c = p;
@@ -78,21 +82,25 @@ __device__ __forceinline__ int64_t live_rows(const ConfArgs& a) {
   return n * a.L;
 }
 
-// -inf for out-of-row lanes of the last partial 16-byte vector
+__device__ __forceinline__ uint32_t word(const uint4& v, int q) {
+  return q == 0 ? v.x : q == 1 ? v.y : q == 2 ? v.z : v.w;
+}
+
+// -inf for the out-of-row elements of the last partial 16-byte vector
+// (value semantics only: no address is taken, so nothing spills to local memory)
 template <bool BF16>
-__device__ __forceinline__ void mask_tail(uint4& v, int tail) {
-  uint32_t* w = reinterpret_cast<uint32_t*>(&v);
+__device__ __forceinline__ uint32_t mask_word(uint32_t w, int q, int tail) {
   if (BF16) {
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      if (2 * q >= tail) w[q] = kBf16NegInf2;
-      else if (2 * q + 1 >= tail) w[q] = (w[q] & 0xFFFFu) | 0xFF800000u;
-    }
-  } else {
-#pragma unroll
-    for (int q = 0; q < 4; ++q)
-      if (q >= tail) w[q] = kF32NegInf;
+    const uint32_t lo = (2 * q < tail) ? (w & 0xFFFFu) : 0xFF80u;
+    const uint32_t hi = (2 * q + 1 < tail) ? (w & 0xFFFF0000u) : 0xFF800000u;
+    return lo | hi;
   }
+  return (q < tail) ? w : kF32NegInf;
+}
+template <bool BF16>
+__device__ __forceinline__ uint4 masked(const uint4& v, int tail) {
+  return make_uint4(mask_word<BF16>(v.x, 0, tail), mask_word<BF16>(v.y, 1, tail),
+                    mask_word<BF16>(v.z, 2, tail), mask_word<BF16>(v.w, 3, tail));
 }
 
 template <bool BF16>
@@ -100,7 +108,7 @@ __device__ __forceinline__ uint4 load_vec(const uint4* p, int vi, int nvec, int 
   uint4 v;
   if (vi < nvec) {
     v = ldg_stream(p + vi);
-    if (tail && vi == nvec - 1) mask_tail<BF16>(v, tail);
+    if (tail && vi == nvec - 1) v = masked<BF16>(v, tail);
   } else {
     const uint32_t f = BF16 ? kBf16NegInf2 : kF32NegInf;
     v = make_uint4(f, f, f, f);
@@ -123,18 +131,16 @@ __device__ __forceinline__ float vec_max(const uint4& v) {
 // first element (0..VE-1) of v equal to m, VE if none
 template <bool BF16>
 __device__ __forceinline__ int vec_first_eq(const uint4& v, float m) {
-  const uint32_t* w = reinterpret_cast<const uint32_t*>(&v);
   int r = BF16 ? 8 : 4;
-  if (BF16) {
 #pragma unroll
-    for (int q = 3; q >= 0; --q) {
-      if (bf_hi(w[q]) == m) r = 2 * q + 1;
-      if (bf_lo(w[q]) == m) r = 2 * q;
+  for (int q = 3; q >= 0; --q) {
+    const uint32_t w = word(v, q);
+    if (BF16) {
+      if (bf_hi(w) == m) r = 2 * q + 1;
+      if (bf_lo(w) == m) r = 2 * q;
+    } else {
+      if (__uint_as_float(w) == m) r = q;
     }
-  } else {
-#pragma unroll
-    for (int q = 3; q >= 0; --q)
-      if (__uint_as_float(w[q]) == m) r = q;
   }
   return r;
 }
@@ -143,11 +149,10 @@ __device__ __forceinline__ int vec_first_eq(const uint4& v, float m) {
 template <bool BF16, bool ENTROPY>
 __device__ __forceinline__ void vec_accum(const uint4& v, f2_t m2, f2_t c2, uint32_t clampw,
                                           f2_t& s2, f2_t& w2) {
-  const uint32_t* w = reinterpret_cast<const uint32_t*>(&v);
   if (BF16) {
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      uint32_t u = ENTROPY ? bmax2_plain(w[q], clampw) : w[q];
+      uint32_t u = ENTROPY ? bmax2_plain(word(v, q), clampw) : word(v, q);
       f2_t a = f2mul(f2sub(f2(bf_lo(u), bf_hi(u)), m2), c2);
       f2_t e = f2(ex2(f2lo(a)), ex2(f2hi(a)));
       s2 = f2add(s2, e);
@@ -156,9 +161,42 @@ __device__ __forceinline__ void vec_accum(const uint4& v, f2_t m2, f2_t c2, uint
   } else {
 #pragma unroll
     for (int q = 0; q < 2; ++q) {
-      f2_t a = f2mul(f2sub(f2(__uint_as_float(w[2 * q]), __uint_as_float(w[2 * q + 1])), m2), c2);
+      f2_t a = f2mul(f2sub(f2(__uint_as_float(word(v, 2 * q)), __uint_as_float(word(v, 2 * q + 1))), m2), c2);
       float a0 = f2lo(a), a1 = f2hi(a);
       if (ENTROPY) {  // -inf (masked) logits: keep 2^a * a = 0 instead of 0 * -inf
+        a0 = fmaxf(a0, -128.f);
+        a1 = fmaxf(a1, -128.f);
+        a = f2(a0, a1);
+      }
+      f2_t e = f2(ex2(a0), ex2(a1));
+      s2 = f2add(s2, e);
+      if (ENTROPY) w2 = f2fma(e, a, w2);
+    }
+  }
+}
+
+// Same, with a = x * c - RN(m * c) in ONE packed FFMA2 per element pair: every
+// exponent carries the same shift d = m*c - RN(m*c) (|d| <= ulp(m*c)/2) plus
+// one rounding, and d cancels exactly in p_max = 2^{a_max} / sum 2^a and in
+// H = log2(s) - w/s, so the fold costs no accuracy.
+template <bool BF16, bool ENTROPY>
+__device__ __forceinline__ void vec_accum_fma(const uint4& v, f2_t nmc2, f2_t c2, uint32_t clampw,
+                                              f2_t& s2, f2_t& w2) {
+  if (BF16) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      uint32_t u = ENTROPY ? bmax2_plain(word(v, q), clampw) : word(v, q);
+      f2_t a = f2fma(f2(bf_lo(u), bf_hi(u)), c2, nmc2);
+      f2_t e = f2(ex2(f2lo(a)), ex2(f2hi(a)));
+      s2 = f2add(s2, e);
+      if (ENTROPY) w2 = f2fma(e, a, w2);
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      f2_t a = f2fma(f2(__uint_as_float(word(v, 2 * q)), __uint_as_float(word(v, 2 * q + 1))), c2, nmc2);
+      float a0 = f2lo(a), a1 = f2hi(a);
+      if (ENTROPY) {
         a0 = fmaxf(a0, -128.f);
         a1 = fmaxf(a1, -128.f);
         a = f2(a0, a1);
@@ -183,92 +221,258 @@ __device__ __forceinline__ uint32_t entropy_clamp_word(float m, float c) {
 }
 
 // ---------------------------------------------------------------------------
-// K1a: one warp per row, row in registers.
+// K1a: G lanes per row (a warp reduces 32/G rows at once), row in registers.
+// Lane j of a group holds the row's 16-byte vectors j, j+G, j+2G, ... (NV of
+// them), so one warp instruction advances 32/G rows and the per-row costs
+// (shuffle trees, argmax, output) are amortised over G*NV*VE elements/lane.
 // ---------------------------------------------------------------------------
-template <bool BF16, bool ENTROPY, int NV>
+// NaN-propagating max of one vector kept as a bf16x2 word (bf16) or fp32
+template <bool BF16>
+__device__ __forceinline__ uint32_t vec_maxw(const uint4& v) {
+  if (BF16) return bmax2(bmax2(v.x, v.y), bmax2(v.z, v.w));
+  return __float_as_uint(fmax3_nan(__uint_as_float(v.x), __uint_as_float(v.y),
+                                   fmax_nan(__uint_as_float(v.z), __uint_as_float(v.w))));
+}
+// does the vector whose max word is w contain the value m (m2w: m as bf16x2)?
+template <bool BF16>
+__device__ __forceinline__ bool maxw_has(uint32_t w, float m, uint32_t m2w) {
+  if (BF16) {
+    uint32_t r;
+    asm("{\n\t.reg .pred p, q;\n\tsetp.eq.bf16x2 p|q, %1, %2;\n\tor.pred p, p, q;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(r) : "r"(w), "r"(m2w));
+    return r != 0;
+  }
+  return __uint_as_float(w) == m;
+}
+
+template <bool BF16, int NV, int G>
+__device__ __forceinline__ void group_mask_tail(uint4 (&v)[NV], int gl, int nvec, int tail) {
+  const int last = nvec - 1;
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    const bool p = (k * G + gl) == last;
+    const uint4 m = masked<BF16>(v[k], tail);
+    v[k] = make_uint4(p ? m.x : v[k].x, p ? m.y : v[k].y, p ? m.z : v[k].z, p ? m.w : v[k].w);
+  }
+}
+
+template <bool BF16, bool ENTROPY, int NV, int G>
+__device__ __forceinline__ void group_reduce_row(const ConfArgs& a, const uint4 (&v)[NV],
+                                                 bool active, int64_t row, int64_t src, int gl,
+                                                 f2_t c2) {
+  constexpr int VE = BF16 ? 8 : 4;
+  const float c = a.c;
+  // 1. row max (exact, NaN-propagating): packed per-vector maxima, then the group
+  uint32_t vmw[NV];
+  uint32_t lw = vec_maxw<BF16>(v[0]);
+  vmw[0] = lw;
+#pragma unroll
+  for (int k = 1; k < NV; ++k) {
+    vmw[k] = vec_maxw<BF16>(v[k]);
+    lw = BF16 ? bmax2(lw, vmw[k]) : __float_as_uint(fmax_nan(__uint_as_float(lw), __uint_as_float(vmw[k])));
+  }
+  float m = BF16 ? fmax_nan(bf_lo(lw), bf_hi(lw)) : __uint_as_float(lw);
+#pragma unroll
+  for (int o = G / 2; o > 0; o >>= 1) m = fmax_nan(m, __shfl_xor_sync(0xFFFFFFFFu, m, o));
+
+  // 2. argmax: lowest vector index holding m, then the first element in it
+  const uint32_t mb = __float_as_uint(m) >> 16;
+  const uint32_t m2w = mb | (mb << 16);
+  unsigned vi = 0xFFFFFFFFu;
+#pragma unroll
+  for (int k = NV - 1; k >= 0; --k)
+    if (maxw_has<BF16>(vmw[k], m, m2w)) vi = (unsigned)(k * G + gl);
+#pragma unroll
+  for (int o = G / 2; o > 0; o >>= 1) vi = min(vi, (unsigned)__shfl_xor_sync(0xFFFFFFFFu, vi, o));
+  const int owner = (int)(vi % G), kstar = (int)(vi / G);
+  int e = 0;
+  if (gl == owner && vi != 0xFFFFFFFFu) {
+    uint4 sel = v[0];
+#pragma unroll
+    for (int k = 1; k < NV; ++k)
+      if (k == kstar) sel = v[k];
+    e = vec_first_eq<BF16>(sel, m);
+  }
+  e = __shfl_sync(0xFFFFFFFFu, e, owner, G);
+  const unsigned am = vi * VE + (unsigned)e;
+
+  // 3. exponentials with the common max: a = x*c - RN(m*c) (one FFMA2 per pair)
+  f2_t s2 = f2(0.f, 0.f), w2 = f2(0.f, 0.f);
+  const bool valid = (m < INFINITY) && (m > -INFINITY);
+  const float nmc = -(m * c);
+  if (valid) {
+    const f2_t nmc2 = f2(nmc, nmc);
+    const uint32_t cw = ENTROPY && BF16 ? entropy_clamp_word(m, c) : 0u;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) vec_accum_fma<BF16, ENTROPY>(v[k], nmc2, c2, cw, s2, w2);
+  }
+  float s = f2lo(s2) + f2hi(s2);
+  float w = ENTROPY ? f2lo(w2) + f2hi(w2) : 0.f;
+#pragma unroll
+  for (int o = G / 2; o > 0; o >>= 1) {
+    s += __shfl_xor_sync(0xFFFFFFFFu, s, o);
+    if (ENTROPY) w += __shfl_xor_sync(0xFFFFFFFFu, w, o);
+  }
+  if (active && gl == 0) {
+    RowOut r{m, s, w, am, ex2(fmaf(m, c, nmc))};
+    write_row(a, row, src, r);
+  }
+}
+
+template <bool L1>
+__device__ __forceinline__ int64_t src_row(const ConfArgs& a, int64_t r) {
+  if (!a.row_index) return r;
+  if (L1) return a.row_index[r];
+  return a.row_index[r / a.L] * a.L + r % a.L;
+}
+
+// predicated 16-byte loads of one group's row, all issued back to back
+template <bool BF16, int NV, int G>
+__device__ __forceinline__ void group_load_row(uint4 (&v)[NV], const uint4* p, int gl, int nvec,
+                                               bool active) {
+  const uint32_t f = BF16 ? kBf16NegInf2 : kF32NegInf;
+  const int lim = active ? nvec : 0;
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    const int vi = k * G + gl;
+    uint4 r = make_uint4(f, f, f, f);
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.lt.s32 p, %4, %5;\n\t"
+        "@p ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%6];\n\t}"
+        : "+r"(r.x), "+r"(r.y), "+r"(r.z), "+r"(r.w)
+        : "r"(vi), "r"(lim), "l"(p + vi));
+    v[k] = r;
+  }
+}
+
+// LDG variant: ping-pong register buffers, the next rows' loads are issued
+// before the current rows are reduced.
+template <bool BF16, bool ENTROPY, int NV, int G, bool L1>
 __global__ void __launch_bounds__(256) conf_warp_kernel(const ConfArgs a) {
-  const int lane = threadIdx.x & 31;
+  constexpr int RPW = 32 / G;      // rows per warp
+  const int lane = threadIdx.x & 31, gl = lane % G, grp = lane / G;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t rows = live_rows(a);
-  const float c = a.c;
-  const f2_t c2 = f2(c, c);
-  constexpr int VE = BF16 ? 8 : 4;
-
-  int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (row >= rows) return;
-  int64_t src = source_row(a, row);
-  uint4 v[NV];
-  {
-    const uint4* p = reinterpret_cast<const uint4*>((const char*)a.logits + src * a.row_bytes);
-#pragma unroll
-    for (int k = 0; k < NV; ++k) v[k] = load_vec<BF16>(p, k * 32 + lane, a.nvec, a.tail);
-  }
+  const f2_t c2 = f2(a.c, a.c);
+  const int nvec = a.nvec;
+  const char* base = (const char*)a.logits;
+  auto ptr = [&](int64_t r, bool act) {
+    return reinterpret_cast<const uint4*>(base + (act ? src_row<L1>(a, r) : 0) * a.row_bytes);
+  };
+  const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (w0 * RPW >= rows) return;
+  uint4 A[NV], B[NV];
+  int64_t rowA = w0 * RPW + grp;
+  bool actA = rowA < rows;
+  group_load_row<BF16, NV, G>(A, ptr(rowA, actA), gl, nvec, actA);
   while (true) {
-    // prefetch the next row before reducing this one
-    const int64_t nrow = row + nwarps;
-    const bool more = nrow < rows;
-    int64_t nsrc = 0;
-    uint4 nv[NV];
-    if (more) {
-      nsrc = source_row(a, nrow);
-      const uint4* p = reinterpret_cast<const uint4*>((const char*)a.logits + nsrc * a.row_bytes);
-#pragma unroll
-      for (int k = 0; k < NV; ++k) nv[k] = load_vec<BF16>(p, k * 32 + lane, a.nvec, a.tail);
-    }
+    const int64_t rowB = rowA + nwarps * RPW;
+    const bool anyB = (rowB - grp) < rows;
+    const bool actB = rowB < rows;
+    if (anyB) group_load_row<BF16, NV, G>(B, ptr(rowB, actB), gl, nvec, actB);
+    if (a.tail) group_mask_tail<BF16, NV, G>(A, gl, nvec, a.tail);
+    group_reduce_row<BF16, ENTROPY, NV, G>(a, A, actA, rowA, actA ? src_row<L1>(a, rowA) : 0, gl, c2);
+    if (!anyB) break;
+    rowA = rowB + nwarps * RPW;
+    const bool anyA = (rowA - grp) < rows;
+    actA = rowA < rows;
+    if (anyA) group_load_row<BF16, NV, G>(A, ptr(rowA, actA), gl, nvec, actA);
+    if (a.tail) group_mask_tail<BF16, NV, G>(B, gl, nvec, a.tail);
+    group_reduce_row<BF16, ENTROPY, NV, G>(a, B, actB, rowB, actB ? src_row<L1>(a, rowB) : 0, gl, c2);
+    if (!anyA) break;
+  }
+}
 
-    // 1. row max (exact, NaN-propagating)
-    float vm[NV];
-    float lm = -INFINITY;
+// ---------------------------------------------------------------------------
+// K1a': the same grouped reduction, rows staged into shared memory by the TMA
+// engine (cp.async.bulk + mbarrier ring).  Warp 0 is the producer: lane 0 arms
+// the stage's "full" barrier with the tile's byte count, the lanes issue one
+// bulk copy per row (gathered rows) or one per tile (dense rows), with an L2
+// evict-first policy.  Warps 1..NCW consume 32/G rows each per stage (LDS.128,
+// conflict-free), reduce them in registers and release the stage through the
+// "empty" barrier.  S stages keep S*NCW*32/G rows in flight per SM.
+// ---------------------------------------------------------------------------
+template <int S>
+struct TmaRing {
+  uint64_t full[S];
+  uint64_t empty[S];
+};
+
+template <bool BF16, bool ENTROPY, int NV, int G, int NCW, int S, bool L1>
+__global__ void __launch_bounds__(32 * (NCW + 1), 1) conf_tma_kernel(const ConfArgs a, int dense) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  constexpr int RPW = 32 / G;
+  constexpr int RPS = NCW * RPW;          // rows per stage
+  TmaRing<S>* ring = reinterpret_cast<TmaRing<S>*>(smem);
+  unsigned char* stage_base = smem + 128 * ((sizeof(TmaRing<S>) + 127) / 128);
+  const int nvec = a.nvec;
+  const uint32_t row_sm = (uint32_t)nvec * 16u;
+  const uint32_t stage_bytes = row_sm * RPS;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t rows = live_rows(a);
+  const int64_t ntiles = (rows + RPS - 1) / RPS;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < S; ++i) {
+      mbar_init(&ring->full[i], 1);
+      mbar_init(&ring->empty[i], NCW);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (warp == 0) {
+    // ---------------- producer ----------------
+    const uint64_t pol = policy_evict_first();
+    const char* base = (const char*)a.logits;
+    int it = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+      const int st = it % S;
+      const uint32_t ph = (uint32_t)(it / S) & 1u;
+      const int64_t r0 = t * RPS;
+      const int nr = (int)min((int64_t)RPS, rows - r0);
+      if (lane == 0) {
+        mbar_wait(&ring->empty[st], ph ^ 1u);
+        mbar_arrive_expect_tx(&ring->full[st], row_sm * (uint32_t)nr);
+      }
+      __syncwarp();
+      unsigned char* dst = stage_base + (size_t)st * stage_bytes;
+      if (dense && !a.row_index) {
+        if (lane == 0)
+          bulk_g2s(dst, base + r0 * a.row_bytes, row_sm * (uint32_t)nr, &ring->full[st], pol);
+      } else {
+        for (int j = lane; j < nr; j += 32)
+          bulk_g2s(dst + (size_t)j * row_sm, base + src_row<L1>(a, r0 + j) * a.row_bytes, row_sm,
+                   &ring->full[st], pol);
+      }
+    }
+    return;
+  }
+  // ---------------- consumers ----------------
+  const int cw = warp - 1, gl = lane % G, grp = lane / G;
+  const f2_t c2 = f2(a.c, a.c);
+  const uint32_t f = BF16 ? kBf16NegInf2 : kF32NegInf;
+  int it = 0;
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+    const int st = it % S;
+    const uint32_t ph = (uint32_t)(it / S) & 1u;
+    const int slot = cw * RPW + grp;
+    const int64_t row = t * RPS + slot;
+    const bool act = row < rows;
+    mbar_wait(&ring->full[st], ph);
+    const unsigned char* srow = stage_base + (size_t)st * stage_bytes + (size_t)slot * row_sm;
+    const int lim = act ? nvec : 0;
+    uint4 v[NV];
 #pragma unroll
     for (int k = 0; k < NV; ++k) {
-      vm[k] = vec_max<BF16>(v[k]);
-      lm = fmax_nan(lm, vm[k]);
+      const int vi = k * G + gl;
+      v[k] = vi < lim ? lds128(srow + (size_t)vi * 16) : make_uint4(f, f, f, f);
     }
-    float m = lm;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) m = fmax_nan(m, __shfl_xor_sync(0xFFFFFFFFu, m, o));
-
-    // 2. argmax: first vector holding m (lowest vector index), then first element in it
-    unsigned my_vi = 0xFFFFFFFFu;
-#pragma unroll
-    for (int k = NV - 1; k >= 0; --k)
-      if (vm[k] == m) my_vi = (unsigned)(k * 32 + lane);
-    const unsigned vstar = __reduce_min_sync(0xFFFFFFFFu, my_vi);
-    unsigned am = 0;
-    if (vstar != 0xFFFFFFFFu) {
-      const int owner = (int)(vstar & 31u), kstar = (int)(vstar >> 5);
-      int e = 0;
-      if (lane == owner) {
-        uint4 sel = v[0];
-#pragma unroll
-        for (int k = 1; k < NV; ++k)
-          if (k == kstar) sel = v[k];
-        e = vec_first_eq<BF16>(sel, m);
-      }
-      e = __shfl_sync(0xFFFFFFFFu, e, owner);
-      am = vstar * VE + (unsigned)e;
-    }
-
-    // 3. exponentials with the common max
-    f2_t s2 = f2(0.f, 0.f), w2 = f2(0.f, 0.f);
-    const bool valid = (m < INFINITY) && (m > -INFINITY);
-    if (valid) {
-      const f2_t m2 = f2(m, m);
-      const uint32_t cw = ENTROPY && BF16 ? entropy_clamp_word(m, c) : 0u;
-#pragma unroll
-      for (int k = 0; k < NV; ++k) vec_accum<BF16, ENTROPY>(v[k], m2, c2, cw, s2, w2);
-    }
-    float s = warp_sum(f2lo(s2) + f2hi(s2));
-    float w = ENTROPY ? warp_sum(f2lo(w2) + f2hi(w2)) : 0.f;
-    if (lane == 0) {
-      RowOut r{m, s, w, am};
-      write_row(a, row, src, r);
-    }
-    if (!more) break;
-    row = nrow;
-    src = nsrc;
-#pragma unroll
-    for (int k = 0; k < NV; ++k) v[k] = nv[k];
+    if (a.tail) group_mask_tail<BF16, NV, G>(v, gl, nvec, a.tail);
+    group_reduce_row<BF16, ENTROPY, NV, G>(a, v, act, row, act ? src_row<L1>(a, row) : 0, gl, c2);
+    // every lane has consumed its staged vectors (the row max read them all)
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&ring->empty[st]);
   }
 }
 
@@ -360,7 +564,7 @@ __global__ void __launch_bounds__(NT) conf_cta_kernel(const ConfArgs a) {
         W += sh_w[i];
         A = min(A, sh_am[i]);
       }
-      RowOut r{M, S, W, A};
+      RowOut r{M, S, W, A, 1.0f};
       write_row(a, row, src, r);
     }
     __syncthreads();
@@ -403,11 +607,18 @@ int occupancy(K kernel, int threads) {
   return b > 0 ? b : 1;
 }
 
-template <bool BF16, bool ENTROPY, int NV>
-cudaError_t launch_warp(const ConfArgs& a, int64_t rows, cudaStream_t s) {
-  auto k = conf_warp_kernel<BF16, ENTROPY, NV>;
-  static int occ = occupancy(k, 256);
-  const int64_t want = (rows + 7) / 8;
+template <bool BF16, bool ENTROPY, int NV, int G, bool L1>
+int warp_occ() {
+  static const int o = occupancy(conf_warp_kernel<BF16, ENTROPY, NV, G, L1>, 256);
+  return o;
+}
+
+template <bool BF16, bool ENTROPY, int NV, int G, bool L1>
+cudaError_t launch_warp_l(const ConfArgs& a, int64_t rows, cudaStream_t s) {
+  auto k = conf_warp_kernel<BF16, ENTROPY, NV, G, L1>;
+  const int occ = warp_occ<BF16, ENTROPY, NV, G, L1>();
+  constexpr int RPB = 8 * (32 / G);      // rows per 256-thread block per pass
+  const int64_t want = (rows + RPB - 1) / RPB;
   const int64_t cap = (int64_t)num_sms() * occ;
   const int grid = (int)(want < cap ? (want > 0 ? want : 1) : cap);
   k<<<grid, 256, 0, s>>>(a);
@@ -415,10 +626,16 @@ cudaError_t launch_warp(const ConfArgs& a, int64_t rows, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+template <bool BF16, bool ENTROPY, int NV, int G>
+cudaError_t launch_warp(const ConfArgs& a, int64_t rows, cudaStream_t s) {
+  return a.L == 1 ? launch_warp_l<BF16, ENTROPY, NV, G, true>(a, rows, s)
+                  : launch_warp_l<BF16, ENTROPY, NV, G, false>(a, rows, s);
+}
+
 template <bool BF16, bool ENTROPY, int NT>
 cudaError_t launch_cta(const ConfArgs& a, int64_t rows, cudaStream_t s) {
   auto k = conf_cta_kernel<BF16, ENTROPY, NT, 8>;
-  static int occ = occupancy(k, NT);
+  static const int occ = occupancy(k, NT);
   const int64_t cap = (int64_t)num_sms() * occ;
   const int grid = (int)(rows < cap ? (rows > 0 ? rows : 1) : cap);
   k<<<grid, NT, 0, s>>>(a);
@@ -426,14 +643,85 @@ cudaError_t launch_cta(const ConfArgs& a, int64_t rows, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+template <bool BF16, bool ENTROPY, int NV, int G, int NCW, int S, bool L1>
+cudaError_t launch_tma_l(const ConfArgs& a, int64_t rows, cudaStream_t s) {
+  auto k = conf_tma_kernel<BF16, ENTROPY, NV, G, NCW, S, L1>;
+  constexpr int RPS = NCW * (32 / G);
+  const size_t ring = 128 * ((sizeof(TmaRing<S>) + 127) / 128);
+  const size_t smem = ring + (size_t)S * RPS * (size_t)a.nvec * 16;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    attr = true;
+  }
+  const int64_t tiles = (rows + RPS - 1) / RPS;
+  const int64_t cap = num_sms();
+  const int grid = (int)(tiles < cap ? (tiles > 0 ? tiles : 1) : cap);
+  const int dense = (a.row_bytes == (int64_t)a.nvec * 16) ? 1 : 0;
+  k<<<grid, 32 * (NCW + 1), smem, s>>>(a, dense);
+  count_launch();
+  return cudaGetLastError();
+}
+
+// default TMA ring shape: 8 consumer warps, 3 stages (<= 3 x 64 KB of rows)
+template <bool BF16, bool ENTROPY, int NV, int G, int NCW = 8, int S = 3>
+cudaError_t launch_tma(const ConfArgs& a, int64_t rows, cudaStream_t s) {
+  return a.L == 1 ? launch_tma_l<BF16, ENTROPY, NV, G, NCW, S, true>(a, rows, s)
+                  : launch_tma_l<BF16, ENTROPY, NV, G, NCW, S, false>(a, rows, s);
+}
+
+// Exploration switch (HS_CONF_VARIANT) for the ViT-sized rows (nvec <= 128,
+// bf16, max-prob): A/B of staging and lane-grouping choices under ncu.
+int conf_variant() {
+  static const int v = [] {
+    const char* e = getenv("HS_CONF_VARIANT");
+    if (!e) return 0;
+    if (!strcmp(e, "ldg16x8")) return 1;
+    if (!strcmp(e, "ldg8x16")) return 2;
+    if (!strcmp(e, "tma8x16n12s2")) return 3;
+    if (!strcmp(e, "tma16x8n16s3")) return 4;
+    if (!strcmp(e, "tma8x16n8s3")) return 5;
+    return 0;
+  }();
+  return v;
+}
+
+int conf_impl() {   // 0 = LDG (registers, default), 1 = TMA ring
+  static const int v = [] {
+    const char* e = getenv("HS_CONF_IMPL");
+    return (e && strcmp(e, "tma") == 0) ? 1 : 0;
+  }();
+  return v;
+}
+
+// Row shapes: G lanes per row, NV 16-byte vectors per lane (G * NV >= nvec).
 template <bool BF16, bool ENTROPY>
 cudaError_t dispatch(const ConfArgs& a, int64_t rows, cudaStream_t s) {
   const int nvec = a.nvec;
-  if (nvec <= 32) return launch_warp<BF16, ENTROPY, 1>(a, rows, s);
-  if (nvec <= 64) return launch_warp<BF16, ENTROPY, 2>(a, rows, s);
-  if (nvec <= 128) return launch_warp<BF16, ENTROPY, 4>(a, rows, s);
-  if (nvec <= 256) return launch_warp<BF16, ENTROPY, 8>(a, rows, s);
-  if (nvec <= 512) return launch_warp<BF16, ENTROPY, 16>(a, rows, s);
+  if (BF16 && !ENTROPY && nvec > 64 && nvec <= 128 && conf_variant() != 0) {
+    switch (conf_variant()) {
+      case 1: return launch_warp<BF16, ENTROPY, 8, 16>(a, rows, s);
+      case 2: return launch_warp<BF16, ENTROPY, 16, 8>(a, rows, s);
+      case 3: return launch_tma<BF16, ENTROPY, 16, 8, 12, 2>(a, rows, s);
+      case 4: return launch_tma<BF16, ENTROPY, 8, 16, 16, 3>(a, rows, s);
+      default: return launch_tma<BF16, ENTROPY, 16, 8, 8, 3>(a, rows, s);
+    }
+  }
+  if (nvec <= 512 && conf_impl() == 1) {
+    if (nvec <= 4) return launch_tma<BF16, ENTROPY, 1, 4>(a, rows, s);
+    if (nvec <= 16) return launch_tma<BF16, ENTROPY, 4, 4>(a, rows, s);
+    if (nvec <= 64) return launch_tma<BF16, ENTROPY, 16, 4>(a, rows, s);
+    if (nvec <= 128) return launch_tma<BF16, ENTROPY, 16, 8>(a, rows, s);
+    if (nvec <= 256) return launch_tma<BF16, ENTROPY, 16, 16>(a, rows, s);
+    return launch_tma<BF16, ENTROPY, 16, 32>(a, rows, s);
+  }
+  if (nvec <= 4) return launch_warp<BF16, ENTROPY, 1, 4>(a, rows, s);
+  if (nvec <= 16) return launch_warp<BF16, ENTROPY, 4, 4>(a, rows, s);
+  if (nvec <= 32) return launch_warp<BF16, ENTROPY, 8, 4>(a, rows, s);
+  if (nvec <= 64) return launch_warp<BF16, ENTROPY, 8, 8>(a, rows, s);
+  if (nvec <= 128) return launch_warp<BF16, ENTROPY, 8, 16>(a, rows, s);
+  if (nvec <= 256) return launch_warp<BF16, ENTROPY, 8, 32>(a, rows, s);
+  if (nvec <= 512) return launch_warp<BF16, ENTROPY, 16, 32>(a, rows, s);
   if (nvec <= 8192) return launch_cta<BF16, ENTROPY, 256>(a, rows, s);
   return launch_cta<BF16, ENTROPY, 512>(a, rows, s);
 }

@@ -83,6 +83,9 @@ size_t calib_ws_bytes(int K, int q);
 cudaError_t launch_calib_init(void* ws, int q, long long target, cudaStream_t s);
 cudaError_t launch_calib_hist(const float* conf, const uint8_t* correct, int K, int64_t N, int q,
                               int round, const int32_t* b_idx, int32_t* hist, cudaStream_t s);
+cudaError_t launch_calib_fused(const float* conf, const uint8_t* correct, int K, int64_t N, int q,
+                               long long target, int32_t* b_idx, float* thr, int64_t* reach,
+                               int64_t* handled, int64_t* correct_total, void* ws, cudaStream_t s);
 cudaError_t launch_calib_select(int K, int q, int round, int32_t* b_idx, float* thr,
                                 int64_t* reach, int64_t* handled, int64_t* correct_total,
                                 void* ws, cudaStream_t s);

@@ -428,3 +428,18 @@ def test_c3_sequences_sampled_launch_config(hs):
         assert_conf_close(r["conf"].cpu().numpy(), ref["conf"])
         assert np.array_equal(r["argmax"].cpu().numpy(), ref["argmax"])
         assert np.array_equal(r["correct"].cpu().numpy(), ref["correct"])
+
+
+def test_calibration_fused_equals_split_rounds(hs, monkeypatch):
+    """The single cooperative launch (default) and the per-round histogram/select
+    launches give identical thresholds and counts."""
+    fam = synth.FAMILIES["c2"]
+    vconf, vok, _ = _gpu_val(hs, fam, 20000)
+    for q in (3, 12, 14):
+        fused = hs.calibrate_thresholds(vconf, vok, log2_bins=q)
+        monkeypatch.setenv("HS_CALIB_SPLIT", "1")
+        split = hs.calibrate_thresholds(vconf, vok, log2_bins=q)
+        monkeypatch.delenv("HS_CALIB_SPLIT")
+        torch.cuda.synchronize()
+        for key in ("b", "t", "reach", "handled", "correct_total"):
+            assert torch.equal(fused[key], split[key]), (q, key)
