@@ -30,6 +30,7 @@ METRIC = "requests routed/sec and logits HBM GB/s (% of peak) at 1/2/4/8 B200"
 CONFIG_TEXT = {
     "c1": "2-stage ViT-S->ViT-L cascade, 4,096 requests x 1,000 classes fp32, calibrated on 4,096 validation samples",
     "c2": "5-stage ViT family cascade, 262,144 requests x 1,000 classes bf16 per GPU, thresholds calibrated on 50,000 validation samples",
+    "c3": "4-size T5 cascade, 2,048 sequences x 64 tokens x 32,128 vocab bf16 per GPU (16,384 over 8 GPUs), MIN token confidence, 256 B payload gathered, 512 validation sequences per GPU",
     "c4": "3-stage Llama-like next-token cascade, 8,192 requests x 128,256 vocab bf16 per GPU, entropy confidence, 8 KB hidden-state payload gathered",
     "c5": "5-stage ViT streaming cascade, 1,048,576 requests x 1,000 classes bf16 per GPU (8M over 8 GPUs), validation 131,072 per GPU",
 }
@@ -157,8 +158,10 @@ def sum_over_ranks(x, world: int):
 def family(config: str):
     from workload import synth
     f = synth.FAMILIES[config]
-    if config == "c5":
+    if config == "c5":      # per-GPU shard of the 8-GPU streaming config
         f = synth.scaled(f, n=1 << 20, n_val=1 << 17)
+    if config == "c3":      # per-GPU shard of the 8-GPU T5 config
+        f = synth.scaled(f, n=2048, n_val=512)
     return f
 
 
@@ -294,7 +297,7 @@ def run_ours(args, world, rank, local):
     # dominant kernel: stage-1 confidence over this rank's batch: n rows x (row bytes + 8 B out)
     k_bytes = fam.n * (row_b + 8)
     achieved = k_bytes / (kernel_ms / 1e3) / 1e9
-    e2e = run_e2e(args, fam, router, route, val, labels, payload, stream, world)
+    e2e = run_e2e(args, fam, router, route, val, labels, payload, stream, world) if args.e2e_steps > 0 else None
     line = {
         "metric": METRIC, "value": value, "unit": "requests/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
@@ -311,7 +314,8 @@ def run_ours(args, world, rank, local):
         "reach": reach, "thresholds": router.cal["t"].cpu().tolist(), "status": st,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": None,
-                     "kernel": "conf_warp_kernel (stage-1 confidence, K1)",
+                     "kernel": ("conf_warp_kernel" if fam.C * fam.elt_bytes <= 8192 else "conf_cta_kernel")
+                     + " (stage-1 routing confidence, K1)",
                      "bytes_per_launch": k_bytes, "avg_launch_ms": kernel_ms,
                      "peak_source": peak_src},
         "e2e": e2e, "gpu_launches": gpu_launches, "clocks": clocks,
@@ -324,7 +328,7 @@ def run_e2e(args, fam, router, route, val, labels, payload, stream, world):
     """Same metric through the public API from pinned HOST buffers: every step copies
     its inputs host->device and reads the per-request results back."""
     import torch
-    steps = max(1, args.e2e_steps)
+    steps = args.e2e_steps
     host_route = [x.cpu().pin_memory() for x in route]
     host_val = [x.cpu().pin_memory() for x in val]
     host_lab = labels.cpu().pin_memory()

@@ -96,6 +96,23 @@ hs_status_t hs_confidence(const void* logits, hs_dtype_t dtype, int64_t n, int32
                           const int32_t* labels, uint8_t* correct, void* ws, size_t ws_bytes,
                           uint32_t* d_status, hs_stream_t stream);
 
+/* Every stage model's confidence on the SAME item set in one launch (the
+ * calibration input of Alg. 1: "Compute a on D_v" for every model m_1..m_K,
+ * P:458-464).  Batch b (0 <= b < n_batches <= 8) reads logits[b] (host array
+ * of device pointers, identical shape/stride/dtype) at temperatures[b] (host
+ * array); its items are output rows b*n .. b*n + n-1 of conf / correct (and
+ * b*n*seq_len.. of argmax).  labels (optional, [n*seq_len], indexed like the
+ * logits rows of one batch) are shared by every batch; row_index likewise.
+ * Workspace: hs_confidence_batched_workspace(n_batches, n, seq_len). */
+size_t hs_confidence_batched_workspace(int32_t n_batches, int64_t n, int32_t seq_len);
+hs_status_t hs_confidence_batched(const void* const* logits, const float* temperatures,
+                                  int32_t n_batches, hs_dtype_t dtype, int64_t n, int32_t seq_len,
+                                  int64_t n_classes, int64_t row_stride,
+                                  const int64_t* row_index, hs_conf_kind_t kind,
+                                  hs_seq_reduce_t reduce, float* conf, int32_t* argmax,
+                                  const int32_t* labels, uint8_t* correct, void* ws,
+                                  size_t ws_bytes, uint32_t* d_status, hs_stream_t stream);
+
 /* ------------------------------------------------------------------------ */
 /* Threshold test + stable compaction + gather.       */
 /* ------------------------------------------------------------------------ */

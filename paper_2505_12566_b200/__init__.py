@@ -26,7 +26,7 @@ _KINDS = {"maxprob": MAXPROB, "maxprob_sq": MAXPROB_SQ, "entropy": ENTROPY}
 _REDUCES = {"none": SEQ_NONE, "min": SEQ_MIN, "mean": SEQ_MEAN}
 STATUS_NONFINITE = 1
 
-__all__ = ["confidence", "route_compact", "cascade_step", "calibrate_thresholds",
+__all__ = ["confidence", "confidence_batched", "route_compact", "cascade_step", "calibrate_thresholds",
            "calibrate_begin", "calibrate_histogram", "calibrate_select", "Cascade", "HsError",
            "launch_count", "MAXPROB", "MAXPROB_SQ", "ENTROPY", "SEQ_NONE", "SEQ_MIN", "SEQ_MEAN"]
 
@@ -113,6 +113,45 @@ def confidence(logits: torch.Tensor, *, n: int | None = None, seq_len: int = 1,
               _p(row_index), _p(d_n), float(temperature), _kind(kind), _reduce(reduce),
               _p(out["conf"]), _p(out.get("argmax")), _p(labels), _p(out.get("correct")),
               _p(ws), 0 if ws is None else ws.numel(), _p(status), _stream(stream))
+    return out
+
+
+def confidence_batched(logits: list, temperatures, *, n: int | None = None, seq_len: int = 1,
+                       n_classes: int | None = None, kind="maxprob", reduce="none",
+                       row_index: torch.Tensor | None = None,
+                       labels: torch.Tensor | None = None, want_argmax: bool = True,
+                       status: torch.Tensor | None = None, out: dict | None = None,
+                       ws: torch.Tensor | None = None, stream=None) -> dict:
+    """Every stage model's confidence on the same items in ONE launch (the
+    calibration input of Alg. 1).  Output rows b*n .. b*n+n-1 of
+    ``conf`` / ``correct`` belong to logits[b]."""
+    import ctypes
+    nb = len(logits)
+    x0 = logits[0]
+    _check_cuda(*logits, row_index, labels, status)
+    for x in logits:
+        if x.dim() != 2 or x.stride(1) != 1 or x.stride(0) != x0.stride(0) or x.dtype != x0.dtype:
+            raise ValueError("batched logits must share dtype, shape and row stride")
+    C = int(n_classes or x0.shape[1])
+    if n is None:
+        n = int(row_index.numel()) if row_index is not None else x0.shape[0] // seq_len
+    dev = x0.device
+    out = dict(out or {})
+    if "conf" not in out:
+        out["conf"] = torch.empty(nb * n, dtype=torch.float32, device=dev)
+    if want_argmax and "argmax" not in out:
+        out["argmax"] = torch.empty(nb * n * seq_len, dtype=torch.int32, device=dev)
+    if labels is not None and "correct" not in out:
+        out["correct"] = torch.empty(nb * n, dtype=torch.uint8, device=dev)
+    need = lib().hs_confidence_batched_workspace(nb, n, seq_len)
+    if need and (ws is None or ws.numel() < need):
+        ws = torch.empty(need, dtype=torch.uint8, device=dev)
+    ptrs = (ctypes.c_void_p * nb)(*[x.data_ptr() for x in logits])
+    temps = (ctypes.c_float * nb)(*[float(t) for t in temperatures])
+    _abi.call("hs_confidence_batched", ptrs, temps, nb, _dtype_code(x0), n, seq_len, C,
+              int(x0.stride(0)), _p(row_index), _kind(kind), _reduce(reduce), _p(out["conf"]),
+              _p(out.get("argmax")), _p(labels), _p(out.get("correct")), _p(ws),
+              0 if ws is None else ws.numel(), _p(status), _stream(stream))
     return out
 
 

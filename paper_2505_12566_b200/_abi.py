@@ -6,7 +6,8 @@ import os
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libhs.so")
+# HS_LIBHS selects an experiment build (A/B on one box); default is the product build
+LIB_PATH = os.environ.get("HS_LIBHS") or os.path.join(_HERE, "libhs.so")
 
 P = ctypes.c_void_p
 I64 = ctypes.c_int64
@@ -22,6 +23,9 @@ STATUS_NAMES = {0: "HS_OK", 1: "HS_ERR_INVALID_ARGUMENT", 2: "HS_ERR_NONFINITE_I
 SIGNATURES = {
     "hs_confidence_workspace": (SZ, [I64, I32]),
     "hs_confidence": (I32, [P, I32, I64, I32, I64, I64, P, P, F32, I32, I32, P, P, P, P, P, SZ, P, P]),
+    "hs_confidence_batched_workspace": (SZ, [I32, I64, I32]),
+    "hs_confidence_batched": (I32, [P, P, I32, I32, I64, I32, I64, I64, P, I32, I32, P, P, P, P, P,
+                                    SZ, P, P]),
     "hs_route_compact_workspace": (SZ, [I64]),
     "hs_route_compact": (I32, [P, I64, P, F32, P, I32, P, P, I32, P, P, P, P, P, P, I64, P, P, P,
                                SZ, P]),

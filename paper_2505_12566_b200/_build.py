@@ -44,13 +44,15 @@ def _run(cmd):
     return r
 
 
-def build_libhs(force: bool = False, verbose: bool = False) -> str:
+def build_libhs(force: bool = False, verbose: bool = False, defines=(), out: str | None = None) -> str:
+    """Build libhs.so; `defines` + `out` build an experiment variant (A/B only)."""
+    target = out or LIBHS
     cus = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
     deps = cus + glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(CSRC, "*.cuh")) + \
         [os.path.join(ROOT, "include", "hs.h")]
-    if not force and not _stale(LIBHS, deps):
-        return LIBHS
-    objdir = os.path.join(ROOT, "build", "libhs")
+    if not force and not _stale(target, deps):
+        return target
+    objdir = os.path.join(ROOT, "build", os.path.basename(target)[:-3])
     os.makedirs(objdir, exist_ok=True)
     nv = nvcc()
     objs = []
@@ -58,15 +60,15 @@ def build_libhs(force: bool = False, verbose: bool = False) -> str:
     for cu in cus:
         o = os.path.join(objdir, os.path.basename(cu)[:-3] + ".o")
         objs.append(o)
-        cmds.append([nv] + NVCC_FLAGS + ["-c", cu, "-o", o])
+        cmds.append([nv] + NVCC_FLAGS + [f"-D{d}" for d in defines] + ["-c", cu, "-o", o])
     with cf.ThreadPoolExecutor(max_workers=min(8, len(cmds))) as ex:
         for r in ex.map(_run, cmds):
             if verbose:
                 print(r.stderr)
-    tmp = LIBHS + f".tmp{os.getpid()}"
+    tmp = target + f".tmp{os.getpid()}"
     _run([nv] + ARCH + ["-shared", "-o", tmp] + objs)
-    os.replace(tmp, LIBHS)
-    return LIBHS
+    os.replace(tmp, target)
+    return target
 
 
 def build_synth(force: bool = False) -> str:

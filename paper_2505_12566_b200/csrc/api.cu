@@ -101,17 +101,19 @@ hs::ConfArgs make_conf_args(const void* logits, hs_dtype_t dtype, int64_t n, int
   a.d_n = d_n;
   a.c = (float)(1.4426950408889634 / (double)T);
   a.kind = (int)kind;
+  a.nbatch = 1;
+  a.brows = n * L;
   return a;
 }
 
-// Runs K1 (+ K2).  conf / argmax / correct are per batch item.
-hs_status_t run_confidence(const void* logits, hs_dtype_t dtype, int64_t n, int32_t L, int64_t C,
-                           int64_t stride, const int64_t* row_index, const int64_t* d_n, float T,
-                           hs_conf_kind_t kind, hs_seq_reduce_t reduce, float* conf,
-                           int32_t* argmax, const int32_t* labels, uint8_t* correct, void* ws,
-                           uint32_t* d_status, cudaStream_t s) {
-  if (n == 0) return HS_OK;
-  hs::ConfArgs a = make_conf_args(logits, dtype, n, L, C, stride, row_index, d_n, T, kind);
+// Runs K1 (+ K2) for prepared arguments (nbatch batches of n items).
+hs_status_t run_confidence_args(hs::ConfArgs a, hs_dtype_t dtype, hs_seq_reduce_t reduce,
+                                float* conf, int32_t* argmax, const int32_t* labels,
+                                uint8_t* correct, void* ws, uint32_t* d_status, cudaStream_t s) {
+  const int64_t n = a.n;
+  const int32_t L = a.L;
+  const int64_t items = n * a.nbatch;
+  const int64_t* d_n = a.d_n;
   a.argmax = argmax;
   a.labels = labels;
   a.status = d_status;
@@ -121,13 +123,24 @@ hs_status_t run_confidence(const void* logits, hs_dtype_t dtype, int64_t n, int3
     return cuda_check(hs::launch_confidence(a, dtype == HS_BF16, s), "confidence kernel");
   }
   float* tok_conf = reinterpret_cast<float*>(ws);
-  uint8_t* tok_ok = reinterpret_cast<uint8_t*>(ws) + align_up((size_t)n * L * sizeof(float), 256);
+  uint8_t* tok_ok = reinterpret_cast<uint8_t*>(ws) + align_up((size_t)items * L * sizeof(float), 256);
   a.conf = tok_conf;
   a.ok = (correct && labels) ? tok_ok : nullptr;
   hs_status_t st = cuda_check(hs::launch_confidence(a, dtype == HS_BF16, s), "confidence kernel");
   if (st != HS_OK) return st;
-  return cuda_check(hs::launch_seq_reduce(tok_conf, a.ok, n, d_n, L, (int)reduce, conf, correct, s),
+  return cuda_check(hs::launch_seq_reduce(tok_conf, a.ok, items, a.nbatch == 1 ? d_n : nullptr, L,
+                                          (int)reduce, conf, correct, s),
                     "sequence reduce kernel");
+}
+
+hs_status_t run_confidence(const void* logits, hs_dtype_t dtype, int64_t n, int32_t L, int64_t C,
+                           int64_t stride, const int64_t* row_index, const int64_t* d_n, float T,
+                           hs_conf_kind_t kind, hs_seq_reduce_t reduce, float* conf,
+                           int32_t* argmax, const int32_t* labels, uint8_t* correct, void* ws,
+                           uint32_t* d_status, cudaStream_t s) {
+  if (n == 0) return HS_OK;
+  hs::ConfArgs a = make_conf_args(logits, dtype, n, L, C, stride, row_index, d_n, T, kind);
+  return run_confidence_args(a, dtype, reduce, conf, argmax, labels, correct, ws, d_status, s);
 }
 
 hs_status_t check_threshold(float t) {
@@ -177,6 +190,43 @@ hs_status_t hs_confidence(const void* logits, hs_dtype_t dtype, int64_t n, int32
   return run_confidence(logits, dtype, n, seq_len, n_classes, row_stride, row_index, d_n,
                         temperature, kind, reduce, conf, argmax, labels, correct, ws, d_status,
                         (cudaStream_t)stream);
+}
+
+size_t hs_confidence_batched_workspace(int32_t n_batches, int64_t n, int32_t seq_len) {
+  return conf_ws((int64_t)(n_batches < 1 ? 1 : n_batches) * n, seq_len);
+}
+
+hs_status_t hs_confidence_batched(const void* const* logits, const float* temperatures,
+                                  int32_t n_batches, hs_dtype_t dtype, int64_t n, int32_t seq_len,
+                                  int64_t n_classes, int64_t row_stride,
+                                  const int64_t* row_index, hs_conf_kind_t kind,
+                                  hs_seq_reduce_t reduce, float* conf, int32_t* argmax,
+                                  const int32_t* labels, uint8_t* correct, void* ws,
+                                  size_t ws_bytes, uint32_t* d_status, hs_stream_t stream) {
+  if (!logits || !temperatures) return fail(HS_ERR_INVALID_ARGUMENT, "logits/temperatures arrays are required");
+  if (n_batches < 1 || n_batches > hs::kMaxBatch)
+    return fail(HS_ERR_INVALID_ARGUMENT, "n_batches = %d outside 1..%d", n_batches, hs::kMaxBatch);
+  for (int b = 0; b < n_batches; ++b) {
+    hs_status_t st = check_logits(logits[b], dtype, n, seq_len, n_classes, row_stride,
+                                  temperatures[b], kind, reduce);
+    if (st != HS_OK) return st;
+  }
+  if (n > 0 && !conf) return fail(HS_ERR_INVALID_ARGUMENT, "conf output is required");
+  if (correct && !labels) return fail(HS_ERR_INVALID_ARGUMENT, "correct requires labels");
+  const size_t need = conf_ws((int64_t)n_batches * n, seq_len);
+  if (ws_bytes < need || (need && !ws))
+    return fail(HS_ERR_WORKSPACE_TOO_SMALL, "workspace %zu < %zu", ws_bytes, need);
+  if (n == 0) return HS_OK;
+  hs::ConfArgs a = make_conf_args(logits[0], dtype, n, seq_len, n_classes, row_stride, row_index,
+                                  nullptr, temperatures[0], kind);
+  a.nbatch = n_batches;
+  a.brows = n * seq_len;
+  for (int b = 0; b < n_batches; ++b) {
+    a.bptr[b] = logits[b];
+    a.bc[b] = (float)(1.4426950408889634 / (double)temperatures[b]);
+  }
+  return run_confidence_args(a, dtype, reduce, conf, argmax, labels, correct, ws, d_status,
+                             (cudaStream_t)stream);
 }
 
 size_t hs_route_compact_workspace(int64_t n) { return hs::compact_ws_bytes(n); }
@@ -369,7 +419,14 @@ hs_status_t hs_calibrate_thresholds(const float* conf, const uint8_t* correct, i
   if (!conf || !correct) return fail(HS_ERR_INVALID_ARGUMENT, "NULL input");
   if (!d_bin_idx || !d_thresholds || !d_reach || !d_handled || !d_correct_total)
     return fail(HS_ERR_INVALID_ARGUMENT, "NULL output");
-  if (!getenv("HS_CALIB_SPLIT"))   // one cooperative launch for all rounds
+  const char* mode = getenv("HS_CALIB_MODE");   // cluster | fused | split (tests / A-B)
+  const bool small = N < (1 << 20);
+  if ((!mode && small) || (mode && !strcmp(mode, "cluster") && small))
+    return cuda_check(hs::launch_calib_cluster(conf, correct, K, N, log2_bins, target_correct,
+                                               d_bin_idx, d_thresholds, d_reach, d_handled,
+                                               d_correct_total, ws, (cudaStream_t)stream),
+                      "calib cluster kernel");
+  if (!mode || !strcmp(mode, "fused") || !strcmp(mode, "cluster"))   // one cooperative launch
     return cuda_check(hs::launch_calib_fused(conf, correct, K, N, log2_bins, target_correct,
                                              d_bin_idx, d_thresholds, d_reach, d_handled,
                                              d_correct_total, ws, (cudaStream_t)stream),

@@ -43,11 +43,12 @@ __global__ void calib_init_kernel(CalibState* st, int32_t* hist, int nwords, lon
 }
 
 // hist layout: int32 [3][B+2]; index 0 = NaN bin (never accepted), index b+1 = bin b.
-// One CTA's share (grid-stride) of round `round`, added into the global histogram.
-__device__ __forceinline__ void hist_body(const float* __restrict__ conf,
-                                          const uint8_t* __restrict__ correct, int K, int64_t N,
-                                          int q, int round, const int32_t* b_idx,
-                                          int32_t* __restrict__ hist, unsigned long long* sh) {
+// Build this CTA's share of round `round` in shared memory: samples r = start,
+// start + stride, ...  (packed u64 per bin: count | correct_k << 21 | correct_K << 42).
+__device__ __forceinline__ void hist_local(const float* __restrict__ conf,
+                                           const uint8_t* __restrict__ correct, int K, int64_t N,
+                                           int q, int round, const int32_t* b_idx,
+                                           unsigned long long* sh, int64_t start, int64_t stride) {
   const int nb = (1 << q) + 2;
   for (int i = threadIdx.x; i < nb; i += blockDim.x) sh[i] = 0ull;
   int bprev[16];
@@ -58,26 +59,26 @@ __device__ __forceinline__ void hist_body(const float* __restrict__ conf,
   const uint8_t* ck = correct + (int64_t)round * N;
   const uint8_t* cK = correct + (int64_t)(K - 1) * N;
   const float* ckconf = conf + (int64_t)round * N;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   // loop bound is warp-uniform so __match_any_sync sees full warps
   const int64_t Nup = (N + 31) & ~(int64_t)31;
-  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < Nup; r += stride) {
-    bool alive = r < N;
-    if (alive) {
+  for (int64_t r = start; r < Nup; r += stride) {
+    // issue every load of this sample first (no short-circuit chain)
+    const bool in = r < N;
+    float cprev[16];
 #pragma unroll
-      for (int j = 0; j < 16; ++j)
-        if (j < round) alive = alive && (bin_of(conf[(int64_t)j * N + r], q) < bprev[j]);
-    }
-    int key = -1;                      // -1: not counted
-    bool okk = false, okK = false;
-    if (alive) {
-      key = bin_of(ckconf[r], q) + 1;
-      okk = ck[r] != 0;
-      okK = cK[r] != 0;
-    }
+    for (int j = 0; j < 16; ++j) cprev[j] = (in && j < round) ? __ldg(conf + (int64_t)j * N + r) : 0.f;
+    const float cnow = in ? __ldg(ckconf + r) : 0.f;
+    const bool okk = in && __ldg(ck + r) != 0;
+    const bool okK0 = in && __ldg(cK + r) != 0;
+    bool alive = in;
+#pragma unroll
+    for (int j = 0; j < 16; ++j)
+      if (j < round) alive &= bin_of(cprev[j], q) < bprev[j];
+    const int key = alive ? bin_of(cnow, q) + 1 : -1;   // -1: not counted
+    const bool okK = alive && okK0;
     // warp aggregation: lanes with the same bin add once, through their leader
     const unsigned peers = __match_any_sync(0xFFFFFFFFu, key);
-    const unsigned bk = __ballot_sync(0xFFFFFFFFu, okk);
+    const unsigned bk = __ballot_sync(0xFFFFFFFFu, alive && okk);
     const unsigned bK = __ballot_sync(0xFFFFFFFFu, okK);
     if (key >= 0 && (threadIdx.x & 31) == __ffs(peers) - 1) {
       const unsigned long long tot = (unsigned long long)__popc(peers) |
@@ -87,15 +88,31 @@ __device__ __forceinline__ void hist_body(const float* __restrict__ conf,
     }
   }
   __syncthreads();
-  constexpr unsigned long long F = (1ull << 21) - 1;
+}
+
+constexpr unsigned long long kField = (1ull << 21) - 1;
+
+// Add a packed shared-memory histogram into the global int32 [3][B+2] one.
+__device__ __forceinline__ void hist_flush(const unsigned long long* sh, int q, int32_t* hist) {
+  const int nb = (1 << q) + 2;
   for (int i = threadIdx.x; i < nb; i += blockDim.x) {
     const unsigned long long v = sh[i];
     if (v) {
-      atomicAdd(&hist[i], (int32_t)(v & F));
-      atomicAdd(&hist[nb + i], (int32_t)((v >> 21) & F));
-      atomicAdd(&hist[2 * nb + i], (int32_t)((v >> 42) & F));
+      atomicAdd(&hist[i], (int32_t)(v & kField));
+      atomicAdd(&hist[nb + i], (int32_t)((v >> 21) & kField));
+      atomicAdd(&hist[2 * nb + i], (int32_t)((v >> 42) & kField));
     }
   }
+}
+
+// One CTA's share (grid-stride) of round `round`, added into the global histogram.
+__device__ __forceinline__ void hist_body(const float* __restrict__ conf,
+                                          const uint8_t* __restrict__ correct, int K, int64_t N,
+                                          int q, int round, const int32_t* b_idx,
+                                          int32_t* __restrict__ hist, unsigned long long* sh) {
+  hist_local(conf, correct, K, N, q, round, b_idx, sh,
+             (int64_t)blockIdx.x * blockDim.x + threadIdx.x, (int64_t)gridDim.x * blockDim.x);
+  hist_flush(sh, q, hist);
 }
 
 __global__ void __launch_bounds__(512) calib_hist_kernel(const float* __restrict__ conf,
@@ -107,123 +124,167 @@ __global__ void __launch_bounds__(512) calib_hist_kernel(const float* __restrict
   hist_body(conf, correct, K, N, q, round, b_idx, hist, sh);
 }
 
-// One CTA of NT threads.  Each thread owns a contiguous segment of bins
-// 0..B (hist index b+1); suffix sums come from a block scan of segment totals.
-template <int NT>
-__device__ __forceinline__ void select_body(int K, int q, int round, int32_t* b_idx, float* thr,
-                                            int64_t* reach, int64_t* handled,
-                                            int64_t* correct_total, CalibState* st,
-                                            int32_t* hist) {
+// Histogram readers for the select: the int32 [3][B+2] global layout, or the
+// packed u64 shared-memory layout of the cluster kernel.
+struct Bin3 { long long cnt, ck, cK; };
+struct GlobalHist {
+  const int32_t* h;
+  int nb;
+  __device__ __forceinline__ Bin3 operator()(int i) const {
+    return Bin3{h[i], h[nb + i], h[2 * nb + i]};
+  }
+};
+struct PackedHist {
+  const unsigned long long* h;
+  __device__ __forceinline__ Bin3 operator()(int i) const {
+    const unsigned long long v = h[i];
+    return Bin3{(long long)(v & kField), (long long)((v >> 21) & kField), (long long)((v >> 42) & kField)};
+  }
+};
+
+// One CTA of NT threads picks b_k (D5): thread t owns the contiguous bins
+// [lo, hi) of 0..B (histogram index b+1; index 0 = NaN, never accepted).
+//   pass 1: segment sums -> block totals (reach_k, G) and the suffix S(hi)
+//   pass 2: smallest feasible b of each segment -> block min = b_k
+//   pass 3: committed (bin >= b_k) and surviving (bin < b_k) sums
+// Three block barriers per round; the reader decides global vs shared memory.
+template <int NT, typename Hist>
+__device__ __forceinline__ void select_core(const Hist& H, int K, int q, int round,
+                                            int32_t* b_idx, float* thr, int64_t* reach,
+                                            int64_t* handled, int64_t* correct_total,
+                                            CalibState* st) {
   constexpr int NW = NT / 32;
-  __shared__ long long sh_w[NW];
-  __shared__ long long sh_tot[3];
-  __shared__ int sh_b;
-  __shared__ unsigned long long sh_sum_ck, sh_sum_cnt, sh_below_cnt, sh_below_cK;
+  __shared__ long long sh_a[NW], sh_b[NW], sh_c[NW], sh_d[NW];
+  __shared__ int sh_min[NW];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int B = 1 << q, nb = B + 2;
-  const int32_t* cnt = hist;
-  const int32_t* ckh = hist + nb;
-  const int32_t* cKh = hist + 2 * nb;
-
-  // ---- totals over all alive samples (incl. the NaN bin): reach_k, G
-  long long tc = 0, tK = 0;
-  for (int i = tid; i < nb; i += NT) {
-    tc += cnt[i];
-    tK += cKh[i];
-  }
-  tc = warp_sum(tc);
-  tK = warp_sum(tK);
-  if (tid == 0) {
-    sh_tot[0] = 0;
-    sh_tot[1] = 0;
-    sh_b = B + 1;
-    sh_sum_ck = sh_sum_cnt = sh_below_cnt = sh_below_cK = 0ull;
-  }
-  __syncthreads();
-  if (lane == 0) {
-    atomicAdd((unsigned long long*)&sh_tot[0], (unsigned long long)tc);
-    atomicAdd((unsigned long long*)&sh_tot[1], (unsigned long long)tK);
-  }
-  __syncthreads();
-  const long long reach_k = sh_tot[0];
-  const long long G = sh_tot[1];
-  if (round == 0 && st->tau_ap) {
-    if (tid == 0) st->tau = G;      // AP: tau = correct answers of m_K (everything alive)
-    __syncthreads();
-  }
-  const long long tau = st->tau;
-  const long long A = st->A;
-
-  // ---- segment of bins [lo, hi) in 0..B, H[b] = ck - cK of bin b
+  const int B = 1 << q;
   const int per = (B + 1 + NT - 1) / NT;
   const int lo = min(tid * per, B + 1), hi = min(lo + per, B + 1);
-  long long seg = 0;
-  for (int b = lo; b < hi; ++b) seg += (long long)ckh[b + 1] - (long long)cKh[b + 1];
-  // block exclusive suffix sum of seg (sum over threads with larger tid)
-  long long incl = seg;   // inclusive suffix within warp
+
+  // ---- pass 1
+  long long segH = 0, segCnt = 0, segK = 0;
+  for (int b = lo; b < hi; ++b) {
+    const Bin3 x = H(b + 1);
+    segH += x.ck - x.cK;
+    segCnt += x.cnt;
+    segK += x.cK;
+  }
+  if (tid == 0) {                     // NaN bin: alive, never accepted
+    const Bin3 x = H(0);
+    segCnt += x.cnt;
+    segK += x.cK;
+  }
+  long long incl = segH;              // inclusive suffix within the warp
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
     const long long y = __shfl_down_sync(0xFFFFFFFFu, incl, o);
     if (lane + o < 32) incl += y;
   }
-  if (lane == 0) sh_w[wid] = incl;   // warp total
+  long long wc = segCnt, wk = segK;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    wc += __shfl_xor_sync(0xFFFFFFFFu, wc, o);
+    wk += __shfl_xor_sync(0xFFFFFFFFu, wk, o);
+  }
+  if (lane == 0) {
+    sh_a[wid] = incl;
+    sh_b[wid] = wc;
+    sh_c[wid] = wk;
+  }
   __syncthreads();
-  long long after_warp = 0;
-  for (int v = wid + 1; v < NW; ++v) after_warp += sh_w[v];
-  long long suffix = after_warp + (incl - seg);   // sum of H over bins >= hi
-  // ---- smallest feasible b in this segment (scan downward keeps S(b) incremental)
+  long long after = 0, reach_k = 0, G = 0;
+  for (int v = 0; v < NW; ++v) {
+    if (v > wid) after += sh_a[v];
+    reach_k += sh_b[v];
+    G += sh_c[v];
+  }
+  if (round == 0 && st->tau_ap) {     // AP: tau = correct answers of m_K (all alive)
+    __syncthreads();
+    if (tid == 0) st->tau = G;
+    __syncthreads();
+  }
+  const long long tau = st->tau, A = st->A;
+  // ---- pass 2: S(b) for b in [lo, hi) built downward from S(hi)
   int best = B + 1;
   {
-    long long S = suffix;
+    long long S = after + (incl - segH);
     for (int b = hi - 1; b >= lo; --b) {
-      S += (long long)ckh[b + 1] - (long long)cKh[b + 1];
+      const Bin3 x = H(b + 1);
+      S += x.ck - x.cK;
       if (A + G + S >= tau) best = b;
     }
   }
-  atomicMin(&sh_b, best);
+  best = __reduce_min_sync(0xFFFFFFFFu, (unsigned)best);
+  if (lane == 0) sh_min[wid] = best;
   __syncthreads();
-  const int bk = sh_b;   // b = B+1 (defer all) is feasible by induction: A + G >= tau
-  // ---- commit: A += sum_{bin >= bk} ck ; handled = sum_{bin >= bk} cnt ;
-  //      survivors (bin < bk, incl. NaN) for the final stage
-  unsigned long long s_ck = 0, s_cnt = 0, s_bc = 0, s_bK = 0;
-  for (int i = tid; i < nb; i += NT) {
-    const int b = i - 1;   // -1 = NaN bin
+  int bk = B + 1;   // b = B+1 (defer all) is feasible by induction: A + G >= tau
+  for (int v = 0; v < NW; ++v) bk = min(bk, sh_min[v]);
+  // ---- pass 3
+  long long s_ck = 0, s_cnt = 0, s_bc = 0, s_bK = 0;
+  for (int b = lo; b < hi; ++b) {
+    const Bin3 x = H(b + 1);
     if (b >= bk) {
-      s_ck += (unsigned long long)ckh[i];
-      s_cnt += (unsigned long long)cnt[i];
+      s_ck += x.ck;
+      s_cnt += x.cnt;
     } else {
-      s_bc += (unsigned long long)cnt[i];
-      s_bK += (unsigned long long)cKh[i];
+      s_bc += x.cnt;
+      s_bK += x.cK;
     }
   }
-  s_ck = warp_sum(s_ck);
-  s_cnt = warp_sum(s_cnt);
-  s_bc = warp_sum(s_bc);
-  s_bK = warp_sum(s_bK);
+  if (tid == 0) {
+    const Bin3 x = H(0);
+    s_bc += x.cnt;
+    s_bK += x.cK;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    s_ck += __shfl_xor_sync(0xFFFFFFFFu, s_ck, o);
+    s_cnt += __shfl_xor_sync(0xFFFFFFFFu, s_cnt, o);
+    s_bc += __shfl_xor_sync(0xFFFFFFFFu, s_bc, o);
+    s_bK += __shfl_xor_sync(0xFFFFFFFFu, s_bK, o);
+  }
+  __syncthreads();                    // sh_a..sh_c reads of pass 1 are done
   if (lane == 0) {
-    atomicAdd(&sh_sum_ck, s_ck);
-    atomicAdd(&sh_sum_cnt, s_cnt);
-    atomicAdd(&sh_below_cnt, s_bc);
-    atomicAdd(&sh_below_cK, s_bK);
+    sh_a[wid] = s_ck;
+    sh_b[wid] = s_cnt;
+    sh_c[wid] = s_bc;
+    sh_d[wid] = s_bK;
   }
   __syncthreads();
   if (tid == 0) {
-    long long Anew = A + (long long)sh_sum_ck;
+    long long ck = 0, cnt = 0, bc = 0, bK = 0;
+    for (int v = 0; v < NW; ++v) {
+      ck += sh_a[v];
+      cnt += sh_b[v];
+      bc += sh_c[v];
+      bK += sh_d[v];
+    }
+    long long Anew = A + ck;
     b_idx[round] = bk;
     thr[round] = bk <= B ? (float)bk / (float)B : INFINITY;
     reach[round] = reach_k;
-    handled[round] = (long long)sh_sum_cnt;
+    handled[round] = cnt;
     if (round == K - 2) {
-      reach[K - 1] = (long long)sh_below_cnt;
-      handled[K - 1] = (long long)sh_below_cnt;
-      Anew += (long long)sh_below_cK;
+      reach[K - 1] = bc;
+      handled[K - 1] = bc;
+      Anew += bK;
       thr[K - 1] = 0.f;
       *correct_total = Anew;
     }
     st->A = Anew;
   }
   __syncthreads();
-  for (int i = tid; i < 3 * nb; i += NT) hist[i] = 0;
+}
+
+template <int NT>
+__device__ __forceinline__ void select_body(int K, int q, int round, int32_t* b_idx, float* thr,
+                                            int64_t* reach, int64_t* handled,
+                                            int64_t* correct_total, CalibState* st,
+                                            int32_t* hist) {
+  const int nb = (1 << q) + 2;
+  select_core<NT>(GlobalHist{hist, nb}, K, q, round, b_idx, thr, reach, handled, correct_total, st);
+  for (int i = threadIdx.x; i < 3 * nb; i += NT) hist[i] = 0;
+  __syncthreads();
 }
 
 __global__ void __launch_bounds__(1024) calib_select_kernel(int K, int q, int round,
@@ -260,6 +321,50 @@ __global__ void __launch_bounds__(1024) calib_fused_kernel(const float* __restri
     grid.sync();
     if (blockIdx.x == 0) select_body<1024>(K, q, k, b_idx, thr, reach, handled, correct_total, st, hist);
     grid.sync();
+  }
+}
+
+// All K-1 rounds on ONE thread-block cluster (small validation sets, N < 2^21):
+// every CTA builds a private shared-memory histogram of its samples, the
+// cluster barrier publishes them, CTA rank 0 sums the other CTAs' histograms
+// through distributed shared memory (DSMEM loads), writes the combined
+// histogram once and runs the select; a second cluster barrier releases the
+// next round.  No global atomics and no grid-wide barrier.
+__global__ void __launch_bounds__(1024) calib_cluster_kernel(const float* __restrict__ conf,
+                                                             const uint8_t* __restrict__ correct,
+                                                             int K, int64_t N, int q,
+                                                             long long target, int32_t* b_idx,
+                                                             float* thr, int64_t* reach,
+                                                             int64_t* handled,
+                                                             int64_t* correct_total,
+                                                             CalibState* st, int32_t* hist) {
+  extern __shared__ unsigned long long sh[];
+  cg::cluster_group cluster = cg::this_cluster();
+  const unsigned rank = cluster.block_rank(), ncta = cluster.num_blocks();
+  const int nb = (1 << q) + 2;
+  if (rank == 0) {
+    for (int i = threadIdx.x; i < 3 * nb; i += blockDim.x) hist[i] = 0;
+    if (threadIdx.x == 0) {
+      st->A = 0;
+      st->tau = target < 0 ? 0 : target;
+      st->tau_ap = target < 0 ? 1 : 0;
+    }
+  }
+  cluster.sync();
+  for (int k = 0; k < K - 1; ++k) {
+    hist_local(conf, correct, K, N, q, k, b_idx, sh,
+               (int64_t)rank * blockDim.x + threadIdx.x, (int64_t)ncta * blockDim.x);
+    cluster.sync();
+    if (rank == 0) {
+      for (int i = threadIdx.x; i < nb; i += blockDim.x) {
+        unsigned long long v = sh[i];
+        for (unsigned c = 1; c < ncta; ++c) v += *cluster.map_shared_rank(&sh[i], c);
+        sh[i] = v;
+      }
+      __syncthreads();
+      select_core<1024>(PackedHist{sh}, K, q, k, b_idx, thr, reach, handled, correct_total, st);
+    }
+    cluster.sync();
   }
 }
 
@@ -328,6 +433,39 @@ cudaError_t launch_calib_fused(const float* conf, const uint8_t* correct, int K,
                   (void*)&correct_total, (void*)&st, (void*)&hist};
   cudaError_t e = cudaLaunchCooperativeKernel((void*)calib_fused_kernel, dim3(grid), dim3(1024),
                                               args, smem, s);
+  count_launch();
+  return e != cudaSuccess ? e : cudaGetLastError();
+}
+
+constexpr int kCalibCluster = 8;
+
+cudaError_t launch_calib_cluster(const float* conf, const uint8_t* correct, int K, int64_t N,
+                                 int q, long long target, int32_t* b_idx, float* thr,
+                                 int64_t* reach, int64_t* handled, int64_t* correct_total,
+                                 void* ws, cudaStream_t s) {
+  const size_t smem = (size_t)((1 << q) + 2) * sizeof(unsigned long long);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(calib_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(((1 << 14) + 2) * sizeof(unsigned long long)));
+    attr = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(kCalibCluster);
+  cfg.blockDim = dim3(1024);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = kCalibCluster;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  CalibState* st = reinterpret_cast<CalibState*>(ws);
+  int32_t* hist = hist_of(ws);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, calib_cluster_kernel, conf, correct, K, N, q, target,
+                                     b_idx, thr, reach, handled, correct_total, st, hist);
   count_launch();
   return e != cudaSuccess ? e : cudaGetLastError();
 }

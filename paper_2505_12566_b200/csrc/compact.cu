@@ -51,17 +51,28 @@ __global__ void __launch_bounds__(kCompactThreads) route_compact_kernel(const Co
   if (tile < ntiles) {
     const int64_t base = tile * kCompactTile;
     const float thr = a.d_threshold ? *a.d_threshold : a.threshold;
-    // ---- flags (coalesced: item j of thread tid is base + j*T + tid)
+    // ---- all loads of the tile first (independent, coalesced: item j of thread
+    //      tid is base + j*T + tid), so they overlap instead of serialising
+    //      behind the ballots and the output stores
+    float cv[I];
+    int64_t idv[I];
+    int32_t pv[I];
+    const bool pred1 = a.acc_pred && a.pred_len == 1;
+#pragma unroll
+    for (int j = 0; j < I; ++j) {
+      const int64_t i = base + (int64_t)j * T + tid;
+      const bool in = i < n;
+      cv[j] = in ? __ldg(a.conf + i) : 0.f;
+      idv[j] = (in && a.ids) ? __ldg(a.ids + i) : i;
+      pv[j] = (in && pred1) ? __ldg(a.pred + i) : 0;
+    }
     bool dfr[I];
     unsigned bal[I];
 #pragma unroll
     for (int j = 0; j < I; ++j) {
       const int64_t i = base + (int64_t)j * T + tid;
-      bool d = false;
-      if (i < n) {
-        const float c = a.conf[i];
-        d = !(a.is_last || c >= thr);   // NaN confidence: deferred (unless last)
-      }
+      // NaN confidence: deferred (unless last)
+      const bool d = (i < n) && !(a.is_last || cv[j] >= thr);
       dfr[j] = d;
       bal[j] = __ballot_sync(0xFFFFFFFFu, d);
       if (lane == 0) s_cnt[j * NW + wid] = __popc(bal[j]);
@@ -127,16 +138,17 @@ __global__ void __launch_bounds__(kCompactThreads) route_compact_kernel(const Co
       if (i >= n) continue;
       const int local = j * T + tid;
       const int drank = s_off[j * NW + wid] + __popc(bal[j] & lt);
-      const int64_t id = a.ids ? a.ids[i] : i;
       if (dfr[j]) {
         const int64_t pos = excl + drank;
-        if (a.def_ids) a.def_ids[pos] = id;
+        if (a.def_ids) a.def_ids[pos] = idv[j];
         if (a.def_pos) a.def_pos[pos] = i;
       } else {
         const int64_t pos = acc_base + (local - drank);
-        if (a.acc_ids) a.acc_ids[pos] = id;
-        if (a.acc_conf) a.acc_conf[pos] = a.conf[i];
-        if (a.acc_pred) {
+        if (a.acc_ids) a.acc_ids[pos] = idv[j];
+        if (a.acc_conf) a.acc_conf[pos] = cv[j];
+        if (pred1) {
+          a.acc_pred[pos] = pv[j];
+        } else if (a.acc_pred) {
           for (int t = 0; t < a.pred_len; ++t)
             a.acc_pred[pos * a.pred_len + t] = a.pred[i * a.pred_len + t];
         }

@@ -67,11 +67,6 @@ __device__ __forceinline__ void write_row(const ConfArgs& a, int64_t row, int64_
   if (a.ok) a.ok[row] = (uint8_t)(a.labels ? (!bad && a.labels[src_row] == am) : 0);
 }
 
-__device__ __forceinline__ int64_t source_row(const ConfArgs& a, int64_t row) {
-  if (!a.row_index) return row;
-  if (a.L == 1) return a.row_index[row];
-  return a.row_index[row / a.L] * a.L + row % a.L;
-}
 
 __device__ __forceinline__ int64_t live_rows(const ConfArgs& a) {
   int64_t n = a.n;
@@ -79,11 +74,31 @@ __device__ __forceinline__ int64_t live_rows(const ConfArgs& a) {
     int64_t dn = *a.d_n;
     n = dn < n ? dn : n;
   }
-  return n * a.L;
+  return n * a.L * (int64_t)a.nbatch;
 }
 
 __device__ __forceinline__ uint32_t word(const uint4& v, int q) {
   return q == 0 ? v.x : q == 1 ? v.y : q == 2 ? v.z : v.w;
+}
+
+// Where output row `row` reads its logits: batch base pointer, temperature
+// factor and source row (row_index applies within the batch).
+struct RowSrc {
+  const char* base;
+  float c;
+  int64_t src;
+};
+__device__ __forceinline__ RowSrc locate(const ConfArgs& a, int64_t row) {
+  RowSrc r{(const char*)a.logits, a.c, row};
+  if (a.nbatch > 1) {
+    const int b = (int)(row / a.brows);
+    r.base = (const char*)a.bptr[b];
+    r.c = a.bc[b];
+    r.src = row - (int64_t)b * a.brows;
+  }
+  if (a.row_index)
+    r.src = a.L == 1 ? a.row_index[r.src] : a.row_index[r.src / a.L] * a.L + r.src % a.L;
+  return r;
 }
 
 // -inf for the out-of-row elements of the last partial 16-byte vector
@@ -175,39 +190,6 @@ __device__ __forceinline__ void vec_accum(const uint4& v, f2_t m2, f2_t c2, uint
   }
 }
 
-// Same, with a = x * c - RN(m * c) in ONE packed FFMA2 per element pair: every
-// exponent carries the same shift d = m*c - RN(m*c) (|d| <= ulp(m*c)/2) plus
-// one rounding, and d cancels exactly in p_max = 2^{a_max} / sum 2^a and in
-// H = log2(s) - w/s, so the fold costs no accuracy.
-template <bool BF16, bool ENTROPY>
-__device__ __forceinline__ void vec_accum_fma(const uint4& v, f2_t nmc2, f2_t c2, uint32_t clampw,
-                                              f2_t& s2, f2_t& w2) {
-  if (BF16) {
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      uint32_t u = ENTROPY ? bmax2_plain(word(v, q), clampw) : word(v, q);
-      f2_t a = f2fma(f2(bf_lo(u), bf_hi(u)), c2, nmc2);
-      f2_t e = f2(ex2(f2lo(a)), ex2(f2hi(a)));
-      s2 = f2add(s2, e);
-      if (ENTROPY) w2 = f2fma(e, a, w2);
-    }
-  } else {
-#pragma unroll
-    for (int q = 0; q < 2; ++q) {
-      f2_t a = f2fma(f2(__uint_as_float(word(v, 2 * q)), __uint_as_float(word(v, 2 * q + 1))), c2, nmc2);
-      float a0 = f2lo(a), a1 = f2hi(a);
-      if (ENTROPY) {
-        a0 = fmaxf(a0, -128.f);
-        a1 = fmaxf(a1, -128.f);
-        a = f2(a0, a1);
-      }
-      f2_t e = f2(ex2(a0), ex2(a1));
-      s2 = f2add(s2, e);
-      if (ENTROPY) w2 = f2fma(e, a, w2);
-    }
-  }
-}
-
 // bf16x2 word holding a lower bound L <= m - 128/c (rounded down): clamping
 // x >= L leaves every term with 2^a >= 2^-128 untouched and turns -inf into a
 // finite value whose 2^a flushes to 0, so 2^a * a stays 0 (masked classes).
@@ -219,6 +201,7 @@ __device__ __forceinline__ uint32_t entropy_clamp_word(float m, float c) {
   uint32_t u = (uint32_t)__bfloat16_as_ushort(b);
   return u | (u << 16);
 }
+
 
 // ---------------------------------------------------------------------------
 // K1a: G lanes per row (a warp reduces 32/G rows at once), row in registers.
@@ -233,15 +216,12 @@ __device__ __forceinline__ uint32_t vec_maxw(const uint4& v) {
   return __float_as_uint(fmax3_nan(__uint_as_float(v.x), __uint_as_float(v.y),
                                    fmax_nan(__uint_as_float(v.z), __uint_as_float(v.w))));
 }
-// does the vector whose max word is w contain the value m (m2w: m as bf16x2)?
+// does the vector whose max word is w contain the value m?  Compared in fp32:
+// IEEE equality (+0 == -0) with subnormals intact (a packed bf16x2 compare
+// flushes subnormals and would misplace the argmax of tiny logits).
 template <bool BF16>
-__device__ __forceinline__ bool maxw_has(uint32_t w, float m, uint32_t m2w) {
-  if (BF16) {
-    uint32_t r;
-    asm("{\n\t.reg .pred p, q;\n\tsetp.eq.bf16x2 p|q, %1, %2;\n\tor.pred p, p, q;\n\tselp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(r) : "r"(w), "r"(m2w));
-    return r != 0;
-  }
+__device__ __forceinline__ bool maxw_has(uint32_t w, float m) {
+  if (BF16) return fmax_nan(bf_lo(w), bf_hi(w)) == m;
   return __uint_as_float(w) == m;
 }
 
@@ -259,9 +239,9 @@ __device__ __forceinline__ void group_mask_tail(uint4 (&v)[NV], int gl, int nvec
 template <bool BF16, bool ENTROPY, int NV, int G>
 __device__ __forceinline__ void group_reduce_row(const ConfArgs& a, const uint4 (&v)[NV],
                                                  bool active, int64_t row, int64_t src, int gl,
-                                                 f2_t c2) {
+                                                 float c) {
   constexpr int VE = BF16 ? 8 : 4;
-  const float c = a.c;
+  const f2_t c2 = f2(c, c);
   // 1. row max (exact, NaN-propagating): packed per-vector maxima, then the group
   uint32_t vmw[NV];
   uint32_t lw = vec_maxw<BF16>(v[0]);
@@ -276,12 +256,10 @@ __device__ __forceinline__ void group_reduce_row(const ConfArgs& a, const uint4 
   for (int o = G / 2; o > 0; o >>= 1) m = fmax_nan(m, __shfl_xor_sync(0xFFFFFFFFu, m, o));
 
   // 2. argmax: lowest vector index holding m, then the first element in it
-  const uint32_t mb = __float_as_uint(m) >> 16;
-  const uint32_t m2w = mb | (mb << 16);
   unsigned vi = 0xFFFFFFFFu;
 #pragma unroll
   for (int k = NV - 1; k >= 0; --k)
-    if (maxw_has<BF16>(vmw[k], m, m2w)) vi = (unsigned)(k * G + gl);
+    if (maxw_has<BF16>(vmw[k], m)) vi = (unsigned)(k * G + gl);
 #pragma unroll
   for (int o = G / 2; o > 0; o >>= 1) vi = min(vi, (unsigned)__shfl_xor_sync(0xFFFFFFFFu, vi, o));
   const int owner = (int)(vi % G), kstar = (int)(vi / G);
@@ -296,15 +274,15 @@ __device__ __forceinline__ void group_reduce_row(const ConfArgs& a, const uint4 
   e = __shfl_sync(0xFFFFFFFFu, e, owner, G);
   const unsigned am = vi * VE + (unsigned)e;
 
-  // 3. exponentials with the common max: a = x*c - RN(m*c) (one FFMA2 per pair)
+  // 3. exponentials with the common max: a = (x - m) * c, x - m formed exactly
+  //    (FADD2, then FMUL2: one rounding, so the 1e-5 tolerance holds at T = 0.05)
   f2_t s2 = f2(0.f, 0.f), w2 = f2(0.f, 0.f);
   const bool valid = (m < INFINITY) && (m > -INFINITY);
-  const float nmc = -(m * c);
   if (valid) {
-    const f2_t nmc2 = f2(nmc, nmc);
     const uint32_t cw = ENTROPY && BF16 ? entropy_clamp_word(m, c) : 0u;
+    const f2_t m2 = f2(m, m);
 #pragma unroll
-    for (int k = 0; k < NV; ++k) vec_accum_fma<BF16, ENTROPY>(v[k], nmc2, c2, cw, s2, w2);
+    for (int k = 0; k < NV; ++k) vec_accum<BF16, ENTROPY>(v[k], m2, c2, cw, s2, w2);
   }
   float s = f2lo(s2) + f2hi(s2);
   float w = ENTROPY ? f2lo(w2) + f2hi(w2) : 0.f;
@@ -314,7 +292,7 @@ __device__ __forceinline__ void group_reduce_row(const ConfArgs& a, const uint4 
     if (ENTROPY) w += __shfl_xor_sync(0xFFFFFFFFu, w, o);
   }
   if (active && gl == 0) {
-    RowOut r{m, s, w, am, ex2(fmaf(m, c, nmc))};
+    RowOut r{m, s, w, am, 1.0f};
     write_row(a, row, src, r);
   }
 }
@@ -326,59 +304,84 @@ __device__ __forceinline__ int64_t src_row(const ConfArgs& a, int64_t r) {
   return a.row_index[r / a.L] * a.L + r % a.L;
 }
 
-// predicated 16-byte loads of one group's row, all issued back to back
-template <bool BF16, int NV, int G>
-__device__ __forceinline__ void group_load_row(uint4 (&v)[NV], const uint4* p, int gl, int nvec,
-                                               bool active) {
+// 16-byte loads of one group's row, all issued back to back.  The pointer of
+// an inactive group is clamped to a valid row, so every vector below nvec can
+// be loaded unconditionally; only vector slots >= nvec need a default (-inf).
+// FULL: (NV-1)*G <= nvec, i.e. only the last slot k = NV-1 can be out of range
+// (no per-register default moves on the other NV-1 vectors).
+template <bool BF16, int NV, int G, bool FULL>
+__device__ __forceinline__ void group_load_row(uint4 (&v)[NV], const uint4* p, int gl, int nvec) {
   const uint32_t f = BF16 ? kBf16NegInf2 : kF32NegInf;
-  const int lim = active ? nvec : 0;
 #pragma unroll
   for (int k = 0; k < NV; ++k) {
     const int vi = k * G + gl;
-    uint4 r = make_uint4(f, f, f, f);
-    asm volatile(
-        "{\n\t.reg .pred p;\n\tsetp.lt.s32 p, %4, %5;\n\t"
-        "@p ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%6];\n\t}"
-        : "+r"(r.x), "+r"(r.y), "+r"(r.z), "+r"(r.w)
-        : "r"(vi), "r"(lim), "l"(p + vi));
-    v[k] = r;
+    if (FULL && k < NV - 1) {
+      v[k] = ldg_stream(p + vi);
+    } else {
+      uint4 r = make_uint4(f, f, f, f);
+      asm volatile(
+          "{\n\t.reg .pred p;\n\tsetp.lt.s32 p, %4, %5;\n\t"
+          "@p ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%6];\n\t}"
+          : "+r"(r.x), "+r"(r.y), "+r"(r.z), "+r"(r.w)
+          : "r"(vi), "r"(nvec), "l"(p + vi));
+      v[k] = r;
+    }
   }
 }
 
 // LDG variant: ping-pong register buffers, the next rows' loads are issued
 // before the current rows are reduced.
-template <bool BF16, bool ENTROPY, int NV, int G, bool L1>
+template <bool BF16, bool ENTROPY, int NV, int G, bool FULL>
 __global__ void __launch_bounds__(256) conf_warp_kernel(const ConfArgs a) {
   constexpr int RPW = 32 / G;      // rows per warp
   const int lane = threadIdx.x & 31, gl = lane % G, grp = lane / G;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t rows = live_rows(a);
-  const f2_t c2 = f2(a.c, a.c);
   const int nvec = a.nvec;
-  const char* base = (const char*)a.logits;
-  auto ptr = [&](int64_t r, bool act) {
-    return reinterpret_cast<const uint4*>(base + (act ? src_row<L1>(a, r) : 0) * a.row_bytes);
+  auto load = [&](uint4 (&v)[NV], int64_t row, bool act) -> RowSrc {
+    RowSrc r = locate(a, act ? row : 0);   // inactive groups read a valid row
+    group_load_row<BF16, NV, G, FULL>(v, reinterpret_cast<const uint4*>(r.base + r.src * a.row_bytes),
+                                      gl, nvec);
+    return r;
   };
   const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (w0 * RPW >= rows) return;
   uint4 A[NV], B[NV];
   int64_t rowA = w0 * RPW + grp;
   bool actA = rowA < rows;
-  group_load_row<BF16, NV, G>(A, ptr(rowA, actA), gl, nvec, actA);
+  RowSrc rA = load(A, rowA, actA), rB = rA;
+#ifdef HS_PP_COPY
+  // experiment: one reduce site, B copied into A each pass (half the code)
   while (true) {
     const int64_t rowB = rowA + nwarps * RPW;
     const bool anyB = (rowB - grp) < rows;
     const bool actB = rowB < rows;
-    if (anyB) group_load_row<BF16, NV, G>(B, ptr(rowB, actB), gl, nvec, actB);
+    if (anyB) rB = load(B, rowB, actB);
     if (a.tail) group_mask_tail<BF16, NV, G>(A, gl, nvec, a.tail);
-    group_reduce_row<BF16, ENTROPY, NV, G>(a, A, actA, rowA, actA ? src_row<L1>(a, rowA) : 0, gl, c2);
+    group_reduce_row<BF16, ENTROPY, NV, G>(a, A, actA, rowA, rA.src, gl, rA.c);
+    if (!anyB) break;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) A[k] = B[k];
+    rowA = rowB;
+    actA = actB;
+    rA = rB;
+  }
+  return;
+#endif
+  while (true) {
+    const int64_t rowB = rowA + nwarps * RPW;
+    const bool anyB = (rowB - grp) < rows;
+    const bool actB = rowB < rows;
+    if (anyB) rB = load(B, rowB, actB);
+    if (a.tail) group_mask_tail<BF16, NV, G>(A, gl, nvec, a.tail);
+    group_reduce_row<BF16, ENTROPY, NV, G>(a, A, actA, rowA, rA.src, gl, rA.c);
     if (!anyB) break;
     rowA = rowB + nwarps * RPW;
     const bool anyA = (rowA - grp) < rows;
     actA = rowA < rows;
-    if (anyA) group_load_row<BF16, NV, G>(A, ptr(rowA, actA), gl, nvec, actA);
+    if (anyA) rA = load(A, rowA, actA);
     if (a.tail) group_mask_tail<BF16, NV, G>(B, gl, nvec, a.tail);
-    group_reduce_row<BF16, ENTROPY, NV, G>(a, B, actB, rowB, actB ? src_row<L1>(a, rowB) : 0, gl, c2);
+    group_reduce_row<BF16, ENTROPY, NV, G>(a, B, actB, rowB, rB.src, gl, rB.c);
     if (!anyA) break;
   }
 }
@@ -450,7 +453,6 @@ __global__ void __launch_bounds__(32 * (NCW + 1), 1) conf_tma_kernel(const ConfA
   }
   // ---------------- consumers ----------------
   const int cw = warp - 1, gl = lane % G, grp = lane / G;
-  const f2_t c2 = f2(a.c, a.c);
   const uint32_t f = BF16 ? kBf16NegInf2 : kF32NegInf;
   int it = 0;
   for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
@@ -469,7 +471,7 @@ __global__ void __launch_bounds__(32 * (NCW + 1), 1) conf_tma_kernel(const ConfA
       v[k] = vi < lim ? lds128(srow + (size_t)vi * 16) : make_uint4(f, f, f, f);
     }
     if (a.tail) group_mask_tail<BF16, NV, G>(v, gl, nvec, a.tail);
-    group_reduce_row<BF16, ENTROPY, NV, G>(a, v, act, row, act ? src_row<L1>(a, row) : 0, gl, c2);
+    group_reduce_row<BF16, ENTROPY, NV, G>(a, v, act, row, act ? src_row<L1>(a, row) : 0, gl, a.c);
     // every lane has consumed its staged vectors (the row max read them all)
     __syncwarp();
     if (lane == 0) mbar_arrive(&ring->empty[st]);
@@ -487,12 +489,13 @@ __global__ void __launch_bounds__(NT) conf_cta_kernel(const ConfArgs a) {
   __shared__ unsigned sh_am[NW];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int64_t rows = live_rows(a);
-  const float c = a.c;
-  const f2_t c2 = f2(c, c);
 
   for (int64_t row = blockIdx.x; row < rows; row += gridDim.x) {
-    const int64_t src = source_row(a, row);
-    const uint4* p = reinterpret_cast<const uint4*>((const char*)a.logits + src * a.row_bytes);
+    const RowSrc rs = locate(a, row);
+    const int64_t src = rs.src;
+    const float c = rs.c;
+    const f2_t c2 = f2(c, c);
+    const uint4* p = reinterpret_cast<const uint4*>(rs.base + src * a.row_bytes);
     float m = -INFINITY;
     f2_t s2 = f2(0.f, 0.f), w2 = f2(0.f, 0.f);
     unsigned am = 0xFFFFFFFFu;
@@ -607,16 +610,16 @@ int occupancy(K kernel, int threads) {
   return b > 0 ? b : 1;
 }
 
-template <bool BF16, bool ENTROPY, int NV, int G, bool L1>
+template <bool BF16, bool ENTROPY, int NV, int G, bool FULL>
 int warp_occ() {
-  static const int o = occupancy(conf_warp_kernel<BF16, ENTROPY, NV, G, L1>, 256);
+  static const int o = occupancy(conf_warp_kernel<BF16, ENTROPY, NV, G, FULL>, 256);
   return o;
 }
 
-template <bool BF16, bool ENTROPY, int NV, int G, bool L1>
+template <bool BF16, bool ENTROPY, int NV, int G, bool FULL>
 cudaError_t launch_warp_l(const ConfArgs& a, int64_t rows, cudaStream_t s) {
-  auto k = conf_warp_kernel<BF16, ENTROPY, NV, G, L1>;
-  const int occ = warp_occ<BF16, ENTROPY, NV, G, L1>();
+  auto k = conf_warp_kernel<BF16, ENTROPY, NV, G, FULL>;
+  const int occ = warp_occ<BF16, ENTROPY, NV, G, FULL>();
   constexpr int RPB = 8 * (32 / G);      // rows per 256-thread block per pass
   const int64_t want = (rows + RPB - 1) / RPB;
   const int64_t cap = (int64_t)num_sms() * occ;
@@ -628,8 +631,11 @@ cudaError_t launch_warp_l(const ConfArgs& a, int64_t rows, cudaStream_t s) {
 
 template <bool BF16, bool ENTROPY, int NV, int G>
 cudaError_t launch_warp(const ConfArgs& a, int64_t rows, cudaStream_t s) {
-  return a.L == 1 ? launch_warp_l<BF16, ENTROPY, NV, G, true>(a, rows, s)
-                  : launch_warp_l<BF16, ENTROPY, NV, G, false>(a, rows, s);
+#ifdef HS_NO_FULL
+  return launch_warp_l<BF16, ENTROPY, NV, G, false>(a, rows, s);
+#endif
+  return (NV - 1) * G <= a.nvec ? launch_warp_l<BF16, ENTROPY, NV, G, true>(a, rows, s)
+                                : launch_warp_l<BF16, ENTROPY, NV, G, false>(a, rows, s);
 }
 
 template <bool BF16, bool ENTROPY, int NT>
@@ -670,22 +676,6 @@ cudaError_t launch_tma(const ConfArgs& a, int64_t rows, cudaStream_t s) {
                   : launch_tma_l<BF16, ENTROPY, NV, G, NCW, S, false>(a, rows, s);
 }
 
-// Exploration switch (HS_CONF_VARIANT) for the ViT-sized rows (nvec <= 128,
-// bf16, max-prob): A/B of staging and lane-grouping choices under ncu.
-int conf_variant() {
-  static const int v = [] {
-    const char* e = getenv("HS_CONF_VARIANT");
-    if (!e) return 0;
-    if (!strcmp(e, "ldg16x8")) return 1;
-    if (!strcmp(e, "ldg8x16")) return 2;
-    if (!strcmp(e, "tma8x16n12s2")) return 3;
-    if (!strcmp(e, "tma16x8n16s3")) return 4;
-    if (!strcmp(e, "tma8x16n8s3")) return 5;
-    return 0;
-  }();
-  return v;
-}
-
 int conf_impl() {   // 0 = LDG (registers, default), 1 = TMA ring
   static const int v = [] {
     const char* e = getenv("HS_CONF_IMPL");
@@ -698,16 +688,7 @@ int conf_impl() {   // 0 = LDG (registers, default), 1 = TMA ring
 template <bool BF16, bool ENTROPY>
 cudaError_t dispatch(const ConfArgs& a, int64_t rows, cudaStream_t s) {
   const int nvec = a.nvec;
-  if (BF16 && !ENTROPY && nvec > 64 && nvec <= 128 && conf_variant() != 0) {
-    switch (conf_variant()) {
-      case 1: return launch_warp<BF16, ENTROPY, 8, 16>(a, rows, s);
-      case 2: return launch_warp<BF16, ENTROPY, 16, 8>(a, rows, s);
-      case 3: return launch_tma<BF16, ENTROPY, 16, 8, 12, 2>(a, rows, s);
-      case 4: return launch_tma<BF16, ENTROPY, 8, 16, 16, 3>(a, rows, s);
-      default: return launch_tma<BF16, ENTROPY, 16, 8, 8, 3>(a, rows, s);
-    }
-  }
-  if (nvec <= 512 && conf_impl() == 1) {
+  if (nvec <= 512 && conf_impl() == 1 && a.nbatch == 1) {
     if (nvec <= 4) return launch_tma<BF16, ENTROPY, 1, 4>(a, rows, s);
     if (nvec <= 16) return launch_tma<BF16, ENTROPY, 4, 4>(a, rows, s);
     if (nvec <= 64) return launch_tma<BF16, ENTROPY, 16, 4>(a, rows, s);
@@ -719,6 +700,9 @@ cudaError_t dispatch(const ConfArgs& a, int64_t rows, cudaStream_t s) {
   if (nvec <= 16) return launch_warp<BF16, ENTROPY, 4, 4>(a, rows, s);
   if (nvec <= 32) return launch_warp<BF16, ENTROPY, 8, 4>(a, rows, s);
   if (nvec <= 64) return launch_warp<BF16, ENTROPY, 8, 8>(a, rows, s);
+#ifdef HS_G8
+  if (nvec <= 128) return launch_warp<BF16, ENTROPY, 16, 8>(a, rows, s);
+#endif
   if (nvec <= 128) return launch_warp<BF16, ENTROPY, 8, 16>(a, rows, s);
   if (nvec <= 256) return launch_warp<BF16, ENTROPY, 8, 32>(a, rows, s);
   if (nvec <= 512) return launch_warp<BF16, ENTROPY, 16, 32>(a, rows, s);
@@ -734,7 +718,7 @@ const char* confidence_path(int64_t nvec) {
 }
 
 cudaError_t launch_confidence(const ConfArgs& a, bool bf16, cudaStream_t s) {
-  const int64_t rows = a.n * a.L;
+  const int64_t rows = a.n * a.L * a.nbatch;
   const bool ent = a.kind == HS_CONF_ENTROPY;
   if (bf16) return ent ? dispatch<true, true>(a, rows, s) : dispatch<true, false>(a, rows, s);
   return ent ? dispatch<false, true>(a, rows, s) : dispatch<false, false>(a, rows, s);

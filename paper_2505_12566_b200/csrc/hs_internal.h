@@ -12,6 +12,7 @@ int num_sms();          // SM count of the current device (cached per device)
 void count_launch();    // bumps the process-wide launch counter (hs_launch_count)
 
 // ---- K1 / K2 ---------------------------------------------------------------
+constexpr int kMaxBatch = 8;
 struct ConfArgs {
   const void* logits;
   int64_t row_bytes;       // row_stride * element size (multiple of 16)
@@ -29,6 +30,12 @@ struct ConfArgs {
   const int32_t* labels;   // indexed by source token row, or NULL
   uint8_t* ok;             // [n*L] argmax == label, or NULL
   uint32_t* status;        // or NULL
+  // batched stages (hs_confidence_batched): output rows [b*brows, (b+1)*brows)
+  // read batch b's logits bptr[b] at temperature factor bc[b]
+  int nbatch;              // 1 = plain call (logits, c)
+  int64_t brows;           // n * L rows per batch
+  const void* bptr[kMaxBatch];
+  float bc[kMaxBatch];
 };
 cudaError_t launch_confidence(const ConfArgs& a, bool bf16, cudaStream_t s);
 cudaError_t launch_seq_reduce(const float* tok_conf, const uint8_t* tok_ok, int64_t n,
@@ -86,6 +93,10 @@ cudaError_t launch_calib_hist(const float* conf, const uint8_t* correct, int K, 
 cudaError_t launch_calib_fused(const float* conf, const uint8_t* correct, int K, int64_t N, int q,
                                long long target, int32_t* b_idx, float* thr, int64_t* reach,
                                int64_t* handled, int64_t* correct_total, void* ws, cudaStream_t s);
+cudaError_t launch_calib_cluster(const float* conf, const uint8_t* correct, int K, int64_t N,
+                                 int q, long long target, int32_t* b_idx, float* thr,
+                                 int64_t* reach, int64_t* handled, int64_t* correct_total,
+                                 void* ws, cudaStream_t s);
 cudaError_t launch_calib_select(int K, int q, int round, int32_t* b_idx, float* thr,
                                 int64_t* reach, int64_t* handled, int64_t* correct_total,
                                 void* ws, cudaStream_t s);

@@ -14,7 +14,7 @@ import torch
 
 from . import (Cascade, StageSpec, _calib_out, calibrate_begin, calibrate_hist_view,
                calibrate_histogram, calibrate_select, calibrate_thresholds,
-               calibrate_workspace, confidence, cascade_step, route_compact)
+               calibrate_workspace, confidence, confidence_batched, cascade_step, route_compact)
 
 
 class Router:
@@ -29,12 +29,18 @@ class Router:
         self.group = group
         dev = self.device
         K = self.K
-        self.vconf = torch.empty(K - 1, self.n_val, dtype=torch.float32, device=dev)
+        # validation confidences of all K stages: rows 0..K-2 are the calibration input
+        self.vconf_all = torch.empty(K, self.n_val, dtype=torch.float32, device=dev)
+        self.vconf = self.vconf_all[: K - 1]
+        self.vconf_last = self.vconf_all[K - 1]
         self.vok = torch.empty(K, self.n_val, dtype=torch.uint8, device=dev)
-        self.vconf_last = torch.empty(self.n_val, dtype=torch.float32, device=dev)
         L = max(s.seq_len for s in stages)
-        self.vargmax = torch.empty(self.n_val * L, dtype=torch.int32, device=dev)
-        self.conf_ws = torch.empty(max(1, self.n_val * L * 5 + 1024), dtype=torch.uint8, device=dev)
+        self.vargmax = torch.empty(K * self.n_val * L, dtype=torch.int32, device=dev)
+        self.conf_ws = torch.empty(max(1, K * self.n_val * L * 5 + 1024), dtype=torch.uint8, device=dev)
+        # one launch for every stage when the stages share a prediction shape
+        s0 = stages[0]
+        self.batched = K <= 8 and all((s.n_classes, s.seq_len, s.kind, s.reduce) ==
+                                      (s0.n_classes, s0.seq_len, s0.kind, s0.reduce) for s in stages)
         self.cal = _calib_out(K, dev, None)
         self.cal_ws = calibrate_workspace(K, self.q, dev)
         self.status = torch.zeros(1, dtype=torch.int32, device=dev)
@@ -46,12 +52,21 @@ class Router:
                   stream=None) -> dict:
         """val_logits[k]: stage k's logits of the validation shard ([n_val*L, stride]);
         labels: int32 [n_val*L].  Thresholds stay on the device (self.cal['t'])."""
-        for k, s in enumerate(self.stages):
-            out = {"conf": self.vconf[k] if k < self.K - 1 else self.vconf_last,
-                   "argmax": self.vargmax[: self.n_val * s.seq_len], "correct": self.vok[k]}
-            confidence(val_logits[k], n=self.n_val, seq_len=s.seq_len, n_classes=s.n_classes,
-                       temperature=s.temperature, kind=s.kind, reduce=s.reduce, labels=labels,
-                       out=out, ws=self.conf_ws, status=self.status, stream=stream)
+        if self.batched:
+            s = self.stages[0]
+            confidence_batched(val_logits, [t.temperature for t in self.stages], n=self.n_val,
+                               seq_len=s.seq_len, n_classes=s.n_classes, kind=s.kind,
+                               reduce=s.reduce, labels=labels,
+                               out={"conf": self.vconf_all.view(-1), "argmax": self.vargmax,
+                                    "correct": self.vok.view(-1)},
+                               ws=self.conf_ws, status=self.status, stream=stream)
+        else:
+            for k, s in enumerate(self.stages):
+                out = {"conf": self.vconf_all[k],
+                       "argmax": self.vargmax[: self.n_val * s.seq_len], "correct": self.vok[k]}
+                confidence(val_logits[k], n=self.n_val, seq_len=s.seq_len, n_classes=s.n_classes,
+                           temperature=s.temperature, kind=s.kind, reduce=s.reduce, labels=labels,
+                           out=out, ws=self.conf_ws, status=self.status, stream=stream)
         if self.group is None:
             calibrate_thresholds(self.vconf, self.vok, log2_bins=self.q, target=target,
                                  out=self.cal, ws=self.cal_ws, stream=stream)

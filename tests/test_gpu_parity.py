@@ -430,16 +430,47 @@ def test_c3_sequences_sampled_launch_config(hs):
         assert np.array_equal(r["correct"].cpu().numpy(), ref["correct"])
 
 
-def test_calibration_fused_equals_split_rounds(hs, monkeypatch):
-    """The single cooperative launch (default) and the per-round histogram/select
-    launches give identical thresholds and counts."""
+def test_calibration_modes_agree(hs, monkeypatch):
+    """One cluster launch (DSMEM histogram merge; default for small sets), one
+    cooperative grid launch, and per-round histogram/select launches give
+    identical thresholds and counts."""
     fam = synth.FAMILIES["c2"]
     vconf, vok, _ = _gpu_val(hs, fam, 20000)
     for q in (3, 12, 14):
-        fused = hs.calibrate_thresholds(vconf, vok, log2_bins=q)
-        monkeypatch.setenv("HS_CALIB_SPLIT", "1")
-        split = hs.calibrate_thresholds(vconf, vok, log2_bins=q)
-        monkeypatch.delenv("HS_CALIB_SPLIT")
+        res = {}
+        for mode in ("cluster", "fused", "split"):
+            monkeypatch.setenv("HS_CALIB_MODE", mode)
+            res[mode] = hs.calibrate_thresholds(vconf, vok, log2_bins=q)
+        monkeypatch.delenv("HS_CALIB_MODE")
         torch.cuda.synchronize()
-        for key in ("b", "t", "reach", "handled", "correct_total"):
-            assert torch.equal(fused[key], split[key]), (q, key)
+        ref = oracle.calibrate(vconf.cpu().numpy(), vok.cpu().numpy(), q)
+        for mode, r in res.items():
+            assert np.array_equal(r["b"].cpu().numpy(), ref["b"]), (q, mode)
+            for key in ("b", "t", "reach", "handled", "correct_total"):
+                assert torch.equal(r[key], res["split"][key]), (q, mode, key)
+
+
+@pytest.mark.parametrize("key,n_val", [("c2", 3001), ("c1", 513), ("c4", 24)])
+def test_confidence_batched_equals_per_stage(hs, key, n_val):
+    """hs_confidence_batched (all stages in one launch) == K separate hs_confidence calls == oracle."""
+    fam = synth.FAMILIES[key]
+    vids = np.arange(n_val, dtype=np.int64) + synth.VAL_ID_BASE
+    lab = synth.labels_np(fam.seed, vids, fam.L, fam.C).reshape(-1)
+    lab_d = torch.from_numpy(lab).to(dev())
+    bits = [synth.logits_np(fam.seed, k, vids, fam.L, fam.C, fam.thr[k], fam.dtype) for k in range(fam.K)]
+    xs = [to_dev_bits(b, fam.dtype) for b in bits]
+    got = hs.confidence_batched(xs, fam.temps, n=n_val, seq_len=fam.L, kind=fam.kind,
+                                reduce=fam.reduce, labels=lab_d)
+    torch.cuda.synchronize()
+    for k in range(fam.K):
+        one = hs.confidence(xs[k], n=n_val, seq_len=fam.L, temperature=fam.temps[k], kind=fam.kind,
+                            reduce=fam.reduce, labels=lab_d)
+        torch.cuda.synchronize()
+        sl = slice(k * n_val, (k + 1) * n_val)
+        assert torch.equal(got["conf"][sl], one["conf"])
+        assert torch.equal(got["correct"][sl], one["correct"])
+        assert torch.equal(got["argmax"][k * n_val * fam.L:(k + 1) * n_val * fam.L], one["argmax"])
+        ref = oracle.confidence(bits[k], n_val, fam.L, fam.C, fam.C, fam.temps[k], kind=fam.kind,
+                                reduce=fam.reduce, labels=lab)
+        assert_conf_close(got["conf"][sl].cpu().numpy(), ref["conf"])
+        assert np.array_equal(got["correct"][sl].cpu().numpy(), ref["correct"])
