@@ -378,43 +378,51 @@ def run_e2e(args, fam, router, route, val, labels, payload, stream, world):
 # ---------------------------------------------------------------------------
 # the oracle on the host cores (cpu_baseline leg and --impl reference)
 # ---------------------------------------------------------------------------
-def oracle_step(fam, frac_n: int, frac_val: int, seed_off: int = 0):
-    """One bounded oracle step on host-generated bytes of the same workload:
-    validation confidences of every stage -> calibration -> cascade routing.
-    Returns (seconds of oracle work, requests routed)."""
+def oracle_inputs(fam, frac_n: int, frac_val: int):
+    """Host bytes of a bounded sample of the workload (same keyed generator)."""
     import numpy as np
-    import oracle
     from workload import synth
     K = fam.K
-    ids = np.arange(frac_n, dtype=np.int64) + seed_off
+    ids = np.arange(frac_n, dtype=np.int64)
     vids = np.arange(frac_val, dtype=np.int64) + synth.VAL_ID_BASE
     lab = synth.labels_np(fam.seed, vids, fam.L, fam.C).reshape(-1)
     vl = [synth.logits_np(fam.seed, k, vids, fam.L, fam.C, fam.thr[k], fam.dtype) for k in range(K)]
     rl = [synth.logits_np(fam.seed, k, ids, fam.L, fam.C, fam.thr[k], fam.dtype) for k in range(K)]
+    return {"n": frac_n, "v": frac_val, "lab": lab, "vl": vl, "rl": rl}
+
+
+def oracle_step(fam, inp):
+    """One oracle step (the oracle as it stands, all host threads): validation
+    confidences of every stage -> calibration -> cascade routing of the sample.
+    Returns (seconds, requests routed)."""
+    import numpy as np
+    import oracle
+    K, nv, n = fam.K, inp["v"], inp["n"]
     t = time.perf_counter()
-    conf = np.empty((K - 1, frac_val))
-    ok = np.empty((K, frac_val), np.uint8)
+    conf = np.empty((K - 1, nv))
+    ok = np.empty((K, nv), np.uint8)
     for k in range(K):
-        r = oracle.confidence(vl[k], frac_val, fam.L, fam.C, fam.C, fam.temps[k], kind=fam.kind,
-                              reduce=fam.reduce, labels=lab)
+        r = oracle.confidence(inp["vl"][k], nv, fam.L, fam.C, fam.C, fam.temps[k], kind=fam.kind,
+                              reduce=fam.reduce, labels=inp["lab"])
         ok[k] = r["correct"]
         if k < K - 1:
             conf[k] = r["conf"]
     cal = oracle.calibrate(conf, ok, fam.log2_bins)
-    batch = np.arange(frac_n, dtype=np.int64)
+    batch = np.arange(n, dtype=np.int64)
     for k in range(K):
-        r = oracle.confidence(rl[k], len(batch), fam.L, fam.C, fam.C, fam.temps[k], kind=fam.kind,
-                              reduce=fam.reduce, row_index=batch)
+        r = oracle.confidence(inp["rl"][k], len(batch), fam.L, fam.C, fam.C, fam.temps[k],
+                              kind=fam.kind, reduce=fam.reduce, row_index=batch)
         acc, dfr = oracle.route(r["conf"], float(np.float32(cal["t"][k])), k == K - 1)
         batch = batch[dfr]
-    return time.perf_counter() - t, frac_n
+    return time.perf_counter() - t, n
 
 
 def cpu_sample_sizes(fam, seconds: float):
-    """Scale the oracle sample so one step takes ~`seconds` on this host."""
-    n0 = min(fam.n, 2048)
+    """Scale the oracle sample so one step takes ~`seconds` on this host (capped
+    at the full per-GPU workload)."""
+    n0 = min(fam.n, 1024)
     v0 = max(64, int(n0 * fam.n_val / fam.n))
-    dt, _ = oracle_step(fam, n0, v0)
+    dt, _ = oracle_step(fam, oracle_inputs(fam, n0, v0))
     scale = max(1.0, seconds / max(dt, 1e-3))
     n = int(min(fam.n, n0 * scale))
     v = int(min(fam.n_val, max(64, n * fam.n_val / fam.n)))
@@ -422,11 +430,19 @@ def cpu_sample_sizes(fam, seconds: float):
 
 
 def cpu_baseline(fam, seconds: float):
+    """The oracle on the host cores, repeated over a bounded sample for ~`seconds`."""
     n, v = cpu_sample_sizes(fam, seconds)
-    dt, routed = oracle_step(fam, n, v)
-    return {"value": routed / dt, "unit": "requests/s", "cores": os.cpu_count(), "kind": "oracle",
-            "sample": f"{n} of {fam.n} requests + {v} of {fam.n_val} validation samples of "
-                      f"{fam.name} (same generator), fp64 C oracle, {dt:.1f} s"}
+    inp = oracle_inputs(fam, n, v)
+    tot, routed, reps = 0.0, 0, 0
+    while tot < seconds and reps < 100:
+        dt, r = oracle_step(fam, inp)
+        tot += dt
+        routed += r
+        reps += 1
+    return {"value": routed / tot, "unit": "requests/s", "cores": os.cpu_count(), "kind": "oracle",
+            "sample": f"{reps} x ({n} of {fam.n} requests + {v} of {fam.n_val} validation samples "
+                      f"of {fam.name}, same generator), fp64 C oracle on {os.cpu_count()} threads, "
+                      f"{tot:.1f} s"}
 
 
 def run_reference(args, world, rank):
@@ -436,12 +452,13 @@ def run_reference(args, world, rank):
     fam = family(args.config)
     budget = 150.0 / max(1, args.steps + args.warmup)
     n, v = cpu_sample_sizes(fam, min(budget, 20.0))
+    inp = oracle_inputs(fam, n, v)
     for _ in range(args.warmup):
-        oracle_step(fam, n, v)
+        oracle_step(fam, inp)
     tot = 0.0
     routed = 0
     for _ in range(args.steps):
-        dt, r = oracle_step(fam, n, v)
+        dt, r = oracle_step(fam, inp)
         tot += dt
         routed += r
     value = routed / tot

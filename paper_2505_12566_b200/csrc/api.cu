@@ -18,6 +18,13 @@ namespace hs {
 
 static std::atomic<uint64_t> g_launches{0};
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("HS_NO_PDL");
+    return !(e && e[0] == '1');
+  }();
+  return on;
+}
 
 int num_sms() {
   static std::mutex mu;
@@ -213,6 +220,8 @@ hs_status_t hs_confidence_batched(const void* const* logits, const float* temper
   }
   if (n > 0 && !conf) return fail(HS_ERR_INVALID_ARGUMENT, "conf output is required");
   if (correct && !labels) return fail(HS_ERR_INVALID_ARGUMENT, "correct requires labels");
+  if ((int64_t)n_batches * n * seq_len >= (int64_t(1) << 32))
+    return fail(HS_ERR_INVALID_ARGUMENT, "n_batches * n * seq_len must be < 2^32");
   const size_t need = conf_ws((int64_t)n_batches * n, seq_len);
   if (ws_bytes < need || (need && !ws))
     return fail(HS_ERR_WORKSPACE_TOO_SMALL, "workspace %zu < %zu", ws_bytes, need);

@@ -6,9 +6,10 @@
 // bin(c) >= b  <=>  c >= b/B), NaN confidences never accepted.
 // Round k (one model) over the validation samples still alive:
 //   K5: one pass builds a shared-memory-privatised histogram over bin(c_k) of
-//       (count, correct_k, correct_K), packed as ONE 64-bit shared atomic per
-//       sample (3 x 21-bit fields), warp-aggregated with __match_any_sync for
-//       the skewed bins near c = 1, flushed with global int32 atomics.
+//       (count, correct_k, correct_K) in three u32 arrays (native 32-bit
+//       shared atomics), warp-aggregated with __match_any_sync for the skewed
+//       bins near c = 1; CTAs merge through DSMEM (one cluster) or global
+//       int32 atomics (many CTAs).
 //   K6: one CTA: suffix scan over the B+2 bins and
 //       b_k = min{ b : A + G + S(b) >= tau } (S is not monotone: every b is
 //       examined), then A += committed correct answers; reach/handled counts.
@@ -34,6 +35,7 @@ __device__ __forceinline__ int bin_of(float c, int q) {
 }
 
 __global__ void calib_init_kernel(CalibState* st, int32_t* hist, int nwords, long long target) {
+  pdl_start();
   for (int i = threadIdx.x; i < nwords; i += blockDim.x) hist[i] = 0;
   if (threadIdx.x == 0) {
     st->A = 0;
@@ -44,16 +46,21 @@ __global__ void calib_init_kernel(CalibState* st, int32_t* hist, int nwords, lon
 
 // hist layout: int32 [3][B+2]; index 0 = NaN bin (never accepted), index b+1 = bin b.
 // Build this CTA's share of round `round` in shared memory: samples r = start,
-// start + stride, ...  (packed u64 per bin: count | correct_k << 21 | correct_K << 42).
+// start + stride, ...  Three u32 arrays (count, correct_k, correct_K per bin):
+// native 32-bit shared atomics (a 64-bit shared add would be a CAS loop).
 __device__ __forceinline__ void hist_local(const float* __restrict__ conf,
                                            const uint8_t* __restrict__ correct, int K, int64_t N,
                                            int q, int round, const int32_t* b_idx,
-                                           unsigned long long* sh, int64_t start, int64_t stride) {
+                                           unsigned* sh, int64_t start, int64_t stride) {
+  __shared__ int s_b[16];
   const int nb = (1 << q) + 2;
-  for (int i = threadIdx.x; i < nb; i += blockDim.x) sh[i] = 0ull;
-  int bprev[16];
-#pragma unroll
-  for (int j = 0; j < 16; ++j) bprev[j] = (j < round) ? b_idx[j] : 0;
+  {  // zero the three arrays with 16-byte stores (3*nb is even; tail handled)
+    const int words = 3 * nb;
+    uint4* sh4 = reinterpret_cast<uint4*>(sh);
+    for (int i = threadIdx.x; i < words / 4; i += blockDim.x) sh4[i] = make_uint4(0, 0, 0, 0);
+    for (int i = (words / 4) * 4 + threadIdx.x; i < words; i += blockDim.x) sh[i] = 0u;
+  }
+  if (threadIdx.x < 16) s_b[threadIdx.x] = threadIdx.x < round ? b_idx[threadIdx.x] : 0;
   __syncthreads();
 
   const uint8_t* ck = correct + (int64_t)round * N;
@@ -62,18 +69,16 @@ __device__ __forceinline__ void hist_local(const float* __restrict__ conf,
   // loop bound is warp-uniform so __match_any_sync sees full warps
   const int64_t Nup = (N + 31) & ~(int64_t)31;
   for (int64_t r = start; r < Nup; r += stride) {
-    // issue every load of this sample first (no short-circuit chain)
     const bool in = r < N;
-    float cprev[16];
-#pragma unroll
-    for (int j = 0; j < 16; ++j) cprev[j] = (in && j < round) ? __ldg(conf + (int64_t)j * N + r) : 0.f;
-    const float cnow = in ? __ldg(ckconf + r) : 0.f;
-    const bool okk = in && __ldg(ck + r) != 0;
-    const bool okK0 = in && __ldg(cK + r) != 0;
+    const int64_t rr = in ? r : 0;
+    // this round's loads first; earlier rounds' confidences decide "alive"
+    const float cnow = __ldg(ckconf + rr);
+    const bool okk = __ldg(ck + rr) != 0;
+    const bool okK0 = __ldg(cK + rr) != 0;
     bool alive = in;
-#pragma unroll
-    for (int j = 0; j < 16; ++j)
-      if (j < round) alive &= bin_of(cprev[j], q) < bprev[j];
+    const float* cp = conf + rr;
+#pragma unroll 4
+    for (int j = 0; j < round; ++j, cp += N) alive &= bin_of(__ldg(cp), q) < s_b[j];
     const int key = alive ? bin_of(cnow, q) + 1 : -1;   // -1: not counted
     const bool okK = alive && okK0;
     // warp aggregation: lanes with the same bin add once, through their leader
@@ -81,27 +86,21 @@ __device__ __forceinline__ void hist_local(const float* __restrict__ conf,
     const unsigned bk = __ballot_sync(0xFFFFFFFFu, alive && okk);
     const unsigned bK = __ballot_sync(0xFFFFFFFFu, okK);
     if (key >= 0 && (threadIdx.x & 31) == __ffs(peers) - 1) {
-      const unsigned long long tot = (unsigned long long)__popc(peers) |
-                                     ((unsigned long long)__popc(peers & bk) << 21) |
-                                     ((unsigned long long)__popc(peers & bK) << 42);
-      atomicAdd(&sh[key], tot);
+      atomicAdd(&sh[key], (unsigned)__popc(peers));
+      const unsigned nk = __popc(peers & bk), nK = __popc(peers & bK);
+      if (nk) atomicAdd(&sh[nb + key], nk);
+      if (nK) atomicAdd(&sh[2 * nb + key], nK);
     }
   }
   __syncthreads();
 }
 
-constexpr unsigned long long kField = (1ull << 21) - 1;
-
-// Add a packed shared-memory histogram into the global int32 [3][B+2] one.
-__device__ __forceinline__ void hist_flush(const unsigned long long* sh, int q, int32_t* hist) {
+// Add a shared-memory histogram into the global int32 [3][B+2] one.
+__device__ __forceinline__ void hist_flush(const unsigned* sh, int q, int32_t* hist) {
   const int nb = (1 << q) + 2;
-  for (int i = threadIdx.x; i < nb; i += blockDim.x) {
-    const unsigned long long v = sh[i];
-    if (v) {
-      atomicAdd(&hist[i], (int32_t)(v & kField));
-      atomicAdd(&hist[nb + i], (int32_t)((v >> 21) & kField));
-      atomicAdd(&hist[2 * nb + i], (int32_t)((v >> 42) & kField));
-    }
+  for (int i = threadIdx.x; i < 3 * nb; i += blockDim.x) {
+    const unsigned v = sh[i];
+    if (v) atomicAdd(&hist[i], (int32_t)v);
   }
 }
 
@@ -109,7 +108,7 @@ __device__ __forceinline__ void hist_flush(const unsigned long long* sh, int q, 
 __device__ __forceinline__ void hist_body(const float* __restrict__ conf,
                                           const uint8_t* __restrict__ correct, int K, int64_t N,
                                           int q, int round, const int32_t* b_idx,
-                                          int32_t* __restrict__ hist, unsigned long long* sh) {
+                                          int32_t* __restrict__ hist, unsigned* sh) {
   hist_local(conf, correct, K, N, q, round, b_idx, sh,
              (int64_t)blockIdx.x * blockDim.x + threadIdx.x, (int64_t)gridDim.x * blockDim.x);
   hist_flush(sh, q, hist);
@@ -120,12 +119,13 @@ __global__ void __launch_bounds__(512) calib_hist_kernel(const float* __restrict
                                                          int K, int64_t N, int q, int round,
                                                          const int32_t* __restrict__ b_idx,
                                                          int32_t* __restrict__ hist) {
-  extern __shared__ unsigned long long sh[];
+  pdl_start();
+  extern __shared__ unsigned sh[];
   hist_body(conf, correct, K, N, q, round, b_idx, hist, sh);
 }
 
 // Histogram readers for the select: the int32 [3][B+2] global layout, or the
-// packed u64 shared-memory layout of the cluster kernel.
+// u32 shared-memory layout of the cluster kernel.
 struct Bin3 { long long cnt, ck, cK; };
 struct GlobalHist {
   const int32_t* h;
@@ -134,11 +134,11 @@ struct GlobalHist {
     return Bin3{h[i], h[nb + i], h[2 * nb + i]};
   }
 };
-struct PackedHist {
-  const unsigned long long* h;
+struct SharedHist {
+  const unsigned* h;
+  int nb;
   __device__ __forceinline__ Bin3 operator()(int i) const {
-    const unsigned long long v = h[i];
-    return Bin3{(long long)(v & kField), (long long)((v >> 21) & kField), (long long)((v >> 42) & kField)};
+    return Bin3{(long long)h[i], (long long)h[nb + i], (long long)h[2 * nb + i]};
   }
 };
 
@@ -292,6 +292,7 @@ __global__ void __launch_bounds__(1024) calib_select_kernel(int K, int q, int ro
                                                             int64_t* reach, int64_t* handled,
                                                             int64_t* correct_total,
                                                             CalibState* st, int32_t* hist) {
+  pdl_start();
   select_body<1024>(K, q, round, b_idx, thr, reach, handled, correct_total, st, hist);
 }
 
@@ -304,7 +305,8 @@ __global__ void __launch_bounds__(1024) calib_fused_kernel(const float* __restri
                                                            int64_t* reach, int64_t* handled,
                                                            int64_t* correct_total, CalibState* st,
                                                            int32_t* hist) {
-  extern __shared__ unsigned long long sh[];
+  pdl_start();
+  extern __shared__ unsigned sh[];
   cg::grid_group grid = cg::this_grid();
   if (blockIdx.x == 0) {
     const int nw = 3 * ((1 << q) + 2);
@@ -324,13 +326,13 @@ __global__ void __launch_bounds__(1024) calib_fused_kernel(const float* __restri
   }
 }
 
-// All K-1 rounds on ONE thread-block cluster (small validation sets, N < 2^21):
+// All K-1 rounds on ONE thread-block cluster (validation sets below 2^20):
 // every CTA builds a private shared-memory histogram of its samples, the
 // cluster barrier publishes them, CTA rank 0 sums the other CTAs' histograms
 // through distributed shared memory (DSMEM loads), writes the combined
 // histogram once and runs the select; a second cluster barrier releases the
 // next round.  No global atomics and no grid-wide barrier.
-__global__ void __launch_bounds__(1024) calib_cluster_kernel(const float* __restrict__ conf,
+__global__ void __launch_bounds__(1024, 1) calib_cluster_kernel(const float* __restrict__ conf,
                                                              const uint8_t* __restrict__ correct,
                                                              int K, int64_t N, int q,
                                                              long long target, int32_t* b_idx,
@@ -338,7 +340,8 @@ __global__ void __launch_bounds__(1024) calib_cluster_kernel(const float* __rest
                                                              int64_t* handled,
                                                              int64_t* correct_total,
                                                              CalibState* st, int32_t* hist) {
-  extern __shared__ unsigned long long sh[];
+  pdl_start();
+  extern __shared__ unsigned sh[];
   cg::cluster_group cluster = cg::this_cluster();
   const unsigned rank = cluster.block_rank(), ncta = cluster.num_blocks();
   const int nb = (1 << q) + 2;
@@ -355,15 +358,18 @@ __global__ void __launch_bounds__(1024) calib_cluster_kernel(const float* __rest
     hist_local(conf, correct, K, N, q, k, b_idx, sh,
                (int64_t)rank * blockDim.x + threadIdx.x, (int64_t)ncta * blockDim.x);
     cluster.sync();
-    if (rank == 0) {
-      for (int i = threadIdx.x; i < nb; i += blockDim.x) {
-        unsigned long long v = sh[i];
-        for (unsigned c = 1; c < ncta; ++c) v += *cluster.map_shared_rank(&sh[i], c);
-        sh[i] = v;
+    // ranks 1.. push their non-empty bins into rank 0's histogram (DSMEM
+    // atomics, no round trip)
+    if (rank != 0) {
+      unsigned* dst = cluster.map_shared_rank(sh, 0);
+      for (int i = threadIdx.x; i < 3 * nb; i += blockDim.x) {
+        const unsigned v = sh[i];
+        if (v) atomicAdd(dst + i, v);
       }
-      __syncthreads();
-      select_core<1024>(PackedHist{sh}, K, q, k, b_idx, thr, reach, handled, correct_total, st);
     }
+    cluster.sync();
+    if (rank == 0)
+      select_core<1024>(SharedHist{sh, nb}, K, q, k, b_idx, thr, reach, handled, correct_total, st);
     cluster.sync();
   }
 }
@@ -381,45 +387,39 @@ static int32_t* hist_of(void* ws) {
 }
 
 cudaError_t launch_calib_init(void* ws, int q, long long target, cudaStream_t s) {
-  calib_init_kernel<<<1, 1024, 0, s>>>(reinterpret_cast<CalibState*>(ws), hist_of(ws),
-                                       3 * ((1 << q) + 2), target);
-  count_launch();
-  return cudaGetLastError();
+  return launch_pdl(calib_init_kernel, dim3(1), dim3(1024), 0, s, reinterpret_cast<CalibState*>(ws),
+                    hist_of(ws), 3 * ((1 << q) + 2), target);
 }
 
 cudaError_t launch_calib_hist(const float* conf, const uint8_t* correct, int K, int64_t N, int q,
                               int round, const int32_t* b_idx, int32_t* hist, cudaStream_t s) {
-  const size_t smem = (size_t)((1 << q) + 2) * sizeof(unsigned long long);
+  const size_t smem = (size_t)3 * ((1 << q) + 2) * sizeof(unsigned);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(calib_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)(((1 << 14) + 2) * sizeof(unsigned long long)));
+                         (int)(3 * ((1 << 14) + 2) * sizeof(unsigned)));
     attr = true;
   }
-  // every CTA sees < 2^21 samples per bin field
   int64_t grid = (N + 512 * 8 - 1) / (512 * 8);
   const int64_t cap = (int64_t)num_sms() * 2;
   if (grid > cap) grid = cap;
-  const int64_t min_grid = (N >> 20) + 1;
-  if (grid < min_grid) grid = min_grid;
   if (grid < 1) grid = 1;
-  calib_hist_kernel<<<(int)grid, 512, smem, s>>>(conf, correct, K, N, q, round, b_idx, hist);
-  count_launch();
-  return cudaGetLastError();
+  return launch_pdl(calib_hist_kernel, dim3((int)grid), dim3(512), smem, s, conf, correct, K, N, q,
+                    round, b_idx, hist);
 }
 
 cudaError_t launch_calib_fused(const float* conf, const uint8_t* correct, int K, int64_t N, int q,
                                long long target, int32_t* b_idx, float* thr, int64_t* reach,
                                int64_t* handled, int64_t* correct_total, void* ws,
                                cudaStream_t s) {
-  const size_t smem = (size_t)((1 << q) + 2) * sizeof(unsigned long long);
+  const size_t smem = (size_t)3 * ((1 << q) + 2) * sizeof(unsigned);
   static int max_blocks = -1;
   if (max_blocks < 0) {
     cudaFuncSetAttribute(calib_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)(((1 << 14) + 2) * sizeof(unsigned long long)));
+                         (int)(3 * ((1 << 14) + 2) * sizeof(unsigned)));
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, calib_fused_kernel, 1024,
-                                                  ((1 << 14) + 2) * sizeof(unsigned long long));
+                                                  3 * ((1 << 14) + 2) * sizeof(unsigned));
     max_blocks = per_sm > 0 ? per_sm * num_sms() : 0;
   }
   int grid = (int)((N + 1023) / 1024);
@@ -443,11 +443,11 @@ cudaError_t launch_calib_cluster(const float* conf, const uint8_t* correct, int 
                                  int q, long long target, int32_t* b_idx, float* thr,
                                  int64_t* reach, int64_t* handled, int64_t* correct_total,
                                  void* ws, cudaStream_t s) {
-  const size_t smem = (size_t)((1 << q) + 2) * sizeof(unsigned long long);
+  const size_t smem = (size_t)3 * ((1 << q) + 2) * sizeof(unsigned);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(calib_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)(((1 << 14) + 2) * sizeof(unsigned long long)));
+                         (int)(3 * ((1 << 14) + 2) * sizeof(unsigned)));
     attr = true;
   }
   cudaLaunchConfig_t cfg = {};
@@ -455,13 +455,15 @@ cudaError_t launch_calib_cluster(const float* conf, const uint8_t* correct, int 
   cfg.blockDim = dim3(1024);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = kCalibCluster;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
   CalibState* st = reinterpret_cast<CalibState*>(ws);
   int32_t* hist = hist_of(ws);
   cudaError_t e = cudaLaunchKernelEx(&cfg, calib_cluster_kernel, conf, correct, K, N, q, target,
@@ -473,10 +475,8 @@ cudaError_t launch_calib_cluster(const float* conf, const uint8_t* correct, int 
 cudaError_t launch_calib_select(int K, int q, int round, int32_t* b_idx, float* thr,
                                 int64_t* reach, int64_t* handled, int64_t* correct_total,
                                 void* ws, cudaStream_t s) {
-  calib_select_kernel<<<1, 1024, 0, s>>>(K, q, round, b_idx, thr, reach, handled, correct_total,
-                                         reinterpret_cast<CalibState*>(ws), hist_of(ws));
-  count_launch();
-  return cudaGetLastError();
+  return launch_pdl(calib_select_kernel, dim3(1), dim3(1024), 0, s, K, q, round, b_idx, thr, reach,
+                    handled, correct_total, reinterpret_cast<CalibState*>(ws), hist_of(ws));
 }
 
 }  // namespace hs

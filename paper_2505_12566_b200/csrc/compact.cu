@@ -26,6 +26,7 @@ __device__ __forceinline__ unsigned long long* tile_status(void* ws) {
 }
 
 __global__ void __launch_bounds__(kCompactThreads) route_compact_kernel(const CompactArgs a) {
+  pdl_start();
   constexpr int T = kCompactThreads, I = kCompactItems, NW = T / 32;
   __shared__ unsigned s_tile;
   __shared__ int s_cnt[I * NW];     // deferred count per (item row j, warp), j-major
@@ -185,6 +186,7 @@ __global__ void __launch_bounds__(256) gather_rows_kernel(const int64_t* __restr
                                                           const int64_t* d_count, int64_t cap,
                                                           const uint4* __restrict__ src,
                                                           int64_t row_vec, uint4* __restrict__ dst) {
+  pdl_start();
   int64_t n = cap;
   if (d_count) n = min(*d_count, cap);
   const int lane = threadIdx.x & 31;
@@ -215,9 +217,7 @@ size_t compact_ws_bytes(int64_t n) {
 cudaError_t launch_route_compact(const CompactArgs& a, cudaStream_t s) {
   const int64_t tiles = (a.n + kCompactTile - 1) / kCompactTile;
   const int grid = (int)(tiles > 0 ? tiles : 1);
-  route_compact_kernel<<<grid, kCompactThreads, 0, s>>>(a);
-  count_launch();
-  return cudaGetLastError();
+  return launch_pdl(route_compact_kernel, dim3(grid), dim3(kCompactThreads), 0, s, a);
 }
 
 cudaError_t launch_gather_rows(const int64_t* pos, const int64_t* d_count, int64_t cap,
@@ -226,10 +226,8 @@ cudaError_t launch_gather_rows(const int64_t* pos, const int64_t* d_count, int64
   const int64_t want = (cap + 7) / 8;
   const int64_t lim = (int64_t)num_sms() * 8;
   const int grid = (int)(want < lim ? want : lim);
-  gather_rows_kernel<<<grid, 256, 0, s>>>(pos, d_count, cap, reinterpret_cast<const uint4*>(src),
-                                          row_bytes / 16, reinterpret_cast<uint4*>(dst));
-  count_launch();
-  return cudaGetLastError();
+  return launch_pdl(gather_rows_kernel, dim3(grid), dim3(256), 0, s, pos, d_count, cap,
+                    reinterpret_cast<const uint4*>(src), row_bytes / 16, reinterpret_cast<uint4*>(dst));
 }
 
 }  // namespace hs

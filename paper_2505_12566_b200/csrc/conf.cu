@@ -91,7 +91,7 @@ struct RowSrc {
 __device__ __forceinline__ RowSrc locate(const ConfArgs& a, int64_t row) {
   RowSrc r{(const char*)a.logits, a.c, row};
   if (a.nbatch > 1) {
-    const int b = (int)(row / a.brows);
+    const int b = (int)((uint32_t)row / (uint32_t)a.brows);   // rows < 2^32
     r.base = (const char*)a.bptr[b];
     r.c = a.bc[b];
     r.src = row - (int64_t)b * a.brows;
@@ -333,6 +333,7 @@ __device__ __forceinline__ void group_load_row(uint4 (&v)[NV], const uint4* p, i
 // before the current rows are reduced.
 template <bool BF16, bool ENTROPY, int NV, int G, bool FULL>
 __global__ void __launch_bounds__(256) conf_warp_kernel(const ConfArgs a) {
+  pdl_start();
   constexpr int RPW = 32 / G;      // rows per warp
   const int lane = threadIdx.x & 31, gl = lane % G, grp = lane / G;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -350,8 +351,9 @@ __global__ void __launch_bounds__(256) conf_warp_kernel(const ConfArgs a) {
   int64_t rowA = w0 * RPW + grp;
   bool actA = rowA < rows;
   RowSrc rA = load(A, rowA, actA), rB = rA;
-#ifdef HS_PP_COPY
-  // experiment: one reduce site, B copied into A each pass (half the code)
+  if (NV >= 16) {
+  // one reduce site, B copied into A each pass: half the code of the ping-pong
+  // below (A/B measured +5% for 16-vector lanes: I-cache and register pressure)
   while (true) {
     const int64_t rowB = rowA + nwarps * RPW;
     const bool anyB = (rowB - grp) < rows;
@@ -367,7 +369,7 @@ __global__ void __launch_bounds__(256) conf_warp_kernel(const ConfArgs a) {
     rA = rB;
   }
   return;
-#endif
+  }
   while (true) {
     const int64_t rowB = rowA + nwarps * RPW;
     const bool anyB = (rowB - grp) < rows;
@@ -403,6 +405,7 @@ struct TmaRing {
 
 template <bool BF16, bool ENTROPY, int NV, int G, int NCW, int S, bool L1>
 __global__ void __launch_bounds__(32 * (NCW + 1), 1) conf_tma_kernel(const ConfArgs a, int dense) {
+  pdl_start();
   extern __shared__ __align__(128) unsigned char smem[];
   constexpr int RPW = 32 / G;
   constexpr int RPS = NCW * RPW;          // rows per stage
@@ -479,98 +482,171 @@ __global__ void __launch_bounds__(32 * (NCW + 1), 1) conf_tma_kernel(const ConfA
 }
 
 // ---------------------------------------------------------------------------
-// K1b: one CTA per row (persistent over rows), per-thread online softmax.
+// K1b: one CTA per row (persistent over rows), per-thread online softmax over
+// chunks of NV vectors per thread, block merge at the end of each row.  The
+// CTA walks its (row, chunk) items in order and always has the next item's
+// loads in flight while reducing the current one; chunks fully inside the row
+// load unconditionally (no per-vector predicate/default moves).
 // ---------------------------------------------------------------------------
+template <bool BF16, int NV, int NT>
+__device__ __forceinline__ void cta_load_chunk(uint4 (&v)[NV], const uint4* p, int base, int tid,
+                                               int nvec, int tail, bool full) {
+  const uint32_t f = BF16 ? kBf16NegInf2 : kF32NegInf;
+  if (full) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) v[k] = ldg_stream(p + base + k * NT + tid);
+  } else {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      const int vi = base + k * NT + tid;
+      uint4 r = make_uint4(f, f, f, f);
+      asm volatile(
+          "{\n\t.reg .pred p;\n\tsetp.lt.s32 p, %4, %5;\n\t"
+          "@p ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%6];\n\t}"
+          : "+r"(r.x), "+r"(r.y), "+r"(r.z), "+r"(r.w)
+          : "r"(vi), "r"(nvec), "l"(p + vi));
+      v[k] = r;
+    }
+    if (tail) {
+#pragma unroll
+      for (int k = 0; k < NV; ++k) {
+        const bool q = (base + k * NT + tid) == nvec - 1;
+        const uint4 m = masked<BF16>(v[k], tail);
+        v[k] = make_uint4(q ? m.x : v[k].x, q ? m.y : v[k].y, q ? m.z : v[k].z, q ? m.w : v[k].w);
+      }
+    }
+  }
+}
+
 template <bool BF16, bool ENTROPY, int NT, int NV>
 __global__ void __launch_bounds__(NT) conf_cta_kernel(const ConfArgs a) {
+  pdl_start();
   constexpr int NW = NT / 32;
   constexpr int VE = BF16 ? 8 : 4;
+  constexpr int CH = NT * NV;                  // vectors per chunk
   __shared__ float sh_m[NW], sh_s[NW], sh_w[NW];
   __shared__ unsigned sh_am[NW];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int64_t rows = live_rows(a);
+  const int nvec = a.nvec;
+  const int nch = (nvec + CH - 1) / CH;
+  if ((int64_t)blockIdx.x >= rows) return;
+  // (row, chunk) items of this CTA in order; the next one is always in flight
+  int64_t rowA = blockIdx.x;
+  int chA = 0;
+  RowSrc rsA = locate(a, rowA), rsB = rsA;
+  const uint4* pA = reinterpret_cast<const uint4*>(rsA.base + rsA.src * a.row_bytes);
+  const uint4* pB = pA;
+  uint4 A[NV], B[NV];
+  cta_load_chunk<BF16, NV, NT>(A, pA, 0, tid, nvec, a.tail, CH <= nvec);
 
-  for (int64_t row = blockIdx.x; row < rows; row += gridDim.x) {
-    const RowSrc rs = locate(a, row);
-    const int64_t src = rs.src;
-    const float c = rs.c;
+  float m = -INFINITY;
+  int mch = -1;                                // chunk where the running max was set
+  f2_t s2 = f2(0.f, 0.f), w2 = f2(0.f, 0.f);
+  while (true) {
+    // ---- next item: same row, next chunk; or the next row of this CTA
+    int64_t rowB = rowA;
+    int chB = chA + 1;
+    if (chB == nch) {
+      chB = 0;
+      rowB = rowA + gridDim.x;
+    }
+    const bool more = rowB < rows;
+    if (more) {
+      if (chB == 0) {
+        rsB = locate(a, rowB);
+        pB = reinterpret_cast<const uint4*>(rsB.base + rsB.src * a.row_bytes);
+      }
+      cta_load_chunk<BF16, NV, NT>(B, pB, chB * CH, tid, nvec, a.tail, (chB + 1) * CH <= nvec);
+    }
+    const float c = rsA.c;
     const f2_t c2 = f2(c, c);
-    const uint4* p = reinterpret_cast<const uint4*>(rs.base + src * a.row_bytes);
-    float m = -INFINITY;
-    f2_t s2 = f2(0.f, 0.f), w2 = f2(0.f, 0.f);
-    unsigned am = 0xFFFFFFFFu;
-    for (int base = 0; base < a.nvec; base += NT * NV) {
-      uint4 v[NV];
+    // ---- chunk max; a new running max rescales (s, w); argmax located at row end
+    float cm = -INFINITY;
 #pragma unroll
-      for (int k = 0; k < NV; ++k) v[k] = load_vec<BF16>(p, base + k * NT + tid, a.nvec, a.tail);
-      float cm = -INFINITY;
+    for (int k = 0; k < NV; ++k) cm = fmax_nan(cm, vec_max<BF16>(A[k]));
+    if (!(cm <= m)) {
+      const float nm = fmax_nan(m, cm);
+      if (m > -INFINITY) {
+        const float d = (m - nm) * c;
+        const float f = ex2(d);
+        const f2_t f2v = f2(f, f);
+        if (ENTROPY) w2 = f2mul(f2v, f2fma(f2(d, d), s2, w2));
+        s2 = f2mul(f2v, s2);
+      }
+      m = nm;
+      mch = chA;
+    }
+    if (m > -INFINITY) {
+      const f2_t m2 = f2(m, m);
+      const uint32_t cw = ENTROPY && BF16 ? entropy_clamp_word(m, c) : 0u;
 #pragma unroll
-      for (int k = 0; k < NV; ++k) cm = fmax_nan(cm, vec_max<BF16>(v[k]));
-      if (!(cm <= m)) {  // new running max (or NaN): rescale, locate its first index
-        const float nm = fmax_nan(m, cm);
-        if (m > -INFINITY) {
-          const float d = (m - nm) * c;
-          const float f = ex2(d);
-          const f2_t f2v = f2(f, f);
-          if (ENTROPY) w2 = f2mul(f2v, f2fma(f2(d, d), s2, w2));
-          s2 = f2mul(f2v, s2);
-        }
-        m = nm;
-        unsigned first = 0xFFFFFFFFu;
+      for (int k = 0; k < NV; ++k) vec_accum<BF16, ENTROPY>(A[k], m2, c2, cw, s2, w2);
+    }
+    if (chA == nch - 1) {
+      // ---- block merge: max, rescale to it, fixed-order sums, min index among maxima
+      float M = m;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) M = fmax_nan(M, __shfl_xor_sync(0xFFFFFFFFu, M, o));
+      if (lane == 0) sh_m[wid] = M;
+      __syncthreads();
+      M = sh_m[0];
+#pragma unroll
+      for (int i = 1; i < NW; ++i) M = fmax_nan(M, sh_m[i]);
+      float sv = 0.f, wv = 0.f;
+      if (m > -INFINITY) {
+        const float d = (m - M) * c;
+        const float f = ex2(d);
+        const float ls = f2lo(s2) + f2hi(s2);
+        sv = f * ls;
+        if (ENTROPY && f > 0.f) wv = f * ((f2lo(w2) + f2hi(w2)) + d * ls);
+      }
+      sv = warp_sum(sv);
+      if (ENTROPY) wv = warp_sum(wv);
+      // argmax: a thread holding M re-reads the chunk where it first saw its
+      // max (rare, L2-hot) and finds the lowest index equal to M
+      unsigned mine = 0xFFFFFFFFu;
+      if (m == M && mch >= 0) {
+        uint4 R[NV];
+        const uint4* pr = reinterpret_cast<const uint4*>(rsA.base + rsA.src * a.row_bytes);
+        cta_load_chunk<BF16, NV, NT>(R, pr, mch * CH, tid, nvec, a.tail, (mch + 1) * CH <= nvec);
 #pragma unroll
         for (int k = NV - 1; k >= 0; --k) {
-          const int e = vec_first_eq<BF16>(v[k], cm);
-          if (e < VE) first = (unsigned)((base + k * NT + tid) * VE + e);
+          const int e = vec_first_eq<BF16>(R[k], M);
+          if (e < VE) mine = (unsigned)((mch * CH + k * NT + tid) * VE + e);
         }
-        am = first;
       }
-      if (m > -INFINITY) {
-        const f2_t m2 = f2(m, m);
-        const uint32_t cw = ENTROPY && BF16 ? entropy_clamp_word(m, c) : 0u;
-#pragma unroll
-        for (int k = 0; k < NV; ++k) vec_accum<BF16, ENTROPY>(v[k], m2, c2, cw, s2, w2);
+      const unsigned wam = __reduce_min_sync(0xFFFFFFFFu, mine);
+      if (lane == 0) {
+        sh_s[wid] = sv;
+        sh_w[wid] = wv;
+        sh_am[wid] = wam;
       }
-    }
-    // ---- block merge: max, rescale to it, fixed-order sums, min index among maxima
-    float M = m;
+      __syncthreads();
+      if (tid == 0) {
+        float S = 0.f, W = 0.f;
+        unsigned AM = 0xFFFFFFFFu;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) M = fmax_nan(M, __shfl_xor_sync(0xFFFFFFFFu, M, o));
-    if (lane == 0) sh_m[wid] = M;
-    __syncthreads();
-    M = sh_m[0];
-#pragma unroll
-    for (int i = 1; i < NW; ++i) M = fmax_nan(M, sh_m[i]);
-    float s = 0.f, w = 0.f;
-    if (m > -INFINITY) {
-      const float d = (m - M) * c;
-      const float f = ex2(d);
-      const float ls = f2lo(s2) + f2hi(s2);
-      s = f * ls;
-      if (ENTROPY && f > 0.f) w = f * ((f2lo(w2) + f2hi(w2)) + d * ls);
-    }
-    s = warp_sum(s);
-    if (ENTROPY) w = warp_sum(w);
-    const unsigned mine = (m == M) ? am : 0xFFFFFFFFu;
-    const unsigned wam = __reduce_min_sync(0xFFFFFFFFu, mine);
-    if (lane == 0) {
-      sh_s[wid] = s;
-      sh_w[wid] = w;
-      sh_am[wid] = wam;
-    }
-    __syncthreads();
-    if (tid == 0) {
-      float S = 0.f, W = 0.f;
-      unsigned A = 0xFFFFFFFFu;
-#pragma unroll
-      for (int i = 0; i < NW; ++i) {
-        S += sh_s[i];
-        W += sh_w[i];
-        A = min(A, sh_am[i]);
+        for (int i = 0; i < NW; ++i) {
+          S += sh_s[i];
+          W += sh_w[i];
+          AM = min(AM, sh_am[i]);
+        }
+        RowOut r{M, S, W, AM, 1.0f};
+        write_row(a, rowA, rsA.src, r);
       }
-      RowOut r{M, S, W, A, 1.0f};
-      write_row(a, row, src, r);
+      __syncthreads();
+      m = -INFINITY;
+      mch = -1;
+      s2 = f2(0.f, 0.f);
+      w2 = f2(0.f, 0.f);
     }
-    __syncthreads();
+    if (!more) break;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) A[k] = B[k];
+    rowA = rowB;
+    chA = chB;
+    rsA = rsB;
   }
 }
 
@@ -580,6 +656,7 @@ __global__ void __launch_bounds__(NT) conf_cta_kernel(const ConfArgs a) {
 __global__ void seq_reduce_kernel(const float* tok_conf, const uint8_t* tok_ok, int64_t n,
                                   const int64_t* d_n, int L, int reduce, float* conf,
                                   uint8_t* correct) {
+  pdl_start();
   int64_t live = n;
   if (d_n) live = min(*d_n, n);
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < live;
@@ -624,9 +701,7 @@ cudaError_t launch_warp_l(const ConfArgs& a, int64_t rows, cudaStream_t s) {
   const int64_t want = (rows + RPB - 1) / RPB;
   const int64_t cap = (int64_t)num_sms() * occ;
   const int grid = (int)(want < cap ? (want > 0 ? want : 1) : cap);
-  k<<<grid, 256, 0, s>>>(a);
-  count_launch();
-  return cudaGetLastError();
+  return launch_pdl(k, dim3(grid), dim3(256), 0, s, a);
 }
 
 template <bool BF16, bool ENTROPY, int NV, int G>
@@ -644,9 +719,7 @@ cudaError_t launch_cta(const ConfArgs& a, int64_t rows, cudaStream_t s) {
   static const int occ = occupancy(k, NT);
   const int64_t cap = (int64_t)num_sms() * occ;
   const int grid = (int)(rows < cap ? (rows > 0 ? rows : 1) : cap);
-  k<<<grid, NT, 0, s>>>(a);
-  count_launch();
-  return cudaGetLastError();
+  return launch_pdl(k, dim3(grid), dim3(NT), 0, s, a);
 }
 
 template <bool BF16, bool ENTROPY, int NV, int G, int NCW, int S, bool L1>
@@ -664,9 +737,7 @@ cudaError_t launch_tma_l(const ConfArgs& a, int64_t rows, cudaStream_t s) {
   const int64_t cap = num_sms();
   const int grid = (int)(tiles < cap ? (tiles > 0 ? tiles : 1) : cap);
   const int dense = (a.row_bytes == (int64_t)a.nvec * 16) ? 1 : 0;
-  k<<<grid, 32 * (NCW + 1), smem, s>>>(a, dense);
-  count_launch();
-  return cudaGetLastError();
+  return launch_pdl(k, dim3(grid), dim3(32 * (NCW + 1)), smem, s, a, dense);
 }
 
 // default TMA ring shape: 8 consumer warps, 3 stages (<= 3 x 64 KB of rows)
@@ -700,14 +771,11 @@ cudaError_t dispatch(const ConfArgs& a, int64_t rows, cudaStream_t s) {
   if (nvec <= 16) return launch_warp<BF16, ENTROPY, 4, 4>(a, rows, s);
   if (nvec <= 32) return launch_warp<BF16, ENTROPY, 8, 4>(a, rows, s);
   if (nvec <= 64) return launch_warp<BF16, ENTROPY, 8, 8>(a, rows, s);
-#ifdef HS_G8
   if (nvec <= 128) return launch_warp<BF16, ENTROPY, 16, 8>(a, rows, s);
-#endif
-  if (nvec <= 128) return launch_warp<BF16, ENTROPY, 8, 16>(a, rows, s);
-  if (nvec <= 256) return launch_warp<BF16, ENTROPY, 8, 32>(a, rows, s);
+  if (nvec <= 256) return launch_warp<BF16, ENTROPY, 16, 16>(a, rows, s);
   if (nvec <= 512) return launch_warp<BF16, ENTROPY, 16, 32>(a, rows, s);
-  if (nvec <= 8192) return launch_cta<BF16, ENTROPY, 256>(a, rows, s);
-  return launch_cta<BF16, ENTROPY, 512>(a, rows, s);
+  // 256-thread CTAs, two per SM: one streams while the other merges a row
+  return launch_cta<BF16, ENTROPY, 256>(a, rows, s);
 }
 
 }  // namespace
@@ -729,9 +797,8 @@ cudaError_t launch_seq_reduce(const float* tok_conf, const uint8_t* tok_ok, int6
                               uint8_t* correct, cudaStream_t s) {
   const int64_t want = (n + 255) / 256;
   const int grid = (int)(want < 4096 ? (want > 0 ? want : 1) : 4096);
-  seq_reduce_kernel<<<grid, 256, 0, s>>>(tok_conf, tok_ok, n, d_n, L, reduce, conf, correct);
-  count_launch();
-  return cudaGetLastError();
+  return launch_pdl(seq_reduce_kernel, dim3(grid), dim3(256), 0, s, tok_conf, tok_ok, n, d_n, L,
+                    reduce, conf, correct);
 }
 
 }  // namespace hs

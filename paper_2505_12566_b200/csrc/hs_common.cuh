@@ -150,6 +150,13 @@ __device__ __forceinline__ uint4 lds128(const void* p) {
   return r;
 }
 
+// ---- programmatic dependent launch: let the next kernel launch now, and wait
+//      until the previous kernel's results are visible (no-ops without PDL)
+__device__ __forceinline__ void pdl_start() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
 template <typename T>
 __device__ __forceinline__ T warp_sum(T v) {
 #pragma unroll

@@ -4,12 +4,36 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <utility>
+
 #include "../../include/hs.h"
 
 namespace hs {
 
 int num_sms();          // SM count of the current device (cached per device)
 void count_launch();    // bumps the process-wide launch counter (hs_launch_count)
+bool pdl_enabled();     // programmatic dependent launch (HS_NO_PDL=1 disables)
+
+// Every libhs kernel is launched with programmatic dependent launch: the next
+// kernel of the stream is scheduled while this one drains, and waits with
+// griddepcontrol.wait (pdl_wait) before touching the previous kernel's output.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                       cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+  count_launch();
+  return e != cudaSuccess ? e : cudaGetLastError();
+}
 
 // ---- K1 / K2 ---------------------------------------------------------------
 constexpr int kMaxBatch = 8;

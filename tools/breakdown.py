@@ -49,13 +49,13 @@ def main():
         names.clear()
         evs.clear()
         mark("start")
-        for k, s in enumerate(router.stages):
-            out = {"conf": router.vconf[k] if k < K - 1 else router.vconf_last,
-                   "argmax": router.vargmax[: router.n_val * s.seq_len], "correct": router.vok[k]}
-            hs.confidence(val[k], n=router.n_val, seq_len=s.seq_len, n_classes=s.n_classes,
-                          temperature=s.temperature, kind=s.kind, reduce=s.reduce, labels=labels,
-                          out=out, ws=router.conf_ws)
-            mark(f"val_conf[{k}]")
+        s0 = router.stages[0]
+        hs.confidence_batched(val, [t.temperature for t in router.stages], n=router.n_val,
+                              seq_len=s0.seq_len, n_classes=s0.n_classes, kind=s0.kind,
+                              reduce=s0.reduce, labels=labels,
+                              out={"conf": router.vconf_all.view(-1), "argmax": router.vargmax,
+                                   "correct": router.vok.view(-1)}, ws=router.conf_ws)
+        mark("val_conf(all stages, one launch)")
         hs.calibrate_thresholds(router.vconf, router.vok, log2_bins=router.q, out=router.cal,
                                 ws=router.cal_ws)
         mark("calibrate")
