@@ -47,6 +47,10 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--placement", default="local", choices=["local", "balanced"],
+                    help="local: every rank serves every stage (no data-path collective); "
+                         "balanced: deferred requests are re-spread over all ranks after "
+                         "every stage with an NCCL all-to-all (dist.forward_deferred)")
     return ap.parse_args()
 
 
@@ -112,13 +116,13 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 # distributed plumbing
 # ---------------------------------------------------------------------------
-def init_dist(args):
+def init_dist(args, force: bool = False):
     import torch
     import torch.distributed as dist
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
+    if world > 1 or force:
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     else:
@@ -324,6 +328,98 @@ def run_ours(args, world, rank, local):
     return line, fam, route, val, labels
 
 
+def run_balanced(args, world, rank, local):
+    """Request-sharded cascade with the BALANCED placement: after
+    every stage the global stable deferred list is re-spread in contiguous blocks
+    over all ranks (count all-gather + one NCCL all-to-all of ids and payload),
+    and each rank routes the block it received.  Calibration sums the per-rank
+    histograms with an NCCL all-reduce.  Host round trip per stage (NCCL split
+    sizes are host values), so the step runs eagerly (no CUDA graph)."""
+    import torch
+    import torch.distributed as dist
+    import workload
+    import paper_2505_12566_b200 as hs
+    from paper_2505_12566_b200 import dist as hsd
+    from workload import synth
+
+    dev = torch.device("cuda", local)
+    fam = family(args.config)
+    K, n, P = fam.K, fam.n, fam.payload_bytes
+    tdt = torch.bfloat16 if fam.dtype == "bf16" else torch.float32
+    # stage 1: this rank's shard (global ids rank*n ..); later stages: any id of
+    # the job can arrive here, so stage k >= 2 logits cover all world*n ids
+    logits = []
+    for k in range(K):
+        rows = n if k == 0 else world * n
+        x = torch.empty(rows * fam.L, fam.C, dtype=tdt, device=dev)
+        workload.gpu_logits(x, fam, k, id_base=rank * n if k == 0 else 0, n=rows)
+        logits.append(x)
+    _, val, labels, payload = build_inputs(synth.scaled(fam, n=1), rank, dev)
+    router = make_router(fam, dev, dist.group.WORLD)
+    cap = world * n                          # worst case: everything lands on one rank
+    ws = hs.workspace(hs.lib().hs_cascade_step_workspace(cap, fam.L), dev)
+    ids0 = torch.arange(rank * n, (rank + 1) * n, dtype=torch.int64, device=dev)
+    pay0 = (torch.randint(0, 255, (n, P), dtype=torch.uint8, device=dev) if P else None)
+    outs = [{"acc_ids": torch.empty(cap, dtype=torch.int64, device=dev),
+             "acc_conf": torch.empty(cap, dtype=torch.float32, device=dev),
+             "acc_pred": torch.empty(cap * fam.L, dtype=torch.int32, device=dev),
+             "next_ids": torch.empty(cap, dtype=torch.int64, device=dev),
+             "counts": torch.zeros(2, dtype=torch.int64, device=dev)} for _ in range(K)]
+    if P:
+        for o in outs:
+            o["next_payload"] = torch.empty(cap * P, dtype=torch.uint8, device=dev)
+
+    def step():
+        cal = router.calibrate(val, labels)
+        ids, pay, nb = ids0, pay0, n
+        for k in range(K):
+            row_index = ids - rank * n if k == 0 else ids
+            o = outs[k]
+            hs.cascade_step(k, K, logits[k], cal["t"][k:k + 1], n=nb, seq_len=fam.L,
+                            n_classes=fam.C, temperature=fam.temps[k], kind=fam.kind,
+                            reduce=fam.reduce, row_index=row_index, ids=ids, payload=pay,
+                            payload_row_bytes=P, out=o, ws=ws)
+            if k == K - 1:
+                break
+            nids, npay, nb = hsd.forward_deferred(
+                o["next_ids"], o["counts"][1:2],
+                payload=o["next_payload"][: cap * P].view(cap, P) if P else None)
+            ids, pay = nids, npay
+
+    stream = torch.cuda.current_stream()
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    l0 = hs.launch_count()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        t0.record(stream)
+        for _ in range(args.steps):
+            step()
+        t1.record(stream)
+        torch.cuda.synchronize()
+    dist.barrier()
+    ms = max_over_ranks(t0.elapsed_time(t1), world) / args.steps
+    launches = hs.launch_count() - l0
+    value = world * n / (ms / 1e3)
+    line = {
+        "metric": METRIC, "value": value, "unit": "requests/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": fam.name, "description": CONFIG_TEXT[args.config],
+                   "requests_per_gpu": n, "validation_per_gpu": fam.n_val, "K": K,
+                   "classes": fam.C, "seq_len": fam.L, "logits_dtype": fam.dtype,
+                   "parallelism": f"request-sharded dp{world}, balanced all-to-all forwarding",
+                   "l2": "inputs larger than L2", "cuda_graph": False},
+        "gpu_launches": launches, "clocks": clk.summary(), "e2e": None,
+        "thresholds": router.cal["t"].cpu().tolist(),
+    }
+    return line, fam
+
+
 def run_e2e(args, fam, router, route, val, labels, payload, stream, world):
     """Same metric through the public API from pinned HOST buffers: every step copies
     its inputs host->device and reads the per-request results back."""
@@ -487,14 +583,23 @@ def main():
         if line is not None:
             print(json.dumps(line), flush=True)
         return
-    world, rank, local = init_dist(args)
-    line, fam, *_ = run_ours(args, world, rank, local)
+    if args.placement == "balanced" and int(os.environ.get("WORLD_SIZE", "1")) == 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29533")
+        os.environ["WORLD_SIZE"] = "1"
+        os.environ["RANK"] = "0"
+        os.environ["LOCAL_RANK"] = "0"
+    world, rank, local = init_dist(args, force=args.placement == "balanced")
+    if args.placement == "balanced":
+        line, fam = run_balanced(args, world, rank, local)
+    else:
+        line, fam, *_ = run_ours(args, world, rank, local)
     if rank == 0:
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(fam, args.cpu_seconds)
         print(json.dumps(line), flush=True)
-    if world > 1:
-        import torch.distributed as dist
+    import torch.distributed as dist
+    if dist.is_initialized():
         dist.barrier()
         dist.destroy_process_group()
 

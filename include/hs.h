@@ -131,9 +131,10 @@ hs_status_t hs_confidence_batched(const void* const* logits, const float* temper
  * d_threshold (optional device float) overrides `threshold` when non-NULL, so
  * thresholds calibrated on the device need no host round trip (its value is
  * not range-checked; a NaN threshold defers everything).
- * Output buffers must hold n entries (worst case).  Workspace:
- * hs_route_compact_workspace(n) bytes, ZERO-FILLED before its first use; every
- * call leaves it zero-filled again (decoupled look-back tile descriptors). */
+ * Output buffers must hold n entries (worst case); n < 2^30.  Workspace:
+ * hs_route_compact_workspace(n) bytes, ZERO-FILLED before its first use and
+ * then reused as is: it holds epoch-tagged decoupled look-back descriptors, so
+ * no call needs a memset (CUDA-graph friendly). */
 size_t hs_route_compact_workspace(int64_t n);
 hs_status_t hs_route_compact(const float* conf, int64_t n, const int64_t* d_n, float threshold,
                              const float* d_threshold, int32_t is_last, const int64_t* ids, const int32_t* pred,
@@ -154,7 +155,7 @@ hs_status_t hs_route_compact(const float* conf, int64_t n, const int64_t* d_n, f
  * next_payload (optional).  d_counts = {#accepted, #deferred}.  d_threshold as
  * for hs_route_compact.
  * Workspace: hs_cascade_step_workspace(n, seq_len) bytes, zero-filled before
- * first use (left zero-filled).  Same errors as the two calls above. */
+ * first use (then reused as is).  n < 2^30.  Same errors as the two calls above. */
 size_t hs_cascade_step_workspace(int64_t n, int32_t seq_len);
 hs_status_t hs_cascade_step(int32_t stage, int32_t n_stages, const void* logits, hs_dtype_t dtype,
                             int64_t n, int32_t seq_len, int64_t n_classes, int64_t row_stride,

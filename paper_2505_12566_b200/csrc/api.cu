@@ -279,7 +279,7 @@ hs_status_t hs_route_compact(const float* conf, int64_t n, const int64_t* d_n, f
                              int32_t* acc_pred, int64_t* def_ids, int64_t* def_pos,
                              const void* payload, int64_t payload_row_bytes, void* def_payload,
                              int64_t* d_counts, void* ws, size_t ws_bytes, hs_stream_t stream) {
-  if (n < 0) return fail(HS_ERR_INVALID_ARGUMENT, "n < 0");
+  if (n < 0 || n >= (int64_t(1) << 30)) return fail(HS_ERR_INVALID_ARGUMENT, "n outside 0..2^30-1");
   if (!is_last && !d_threshold) {
     hs_status_t st = check_threshold(threshold);
     if (st != HS_OK) return st;
@@ -329,6 +329,7 @@ hs_status_t hs_cascade_step(int32_t stage, int32_t n_stages, const void* logits,
                             size_t ws_bytes, uint32_t* d_status, hs_stream_t stream) {
   if (n_stages < 1 || stage < 0 || stage >= n_stages)
     return fail(HS_ERR_INVALID_ARGUMENT, "stage %d outside 0..n_stages-1 (%d)", stage, n_stages);
+  if (n >= (int64_t(1) << 30)) return fail(HS_ERR_INVALID_ARGUMENT, "n must be < 2^30 per call");
   const int is_last = stage == n_stages - 1;
   hs_status_t st = check_logits(logits, dtype, n, seq_len, n_classes, row_stride, temperature, kind, reduce);
   if (st != HS_OK) return st;
@@ -428,14 +429,15 @@ hs_status_t hs_calibrate_thresholds(const float* conf, const uint8_t* correct, i
   if (!conf || !correct) return fail(HS_ERR_INVALID_ARGUMENT, "NULL input");
   if (!d_bin_idx || !d_thresholds || !d_reach || !d_handled || !d_correct_total)
     return fail(HS_ERR_INVALID_ARGUMENT, "NULL output");
-  const char* mode = getenv("HS_CALIB_MODE");   // cluster | fused | split (tests / A-B)
-  const bool small = N < (1 << 20);
-  if ((!mode && small) || (mode && !strcmp(mode, "cluster") && small))
+  // default: all rounds in one cooperative launch; HS_CALIB_MODE=cluster|split
+  // selects the one-cluster (DSMEM) kernel or per-round launches (tests / A-B)
+  const char* mode = getenv("HS_CALIB_MODE");
+  if (mode && !strcmp(mode, "cluster") && N < (1 << 20))
     return cuda_check(hs::launch_calib_cluster(conf, correct, K, N, log2_bins, target_correct,
                                                d_bin_idx, d_thresholds, d_reach, d_handled,
                                                d_correct_total, ws, (cudaStream_t)stream),
                       "calib cluster kernel");
-  if (!mode || !strcmp(mode, "fused") || !strcmp(mode, "cluster"))   // one cooperative launch
+  if (!mode || strcmp(mode, "split"))
     return cuda_check(hs::launch_calib_fused(conf, correct, K, N, log2_bins, target_correct,
                                              d_bin_idx, d_thresholds, d_reach, d_handled,
                                              d_correct_total, ws, (cudaStream_t)stream),

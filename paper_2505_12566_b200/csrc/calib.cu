@@ -48,18 +48,22 @@ __global__ void calib_init_kernel(CalibState* st, int32_t* hist, int nwords, lon
 // Build this CTA's share of round `round` in shared memory: samples r = start,
 // start + stride, ...  Three u32 arrays (count, correct_k, correct_K per bin):
 // native 32-bit shared atomics (a 64-bit shared add would be a CAS loop).
-__device__ __forceinline__ void hist_local(const float* __restrict__ conf,
-                                           const uint8_t* __restrict__ correct, int K, int64_t N,
-                                           int q, int round, const int32_t* b_idx,
-                                           unsigned* sh, int64_t start, int64_t stride) {
+__device__ __forceinline__ void hist_zero(unsigned* sh, int q) {
+  const int words = 3 * ((1 << q) + 2);
+  uint4* sh4 = reinterpret_cast<uint4*>(sh);
+  for (int i = threadIdx.x; i < words / 4; i += blockDim.x) sh4[i] = make_uint4(0, 0, 0, 0);
+  for (int i = (words / 4) * 4 + threadIdx.x; i < words; i += blockDim.x) sh[i] = 0u;
+}
+
+// Accumulate samples r = start, start + stride, ... of round `round` into the
+// shared-memory histogram `sh` -- this CTA's, or (cluster kernel) rank 0's
+// through distributed shared memory.  No zeroing, no trailing barrier.
+__device__ __forceinline__ void hist_accumulate(const float* __restrict__ conf,
+                                                const uint8_t* __restrict__ correct, int K,
+                                                int64_t N, int q, int round, const int32_t* b_idx,
+                                                unsigned* sh, int64_t start, int64_t stride) {
   __shared__ int s_b[16];
   const int nb = (1 << q) + 2;
-  {  // zero the three arrays with 16-byte stores (3*nb is even; tail handled)
-    const int words = 3 * nb;
-    uint4* sh4 = reinterpret_cast<uint4*>(sh);
-    for (int i = threadIdx.x; i < words / 4; i += blockDim.x) sh4[i] = make_uint4(0, 0, 0, 0);
-    for (int i = (words / 4) * 4 + threadIdx.x; i < words; i += blockDim.x) sh[i] = 0u;
-  }
   if (threadIdx.x < 16) s_b[threadIdx.x] = threadIdx.x < round ? b_idx[threadIdx.x] : 0;
   __syncthreads();
 
@@ -92,6 +96,14 @@ __device__ __forceinline__ void hist_local(const float* __restrict__ conf,
       if (nK) atomicAdd(&sh[2 * nb + key], nK);
     }
   }
+}
+
+__device__ __forceinline__ void hist_local(const float* __restrict__ conf,
+                                           const uint8_t* __restrict__ correct, int K, int64_t N,
+                                           int q, int round, const int32_t* b_idx,
+                                           unsigned* sh, int64_t start, int64_t stride) {
+  hist_zero(sh, q);
+  hist_accumulate(conf, correct, K, N, q, round, b_idx, sh, start, stride);
   __syncthreads();
 }
 
@@ -147,131 +159,140 @@ struct SharedHist {
 //   pass 1: segment sums -> block totals (reach_k, G) and the suffix S(hi)
 //   pass 2: smallest feasible b of each segment -> block min = b_k
 //   pass 3: committed (bin >= b_k) and surviving (bin < b_k) sums
-// Three block barriers per round; the reader decides global vs shared memory.
+// Cross-warp steps go through warp 0 (one shuffle scan), so no thread loops
+// over all warps.  Counts fit int32 (N < 2^31); feasibility is tested in int64.
 template <int NT, typename Hist>
 __device__ __forceinline__ void select_core(const Hist& H, int K, int q, int round,
                                             int32_t* b_idx, float* thr, int64_t* reach,
                                             int64_t* handled, int64_t* correct_total,
                                             CalibState* st) {
   constexpr int NW = NT / 32;
-  __shared__ long long sh_a[NW], sh_b[NW], sh_c[NW], sh_d[NW];
-  __shared__ int sh_min[NW];
+  static_assert(NW <= 32, "one warp scans the warp totals");
+  __shared__ int sh_x[NW], sh_y[NW], sh_z[NW], sh_u[NW];
+  __shared__ int sh_tot[2];
+  __shared__ int sh_bk;
+  __shared__ long long sh_tau, sh_A;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int B = 1 << q;
   const int per = (B + 1 + NT - 1) / NT;
   const int lo = min(tid * per, B + 1), hi = min(lo + per, B + 1);
 
   // ---- pass 1
-  long long segH = 0, segCnt = 0, segK = 0;
+  int segH = 0, segCnt = 0, segK = 0;
   for (int b = lo; b < hi; ++b) {
     const Bin3 x = H(b + 1);
-    segH += x.ck - x.cK;
-    segCnt += x.cnt;
-    segK += x.cK;
+    segH += (int)(x.ck - x.cK);
+    segCnt += (int)x.cnt;
+    segK += (int)x.cK;
   }
   if (tid == 0) {                     // NaN bin: alive, never accepted
     const Bin3 x = H(0);
-    segCnt += x.cnt;
-    segK += x.cK;
+    segCnt += (int)x.cnt;
+    segK += (int)x.cK;
   }
-  long long incl = segH;              // inclusive suffix within the warp
+  int incl = segH;                    // inclusive suffix within the warp
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
-    const long long y = __shfl_down_sync(0xFFFFFFFFu, incl, o);
+    const int y = __shfl_down_sync(0xFFFFFFFFu, incl, o);
     if (lane + o < 32) incl += y;
   }
-  long long wc = segCnt, wk = segK;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    wc += __shfl_xor_sync(0xFFFFFFFFu, wc, o);
-    wk += __shfl_xor_sync(0xFFFFFFFFu, wk, o);
-  }
+  const int wc = __reduce_add_sync(0xFFFFFFFFu, segCnt);
+  const int wk = __reduce_add_sync(0xFFFFFFFFu, segK);
   if (lane == 0) {
-    sh_a[wid] = incl;
-    sh_b[wid] = wc;
-    sh_c[wid] = wk;
+    sh_x[wid] = incl;                 // warp total of H
+    sh_y[wid] = wc;
+    sh_z[wid] = wk;
   }
   __syncthreads();
-  long long after = 0, reach_k = 0, G = 0;
-  for (int v = 0; v < NW; ++v) {
-    if (v > wid) after += sh_a[v];
-    reach_k += sh_b[v];
-    G += sh_c[v];
+  if (wid == 0) {
+    const int h = lane < NW ? sh_x[lane] : 0;
+    int suf = h;                      // inclusive suffix over warps
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_down_sync(0xFFFFFFFFu, suf, o);
+      if (lane + o < 32) suf += y;
+    }
+    const int tc = __reduce_add_sync(0xFFFFFFFFu, lane < NW ? sh_y[lane] : 0);
+    const int tk = __reduce_add_sync(0xFFFFFFFFu, lane < NW ? sh_z[lane] : 0);
+    if (lane < NW) sh_u[lane] = suf - h;   // H of all warps after this one
+    if (lane == 0) {
+      sh_tot[0] = tc;
+      sh_tot[1] = tk;
+      if (round == 0 && st->tau_ap) st->tau = tk;   // AP: tau = correct answers of m_K
+      sh_tau = st->tau;
+      sh_A = st->A;
+    }
   }
-  if (round == 0 && st->tau_ap) {     // AP: tau = correct answers of m_K (all alive)
-    __syncthreads();
-    if (tid == 0) st->tau = G;
-    __syncthreads();
-  }
-  const long long tau = st->tau, A = st->A;
+  __syncthreads();
+  const long long reach_k = sh_tot[0], G = sh_tot[1], tau = sh_tau, A = sh_A;
   // ---- pass 2: S(b) for b in [lo, hi) built downward from S(hi)
   int best = B + 1;
   {
-    long long S = after + (incl - segH);
+    long long S = (long long)sh_u[wid] + (incl - segH);
     for (int b = hi - 1; b >= lo; --b) {
       const Bin3 x = H(b + 1);
       S += x.ck - x.cK;
       if (A + G + S >= tau) best = b;
     }
   }
-  best = __reduce_min_sync(0xFFFFFFFFu, (unsigned)best);
-  if (lane == 0) sh_min[wid] = best;
+  best = (int)__reduce_min_sync(0xFFFFFFFFu, (unsigned)best);
+  if (lane == 0) sh_x[wid] = best;
   __syncthreads();
-  int bk = B + 1;   // b = B+1 (defer all) is feasible by induction: A + G >= tau
-  for (int v = 0; v < NW; ++v) bk = min(bk, sh_min[v]);
+  if (wid == 0) {
+    const unsigned v = lane < NW ? (unsigned)sh_x[lane] : (unsigned)(B + 1);
+    const int bk = (int)__reduce_min_sync(0xFFFFFFFFu, v);
+    if (lane == 0) sh_bk = bk;   // b = B+1 (defer all) is feasible by induction
+  }
+  __syncthreads();
+  const int bk = sh_bk;
   // ---- pass 3
-  long long s_ck = 0, s_cnt = 0, s_bc = 0, s_bK = 0;
+  int s_ck = 0, s_cnt = 0, s_bc = 0, s_bK = 0;
   for (int b = lo; b < hi; ++b) {
     const Bin3 x = H(b + 1);
     if (b >= bk) {
-      s_ck += x.ck;
-      s_cnt += x.cnt;
+      s_ck += (int)x.ck;
+      s_cnt += (int)x.cnt;
     } else {
-      s_bc += x.cnt;
-      s_bK += x.cK;
+      s_bc += (int)x.cnt;
+      s_bK += (int)x.cK;
     }
   }
   if (tid == 0) {
     const Bin3 x = H(0);
-    s_bc += x.cnt;
-    s_bK += x.cK;
+    s_bc += (int)x.cnt;
+    s_bK += (int)x.cK;
   }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    s_ck += __shfl_xor_sync(0xFFFFFFFFu, s_ck, o);
-    s_cnt += __shfl_xor_sync(0xFFFFFFFFu, s_cnt, o);
-    s_bc += __shfl_xor_sync(0xFFFFFFFFu, s_bc, o);
-    s_bK += __shfl_xor_sync(0xFFFFFFFFu, s_bK, o);
-  }
-  __syncthreads();                    // sh_a..sh_c reads of pass 1 are done
+  s_ck = __reduce_add_sync(0xFFFFFFFFu, s_ck);
+  s_cnt = __reduce_add_sync(0xFFFFFFFFu, s_cnt);
+  s_bc = __reduce_add_sync(0xFFFFFFFFu, s_bc);
+  s_bK = __reduce_add_sync(0xFFFFFFFFu, s_bK);
   if (lane == 0) {
-    sh_a[wid] = s_ck;
-    sh_b[wid] = s_cnt;
-    sh_c[wid] = s_bc;
-    sh_d[wid] = s_bK;
+    sh_x[wid] = s_ck;
+    sh_y[wid] = s_cnt;
+    sh_z[wid] = s_bc;
+    sh_u[wid] = s_bK;
   }
   __syncthreads();
-  if (tid == 0) {
-    long long ck = 0, cnt = 0, bc = 0, bK = 0;
-    for (int v = 0; v < NW; ++v) {
-      ck += sh_a[v];
-      cnt += sh_b[v];
-      bc += sh_c[v];
-      bK += sh_d[v];
+  if (wid == 0) {
+    const int ck = __reduce_add_sync(0xFFFFFFFFu, lane < NW ? sh_x[lane] : 0);
+    const int cnt = __reduce_add_sync(0xFFFFFFFFu, lane < NW ? sh_y[lane] : 0);
+    const int bc = __reduce_add_sync(0xFFFFFFFFu, lane < NW ? sh_z[lane] : 0);
+    const int bK = __reduce_add_sync(0xFFFFFFFFu, lane < NW ? sh_u[lane] : 0);
+    if (lane == 0) {
+      long long Anew = A + ck;
+      b_idx[round] = bk;
+      thr[round] = bk <= B ? (float)bk / (float)B : INFINITY;
+      reach[round] = reach_k;
+      handled[round] = cnt;
+      if (round == K - 2) {
+        reach[K - 1] = bc;
+        handled[K - 1] = bc;
+        Anew += bK;
+        thr[K - 1] = 0.f;
+        *correct_total = Anew;
+      }
+      st->A = Anew;
     }
-    long long Anew = A + ck;
-    b_idx[round] = bk;
-    thr[round] = bk <= B ? (float)bk / (float)B : INFINITY;
-    reach[round] = reach_k;
-    handled[round] = cnt;
-    if (round == K - 2) {
-      reach[K - 1] = bc;
-      handled[K - 1] = bc;
-      Anew += bK;
-      thr[K - 1] = 0.f;
-      *correct_total = Anew;
-    }
-    st->A = Anew;
   }
   __syncthreads();
 }
@@ -287,13 +308,13 @@ __device__ __forceinline__ void select_body(int K, int q, int round, int32_t* b_
   __syncthreads();
 }
 
-__global__ void __launch_bounds__(1024) calib_select_kernel(int K, int q, int round,
+__global__ void __launch_bounds__(256) calib_select_kernel(int K, int q, int round,
                                                             int32_t* b_idx, float* thr,
                                                             int64_t* reach, int64_t* handled,
                                                             int64_t* correct_total,
                                                             CalibState* st, int32_t* hist) {
   pdl_start();
-  select_body<1024>(K, q, round, b_idx, thr, reach, handled, correct_total, st, hist);
+  select_body<256>(K, q, round, b_idx, thr, reach, handled, correct_total, st, hist);
 }
 
 // All K-1 rounds in one cooperative launch (single GPU): histogram by every
@@ -358,8 +379,7 @@ __global__ void __launch_bounds__(1024, 1) calib_cluster_kernel(const float* __r
     hist_local(conf, correct, K, N, q, k, b_idx, sh,
                (int64_t)rank * blockDim.x + threadIdx.x, (int64_t)ncta * blockDim.x);
     cluster.sync();
-    // ranks 1.. push their non-empty bins into rank 0's histogram (DSMEM
-    // atomics, no round trip)
+    // ranks 1.. push their non-empty bins into rank 0's histogram (DSMEM atomics)
     if (rank != 0) {
       unsigned* dst = cluster.map_shared_rank(sh, 0);
       for (int i = threadIdx.x; i < 3 * nb; i += blockDim.x) {
@@ -422,7 +442,9 @@ cudaError_t launch_calib_fused(const float* conf, const uint8_t* correct, int K,
                                                   3 * ((1 << 14) + 2) * sizeof(unsigned));
     max_blocks = per_sm > 0 ? per_sm * num_sms() : 0;
   }
-  int grid = (int)((N + 1023) / 1024);
+  // ~4K samples per CTA: enough parallelism for the histogram pass while
+  // keeping the flush (global atomics on the hot bins near c = 1) small
+  int grid = (int)((N + 4095) / 4096);
   if (grid > num_sms()) grid = num_sms();
   if (grid > max_blocks) grid = max_blocks;
   if (grid < 1) grid = 1;
@@ -475,7 +497,7 @@ cudaError_t launch_calib_cluster(const float* conf, const uint8_t* correct, int 
 cudaError_t launch_calib_select(int K, int q, int round, int32_t* b_idx, float* thr,
                                 int64_t* reach, int64_t* handled, int64_t* correct_total,
                                 void* ws, cudaStream_t s) {
-  return launch_pdl(calib_select_kernel, dim3(1), dim3(1024), 0, s, K, q, round, b_idx, thr, reach,
+  return launch_pdl(calib_select_kernel, dim3(1), dim3(256), 0, s, K, q, round, b_idx, thr, reach,
                     handled, correct_total, reinterpret_cast<CalibState*>(ws), hist_of(ws));
 }
 

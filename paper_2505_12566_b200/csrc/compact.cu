@@ -4,12 +4,14 @@
 // larger model iff its confidence is below the stage threshold (ties accept;
 // the last model answers everything).  The deferred items must form the next
 // stage's batch in their original order, so the split is a stable partition:
-// a single-pass scan with decoupled look-back (Merrill & Garland).  Each
-// 4,096-item tile takes a ticket (so tiles wait only on tiles already running),
-// ranks its items with warp ballots, publishes its deferred count, and walks
-// back over predecessor descriptors (64-bit {flag, count}, release/acquire at
-// gpu scope) for its exclusive prefix.  The last CTA to finish re-zeroes the
-// descriptors, so the workspace needs no memset between calls (graph-friendly).
+// a single-pass scan with decoupled look-back (Merrill & Garland).  CTA b owns
+// the 4,096-item tile b (blocks are dispatched in index order, as in CUB's
+// single-pass scan), ranks its items with warp ballots, publishes its deferred
+// count, and walks back over predecessor descriptors for its exclusive prefix.
+// Descriptors are 64-bit {epoch:32 | flag:2 | count:30}, written with
+// st.release and read with ld.acquire at gpu scope; the epoch (bumped by the
+// last tile of every launch) makes stale descriptors from earlier launches
+// read as "not ready", so there is no reset pass and no memset between calls.
 #include "hs_common.cuh"
 #include "hs_internal.h"
 
@@ -17,22 +19,23 @@ namespace hs {
 
 namespace {
 
-constexpr unsigned long long kFlagA = 1ull << 62;   // aggregate available
-constexpr unsigned long long kFlagP = 2ull << 62;   // inclusive prefix available
-constexpr unsigned long long kValMask = (1ull << 62) - 1;
+constexpr unsigned long long kFlagA = 1ull << 30;   // aggregate available
+constexpr unsigned long long kFlagP = 2ull << 30;   // inclusive prefix available
+constexpr unsigned long long kValMask = (1ull << 30) - 1;
 
 __device__ __forceinline__ unsigned long long* tile_status(void* ws) {
   return reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(ws) + sizeof(CompactWs));
+}
+__device__ __forceinline__ unsigned desc_flag(unsigned long long d, unsigned epoch) {
+  return (unsigned)(d >> 32) == epoch ? (unsigned)((d >> 30) & 3u) : 0u;   // 0 = not ready
 }
 
 __global__ void __launch_bounds__(kCompactThreads) route_compact_kernel(const CompactArgs a) {
   pdl_start();
   constexpr int T = kCompactThreads, I = kCompactItems, NW = T / 32;
-  __shared__ unsigned s_tile;
   __shared__ int s_cnt[I * NW];     // deferred count per (item row j, warp), j-major
   __shared__ int s_off[I * NW];     // exclusive offsets within the tile
   __shared__ long long s_excl;
-  __shared__ int s_last;
 
   CompactWs* ws = reinterpret_cast<CompactWs*>(a.ws);
   unsigned long long* st = tile_status(a.ws);
@@ -41,15 +44,19 @@ __global__ void __launch_bounds__(kCompactThreads) route_compact_kernel(const Co
   int64_t n = a.n;
   if (a.d_n) n = min(*a.d_n, a.n);
   const int64_t ntiles = (n + kCompactTile - 1) / kCompactTile;
-
-  if (tid == 0) {
-    s_tile = atomicAdd(&ws->ticket, 1u);
-    s_last = 0;
+  const int64_t tile = blockIdx.x;
+  if (ntiles == 0) {
+    if (tile == 0 && tid == 0) {
+      a.counts[0] = 0;
+      a.counts[1] = 0;
+    }
+    return;
   }
-  __syncthreads();
-  const int64_t tile = s_tile;
+  if (tile >= ntiles) return;
+  const unsigned epoch = *(volatile unsigned*)&ws->epoch;
+  const unsigned long long etag = (unsigned long long)epoch << 32;
 
-  if (tile < ntiles) {
+  {
     const int64_t base = tile * kCompactTile;
     const float thr = a.d_threshold ? *a.d_threshold : a.threshold;
     // ---- all loads of the tile first (independent, coalesced: item j of thread
@@ -105,17 +112,17 @@ __global__ void __launch_bounds__(kCompactThreads) route_compact_kernel(const Co
       // ---- decoupled look-back for the deferred count before this tile
       long long excl = 0;
       if (tile == 0) {
-        if (lane == 0) st_release(&st[0], kFlagP | (unsigned long long)agg);
+        if (lane == 0) st_release(&st[0], etag | kFlagP | (unsigned long long)agg);
       } else {
-        if (lane == 0) st_release(&st[tile], kFlagA | (unsigned long long)agg);
+        if (lane == 0) st_release(&st[tile], etag | kFlagA | (unsigned long long)agg);
         int64_t pred = tile - 1;
         while (true) {
           const int64_t idx = pred - lane;
-          unsigned long long d = (idx >= 0) ? ld_acquire(&st[idx]) : kFlagP;
-          while (__any_sync(0xFFFFFFFFu, (d >> 62) == 0)) {
-            if ((d >> 62) == 0) d = ld_acquire(&st[idx]);
+          unsigned long long d = (idx >= 0) ? ld_acquire(&st[idx]) : (etag | kFlagP);
+          while (__any_sync(0xFFFFFFFFu, desc_flag(d, epoch) == 0)) {
+            if (desc_flag(d, epoch) == 0) d = ld_acquire(&st[idx]);
           }
-          const unsigned pm = __ballot_sync(0xFFFFFFFFu, (d >> 62) == 2);
+          const unsigned pm = __ballot_sync(0xFFFFFFFFu, desc_flag(d, epoch) == 2);
           long long val = (long long)(d & kValMask);
           if (pm) {
             const int first = __ffs(pm) - 1;
@@ -125,7 +132,13 @@ __global__ void __launch_bounds__(kCompactThreads) route_compact_kernel(const Co
           excl += warp_sum(val);
           pred -= 32;
         }
-        if (lane == 0) st_release(&st[tile], kFlagP | (unsigned long long)(excl + agg));
+        if (lane == 0) st_release(&st[tile], etag | kFlagP | (unsigned long long)(excl + agg));
+      }
+      if (lane == 0 && tile == ntiles - 1) {
+        // the last tile knows the totals; it also retires this launch's epoch
+        a.counts[0] = n - (excl + agg);
+        a.counts[1] = excl + agg;
+        ws->epoch = epoch + 1u;
       }
       if (lane == 0) s_excl = excl;
     }
@@ -157,28 +170,6 @@ __global__ void __launch_bounds__(kCompactThreads) route_compact_kernel(const Co
     }
   }
 
-  // ---- completion: the last CTA publishes the counts and re-zeroes the workspace
-  __syncthreads();
-  if (tid == 0) {
-    __threadfence();
-    const unsigned d = atomicAdd(&ws->done, 1u);
-    if (d == gridDim.x - 1) {
-      __threadfence();
-      long long tot_def = 0;
-      if (ntiles > 0) tot_def = (long long)(ld_acquire(&st[ntiles - 1]) & kValMask);
-      a.counts[0] = n - tot_def;
-      a.counts[1] = tot_def;
-      s_last = 1;
-    }
-  }
-  __syncthreads();
-  if (s_last) {
-    for (int64_t t = tid; t < ntiles; t += T) st[t] = 0ull;
-    if (tid == 0) {
-      ws->ticket = 0u;
-      ws->done = 0u;
-    }
-  }
 }
 
 // K4: dst[j] = src[pos[j]] for j < *d_count, rows of row_bytes (multiple of 16)

@@ -72,9 +72,9 @@ constexpr int kCompactThreads = 256;
 constexpr int kCompactItems = 16;
 constexpr int kCompactTile = kCompactThreads * kCompactItems;   // 4096 items per tile
 
-struct CompactWs {          // zero-filled between calls (the last CTA resets it)
-  unsigned int ticket;
-  unsigned int done;
+struct CompactWs {          // zero-filled before first use; then self-maintaining
+  unsigned int epoch;       // launch counter tagging the tile descriptors
+  unsigned int pad0;
   unsigned long long pad[3];
   // unsigned long long status[n_tiles] follows (32-byte header)
 };
