@@ -342,7 +342,24 @@ __global__ void __launch_bounds__(1024) calib_fused_kernel(const float* __restri
   for (int k = 0; k < K - 1; ++k) {
     hist_body(conf, correct, K, N, q, k, b_idx, hist, sh);
     grid.sync();
-    if (blockIdx.x == 0) select_body<1024>(K, q, k, b_idx, thr, reach, handled, correct_total, st, hist);
+    if (blockIdx.x == 0) {
+      // pull the summed histogram into shared memory once (and re-zero it for
+      // the next round), then select from shared memory
+      const int words = 3 * ((1 << q) + 2);
+      uint4* g4 = reinterpret_cast<uint4*>(hist);
+      uint4* s4 = reinterpret_cast<uint4*>(sh);
+      for (int i = threadIdx.x; i < words / 4; i += blockDim.x) {
+        s4[i] = g4[i];
+        g4[i] = make_uint4(0, 0, 0, 0);
+      }
+      for (int i = (words / 4) * 4 + threadIdx.x; i < words; i += blockDim.x) {
+        sh[i] = (unsigned)hist[i];
+        hist[i] = 0;
+      }
+      __syncthreads();
+      select_core<1024>(SharedHist{sh, (1 << q) + 2}, K, q, k, b_idx, thr, reach, handled,
+                        correct_total, st);
+    }
     grid.sync();
   }
 }

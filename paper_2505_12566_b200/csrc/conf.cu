@@ -88,17 +88,35 @@ struct RowSrc {
   float c;
   int64_t src;
 };
-__device__ __forceinline__ RowSrc locate(const ConfArgs& a, int64_t row) {
-  RowSrc r{(const char*)a.logits, a.c, row};
+__device__ __forceinline__ int64_t batch_local(const ConfArgs& a, int64_t row, int* b) {
+  *b = 0;
   if (a.nbatch > 1) {
-    const int b = (int)((uint32_t)row / (uint32_t)a.brows);   // rows < 2^32
+    *b = (int)((uint32_t)row / (uint32_t)a.brows);   // rows < 2^32
+    return row - (int64_t)(*b) * a.brows;
+  }
+  return row;
+}
+// The gathered-row lookup (row_index) of `row`, issued ahead of its use so the
+// dependent logits loads of a later iteration do not wait on it.
+__device__ __forceinline__ int64_t fetch_index(const ConfArgs& a, int64_t row) {
+  if (!a.row_index) return 0;
+  int b;
+  const int64_t local = batch_local(a, row, &b);
+  return a.L == 1 ? a.row_index[local] : a.row_index[local / a.L];
+}
+__device__ __forceinline__ RowSrc locate_with(const ConfArgs& a, int64_t row, int64_t fetched) {
+  int b;
+  const int64_t local = batch_local(a, row, &b);
+  RowSrc r{(const char*)a.logits, a.c, local};
+  if (a.nbatch > 1) {
     r.base = (const char*)a.bptr[b];
     r.c = a.bc[b];
-    r.src = row - (int64_t)b * a.brows;
   }
-  if (a.row_index)
-    r.src = a.L == 1 ? a.row_index[r.src] : a.row_index[r.src / a.L] * a.L + r.src % a.L;
+  if (a.row_index) r.src = a.L == 1 ? fetched : fetched * a.L + local % a.L;
   return r;
+}
+__device__ __forceinline__ RowSrc locate(const ConfArgs& a, int64_t row) {
+  return locate_with(a, row, fetch_index(a, row));
 }
 
 // -inf for the out-of-row elements of the last partial 16-byte vector
@@ -336,29 +354,33 @@ __global__ void __launch_bounds__(256) conf_warp_kernel(const ConfArgs a) {
   pdl_start();
   constexpr int RPW = 32 / G;      // rows per warp
   const int lane = threadIdx.x & 31, gl = lane % G, grp = lane / G;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t stride = (((int64_t)gridDim.x * blockDim.x) >> 5) * RPW;
   const int64_t rows = live_rows(a);
   const int nvec = a.nvec;
-  auto load = [&](uint4 (&v)[NV], int64_t row, bool act) -> RowSrc {
-    RowSrc r = locate(a, act ? row : 0);   // inactive groups read a valid row
-    group_load_row<BF16, NV, G, FULL>(v, reinterpret_cast<const uint4*>(r.base + r.src * a.row_bytes),
-                                      gl, nvec);
-    return r;
-  };
   const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (w0 * RPW >= rows) return;
+  // Three-deep pipeline per group: row indices two rows ahead, logits one row
+  // ahead (registers B), the current row (registers A) being reduced.  One
+  // reduce site, B copied into A each pass (A/B: +1.5-5 % over two sites).
   uint4 A[NV], B[NV];
   int64_t rowA = w0 * RPW + grp;
   bool actA = rowA < rows;
-  RowSrc rA = load(A, rowA, actA), rB = rA;
-  if (NV >= 16) {
-  // one reduce site, B copied into A each pass: half the code of the ping-pong
-  // below (A/B measured +5% for 16-vector lanes: I-cache and register pressure)
+  RowSrc rA = locate(a, actA ? rowA : 0), rB = rA;   // inactive groups read a valid row
+  group_load_row<BF16, NV, G, FULL>(A, reinterpret_cast<const uint4*>(rA.base + rA.src * a.row_bytes),
+                                    gl, nvec);
+  int64_t rowB = rowA + stride;
+  int64_t fB = fetch_index(a, rowB < rows ? rowB : 0);
   while (true) {
-    const int64_t rowB = rowA + nwarps * RPW;
     const bool anyB = (rowB - grp) < rows;
     const bool actB = rowB < rows;
-    if (anyB) rB = load(B, rowB, actB);
+    const int64_t rowC = rowB + stride;
+    int64_t fC = 0;
+    if (anyB) {
+      rB = locate_with(a, actB ? rowB : 0, actB ? fB : fetch_index(a, 0));
+      group_load_row<BF16, NV, G, FULL>(B, reinterpret_cast<const uint4*>(rB.base + rB.src * a.row_bytes),
+                                        gl, nvec);
+      fC = fetch_index(a, rowC < rows ? rowC : 0);
+    }
     if (a.tail) group_mask_tail<BF16, NV, G>(A, gl, nvec, a.tail);
     group_reduce_row<BF16, ENTROPY, NV, G>(a, A, actA, rowA, rA.src, gl, rA.c);
     if (!anyB) break;
@@ -367,24 +389,8 @@ __global__ void __launch_bounds__(256) conf_warp_kernel(const ConfArgs a) {
     rowA = rowB;
     actA = actB;
     rA = rB;
-  }
-  return;
-  }
-  while (true) {
-    const int64_t rowB = rowA + nwarps * RPW;
-    const bool anyB = (rowB - grp) < rows;
-    const bool actB = rowB < rows;
-    if (anyB) rB = load(B, rowB, actB);
-    if (a.tail) group_mask_tail<BF16, NV, G>(A, gl, nvec, a.tail);
-    group_reduce_row<BF16, ENTROPY, NV, G>(a, A, actA, rowA, rA.src, gl, rA.c);
-    if (!anyB) break;
-    rowA = rowB + nwarps * RPW;
-    const bool anyA = (rowA - grp) < rows;
-    actA = rowA < rows;
-    if (anyA) rA = load(A, rowA, actA);
-    if (a.tail) group_mask_tail<BF16, NV, G>(B, gl, nvec, a.tail);
-    group_reduce_row<BF16, ENTROPY, NV, G>(a, B, actB, rowB, rB.src, gl, rB.c);
-    if (!anyA) break;
+    rowB = rowC;
+    fB = fC;
   }
 }
 
