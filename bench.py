@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--force-dist", action="store_true",
+                    help="initialise NCCL even at one GPU (exercises the sharded calibration path)")
     ap.add_argument("--placement", default="local", choices=["local", "balanced"],
                     help="local: every rank serves every stage (no data-path collective); "
                          "balanced: deferred requests are re-spread over all ranks after "
@@ -222,7 +224,7 @@ def run_ours(args, world, rank, local):
 
     dev = torch.device("cuda", local)
     fam = family(args.config)
-    group = dist.group.WORLD if world > 1 else None
+    group = dist.group.WORLD if dist.is_initialized() else None
     route, val, labels, payload = build_inputs(fam, rank, dev)
     router = make_router(fam, dev, group)
     ev = (timing_event(), timing_event())
@@ -583,13 +585,13 @@ def main():
         if line is not None:
             print(json.dumps(line), flush=True)
         return
-    if args.placement == "balanced" and int(os.environ.get("WORLD_SIZE", "1")) == 1:
+    if (args.placement == "balanced" or args.force_dist) and int(os.environ.get("WORLD_SIZE", "1")) == 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         os.environ.setdefault("MASTER_PORT", "29533")
         os.environ["WORLD_SIZE"] = "1"
         os.environ["RANK"] = "0"
         os.environ["LOCAL_RANK"] = "0"
-    world, rank, local = init_dist(args, force=args.placement == "balanced")
+    world, rank, local = init_dist(args, force=args.placement == "balanced" or args.force_dist)
     if args.placement == "balanced":
         line, fam = run_balanced(args, world, rank, local)
     else:

@@ -179,8 +179,12 @@ hs_status_t hs_cascade_step(int32_t stage, int32_t n_stages, const void* logits,
  * Inputs: conf [(K-1) x N] fp32 (stage k's confidence of sample r at k*N + r),
  * correct [K x N] u8 (0/1).  Outputs (device): d_bin_idx[K-1], d_thresholds[K],
  * d_reach[K], d_handled[K], d_correct_total[1] (int64 counts).
- * log2_bins in [1, 14]; K >= 2; N >= 1; refine_passes must be 0 (the optional
- * refinement of DESIGN.md is not implemented on the GPU: HS_ERR_UNSUPPORTED).
+ * log2_bins in [1, 14]; 2 <= K <= 17; N >= 1.  refine_passes (0..64) optional
+ * passes after the greedy sweep, each re-picking b_k = min{b : A_k +
+ * sum_{alive_k, bin>=b} correct_k + sum_{alive_k, bin<b} C_{k+1} >= tau} for
+ * k = 0..K-2 in order, with alive_k / A_k (answers given before k) / C_{k+1}
+ * (downstream cascade correctness) under the current thresholds; never raises
+ * any b_k; reach / handled / correct_total are then recomputed by a replay.
  * Workspace: hs_calibrate_workspace(K, log2_bins) bytes (no zero-fill needed).
  * Entirely stream-ordered (capturable in a CUDA graph). */
 size_t hs_calibrate_workspace(int32_t K, int32_t log2_bins);

@@ -416,19 +416,12 @@ hs_status_t hs_calibrate_select(int32_t K, int32_t log2_bins, int32_t round, int
                     "calib select");
 }
 
-hs_status_t hs_calibrate_thresholds(const float* conf, const uint8_t* correct, int32_t K, int64_t N,
-                                    int32_t log2_bins, int64_t target_correct,
-                                    int32_t refine_passes, int32_t* d_bin_idx,
+static hs_status_t calibrate_greedy(const float* conf, const uint8_t* correct, int32_t K, int64_t N,
+                                    int32_t log2_bins, int64_t target_correct, int32_t* d_bin_idx,
                                     float* d_thresholds, int64_t* d_reach, int64_t* d_handled,
                                     int64_t* d_correct_total, void* ws, size_t ws_bytes,
                                     hs_stream_t stream) {
-  hs_status_t st = check_calib(K, log2_bins, ws, ws_bytes);
-  if (st != HS_OK) return st;
-  if (N <= 0) return fail(HS_ERR_INVALID_ARGUMENT, "empty validation set (N = %lld)", (long long)N);
-  if (refine_passes != 0) return fail(HS_ERR_UNSUPPORTED, "refine_passes > 0 is not implemented on the GPU");
-  if (!conf || !correct) return fail(HS_ERR_INVALID_ARGUMENT, "NULL input");
-  if (!d_bin_idx || !d_thresholds || !d_reach || !d_handled || !d_correct_total)
-    return fail(HS_ERR_INVALID_ARGUMENT, "NULL output");
+  hs_status_t st = HS_OK;
   // default: all rounds in one cooperative launch; HS_CALIB_MODE=cluster|split
   // selects the one-cluster (DSMEM) kernel or per-round launches (tests / A-B)
   const char* mode = getenv("HS_CALIB_MODE");
@@ -450,6 +443,29 @@ hs_status_t hs_calibrate_thresholds(const float* conf, const uint8_t* correct, i
                                d_correct_total, ws, ws_bytes, stream);
   }
   return st;
+}
+
+hs_status_t hs_calibrate_thresholds(const float* conf, const uint8_t* correct, int32_t K, int64_t N,
+                                    int32_t log2_bins, int64_t target_correct,
+                                    int32_t refine_passes, int32_t* d_bin_idx,
+                                    float* d_thresholds, int64_t* d_reach, int64_t* d_handled,
+                                    int64_t* d_correct_total, void* ws, size_t ws_bytes,
+                                    hs_stream_t stream) {
+  hs_status_t st = check_calib(K, log2_bins, ws, ws_bytes);
+  if (st != HS_OK) return st;
+  if (N <= 0) return fail(HS_ERR_INVALID_ARGUMENT, "empty validation set (N = %lld)", (long long)N);
+  if (refine_passes < 0 || refine_passes > 64)
+    return fail(HS_ERR_INVALID_ARGUMENT, "refine_passes = %d outside 0..64", refine_passes);
+  if (!conf || !correct) return fail(HS_ERR_INVALID_ARGUMENT, "NULL input");
+  if (!d_bin_idx || !d_thresholds || !d_reach || !d_handled || !d_correct_total)
+    return fail(HS_ERR_INVALID_ARGUMENT, "NULL output");
+  st = calibrate_greedy(conf, correct, K, N, log2_bins, target_correct, d_bin_idx, d_thresholds,
+                        d_reach, d_handled, d_correct_total, ws, ws_bytes, stream);
+  if (st != HS_OK || refine_passes == 0) return st;
+  return cuda_check(hs::launch_calib_refine(conf, correct, K, N, log2_bins, refine_passes, d_bin_idx,
+                                            d_thresholds, d_reach, d_handled, d_correct_total, ws,
+                                            (cudaStream_t)stream),
+                    "calib refinement");
 }
 
 }  // extern "C"

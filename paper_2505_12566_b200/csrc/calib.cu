@@ -16,6 +16,7 @@
 // Histograms are integers, so a request-sharded calibration sums them across
 // GPUs (all-reduce) and every rank selects the same b_k.
 #include <cooperative_groups.h>
+#include <cstdio>
 
 #include "hs_common.cuh"
 #include "hs_internal.h"
@@ -329,6 +330,18 @@ __global__ void __launch_bounds__(1024) calib_fused_kernel(const float* __restri
   pdl_start();
   extern __shared__ unsigned sh[];
   cg::grid_group grid = cg::this_grid();
+#ifdef HS_CALIB_TRACE
+  unsigned long long t0, tt;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+#define HS_TR(tag)                                                             \
+  if (blockIdx.x == 0 && threadIdx.x == 0) {                                   \
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt));                     \
+    printf("calib trace k=%d %s %llu ns\n", k, tag, tt - t0);                   \
+  }
+#else
+#define HS_TR(tag)
+#endif
+  int k = -1;
   if (blockIdx.x == 0) {
     const int nw = 3 * ((1 << q) + 2);
     for (int i = threadIdx.x; i < nw; i += blockDim.x) hist[i] = 0;
@@ -339,9 +352,12 @@ __global__ void __launch_bounds__(1024) calib_fused_kernel(const float* __restri
     }
   }
   grid.sync();
-  for (int k = 0; k < K - 1; ++k) {
+  HS_TR("init");
+  for (k = 0; k < K - 1; ++k) {
     hist_body(conf, correct, K, N, q, k, b_idx, hist, sh);
+    HS_TR("hist");
     grid.sync();
+    HS_TR("sync1");
     if (blockIdx.x == 0) {
       // pull the summed histogram into shared memory once (and re-zero it for
       // the next round), then select from shared memory
@@ -357,10 +373,13 @@ __global__ void __launch_bounds__(1024) calib_fused_kernel(const float* __restri
         hist[i] = 0;
       }
       __syncthreads();
+      HS_TR("pulled");
       select_core<1024>(SharedHist{sh, (1 << q) + 2}, K, q, k, b_idx, thr, reach, handled,
                         correct_total, st);
+      HS_TR("select");
     }
     grid.sync();
+    HS_TR("sync2");
   }
 }
 
@@ -409,6 +428,119 @@ __global__ void __launch_bounds__(1024, 1) calib_cluster_kernel(const float* __r
       select_core<1024>(SharedHist{sh, nb}, K, q, k, b_idx, thr, reach, handled, correct_total, st);
     cluster.sync();
   }
+}
+
+// ---------------------------------------------------------------------------
+// Optional refinement passes: re-pick each b_k given the
+// current downstream thresholds.  Round k of a pass histograms the samples that
+// still reach model k under the current thresholds, with the third channel
+// holding the correctness of the DOWNSTREAM cascade (k+1 .. K-1 under the
+// current b) instead of correct_K, and accumulates A_k = correct answers given
+// before k.  The ordinary select then yields
+//   b_k = min{ b : A_k + sum_{bin>=b} correct_k + sum_{bin<b} C_down >= tau }.
+// ---------------------------------------------------------------------------
+__global__ void calib_refine_begin_kernel(CalibState* st) {
+  pdl_start();
+  if (threadIdx.x == 0) {
+    st->A = 0;
+    st->tau_ap = 0;   // tau is fixed by the greedy pass
+  }
+}
+
+__global__ void __launch_bounds__(512) calib_refine_hist_kernel(const float* __restrict__ conf,
+                                                                const uint8_t* __restrict__ correct,
+                                                                int K, int64_t N, int q, int k,
+                                                                const int32_t* __restrict__ b_idx,
+                                                                int32_t* __restrict__ hist,
+                                                                CalibState* st) {
+  pdl_start();
+  extern __shared__ unsigned sh[];
+  __shared__ int s_b[16];
+  __shared__ unsigned long long s_A;
+  const int nb = (1 << q) + 2;
+  hist_zero(sh, q);
+  if (threadIdx.x < 16) s_b[threadIdx.x] = threadIdx.x < K - 1 ? b_idx[threadIdx.x] : 0;
+  if (threadIdx.x == 0) s_A = 0ull;
+  __syncthreads();
+  unsigned long long myA = 0;
+  const int64_t Nup = (N + 31) & ~(int64_t)31;
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < Nup;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    const bool in = r < N;
+    int key = -1;
+    bool okk = false, okD = false;
+    if (in) {
+      int j = 0;
+      while (j < k && bin_of(__ldg(conf + (int64_t)j * N + r), q) < s_b[j]) ++j;
+      if (j < k) {
+        myA += __ldg(correct + (int64_t)j * N + r);
+      } else {
+        int d = k + 1;
+        while (d < K - 1 && bin_of(__ldg(conf + (int64_t)d * N + r), q) < s_b[d]) ++d;
+        key = bin_of(__ldg(conf + (int64_t)k * N + r), q) + 1;
+        okk = __ldg(correct + (int64_t)k * N + r) != 0;
+        okD = __ldg(correct + (int64_t)d * N + r) != 0;
+      }
+    }
+    const unsigned peers = __match_any_sync(0xFFFFFFFFu, key);
+    const unsigned bk = __ballot_sync(0xFFFFFFFFu, okk);
+    const unsigned bD = __ballot_sync(0xFFFFFFFFu, okD);
+    if (key >= 0 && (threadIdx.x & 31) == __ffs(peers) - 1) {
+      atomicAdd(&sh[key], (unsigned)__popc(peers));
+      const unsigned nk = __popc(peers & bk), nD = __popc(peers & bD);
+      if (nk) atomicAdd(&sh[nb + key], nk);
+      if (nD) atomicAdd(&sh[2 * nb + key], nD);
+    }
+  }
+  myA = warp_sum(myA);
+  if ((threadIdx.x & 31) == 0 && myA) atomicAdd(&s_A, myA);
+  __syncthreads();
+  hist_flush(sh, q, hist);
+  if (threadIdx.x == 0 && s_A) atomicAdd(reinterpret_cast<unsigned long long*>(&st->A), s_A);
+}
+
+// Final replay under the chosen thresholds: reach / handled per model and the
+// cascade's correct count (after refinement passes).
+__global__ void calib_replay_zero_kernel(int K, int64_t* reach, int64_t* handled,
+                                         int64_t* correct_total) {
+  pdl_start();
+  for (int k = threadIdx.x; k < K; k += blockDim.x) {
+    reach[k] = 0;
+    handled[k] = 0;
+  }
+  if (threadIdx.x == 0) *correct_total = 0;
+}
+
+__global__ void __launch_bounds__(512) calib_replay_kernel(const float* __restrict__ conf,
+                                                           const uint8_t* __restrict__ correct,
+                                                           int K, int64_t N, int q,
+                                                           const int32_t* __restrict__ b_idx,
+                                                           int64_t* reach, int64_t* handled,
+                                                           int64_t* correct_total) {
+  pdl_start();
+  __shared__ int s_b[16];
+  __shared__ unsigned long long s_reach[17], s_hand[17], s_ok;
+  if (threadIdx.x < 17) {
+    s_reach[threadIdx.x] = 0;
+    s_hand[threadIdx.x] = 0;
+  }
+  if (threadIdx.x < 16) s_b[threadIdx.x] = threadIdx.x < K - 1 ? b_idx[threadIdx.x] : 0;
+  if (threadIdx.x == 0) s_ok = 0;
+  __syncthreads();
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < N;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    int j = 0;
+    while (j < K - 1 && bin_of(__ldg(conf + (int64_t)j * N + r), q) < s_b[j]) ++j;
+    for (int i = 0; i <= j; ++i) atomicAdd(&s_reach[i], 1ull);
+    atomicAdd(&s_hand[j], 1ull);
+    if (__ldg(correct + (int64_t)j * N + r)) atomicAdd(&s_ok, 1ull);
+  }
+  __syncthreads();
+  if (threadIdx.x < K) {
+    if (s_reach[threadIdx.x]) atomicAdd(reinterpret_cast<unsigned long long*>(&reach[threadIdx.x]), s_reach[threadIdx.x]);
+    if (s_hand[threadIdx.x]) atomicAdd(reinterpret_cast<unsigned long long*>(&handled[threadIdx.x]), s_hand[threadIdx.x]);
+  }
+  if (threadIdx.x == 0 && s_ok) atomicAdd(reinterpret_cast<unsigned long long*>(correct_total), s_ok);
 }
 
 }  // namespace
@@ -474,6 +606,41 @@ cudaError_t launch_calib_fused(const float* conf, const uint8_t* correct, int K,
                                               args, smem, s);
   count_launch();
   return e != cudaSuccess ? e : cudaGetLastError();
+}
+
+cudaError_t launch_calib_refine(const float* conf, const uint8_t* correct, int K, int64_t N, int q,
+                                int passes, int32_t* b_idx, float* thr, int64_t* reach,
+                                int64_t* handled, int64_t* correct_total, void* ws,
+                                cudaStream_t s) {
+  CalibState* st = reinterpret_cast<CalibState*>(ws);
+  int32_t* hist = hist_of(ws);
+  const size_t smem = (size_t)3 * ((1 << q) + 2) * sizeof(unsigned);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(calib_refine_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(3 * ((1 << 14) + 2) * sizeof(unsigned)));
+    attr = true;
+  }
+  int64_t grid = (N + 4095) / 4096;
+  if (grid > num_sms()) grid = num_sms();
+  if (grid < 1) grid = 1;
+  cudaError_t e = cudaSuccess;
+  for (int p = 0; p < passes && e == cudaSuccess; ++p) {
+    for (int k = 0; k < K - 1 && e == cudaSuccess; ++k) {
+      e = launch_pdl(calib_refine_begin_kernel, dim3(1), dim3(32), 0, s, st);
+      if (e == cudaSuccess)
+        e = launch_pdl(calib_refine_hist_kernel, dim3((int)grid), dim3(512), smem, s, conf, correct,
+                       K, N, q, k, (const int32_t*)b_idx, hist, st);
+      if (e == cudaSuccess)
+        e = launch_calib_select(K, q, k, b_idx, thr, reach, handled, correct_total, ws, s);
+    }
+  }
+  if (e == cudaSuccess)
+    e = launch_pdl(calib_replay_zero_kernel, dim3(1), dim3(32), 0, s, K, reach, handled, correct_total);
+  if (e == cudaSuccess)
+    e = launch_pdl(calib_replay_kernel, dim3((int)grid), dim3(512), 0, s, conf, correct, K, N, q,
+                   (const int32_t*)b_idx, reach, handled, correct_total);
+  return e;
 }
 
 constexpr int kCalibCluster = 8;

@@ -121,6 +121,9 @@ cudaError_t launch_calib_cluster(const float* conf, const uint8_t* correct, int 
                                  int q, long long target, int32_t* b_idx, float* thr,
                                  int64_t* reach, int64_t* handled, int64_t* correct_total,
                                  void* ws, cudaStream_t s);
+cudaError_t launch_calib_refine(const float* conf, const uint8_t* correct, int K, int64_t N, int q,
+                                int passes, int32_t* b_idx, float* thr, int64_t* reach,
+                                int64_t* handled, int64_t* correct_total, void* ws, cudaStream_t s);
 cudaError_t launch_calib_select(int K, int q, int round, int32_t* b_idx, float* thr,
                                 int64_t* reach, int64_t* handled, int64_t* correct_total,
                                 void* ws, cudaStream_t s);

@@ -82,8 +82,8 @@ def test_route_and_calibrate_argument_errors(libhs):
     assert rc == 1 and "log2_bins" in lib.hs_last_error().decode()
     rc = lib.hs_calibrate_thresholds(256, 512, 3, 0, 12, -1, 0, 1, 2, 3, 4, 5, 1024, 1 << 20, None)
     assert rc == 1 and "empty" in lib.hs_last_error().decode()
-    rc = lib.hs_calibrate_thresholds(256, 512, 3, 10, 12, -1, 2, 1, 2, 3, 4, 5, 1024, 1 << 20, None)
-    assert rc == 6   # refinement not on the GPU
+    rc = lib.hs_calibrate_thresholds(256, 512, 3, 10, 12, -1, 65, 1, 2, 3, 4, 5, 1024, 1 << 20, None)
+    assert rc == 1 and "refine_passes" in lib.hs_last_error().decode()
     rc = lib.hs_cascade_step(3, 3, 256, 1, 10, 1, 1000, 1000, None, None, 1.0, 0, 0, 0.5, None,
                              None, None, 0, None, None, None, None, None, 512, 1024, 1 << 20,
                              None, None)

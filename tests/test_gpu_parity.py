@@ -475,3 +475,43 @@ def test_confidence_batched_equals_per_stage(hs, key, n_val):
                                 reduce=fam.reduce, labels=lab)
         assert_conf_close(got["conf"][sl].cpu().numpy(), ref["conf"])
         assert np.array_equal(got["correct"][sl].cpu().numpy(), ref["correct"])
+
+
+@pytest.mark.parametrize("passes", [1, 3])
+@pytest.mark.parametrize("q", [4, 12])
+def test_calibration_refinement_bit_exact(hs, passes, q):
+    """GPU refinement passes == oracle refinement (same thresholds, counts, correct total)."""
+    fam = synth.FAMILIES["c2"]
+    vconf, vok, _ = _gpu_val(hs, fam, 20000)
+    g = hs.calibrate_thresholds(vconf, vok, log2_bins=q, refine_passes=passes)
+    greedy = hs.calibrate_thresholds(vconf, vok, log2_bins=q)
+    torch.cuda.synchronize()
+    ref = oracle.calibrate(vconf.cpu().numpy(), vok.cpu().numpy(), q, refine_passes=passes)
+    assert np.array_equal(g["b"].cpu().numpy(), ref["b"])
+    assert np.array_equal(g["reach"].cpu().numpy(), ref["reach"])
+    assert np.array_equal(g["handled"].cpu().numpy(), ref["handled"])
+    assert int(g["correct_total"].item()) == ref["correct_total"] >= ref["tau"]
+    assert np.array_equal(g["t"].cpu().numpy().astype(np.float64), ref["t"])
+    assert np.all(g["b"].cpu().numpy() <= greedy["b"].cpu().numpy())     # never raises b_k
+
+
+def test_calibration_refinement_small_random(hs):
+    """Random small validation sets (K <= 5, N <= 300) incl. NaN confidences."""
+    rng = np.random.default_rng(11)
+    for _ in range(30):
+        K = int(rng.integers(3, 6))
+        N = int(rng.integers(1, 300))
+        q = int(rng.integers(1, 6))
+        d = rng.uniform(size=N)
+        ok = np.stack([(d + 0.3 * rng.normal(size=N) < 0.5 + 0.1 * k) for k in range(K)]).astype(np.uint8)
+        conf = np.clip(np.where(ok[:-1] == 1, rng.beta(5, 2, (K - 1, N)), rng.beta(2, 3, (K - 1, N))), 0, 1)
+        conf[rng.uniform(size=conf.shape) < 0.03] = np.nan
+        c = torch.from_numpy(conf.astype(np.float32)).to(dev())
+        o = torch.from_numpy(ok).to(dev())
+        for passes in (0, 2):
+            g = hs.calibrate_thresholds(c, o, log2_bins=q, refine_passes=passes)
+            torch.cuda.synchronize()
+            ref = oracle.calibrate(conf.astype(np.float32).astype(np.float64), ok, q, refine_passes=passes)
+            assert np.array_equal(g["b"].cpu().numpy(), ref["b"]), (K, N, q, passes)
+            assert np.array_equal(g["handled"].cpu().numpy(), ref["handled"])
+            assert int(g["correct_total"].item()) == ref["correct_total"]

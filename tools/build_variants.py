@@ -7,10 +7,10 @@ sys.path.insert(0, ROOT)
 from paper_2505_12566_b200 import _build  # noqa: E402
 
 VARIANTS = {
-    "ppcopy": ["HS_PP_COPY"],
-    "g8": ["HS_G8"],
-    "g8pp": ["HS_G8", "HS_PP_COPY"],
-    "tma": [],          # same build; selected at run time with HS_CONF_IMPL=tma
+    "lb2": ["HS_WARP_MINB=2"],          # G=8 NV=16 capped at 128 regs (16 warps/SM)
+    "g16": ["HS_G16"],                  # G=16 NV=8 (~100 regs, 16 warps/SM)
+    "g16lb2": ["HS_G16", "HS_WARP_MINB=2"],
+    "ctrace": ["HS_CALIB_TRACE"],
 }
 
 if __name__ == "__main__":
