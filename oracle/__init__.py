@@ -60,6 +60,12 @@ def lib():
             L.hso_calibrate.argtypes = [ctypes.c_int, _I64, _P, _P, ctypes.c_int, _I64,
                                         ctypes.c_int, _P, _P, _P, _P, _P]
             L.hso_calibrate.restype = ctypes.c_int
+            L.hso_skip_edges.argtypes = [ctypes.c_double, ctypes.c_int, ctypes.c_int, _P]
+            L.hso_skip_edges.restype = None
+            L.hso_skip_band.argtypes = [ctypes.c_double, _P, ctypes.c_int]
+            L.hso_skip_band.restype = ctypes.c_int
+            L.hso_cascade_skip.argtypes = [ctypes.c_int, _I64, _P, _P, ctypes.c_int, _P, _P]
+            L.hso_cascade_skip.restype = None
             _lib = L
     return _lib
 
@@ -148,6 +154,41 @@ def cascade(conf_by_stage: np.ndarray, thresholds) -> np.ndarray:
     out = np.empty(n, np.int32)
     lib().hso_cascade(int(K), int(n), _ptr(c), _ptr(t), _ptr(out))
     return out
+
+
+SKIP_UNIFORM, SKIP_DECADE = 0, 1
+
+
+def skip_edges(t: float, s: int, mode: int = SKIP_UNIFORM) -> np.ndarray:
+    """fp32 band edges inside [0, t) for s successor models (P:541 / S:320)."""
+    out = np.zeros(max(s - 1, 1), np.float32)
+    lib().hso_skip_edges(float(t), int(s), int(mode), _ptr(out))
+    return out[: max(s - 1, 0)]
+
+
+def skip_band(c: float, edges: np.ndarray) -> int:
+    e = np.ascontiguousarray(edges, dtype=np.float32)
+    if e.size == 0:
+        return 0
+    return int(lib().hso_skip_band(float(c), _ptr(e), int(e.size + 1)))
+
+
+def cascade_skip(conf_by_stage: np.ndarray, thresholds, mode: int = SKIP_UNIFORM):
+    """(stage_of, visits bitmask) with skip connections."""
+    c = np.ascontiguousarray(conf_by_stage, dtype=np.float64)
+    K, n = c.shape
+    t = np.zeros(K, np.float64)
+    tt = np.asarray(thresholds, dtype=np.float64).reshape(-1)
+    t[: min(K, tt.size)] = tt[: min(K, tt.size)]
+    stage_of = np.empty(n, np.int32)
+    visits = np.empty(n, np.uint32)
+    lib().hso_cascade_skip(int(K), int(n), _ptr(c), _ptr(t), int(mode), _ptr(stage_of), _ptr(visits))
+    return stage_of, visits
+
+
+def skip_stage_lists(stage_of: np.ndarray, visits: np.ndarray, K: int):
+    """Per model k: (batch = requests visiting k, accepted at k), increasing order."""
+    return [(np.flatnonzero((visits >> k) & 1), np.flatnonzero(stage_of == k)) for k in range(K)]
 
 
 def stage_lists(stage_of: np.ndarray, K: int):

@@ -329,3 +329,54 @@ int hso_calibrate(int K, int64_t N, const double* conf, const uint8_t* correct, 
     free(bins); free(alive); free(it);
     return 0;
 }
+
+/* ------------------------------------------------------------------------- */
+/* NEXT-1: skip connections (§IV-C, Alg. 2 line 5 P:530).    */
+/*   "The confidence interval below thresholds is uniformly partitioned into  */
+/*   the number of successor models"; "the request with the lowest    */
+/*   confidence should be routed to the largest model" and "requests with a   */
+/*   confidence score close to the threshold are routed to the successor     */
+/*   model".  Stage k (0-based, K models) has s = K-1-k successor  */
+/*   models and s-1 band edges inside [0, t_k):                               */
+/*     mode 0 (uniform):   e_i = t_k * (s - i) / s,  i = 1..s-1         */
+/*     mode 1 (decade, "LogUniform" reading): e_i = t_k * 10^-i         */
+/*   each edge is rounded to fp32 (the value both the router and this oracle   */
+/*   compare against).  A deferred request with confidence c goes to model    */
+/*   k + 1 + j, j = #{i : c < e_i} (j = 0: immediate successor; c below every */
+/*   edge: the largest model).  NaN confidences count as below every edge.    */
+/* ------------------------------------------------------------------------- */
+void hso_skip_edges(double t, int s, int mode, float* edges /* [s-1] */) {
+    for (int i = 1; i < s; ++i) {
+        double e = mode == 1 ? t * pow(10.0, -(double)i) : t * (double)(s - i) / (double)s;
+        edges[i - 1] = (float)e;
+    }
+}
+
+int hso_skip_band(double c, const float* edges, int s) {
+    int j = 0;
+    for (int i = 1; i < s; ++i)
+        if (!(c >= (double)edges[i - 1])) ++j;   /* c < e_i, or NaN */
+    return j;
+}
+
+/* Per request: the models it visits (bit k of visits[r]) and the one that
+ * answers (stage_of[r]).  conf[k*n + r] as in hso_cascade; t[0..K-2]. */
+void hso_cascade_skip(int K, int64_t n, const double* conf, const double* t, int mode,
+                      int32_t* stage_of, uint32_t* visits) {
+    float edges[64];
+    for (int64_t r = 0; r < n; ++r) {
+        int k = 0;
+        uint32_t v = 0;
+        while (1) {
+            v |= 1u << k;
+            if (k == K - 1) break;
+            const double c = conf[(int64_t)k * n + r];
+            if (c >= t[k]) break;
+            const int s = K - 1 - k;
+            hso_skip_edges(t[k], s, mode, edges);
+            k = k + 1 + hso_skip_band(c, edges, s);
+        }
+        stage_of[r] = k;
+        visits[r] = v;
+    }
+}

@@ -172,3 +172,63 @@ def test_bin_threshold_equivalence_fp32():
         for b in rng.integers(0, B + 2, size=30):
             t = np.float32(b / B) if b <= B else np.float32(np.inf)
             assert np.array_equal(bins >= b, c >= t)
+
+
+# ---------------------------------------------------------------------------
+# NEXT-1 skip connections
+# ---------------------------------------------------------------------------
+def test_skip_golden():
+    d = json.load(open(os.path.join(GOLD, "skip_bands.json")))
+    np.testing.assert_allclose(oracle.skip_edges(0.7, 2, oracle.SKIP_UNIFORM), d["edges_uniform_t0.7_s2"], rtol=1e-7)
+    np.testing.assert_allclose(oracle.skip_edges(0.7, 2, oracle.SKIP_DECADE), d["edges_decade_t0.7_s2"], rtol=1e-7)
+    np.testing.assert_allclose(oracle.skip_edges(0.9, 4, oracle.SKIP_UNIFORM), d["edges_uniform_t0.9_s4"], rtol=1e-7)
+    np.testing.assert_allclose(oracle.skip_edges(0.9, 4, oracle.SKIP_DECADE), d["edges_decade_t0.9_s4"], rtol=1e-6)
+    K, t = d["K"], d["t"]
+    for case in d["cases"]:
+        mode = oracle.SKIP_UNIFORM if case["mode"] == "uniform" else oracle.SKIP_DECADE
+        e = oracle.skip_edges(t[0], K - 1, mode)
+        c1 = np.float32(case["c1"]).astype(np.float64)
+        if "next" in case:
+            assert 1 + oracle.skip_band(c1, e) == case["next"], case
+        if "stage" in case:
+            conf = np.array([[c1], [0.1], [0.9]])
+            s, v = oracle.cascade_skip(conf, t, mode)
+            assert s[0] == case["stage"]
+            if "visits" in case:
+                assert [k for k in range(K) if (v[0] >> k) & 1] == case["visits"]
+
+
+def test_skip_reduces_to_sequential():
+    """One successor (K=2) or all edges above every confidence -> plain cascade."""
+    rng = np.random.default_rng(4)
+    conf = rng.uniform(size=(2, 500))
+    s1 = oracle.cascade(conf, [0.6, 0.0])
+    s2, v = oracle.cascade_skip(conf, [0.6, 0.0])
+    assert np.array_equal(s1, s2)
+
+
+def test_skip_invariants_random():
+    """Skips only jump forward; the answering model is >= the no-skip one's
+    (S:206 'skip soundness'); visits are a subset of 0..stage; every request is
+    answered exactly once (rho conservation)."""
+    rng = np.random.default_rng(8)
+    K, n = 5, 2000
+    conf = rng.uniform(size=(K, n))
+    conf[rng.uniform(size=(K, n)) < 0.01] = np.nan
+    t = [0.6, 0.5, 0.7, 0.4, 0.0]
+    seq = oracle.cascade(conf, t)
+    for mode in (oracle.SKIP_UNIFORM, oracle.SKIP_DECADE):
+        s, v = oracle.cascade_skip(conf, t, mode)
+        assert np.all(s >= seq)
+        assert np.all(v & 1)                                   # everyone starts at m_1
+        assert np.all((v >> s) & 1) and np.all(v >> (s + 1) == 0)
+        lists = oracle.skip_stage_lists(s, v, K)
+        assert sum(len(a) for _, a in lists) == n
+        # brute force: replay with explicit band lookups in Python
+        for r in range(0, n, 37):
+            k, path = 0, [0]
+            while k < K - 1 and not (conf[k, r] >= t[k]):
+                e = oracle.skip_edges(t[k], K - 1 - k, mode)
+                k = k + 1 + int(sum(1 for x in e if not (conf[k, r] >= float(x))))
+                path.append(k)
+            assert k == s[r] and sum(1 << p for p in path) == v[r]
