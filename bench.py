@@ -576,14 +576,28 @@ def run_reference(args, world, rank):
                     "d2h_bytes_per_step": 0}}
 
 
+def _claim_stdout():
+    """Route C-level stdout (NCCL's version banner, library prints) to stderr for
+    the whole run; return a writer for the one JSON line on the real stdout."""
+    sys.stdout.flush()
+    real = os.dup(1)
+    os.dup2(2, 1)
+
+    def emit(line: str):
+        os.write(real, (line + "\n").encode())
+
+    return emit
+
+
 def main():
+    emit = _claim_stdout()
     args = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if args.impl == "reference":
         line = run_reference(args, world, rank)
         if line is not None:
-            print(json.dumps(line), flush=True)
+            emit(json.dumps(line))
         return
     if (args.placement == "balanced" or args.force_dist) and int(os.environ.get("WORLD_SIZE", "1")) == 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
@@ -599,7 +613,7 @@ def main():
     if rank == 0:
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(fam, args.cpu_seconds)
-        print(json.dumps(line), flush=True)
+        emit(json.dumps(line))
     import torch.distributed as dist
     if dist.is_initialized():
         dist.barrier()

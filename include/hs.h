@@ -144,6 +144,35 @@ hs_status_t hs_route_compact(const float* conf, int64_t n, const int64_t* d_n, f
                              int64_t* d_counts, void* ws, size_t ws_bytes, hs_stream_t stream);
 
 /* ------------------------------------------------------------------------ */
+/* Skip connections (NEXT-1; §IV-C, Alg. 2 line 5 P:530).   */
+/* ------------------------------------------------------------------------ */
+/* A deferred request jumps over models that are unlikely to be confident:
+ * stage k (0-based, n_stages = K models) has s = K-1-k successors and s-1
+ * band edges inside [0, t_k), each rounded to fp32:
+ *   mode 0 uniform ("uniformly partitioned"): e_i = t_k * (s - i) / s
+ *   mode 1 decade  ("LogUniform(0, t_i)", P:530 read as S:320):  e_i = t_k / 10^i
+ * A request with c < t_k goes to model k + 1 + #{i : c < e_i} (the lowest
+ * confidence reaches the largest model).  Requests are tracked in a
+ * per-request int32 array dest[n_req] (caller-owned, device): dest[r] = the
+ * model r must visit next, or K + k once model k answered it.  Start with
+ * dest = 0 for every request.
+ *   hs_skip_select: batch of model k = requests r with dest[r] == k, in
+ *     increasing r (stable compaction; d_counts = {#other, #selected}).
+ *   hs_skip_route: threshold test of a batch (conf[i] of request ids[i]);
+ *     accepted -> acc lists exactly as hs_route_compact; every item updates
+ *     dest[ids[i]].  d_threshold as in hs_route_compact.
+ * Workspaces: hs_route_compact_workspace(n), zero-filled before first use.
+ * hs_skip_edges (host-only, pure): the fp32 edges for a host threshold. */
+hs_status_t hs_skip_edges(float threshold, int32_t successors, int32_t mode, float* edges /*host [successors-1]*/);
+hs_status_t hs_skip_select(const int32_t* dest, int64_t n_req, int32_t stage, int64_t* batch_ids,
+                           int64_t* d_counts, void* ws, size_t ws_bytes, hs_stream_t stream);
+hs_status_t hs_skip_route(const float* conf, int64_t n, const int64_t* d_n, float threshold,
+                          const float* d_threshold, int32_t stage, int32_t n_stages, int32_t mode,
+                          const int64_t* ids, const int32_t* pred, int32_t pred_len,
+                          int64_t* acc_ids, float* acc_conf, int32_t* acc_pred, int32_t* dest,
+                          int64_t* d_counts, void* ws, size_t ws_bytes, hs_stream_t stream);
+
+/* ------------------------------------------------------------------------ */
 /* One cascade stage m_k: confidence -> threshold test -> compaction/gather.  */
 /* ------------------------------------------------------------------------ */
 /* stage: 0-based index k of the model; is_last = (stage == n_stages - 1).

@@ -339,15 +339,17 @@ int hso_calibrate(int K, int64_t N, const double* conf, const uint8_t* correct, 
 /*   model".  Stage k (0-based, K models) has s = K-1-k successor  */
 /*   models and s-1 band edges inside [0, t_k):                               */
 /*     mode 0 (uniform):   e_i = t_k * (s - i) / s,  i = 1..s-1         */
-/*     mode 1 (decade, "LogUniform" reading): e_i = t_k * 10^-i         */
+/*     mode 1 (decade, "LogUniform" reading): e_i = t_k / 10^i          */
 /*   each edge is rounded to fp32 (the value both the router and this oracle   */
 /*   compare against).  A deferred request with confidence c goes to model    */
 /*   k + 1 + j, j = #{i : c < e_i} (j = 0: immediate successor; c below every */
 /*   edge: the largest model).  NaN confidences count as below every edge.    */
 /* ------------------------------------------------------------------------- */
 void hso_skip_edges(double t, int s, int mode, float* edges /* [s-1] */) {
+    double p10 = 1.0;                      /* 10^i, exact in fp64 for i <= 22 */
     for (int i = 1; i < s; ++i) {
-        double e = mode == 1 ? t * pow(10.0, -(double)i) : t * (double)(s - i) / (double)s;
+        p10 *= 10.0;
+        double e = mode == 1 ? t / p10 : t * (double)(s - i) / (double)s;
         edges[i - 1] = (float)e;
     }
 }

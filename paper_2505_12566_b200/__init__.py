@@ -390,3 +390,128 @@ class Cascade:
                         "pred": o["acc_pred"][:na * s.seq_len].cpu(), "n_acc": na,
                         "n_def": int(counts[k, 1])})
         return res
+
+
+# ---------------------------------------------------------------------------
+# Skip connections (NEXT-1): hs_skip_select / hs_skip_route
+# ---------------------------------------------------------------------------
+SKIP_UNIFORM, SKIP_DECADE = 0, 1
+
+
+def skip_edges(threshold: float, successors: int, mode: int = SKIP_UNIFORM) -> list:
+    """fp32 band edges inside [0, t) (host helper, hs_skip_edges)."""
+    import ctypes
+    n = max(successors - 1, 0)
+    buf = (ctypes.c_float * max(n, 1))()
+    _abi.call("hs_skip_edges", float(threshold), int(successors), int(mode), ctypes.addressof(buf))
+    return [buf[i] for i in range(n)]
+
+
+def skip_select(dest: torch.Tensor, stage: int, *, out: dict | None = None,
+                ws: torch.Tensor | None = None, stream=None) -> dict:
+    """Batch of model `stage`: requests r with dest[r] == stage, increasing r."""
+    _check_cuda(dest)
+    n = int(dest.numel())
+    out = dict(out or {})
+    if "ids" not in out:
+        out["ids"] = torch.empty(max(n, 1), dtype=torch.int64, device=dest.device)
+    if "counts" not in out:
+        out["counts"] = torch.zeros(2, dtype=torch.int64, device=dest.device)
+    if ws is None:
+        ws = workspace(lib().hs_route_compact_workspace(n), dest.device)
+    _abi.call("hs_skip_select", _p(dest), n, int(stage), _p(out["ids"]), _p(out["counts"]), _p(ws),
+              ws.numel(), _stream(stream))
+    return out
+
+
+def skip_route(conf: torch.Tensor, threshold, stage: int, n_stages: int, dest: torch.Tensor,
+               ids: torch.Tensor, *, mode: int = SKIP_UNIFORM, n: int | None = None,
+               d_n: torch.Tensor | None = None, pred: torch.Tensor | None = None,
+               pred_len: int = 1, out: dict | None = None, ws: torch.Tensor | None = None,
+               stream=None) -> dict:
+    """Threshold test of model `stage`'s batch with skip bands; updates dest."""
+    _check_cuda(conf, dest, ids, d_n, pred)
+    n = int(conf.numel() if n is None else n)
+    dev = conf.device
+    out = dict(out or {})
+    if "acc_ids" not in out:
+        out["acc_ids"] = torch.empty(max(n, 1), dtype=torch.int64, device=dev)
+    if "acc_conf" not in out:
+        out["acc_conf"] = torch.empty(max(n, 1), dtype=torch.float32, device=dev)
+    if pred is not None and "acc_pred" not in out:
+        out["acc_pred"] = torch.empty(max(n, 1) * pred_len, dtype=torch.int32, device=dev)
+    if "counts" not in out:
+        out["counts"] = torch.zeros(2, dtype=torch.int64, device=dev)
+    if ws is None:
+        ws = workspace(lib().hs_route_compact_workspace(n), dev)
+    d_thr = threshold if isinstance(threshold, torch.Tensor) else None
+    thr = 0.0 if d_thr is not None else float(threshold)
+    _abi.call("hs_skip_route", _p(conf), n, _p(d_n), thr, _p(d_thr), int(stage), int(n_stages),
+              int(mode), _p(ids), _p(pred), int(pred_len), _p(out["acc_ids"]), _p(out["acc_conf"]),
+              _p(out.get("acc_pred")), _p(dest), _p(out["counts"]), _p(ws), ws.numel(),
+              _stream(stream))
+    return out
+
+
+class SkipCascade:
+    """The cascade with skip connections: per model k, select its batch from the
+    per-request `dest` array (hs_skip_select), compute the confidences of those
+    rows (hs_confidence, logits indexed by request id), then threshold + band
+    routing (hs_skip_route).  No host round trip; `dest[r] - K` is the model
+    that answered request r when all stages ran."""
+
+    def __init__(self, n_req: int, stages: list[StageSpec], device, mode: int = SKIP_UNIFORM):
+        self.n = int(n_req)
+        self.stages = stages
+        self.K = len(stages)
+        self.mode = int(mode)
+        dev = torch.device(device)
+        self.device = dev
+        L = max(s.seq_len for s in stages)
+        self.dest = torch.zeros(self.n, dtype=torch.int32, device=dev)
+        self.counts = torch.zeros(self.K, 2, dtype=torch.int64, device=dev)
+        self.sel_counts = torch.zeros(self.K, 2, dtype=torch.int64, device=dev)
+        self.batch = [torch.empty(self.n, dtype=torch.int64, device=dev) for _ in range(self.K)]
+        self.conf = torch.empty(self.n, dtype=torch.float32, device=dev)
+        self.argmax = torch.empty(self.n * L, dtype=torch.int32, device=dev)
+        self.outs = [{"acc_ids": torch.empty(self.n, dtype=torch.int64, device=dev),
+                      "acc_conf": torch.empty(self.n, dtype=torch.float32, device=dev),
+                      "acc_pred": torch.empty(self.n * s.seq_len, dtype=torch.int32, device=dev),
+                      "counts": self.counts[k]} for k, s in enumerate(stages)]
+        self.ws_sel = workspace(lib().hs_route_compact_workspace(self.n), dev)
+        self.ws_route = workspace(lib().hs_route_compact_workspace(self.n), dev)
+        self.ws_conf = torch.empty(max(16, self.n * L * 5 + 1024), dtype=torch.uint8, device=dev)
+        self.ids0 = torch.arange(self.n, dtype=torch.int64, device=dev)
+        self.status = torch.zeros(1, dtype=torch.int32, device=dev)
+
+    def route(self, logits: list, thresholds, stream=None):
+        d_thr = thresholds if isinstance(thresholds, torch.Tensor) else None
+        self.dest.zero_()
+        for k, s in enumerate(self.stages):
+            if k == 0:
+                ids, d_n = self.ids0, None
+            else:
+                skip_select(self.dest, k, out={"ids": self.batch[k], "counts": self.sel_counts[k]},
+                            ws=self.ws_sel, stream=stream)
+                ids, d_n = self.batch[k], self.sel_counts[k][1:2]
+            confidence(logits[k], n=self.n, seq_len=s.seq_len, n_classes=s.n_classes,
+                       temperature=s.temperature, kind=s.kind, reduce=s.reduce, row_index=ids,
+                       d_n=d_n, out={"conf": self.conf, "argmax": self.argmax}, ws=self.ws_conf,
+                       status=self.status, stream=stream)
+            thr = d_thr[k:k + 1] if d_thr is not None else float(thresholds[k] if k < self.K - 1 else 0.0)
+            skip_route(self.conf, thr, k, self.K, self.dest, ids, mode=self.mode, n=self.n, d_n=d_n,
+                       pred=self.argmax, pred_len=s.seq_len, out=self.outs[k], ws=self.ws_route,
+                       stream=stream)
+        return self
+
+    def results(self):
+        counts = self.counts.cpu()
+        sel = self.sel_counts.cpu()
+        res = []
+        for k, s in enumerate(self.stages):
+            na = int(counts[k, 0])
+            nb = self.n if k == 0 else int(sel[k, 1])
+            res.append({"ids": self.outs[k]["acc_ids"][:na].cpu(),
+                        "batch": (self.ids0 if k == 0 else self.batch[k])[:nb].cpu(),
+                        "pred": self.outs[k]["acc_pred"][:na * s.seq_len].cpu(), "n_acc": na})
+        return res

@@ -29,6 +29,9 @@ SIGNATURES = {
     "hs_route_compact_workspace": (SZ, [I64]),
     "hs_route_compact": (I32, [P, I64, P, F32, P, I32, P, P, I32, P, P, P, P, P, P, I64, P, P, P,
                                SZ, P]),
+    "hs_skip_edges": (I32, [F32, I32, I32, P]),
+    "hs_skip_select": (I32, [P, I64, I32, P, P, P, SZ, P]),
+    "hs_skip_route": (I32, [P, I64, P, F32, P, I32, I32, I32, P, P, I32, P, P, P, P, P, P, SZ, P]),
     "hs_cascade_step_workspace": (SZ, [I64, I32]),
     "hs_cascade_step": (I32, [I32, I32, P, I32, I64, I32, I64, I64, P, P, F32, I32, I32, F32, P, P,
                               P, I64, P, P, P, P, P, P, P, SZ, P, P]),

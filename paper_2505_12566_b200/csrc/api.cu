@@ -299,6 +299,76 @@ hs_status_t hs_route_compact(const float* conf, int64_t n, const int64_t* d_n, f
                             def_payload, d_counts, ws, (cudaStream_t)stream);
 }
 
+hs_status_t hs_skip_edges(float threshold, int32_t successors, int32_t mode, float* edges) {
+  if (successors < 1 || successors - 1 > hs::kMaxSkipEdges)
+    return fail(HS_ERR_INVALID_ARGUMENT, "successors = %d outside 1..%d", successors, hs::kMaxSkipEdges + 1);
+  if (mode != 0 && mode != 1) return fail(HS_ERR_INVALID_ARGUMENT, "skip mode must be 0 or 1");
+  if (successors > 1 && !edges) return fail(HS_ERR_INVALID_ARGUMENT, "edges is NULL");
+  double p10 = 1.0;
+  for (int i = 1; i < successors; ++i) {
+    p10 *= 10.0;
+    edges[i - 1] = mode == 1 ? (float)((double)threshold / p10)
+                             : (float)((double)threshold * (double)(successors - i) / (double)successors);
+  }
+  return HS_OK;
+}
+
+hs_status_t hs_skip_select(const int32_t* dest, int64_t n_req, int32_t stage, int64_t* batch_ids,
+                           int64_t* d_counts, void* ws, size_t ws_bytes, hs_stream_t stream) {
+  if (n_req < 0 || n_req >= (int64_t(1) << 30)) return fail(HS_ERR_INVALID_ARGUMENT, "n_req outside 0..2^30-1");
+  if (!d_counts || (n_req > 0 && (!dest || !batch_ids))) return fail(HS_ERR_INVALID_ARGUMENT, "NULL argument");
+  if (!ws || ws_bytes < hs::compact_ws_bytes(n_req))
+    return fail(HS_ERR_WORKSPACE_TOO_SMALL, "workspace %zu < %zu", ws_bytes, hs::compact_ws_bytes(n_req));
+  hs::CompactArgs a{};
+  a.n = n_req;
+  a.sel_dest = dest;
+  a.sel_k = stage;
+  a.def_ids = batch_ids;
+  a.counts = d_counts;
+  a.ws = ws;
+  return cuda_check(hs::launch_route_compact(a, (cudaStream_t)stream), "skip select kernel");
+}
+
+hs_status_t hs_skip_route(const float* conf, int64_t n, const int64_t* d_n, float threshold,
+                          const float* d_threshold, int32_t stage, int32_t n_stages, int32_t mode,
+                          const int64_t* ids, const int32_t* pred, int32_t pred_len,
+                          int64_t* acc_ids, float* acc_conf, int32_t* acc_pred, int32_t* dest,
+                          int64_t* d_counts, void* ws, size_t ws_bytes, hs_stream_t stream) {
+  if (n < 0 || n >= (int64_t(1) << 30)) return fail(HS_ERR_INVALID_ARGUMENT, "n outside 0..2^30-1");
+  if (n_stages < 1 || n_stages - 2 > hs::kMaxSkipEdges || stage < 0 || stage >= n_stages)
+    return fail(HS_ERR_INVALID_ARGUMENT, "stage %d / n_stages %d out of range", stage, n_stages);
+  if (mode != 0 && mode != 1) return fail(HS_ERR_INVALID_ARGUMENT, "skip mode must be 0 or 1");
+  const int is_last = stage == n_stages - 1;
+  if (!is_last && !d_threshold) {
+    hs_status_t st = check_threshold(threshold);
+    if (st != HS_OK) return st;
+  }
+  if (!d_counts || (n > 0 && (!conf || !ids || !dest))) return fail(HS_ERR_INVALID_ARGUMENT, "NULL argument");
+  if (acc_pred && (!pred || pred_len < 1)) return fail(HS_ERR_INVALID_ARGUMENT, "acc_pred requires pred and pred_len >= 1");
+  if (!ws || ws_bytes < hs::compact_ws_bytes(n))
+    return fail(HS_ERR_WORKSPACE_TOO_SMALL, "workspace %zu < %zu", ws_bytes, hs::compact_ws_bytes(n));
+  hs::CompactArgs a{};
+  a.conf = conf;
+  a.n = n;
+  a.d_n = d_n;
+  a.threshold = threshold;
+  a.d_threshold = d_threshold;
+  a.is_last = is_last;
+  a.ids = ids;
+  a.pred = pred;
+  a.pred_len = pred_len;
+  a.acc_ids = acc_ids;
+  a.acc_conf = acc_conf;
+  a.acc_pred = acc_pred;
+  a.counts = d_counts;
+  a.ws = ws;
+  a.skip_dest = dest;
+  a.skip_K = n_stages;
+  a.skip_stage = stage;
+  a.skip_mode = mode;
+  return cuda_check(hs::launch_route_compact(a, (cudaStream_t)stream), "skip route kernel");
+}
+
 // cascade-step workspace: [compact ws][conf f32 n][argmax i32 n*L][def_pos i64 n][conf ws]
 static size_t step_layout(int64_t n, int32_t L, size_t* o_conf, size_t* o_am, size_t* o_pos,
                           size_t* o_cws) {

@@ -17,6 +17,7 @@
 // GPUs (all-reduce) and every rank selects the same b_k.
 #include <cooperative_groups.h>
 #include <cstdio>
+#include <cstdlib>
 
 #include "hs_common.cuh"
 #include "hs_internal.h"
@@ -24,6 +25,10 @@
 namespace hs {
 
 namespace cg = cooperative_groups;
+
+#ifdef HS_CALIB_TRACE
+__device__ unsigned long long g_calib_trace[64];
+#endif
 
 namespace {
 
@@ -331,12 +336,12 @@ __global__ void __launch_bounds__(1024) calib_fused_kernel(const float* __restri
   extern __shared__ unsigned sh[];
   cg::grid_group grid = cg::this_grid();
 #ifdef HS_CALIB_TRACE
-  unsigned long long t0, tt;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  int tr = 0;
 #define HS_TR(tag)                                                             \
-  if (blockIdx.x == 0 && threadIdx.x == 0) {                                   \
+  if (blockIdx.x == 0 && threadIdx.x == 0 && tr < 64) {                        \
+    unsigned long long tt;                                                     \
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt));                     \
-    printf("calib trace k=%d %s %llu ns\n", k, tag, tt - t0);                   \
+    g_calib_trace[tr++] = tt;                                                  \
   }
 #else
 #define HS_TR(tag)
@@ -427,6 +432,272 @@ __global__ void __launch_bounds__(1024, 1) calib_cluster_kernel(const float* __r
     if (rank == 0)
       select_core<1024>(SharedHist{sh, nb}, K, q, k, b_idx, thr, reach, handled, correct_total, st);
     cluster.sync();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Resident variant of the cooperative kernel (default when the samples fit):
+// every CTA loads ITS samples once -- the fp32 bins of stages 0..K-2 (int16,
+// NaN -> -1) and the K correct bits -- into shared memory, so a round touches
+// no per-sample global memory.  One grid barrier per round: the CTAs flush
+// their histograms into a rotating set of three global buffers (round k uses
+// buffer k % 3 and zeroes buffer (k+1) % 3, which every CTA stopped reading
+// two barriers ago), then EVERY CTA pulls the summed histogram and runs the
+// same deterministic select, so nobody waits for a broadcast of b_k.  CTA 0
+// alone writes the outputs.
+//
+// The global buffers hold one packed u64 per bin -- count | correct_k << 21 |
+// correct_K << 42 (N < 2^21, checked by the launcher) -- so a flush is one
+// red.add.u64 per non-empty bin, and the select reads its contiguous bins
+// straight from L2 into registers (no shared-memory staging of the histogram).
+// ---------------------------------------------------------------------------
+struct SelState {            // per-CTA copy of the select state + outputs
+  CalibState st;
+  int32_t b[16];
+  float t[17];
+  int64_t reach[17], handled[17], total;
+};
+
+constexpr int kPackBits = 21;
+constexpr unsigned long long kPackMask = (1ull << kPackBits) - 1;
+
+// select_core's three passes (same arithmetic, same tie rules) on a packed
+// global histogram whose bins [lo, lo + n) sit in this thread's registers.
+template <int NT, int PMAX>
+__device__ __forceinline__ void select_packed(const unsigned long long* __restrict__ g, int K,
+                                              int q, int round, SelState* ss) {
+  constexpr int NW = NT / 32;
+  static_assert(NW <= 32, "one warp scans the warp totals");
+  __shared__ int sh_x[NW], sh_y[NW], sh_z[NW], sh_u[NW];
+  __shared__ int sh_tot[2];
+  __shared__ int sh_bk;
+  __shared__ long long sh_tau, sh_A;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int B = 1 << q;
+  const int per = (B + 1 + NT - 1) / NT;          // <= PMAX (checked by the launcher)
+  const int lo = min(tid * per, B + 1), n = min(per, B + 1 - lo);
+  unsigned long long v[PMAX];
+#pragma unroll
+  for (int i = 0; i < PMAX; ++i) v[i] = i < n ? __ldcg(g + lo + i + 1) : 0ull;
+  const unsigned long long v0 = tid == 0 ? __ldcg(g) : 0ull;   // NaN bin: never accepted
+#define HS_CNT(x) ((int)((x) & kPackMask))
+#define HS_CK(x) ((int)(((x) >> kPackBits) & kPackMask))
+#define HS_CKK(x) ((int)((x) >> (2 * kPackBits)))
+  // ---- pass 1
+  int segH = 0, segCnt = HS_CNT(v0), segK = HS_CKK(v0);
+#pragma unroll
+  for (int i = 0; i < PMAX; ++i) {
+    segH += HS_CK(v[i]) - HS_CKK(v[i]);
+    segCnt += HS_CNT(v[i]);
+    segK += HS_CKK(v[i]);
+  }
+  int incl = segH;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_down_sync(0xFFFFFFFFu, incl, o);
+    if (lane + o < 32) incl += y;
+  }
+  const int wc = __reduce_add_sync(0xFFFFFFFFu, segCnt);
+  const int wk = __reduce_add_sync(0xFFFFFFFFu, segK);
+  if (lane == 0) {
+    sh_x[wid] = incl;
+    sh_y[wid] = wc;
+    sh_z[wid] = wk;
+  }
+  __syncthreads();
+  if (wid == 0) {
+    const int h = lane < NW ? sh_x[lane] : 0;
+    int suf = h;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_down_sync(0xFFFFFFFFu, suf, o);
+      if (lane + o < 32) suf += y;
+    }
+    const int tc = __reduce_add_sync(0xFFFFFFFFu, lane < NW ? sh_y[lane] : 0);
+    const int tk = __reduce_add_sync(0xFFFFFFFFu, lane < NW ? sh_z[lane] : 0);
+    if (lane < NW) sh_u[lane] = suf - h;
+    if (lane == 0) {
+      sh_tot[0] = tc;
+      sh_tot[1] = tk;
+      if (round == 0 && ss->st.tau_ap) ss->st.tau = tk;   // AP: tau = correct answers of m_K
+      sh_tau = ss->st.tau;
+      sh_A = ss->st.A;
+    }
+  }
+  __syncthreads();
+  const long long reach_k = sh_tot[0], G = sh_tot[1], tau = sh_tau, A = sh_A;
+  // ---- pass 2
+  int best = B + 1;
+  {
+    long long S = (long long)sh_u[wid] + (incl - segH);
+#pragma unroll
+    for (int i = PMAX - 1; i >= 0; --i) {
+      if (i < n) {
+        S += HS_CK(v[i]) - HS_CKK(v[i]);
+        if (A + G + S >= tau) best = lo + i;
+      }
+    }
+  }
+  best = (int)__reduce_min_sync(0xFFFFFFFFu, (unsigned)best);
+  if (lane == 0) sh_x[wid] = best;
+  __syncthreads();
+  if (wid == 0) {
+    const unsigned x = lane < NW ? (unsigned)sh_x[lane] : (unsigned)(B + 1);
+    const int bk = (int)__reduce_min_sync(0xFFFFFFFFu, x);
+    if (lane == 0) sh_bk = bk;
+  }
+  __syncthreads();
+  const int bk = sh_bk;
+  // ---- pass 3
+  int s_ck = 0, s_cnt = 0, s_bc = HS_CNT(v0), s_bK = HS_CKK(v0);
+#pragma unroll
+  for (int i = 0; i < PMAX; ++i) {
+    if (lo + i >= bk) {              // empty tail slots are zero
+      s_ck += HS_CK(v[i]);
+      s_cnt += HS_CNT(v[i]);
+    } else {
+      s_bc += HS_CNT(v[i]);
+      s_bK += HS_CKK(v[i]);
+    }
+  }
+#undef HS_CNT
+#undef HS_CK
+#undef HS_CKK
+  s_ck = __reduce_add_sync(0xFFFFFFFFu, s_ck);
+  s_cnt = __reduce_add_sync(0xFFFFFFFFu, s_cnt);
+  s_bc = __reduce_add_sync(0xFFFFFFFFu, s_bc);
+  s_bK = __reduce_add_sync(0xFFFFFFFFu, s_bK);
+  if (lane == 0) {
+    sh_x[wid] = s_ck;
+    sh_y[wid] = s_cnt;
+    sh_z[wid] = s_bc;
+    sh_u[wid] = s_bK;
+  }
+  __syncthreads();
+  if (wid == 0) {
+    const int ck = __reduce_add_sync(0xFFFFFFFFu, lane < NW ? sh_x[lane] : 0);
+    const int cnt = __reduce_add_sync(0xFFFFFFFFu, lane < NW ? sh_y[lane] : 0);
+    const int bc = __reduce_add_sync(0xFFFFFFFFu, lane < NW ? sh_z[lane] : 0);
+    const int bK = __reduce_add_sync(0xFFFFFFFFu, lane < NW ? sh_u[lane] : 0);
+    if (lane == 0) {
+      long long Anew = A + ck;
+      ss->b[round] = bk;
+      ss->t[round] = bk <= B ? (float)bk / (float)B : INFINITY;
+      ss->reach[round] = reach_k;
+      ss->handled[round] = cnt;
+      if (round == K - 2) {
+        ss->reach[K - 1] = bc;
+        ss->handled[K - 1] = bc;
+        Anew += bK;
+        ss->t[K - 1] = 0.f;
+        ss->total = Anew;
+      }
+      ss->st.A = Anew;
+    }
+  }
+  __syncthreads();
+}
+
+constexpr int kResidentThreads = 1024;
+
+// PMAX = bins per thread in the select, ceil((2^q + 1) / 1024): one
+// instantiation per range of q keeps the bins in registers.
+template <int PMAX>
+__global__ void __launch_bounds__(kResidentThreads, 1) calib_resident_kernel(
+    const float* __restrict__ conf, const uint8_t* __restrict__ correct, int K, int64_t N, int q,
+    long long target, int32_t* b_idx, float* thr, int64_t* reach, int64_t* handled,
+    int64_t* correct_total, CalibState* st_out, unsigned long long* hist3, int per_cta) {
+  pdl_start();
+#ifdef HS_CALIB_TRACE
+  int tr = 0;
+#endif
+  extern __shared__ __align__(16) unsigned char smraw[];
+  cg::grid_group grid = cg::this_grid();
+  const int nb = (1 << q) + 2;
+  const int hw = 3 * nb;                                   // u32 words of the local histogram
+  unsigned* sh = reinterpret_cast<unsigned*>(smraw);        // local histogram (SoA)
+  SelState* ss = reinterpret_cast<SelState*>(smraw + (size_t)hw * 4 + 16 - ((size_t)hw * 4) % 16);
+  int16_t* sbin = reinterpret_cast<int16_t*>(ss + 1);       // [(K-1) x per_cta]
+  uint16_t* sok = reinterpret_cast<uint16_t*>(sbin + (size_t)(K - 1) * per_cta);
+  const int tid = threadIdx.x;
+  const int64_t r0 = (int64_t)blockIdx.x * per_cta;
+  const int m = (int)max((int64_t)0, min((int64_t)per_cta, N - r0));
+  // ---- resident samples
+  for (int i = tid; i < m; i += blockDim.x) {
+    const int64_t r = r0 + i;
+    uint16_t ok = 0;
+    for (int k = 0; k < K; ++k) ok |= (uint16_t)(__ldg(correct + (int64_t)k * N + r) != 0) << k;
+    sok[i] = ok;
+    for (int k = 0; k < K - 1; ++k) sbin[(size_t)k * per_cta + i] = (int16_t)bin_of(__ldg(conf + (int64_t)k * N + r), q);
+  }
+  for (int i = tid; i < hw; i += blockDim.x) sh[i] = 0u;   // the flush re-zeroes it
+  if (tid == 0) {
+    ss->st.A = 0;
+    ss->st.tau = target < 0 ? 0 : target;
+    ss->st.tau_ap = target < 0 ? 1 : 0;
+  }
+  // buffer 0 must be zero for round 0: zeroed here, ordered by the first barrier
+  for (int i = blockIdx.x * blockDim.x + tid; i < nb; i += gridDim.x * blockDim.x) hist3[i] = 0ull;
+  grid.sync();
+  HS_TR("init");
+  const int mup = (m + 31) & ~31;
+  for (int k = 0; k < K - 1; ++k) {
+    unsigned long long* cur = hist3 + (size_t)(k % 3) * nb;
+    unsigned long long* nxt = hist3 + (size_t)((k + 1) % 3) * nb;
+    for (int i = blockIdx.x * blockDim.x + tid; i < nb; i += gridDim.x * blockDim.x) nxt[i] = 0ull;
+    for (int i = tid; i < mup; i += blockDim.x) {
+      bool alive = i < m;
+      int key = -1;
+      bool okk = false, okK = false;
+      if (alive) {
+        for (int j = 0; j < k; ++j) alive &= sbin[(size_t)j * per_cta + i] < ss->b[j];
+        if (alive) {
+          const uint16_t ok = sok[i];
+          key = sbin[(size_t)k * per_cta + i] + 1;
+          okk = (ok >> k) & 1u;
+          okK = (ok >> (K - 1)) & 1u;
+        }
+      }
+      const unsigned peers = __match_any_sync(0xFFFFFFFFu, key);
+      const unsigned bk = __ballot_sync(0xFFFFFFFFu, okk);
+      const unsigned bK = __ballot_sync(0xFFFFFFFFu, okK);
+      if (key >= 0 && (tid & 31) == __ffs(peers) - 1) {
+        atomicAdd(&sh[key], (unsigned)__popc(peers));
+        const unsigned nk = __popc(peers & bk), nK = __popc(peers & bK);
+        if (nk) atomicAdd(&sh[nb + key], nk);
+        if (nK) atomicAdd(&sh[2 * nb + key], nK);
+      }
+    }
+    __syncthreads();
+    HS_TR("local");
+    for (int i = tid; i < nb; i += blockDim.x) {
+      const unsigned c = sh[i];
+      if (c) {       // correct counts are only taken on counted samples
+        const unsigned long long ck = sh[nb + i], cK = sh[2 * nb + i];
+        sh[i] = 0u;
+        sh[nb + i] = 0u;
+        sh[2 * nb + i] = 0u;
+        atomicAdd(cur + i, (unsigned long long)c | (ck << kPackBits) | (cK << (2 * kPackBits)));
+      }
+    }
+    HS_TR("flush");
+    grid.sync();
+    HS_TR("sync");
+    // every CTA selects from the summed histogram (identical results)
+    select_packed<kResidentThreads, PMAX>(cur, K, q, k, ss);
+    HS_TR("select");
+  }
+  if (blockIdx.x == 0) {
+    for (int k = tid; k < K; k += blockDim.x) {
+      if (k < K - 1) b_idx[k] = ss->b[k];
+      thr[k] = ss->t[k];
+      reach[k] = ss->reach[k];
+      handled[k] = ss->handled[k];
+    }
+    if (tid == 0) {
+      *correct_total = ss->total;
+      *st_out = ss->st;            // refinement passes continue from tau (D5)
+    }
   }
 }
 
@@ -548,7 +819,7 @@ __global__ void __launch_bounds__(512) calib_replay_kernel(const float* __restri
 size_t calib_hist_bytes(int q) { return (size_t)3 * ((1u << q) + 2) * sizeof(int32_t); }
 size_t calib_ws_bytes(int K, int q) {
   (void)K;
-  return sizeof(CalibState) + calib_hist_bytes(q);
+  return sizeof(CalibState) + 3 * calib_hist_bytes(q);   // 3 rotating buffers (resident kernel)
 }
 
 static int32_t* hist_of(void* ws) {
@@ -577,10 +848,61 @@ cudaError_t launch_calib_hist(const float* conf, const uint8_t* correct, int K, 
                     round, b_idx, hist);
 }
 
+static cudaError_t launch_calib_resident(const float* conf, const uint8_t* correct, int K,
+                                        int64_t N, int q, long long target, int32_t* b_idx,
+                                        float* thr, int64_t* reach, int64_t* handled,
+                                        int64_t* correct_total, void* ws, cudaStream_t s,
+                                        bool* launched) {
+  *launched = false;
+  const size_t hbytes = (size_t)3 * ((1 << q) + 2) * sizeof(unsigned);
+  const size_t head = hbytes + 16 - hbytes % 16 + sizeof(SelState);
+  const size_t cap = 220 * 1024;
+  int grid = (int)((N + 4095) / 4096);
+  if (grid > num_sms()) grid = num_sms();
+  if (grid < 1) grid = 1;
+  const int64_t per = (N + grid - 1) / grid;
+  const size_t smem = head + (size_t)per * (2 * (size_t)(K - 1) + 2) + 16;
+  // packed u64 bins need N < 2^21; K <= 16 correct bits per sample
+  if (K > 16 || N >= (int64_t(1) << kPackBits) || q > 14 || smem > cap) return cudaSuccess;
+  const int pm = q <= 9 ? 1 : q <= 11 ? 3 : q == 12 ? 5 : q == 13 ? 9 : 17;
+  void (*kern)(const float*, const uint8_t*, int, int64_t, int, long long, int32_t*, float*,
+               int64_t*, int64_t*, int64_t*, CalibState*, unsigned long long*, int) =
+      pm == 1 ? calib_resident_kernel<1> : pm == 3 ? calib_resident_kernel<3>
+      : pm == 5 ? calib_resident_kernel<5> : pm == 9 ? calib_resident_kernel<9>
+                                                     : calib_resident_kernel<17>;
+  static bool attr[5] = {false, false, false, false, false};
+  const int slot = pm == 1 ? 0 : pm == 3 ? 1 : pm == 5 ? 2 : pm == 9 ? 3 : 4;
+  if (!attr[slot]) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cap);
+    attr[slot] = true;
+  }
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kResidentThreads, smem);
+  if (per_sm < 1 || grid > per_sm * num_sms()) return cudaSuccess;
+  // 3 x (B+2) u64 fit in the 3 x 3 x (B+2) u32 the workspace reserves
+  unsigned long long* hist3 = reinterpret_cast<unsigned long long*>(hist_of(ws));
+  CalibState* st = reinterpret_cast<CalibState*>(ws);
+  int per_cta = (int)per;
+  void* args[] = {(void*)&conf, (void*)&correct, (void*)&K, (void*)&N, (void*)&q, (void*)&target,
+                  (void*)&b_idx, (void*)&thr, (void*)&reach, (void*)&handled,
+                  (void*)&correct_total, (void*)&st, (void*)&hist3, (void*)&per_cta};
+  cudaError_t e = cudaLaunchCooperativeKernel((void*)kern, dim3(grid), dim3(kResidentThreads),
+                                              args, smem, s);
+  count_launch();
+  *launched = true;
+  return e != cudaSuccess ? e : cudaGetLastError();
+}
+
 cudaError_t launch_calib_fused(const float* conf, const uint8_t* correct, int K, int64_t N, int q,
                                long long target, int32_t* b_idx, float* thr, int64_t* reach,
                                int64_t* handled, int64_t* correct_total, void* ws,
                                cudaStream_t s) {
+  if (!getenv("HS_CALIB_NORESIDENT")) {
+    bool launched = false;
+    const cudaError_t e = launch_calib_resident(conf, correct, K, N, q, target, b_idx, thr, reach,
+                                                handled, correct_total, ws, s, &launched);
+    if (launched || e != cudaSuccess) return e;
+  }
   const size_t smem = (size_t)3 * ((1 << q) + 2) * sizeof(unsigned);
   static int max_blocks = -1;
   if (max_blocks < 0) {
@@ -624,7 +946,8 @@ cudaError_t launch_calib_refine(const float* conf, const uint8_t* correct, int K
   int64_t grid = (N + 4095) / 4096;
   if (grid > num_sms()) grid = num_sms();
   if (grid < 1) grid = 1;
-  cudaError_t e = cudaSuccess;
+  // the greedy kernels leave the histogram buffers in an unspecified state
+  cudaError_t e = passes > 0 ? cudaMemsetAsync(hist, 0, calib_hist_bytes(q), s) : cudaSuccess;
   for (int p = 0; p < passes && e == cudaSuccess; ++p) {
     for (int k = 0; k < K - 1 && e == cudaSuccess; ++k) {
       e = launch_pdl(calib_refine_begin_kernel, dim3(1), dim3(32), 0, s, st);
@@ -686,3 +1009,10 @@ cudaError_t launch_calib_select(int K, int q, int round, int32_t* b_idx, float* 
 }
 
 }  // namespace hs
+
+#ifdef HS_CALIB_TRACE
+// experiment builds only: phase timestamps of the last fused calibration launch
+extern "C" int hs_debug_calib_trace(unsigned long long* out) {
+  return (int)cudaMemcpyFromSymbol(out, hs::g_calib_trace, sizeof(unsigned long long) * 64);
+}
+#endif

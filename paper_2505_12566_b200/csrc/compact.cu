@@ -58,7 +58,24 @@ __global__ void __launch_bounds__(kCompactThreads) route_compact_kernel(const Co
 
   {
     const int64_t base = tile * kCompactTile;
-    const float thr = a.d_threshold ? *a.d_threshold : a.threshold;
+    const float thr = a.sel_dest ? 0.5f : (a.d_threshold ? *a.d_threshold : a.threshold);
+    // skip connections: band edges of this model's
+    // successors, computed from the (possibly device-resident) threshold
+    float edges[kMaxSkipEdges];
+    int nedges = 0;
+    if (a.skip_dest) {
+      nedges = a.skip_K - 2 - a.skip_stage;   // s - 1 edges for s = K-1-k successors
+      if (nedges > kMaxSkipEdges) nedges = kMaxSkipEdges;
+      const int sc = nedges + 1;
+      double p10 = 1.0;
+#pragma unroll
+      for (int e = 0; e < kMaxSkipEdges; ++e) {
+        p10 *= 10.0;
+        if (e < nedges)
+          edges[e] = a.skip_mode == 1 ? (float)((double)thr / p10)
+                                      : (float)((double)thr * (double)(sc - 1 - e) / (double)sc);
+      }
+    }
     // ---- all loads of the tile first (independent, coalesced: item j of thread
     //      tid is base + j*T + tid), so they overlap instead of serialising
     //      behind the ballots and the output stores
@@ -70,7 +87,9 @@ __global__ void __launch_bounds__(kCompactThreads) route_compact_kernel(const Co
     for (int j = 0; j < I; ++j) {
       const int64_t i = base + (int64_t)j * T + tid;
       const bool in = i < n;
-      cv[j] = in ? __ldg(a.conf + i) : 0.f;
+      // selection mode (skip connections): the "conf" of item i is whether
+      // request i is due at model sel_k (1) or not (0)
+      cv[j] = in ? (a.sel_dest ? (__ldg(a.sel_dest + i) == a.sel_k ? 0.f : 1.f) : __ldg(a.conf + i)) : 0.f;
       idv[j] = (in && a.ids) ? __ldg(a.ids + i) : i;
       pv[j] = (in && pred1) ? __ldg(a.pred + i) : 0;
     }
@@ -79,7 +98,8 @@ __global__ void __launch_bounds__(kCompactThreads) route_compact_kernel(const Co
 #pragma unroll
     for (int j = 0; j < I; ++j) {
       const int64_t i = base + (int64_t)j * T + tid;
-      // NaN confidence: deferred (unless last)
+      // NaN confidence: deferred (unless last).  Selection mode: "deferred" =
+      // selected (cv = 0 < thr = 0.5)
       const bool d = (i < n) && !(a.is_last || cv[j] >= thr);
       dfr[j] = d;
       bal[j] = __ballot_sync(0xFFFFFFFFu, d);
@@ -152,6 +172,18 @@ __global__ void __launch_bounds__(kCompactThreads) route_compact_kernel(const Co
       if (i >= n) continue;
       const int local = j * T + tid;
       const int drank = s_off[j * NW + wid] + __popc(bal[j] & lt);
+      if (a.skip_dest) {
+        // next model of request idv[j]: k+1+band (deferred) or K+k (answered at k)
+        int dst = a.skip_K + a.skip_stage;
+        if (dfr[j]) {
+          int band = 0;
+#pragma unroll
+          for (int e = 0; e < kMaxSkipEdges; ++e)
+            if (e < nedges && !(cv[j] >= edges[e])) ++band;   // c < edge, or NaN
+          dst = a.skip_stage + 1 + band;
+        }
+        a.skip_dest[idv[j]] = dst;
+      }
       if (dfr[j]) {
         const int64_t pos = excl + drank;
         if (a.def_ids) a.def_ids[pos] = idv[j];

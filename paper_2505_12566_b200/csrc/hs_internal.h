@@ -97,7 +97,16 @@ struct CompactArgs {
   int64_t* def_pos;
   int64_t* counts;
   void* ws;
+  // selection mode (skip connections): select items i with sel_dest[i] == sel_k
+  const int32_t* sel_dest;
+  int sel_k;
+  // skip-route mode: write skip_dest[ids[i]] = next model (or K + stage when answered)
+  int32_t* skip_dest;
+  int skip_K;
+  int skip_stage;
+  int skip_mode;         // 0 uniform, 1 decade ("LogUniform")
 };
+constexpr int kMaxSkipEdges = 15;
 cudaError_t launch_route_compact(const CompactArgs& a, cudaStream_t s);
 cudaError_t launch_gather_rows(const int64_t* pos, const int64_t* d_count, int64_t cap,
                                const void* src, int64_t row_bytes, void* dst, cudaStream_t s);

@@ -105,3 +105,17 @@ def test_product_never_imports_oracle():
         for f in files:
             if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
                 assert not bad.search(open(os.path.join(dirpath, f)).read()), f
+
+
+def test_skip_edges_host_helper_matches_oracle(libhs):
+    """hs_skip_edges is host arithmetic (no device work): same fp32 edges as the
+    oracle's P:541 / S:320 bands, for the fp32 threshold the router compares."""
+    import numpy as np
+    import oracle
+    import paper_2505_12566_b200 as hs
+    for t in (0.0, 0.25, 0.7, 0.999, 1.0):
+        t32 = float(np.float32(t))
+        for s_ in range(1, 8):
+            for mode in (hs.SKIP_UNIFORM, hs.SKIP_DECADE):
+                assert np.array_equal(np.array(hs.skip_edges(t32, s_, mode), np.float32),
+                                      oracle.skip_edges(t32, s_, mode)), (t, s_, mode)

@@ -439,9 +439,12 @@ def test_calibration_modes_agree(hs, monkeypatch):
     vconf, vok, _ = _gpu_val(hs, fam, 20000)
     for q in (3, 12, 14):
         res = {}
-        for mode in ("cluster", "fused", "split"):
-            monkeypatch.setenv("HS_CALIB_MODE", mode)
+        for mode in ("cluster", "fused", "fused_streaming", "split"):
+            monkeypatch.setenv("HS_CALIB_MODE", mode.split("_")[0])
+            if mode == "fused_streaming":          # the non-resident cooperative kernel
+                monkeypatch.setenv("HS_CALIB_NORESIDENT", "1")
             res[mode] = hs.calibrate_thresholds(vconf, vok, log2_bins=q)
+            monkeypatch.delenv("HS_CALIB_NORESIDENT", raising=False)
         monkeypatch.delenv("HS_CALIB_MODE")
         torch.cuda.synchronize()
         ref = oracle.calibrate(vconf.cpu().numpy(), vok.cpu().numpy(), q)
@@ -449,6 +452,34 @@ def test_calibration_modes_agree(hs, monkeypatch):
             assert np.array_equal(r["b"].cpu().numpy(), ref["b"]), (q, mode)
             for key in ("b", "t", "reach", "handled", "correct_total"):
                 assert torch.equal(r[key], res["split"][key]), (q, mode, key)
+
+
+@pytest.mark.parametrize("K,N,q", [(2, 1, 12), (3, 4095, 8), (7, 300001, 12), (16, 70000, 10),
+                                   (4, 100000, 14), (3, 20000, 13), (6, 200000, 1), (5, 50000, 11),
+                                   (5, 1 << 22, 12)])
+def test_calibration_resident_vs_streaming(hs, monkeypatch, K, N, q):
+    """The resident cooperative kernel (samples in shared memory, three rotating
+    histograms, redundant per-CTA select) == the streaming one == the oracle.
+    The last case does not fit shared memory and exercises the fallback."""
+    g = torch.Generator().manual_seed(K * 1000 + q)
+    conf = torch.rand(K - 1, N, generator=g)
+    conf[:, ::97] = float("nan")
+    conf[:, 1::89] = 1.0
+    ok = (torch.rand(K, N, generator=g) < 0.75).to(torch.uint8)
+    d_conf, d_ok = conf.to(dev()), ok.to(dev())
+    res = {}
+    for mode in ("resident", "streaming"):
+        if mode == "streaming":
+            monkeypatch.setenv("HS_CALIB_NORESIDENT", "1")
+        res[mode] = hs.calibrate_thresholds(d_conf, d_ok, log2_bins=q)
+        monkeypatch.delenv("HS_CALIB_NORESIDENT", raising=False)
+    torch.cuda.synchronize()
+    for key in ("b", "t", "reach", "handled", "correct_total"):
+        assert torch.equal(res["resident"][key], res["streaming"][key]), key
+    if N <= 300001:
+        ref = oracle.calibrate(conf.numpy(), ok.numpy(), q)
+        assert np.array_equal(res["resident"]["b"].cpu().numpy(), ref["b"])
+        assert int(res["resident"]["correct_total"]) == ref["correct_total"]
 
 
 @pytest.mark.parametrize("key,n_val", [("c2", 3001), ("c1", 513), ("c4", 24)])
@@ -515,3 +546,54 @@ def test_calibration_refinement_small_random(hs):
             assert np.array_equal(g["b"].cpu().numpy(), ref["b"]), (K, N, q, passes)
             assert np.array_equal(g["handled"].cpu().numpy(), ref["handled"])
             assert int(g["correct_total"].item()) == ref["correct_total"]
+
+
+# ---------------------------------------------------------------------------
+# NEXT-1 skip connections
+# ---------------------------------------------------------------------------
+def test_skip_edges_match_oracle(hs):
+    # the C-ABI takes the fp32 threshold the router compares against (D3)
+    for t in (0.0, 0.25, 0.7, 0.999, 1.0):
+        t32 = float(np.float32(t))
+        for s_ in range(1, 8):
+            for mode in (0, 1):
+                assert np.array_equal(np.array(hs.skip_edges(t32, s_, mode), np.float32),
+                                      oracle.skip_edges(t32, s_, mode)), (t, s_, mode)
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+@pytest.mark.parametrize("key,n", [("c2", 20000), ("c1", 4096)])
+def test_skip_cascade_vs_oracle(hs, mode, key, n):
+    fam = synth.FAMILIES[key]
+    K = fam.K
+    ids = np.arange(n, dtype=np.int64)
+    logits, conf_o = [], []
+    for k in range(K):
+        bits = synth.logits_np(fam.seed, k, ids, fam.L, fam.C, fam.thr[k], fam.dtype)
+        logits.append(to_dev_bits(bits, fam.dtype))
+        conf_o.append(oracle.confidence(bits, n, fam.L, fam.C, fam.C, fam.temps[k], kind=fam.kind,
+                                        reduce=fam.reduce)["conf"])
+    conf_o = np.stack(conf_o)
+    t = [0.9, 0.8, 0.7, 0.6, 0.0][-K:] if K > 2 else [0.8, 0.0]
+    t = np.array(t, np.float32).astype(np.float64)
+    sc = hs.SkipCascade(n, [hs.StageSpec(fam.C, fam.temps[k], fam.L, fam.kind, fam.reduce)
+                            for k in range(K)], dev(), mode=mode)
+    sc.route(logits, t.tolist())
+    res = sc.results()
+    stage_of, visits = oracle.cascade_skip(conf_o, t, mode)
+    lists = oracle.skip_stage_lists(stage_of, visits, K)
+    # requests near a threshold or a band edge may legitimately differ: exclude them
+    near = np.zeros(n, bool)
+    for k in range(K - 1):
+        near |= np.abs(conf_o[k] - t[k]) <= REL * t[k]
+        for e in oracle.skip_edges(t[k], K - 1 - k, mode):
+            near |= np.abs(conf_o[k] - e) <= REL * max(float(e), 1e-30)
+    for k in range(K):
+        gb, ga = res[k]["batch"].numpy(), res[k]["ids"].numpy()
+        wb, wa = lists[k]
+        assert np.array_equal(gb[~near[gb]], wb[~near[wb]]), k
+        assert np.array_equal(ga[~near[ga]], wa[~near[wa]]), k
+    d = sc.dest.cpu().numpy() - K
+    assert np.array_equal(d[~near], stage_of[~near])
+    if mode == 0 and K > 2:
+        assert (visits & 2 == 0).sum() > 0          # some requests really skipped model 2

@@ -18,10 +18,14 @@ def main():
             conf = torch.rand(K - 1, N, generator=g).to(dev)
             ok = (torch.rand(K, N, generator=g) < 0.8).to(torch.uint8).to(dev)
             for q in (4, 12):
-                for mode in ("cluster", "fused", "split"):
+                for mode in ("cluster", "fused", "fused_streaming", "split"):
                     if mode == "cluster" and N >= (1 << 20):
                         continue
-                    os.environ["HS_CALIB_MODE"] = mode
+                    os.environ["HS_CALIB_MODE"] = mode.split("_")[0]
+                    if mode == "fused_streaming":
+                        os.environ["HS_CALIB_NORESIDENT"] = "1"
+                    else:
+                        os.environ.pop("HS_CALIB_NORESIDENT", None)
                     out = hs._calib_out(K, dev, None)
                     ws = hs.calibrate_workspace(K, q, dev)
                     s = torch.cuda.Stream()
