@@ -230,6 +230,8 @@ hs_status_t hs_confidence_batched(const void* const* logits, const float* temper
                                   nullptr, temperatures[0], kind);
   a.nbatch = n_batches;
   a.brows = n * seq_len;
+  // exact for every row < 2^32: (2^64 + e) / d with e < d, row * e < 2^64
+  a.bmagic = a.brows >= 2 ? (uint64_t)(~0ull / (uint64_t)a.brows) + 1ull : 0ull;
   for (int b = 0; b < n_batches; ++b) {
     a.bptr[b] = logits[b];
     a.bc[b] = (float)(1.4426950408889634 / (double)temperatures[b]);

@@ -204,6 +204,183 @@ __global__ void __launch_bounds__(kCompactThreads) route_compact_kernel(const Co
 
 }
 
+// ---------------------------------------------------------------------------
+// K3 fast path (the plain cascade split: no selection / skip modes, at most one
+// prediction word per item): thread t owns the 8 consecutive items
+// base + 8t .. base + 8t + 7, loaded with 128-bit loads when the tile is full
+// and the arrays are 16-byte aligned.  Ranks come from a block scan of the
+// per-thread deferred counts; the split is staged in shared memory in tile
+// order (accepted first, then deferred) and written out coalesced.
+// ---------------------------------------------------------------------------
+constexpr int kFastItems = 8;
+static_assert(kFastItems * kCompactThreads == kCompactTile, "one tile per CTA");
+
+__global__ void __launch_bounds__(kCompactThreads) route_compact_fast_kernel(const CompactArgs a,
+                                                                             int vec) {
+  pdl_start();
+  constexpr int T = kCompactThreads, I = kFastItems, NW = T / 32, TILE = kCompactTile;
+  __shared__ long long s_id[TILE];     // accepted ids [0, A_t), deferred ids [A_t, tn)
+  __shared__ long long s_aux[TILE];    // accepted: pred << 32 | conf bits; deferred: position
+  __shared__ int s_woff[NW];
+  __shared__ long long s_excl;
+  __shared__ int s_agg;
+
+  CompactWs* ws = reinterpret_cast<CompactWs*>(a.ws);
+  unsigned long long* st = tile_status(a.ws);
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  int64_t n = a.n;
+  if (a.d_n) n = min(*a.d_n, a.n);
+  const int64_t ntiles = (n + TILE - 1) / TILE;
+  const int64_t tile = blockIdx.x;
+  if (ntiles == 0) {
+    if (tile == 0 && tid == 0) {
+      a.counts[0] = 0;
+      a.counts[1] = 0;
+    }
+    return;
+  }
+  if (tile >= ntiles) return;
+  const unsigned epoch = *(volatile unsigned*)&ws->epoch;
+  const unsigned long long etag = (unsigned long long)epoch << 32;
+  const int64_t base = tile * TILE;
+  const int tn = (int)min((int64_t)TILE, n - base);
+  const int64_t i0 = base + (int64_t)tid * I;
+  const float thr = a.d_threshold ? *a.d_threshold : a.threshold;
+  const bool pred1 = a.acc_pred && a.pred_len == 1;
+
+  float cv[I];
+  int64_t idv[I];
+  int32_t pv[I];
+  if (vec && i0 + I <= n) {
+    const float4* c4 = reinterpret_cast<const float4*>(a.conf + i0);
+    const float4 x0 = __ldg(c4), x1 = __ldg(c4 + 1);
+    cv[0] = x0.x; cv[1] = x0.y; cv[2] = x0.z; cv[3] = x0.w;
+    cv[4] = x1.x; cv[5] = x1.y; cv[6] = x1.z; cv[7] = x1.w;
+    if (a.ids) {
+      const longlong2* q = reinterpret_cast<const longlong2*>(a.ids + i0);
+#pragma unroll
+      for (int j = 0; j < I / 2; ++j) {
+        const longlong2 y = __ldg(q + j);
+        idv[2 * j] = y.x;
+        idv[2 * j + 1] = y.y;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < I; ++j) idv[j] = i0 + j;
+    }
+    if (pred1) {
+      const int4* q = reinterpret_cast<const int4*>(a.pred + i0);
+      const int4 p0 = __ldg(q), p1 = __ldg(q + 1);
+      pv[0] = p0.x; pv[1] = p0.y; pv[2] = p0.z; pv[3] = p0.w;
+      pv[4] = p1.x; pv[5] = p1.y; pv[6] = p1.z; pv[7] = p1.w;
+    } else {
+#pragma unroll
+      for (int j = 0; j < I; ++j) pv[j] = 0;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < I; ++j) {
+      const int64_t i = i0 + j;
+      const bool in = i < n;
+      cv[j] = in ? __ldg(a.conf + i) : 0.f;
+      idv[j] = (in && a.ids) ? __ldg(a.ids + i) : i;
+      pv[j] = (in && pred1) ? __ldg(a.pred + i) : 0;
+    }
+  }
+  // D3 per item (NaN defers; the last stage accepts all), D4 ranks
+  unsigned dm = 0;
+#pragma unroll
+  for (int j = 0; j < I; ++j)
+    dm |= (unsigned)((i0 + j < n) && !(a.is_last || cv[j] >= thr)) << j;
+  const int cnt = __popc(dm);
+  int incl = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) s_woff[wid] = incl;
+  __syncthreads();
+  if (wid == 0) {
+    const int wv = lane < NW ? s_woff[lane] : 0;
+    int wi = wv;
+#pragma unroll
+    for (int o = 1; o < NW; o <<= 1) {
+      const int y = __shfl_up_sync(0xFFFFFFFFu, wi, o);
+      if (lane >= o) wi += y;
+    }
+    if (lane < NW) s_woff[lane] = wi - wv;
+    const long long agg = __shfl_sync(0xFFFFFFFFu, wi, NW - 1);
+    long long excl = 0;
+    if (tile == 0) {
+      if (lane == 0) st_release(&st[0], etag | kFlagP | (unsigned long long)agg);
+    } else {
+      if (lane == 0) st_release(&st[tile], etag | kFlagA | (unsigned long long)agg);
+      int64_t pred = tile - 1;
+      while (true) {
+        const int64_t idx = pred - lane;
+        unsigned long long d = (idx >= 0) ? ld_acquire(&st[idx]) : (etag | kFlagP);
+        while (__any_sync(0xFFFFFFFFu, desc_flag(d, epoch) == 0)) {
+          if (desc_flag(d, epoch) == 0) d = ld_acquire(&st[idx]);
+        }
+        const unsigned pm = __ballot_sync(0xFFFFFFFFu, desc_flag(d, epoch) == 2);
+        const long long val = (long long)(d & kValMask);
+        if (pm) {
+          const int first = __ffs(pm) - 1;
+          excl += warp_sum(lane <= first ? val : 0ll);
+          break;
+        }
+        excl += warp_sum(val);
+        pred -= 32;
+      }
+      if (lane == 0) st_release(&st[tile], etag | kFlagP | (unsigned long long)(excl + agg));
+    }
+    if (lane == 0) {
+      if (tile == ntiles - 1) {
+        a.counts[0] = n - (excl + agg);
+        a.counts[1] = excl + agg;
+        ws->epoch = epoch + 1u;
+      }
+      s_excl = excl;
+      s_agg = (int)agg;
+    }
+  }
+  __syncthreads();
+  const long long excl = s_excl;
+  const int nacc = tn - s_agg;
+  // stage in tile order: accepted at [0, nacc), deferred at [nacc, tn)
+  int dr = s_woff[wid] + incl - cnt;          // deferred items of this tile before item i0
+  int ar = tid * I - dr;                      // accepted items before item i0
+#pragma unroll
+  for (int j = 0; j < I; ++j) {
+    if (i0 + j >= n) break;
+    if ((dm >> j) & 1u) {
+      s_id[nacc + dr] = idv[j];
+      s_aux[nacc + dr] = i0 + j;
+      ++dr;
+    } else {
+      s_id[ar] = idv[j];
+      s_aux[ar] = ((long long)(uint32_t)pv[j] << 32) | (long long)__float_as_uint(cv[j]);
+      ++ar;
+    }
+  }
+  __syncthreads();
+  const int64_t acc_base = base - excl;       // accepted items before this tile
+  for (int p = tid; p < tn; p += T) {
+    const long long id = s_id[p], aux = s_aux[p];
+    if (p < nacc) {
+      const int64_t pos = acc_base + p;
+      if (a.acc_ids) a.acc_ids[pos] = id;
+      if (a.acc_conf) a.acc_conf[pos] = __uint_as_float((uint32_t)aux);
+      if (pred1) a.acc_pred[pos] = (int32_t)(aux >> 32);
+    } else {
+      const int64_t pos = excl + (p - nacc);
+      if (a.def_ids) a.def_ids[pos] = id;
+      if (a.def_pos) a.def_pos[pos] = aux;
+    }
+  }
+}
+
 // K4: dst[j] = src[pos[j]] for j < *d_count, rows of row_bytes (multiple of 16)
 __global__ void __launch_bounds__(256) gather_rows_kernel(const int64_t* __restrict__ pos,
                                                           const int64_t* d_count, int64_t cap,
@@ -237,9 +414,16 @@ size_t compact_ws_bytes(int64_t n) {
   return sizeof(CompactWs) + (size_t)(tiles > 0 ? tiles : 1) * sizeof(unsigned long long);
 }
 
+static bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
+
 cudaError_t launch_route_compact(const CompactArgs& a, cudaStream_t s) {
   const int64_t tiles = (a.n + kCompactTile - 1) / kCompactTile;
   const int grid = (int)(tiles > 0 ? tiles : 1);
+  const bool fast = !a.sel_dest && !a.skip_dest && (!a.acc_pred || a.pred_len == 1);
+  if (fast) {
+    const int vec = aligned16(a.conf) && aligned16(a.ids) && (!a.acc_pred || aligned16(a.pred));
+    return launch_pdl(route_compact_fast_kernel, dim3(grid), dim3(kCompactThreads), 0, s, a, vec);
+  }
   return launch_pdl(route_compact_kernel, dim3(grid), dim3(kCompactThreads), 0, s, a);
 }
 

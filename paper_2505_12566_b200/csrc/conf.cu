@@ -14,11 +14,14 @@
 // formed exactly before scaling so the 1e-5 relative confidence tolerance holds
 // even at T = 0.05.
 //
-// Two launch shapes:
-//   * conf_warp_kernel  -- one warp per row, the whole row in registers
-//     (C <= 4096 bf16 / 2048 fp32: ViT/GLUE classifiers).  Exact two-step
-//     (row max by shuffle, then exponentials) -- no online rescaling.  The next
-//     row's loads are issued before the current row is reduced.
+// Launch shapes:
+//   * conf_async_kernel -- G lanes per row, the row in registers, the next row
+//     prefetched by per-lane cp.async into a per-warp shared-memory double
+//     buffer (default for rows of <= 128 x 16 B: ViT/ImageNet classifiers).
+//   * conf_warp_kernel  -- the same reduction with a register double buffer
+//     (rows up to 512 x 16 B, e.g. C <= 4096 bf16 / 2048 fp32).  Exact
+//     two-step (row max by shuffle, then exponentials) -- no online rescaling.
+//   * conf_tma_kernel   -- the same with a TMA bulk-copy ring (selectable).
 //   * conf_cta_kernel   -- one CTA per row, persistent over rows, per-thread
 //     online (max, sum, weighted sum) over 8-vector chunks, block merge
 //     (vocabulary-sized rows: T5 32,128, Llama 128,256).
@@ -41,7 +44,8 @@ struct RowOut {
   float e0;    // 2^a of the max element (1 when a is formed as (x - m) * c)
 };
 
-__device__ __forceinline__ void write_row(const ConfArgs& a, int64_t row, int64_t src_row,
+// `lab`: the row's label, loaded by the caller ahead of time (a.labels only)
+__device__ __forceinline__ void write_row(const ConfArgs& a, int64_t row, int32_t lab,
                                           const RowOut& r) {
   const bool bad = !(r.m < INFINITY) || (r.m == -INFINITY);
   float c;
@@ -64,7 +68,7 @@ __device__ __forceinline__ void write_row(const ConfArgs& a, int64_t row, int64_
   }
   a.conf[row] = c;
   if (a.argmax) a.argmax[row] = am;
-  if (a.ok) a.ok[row] = (uint8_t)(a.labels ? (!bad && a.labels[src_row] == am) : 0);
+  if (a.ok) a.ok[row] = (uint8_t)(a.labels ? (!bad && lab == am) : 0);
 }
 
 
@@ -91,7 +95,8 @@ struct RowSrc {
 __device__ __forceinline__ int64_t batch_local(const ConfArgs& a, int64_t row, int* b) {
   *b = 0;
   if (a.nbatch > 1) {
-    *b = (int)((uint32_t)row / (uint32_t)a.brows);   // rows < 2^32
+    // rows < 2^32: multiply by the host-computed reciprocal (no integer divide)
+    *b = a.bmagic ? (int)__umul64hi((uint64_t)row, a.bmagic) : (int)row;
     return row - (int64_t)(*b) * a.brows;
   }
   return row;
@@ -117,6 +122,10 @@ __device__ __forceinline__ RowSrc locate_with(const ConfArgs& a, int64_t row, in
 }
 __device__ __forceinline__ RowSrc locate(const ConfArgs& a, int64_t row) {
   return locate_with(a, row, fetch_index(a, row));
+}
+// the label of a located row, issued with its logits loads (used at write time)
+__device__ __forceinline__ int32_t fetch_label(const ConfArgs& a, const RowSrc& r) {
+  return a.labels ? __ldg(a.labels + r.src) : 0;
 }
 
 // -inf for the out-of-row elements of the last partial 16-byte vector
@@ -254,10 +263,27 @@ __device__ __forceinline__ void group_mask_tail(uint4 (&v)[NV], int gl, int nvec
   }
 }
 
+// first element of the bf16 vector x equal to the NORMAL bf16 value whose
+// bits are mb2 = (mb, mb): packed compare (exact for normal m; a subnormal
+// element would be flushed to 0 != m)
+__device__ __forceinline__ int vec_first_eq_bf16n(const uint4& x, uint32_t mb2) {
+  int r = 8;
+#pragma unroll
+  for (int q = 3; q >= 0; --q) {
+    asm("{\n\t.reg .pred p, h;\n\t"
+        "setp.eq.bf16x2 p|h, %1, %2;\n\t"
+        "@h mov.s32 %0, %3;\n\t"
+        "@p mov.s32 %0, %4;\n\t}"
+        : "+r"(r)
+        : "r"(word(x, q)), "r"(mb2), "r"(2 * q + 1), "r"(2 * q));
+  }
+  return r;
+}
+
 template <bool BF16, bool ENTROPY, int NV, int G>
 __device__ __forceinline__ void group_reduce_row(const ConfArgs& a, const uint4 (&v)[NV],
                                                  bool active, int64_t row, int64_t src, int gl,
-                                                 float c) {
+                                                 float c, const uint4* rowp, int32_t lab) {
   constexpr int VE = BF16 ? 8 : 4;
   const f2_t c2 = f2(c, c);
   // 1. row max (exact, NaN-propagating): packed per-vector maxima, then the group
@@ -273,30 +299,59 @@ __device__ __forceinline__ void group_reduce_row(const ConfArgs& a, const uint4 
 #pragma unroll
   for (int o = G / 2; o > 0; o >>= 1) m = fmax_nan(m, __shfl_xor_sync(0xFFFFFFFFu, m, o));
 
-  // 2. argmax: lowest vector index holding m, then the first element in it
+  // 2. argmax = lowest index holding m.  (i) each lane: lowest of its vectors
+  //    whose packed max contains m; (ii) group min -> vector vi; (iii) lane 0
+  //    re-reads that one 16-byte vector (an L2 hit: the row was just streamed)
+  //    and finds the first element equal to m after the exponential pass has
+  //    hidden the load.  A normal bf16 m is matched with one packed compare per
+  //    vector; a zero/subnormal m (or fp32) takes the exact fp32 compares.
+#ifdef HS_EXP_NOARGMAX
+  const unsigned am = 0;
+#else
   unsigned vi = 0xFFFFFFFFu;
+  // zero / subnormal row max (rare): packed compares would flush; exact path
+  const bool slow = BF16 && (m == m) && !(fabsf(m) >= 1.17549435e-38f);
+  const bool anyslow = BF16 && __any_sync(0xFFFFFFFFu, slow);
+  const uint32_t mb2 = (__float_as_uint(m) >> 16) * 0x10001u;
 #pragma unroll
-  for (int k = NV - 1; k >= 0; --k)
-    if (maxw_has<BF16>(vmw[k], m)) vi = (unsigned)(k * G + gl);
+  for (int k = NV - 1; k >= 0; --k) {
+    const unsigned idx = (unsigned)(k * G + gl);
+    if (BF16) {
+      asm("{\n\t.reg .pred p, h;\n\t"
+          "setp.eq.bf16x2 p|h, %1, %2;\n\t"
+          "@h mov.u32 %0, %3;\n\t"
+          "@p mov.u32 %0, %3;\n\t}"
+          : "+r"(vi)
+          : "r"(vmw[k]), "r"(mb2), "r"(idx));
+    } else if (__uint_as_float(vmw[k]) == m) {
+      vi = idx;
+    }
+  }
+  if (anyslow) {
+    if (slow) {
+      vi = 0xFFFFFFFFu;
+#pragma unroll
+      for (int k = NV - 1; k >= 0; --k)
+        if (maxw_has<BF16>(vmw[k], m)) vi = (unsigned)(k * G + gl);
+    }
+  }
 #pragma unroll
   for (int o = G / 2; o > 0; o >>= 1) vi = min(vi, (unsigned)__shfl_xor_sync(0xFFFFFFFFu, vi, o));
-  const int owner = (int)(vi % G), kstar = (int)(vi / G);
-  int e = 0;
-  if (gl == owner && vi != 0xFFFFFFFFu) {
-    uint4 sel = v[0];
-#pragma unroll
-    for (int k = 1; k < NV; ++k)
-      if (k == kstar) sel = v[k];
-    e = vec_first_eq<BF16>(sel, m);
-  }
-  e = __shfl_sync(0xFFFFFFFFu, e, owner, G);
-  const unsigned am = vi * VE + (unsigned)e;
+  // every lane of the group reads the same vector (one broadcast transaction);
+  // an invalid row (no match) reads vector 0 and is discarded by write_row
+  const uint4 xv = __ldg(rowp + (vi < (unsigned)a.nvec ? vi : 0u));
+#endif
 
   // 3. exponentials with the common max: a = (x - m) * c, x - m formed exactly
   //    (FADD2, then FMUL2: one rounding, so the 1e-5 tolerance holds at T = 0.05)
   f2_t s2 = f2(0.f, 0.f), w2 = f2(0.f, 0.f);
   const bool valid = (m < INFINITY) && (m > -INFINITY);
-  if (valid) {
+#ifdef HS_EXP_NOEXP
+  if (valid) s2 = f2(1.f, 0.f);
+  if (false) {
+#else
+  {   // unconditional: an invalid row's sums are discarded by write_row
+#endif
     const uint32_t cw = ENTROPY && BF16 ? entropy_clamp_word(m, c) : 0u;
     const f2_t m2 = f2(m, m);
 #pragma unroll
@@ -309,9 +364,16 @@ __device__ __forceinline__ void group_reduce_row(const ConfArgs& a, const uint4 
     s += __shfl_xor_sync(0xFFFFFFFFu, s, o);
     if (ENTROPY) w += __shfl_xor_sync(0xFFFFFFFFu, w, o);
   }
+#ifndef HS_EXP_NOARGMAX
+  int e = BF16 ? vec_first_eq_bf16n(xv, mb2) : vec_first_eq<false>(xv, m);
+  if (anyslow) {
+    if (slow) e = vec_first_eq<true>(xv, m);
+  }
+  const unsigned am = vi * VE + (unsigned)e;
+#endif
   if (active && gl == 0) {
     RowOut r{m, s, w, am, 1.0f};
-    write_row(a, row, src, r);
+    write_row(a, row, lab, r);
   }
 }
 
@@ -370,6 +432,7 @@ __global__ void __launch_bounds__(256, (NV <= 8 ? 2 : 1)) conf_warp_kernel(const
   RowSrc rA = locate(a, actA ? rowA : 0), rB = rA;   // inactive groups read a valid row
   group_load_row<BF16, NV, G, FULL>(A, reinterpret_cast<const uint4*>(rA.base + rA.src * a.row_bytes),
                                     gl, nvec);
+  int32_t labA = fetch_label(a, rA), labB = 0;
   int64_t rowB = rowA + stride;
   int64_t fB = fetch_index(a, rowB < rows ? rowB : 0);
   while (true) {
@@ -381,19 +444,128 @@ __global__ void __launch_bounds__(256, (NV <= 8 ? 2 : 1)) conf_warp_kernel(const
       rB = locate_with(a, actB ? rowB : 0, actB ? fB : fetch_index(a, 0));
       group_load_row<BF16, NV, G, FULL>(B, reinterpret_cast<const uint4*>(rB.base + rB.src * a.row_bytes),
                                         gl, nvec);
+      labB = fetch_label(a, rB);
       fC = fetch_index(a, rowC < rows ? rowC : 0);
     }
     if (a.tail) group_mask_tail<BF16, NV, G>(A, gl, nvec, a.tail);
-    group_reduce_row<BF16, ENTROPY, NV, G>(a, A, actA, rowA, rA.src, gl, rA.c);
+    group_reduce_row<BF16, ENTROPY, NV, G>(a, A, actA, rowA, rA.src, gl, rA.c,
+                                           reinterpret_cast<const uint4*>(rA.base + rA.src * a.row_bytes),
+                                           labA);
     if (!anyB) break;
 #pragma unroll
     for (int k = 0; k < NV; ++k) A[k] = B[k];
     rowA = rowB;
     actA = actB;
     rA = rB;
+    labA = labB;
     rowB = rowC;
     fB = fC;
   }
+}
+
+// ---------------------------------------------------------------------------
+// K1a (async): the same grouped reduction, but the next row is prefetched with
+// per-lane cp.async (16 B, L2-only) into a per-warp shared-memory double
+// buffer instead of a second register set.  Each lane copies exactly the
+// vectors it will reduce, so its own cp.async.wait_group is the only
+// synchronisation (no barrier, no cross-lane hand-off).  Freeing the 32
+// prefetch registers lets three CTAs (24 warps) share an SM, and the register
+// copy B -> A disappears.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool pred) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %2, 0;\n\t"
+      "@p cp.async.cg.shared.global [%0], [%1], 16;\n\t}"
+      ::"r"(dst), "l"(src), "r"((int)pred) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+template <int NV, int G, bool FULL>
+__device__ __forceinline__ void group_prefetch_row(uint32_t sdst, const uint4* p, int gl, int nvec) {
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    const int vi = k * G + gl;
+    cp_async16(sdst + (uint32_t)(k * G * 16), p + vi, (FULL && k < NV - 1) || vi < nvec);
+  }
+}
+
+template <bool BF16, int NV, int G, bool FULL>
+__device__ __forceinline__ void group_lds_row(uint4 (&v)[NV], uint32_t ssrc, int gl, int nvec) {
+  const uint32_t f = BF16 ? kBf16NegInf2 : kF32NegInf;
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    const int vi = k * G + gl;
+    uint4 r = make_uint4(f, f, f, f);
+    if ((FULL && k < NV - 1) || vi < nvec)
+      asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                   : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "r"(ssrc + (uint32_t)(k * G * 16)));
+    v[k] = r;
+  }
+}
+
+constexpr int kAsyncThreads = 256;
+template <int NV, int G>
+constexpr int async_smem_bytes() { return (kAsyncThreads / 32) * 2 * (32 / G) * G * NV * 16; }
+
+template <bool BF16, bool ENTROPY, int NV, int G, bool FULL>
+__global__ void __launch_bounds__(kAsyncThreads, 3) conf_async_kernel(const ConfArgs a) {
+  pdl_start();
+  extern __shared__ __align__(16) unsigned char smem[];
+  constexpr int RPW = 32 / G;
+  constexpr uint32_t ROWB = G * NV * 16;              // one group's row slot
+  constexpr uint32_t STAGEB = RPW * ROWB;             // one warp's stage
+  const int lane = threadIdx.x & 31, gl = lane % G, grp = lane / G, warp = threadIdx.x >> 5;
+  const int64_t stride = (((int64_t)gridDim.x * blockDim.x) >> 5) * RPW;
+  const int64_t rows = live_rows(a);
+  const int nvec = a.nvec;
+  const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (w0 * RPW >= rows) return;
+  // lane gl's vector k of stage st sits at base + st*STAGEB + grp*ROWB + k*G*16 + gl*16:
+  // a quarter-warp reads 128 contiguous bytes (conflict-free LDS.128)
+  const uint32_t sbase = smem_u32(smem) + (uint32_t)warp * 2u * STAGEB + (uint32_t)grp * ROWB +
+                         (uint32_t)gl * 16u;
+  int64_t rowA = w0 * RPW + grp;
+  bool actA = rowA < rows;
+  RowSrc rA = locate(a, actA ? rowA : 0);
+  group_prefetch_row<NV, G, FULL>(sbase, reinterpret_cast<const uint4*>(rA.base + rA.src * a.row_bytes),
+                                  gl, nvec);
+  cp_async_commit();
+  int32_t labA = fetch_label(a, rA), labB = 0;
+  int64_t rowB = rowA + stride;
+  int64_t fB = fetch_index(a, rowB < rows ? rowB : 0);
+  uint4 A[NV];
+  for (int it = 0;; ++it) {
+    const bool anyB = (rowB - grp) < rows;
+    const bool actB = rowB < rows;
+    const int64_t rowC = rowB + stride;
+    int64_t fC = 0;
+    RowSrc rB = rA;
+    if (anyB) {
+      rB = locate_with(a, actB ? rowB : 0, actB ? fB : fetch_index(a, 0));
+      group_prefetch_row<NV, G, FULL>(sbase + (uint32_t)((it + 1) & 1) * STAGEB,
+                                      reinterpret_cast<const uint4*>(rB.base + rB.src * a.row_bytes),
+                                      gl, nvec);
+      labB = fetch_label(a, rB);
+      fC = fetch_index(a, rowC < rows ? rowC : 0);
+    }
+    cp_async_commit();
+    cp_async_wait<1>();        // this lane's copies of row A have landed
+    group_lds_row<BF16, NV, G, FULL>(A, sbase + (uint32_t)(it & 1) * STAGEB, gl, nvec);
+    if (a.tail) group_mask_tail<BF16, NV, G>(A, gl, nvec, a.tail);
+    group_reduce_row<BF16, ENTROPY, NV, G>(a, A, actA, rowA, rA.src, gl, rA.c,
+                                           reinterpret_cast<const uint4*>(rA.base + rA.src * a.row_bytes),
+                                           labA);
+    if (!anyB) break;
+    rowA = rowB;
+    actA = actB;
+    rA = rB;
+    labA = labB;
+    rowB = rowC;
+    fB = fC;
+  }
+  cp_async_wait<0>();
 }
 
 // ---------------------------------------------------------------------------
@@ -482,7 +654,10 @@ __global__ void __launch_bounds__(32 * (NCW + 1), 1) conf_tma_kernel(const ConfA
       v[k] = vi < lim ? lds128(srow + (size_t)vi * 16) : make_uint4(f, f, f, f);
     }
     if (a.tail) group_mask_tail<BF16, NV, G>(v, gl, nvec, a.tail);
-    group_reduce_row<BF16, ENTROPY, NV, G>(a, v, act, row, act ? src_row<L1>(a, row) : 0, gl, a.c);
+    const int64_t src = act ? src_row<L1>(a, row) : 0;
+    group_reduce_row<BF16, ENTROPY, NV, G>(a, v, act, row, src, gl, a.c,
+                                           reinterpret_cast<const uint4*>((const char*)a.logits + src * a.row_bytes),
+                                           a.labels ? __ldg(a.labels + src) : 0);
     // every lane has consumed its staged vectors (the row max read them all)
     __syncwarp();
     if (lane == 0) mbar_arrive(&ring->empty[st]);
@@ -641,7 +816,7 @@ __global__ void __launch_bounds__(NT) conf_cta_kernel(const ConfArgs a) {
           AM = min(AM, sh_am[i]);
         }
         RowOut r{M, S, W, AM, 1.0f};
-        write_row(a, rowA, rsA.src, r);
+        write_row(a, rowA, a.labels ? __ldg(a.labels + rsA.src) : 0, r);
       }
       __syncthreads();
       m = -INFINITY;
@@ -712,8 +887,32 @@ cudaError_t launch_warp_l(const ConfArgs& a, int64_t rows, cudaStream_t s) {
   return launch_pdl(k, dim3(grid), dim3(256), 0, s, a);
 }
 
+template <bool BF16, bool ENTROPY, int NV, int G, bool FULL>
+cudaError_t launch_async_l(const ConfArgs& a, int64_t rows, cudaStream_t s) {
+  auto k = conf_async_kernel<BF16, ENTROPY, NV, G, FULL>;
+  constexpr int smem = async_smem_bytes<NV, G>();
+  static const int occ = [&] {
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    int b = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k, kAsyncThreads, smem);
+    return b > 0 ? b : 1;
+  }();
+  constexpr int RPB = (kAsyncThreads / 32) * (32 / G);
+  const int64_t want = (rows + RPB - 1) / RPB;
+  const int64_t cap = (int64_t)num_sms() * occ;
+  const int grid = (int)(want < cap ? (want > 0 ? want : 1) : cap);
+  return launch_pdl(k, dim3(grid), dim3(kAsyncThreads), smem, s, a);
+}
+
+int conf_impl();
+
 template <bool BF16, bool ENTROPY, int NV, int G>
 cudaError_t launch_warp(const ConfArgs& a, int64_t rows, cudaStream_t s) {
+  if constexpr (NV <= 8) {   // the async variant holds one row set in registers (<= 80 regs)
+    if (conf_impl() == 2)
+      return (NV - 1) * G <= a.nvec ? launch_async_l<BF16, ENTROPY, NV, G, true>(a, rows, s)
+                                    : launch_async_l<BF16, ENTROPY, NV, G, false>(a, rows, s);
+  }
 #ifdef HS_NO_FULL
   return launch_warp_l<BF16, ENTROPY, NV, G, false>(a, rows, s);
 #endif
@@ -755,10 +954,14 @@ cudaError_t launch_tma(const ConfArgs& a, int64_t rows, cudaStream_t s) {
                   : launch_tma_l<BF16, ENTROPY, NV, G, NCW, S, false>(a, rows, s);
 }
 
-int conf_impl() {   // 0 = LDG (registers, default), 1 = TMA ring
+// 2 = cp.async double buffer (default; A/B on two boxes: +2.6 % and +9.6 % K1
+// bandwidth over 0), 0 = LDG register double buffer, 1 = TMA bulk ring
+int conf_impl() {
   static const int v = [] {
     const char* e = getenv("HS_CONF_IMPL");
-    return (e && strcmp(e, "tma") == 0) ? 1 : 0;
+    if (e && strcmp(e, "tma") == 0) return 1;
+    if (e && strcmp(e, "ldg") == 0) return 0;
+    return 2;
   }();
   return v;
 }

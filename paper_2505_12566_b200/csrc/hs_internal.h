@@ -58,6 +58,8 @@ struct ConfArgs {
   // read batch b's logits bptr[b] at temperature factor bc[b]
   int nbatch;              // 1 = plain call (logits, c)
   int64_t brows;           // n * L rows per batch
+  uint64_t bmagic;         // ceil(2^64 / brows): row / brows = umul64hi(row, bmagic) for
+                           // row < 2^32 (brows >= 2; brows == 1 -> 0, quotient = row)
   const void* bptr[kMaxBatch];
   float bc[kMaxBatch];
 };
@@ -69,8 +71,8 @@ const char* confidence_path(int64_t nvec);
 
 // ---- K3 / K4 ---------------------------------------------------------------
 constexpr int kCompactThreads = 256;
-constexpr int kCompactItems = 16;
-constexpr int kCompactTile = kCompactThreads * kCompactItems;   // 4096 items per tile
+constexpr int kCompactItems = 8;
+constexpr int kCompactTile = kCompactThreads * kCompactItems;   // 2048 items per tile
 
 struct CompactWs {          // zero-filled before first use; then self-maintaining
   unsigned int epoch;       // launch counter tagging the tile descriptors

@@ -37,8 +37,9 @@ def test_header_compiles_as_c(tmp_path):
 def test_workspace_queries_are_pure(libhs):
     lib = libhs.lib()
     assert lib.hs_route_compact_workspace(0) > 0
-    assert lib.hs_route_compact_workspace(4096) == lib.hs_route_compact_workspace(1)
-    assert lib.hs_route_compact_workspace(4097) == lib.hs_route_compact_workspace(4096) + 8
+    # one 8-byte look-back descriptor per 2,048-item tile
+    assert lib.hs_route_compact_workspace(2048) == lib.hs_route_compact_workspace(1)
+    assert lib.hs_route_compact_workspace(2049) == lib.hs_route_compact_workspace(2048) + 8
     assert lib.hs_confidence_workspace(100, 1) == 0
     assert lib.hs_confidence_workspace(100, 64) >= 100 * 64 * 5
     assert lib.hs_calibrate_workspace(5, 12) >= 3 * (4096 + 2) * 4

@@ -196,7 +196,7 @@ def _route_ref(conf32: np.ndarray, t: float, is_last: bool):
     return oracle.route(conf32.astype(np.float64), float(np.float32(t)), is_last)
 
 
-@pytest.mark.parametrize("n", [0, 1, 31, 4095, 4096, 4097, 12289, 262144])
+@pytest.mark.parametrize("n", [0, 1, 31, 2047, 2048, 2049, 4095, 4096, 4097, 12289, 262144])
 def test_route_compact_exact(hs, n):
     rng = np.random.default_rng(n)
     c = rng.uniform(size=n).astype(np.float32)
@@ -227,6 +227,40 @@ def test_route_compact_exact(hs, n):
     # the workspace is reused across calls without a memset (epoch-tagged descriptors)
     epoch = int(ws[:4].view(torch.int32).item())
     assert epoch == (5 if n > 0 else 0)
+
+
+@pytest.mark.parametrize("n", [1, 7, 8, 9, 2047, 2048, 2049, 6151, 262144, 300001])
+@pytest.mark.parametrize("offset", [0, 1])
+def test_route_compact_fast_path(hs, n, offset):
+    """The plain cascade split (pred_len = 1 or no pred): 8 consecutive items per
+    thread, 128-bit loads when aligned (offset 0) and scalar loads otherwise
+    (offset 1 shifts every array by one element), staged coalesced stores."""
+    rng = np.random.default_rng(1000 + n + offset)
+    c = rng.uniform(size=n + offset).astype(np.float32)
+    c[rng.uniform(size=n + offset) < 0.02] = np.nan
+    c[rng.uniform(size=n + offset) < 0.05] = np.float32(0.5)
+    ids_all = torch.from_numpy(rng.integers(0, 1 << 40, size=n + offset)).to(dev())
+    pred_all = torch.from_numpy(rng.integers(0, 1000, size=n + offset).astype(np.int32)).to(dev())
+    cd = torch.from_numpy(c).to(dev())[offset:]
+    ids, pred = ids_all[offset:], pred_all[offset:]
+    ch = c[offset:]
+    ws = hs.workspace(hs.lib().hs_route_compact_workspace(n), dev())
+    for t, last, with_ids, with_pred in ((0.5, False, True, True), (0.0, False, False, True),
+                                         (math.inf, False, True, False), (0.25, True, True, True),
+                                         (0.9, False, False, False)):
+        o = hs.route_compact(cd, t, is_last=last, ids=ids if with_ids else None,
+                             pred=pred if with_pred else None, pred_len=1, ws=ws)
+        torch.cuda.synchronize()
+        acc, dfr = _route_ref(ch, t, last)
+        na, nd = o["counts"].cpu().tolist()
+        assert (na, nd) == (len(acc), len(dfr)), (t, last)
+        idh = ids.cpu().numpy() if with_ids else np.arange(n)
+        assert np.array_equal(o["acc_ids"][:na].cpu().numpy(), idh[acc])
+        assert np.array_equal(o["def_ids"][:nd].cpu().numpy(), idh[dfr])
+        assert np.array_equal(o["def_pos"][:nd].cpu().numpy(), dfr)
+        np.testing.assert_array_equal(o["acc_conf"][:na].cpu().numpy(), ch[acc])
+        if with_pred:
+            assert np.array_equal(o["acc_pred"][:na].cpu().numpy(), pred.cpu().numpy()[acc])
 
 
 def test_route_device_threshold_and_count(hs):

@@ -7,10 +7,9 @@ sys.path.insert(0, ROOT)
 from paper_2505_12566_b200 import _build  # noqa: E402
 
 VARIANTS = {
-    "lb2": ["HS_WARP_MINB=2"],          # G=8 NV=16 capped at 128 regs (16 warps/SM)
-    "g16": ["HS_G16"],                  # G=16 NV=8 (~100 regs, 16 warps/SM)
-    "g16lb2": ["HS_G16", "HS_WARP_MINB=2"],
-    "ctrace": ["HS_CALIB_TRACE"],
+    "ctrace": ["HS_CALIB_TRACE"],        # globaltimer trace of the calibration kernels
+    "noargmax": ["HS_EXP_NOARGMAX"],     # upper bounds: K1 without the argmax ...
+    "noexp": ["HS_EXP_NOEXP"],           # ... or without the exponential pass
 }
 
 if __name__ == "__main__":
