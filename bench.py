@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-overlap", action="store_true",
+                    help="run routing stage 1 strictly after the calibration (no PDL overlap)")
     ap.add_argument("--force-dist", action="store_true",
                     help="initialise NCCL even at one GPU (exercises the sharded calibration path)")
     ap.add_argument("--placement", default="local", choices=["local", "balanced"],
@@ -230,8 +232,10 @@ def run_ours(args, world, rank, local):
     ev = (timing_event(), timing_event())
 
     def step():
-        router.calibrate(val, labels)
-        router.route(route, payload=payload, time_stage0=ev)
+        # K1 on the validation shard is the timed launch (events around it); the
+        # routing stage-1 K1 then runs next to the latency-bound calibration
+        router.calibrate(val, labels, time_val=ev)
+        router.route(route, payload=payload, overlap_first=not args.no_overlap)
 
     stream = torch.cuda.Stream(device=dev)
     torch.cuda.synchronize()
@@ -300,8 +304,9 @@ def run_ours(args, world, rank, local):
     n_all = fam.n * world
     value = n_all / (ms / 1e3)
     peak, peak_src = peaks()
-    # dominant kernel: stage-1 confidence over this rank's batch: n rows x (row bytes + 8 B out)
-    k_bytes = fam.n * (row_b + 8)
+    # dominant kernel: K1 over the validation shard, all K stages in one launch:
+    # per token row, logits + conf (4 B) + argmax (4 B) + label (4 B) + correct (1 B)
+    k_bytes = fam.K * fam.n_val * fam.L * (row_b + 13)
     achieved = k_bytes / (kernel_ms / 1e3) / 1e9
     e2e = run_e2e(args, fam, router, route, val, labels, payload, stream, world) if args.e2e_steps > 0 else None
     line = {
@@ -320,8 +325,10 @@ def run_ours(args, world, rank, local):
         "reach": reach, "thresholds": router.cal["t"].cpu().tolist(), "status": st,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": None,
-                     "kernel": ("conf_warp_kernel" if fam.C * fam.elt_bytes <= 8192 else "conf_cta_kernel")
-                     + " (stage-1 routing confidence, K1)",
+                     "kernel": ("conf_async_kernel" if fam.C * fam.elt_bytes <= 2048 else
+                                "conf_warp_kernel" if fam.C * fam.elt_bytes <= 8192 else "conf_cta_kernel")
+                     + f" (K1 on the validation shard: {fam.K} stages x {fam.n_val} items in one launch"
+                     + (", + K2 sequence reduce" if fam.L > 1 else "") + ")",
                      "bytes_per_launch": k_bytes, "avg_launch_ms": kernel_ms,
                      "peak_source": peak_src},
         "e2e": e2e, "gpu_launches": gpu_launches, "clocks": clocks,

@@ -194,6 +194,26 @@ hs_status_t hs_cascade_step(int32_t stage, int32_t n_stages, const void* logits,
                             int64_t* acc_ids, float* acc_conf, int32_t* acc_pred,
                             int64_t* next_ids, void* next_payload, int64_t* d_counts, void* ws,
                             size_t ws_bytes, uint32_t* d_status, hs_stream_t stream);
+/* hs_cascade_step_ex: hs_cascade_step plus flags.
+ *   HS_STEP_OVERLAP_PREVIOUS: the stage's confidence kernel starts while the
+ *   previous libhs kernel on the stream is still running (programmatic
+ *   dependent launch without the early wait), e.g. routing stage 0 next to the
+ *   latency-bound calibration it does not depend on.  The CALLER guarantees that
+ *   the previous libhs call neither writes this step's inputs (logits,
+ *   row_index, d_n, ids, payload) nor reads or writes this step's workspace.
+ *   Stream order is otherwise preserved: the step's kernels complete after the
+ *   previous kernel, and the threshold test waits for it (d_threshold may be
+ *   produced by it).  Unknown flag bits -> HS_ERR_INVALID_ARGUMENT. */
+#define HS_STEP_OVERLAP_PREVIOUS 1u
+hs_status_t hs_cascade_step_ex(int32_t stage, int32_t n_stages, const void* logits, hs_dtype_t dtype,
+                               int64_t n, int32_t seq_len, int64_t n_classes, int64_t row_stride,
+                               const int64_t* row_index, const int64_t* d_n, float temperature,
+                               hs_conf_kind_t kind, hs_seq_reduce_t reduce, float threshold,
+                               const float* d_threshold, const int64_t* ids, const void* payload,
+                               int64_t payload_row_bytes, int64_t* acc_ids, float* acc_conf,
+                               int32_t* acc_pred, int64_t* next_ids, void* next_payload,
+                               int64_t* d_counts, void* ws, size_t ws_bytes, uint32_t* d_status,
+                               uint32_t flags, hs_stream_t stream);
 
 /* ------------------------------------------------------------------------ */
 /* Offline Accuracy-Preserving threshold calibration (Alg. 1, AP).  */

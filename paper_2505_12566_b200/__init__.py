@@ -22,6 +22,7 @@ from ._abi import HsError, lib
 
 MAXPROB, MAXPROB_SQ, ENTROPY = 0, 1, 2
 SEQ_NONE, SEQ_MIN, SEQ_MEAN = 0, 1, 2
+HS_STEP_OVERLAP_PREVIOUS = 1     # hs_cascade_step_ex flag (include/hs.h)
 _KINDS = {"maxprob": MAXPROB, "maxprob_sq": MAXPROB_SQ, "entropy": ENTROPY}
 _REDUCES = {"none": SEQ_NONE, "min": SEQ_MIN, "mean": SEQ_MEAN}
 STATUS_NONFINITE = 1
@@ -210,8 +211,13 @@ def cascade_step(stage: int, n_stages: int, logits: torch.Tensor, threshold, *, 
                  d_n: torch.Tensor | None = None, ids: torch.Tensor | None = None,
                  payload: torch.Tensor | None = None, payload_row_bytes: int = 0,
                  out: dict | None = None, ws: torch.Tensor | None = None,
-                 status: torch.Tensor | None = None, stream=None) -> dict:
-    """One model m_k of the cascade: confidence -> threshold -> compaction/gather."""
+                 status: torch.Tensor | None = None, overlap_previous: bool = False,
+                 stream=None) -> dict:
+    """One model m_k of the cascade: confidence -> threshold -> compaction/gather.
+
+    ``overlap_previous`` (HS_STEP_OVERLAP_PREVIOUS): the confidence kernel runs
+    next to the previous libhs kernel on the stream; the caller guarantees that
+    kernel does not touch this step's inputs or workspace."""
     _check_cuda(logits, row_index, d_n, ids, payload, status)
     C = int(n_classes or logits.shape[1])
     dev = logits.device
@@ -234,12 +240,13 @@ def cascade_step(stage: int, n_stages: int, logits: torch.Tensor, threshold, *, 
         ws = workspace(need, dev)
     d_thr = threshold if isinstance(threshold, torch.Tensor) else None
     thr = 0.0 if d_thr is not None else float(threshold)
-    _abi.call("hs_cascade_step", int(stage), int(n_stages), _p(logits), _dtype_code(logits), int(n),
-              int(seq_len), C, int(logits.stride(0)), _p(row_index), _p(d_n), float(temperature),
-              _kind(kind), _reduce(reduce), thr, _p(d_thr), _p(ids), _p(payload),
+    _abi.call("hs_cascade_step_ex", int(stage), int(n_stages), _p(logits), _dtype_code(logits),
+              int(n), int(seq_len), C, int(logits.stride(0)), _p(row_index), _p(d_n),
+              float(temperature), _kind(kind), _reduce(reduce), thr, _p(d_thr), _p(ids), _p(payload),
               int(payload_row_bytes), _p(out["acc_ids"]), _p(out["acc_conf"]), _p(out["acc_pred"]),
               _p(out["next_ids"]), _p(out.get("next_payload")), _p(out["counts"]), _p(ws),
-              ws.numel(), _p(status), _stream(stream))
+              ws.numel(), _p(status), HS_STEP_OVERLAP_PREVIOUS if overlap_previous else 0,
+              _stream(stream))
     return out
 
 
@@ -361,7 +368,10 @@ class Cascade:
         self.ws = workspace(lib().hs_cascade_step_workspace(n_cap, L), dev)
 
     def route(self, logits: list, thresholds, *, n: int | None = None, ids=None, payload=None,
-              by_id: bool = True, stream=None):
+              by_id: bool = True, overlap_first: bool = False, stream=None):
+        """Run the K stages.  ``overlap_first``: stage 1's confidence kernel runs
+        next to the previous libhs kernel (e.g. the calibration it does not
+        depend on); see hs_cascade_step_ex / HS_STEP_OVERLAP_PREVIOUS."""
         n = self.n_cap if n is None else int(n)
         d_thr = thresholds if isinstance(thresholds, torch.Tensor) else None
         for k, s in enumerate(self.stages):
@@ -376,7 +386,8 @@ class Cascade:
                          temperature=s.temperature, kind=s.kind, reduce=s.reduce,
                          row_index=row_index, d_n=prev["counts"][1:2] if k else None,
                          ids=cur_ids, payload=cur_payload, payload_row_bytes=self.P,
-                         out=self.outs[k], ws=self.ws, status=self.status, stream=stream)
+                         out=self.outs[k], ws=self.ws, status=self.status,
+                         overlap_previous=overlap_first and k == 0, stream=stream)
         return self
 
     def results(self):

@@ -373,8 +373,10 @@ hs_status_t hs_skip_route(const float* conf, int64_t n, const int64_t* d_n, floa
 
 // cascade-step workspace: [compact ws][conf f32 n][argmax i32 n*L][def_pos i64 n][conf ws]
 static size_t step_layout(int64_t n, int32_t L, size_t* o_conf, size_t* o_am, size_t* o_pos,
-                          size_t* o_cws) {
+                          size_t* o_cws, size_t* o_tick = nullptr) {
   size_t off = align_up(hs::compact_ws_bytes(n), 256);
+  if (o_tick) *o_tick = off;           // K1 row-group ticket + finished-CTA count
+  off += 256;
   *o_conf = off;
   off = align_up(off + (size_t)n * sizeof(float), 256);
   *o_am = off;
@@ -399,6 +401,23 @@ hs_status_t hs_cascade_step(int32_t stage, int32_t n_stages, const void* logits,
                             int64_t* acc_ids, float* acc_conf, int32_t* acc_pred,
                             int64_t* next_ids, void* next_payload, int64_t* d_counts, void* ws,
                             size_t ws_bytes, uint32_t* d_status, hs_stream_t stream) {
+  return hs_cascade_step_ex(stage, n_stages, logits, dtype, n, seq_len, n_classes, row_stride,
+                            row_index, d_n, temperature, kind, reduce, threshold, d_threshold, ids,
+                            payload, payload_row_bytes, acc_ids, acc_conf, acc_pred, next_ids,
+                            next_payload, d_counts, ws, ws_bytes, d_status, 0u, stream);
+}
+
+hs_status_t hs_cascade_step_ex(int32_t stage, int32_t n_stages, const void* logits, hs_dtype_t dtype,
+                               int64_t n, int32_t seq_len, int64_t n_classes, int64_t row_stride,
+                               const int64_t* row_index, const int64_t* d_n, float temperature,
+                               hs_conf_kind_t kind, hs_seq_reduce_t reduce, float threshold,
+                               const float* d_threshold, const int64_t* ids, const void* payload,
+                               int64_t payload_row_bytes, int64_t* acc_ids, float* acc_conf,
+                               int32_t* acc_pred, int64_t* next_ids, void* next_payload,
+                               int64_t* d_counts, void* ws, size_t ws_bytes, uint32_t* d_status,
+                               uint32_t flags, hs_stream_t stream) {
+  if (flags & ~(uint32_t)HS_STEP_OVERLAP_PREVIOUS)
+    return fail(HS_ERR_INVALID_ARGUMENT, "unknown flags 0x%x", flags);
   if (n_stages < 1 || stage < 0 || stage >= n_stages)
     return fail(HS_ERR_INVALID_ARGUMENT, "stage %d outside 0..n_stages-1 (%d)", stage, n_stages);
   if (n >= (int64_t(1) << 30)) return fail(HS_ERR_INVALID_ARGUMENT, "n must be < 2^30 per call");
@@ -413,8 +432,8 @@ hs_status_t hs_cascade_step(int32_t stage, int32_t n_stages, const void* logits,
   if (next_payload && (!payload || payload_row_bytes <= 0 || (payload_row_bytes & 15) ||
                        !aligned16(payload) || !aligned16(next_payload)))
     return fail(HS_ERR_INVALID_ARGUMENT, "payload rows must be 16-byte aligned multiples of 16 bytes");
-  size_t o_conf, o_am, o_pos, o_cws;
-  const size_t need = step_layout(n, seq_len, &o_conf, &o_am, &o_pos, &o_cws);
+  size_t o_conf, o_am, o_pos, o_cws, o_tick;
+  const size_t need = step_layout(n, seq_len, &o_conf, &o_am, &o_pos, &o_cws, &o_tick);
   if (!ws || ws_bytes < need) return fail(HS_ERR_WORKSPACE_TOO_SMALL, "workspace %zu < %zu", ws_bytes, need);
   cudaStream_t s = (cudaStream_t)stream;
   char* w = reinterpret_cast<char*>(ws);
@@ -425,8 +444,16 @@ hs_status_t hs_cascade_step(int32_t stage, int32_t n_stages, const void* logits,
     st = cuda_check(cudaMemsetAsync(d_counts, 0, 2 * sizeof(int64_t), s), "memset counts");
     return st;
   }
-  st = run_confidence(logits, dtype, n, seq_len, n_classes, row_stride, row_index, d_n, temperature,
-                      kind, reduce, conf, am, nullptr, nullptr, w + o_cws, d_status, s);
+  {
+    hs::ConfArgs a = make_conf_args(logits, dtype, n, seq_len, n_classes, row_stride, row_index, d_n,
+                                    temperature, kind);
+    if (flags & HS_STEP_OVERLAP_PREVIOUS) {
+      // CTAs that start late (SMs held by the previous kernel) take fewer rows
+      a.ticket = reinterpret_cast<unsigned int*>(w + o_tick);
+      a.late_wait = 1;
+    }
+    st = run_confidence_args(a, dtype, reduce, conf, am, nullptr, nullptr, w + o_cws, d_status, s);
+  }
   if (st != HS_OK) return st;
   return route_compact_impl(conf, n, d_n, threshold, d_threshold, is_last, ids, am, seq_len, acc_ids, acc_conf,
                             acc_pred, next_ids, next_payload ? pos : nullptr, payload,

@@ -641,6 +641,7 @@ __global__ void __launch_bounds__(kResidentThreads, 1) calib_resident_kernel(
   grid.sync();
   HS_TR("init");
   const int mup = (m + 31) & ~31;
+  const bool aggregate = q < 8;      // block-uniform
   for (int k = 0; k < K - 1; ++k) {
     unsigned long long* cur = hist3 + (size_t)(k % 3) * nb;
     unsigned long long* nxt = hist3 + (size_t)((k + 1) % 3) * nb;
@@ -658,6 +659,15 @@ __global__ void __launch_bounds__(kResidentThreads, 1) calib_resident_kernel(
           okK = (ok >> (K - 1)) & 1u;
         }
       }
+      if (!aggregate) {            // many bins: lanes rarely share one
+        if (key >= 0) {
+          atomicAdd(&sh[key], 1u);
+          if (okk) atomicAdd(&sh[nb + key], 1u);
+          if (okK) atomicAdd(&sh[2 * nb + key], 1u);
+        }
+        continue;
+      }
+      // few bins: lanes with the same bin add once, through their leader
       const unsigned peers = __match_any_sync(0xFFFFFFFFu, key);
       const unsigned bk = __ballot_sync(0xFFFFFFFFu, okk);
       const unsigned bK = __ballot_sync(0xFFFFFFFFu, okK);

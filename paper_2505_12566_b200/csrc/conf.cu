@@ -120,6 +120,32 @@ __device__ __forceinline__ RowSrc locate_with(const ConfArgs& a, int64_t row, in
   if (a.row_index) r.src = a.L == 1 ? fetched : fetched * a.L + local % a.L;
   return r;
 }
+// Batched launches: the rows of one group only increase, so the group keeps
+// the bounds of its current batch and re-derives them only when a row leaves
+// them (at most nbatch - 1 times, plus the clamped rows of inactive groups).
+struct BatchCur {
+  uint32_t start, end;     // batched rows < 2^32
+  const char* base;
+  float c;
+};
+__device__ __forceinline__ BatchCur cur_init(const ConfArgs& a) {
+  return BatchCur{0u, a.nbatch > 1 ? 0u : 0xFFFFFFFFu, (const char*)a.logits, a.c};
+}
+__device__ __forceinline__ RowSrc locate_cur(const ConfArgs& a, BatchCur& k, int64_t row,
+                                             int64_t fetched) {
+  if ((uint32_t)row < k.start || (uint32_t)row >= k.end) {
+    int b;
+    const int64_t local = batch_local(a, row, &b);
+    k.start = (uint32_t)(row - local);
+    k.end = k.start + (uint32_t)a.brows;
+    k.base = (const char*)a.bptr[b];
+    k.c = a.bc[b];
+  }
+  const int64_t local = row - (int64_t)k.start;
+  RowSrc r{k.base, k.c, local};
+  if (a.row_index) r.src = a.L == 1 ? fetched : fetched * a.L + local % a.L;
+  return r;
+}
 __device__ __forceinline__ RowSrc locate(const ConfArgs& a, int64_t row) {
   return locate_with(a, row, fetch_index(a, row));
 }
@@ -282,7 +308,7 @@ __device__ __forceinline__ int vec_first_eq_bf16n(const uint4& x, uint32_t mb2) 
 
 template <bool BF16, bool ENTROPY, int NV, int G>
 __device__ __forceinline__ void group_reduce_row(const ConfArgs& a, const uint4 (&v)[NV],
-                                                 bool active, int64_t row, int64_t src, int gl,
+                                                 bool active, int64_t row, int gl,
                                                  float c, const uint4* rowp, int32_t lab) {
   constexpr int VE = BF16 ? 8 : 4;
   const f2_t c2 = f2(c, c);
@@ -448,7 +474,7 @@ __global__ void __launch_bounds__(256, (NV <= 8 ? 2 : 1)) conf_warp_kernel(const
       fC = fetch_index(a, rowC < rows ? rowC : 0);
     }
     if (a.tail) group_mask_tail<BF16, NV, G>(A, gl, nvec, a.tail);
-    group_reduce_row<BF16, ENTROPY, NV, G>(a, A, actA, rowA, rA.src, gl, rA.c,
+    group_reduce_row<BF16, ENTROPY, NV, G>(a, A, actA, rowA, gl, rA.c,
                                            reinterpret_cast<const uint4*>(rA.base + rA.src * a.row_bytes),
                                            labA);
     if (!anyB) break;
@@ -509,63 +535,105 @@ constexpr int kAsyncThreads = 256;
 template <int NV, int G>
 constexpr int async_smem_bytes() { return (kAsyncThreads / 32) * 2 * (32 / G) * G * NV * 16; }
 
-template <bool BF16, bool ENTROPY, int NV, int G, bool FULL>
+template <bool BF16, bool ENTROPY, int NV, int G, bool FULL, bool DYN>
 __global__ void __launch_bounds__(kAsyncThreads, 3) conf_async_kernel(const ConfArgs a) {
-  pdl_start();
+  if (a.late_wait) pdl_trigger(); else pdl_start();
   extern __shared__ __align__(16) unsigned char smem[];
   constexpr int RPW = 32 / G;
   constexpr uint32_t ROWB = G * NV * 16;              // one group's row slot
   constexpr uint32_t STAGEB = RPW * ROWB;             // one warp's stage
   const int lane = threadIdx.x & 31, gl = lane % G, grp = lane / G, warp = threadIdx.x >> 5;
-  const int64_t stride = (((int64_t)gridDim.x * blockDim.x) >> 5) * RPW;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t rows = live_rows(a);
   const int nvec = a.nvec;
-  const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (w0 * RPW >= rows) return;
-  // lane gl's vector k of stage st sits at base + st*STAGEB + grp*ROWB + k*G*16 + gl*16:
-  // a quarter-warp reads 128 contiguous bytes (conflict-free LDS.128)
-  const uint32_t sbase = smem_u32(smem) + (uint32_t)warp * 2u * STAGEB + (uint32_t)grp * ROWB +
-                         (uint32_t)gl * 16u;
-  int64_t rowA = w0 * RPW + grp;
-  bool actA = rowA < rows;
-  RowSrc rA = locate(a, actA ? rowA : 0);
-  group_prefetch_row<NV, G, FULL>(sbase, reinterpret_cast<const uint4*>(rA.base + rA.src * a.row_bytes),
-                                  gl, nvec);
-  cp_async_commit();
-  int32_t labA = fetch_label(a, rA), labB = 0;
-  int64_t rowB = rowA + stride;
-  int64_t fB = fetch_index(a, rowB < rows ? rowB : 0);
-  uint4 A[NV];
-  for (int it = 0;; ++it) {
-    const bool anyB = (rowB - grp) < rows;
-    const bool actB = rowB < rows;
-    const int64_t rowC = rowB + stride;
-    int64_t fC = 0;
-    RowSrc rB = rA;
-    if (anyB) {
-      rB = locate_with(a, actB ? rowB : 0, actB ? fB : fetch_index(a, 0));
-      group_prefetch_row<NV, G, FULL>(sbase + (uint32_t)((it + 1) & 1) * STAGEB,
-                                      reinterpret_cast<const uint4*>(rB.base + rB.src * a.row_bytes),
-                                      gl, nvec);
-      labB = fetch_label(a, rB);
-      fC = fetch_index(a, rowC < rows ? rowC : 0);
+  constexpr bool dyn = DYN;   // a.ticket != NULL
+  // row group g = rows g*RPW .. g*RPW + RPW-1: static (warp w takes w, w + nwarps,
+  // ...) or claimed from the ticket, so CTAs that start late (SMs still busy with
+  // the previous kernel) just take fewer groups
+  // dynamic claims come in chunks of kChunk groups per warp (one atomic per
+  // kChunk * RPW rows keeps the single ticket word off the critical path)
+  constexpr int kChunk = 8;
+  int64_t cnext = 0, cend = 0;
+  auto next_group = [&](int64_t g) -> int64_t {
+    if (!dyn) return g + nwarps;
+    if (cnext == cend) {
+      unsigned t = 0;
+      if (lane == 0) t = atomicAdd(a.ticket, (unsigned)kChunk);
+      cnext = (int64_t)__shfl_sync(0xFFFFFFFFu, t, 0);
+      cend = cnext + kChunk;
     }
+    return cnext++;
+  };
+  const int64_t g0 = dyn ? next_group(0) : ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (g0 * RPW < rows) {
+    // lane gl's vector k of stage st sits at base + st*STAGEB + grp*ROWB + k*G*16 + gl*16:
+    // a quarter-warp reads 128 contiguous bytes (conflict-free LDS.128)
+    const uint32_t sbase = smem_u32(smem) + (uint32_t)warp * 2u * STAGEB + (uint32_t)grp * ROWB +
+                           (uint32_t)gl * 16u;
+    BatchCur cur = cur_init(a);
+    // row A (being reduced) and row B (in flight) of this group: row pointer,
+    // temperature factor, label; row C's gathered index is fetched one pass ahead
+    int64_t rowA = g0 * RPW + grp;
+    bool actA = rowA < rows;
+    const uint4* pA;
+    float cA;
+    int32_t labA;
+    {
+      const RowSrc r = locate_cur(a, cur, actA ? rowA : 0, fetch_index(a, actA ? rowA : 0));
+      pA = reinterpret_cast<const uint4*>(r.base + r.src * a.row_bytes);
+      cA = r.c;
+      labA = fetch_label(a, r);
+    }
+    group_prefetch_row<NV, G, FULL>(sbase, pA, gl, nvec);
     cp_async_commit();
-    cp_async_wait<1>();        // this lane's copies of row A have landed
-    group_lds_row<BF16, NV, G, FULL>(A, sbase + (uint32_t)(it & 1) * STAGEB, gl, nvec);
-    if (a.tail) group_mask_tail<BF16, NV, G>(A, gl, nvec, a.tail);
-    group_reduce_row<BF16, ENTROPY, NV, G>(a, A, actA, rowA, rA.src, gl, rA.c,
-                                           reinterpret_cast<const uint4*>(rA.base + rA.src * a.row_bytes),
-                                           labA);
-    if (!anyB) break;
-    rowA = rowB;
-    actA = actB;
-    rA = rB;
-    labA = labB;
-    rowB = rowC;
-    fB = fC;
+    int64_t gB = next_group(g0);
+    int64_t fB = fetch_index(a, gB * RPW + grp < rows ? gB * RPW + grp : 0);
+    uint4 A[NV];
+    for (int it = 0;; ++it) {
+      const int64_t rowB = gB * RPW + grp;
+      const bool anyB = gB * RPW < rows;      // warp-uniform
+      const bool actB = rowB < rows;
+      int64_t gC = 0, fC = 0;
+      const uint4* pB = pA;
+      float cB = cA;
+      int32_t labB = 0;
+      if (anyB) {
+        const RowSrc r = locate_cur(a, cur, actB ? rowB : 0, actB ? fB : fetch_index(a, 0));
+        pB = reinterpret_cast<const uint4*>(r.base + r.src * a.row_bytes);
+        cB = r.c;
+        group_prefetch_row<NV, G, FULL>(sbase + (uint32_t)((it + 1) & 1) * STAGEB, pB, gl, nvec);
+        labB = fetch_label(a, r);
+        gC = next_group(gB);
+        const int64_t rowC = gC * RPW + grp;
+        fC = fetch_index(a, rowC < rows ? rowC : 0);
+      }
+      cp_async_commit();
+      cp_async_wait<1>();        // this lane's copies of row A have landed
+      group_lds_row<BF16, NV, G, FULL>(A, sbase + (uint32_t)(it & 1) * STAGEB, gl, nvec);
+      if (a.tail) group_mask_tail<BF16, NV, G>(A, gl, nvec, a.tail);
+      group_reduce_row<BF16, ENTROPY, NV, G>(a, A, actA, rowA, gl, cA, pA, labA);
+      if (!anyB) break;
+      rowA = rowB;
+      actA = actB;
+      pA = pB;
+      cA = cB;
+      labA = labB;
+      gB = gC;
+      fB = fC;
+    }
+    cp_async_wait<0>();
   }
-  cp_async_wait<0>();
+  if (dyn) {
+    __syncthreads();                 // every warp of this CTA is done claiming
+    if (threadIdx.x == 0) {
+      const unsigned done = atomicAdd(a.ticket + 1, 1u);
+      if (done == gridDim.x - 1) {   // last CTA: rearm for the next launch
+        a.ticket[0] = 0u;
+        a.ticket[1] = 0u;
+      }
+    }
+  }
+  if (a.late_wait) pdl_wait();       // completes only after the previous kernel
 }
 
 // ---------------------------------------------------------------------------
@@ -655,7 +723,7 @@ __global__ void __launch_bounds__(32 * (NCW + 1), 1) conf_tma_kernel(const ConfA
     }
     if (a.tail) group_mask_tail<BF16, NV, G>(v, gl, nvec, a.tail);
     const int64_t src = act ? src_row<L1>(a, row) : 0;
-    group_reduce_row<BF16, ENTROPY, NV, G>(a, v, act, row, src, gl, a.c,
+    group_reduce_row<BF16, ENTROPY, NV, G>(a, v, act, row, gl, a.c,
                                            reinterpret_cast<const uint4*>((const char*)a.logits + src * a.row_bytes),
                                            a.labels ? __ldg(a.labels + src) : 0);
     // every lane has consumed its staged vectors (the row max read them all)
@@ -887,9 +955,9 @@ cudaError_t launch_warp_l(const ConfArgs& a, int64_t rows, cudaStream_t s) {
   return launch_pdl(k, dim3(grid), dim3(256), 0, s, a);
 }
 
-template <bool BF16, bool ENTROPY, int NV, int G, bool FULL>
-cudaError_t launch_async_l(const ConfArgs& a, int64_t rows, cudaStream_t s) {
-  auto k = conf_async_kernel<BF16, ENTROPY, NV, G, FULL>;
+template <bool BF16, bool ENTROPY, int NV, int G, bool FULL, bool DYN>
+cudaError_t launch_async_d(const ConfArgs& a, int64_t rows, cudaStream_t s) {
+  auto k = conf_async_kernel<BF16, ENTROPY, NV, G, FULL, DYN>;
   constexpr int smem = async_smem_bytes<NV, G>();
   static const int occ = [&] {
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -902,6 +970,12 @@ cudaError_t launch_async_l(const ConfArgs& a, int64_t rows, cudaStream_t s) {
   const int64_t cap = (int64_t)num_sms() * occ;
   const int grid = (int)(want < cap ? (want > 0 ? want : 1) : cap);
   return launch_pdl(k, dim3(grid), dim3(kAsyncThreads), smem, s, a);
+}
+
+template <bool BF16, bool ENTROPY, int NV, int G, bool FULL>
+cudaError_t launch_async_l(const ConfArgs& a, int64_t rows, cudaStream_t s) {
+  return a.ticket ? launch_async_d<BF16, ENTROPY, NV, G, FULL, true>(a, rows, s)
+                  : launch_async_d<BF16, ENTROPY, NV, G, FULL, false>(a, rows, s);
 }
 
 int conf_impl();

@@ -152,6 +152,13 @@ __device__ __forceinline__ uint4 lds128(const void* p) {
 
 // ---- programmatic dependent launch: let the next kernel launch now, and wait
 //      until the previous kernel's results are visible (no-ops without PDL)
+// the two halves of pdl_start, for kernels that may run before the previous
+// kernel of the stream has finished (HS_STEP_OVERLAP_PREVIOUS)
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 __device__ __forceinline__ void pdl_start() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   asm volatile("griddepcontrol.wait;" ::: "memory");

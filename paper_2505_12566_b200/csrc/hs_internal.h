@@ -62,6 +62,12 @@ struct ConfArgs {
                            // row < 2^32 (brows >= 2; brows == 1 -> 0, quotient = row)
   const void* bptr[kMaxBatch];
   float bc[kMaxBatch];
+  // async kernel only: rows claimed in warp-sized groups from ticket[0] (reset
+  // to 0 by the last CTA through ticket[1]); NULL = static grid-stride rows
+  unsigned int* ticket;
+  // async kernel only: read the inputs without waiting for the previous kernel
+  // of the stream, wait for it just before exiting (stream order preserved)
+  int late_wait;
 };
 cudaError_t launch_confidence(const ConfArgs& a, bool bf16, cudaStream_t s);
 cudaError_t launch_seq_reduce(const float* tok_conf, const uint8_t* tok_ok, int64_t n,

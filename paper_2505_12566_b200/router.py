@@ -49,9 +49,13 @@ class Router:
 
     # ---- offline: Alg. 1 / AP thresholds -----------------------
     def calibrate(self, val_logits: list, labels: torch.Tensor, *, target: int = -1,
-                  stream=None) -> dict:
+                  time_val=None, stream=None) -> dict:
         """val_logits[k]: stage k's logits of the validation shard ([n_val*L, stride]);
-        labels: int32 [n_val*L].  Thresholds stay on the device (self.cal['t'])."""
+        labels: int32 [n_val*L].  Thresholds stay on the device (self.cal['t']).
+        ``time_val``: a pair of CUDA events recorded around the validation
+        confidence launch(es)."""
+        if time_val is not None:
+            time_val[0].record()
         if self.batched:
             s = self.stages[0]
             confidence_batched(val_logits, [t.temperature for t in self.stages], n=self.n_val,
@@ -67,6 +71,8 @@ class Router:
                 confidence(val_logits[k], n=self.n_val, seq_len=s.seq_len, n_classes=s.n_classes,
                            temperature=s.temperature, kind=s.kind, reduce=s.reduce, labels=labels,
                            out=out, ws=self.conf_ws, status=self.status, stream=stream)
+        if time_val is not None:
+            time_val[1].record()
         if self.group is None:
             calibrate_thresholds(self.vconf, self.vok, log2_bins=self.q, target=target,
                                  out=self.cal, ws=self.cal_ws, stream=stream)
@@ -84,52 +90,12 @@ class Router:
 
     # ---- online: the cascade ------------------------------------
     def route(self, logits: list, *, n: int | None = None, ids=None, payload=None,
-              by_id: bool = True, thresholds=None, time_stage0=None, stream=None):
-        """Route a batch; thresholds default to the calibrated device vector."""
+              by_id: bool = True, thresholds=None, overlap_first: bool = False, stream=None):
+        """Route a batch; thresholds default to the calibrated device vector.
+        ``overlap_first``: stage 1's confidence runs next to the calibration
+        (HS_STEP_OVERLAP_PREVIOUS; it reads neither the calibration's buffers nor
+        is read by it -- only the threshold test waits for the thresholds)."""
         thr = self.cal["t"] if thresholds is None else thresholds
-        if time_stage0 is None:
-            self.cascade.route(logits, thr, n=n, ids=ids, payload=payload, by_id=by_id,
-                               stream=stream)
-        else:
-            self._route_timed(logits, thr, n, ids, payload, by_id, time_stage0, stream)
+        self.cascade.route(logits, thr, n=n, ids=ids, payload=payload, by_id=by_id,
+                           overlap_first=overlap_first, stream=stream)
         return self.cascade
-
-    def _route_timed(self, logits, thr, n, ids, payload, by_id, events, stream):
-        """Same kernels as Cascade.route, with stage 0 split into hs_confidence +
-        hs_route_compact so CUDA events can bracket the confidence kernel alone."""
-        c = self.cascade
-        n = c.n_cap if n is None else int(n)
-        s0 = self.stages[0]
-        o0 = c.outs[0]
-        d_thr = thr if isinstance(thr, torch.Tensor) else None
-        t0 = d_thr[0:1] if d_thr is not None else float(thr[0])
-        if not hasattr(self, "_s0"):
-            self._s0 = {"conf": torch.empty(n, dtype=torch.float32, device=self.device),
-                        "argmax": torch.empty(n * s0.seq_len, dtype=torch.int32, device=self.device)}
-            self._s0_ws = torch.empty(max(16, n * s0.seq_len * 5 + 1024), dtype=torch.uint8,
-                                      device=self.device)
-            self._s0_cws = torch.zeros(1 << 20, dtype=torch.uint8, device=self.device)
-        events[0].record()
-        confidence(logits[0], n=n, seq_len=s0.seq_len, n_classes=s0.n_classes,
-                   temperature=s0.temperature, kind=s0.kind, reduce=s0.reduce,
-                   row_index=ids if by_id else None, out=self._s0, ws=self._s0_ws,
-                   status=self.status, stream=stream)
-        events[1].record()
-        route_compact(self._s0["conf"], t0, is_last=self.K == 1, n=n, ids=ids,
-                      pred=self._s0["argmax"], pred_len=s0.seq_len, payload=payload,
-                      out={"acc_ids": o0["acc_ids"], "acc_conf": o0["acc_conf"],
-                           "acc_pred": o0["acc_pred"], "def_ids": o0["next_ids"],
-                           "def_pos": self._s0.setdefault("pos", torch.empty(n, dtype=torch.int64, device=self.device)),
-                           "counts": o0["counts"],
-                           **({"def_payload": o0["next_payload"].view(n, -1)} if payload is not None and "next_payload" in o0 else {})},
-                      ws=self._s0_cws, stream=stream)
-        for k in range(1, self.K):
-            s = self.stages[k]
-            prev = c.outs[k - 1]
-            thr_k = d_thr[k:k + 1] if d_thr is not None else float(thr[k] if k < self.K - 1 else 0.0)
-            cascade_step(k, self.K, logits[k], thr_k, n=n, seq_len=s.seq_len,
-                         n_classes=s.n_classes, temperature=s.temperature, kind=s.kind,
-                         reduce=s.reduce, row_index=prev["next_ids"] if by_id else None,
-                         d_n=prev["counts"][1:2], ids=prev["next_ids"],
-                         payload=prev.get("next_payload"), payload_row_bytes=c.P,
-                         out=c.outs[k], ws=c.ws, status=self.status, stream=stream)

@@ -10,6 +10,7 @@ import pytest
 import torch
 
 import oracle
+import workload
 from workload import synth
 
 pytestmark = pytest.mark.gpu
@@ -326,6 +327,57 @@ def test_cascade_vs_oracle(hs, key, n):
 # ---------------------------------------------------------------------------
 # K5/K6 calibration
 # ---------------------------------------------------------------------------
+@pytest.mark.parametrize("graph", [False, True])
+def test_router_overlap_first_equals_serial(hs, graph):
+    """HS_STEP_OVERLAP_PREVIOUS: routing stage 1's K1 runs next to the
+    calibration (no early PDL wait, rows claimed from the step ticket).  The
+    cascade must equal the strictly serial one bit for bit, eagerly and when
+    replayed from a CUDA graph, over repeated steps (ticket re-arming)."""
+    from paper_2505_12566_b200.router import Router
+    fam = synth.FAMILIES["c2"]
+    n, n_val = 131072, 20000
+    stages = [hs.StageSpec(fam.C, fam.temps[k], fam.L, fam.kind, fam.reduce) for k in range(fam.K)]
+    route, val = [], []
+    for k in range(fam.K):
+        x = torch.empty(n, fam.C, dtype=torch.bfloat16, device=dev())
+        workload.gpu_logits(x, fam, k, n=n)
+        route.append(x)
+        v = torch.empty(n_val, fam.C, dtype=torch.bfloat16, device=dev())
+        workload.gpu_logits(v, fam, k, n=n_val, id_base=synth.VAL_ID_BASE)
+        val.append(v)
+    lab = torch.empty(n_val, dtype=torch.int32, device=dev())
+    workload.gpu_labels(lab, fam, id_base=synth.VAL_ID_BASE, n=n_val)
+
+    def run(overlap):
+        r = Router(stages, n, n_val, dev(), log2_bins=fam.log2_bins)
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            def step():
+                r.calibrate(val, lab)
+                r.route(route, overlap_first=overlap)
+            step()
+            if graph:
+                s.synchronize()
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=s):
+                    step()
+                for _ in range(3):
+                    g.replay()
+            else:
+                for _ in range(3):
+                    step()
+        torch.cuda.synchronize()
+        return r.cal["t"].cpu(), r.cascade.results()
+
+    t0, res0 = run(False)
+    t1, res1 = run(True)
+    assert torch.equal(t0, t1)
+    assert [x["n_acc"] for x in res0] == [x["n_acc"] for x in res1]
+    for a, b in zip(res0, res1):
+        for key in ("ids", "conf", "pred"):
+            assert torch.equal(a[key], b[key]), key
+
+
 def _gpu_val(hs, fam, n_val):
     K = fam.K
     vids = np.arange(n_val, dtype=np.int64) + synth.VAL_ID_BASE
