@@ -201,6 +201,18 @@ def build_inputs(fam, rank: int, dev):
     return route, val, labels, payload
 
 
+def committed_traffic(config: str):
+    """DRAM bytes per launch of the roofline kernel from the committed ncu
+    capture (profiles/r01_k1_traffic.json, written by tools/ncu_summary.py
+    traffic), when it was taken on this config; else None."""
+    path = os.path.join(ROOT, "profiles", "r01_k1_traffic.json")
+    try:
+        rec = json.load(open(path))
+    except (OSError, ValueError):
+        return None
+    return rec.get("dram_bytes_per_launch") if rec.get("config") == config else None
+
+
 def make_router(fam, dev, group):
     import paper_2505_12566_b200 as hs
     from paper_2505_12566_b200.router import Router
@@ -308,6 +320,7 @@ def run_ours(args, world, rank, local):
     # per token row, logits + conf (4 B) + argmax (4 B) + label (4 B) + correct (1 B)
     k_bytes = fam.K * fam.n_val * fam.L * (row_b + 13)
     achieved = k_bytes / (kernel_ms / 1e3) / 1e9
+    traffic = committed_traffic(args.config)
     e2e = run_e2e(args, fam, router, route, val, labels, payload, stream, world) if args.e2e_steps > 0 else None
     line = {
         "metric": METRIC, "value": value, "unit": "requests/s", "n_gpus": world,
@@ -324,7 +337,7 @@ def run_ours(args, world, rank, local):
         "logits_frac_of_peak": step_bytes_all / world / (ms / 1e3) / 1e9 / peak,
         "reach": reach, "thresholds": router.cal["t"].cpu().tolist(), "status": st,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": None,
+                     "frac": achieved / peak, "traffic": traffic,
                      "kernel": ("conf_async_kernel" if fam.C * fam.elt_bytes <= 2048 else
                                 "conf_warp_kernel" if fam.C * fam.elt_bytes <= 8192 else "conf_cta_kernel")
                      + f" (K1 on the validation shard: {fam.K} stages x {fam.n_val} items in one launch"

@@ -2,6 +2,7 @@
 
   python tools/ncu_summary.py full  <report.ncu-rep> [--bytes N]   # one --set full capture
   python tools/ncu_summary.py launches <launches.csv> [--step N]   # gpu__time_duration list
+  python tools/ncu_summary.py traffic <report.ncu-rep> <config> <out.json>
 
 `full` prints the headline metrics (duration, DRAM bytes and throughput, issue,
 pipe utilisation, stall reasons) and the dynamic SASS opcode mix; `launches`
@@ -12,6 +13,7 @@ from __future__ import annotations
 import collections
 import csv
 import io
+import os
 import subprocess
 import sys
 
@@ -94,10 +96,29 @@ def launches(path: str, step: int | None = None):
         print(f"  {100 * v / tot:5.1f}%  {v / 1e3:10.1f} us  {k}")
 
 
+def traffic(path: str, config: str, out: str):
+    """Write the DRAM bytes of one `--set full` capture for bench.py's roofline."""
+    import json
+    raw = list(csv.reader(io.StringIO(_ncu(["-i", path, "--page", "raw", "--csv"]))))
+    hdr, units, vals = raw[0], raw[1], raw[2]
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    tot = 0.0
+    for key in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+        i = hdr.index(key)
+        tot += float(vals[i]) * scale.get(units[i], 1)
+    rec = {"config": config, "kernel": vals[hdr.index("Kernel Name")],
+           "dram_bytes_per_launch": int(round(tot)), "source": os.path.basename(path),
+           "capture": "ncu --set full --clock-control none (one launch)"}
+    json.dump(rec, open(out, "w"), indent=1)
+    print(rec)
+
+
 if __name__ == "__main__":
     mode, path = sys.argv[1], sys.argv[2]
     if mode == "full":
         b = float(sys.argv[sys.argv.index("--bytes") + 1]) if "--bytes" in sys.argv else None
         full(path, b)
+    elif mode == "traffic":       # traffic <report> <config> <out.json>
+        traffic(path, sys.argv[3], sys.argv[4])
     else:
         launches(path)
