@@ -896,8 +896,21 @@ static cudaError_t launch_calib_resident(const float* conf, const uint8_t* corre
   void* args[] = {(void*)&conf, (void*)&correct, (void*)&K, (void*)&N, (void*)&q, (void*)&target,
                   (void*)&b_idx, (void*)&thr, (void*)&reach, (void*)&handled,
                   (void*)&correct_total, (void*)&st, (void*)&hist3, (void*)&per_cta};
-  cudaError_t e = cudaLaunchCooperativeKernel((void*)kern, dim3(grid), dim3(kResidentThreads),
-                                              args, smem, s);
+  // cooperative (grid barriers) + programmatic dependent launch: the CTAs are
+  // placed as the previous kernel's CTAs retire and wait in griddepcontrol.wait
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kResidentThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
+  cudaError_t e = cudaLaunchKernelExC(&cfg, (const void*)kern, args);
   count_launch();
   *launched = true;
   return e != cudaSuccess ? e : cudaGetLastError();
