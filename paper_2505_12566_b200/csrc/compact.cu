@@ -228,30 +228,18 @@ __global__ void __launch_bounds__(kCompactThreads) route_compact_fast_kernel(con
   CompactWs* ws = reinterpret_cast<CompactWs*>(a.ws);
   unsigned long long* st = tile_status(a.ws);
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  int64_t n = a.n;
-  if (a.d_n) n = min(*a.d_n, a.n);
-  const int64_t ntiles = (n + TILE - 1) / TILE;
   const int64_t tile = blockIdx.x;
-  if (ntiles == 0) {
-    if (tile == 0 && tid == 0) {
-      a.counts[0] = 0;
-      a.counts[1] = 0;
-    }
-    return;
-  }
-  if (tile >= ntiles) return;
-  const unsigned epoch = *(volatile unsigned*)&ws->epoch;
-  const unsigned long long etag = (unsigned long long)epoch << 32;
   const int64_t base = tile * TILE;
-  const int tn = (int)min((int64_t)TILE, n - base);
   const int64_t i0 = base + (int64_t)tid * I;
-  const float thr = a.d_threshold ? *a.d_threshold : a.threshold;
   const bool pred1 = a.acc_pred && a.pred_len == 1;
-
+  // The item loads are issued speculatively within the capacity a.n (the
+  // buffers are capacity-sized) together with the device count and threshold,
+  // so the tile's data and *d_n arrive after one memory latency, not two.
+  const int64_t ncap = a.n;
   float cv[I];
   int64_t idv[I];
   int32_t pv[I];
-  if (vec && i0 + I <= n) {
+  if (vec && i0 + I <= ncap) {
     const float4* c4 = reinterpret_cast<const float4*>(a.conf + i0);
     const float4 x0 = __ldg(c4), x1 = __ldg(c4 + 1);
     cv[0] = x0.x; cv[1] = x0.y; cv[2] = x0.z; cv[3] = x0.w;
@@ -281,12 +269,27 @@ __global__ void __launch_bounds__(kCompactThreads) route_compact_fast_kernel(con
 #pragma unroll
     for (int j = 0; j < I; ++j) {
       const int64_t i = i0 + j;
-      const bool in = i < n;
+      const bool in = i < ncap;
       cv[j] = in ? __ldg(a.conf + i) : 0.f;
       idv[j] = (in && a.ids) ? __ldg(a.ids + i) : i;
       pv[j] = (in && pred1) ? __ldg(a.pred + i) : 0;
     }
   }
+  int64_t n = ncap;
+  if (a.d_n) n = min(*a.d_n, ncap);
+  const float thr = a.d_threshold ? *a.d_threshold : a.threshold;
+  const int64_t ntiles = (n + TILE - 1) / TILE;
+  if (ntiles == 0) {
+    if (tile == 0 && tid == 0) {
+      a.counts[0] = 0;
+      a.counts[1] = 0;
+    }
+    return;
+  }
+  if (tile >= ntiles) return;
+  const unsigned epoch = *(volatile unsigned*)&ws->epoch;
+  const unsigned long long etag = (unsigned long long)epoch << 32;
+  const int tn = (int)min((int64_t)TILE, n - base);
   // D3 per item (NaN defers; the last stage accepts all), D4 ranks
   unsigned dm = 0;
 #pragma unroll

@@ -544,9 +544,11 @@ __global__ void __launch_bounds__(kAsyncThreads, 3) conf_async_kernel(const Conf
   constexpr uint32_t STAGEB = RPW * ROWB;             // one warp's stage
   const int lane = threadIdx.x & 31, gl = lane % G, grp = lane / G, warp = threadIdx.x >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const int64_t rows = live_rows(a);
   const int nvec = a.nvec;
   constexpr bool dyn = DYN;   // a.ticket != NULL
+  // row-index reads are speculative within the capacity (capacity-sized
+  // buffers), so they overlap the read of the device count *d_n
+  const int64_t cap = a.n * a.L * (int64_t)a.nbatch;
   // row group g = rows g*RPW .. g*RPW + RPW-1: static (warp w takes w, w + nwarps,
   // ...) or claimed from the ticket, so CTAs that start late (SMs still busy with
   // the previous kernel) just take fewer groups
@@ -565,6 +567,8 @@ __global__ void __launch_bounds__(kAsyncThreads, 3) conf_async_kernel(const Conf
     return cnext++;
   };
   const int64_t g0 = dyn ? next_group(0) : ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t fA = fetch_index(a, g0 * RPW + grp < cap ? g0 * RPW + grp : 0);
+  const int64_t rows = live_rows(a);
   if (g0 * RPW < rows) {
     // lane gl's vector k of stage st sits at base + st*STAGEB + grp*ROWB + k*G*16 + gl*16:
     // a quarter-warp reads 128 contiguous bytes (conflict-free LDS.128)
@@ -579,7 +583,7 @@ __global__ void __launch_bounds__(kAsyncThreads, 3) conf_async_kernel(const Conf
     float cA;
     int32_t labA;
     {
-      const RowSrc r = locate_cur(a, cur, actA ? rowA : 0, fetch_index(a, actA ? rowA : 0));
+      const RowSrc r = locate_cur(a, cur, actA ? rowA : 0, actA ? fA : fetch_index(a, 0));
       pA = reinterpret_cast<const uint4*>(r.base + r.src * a.row_bytes);
       cA = r.c;
       labA = fetch_label(a, r);
@@ -587,7 +591,7 @@ __global__ void __launch_bounds__(kAsyncThreads, 3) conf_async_kernel(const Conf
     group_prefetch_row<NV, G, FULL>(sbase, pA, gl, nvec);
     cp_async_commit();
     int64_t gB = next_group(g0);
-    int64_t fB = fetch_index(a, gB * RPW + grp < rows ? gB * RPW + grp : 0);
+    int64_t fB = fetch_index(a, gB * RPW + grp < cap ? gB * RPW + grp : 0);
     uint4 A[NV];
     for (int it = 0;; ++it) {
       const int64_t rowB = gB * RPW + grp;
@@ -605,7 +609,7 @@ __global__ void __launch_bounds__(kAsyncThreads, 3) conf_async_kernel(const Conf
         labB = fetch_label(a, r);
         gC = next_group(gB);
         const int64_t rowC = gC * RPW + grp;
-        fC = fetch_index(a, rowC < rows ? rowC : 0);
+        fC = fetch_index(a, rowC < cap ? rowC : 0);
       }
       cp_async_commit();
       cp_async_wait<1>();        // this lane's copies of row A have landed
