@@ -317,8 +317,9 @@ def run_ours(args, world, rank, local):
     value = n_all / (ms / 1e3)
     peak, peak_src = peaks()
     # dominant kernel: K1 over the validation shard, all K stages in one launch:
-    # per token row, logits + conf (4 B) + argmax (4 B) + label (4 B) + correct (1 B)
-    k_bytes = fam.K * fam.n_val * fam.L * (row_b + 13)
+    # per item, its L token rows of logits (row_b) + per token conf (4 B),
+    # argmax (4 B), label (4 B) and correct bit (1 B)
+    k_bytes = fam.K * fam.n_val * (row_b + 13 * fam.L)
     achieved = k_bytes / (kernel_ms / 1e3) / 1e9
     traffic = committed_traffic(args.config)
     e2e = run_e2e(args, fam, router, route, val, labels, payload, stream, world) if args.e2e_steps > 0 else None
