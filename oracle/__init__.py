@@ -50,8 +50,10 @@ def lib():
             L.hso_row_stats.argtypes = [_P, _I64, ctypes.c_double, _P, _P, _P]
             L.hso_row_stats.restype = ctypes.c_int
             L.hso_confidence.argtypes = [_P, ctypes.c_int, _I64, ctypes.c_int, _I64, _I64, _P,
-                                         ctypes.c_double, ctypes.c_int, ctypes.c_int,
+                                         ctypes.c_double, ctypes.c_int, ctypes.c_int, _I64,
                                          _P, _P, _P, _P, _P, ctypes.c_int]
+            L.hso_row_stats_topk.argtypes = [_P, _I64, ctypes.c_double, _I64, _P, _P, _P]
+            L.hso_row_stats_topk.restype = ctypes.c_int
             L.hso_confidence.restype = ctypes.c_int
             L.hso_route.argtypes = [_P, _I64, ctypes.c_double, ctypes.c_int, _P, _P, _P, _P]
             L.hso_route.restype = None
@@ -81,12 +83,18 @@ def default_threads() -> int:
 # --------------------------------------------------------------------------
 # D1: one row.  P:373-391 (temperature-scaled softmax).
 # --------------------------------------------------------------------------
-def row_stats(x, T: float = 1.0):
-    """(p_max, H [nats], argmax) of one logits row in fp64; None if invalid."""
+def row_stats(x, T: float = 1.0, top_k: int = 0):
+    """(p_max, H [nats], argmax) of one logits row in fp64; None if invalid.
+    top_k > 0: statistics of the softmax restricted to the K largest logits
+    (NEXT-2, reading G4)."""
     x = np.ascontiguousarray(np.asarray(x, dtype=np.float64))
     p = ctypes.c_double()
     h = ctypes.c_double()
     a = ctypes.c_int64()
+    if top_k:
+        rc = lib().hso_row_stats_topk(_ptr(x), x.size, float(T), int(top_k), ctypes.byref(p),
+                                      ctypes.byref(h), ctypes.byref(a))
+        return None if rc != 0 else (p.value, h.value, a.value)
     rc = lib().hso_row_stats(_ptr(x), x.size, float(T), ctypes.byref(p), ctypes.byref(h),
                              ctypes.byref(a))
     if rc != 0:
@@ -99,7 +107,7 @@ def row_stats(x, T: float = 1.0):
 # --------------------------------------------------------------------------
 def confidence(logits: np.ndarray, n_seq: int, seq_len: int, n_classes: int, row_stride: int,
                temperature: float, kind: int = MAXPROB, reduce: int = SEQ_NONE,
-               row_index=None, labels=None, nthreads: int | None = None):
+               row_index=None, labels=None, nthreads: int | None = None, top_k: int = 0):
     """Per-item confidence of a batch of logits rows.
 
     ``logits``: a flat float32 array, or a uint16 array of raw bf16 bits.
@@ -121,7 +129,7 @@ def confidence(logits: np.ndarray, n_seq: int, seq_len: int, n_classes: int, row
     correct = np.empty(n_seq, np.uint8) if lab is not None else None
     rc = lib().hso_confidence(_ptr(flat), dtype, n_seq, int(seq_len), int(n_classes),
                               int(row_stride), _ptr(ri), float(temperature), int(kind),
-                              int(reduce), _ptr(conf), _ptr(argmax), _ptr(lab), _ptr(correct),
+                              int(reduce), int(top_k), _ptr(conf), _ptr(argmax), _ptr(lab), _ptr(correct),
                               _ptr(bad), int(nthreads or default_threads()))
     if rc != 0:
         raise ValueError("oracle: invalid argument")

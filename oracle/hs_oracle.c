@@ -93,6 +93,52 @@ int hso_row_stats(const double* x, int64_t C, double T,
     return 0;
 }
 
+/* ------------------------------------------------------------------------- */
+/* D1' (NEXT-2). Top-K restricted confidence for generation models.         */
+/*   "We assign P = TopK(P) to enhance the prediction, while the  */
+/*   rest is the same as classification"; f = TopK(softmax(theta(P))^2).    */
+/*   Reading: restrict the row to its K largest  */
+/*   logits, softmax over the restricted set at temperature T, then the same */
+/*   confidence as D1 (p_max, p_max^2 or exp(-H) of the restricted           */
+/*   distribution).  The K largest VALUES are a unique multiset, so ties at  */
+/*   the K-th place do not matter.  K >= C is the full softmax.  Validity    */
+/*   and the argmax are those of the full row (argmax invariance).    */
+/* ------------------------------------------------------------------------- */
+static int cmp_desc(const void* a, const void* b) {
+    double x = *(const double*)a, y = *(const double*)b;
+    return (x < y) - (x > y);
+}
+
+int hso_row_stats_topk(const double* x, int64_t C, double T, int64_t K,
+                       double* p_max, double* entropy, int64_t* argmax) {
+    double p, H;
+    int64_t am;
+    if (hso_row_stats(x, C, T, &p, &H, &am) != 0) return 1;   /* full-row checks */
+    if (K <= 0 || K >= C) {
+        *p_max = p; *entropy = H; *argmax = am;
+        return 0;
+    }
+    double* v = (double*)malloc(sizeof(double) * (size_t)C);
+    memcpy(v, x, sizeof(double) * (size_t)C);
+    qsort(v, (size_t)C, sizeof(double), cmp_desc);        /* v[0] >= v[1] >= ... */
+    int64_t k_finite = 0;
+    while (k_finite < K && !isinf(v[k_finite])) ++k_finite;  /* -inf: masked, p = 0 */
+    /* restricted statistics: the K largest values as their own prediction vector */
+    nsum_t s = {0, 0}, w = {0, 0};
+    for (int64_t j = 0; j < k_finite; ++j) {
+        double a = (v[j] - v[0]) / T;
+        double e = exp(a);
+        nsum_add(&s, e);
+        nsum_add(&w, e * a);
+    }
+    double S = nsum_get(&s), W = nsum_get(&w);
+    free(v);
+    *p_max = 1.0 / S;
+    *entropy = log(S) - W / S;
+    *argmax = am;
+    return 0;
+}
+
 /* step 7: the confidence of one row from its statistics.
  *   MAXPROB    : p_max                      (north_star; reading G1)
  *   MAXPROB_SQ : p_max^2                    (P:415 taken literally, G1)
@@ -115,7 +161,7 @@ static double conf_of(int kind, double p_max, double H) {
 /* ------------------------------------------------------------------------- */
 typedef struct {
     const void* logits; int dtype; int64_t n_seq; int L; int64_t C; int64_t stride;
-    const int64_t* row_index; double T; int kind; int reduce;
+    const int64_t* row_index; double T; int kind; int reduce; int64_t top_k;
     double* conf; int32_t* argmax; const int32_t* labels; uint8_t* correct; uint8_t* bad;
     int64_t lo, hi;
 } conf_job_t;
@@ -133,7 +179,7 @@ static void* conf_worker(void* arg) {
             for (int64_t j = 0; j < J->C; ++j)
                 row[j] = load_logit(J->logits, J->dtype, tok * J->stride + j);
             double p, H; int64_t am;
-            if (hso_row_stats(row, J->C, J->T, &p, &H, &am) != 0) {
+            if (hso_row_stats_topk(row, J->C, J->T, J->top_k, &p, &H, &am) != 0) {
                 any_bad = 1; am = -1; p = NAN; H = NAN;
             }
             double c = conf_of(J->kind, p, H);
@@ -158,16 +204,16 @@ static void* conf_worker(void* arg) {
  * L < 1, NONE with L > 1, stride < C). */
 int hso_confidence(const void* logits, int dtype, int64_t n_seq, int L, int64_t C,
                    int64_t stride, const int64_t* row_index, double T, int kind, int reduce,
-                   double* conf, int32_t* argmax, const int32_t* labels, uint8_t* correct,
-                   uint8_t* bad, int nthreads) {
-    if (C < 2 || !(T > 0) || isinf(T) || L < 1 || stride < C || n_seq < 0) return -1;
+                   int64_t top_k, double* conf, int32_t* argmax, const int32_t* labels,
+                   uint8_t* correct, uint8_t* bad, int nthreads) {
+    if (C < 2 || !(T > 0) || isinf(T) || L < 1 || stride < C || n_seq < 0 || top_k < 0) return -1;
     if (reduce == ORC_SEQ_NONE && L != 1) return -1;
     if (nthreads < 1) nthreads = 1;
     if (n_seq < nthreads) nthreads = n_seq > 0 ? (int)n_seq : 1;
     conf_job_t* jobs = (conf_job_t*)calloc((size_t)nthreads, sizeof(conf_job_t));
     pthread_t* th = (pthread_t*)calloc((size_t)nthreads, sizeof(pthread_t));
     for (int w = 0; w < nthreads; ++w) {
-        conf_job_t J = {logits, dtype, n_seq, L, C, stride, row_index, T, kind, reduce,
+        conf_job_t J = {logits, dtype, n_seq, L, C, stride, row_index, T, kind, reduce, top_k,
                         conf, argmax, labels, correct, bad,
                         n_seq * w / nthreads, n_seq * (w + 1) / nthreads};
         jobs[w] = J;

@@ -193,3 +193,82 @@ def test_threads_do_not_change_result():
     a = oracle.confidence(x, 513, 1, 77, 77, 1.0, nthreads=1)
     b = oracle.confidence(x, 513, 1, 77, 77, 1.0, nthreads=7)
     assert np.array_equal(a["conf"], b["conf"])
+
+
+# ---------------------------------------------------------------------------
+# NEXT-2: Top-K restricted confidence (reading G4)
+# ---------------------------------------------------------------------------
+def test_topk_geometric_closed_form():
+    """logits (3, 2, 1, 0, ...) over a 50,000 vocabulary, top_k = 10,
+    T = 1: the restricted softmax of 10 consecutive integers is a geometric
+    series, p_max = (1 - e^-1) / (1 - e^-10)."""
+    x = 3.0 - np.arange(50000, dtype=np.float64)
+    p, H, am = oracle.row_stats(x, 1.0, top_k=10)
+    want = (1 - math.exp(-1)) / (1 - math.exp(-10))
+    assert p == pytest.approx(want, rel=1e-14) and am == 0
+    # entropy of the truncated geometric distribution, summed independently
+    q = np.array([math.exp(-i) for i in range(10)]) / sum(math.exp(-i) for i in range(10))
+    assert H == pytest.approx(float(-(q * np.log(q)).sum()), rel=1e-13)
+
+
+def test_topk_symmetry_and_degenerate_k():
+    # S:135: top-2 restricted logits equal -> p = 1/2 (squared: 0.25)
+    r = oracle.confidence(np.array([7, 7, 1, 0, -3], np.float32), 1, 1, 5, 5, 1.0,
+                          kind=oracle.MAXPROB_SQ, top_k=2)
+    assert r["conf"][0] == 0.25
+    # K = 1: the restricted distribution is a point mass
+    p, H, _ = oracle.row_stats(np.array([0.3, 2.0, -1.0]), 0.7, top_k=1)
+    assert p == 1.0 and H == 0.0
+    # K >= C: the full softmax
+    x = np.random.default_rng(4).normal(size=37)
+    for K in (37, 38, 1000):
+        assert oracle.row_stats(x, 1.3, top_k=K) == oracle.row_stats(x, 1.3)
+
+
+def test_topk_ties_at_the_boundary_and_masked():
+    # the K largest VALUES are unique even when the K-th place is tied
+    p, _, _ = oracle.row_stats(np.array([1.0, 5.0, 1.0, 1.0]), 1.0, top_k=2)
+    assert p == pytest.approx(1 / (1 + math.exp(-4)), rel=1e-15)
+    # -inf (masked) classes inside the top K contribute p = 0
+    p, _, am = oracle.row_stats(np.array([2.0, -np.inf, 1.0, -np.inf]), 1.0, top_k=3)
+    assert p == pytest.approx(1 / (1 + math.exp(-1)), rel=1e-15) and am == 0
+
+
+def test_topk_library_special_case():
+    """torch.topk + torch.softmax / Categorical.entropy in fp64 on random rows."""
+    rng = np.random.default_rng(11)
+    for _ in range(40):
+        C = int(rng.integers(2, 3000))
+        K = int(rng.integers(1, 40))
+        T = float(rng.uniform(0.05, 5))
+        x = rng.normal(scale=rng.uniform(0.1, 8), size=C)
+        v = torch.topk(torch.from_numpy(x), min(K, C)).values / T
+        pr = torch.softmax(v, 0)
+        p, H, am = oracle.row_stats(x, T, top_k=K)
+        assert p == pytest.approx(float(pr.max()), rel=1e-12)
+        assert H == pytest.approx(float(torch.distributions.Categorical(probs=pr).entropy()),
+                                  rel=1e-9, abs=1e-12)
+        assert am == int(np.argmax(x))
+
+
+def test_topk_generation_sequence_min():
+    """the sequence confidence is the minimum over its tokens; each
+    token restricted to its top K."""
+    rng = np.random.default_rng(12)
+    L, C, K = 6, 500, 8
+    x = rng.normal(size=(3 * L, C)).astype(np.float32)
+    r = oracle.confidence(x, 3, L, C, C, 0.9, kind=oracle.MAXPROB_SQ, reduce=oracle.SEQ_MIN,
+                          top_k=K)
+    for i in range(3):
+        per_tok = [oracle.row_stats(x[i * L + t].astype(np.float64), 0.9, top_k=K)[0] ** 2
+                   for t in range(L)]
+        assert r["conf"][i] == min(per_tok)
+
+
+def test_qa_hand_example_both_sides():
+    """S:144 (corrected value): start (2,1,0), end (0,1,2), T = 1:
+    both sides have p = e^2/(e^2+e+1); MIN = that value (squared: 0.44254...)."""
+    x = np.array([[2, 1, 0], [0, 1, 2]], np.float32)
+    r = oracle.confidence(x, 1, 2, 3, 3, 1.0, kind=oracle.MAXPROB_SQ, reduce=oracle.SEQ_MIN)
+    e = math.e
+    assert r["conf"][0] == pytest.approx((e * e / (e * e + e + 1)) ** 2, rel=1e-15)
