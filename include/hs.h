@@ -96,6 +96,20 @@ hs_status_t hs_confidence(const void* logits, hs_dtype_t dtype, int64_t n, int32
                           const int32_t* labels, uint8_t* correct, void* ws, size_t ws_bytes,
                           uint32_t* d_status, hs_stream_t stream);
 
+/* hs_confidence_topk (NEXT-2; "P = TopK(P)", reading G4): as
+ * hs_confidence, with every token row's softmax restricted to its top_k
+ * largest logits (0 = the full row, as hs_confidence; top_k >= n_classes is
+ * the full row too).  c = p_max / p_max^2 / exp(-H) of the restricted
+ * distribution; validity, argmax and correct bits are those of the full row.
+ * The K largest VALUES form a unique multiset, so ties at the K-th place do not
+ * matter.  top_k outside 0..32 -> INVALID_ARGUMENT. */
+hs_status_t hs_confidence_topk(const void* logits, hs_dtype_t dtype, int64_t n, int32_t seq_len,
+                               int64_t n_classes, int64_t row_stride, const int64_t* row_index,
+                               const int64_t* d_n, float temperature, hs_conf_kind_t kind,
+                               hs_seq_reduce_t reduce, int32_t top_k, float* conf, int32_t* argmax,
+                               const int32_t* labels, uint8_t* correct, void* ws, size_t ws_bytes,
+                               uint32_t* d_status, hs_stream_t stream);
+
 /* Every stage model's confidence on the SAME item set in one launch (the
  * calibration input of Alg. 1: "Compute a on D_v" for every model m_1..m_K,
  * P:458-464).  Batch b (0 <= b < n_batches <= 8) reads logits[b] (host array
@@ -203,7 +217,8 @@ hs_status_t hs_cascade_step(int32_t stage, int32_t n_stages, const void* logits,
  *   row_index, d_n, ids, payload) nor reads or writes this step's workspace.
  *   Stream order is otherwise preserved: the step's kernels complete after the
  *   previous kernel, and the threshold test waits for it (d_threshold may be
- *   produced by it).  Unknown flag bits -> HS_ERR_INVALID_ARGUMENT. */
+ *   produced by it).  Unknown flag bits -> HS_ERR_INVALID_ARGUMENT.
+ * top_k: the stage's confidence over its top_k logits (hs_confidence_topk). */
 #define HS_STEP_OVERLAP_PREVIOUS 1u
 hs_status_t hs_cascade_step_ex(int32_t stage, int32_t n_stages, const void* logits, hs_dtype_t dtype,
                                int64_t n, int32_t seq_len, int64_t n_classes, int64_t row_stride,
@@ -213,7 +228,7 @@ hs_status_t hs_cascade_step_ex(int32_t stage, int32_t n_stages, const void* logi
                                int64_t payload_row_bytes, int64_t* acc_ids, float* acc_conf,
                                int32_t* acc_pred, int64_t* next_ids, void* next_payload,
                                int64_t* d_counts, void* ws, size_t ws_bytes, uint32_t* d_status,
-                               uint32_t flags, hs_stream_t stream);
+                               int32_t top_k, uint32_t flags, hs_stream_t stream);
 
 /* ------------------------------------------------------------------------ */
 /* Offline Accuracy-Preserving threshold calibration (Alg. 1, AP).  */

@@ -85,13 +85,15 @@ def confidence(logits: torch.Tensor, *, n: int | None = None, seq_len: int = 1,
                reduce="none", row_index: torch.Tensor | None = None,
                d_n: torch.Tensor | None = None, labels: torch.Tensor | None = None,
                want_argmax: bool = True, status: torch.Tensor | None = None,
-               out: dict | None = None, ws: torch.Tensor | None = None, stream=None) -> dict:
+               out: dict | None = None, ws: torch.Tensor | None = None, top_k: int = 0,
+               stream=None) -> dict:
     """Per-item confidence of a batch of logits rows.
 
     ``logits``: [rows, row_stride] bf16/fp32 on the GPU (row-major; the first
     ``n_classes`` entries of a row are the prediction vector).  Returns dict of
     ``conf`` f32[n], ``argmax`` i32[n*seq_len] and ``correct`` u8[n] (when
-    ``labels`` is given)."""
+    ``labels`` is given).  ``top_k`` > 0: softmax restricted to each row's
+    top_k logits (NEXT-2; hs_confidence_topk)."""
     _check_cuda(logits, row_index, d_n, labels, status)
     if logits.dim() != 2 or logits.stride(1) != 1:
         raise ValueError("logits must be a 2-D row-major tensor")
@@ -110,8 +112,8 @@ def confidence(logits: torch.Tensor, *, n: int | None = None, seq_len: int = 1,
     need = lib().hs_confidence_workspace(n, seq_len)
     if need and (ws is None or ws.numel() < need):
         ws = torch.empty(need, dtype=torch.uint8, device=dev)
-    _abi.call("hs_confidence", _p(logits), _dtype_code(logits), n, seq_len, C, stride,
-              _p(row_index), _p(d_n), float(temperature), _kind(kind), _reduce(reduce),
+    _abi.call("hs_confidence_topk", _p(logits), _dtype_code(logits), n, seq_len, C, stride,
+              _p(row_index), _p(d_n), float(temperature), _kind(kind), _reduce(reduce), int(top_k),
               _p(out["conf"]), _p(out.get("argmax")), _p(labels), _p(out.get("correct")),
               _p(ws), 0 if ws is None else ws.numel(), _p(status), _stream(stream))
     return out
@@ -212,7 +214,7 @@ def cascade_step(stage: int, n_stages: int, logits: torch.Tensor, threshold, *, 
                  payload: torch.Tensor | None = None, payload_row_bytes: int = 0,
                  out: dict | None = None, ws: torch.Tensor | None = None,
                  status: torch.Tensor | None = None, overlap_previous: bool = False,
-                 stream=None) -> dict:
+                 top_k: int = 0, stream=None) -> dict:
     """One model m_k of the cascade: confidence -> threshold -> compaction/gather.
 
     ``overlap_previous`` (HS_STEP_OVERLAP_PREVIOUS): the confidence kernel runs
@@ -245,7 +247,7 @@ def cascade_step(stage: int, n_stages: int, logits: torch.Tensor, threshold, *, 
               float(temperature), _kind(kind), _reduce(reduce), thr, _p(d_thr), _p(ids), _p(payload),
               int(payload_row_bytes), _p(out["acc_ids"]), _p(out["acc_conf"]), _p(out["acc_pred"]),
               _p(out["next_ids"]), _p(out.get("next_payload")), _p(out["counts"]), _p(ws),
-              ws.numel(), _p(status), HS_STEP_OVERLAP_PREVIOUS if overlap_previous else 0,
+              ws.numel(), _p(status), int(top_k), HS_STEP_OVERLAP_PREVIOUS if overlap_previous else 0,
               _stream(stream))
     return out
 
@@ -332,6 +334,7 @@ class StageSpec:
     seq_len: int = 1
     kind: int = MAXPROB
     reduce: int = SEQ_NONE
+    top_k: int = 0          # NEXT-2: restricted softmax over the top_k logits (0 = full)
 
 
 class Cascade:
@@ -387,7 +390,8 @@ class Cascade:
                          row_index=row_index, d_n=prev["counts"][1:2] if k else None,
                          ids=cur_ids, payload=cur_payload, payload_row_bytes=self.P,
                          out=self.outs[k], ws=self.ws, status=self.status,
-                         overlap_previous=overlap_first and k == 0, stream=stream)
+                         overlap_previous=overlap_first and k == 0, top_k=s.top_k,
+                         stream=stream)
         return self
 
     def results(self):

@@ -23,6 +23,8 @@ STATUS_NAMES = {0: "HS_OK", 1: "HS_ERR_INVALID_ARGUMENT", 2: "HS_ERR_NONFINITE_I
 SIGNATURES = {
     "hs_confidence_workspace": (SZ, [I64, I32]),
     "hs_confidence": (I32, [P, I32, I64, I32, I64, I64, P, P, F32, I32, I32, P, P, P, P, P, SZ, P, P]),
+    "hs_confidence_topk": (I32, [P, I32, I64, I32, I64, I64, P, P, F32, I32, I32, I32, P, P, P, P, P, SZ,
+                                 P, P]),
     "hs_confidence_batched_workspace": (SZ, [I32, I64, I32]),
     "hs_confidence_batched": (I32, [P, P, I32, I32, I64, I32, I64, I64, P, I32, I32, P, P, P, P, P,
                                     SZ, P, P]),
@@ -36,7 +38,7 @@ SIGNATURES = {
     "hs_cascade_step": (I32, [I32, I32, P, I32, I64, I32, I64, I64, P, P, F32, I32, I32, F32, P, P,
                               P, I64, P, P, P, P, P, P, P, SZ, P, P]),
     "hs_cascade_step_ex": (I32, [I32, I32, P, I32, I64, I32, I64, I64, P, P, F32, I32, I32, F32, P, P,
-                                 P, I64, P, P, P, P, P, P, P, SZ, P, ctypes.c_uint32, P]),
+                                 P, I64, P, P, P, P, P, P, P, SZ, P, I32, ctypes.c_uint32, P]),
     "hs_calibrate_workspace": (SZ, [I32, I32]),
     "hs_calibrate_thresholds": (I32, [P, P, I32, I64, I32, I64, I32, P, P, P, P, P, P, SZ, P]),
     "hs_calibrate_begin": (I32, [I32, I32, I64, P, SZ, P]),

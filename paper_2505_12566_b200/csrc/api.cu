@@ -188,15 +188,31 @@ hs_status_t hs_confidence(const void* logits, hs_dtype_t dtype, int64_t n, int32
                           hs_seq_reduce_t reduce, float* conf, int32_t* argmax,
                           const int32_t* labels, uint8_t* correct, void* ws, size_t ws_bytes,
                           uint32_t* d_status, hs_stream_t stream) {
+  return hs_confidence_topk(logits, dtype, n, seq_len, n_classes, row_stride, row_index, d_n,
+                            temperature, kind, reduce, 0, conf, argmax, labels, correct, ws,
+                            ws_bytes, d_status, stream);
+}
+
+hs_status_t hs_confidence_topk(const void* logits, hs_dtype_t dtype, int64_t n, int32_t seq_len,
+                               int64_t n_classes, int64_t row_stride, const int64_t* row_index,
+                               const int64_t* d_n, float temperature, hs_conf_kind_t kind,
+                               hs_seq_reduce_t reduce, int32_t top_k, float* conf, int32_t* argmax,
+                               const int32_t* labels, uint8_t* correct, void* ws, size_t ws_bytes,
+                               uint32_t* d_status, hs_stream_t stream) {
   hs_status_t st = check_logits(logits, dtype, n, seq_len, n_classes, row_stride, temperature, kind, reduce);
   if (st != HS_OK) return st;
+  if (top_k < 0 || top_k > hs::kTopkMax)
+    return fail(HS_ERR_INVALID_ARGUMENT, "top_k = %d outside 0..%d", top_k, hs::kTopkMax);
   if (n > 0 && !conf) return fail(HS_ERR_INVALID_ARGUMENT, "conf output is required");
   if (correct && !labels) return fail(HS_ERR_INVALID_ARGUMENT, "correct requires labels");
   if (ws_bytes < conf_ws(n, seq_len) || (conf_ws(n, seq_len) && !ws))
     return fail(HS_ERR_WORKSPACE_TOO_SMALL, "workspace %zu < %zu", ws_bytes, conf_ws(n, seq_len));
-  return run_confidence(logits, dtype, n, seq_len, n_classes, row_stride, row_index, d_n,
-                        temperature, kind, reduce, conf, argmax, labels, correct, ws, d_status,
-                        (cudaStream_t)stream);
+  if (n == 0) return HS_OK;
+  hs::ConfArgs a = make_conf_args(logits, dtype, n, seq_len, n_classes, row_stride, row_index, d_n,
+                                  temperature, kind);
+  a.top_k = top_k;
+  return run_confidence_args(a, dtype, reduce, conf, argmax, labels, correct, ws, d_status,
+                             (cudaStream_t)stream);
 }
 
 size_t hs_confidence_batched_workspace(int32_t n_batches, int64_t n, int32_t seq_len) {
@@ -404,7 +420,7 @@ hs_status_t hs_cascade_step(int32_t stage, int32_t n_stages, const void* logits,
   return hs_cascade_step_ex(stage, n_stages, logits, dtype, n, seq_len, n_classes, row_stride,
                             row_index, d_n, temperature, kind, reduce, threshold, d_threshold, ids,
                             payload, payload_row_bytes, acc_ids, acc_conf, acc_pred, next_ids,
-                            next_payload, d_counts, ws, ws_bytes, d_status, 0u, stream);
+                            next_payload, d_counts, ws, ws_bytes, d_status, 0, 0u, stream);
 }
 
 hs_status_t hs_cascade_step_ex(int32_t stage, int32_t n_stages, const void* logits, hs_dtype_t dtype,
@@ -415,9 +431,11 @@ hs_status_t hs_cascade_step_ex(int32_t stage, int32_t n_stages, const void* logi
                                int64_t payload_row_bytes, int64_t* acc_ids, float* acc_conf,
                                int32_t* acc_pred, int64_t* next_ids, void* next_payload,
                                int64_t* d_counts, void* ws, size_t ws_bytes, uint32_t* d_status,
-                               uint32_t flags, hs_stream_t stream) {
+                               int32_t top_k, uint32_t flags, hs_stream_t stream) {
   if (flags & ~(uint32_t)HS_STEP_OVERLAP_PREVIOUS)
     return fail(HS_ERR_INVALID_ARGUMENT, "unknown flags 0x%x", flags);
+  if (top_k < 0 || top_k > hs::kTopkMax)
+    return fail(HS_ERR_INVALID_ARGUMENT, "top_k = %d outside 0..%d", top_k, hs::kTopkMax);
   if (n_stages < 1 || stage < 0 || stage >= n_stages)
     return fail(HS_ERR_INVALID_ARGUMENT, "stage %d outside 0..n_stages-1 (%d)", stage, n_stages);
   if (n >= (int64_t(1) << 30)) return fail(HS_ERR_INVALID_ARGUMENT, "n must be < 2^30 per call");
@@ -447,6 +465,7 @@ hs_status_t hs_cascade_step_ex(int32_t stage, int32_t n_stages, const void* logi
   {
     hs::ConfArgs a = make_conf_args(logits, dtype, n, seq_len, n_classes, row_stride, row_index, d_n,
                                     temperature, kind);
+    a.top_k = top_k;
     if (flags & HS_STEP_OVERLAP_PREVIOUS) {
       // CTAs that start late (SMs held by the previous kernel) take fewer rows
       a.ticket = reinterpret_cast<unsigned int*>(w + o_tick);

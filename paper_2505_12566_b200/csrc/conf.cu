@@ -490,6 +490,175 @@ __global__ void __launch_bounds__(256, (NV <= 8 ? 2 : 1)) conf_warp_kernel(const
 }
 
 // ---------------------------------------------------------------------------
+// K1c (NEXT-2): Top-K restricted confidence (reading G4): the
+// softmax over the K largest logits of the row, K <= 32.  One warp per row,
+// streaming the row in chunks of 32 lanes x 4 vectors (next chunk in flight).
+// No exponential per element: per 16-byte vector the packed NaN-propagating
+// max, the lane's running max / first vector (argmax), and one exact fp32
+// compare of the vector max against wt, a lower bound of the row's K-th
+// largest value.  Vectors holding an element > wt are rare: their elements
+// > wt are appended to a per-warp shared buffer, merged into the warp's list
+// (lane j holds entry j) by K max-extractions (redux.sync) when it fills.
+//   Seed: wt = K-th largest of the 32 lane maxima of the first chunk and the
+//   list = K copies of wt.  Invariant: top-K(row) = top-K(list U elements >
+//   wt seen later) -- at least K elements are >= wt, so elements <= wt can be
+//   replaced by copies of wt.  Exact for ties (multisets of values).
+// ---------------------------------------------------------------------------
+constexpr int kTopkU = 4;        // vectors per lane per chunk
+constexpr int kTopkBuf = 64;     // per-warp candidate buffer
+
+__device__ __forceinline__ uint32_t f_order(float f) {   // monotone float -> u32
+  const uint32_t u = __float_as_uint(f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float f_unorder(uint32_t k) {
+  return __uint_as_float((k & 0x80000000u) ? (k & 0x7FFFFFFFu) : ~k);
+}
+template <bool BF16>
+__device__ __forceinline__ float elem(const uint4& v, int e) {
+  const uint32_t w = word(v, BF16 ? e >> 1 : e);
+  if (BF16) return (e & 1) ? bf_hi(w) : bf_lo(w);
+  return __uint_as_float(w);
+}
+
+// new list = the K largest of {list, buf[0..nb)} (descending: lane j = entry j)
+__device__ __forceinline__ float topk_merge(float lst, const float* buf, int nb, int K, int lane) {
+  float v0 = lane < K ? lst : -INFINITY;
+  float v1 = lane < nb ? buf[lane] : -INFINITY;
+  float v2 = lane + 32 < nb ? buf[lane + 32] : -INFINITY;
+  float out = -INFINITY;
+  for (int j = 0; j < K; ++j) {
+    const float lm = fmaxf(v0, fmaxf(v1, v2));
+    const uint32_t key = f_order(lm);
+    const uint32_t mk = __reduce_max_sync(0xFFFFFFFFu, key);
+    const unsigned bal = __ballot_sync(0xFFFFFFFFu, key == mk);
+    if (lane == __ffs(bal) - 1) {          // remove one instance
+      if (v0 == lm) v0 = -INFINITY;
+      else if (v1 == lm) v1 = -INFINITY;
+      else v2 = -INFINITY;
+    }
+    if (lane == j) out = f_unorder(mk);
+  }
+  return out;
+}
+
+template <bool BF16, bool ENTROPY>
+__global__ void __launch_bounds__(256, 2) conf_topk_kernel(const ConfArgs a) {
+  pdl_start();
+  constexpr int VE = BF16 ? 8 : 4, U = kTopkU;
+  __shared__ float s_buf[8][kTopkBuf];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  float* buf = s_buf[warp];
+  const int64_t rows = live_rows(a);
+  const int nvec = a.nvec, K = a.top_k;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const uint32_t ninf = BF16 ? kBf16NegInf2 : kF32NegInf;
+  for (int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; row < rows; row += nwarps) {
+    const RowSrc r = locate(a, row);
+    const uint4* p = reinterpret_cast<const uint4*>(r.base + r.src * a.row_bytes);
+    const int32_t lab = fetch_label(a, r);
+    uint4 x[U], y[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int vi = u * 32 + lane;
+      x[u] = vi < nvec ? ldg_stream(p + vi) : make_uint4(ninf, ninf, ninf, ninf);
+    }
+    uint32_t mw = ninf;                   // NaN-propagating packed row max
+    float best = -INFINITY;               // lane max (exact fp32) and its first vector
+    int bestv = 0x7FFFFFFF;
+    float lst = -INFINITY, wt = -INFINITY;
+    int nb = 0;
+    for (int v0 = 0; v0 < nvec; v0 += 32 * U) {
+      const int v1 = v0 + 32 * U;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {       // next chunk in flight
+        const int vi = v1 + u * 32 + lane;
+        y[u] = vi < nvec ? ldg_stream(p + vi) : make_uint4(ninf, ninf, ninf, ninf);
+      }
+      if (a.tail) {
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (v0 + u * 32 + lane == nvec - 1) x[u] = masked<BF16>(x[u], a.tail);
+      }
+      float cmax[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint32_t w = vec_maxw<BF16>(x[u]);
+        mw = BF16 ? bmax2(mw, w) : __float_as_uint(fmax_nan(__uint_as_float(mw), __uint_as_float(w)));
+        cmax[u] = BF16 ? fmaxf(bf_lo(w), bf_hi(w)) : __uint_as_float(w);
+        if (cmax[u] > best) {
+          best = cmax[u];
+          bestv = v0 + u * 32 + lane;
+        }
+      }
+      if (v0 == 0) {
+        // seed: wt = K-th largest lane max of the first chunk, list = K copies
+        float lm = fmaxf(fmaxf(cmax[0], cmax[1]), fmaxf(cmax[2], cmax[3]));
+        uint32_t key = f_order(lm);
+        for (int j = 0; j < K; ++j) {
+          const uint32_t mk = __reduce_max_sync(0xFFFFFFFFu, key);
+          wt = f_unorder(mk);
+          const unsigned bal = __ballot_sync(0xFFFFFFFFu, key == mk);
+          if (lane == __ffs(bal) - 1) key = 0u;        // below every float key
+        }
+        lst = wt;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const bool cand = cmax[u] > wt;
+        if (__any_sync(0xFFFFFFFFu, cand)) {
+#pragma unroll
+          for (int e = 0; e < VE; ++e) {
+            const float val = elem<BF16>(x[u], e);
+            const bool c = cand && val > wt;
+            const unsigned bal = __ballot_sync(0xFFFFFFFFu, c);
+            if (c) buf[nb + __popc(bal & lanemask_lt())] = val;
+            nb += __popc(bal);
+            if (nb > kTopkBuf - 32) {      // warp-uniform: merge, raise wt
+              __syncwarp();
+              lst = topk_merge(lst, buf, nb, K, lane);
+              wt = __shfl_sync(0xFFFFFFFFu, lst, K - 1);
+              nb = 0;
+              __syncwarp();
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) x[u] = y[u];
+    }
+    __syncwarp();
+    if (nb) lst = topk_merge(lst, buf, nb, K, lane);
+    __syncwarp();
+    // row statistics over the K list entries (m = the row max = entry 0)
+    float m = BF16 ? fmax_nan(bf_lo(mw), bf_hi(mw)) : __uint_as_float(mw);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmax_nan(m, __shfl_xor_sync(0xFFFFFFFFu, m, o));
+    const float c = r.c;
+    float e = 0.f, ea = 0.f;
+    if (lane < K && lst > -INFINITY) {
+      const float av = (lst - m) * c;
+      e = ex2(av);
+      ea = e * av;
+    }
+    const float s = warp_sum(e);
+    const float w = ENTROPY ? warp_sum(ea) : 0.f;
+    // argmax: lowest vector whose max equals m (exact fp32), then its first element
+    unsigned vi = (best == m) ? (unsigned)bestv : 0xFFFFFFFFu;
+    vi = __reduce_min_sync(0xFFFFFFFFu, vi);
+    unsigned am = 0xFFFFFFFFu;
+    if (lane == 0 && vi < (unsigned)nvec) {
+      const uint4 xv = __ldg(p + vi);
+      am = vi * VE + (unsigned)vec_first_eq<BF16>(xv, m);
+    }
+    if (lane == 0) {
+      RowOut ro{m, s, w, am, 1.0f};
+      write_row(a, row, lab, ro);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // K1a (async): the same grouped reduction, but the next row is prefetched with
 // per-lane cp.async (16 B, L2-only) into a per-warp shared-memory double
 // buffer instead of a second register set.  Each lane copies exactly the
@@ -1074,9 +1243,23 @@ const char* confidence_path(int64_t nvec) {
   return "cta-per-row";
 }
 
+template <bool BF16, bool ENTROPY>
+cudaError_t launch_topk(const ConfArgs& a, int64_t rows, cudaStream_t s) {
+  auto k = conf_topk_kernel<BF16, ENTROPY>;
+  static const int occ = occupancy(k, 256);
+  const int64_t want = (rows + 7) / 8;
+  const int64_t cap = (int64_t)num_sms() * occ;
+  const int grid = (int)(want < cap ? (want > 0 ? want : 1) : cap);
+  return launch_pdl(k, dim3(grid), dim3(256), 0, s, a);
+}
+
 cudaError_t launch_confidence(const ConfArgs& a, bool bf16, cudaStream_t s) {
   const int64_t rows = a.n * a.L * a.nbatch;
   const bool ent = a.kind == HS_CONF_ENTROPY;
+  if (a.top_k > 0 && (int64_t)a.top_k < a.C) {
+    if (bf16) return ent ? launch_topk<true, true>(a, rows, s) : launch_topk<true, false>(a, rows, s);
+    return ent ? launch_topk<false, true>(a, rows, s) : launch_topk<false, false>(a, rows, s);
+  }
   if (bf16) return ent ? dispatch<true, true>(a, rows, s) : dispatch<true, false>(a, rows, s);
   return ent ? dispatch<false, true>(a, rows, s) : dispatch<false, false>(a, rows, s);
 }

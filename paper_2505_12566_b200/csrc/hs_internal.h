@@ -68,7 +68,10 @@ struct ConfArgs {
   // async kernel only: read the inputs without waiting for the previous kernel
   // of the stream, wait for it just before exiting (stream order preserved)
   int late_wait;
+  // NEXT-2: softmax restricted to the top_k largest logits (0 = full row)
+  int top_k;
 };
+constexpr int kTopkMax = 32;
 cudaError_t launch_confidence(const ConfArgs& a, bool bf16, cudaStream_t s);
 cudaError_t launch_seq_reduce(const float* tok_conf, const uint8_t* tok_ok, int64_t n,
                               const int64_t* d_n, int L, int reduce, float* conf,

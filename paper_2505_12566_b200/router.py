@@ -39,8 +39,9 @@ class Router:
         self.conf_ws = torch.empty(max(1, K * self.n_val * L * 5 + 1024), dtype=torch.uint8, device=dev)
         # one launch for every stage when the stages share a prediction shape
         s0 = stages[0]
-        self.batched = K <= 8 and all((s.n_classes, s.seq_len, s.kind, s.reduce) ==
-                                      (s0.n_classes, s0.seq_len, s0.kind, s0.reduce) for s in stages)
+        self.batched = K <= 8 and all((s.n_classes, s.seq_len, s.kind, s.reduce, s.top_k) ==
+                                      (s0.n_classes, s0.seq_len, s0.kind, s0.reduce, 0)
+                                      for s in stages)
         self.cal = _calib_out(K, dev, None)
         self.cal_ws = calibrate_workspace(K, self.q, dev)
         self.status = torch.zeros(1, dtype=torch.int32, device=dev)
@@ -70,7 +71,8 @@ class Router:
                        "argmax": self.vargmax[: self.n_val * s.seq_len], "correct": self.vok[k]}
                 confidence(val_logits[k], n=self.n_val, seq_len=s.seq_len, n_classes=s.n_classes,
                            temperature=s.temperature, kind=s.kind, reduce=s.reduce, labels=labels,
-                           out=out, ws=self.conf_ws, status=self.status, stream=stream)
+                           out=out, ws=self.conf_ws, status=self.status, top_k=s.top_k,
+                           stream=stream)
         if time_val is not None:
             time_val[1].record()
         if self.group is None:

@@ -683,3 +683,127 @@ def test_skip_cascade_vs_oracle(hs, mode, key, n):
     assert np.array_equal(d[~near], stage_of[~near])
     if mode == 0 and K > 2:
         assert (visits & 2 == 0).sum() > 0          # some requests really skipped model 2
+
+
+# ---------------------------------------------------------------------------
+# NEXT-2: Top-K restricted confidence (reading G4): K1c vs oracle
+# ---------------------------------------------------------------------------
+def _topk_rows(rng, rows, C, mode):
+    if mode == "normal":
+        return rng.normal(scale=3.0, size=(rows, C)).astype(np.float32)
+    if mode == "ties":         # quantised codes: many equal values around the K-th place
+        return (rng.integers(-40, 40, size=(rows, C)) * 0.0625).astype(np.float32)
+    if mode == "ascending":    # worst case for the first-chunk seed
+        return np.tile(np.linspace(-20, 20, C, dtype=np.float32), (rows, 1))
+    if mode == "descending":
+        return np.tile(np.linspace(20, -20, C, dtype=np.float32), (rows, 1))
+    if mode == "masked":       # few finite classes: fewer than K finite values per row
+        x = np.full((rows, C), -np.inf, np.float32)
+        for i in range(rows):
+            j = rng.choice(C, size=min(C, 1 + i % 5), replace=False)
+            x[i, j] = rng.normal(size=j.size)
+        return x
+    if mode == "tiny":         # zeros and subnormals around the maximum
+        x = np.zeros((rows, C), np.float32)
+        x[:, ::3] = np.float32(1e-40)
+        x[:, 1::7] = np.float32(-1e-41)
+        return x
+    raise ValueError(mode)
+
+
+def _bf16_bits(x32: np.ndarray) -> np.ndarray:
+    return (torch.from_numpy(x32).to(torch.bfloat16).view(torch.int16).numpy().view(np.uint16))
+
+
+@pytest.mark.parametrize("C", [2, 7, 129, 1000, 4099, 32128])
+@pytest.mark.parametrize("dtype", ["bf16", "fp32"])
+def test_topk_confidence_vs_oracle(hs, C, dtype):
+    rng = np.random.default_rng(C + (1 if dtype == "bf16" else 0))
+    rows = 24 if C > 10000 else 96
+    for mode in ("normal", "ties", "ascending", "descending", "masked", "tiny"):
+        x32 = _topk_rows(rng, rows, C, mode)
+        bits = _bf16_bits(x32) if dtype == "bf16" else x32
+        x = to_dev_bits(bits, dtype, (C + 7) // 8 * 8)
+        lab = rng.integers(0, C, size=rows).astype(np.int32)
+        for K in (1, 2, 10, 32):
+            for T, kind in ((1.0, 0), (0.05, 1), (20.0, 2)):
+                r = hs.confidence(x, n=rows, n_classes=C, temperature=T, kind=kind, top_k=K,
+                                  labels=torch.from_numpy(lab).to(dev()))
+                torch.cuda.synchronize()
+                ref = oracle.confidence(host_bits(x), rows, 1, C, x.stride(0), T, kind=kind,
+                                        top_k=K, labels=lab)
+                assert_conf_close(r["conf"].cpu().numpy(), ref["conf"])
+                assert np.array_equal(r["argmax"].cpu().numpy(), ref["argmax"]), (mode, K)
+                assert np.array_equal(r["correct"].cpu().numpy(), ref["correct"]), (mode, K)
+
+
+def test_topk_invalid_rows_and_full_fallback(hs):
+    C = 300
+    x32 = np.random.default_rng(3).normal(size=(6, C)).astype(np.float32)
+    x32[0, 5] = np.nan
+    x32[1, 7] = np.inf
+    x32[2, :] = -np.inf
+    x = to_dev_bits(x32, "fp32")
+    st = torch.zeros(1, dtype=torch.int32, device=dev())
+    r = hs.confidence(x, n=6, n_classes=C, top_k=8, status=st)
+    torch.cuda.synchronize()
+    c = r["conf"].cpu().numpy()
+    assert np.isnan(c[:3]).all() and not np.isnan(c[3:]).any() and int(st.item()) & 1
+    assert (r["argmax"].cpu().numpy()[:3] == -1).all()
+    # top_k >= C is the full softmax
+    full = hs.confidence(x, n=6, n_classes=C)["conf"].cpu().numpy()
+    big = hs.confidence(x, n=6, n_classes=C, top_k=32)["conf"].cpu().numpy()
+    x2 = to_dev_bits(x32[:, :20].copy(), "fp32")
+    a = hs.confidence(x2, n=6, n_classes=20, top_k=32)["conf"].cpu().numpy()
+    b = hs.confidence(x2, n=6, n_classes=20)["conf"].cpu().numpy()
+    torch.cuda.synchronize()
+    assert np.array_equal(a, b, equal_nan=True)
+    assert not np.array_equal(big[3:], full[3:])        # 32 < 300: restricted
+    with pytest.raises(Exception):
+        hs.confidence(x, n=6, n_classes=C, top_k=33)
+
+
+def test_topk_generation_sequences_vs_oracle(hs):
+    """C3-like: T5 vocabulary, 64-token sequences, MIN over tokens of the top-K
+    restricted confidence, gathered rows."""
+    fam = synth.FAMILIES["c3"]
+    n = 6
+    ids = np.array([5, 0, 17, 3, 9, 11], np.int64)
+    bits = synth.logits_np(fam.seed, 1, np.arange(18, dtype=np.int64), fam.L, fam.C, fam.thr[1],
+                           fam.dtype)
+    x = to_dev_bits(bits, fam.dtype)
+    lab = synth.labels_np(fam.seed, np.arange(18, dtype=np.int64), fam.L, fam.C).reshape(-1)
+    for K, reduce in ((10, oracle.SEQ_MIN), (4, oracle.SEQ_MEAN)):
+        r = hs.confidence(x, n=n, seq_len=fam.L, n_classes=fam.C, temperature=fam.temps[1],
+                          kind=1, reduce=reduce, top_k=K, row_index=torch.from_numpy(ids).to(dev()),
+                          labels=torch.from_numpy(lab).to(dev()))
+        torch.cuda.synchronize()
+        ref = oracle.confidence(bits, n, fam.L, fam.C, fam.C, fam.temps[1], kind=1, reduce=reduce,
+                                row_index=ids, labels=lab, top_k=K)
+        assert_conf_close(r["conf"].cpu().numpy(), ref["conf"])
+        assert np.array_equal(r["argmax"].cpu().numpy(), ref["argmax"])
+        assert np.array_equal(r["correct"].cpu().numpy(), ref["correct"])
+
+
+def test_topk_cascade_step_vs_oracle(hs):
+    """A 3-stage cascade whose stages use top-K confidence (StageSpec.top_k)."""
+    rng = np.random.default_rng(21)
+    n, C, K = 3000, 4096, 8
+    xs, conf_o = [], []
+    for k in range(3):
+        x32 = rng.normal(scale=2.0 + k, size=(n, C)).astype(np.float32)
+        bits = _bf16_bits(x32)
+        xs.append(to_dev_bits(bits, "bf16"))
+        conf_o.append(oracle.confidence(bits, n, 1, C, C, 1.0, kind=0, top_k=K)["conf"])
+    conf_o = np.stack(conf_o)
+    t = [0.55, 0.45, 0.0]
+    casc = hs.Cascade(n, [hs.StageSpec(C, 1.0, 1, 0, 0, top_k=K) for _ in range(3)], dev())
+    casc.route(xs, t)
+    res = casc.results()
+    tt = np.array(np.float32(t), np.float64)
+    stage_of = oracle.cascade(conf_o, tt)
+    lists = oracle.stage_lists(stage_of, 3)
+    near = near_mask(conf_o, tt)
+    for k in range(3):
+        got, want = res[k]["ids"].numpy(), lists[k][1]
+        assert np.array_equal(got[~near[got]], want[~near[want]])
