@@ -33,6 +33,7 @@ CONFIG_TEXT = {
     "c3": "4-size T5 cascade, 2,048 sequences x 64 tokens x 32,128 vocab bf16 per GPU (16,384 over 8 GPUs), MIN token confidence, 256 B payload gathered, 512 validation sequences per GPU",
     "c4": "3-stage Llama-like next-token cascade, 8,192 requests x 128,256 vocab bf16 per GPU, entropy confidence, 8 KB hidden-state payload gathered",
     "c5": "5-stage ViT streaming cascade, 1,048,576 requests x 1,000 classes bf16 per GPU (8M over 8 GPUs), validation 131,072 per GPU",
+    "c3k": "c3 with the Top-K (K = 10) restricted token confidence of P:420-424 (NEXT-2), MIN over 64 tokens",
 }
 
 
@@ -165,9 +166,13 @@ def sum_over_ranks(x, world: int):
 # ---------------------------------------------------------------------------
 def family(config: str):
     from workload import synth
-    f = synth.FAMILIES[config]
+    f = synth.FAMILIES.get(config)
     if config == "c5":      # per-GPU shard of the 8-GPU streaming config
         f = synth.scaled(f, n=1 << 20, n_val=1 << 17)
+    if config == "c3k":     # NEXT-2: the T5 shard with Top-K token confidence
+        import dataclasses
+        f = dataclasses.replace(synth.scaled(synth.FAMILIES["c3"], n=2048, n_val=512),
+                                name="c3k_t5x4_top10_bf16", top_k=10)
     if config == "c3":      # per-GPU shard of the 8-GPU T5 config
         f = synth.scaled(f, n=2048, n_val=512)
     return f
@@ -216,7 +221,8 @@ def committed_traffic(config: str):
 def make_router(fam, dev, group):
     import paper_2505_12566_b200 as hs
     from paper_2505_12566_b200.router import Router
-    stages = [hs.StageSpec(fam.C, fam.temps[k], fam.L, fam.kind, fam.reduce) for k in range(fam.K)]
+    stages = [hs.StageSpec(fam.C, fam.temps[k], fam.L, fam.kind, fam.reduce, fam.top_k)
+              for k in range(fam.K)]
     return Router(stages, fam.n, fam.n_val, dev, log2_bins=fam.log2_bins,
                   payload_row_bytes=fam.payload_bytes, group=group)
 
@@ -330,7 +336,8 @@ def run_ours(args, world, rank, local):
         "config": {"workload": fam.name, "description": CONFIG_TEXT[args.config],
                    "requests_per_gpu": fam.n, "validation_per_gpu": fam.n_val, "K": fam.K,
                    "classes": fam.C, "seq_len": fam.L, "logits_dtype": fam.dtype,
-                   "confidence": ["maxprob", "maxprob_sq", "entropy"][fam.kind],
+                   "confidence": ["maxprob", "maxprob_sq", "entropy"][fam.kind]
+                   + (f" over the top {fam.top_k} logits" if fam.top_k else ""),
                    "log2_bins": fam.log2_bins, "parallelism": f"request-sharded dp{world}",
                    "l2": "inputs larger than L2 (per-step logits working set >> 126 MB)",
                    "cuda_graph": graph is not None},
@@ -339,7 +346,8 @@ def run_ours(args, world, rank, local):
         "reach": reach, "thresholds": router.cal["t"].cpu().tolist(), "status": st,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
-                     "kernel": ("conf_async_kernel" if fam.C * fam.elt_bytes <= 2048 else
+                     "kernel": ("conf_topk_kernel" if fam.top_k else
+                                "conf_async_kernel" if fam.C * fam.elt_bytes <= 2048 else
                                 "conf_warp_kernel" if fam.C * fam.elt_bytes <= 8192 else "conf_cta_kernel")
                      + f" (K1 on the validation shard: {fam.K} stages x {fam.n_val} items in one launch"
                      + (", + K2 sequence reduce" if fam.L > 1 else "") + ")",
@@ -522,7 +530,7 @@ def oracle_step(fam, inp):
     ok = np.empty((K, nv), np.uint8)
     for k in range(K):
         r = oracle.confidence(inp["vl"][k], nv, fam.L, fam.C, fam.C, fam.temps[k], kind=fam.kind,
-                              reduce=fam.reduce, labels=inp["lab"])
+                              reduce=fam.reduce, labels=inp["lab"], top_k=fam.top_k)
         ok[k] = r["correct"]
         if k < K - 1:
             conf[k] = r["conf"]
@@ -530,7 +538,7 @@ def oracle_step(fam, inp):
     batch = np.arange(n, dtype=np.int64)
     for k in range(K):
         r = oracle.confidence(inp["rl"][k], len(batch), fam.L, fam.C, fam.C, fam.temps[k],
-                              kind=fam.kind, reduce=fam.reduce, row_index=batch)
+                              kind=fam.kind, reduce=fam.reduce, row_index=batch, top_k=fam.top_k)
         acc, dfr = oracle.route(r["conf"], float(np.float32(cal["t"][k])), k == K - 1)
         batch = batch[dfr]
     return time.perf_counter() - t, n

@@ -496,16 +496,19 @@ __global__ void __launch_bounds__(256, (NV <= 8 ? 2 : 1)) conf_warp_kernel(const
 // No exponential per element: per 16-byte vector the packed NaN-propagating
 // max, the lane's running max / first vector (argmax), and one exact fp32
 // compare of the vector max against wt, a lower bound of the row's K-th
-// largest value.  Vectors holding an element > wt are rare: their elements
-// > wt are appended to a per-warp shared buffer, merged into the warp's list
-// (lane j holds entry j) by K max-extractions (redux.sync) when it fills.
+// largest value.  A lane whose vector has elements > wt appends them to its
+// own shared-memory column (no warp vote per element); at the end of a chunk,
+// if some column may overflow, and at the end of the row, the columns are
+// merged into the warp's top-K list (lane j = entry j) by K max-extractions
+// (redux.sync over the lanes' current candidate maxima; only the owner lane
+// rescans its column).
 //   Seed: wt = K-th largest of the 32 lane maxima of the first chunk and the
 //   list = K copies of wt.  Invariant: top-K(row) = top-K(list U elements >
 //   wt seen later) -- at least K elements are >= wt, so elements <= wt can be
 //   replaced by copies of wt.  Exact for ties (multisets of values).
 // ---------------------------------------------------------------------------
-constexpr int kTopkU = 4;        // vectors per lane per chunk
-constexpr int kTopkBuf = 64;     // per-warp candidate buffer
+constexpr int kTopkU = 4;                  // vectors per lane per chunk
+constexpr int kTopkPB = 40;                // candidate slots per lane (>= 32 per chunk + slack)
 
 __device__ __forceinline__ uint32_t f_order(float f) {   // monotone float -> u32
   const uint32_t u = __float_as_uint(f);
@@ -521,34 +524,43 @@ __device__ __forceinline__ float elem(const uint4& v, int e) {
   return __uint_as_float(w);
 }
 
-// new list = the K largest of {list, buf[0..nb)} (descending: lane j = entry j)
-__device__ __forceinline__ float topk_merge(float lst, const float* buf, int nb, int K, int lane) {
-  float v0 = lane < K ? lst : -INFINITY;
-  float v1 = lane < nb ? buf[lane] : -INFINITY;
-  float v2 = lane + 32 < nb ? buf[lane + 32] : -INFINITY;
+// new list = the K largest of {list} U {column of lane l: col[0..pn_l)}
+// (col[i] = slot i of this lane; stride 32 floats between slots)
+__device__ __noinline__ float topk_merge(float lst, float* col, int pn, int K, int lane) {
+  float lmax = lane < K ? lst : -INFINITY;   // this lane's best remaining value
+  int src = -1;                              // -1: the list entry, i: col[i]
+  for (int i = 0; i < pn; ++i) {
+    const float v = col[i * 32];
+    if (v > lmax) { lmax = v; src = i; }
+  }
+  bool used_list = lane >= K;
   float out = -INFINITY;
   for (int j = 0; j < K; ++j) {
-    const float lm = fmaxf(v0, fmaxf(v1, v2));
-    const uint32_t key = f_order(lm);
+    const uint32_t key = f_order(lmax);
     const uint32_t mk = __reduce_max_sync(0xFFFFFFFFu, key);
     const unsigned bal = __ballot_sync(0xFFFFFFFFu, key == mk);
-    if (lane == __ffs(bal) - 1) {          // remove one instance
-      if (v0 == lm) v0 = -INFINITY;
-      else if (v1 == lm) v1 = -INFINITY;
-      else v2 = -INFINITY;
-    }
     if (lane == j) out = f_unorder(mk);
+    if (lane == __ffs(bal) - 1) {            // consume it, rescan this lane
+      if (src < 0) used_list = true;
+      else col[src * 32] = -INFINITY;
+      lmax = used_list ? -INFINITY : lst;
+      src = -1;
+      for (int i = 0; i < pn; ++i) {
+        const float v = col[i * 32];
+        if (v > lmax) { lmax = v; src = i; }
+      }
+    }
   }
   return out;
 }
 
 template <bool BF16, bool ENTROPY>
-__global__ void __launch_bounds__(256, 2) conf_topk_kernel(const ConfArgs a) {
+__global__ void __launch_bounds__(256, 3) conf_topk_kernel(const ConfArgs a) {
   pdl_start();
   constexpr int VE = BF16 ? 8 : 4, U = kTopkU;
-  __shared__ float s_buf[8][kTopkBuf];
+  __shared__ float s_col[8][kTopkPB][32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  float* buf = s_buf[warp];
+  float* col = &s_col[warp][0][lane];
   const int64_t rows = live_rows(a);
   const int nvec = a.nvec, K = a.top_k;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -558,43 +570,53 @@ __global__ void __launch_bounds__(256, 2) conf_topk_kernel(const ConfArgs a) {
     const uint4* p = reinterpret_cast<const uint4*>(r.base + r.src * a.row_bytes);
     const int32_t lab = fetch_label(a, r);
     uint4 x[U], y[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int vi = u * 32 + lane;
-      x[u] = vi < nvec ? ldg_stream(p + vi) : make_uint4(ninf, ninf, ninf, ninf);
-    }
-    uint32_t mw = ninf;                   // NaN-propagating packed row max
-    float best = -INFINITY;               // lane max (exact fp32) and its first vector
+    uint32_t mw = ninf;                   // NaN-propagating packed lane max
+    // argmax bookkeeping.  bf16: the first vector where the lo / hi half of the
+    // lane's packed max rose (one packed compare per vector; exact whenever the
+    // row max is a normal number -- zero/subnormal maxima are re-scanned below).
+    // fp32: the lane's exact max and its first vector.
+    int bv_lo = 0x7FFFFFFF, bv_hi = 0x7FFFFFFF;
+    float best = -INFINITY;
     int bestv = 0x7FFFFFFF;
     float lst = -INFINITY, wt = -INFINITY;
-    int nb = 0;
-    for (int v0 = 0; v0 < nvec; v0 += 32 * U) {
-      const int v1 = v0 + 32 * U;
-#pragma unroll
-      for (int u = 0; u < U; ++u) {       // next chunk in flight
-        const int vi = v1 + u * 32 + lane;
-        y[u] = vi < nvec ? ldg_stream(p + vi) : make_uint4(ninf, ninf, ninf, ninf);
-      }
+    int pn = 0;                           // this lane's buffered candidates
+    // one chunk: vectors v0 + u*32 + lane of this lane, in registers `c`
+    auto chunk = [&](uint4 (&c)[U], int v0) {
       if (a.tail) {
 #pragma unroll
         for (int u = 0; u < U; ++u)
-          if (v0 + u * 32 + lane == nvec - 1) x[u] = masked<BF16>(x[u], a.tail);
+          if (v0 + u * 32 + lane == nvec - 1) c[u] = masked<BF16>(c[u], a.tail);
       }
-      float cmax[U];
+      uint32_t cw = ninf;                 // packed max of this lane's chunk
+      uint32_t wv[U];                     // packed max of each vector
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const uint32_t w = vec_maxw<BF16>(x[u]);
-        mw = BF16 ? bmax2(mw, w) : __float_as_uint(fmax_nan(__uint_as_float(mw), __uint_as_float(w)));
-        cmax[u] = BF16 ? fmaxf(bf_lo(w), bf_hi(w)) : __uint_as_float(w);
-        if (cmax[u] > best) {
-          best = cmax[u];
-          bestv = v0 + u * 32 + lane;
+        const uint32_t w = vec_maxw<BF16>(c[u]);
+        wv[u] = w;
+        const int vi = v0 + u * 32 + lane;
+        if (BF16) {
+          asm("{\n\t.reg .pred p, h;\n\t"
+              "setp.gt.bf16x2 p|h, %2, %3;\n\t"
+              "@p mov.s32 %0, %4;\n\t"
+              "@h mov.s32 %1, %4;\n\t}"
+              : "+r"(bv_lo), "+r"(bv_hi)
+              : "r"(w), "r"(mw), "r"(vi));
+          mw = bmax2(mw, w);
+          cw = bmax2(cw, w);
+        } else {
+          const float f = __uint_as_float(w);
+          mw = __float_as_uint(fmax_nan(__uint_as_float(mw), f));
+          cw = __float_as_uint(fmaxf(__uint_as_float(cw), f));
+          if (f > best) {
+            best = f;
+            bestv = vi;
+          }
         }
       }
+      const float lmx = BF16 ? fmaxf(bf_lo(cw), bf_hi(cw)) : __uint_as_float(cw);
       if (v0 == 0) {
         // seed: wt = K-th largest lane max of the first chunk, list = K copies
-        float lm = fmaxf(fmaxf(cmax[0], cmax[1]), fmaxf(cmax[2], cmax[3]));
-        uint32_t key = f_order(lm);
+        uint32_t key = f_order(lmx);
         for (int j = 0; j < K; ++j) {
           const uint32_t mk = __reduce_max_sync(0xFFFFFFFFu, key);
           wt = f_unorder(mk);
@@ -603,32 +625,54 @@ __global__ void __launch_bounds__(256, 2) conf_topk_kernel(const ConfArgs a) {
         }
         lst = wt;
       }
+      if (lmx > wt) {                     // rare: append this lane's elements > wt
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const bool cand = cmax[u] > wt;
-        if (__any_sync(0xFFFFFFFFu, cand)) {
+        for (int u = 0; u < U; ++u) {
+          const float vm = BF16 ? fmaxf(bf_lo(wv[u]), bf_hi(wv[u])) : __uint_as_float(wv[u]);
+          if (vm > wt) {                  // only the vectors that hold one
 #pragma unroll
-          for (int e = 0; e < VE; ++e) {
-            const float val = elem<BF16>(x[u], e);
-            const bool c = cand && val > wt;
-            const unsigned bal = __ballot_sync(0xFFFFFFFFu, c);
-            if (c) buf[nb + __popc(bal & lanemask_lt())] = val;
-            nb += __popc(bal);
-            if (nb > kTopkBuf - 32) {      // warp-uniform: merge, raise wt
-              __syncwarp();
-              lst = topk_merge(lst, buf, nb, K, lane);
-              wt = __shfl_sync(0xFFFFFFFFu, lst, K - 1);
-              nb = 0;
-              __syncwarp();
+            for (int e = 0; e < VE; ++e) {
+              const float val = elem<BF16>(c[u], e);
+              if (val > wt) col[32 * pn++] = val;
             }
           }
         }
       }
+      // merge as soon as K candidates are buffered (raises wt early, so later
+      // chunks rarely have any) or when a column could overflow in the next chunk
+      if (__reduce_add_sync(0xFFFFFFFFu, (unsigned)pn) >= (unsigned)K ||
+          __any_sync(0xFFFFFFFFu, pn > kTopkPB - 32)) {
+        __syncwarp();
+        lst = topk_merge(lst, col, pn, K, lane);
+        wt = __shfl_sync(0xFFFFFFFFu, lst, K - 1);
+        pn = 0;
+        __syncwarp();
+      }
+    };
+    auto load = [&](uint4 (&c)[U], int v0) {
+      if (v0 + 32 * U <= nvec) {          // full chunk: unconditional loads
 #pragma unroll
-      for (int u = 0; u < U; ++u) x[u] = y[u];
+        for (int u = 0; u < U; ++u) c[u] = ldg_stream(p + v0 + u * 32 + lane);
+      } else {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int vi = v0 + u * 32 + lane;
+          c[u] = vi < nvec ? ldg_stream(p + vi) : make_uint4(ninf, ninf, ninf, ninf);
+        }
+      }
+    };
+    // ping-pong: the next chunk's loads are issued before the current chunk
+    load(x, 0);
+    for (int v0 = 0;; v0 += 64 * U) {
+      load(y, v0 + 32 * U);
+      chunk(x, v0);
+      if (v0 + 32 * U >= nvec) break;
+      load(x, v0 + 64 * U);
+      chunk(y, v0 + 32 * U);
+      if (v0 + 64 * U >= nvec) break;
     }
     __syncwarp();
-    if (nb) lst = topk_merge(lst, buf, nb, K, lane);
+    if (__any_sync(0xFFFFFFFFu, pn > 0)) lst = topk_merge(lst, col, pn, K, lane);
     __syncwarp();
     // row statistics over the K list entries (m = the row max = entry 0)
     float m = BF16 ? fmax_nan(bf_lo(mw), bf_hi(mw)) : __uint_as_float(mw);
@@ -643,9 +687,27 @@ __global__ void __launch_bounds__(256, 2) conf_topk_kernel(const ConfArgs a) {
     }
     const float s = warp_sum(e);
     const float w = ENTROPY ? warp_sum(ea) : 0.f;
-    // argmax: lowest vector whose max equals m (exact fp32), then its first element
-    unsigned vi = (best == m) ? (unsigned)bestv : 0xFFFFFFFFu;
-    vi = __reduce_min_sync(0xFFFFFFFFu, vi);
+    // argmax: lowest vector holding m, then its first element (exact fp32)
+    unsigned vi;
+    if (BF16) {
+      const float lo = bf_lo(mw), hi = bf_hi(mw);
+      const int fv = lo > hi ? bv_lo : hi > lo ? bv_hi : min(bv_lo, bv_hi);
+      vi = (fmaxf(lo, hi) == m) ? (unsigned)fv : 0xFFFFFFFFu;
+      vi = __reduce_min_sync(0xFFFFFFFFu, vi);
+      if (__any_sync(0xFFFFFFFFu, m == m && !(fabsf(m) >= 1.17549435e-38f))) {
+        // zero / subnormal row max: the packed compares flushed; exact re-scan
+        unsigned f = 0xFFFFFFFFu;
+        for (int v = lane; v < nvec; v += 32) {
+          uint4 q = __ldg(p + v);
+          if (a.tail && v == nvec - 1) q = masked<BF16>(q, a.tail);
+          if (maxw_has<BF16>(vec_maxw<BF16>(q), m)) { f = (unsigned)v; break; }
+        }
+        vi = __reduce_min_sync(0xFFFFFFFFu, f);
+      }
+    } else {
+      vi = (best == m) ? (unsigned)bestv : 0xFFFFFFFFu;
+      vi = __reduce_min_sync(0xFFFFFFFFu, vi);
+    }
     unsigned am = 0xFFFFFFFFu;
     if (lane == 0 && vi < (unsigned)nvec) {
       const uint4 xv = __ldg(p + vi);

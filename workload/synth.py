@@ -161,6 +161,7 @@ class Family:
     payload_bytes: int = 0      # deferred-request payload row (bytes)
     log2_bins: int = 12
     seed: int = 0x250512566
+    top_k: int = 0              # NEXT-2: stage confidence over the top_k logits (0 = full)
 
     @property
     def K(self):
