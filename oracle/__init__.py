@@ -62,6 +62,11 @@ def lib():
             L.hso_calibrate.argtypes = [ctypes.c_int, _I64, _P, _P, ctypes.c_int, _I64,
                                         ctypes.c_int, _P, _P, _P, _P, _P]
             L.hso_calibrate.restype = ctypes.c_int
+            L.hso_nll.argtypes = [_P, ctypes.c_int, _I64, _I64, _I64, _P, ctypes.c_double, _P]
+            L.hso_nll.restype = ctypes.c_double
+            L.hso_fit_temperature.argtypes = [_P, ctypes.c_int, _I64, _I64, _I64, _P,
+                                              ctypes.c_double, ctypes.c_double]
+            L.hso_fit_temperature.restype = ctypes.c_double
             L.hso_skip_edges.argtypes = [ctypes.c_double, ctypes.c_int, ctypes.c_int, _P]
             L.hso_skip_edges.restype = None
             L.hso_skip_band.argtypes = [ctypes.c_double, _P, ctypes.c_int]
@@ -162,6 +167,44 @@ def cascade(conf_by_stage: np.ndarray, thresholds) -> np.ndarray:
     out = np.empty(n, np.int32)
     lib().hso_cascade(int(K), int(n), _ptr(c), _ptr(t), _ptr(out))
     return out
+
+
+# --------------------------------------------------------------------------
+# NEXT-3: temperature fitting, Eq. 1; clamp range S:112.
+# --------------------------------------------------------------------------
+T_MIN, T_MAX = float(np.exp(-4.0)), float(np.exp(4.0))
+
+
+def _rows(logits):
+    flat = np.ascontiguousarray(logits)
+    if flat.dtype == np.float32:
+        return flat, F32
+    if flat.dtype == np.uint16:
+        return flat, BF16
+    raise TypeError("oracle takes float32 or raw-bf16 (uint16) logits")
+
+
+def nll(logits, labels, T: float, n_classes: int | None = None, row_stride: int | None = None):
+    """(mean NLL of the temperature-scaled softmax, rows used) in fp64."""
+    x, dt = _rows(logits)
+    n = x.shape[0]
+    C = int(n_classes or x.shape[1])
+    stride = int(row_stride or x.shape[1])
+    lab = np.ascontiguousarray(labels, dtype=np.int32)
+    used = ctypes.c_int64()
+    v = lib().hso_nll(_ptr(x), dt, n, C, stride, _ptr(lab), float(T), ctypes.byref(used))
+    return v, used.value
+
+
+def fit_temperature(logits, labels, n_classes: int | None = None, row_stride: int | None = None,
+                    t_lo: float = T_MIN, t_hi: float = T_MAX) -> float:
+    """argmin_T NLL(T) over [t_lo, t_hi] (bisection on the beta-derivative)."""
+    x, dt = _rows(logits)
+    n = x.shape[0]
+    C = int(n_classes or x.shape[1])
+    stride = int(row_stride or x.shape[1])
+    lab = np.ascontiguousarray(labels, dtype=np.int32)
+    return lib().hso_fit_temperature(_ptr(x), dt, n, C, stride, _ptr(lab), float(t_lo), float(t_hi))
 
 
 SKIP_UNIFORM, SKIP_DECADE = 0, 1

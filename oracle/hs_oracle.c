@@ -225,6 +225,78 @@ int hso_confidence(const void* logits, int dtype, int64_t n_seq, int L, int64_t 
 }
 
 /* ------------------------------------------------------------------------- */
+/* NEXT-3. Temperature fitting (Eq. 1).                                      */
+/*   "learn parameters theta that minimize the NLL between        */
+/*   confidence scores and labels Y on the validation dataset" with Temperature */
+/*   Scaling: NLL(T) = (1/n) sum_i [ log sum_j exp(x_ij / T) - x_iy / T ]. */
+/*   The minimiser over the clamp range T in [e^-4, e^4] has a plain   */
+/*   definition; NLL is convex in beta = 1/T (a log-sum-exp of functions linear */
+/*   in beta minus a linear term), so dNLL/dbeta = mean_i (E_p[x_i] - x_iy) is */
+/*   non-decreasing and the minimiser is where it changes sign (or a clamp     */
+/*   end).  This oracle evaluates that derivative in fp64 (Neumaier sums) and */
+/*   bisects on beta to 1e-15 relative.  Rows with a non-finite entry are     */
+/*   skipped (masked -inf classes are allowed, p = 0).                        */
+/* ------------------------------------------------------------------------- */
+static void nll_terms(const void* logits, int dtype, int64_t n, int64_t C, int64_t stride,
+                      const int32_t* labels, double beta, double* nll, double* grad, int64_t* used) {
+    nsum_t L = {0, 0}, G = {0, 0};
+    int64_t u = 0;
+    double* row = (double*)malloc(sizeof(double) * (size_t)C);
+    for (int64_t i = 0; i < n; ++i) {
+        int ok = 1, any = 0;
+        double mx = -INFINITY;
+        for (int64_t j = 0; j < C; ++j) {
+            row[j] = load_logit(logits, dtype, i * stride + j);
+            if (isnan(row[j]) || (isinf(row[j]) && row[j] > 0)) ok = 0;
+            if (!isinf(row[j])) { any = 1; if (row[j] > mx) mx = row[j]; }
+        }
+        double xy = row[labels[i]];
+        if (!ok || !any || isinf(xy)) continue;
+        nsum_t s = {0, 0}, sx = {0, 0};
+        for (int64_t j = 0; j < C; ++j) {
+            if (isinf(row[j])) continue;
+            double e = exp(beta * (row[j] - mx));
+            nsum_add(&s, e);
+            nsum_add(&sx, e * (row[j] - mx));
+        }
+        double S = nsum_get(&s);
+        nsum_add(&L, beta * (mx - xy) + log(S));          /* LSE(beta x) - beta x_y */
+        nsum_add(&G, nsum_get(&sx) / S - (xy - mx));       /* E_p[x] - x_y          */
+        ++u;
+    }
+    free(row);
+    *nll = u ? nsum_get(&L) / (double)u : NAN;
+    *grad = u ? nsum_get(&G) / (double)u : NAN;
+    *used = u;
+}
+
+/* mean NLL at temperature T (Eq. 1's objective); rows used -> *used */
+double hso_nll(const void* logits, int dtype, int64_t n, int64_t C, int64_t stride,
+               const int32_t* labels, double T, int64_t* used) {
+    double nll, g;
+    nll_terms(logits, dtype, n, C, stride, labels, 1.0 / T, &nll, &g, used);
+    return nll;
+}
+
+/* argmin_{T in [t_lo, t_hi]} NLL(T); returns T (NAN if no usable row) */
+double hso_fit_temperature(const void* logits, int dtype, int64_t n, int64_t C, int64_t stride,
+                           const int32_t* labels, double t_lo, double t_hi) {
+    double b_lo = 1.0 / t_hi, b_hi = 1.0 / t_lo, nll, g;
+    int64_t used;
+    nll_terms(logits, dtype, n, C, stride, labels, b_lo, &nll, &g, &used);
+    if (!used) return NAN;
+    if (g >= 0) return t_hi;                     /* increasing over the range */
+    nll_terms(logits, dtype, n, C, stride, labels, b_hi, &nll, &g, &used);
+    if (g <= 0) return t_lo;                     /* decreasing over the range */
+    for (int it = 0; it < 200 && (b_hi - b_lo) > 1e-15 * b_hi; ++it) {
+        double b = 0.5 * (b_lo + b_hi);
+        nll_terms(logits, dtype, n, C, stride, labels, b, &nll, &g, &used);
+        if (g > 0) b_hi = b; else b_lo = b;
+    }
+    return 2.0 / (b_lo + b_hi);
+}
+
+/* ------------------------------------------------------------------------- */
 /* D3 + D4. Threshold test and stable split of one stage's batch.            */
 /*   "requests with scores below a threshold at a model in the    */
 /*   dataflow are passed to larger models" -> defer iff c < t, accept iff    */
