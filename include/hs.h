@@ -69,6 +69,7 @@ typedef enum { HS_CONF_MAXPROB = 0, HS_CONF_MAXPROB_SQ = 1, HS_CONF_ENTROPY = 2 
 typedef enum { HS_SEQ_NONE = 0, HS_SEQ_MIN = 1, HS_SEQ_MEAN = 2 } hs_seq_reduce_t;
 
 #define HS_STATUS_NONFINITE 1u
+#define HS_STATUS_NOT_CONVERGED 2u   /* hs_fit_temperature: pass budget exhausted */
 
 /* ------------------------------------------------------------------------ */
 /* Confidence.                                        */
@@ -280,6 +281,41 @@ hs_status_t hs_calibrate_select(int32_t K, int32_t log2_bins, int32_t round, int
                                 float* d_thresholds, int64_t* d_reach, int64_t* d_handled,
                                 int64_t* d_correct_total, void* ws, size_t ws_bytes,
                                 hs_stream_t stream);
+
+/* ------------------------------------------------------------------------ */
+/* Temperature fitting (NEXT-3; Eq. 1; clamp range S:112).         */
+/* ------------------------------------------------------------------------ */
+/* For every stage model b (0 <= b < n_batches <= 8), on the SAME labelled
+ * validation rows ("learn parameters theta that minimize the NLL between
+ * confidence scores and labels Y on the validation dataset"):
+ *   T_b = argmin_{t_lo <= T <= t_hi} NLL_b(T),
+ *   NLL_b(T) = (1/u_b) sum_{used rows i} [ log sum_j exp(x_ij / T) - x_{i,labels[i]} / T ].
+ * logits[b] (host array of device pointers): [n x row_stride] row-major, dtype
+ * elements, n_classes valid per row; labels: device int32 [n], shared.  A row
+ * is USED iff it is valid (no NaN / +inf, not all -inf) and its label logit is
+ * finite with 0 <= label < n_classes; -inf entries are masked classes.  Rows
+ * with NaN / +inf (or all -inf) also set HS_STATUS_NONFINITE in *d_status.
+ * NLL is convex in beta = 1/T; the minimiser is found by a safeguarded Newton
+ * iteration on beta (one pass over the logits per iterate; ~4-6 passes),
+ * converged when a Newton step or the bracket is below 2^-21 relative; a
+ * clamp end is returned exactly.  All passes of all stage models run in ONE
+ * persistent cooperative kernel launch (one CTA per SM).
+ * Outputs (device): d_T[b] fp32 (NaN if no row is used), and optionally
+ * d_nll[b] (fp64 mean NLL at the last temperature swept, within the
+ * tolerance of d_T[b]), d_passes[b] (passes at a temperature), d_used[b].
+ * max_passes (1..256) bounds the passes; when a model has not converged within
+ * it, d_T[b] is the last swept temperature and HS_STATUS_NOT_CONVERGED is ORed
+ * into *d_status.  Requires 0 < t_lo <= t_hi < inf.  Workspace:
+ * hs_fit_temperature_workspace(n_batches, n) bytes (no zero-fill needed).
+ * Errors: INVALID_ARGUMENT (as hs_confidence, plus the range, max_passes and
+ * required pointers), WORKSPACE_TOO_SMALL, CUDA (launch failure, e.g. a
+ * cooperative launch that cannot be co-resident). */
+size_t hs_fit_temperature_workspace(int32_t n_batches, int64_t n);
+hs_status_t hs_fit_temperature(const void* const* logits, int32_t n_batches, hs_dtype_t dtype,
+                               int64_t n, int64_t n_classes, int64_t row_stride,
+                               const int32_t* labels, double t_lo, double t_hi, int32_t max_passes,
+                               float* d_T, double* d_nll, int32_t* d_passes, int64_t* d_used,
+                               void* ws, size_t ws_bytes, uint32_t* d_status, hs_stream_t stream);
 
 /* ------------------------------------------------------------------------ */
 /* Diagnostics.                                                              */

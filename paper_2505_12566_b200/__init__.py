@@ -26,9 +26,10 @@ HS_STEP_OVERLAP_PREVIOUS = 1     # hs_cascade_step_ex flag (include/hs.h)
 _KINDS = {"maxprob": MAXPROB, "maxprob_sq": MAXPROB_SQ, "entropy": ENTROPY}
 _REDUCES = {"none": SEQ_NONE, "min": SEQ_MIN, "mean": SEQ_MEAN}
 STATUS_NONFINITE = 1
+STATUS_NOT_CONVERGED = 2
 
 __all__ = ["confidence", "confidence_batched", "route_compact", "cascade_step", "calibrate_thresholds",
-           "calibrate_begin", "calibrate_histogram", "calibrate_select", "Cascade", "HsError",
+           "calibrate_begin", "calibrate_histogram", "calibrate_select", "fit_temperature", "Cascade", "HsError",
            "launch_count", "MAXPROB", "MAXPROB_SQ", "ENTROPY", "SEQ_NONE", "SEQ_MIN", "SEQ_MEAN"]
 
 
@@ -155,6 +156,45 @@ def confidence_batched(logits: list, temperatures, *, n: int | None = None, seq_
               int(x0.stride(0)), _p(row_index), _kind(kind), _reduce(reduce), _p(out["conf"]),
               _p(out.get("argmax")), _p(labels), _p(out.get("correct")), _p(ws),
               0 if ws is None else ws.numel(), _p(status), _stream(stream))
+    return out
+
+
+# ---------------------------------------------------------------------------
+# hs_fit_temperature (NEXT-3: Eq. 1)
+# ---------------------------------------------------------------------------
+T_MIN, T_MAX = 0.01831563888873418, 54.598150033144236     # e^-4, e^4: clamp range of S:112
+
+
+def fit_temperature(logits: list, labels: torch.Tensor, *, n: int | None = None,
+                    n_classes: int | None = None, t_lo: float = T_MIN, t_hi: float = T_MAX,
+                    max_passes: int = 64, status: torch.Tensor | None = None,
+                    out: dict | None = None, ws: torch.Tensor | None = None, stream=None) -> dict:
+    """Fit one temperature per stage model on the same labelled validation rows
+    (Eq. 1: minimise the NLL of softmax(x / T) over [t_lo, t_hi]); all stage
+    models in one persistent launch.  Returns ``T`` f32[K], ``nll`` f64[K]
+    (mean NLL at the last swept temperature), ``passes`` i32[K], ``used`` i64[K]."""
+    import ctypes
+    nb = len(logits)
+    x0 = logits[0]
+    _check_cuda(*logits, labels, status)
+    for x in logits:
+        if x.dim() != 2 or x.stride(1) != 1 or x.stride(0) != x0.stride(0) or x.dtype != x0.dtype:
+            raise ValueError("stage logits must share dtype, shape and row stride")
+    C = int(n_classes or x0.shape[1])
+    n = int(x0.shape[0] if n is None else n)
+    dev = x0.device
+    out = dict(out or {})
+    out.setdefault("T", torch.empty(nb, dtype=torch.float32, device=dev))
+    out.setdefault("nll", torch.empty(nb, dtype=torch.float64, device=dev))
+    out.setdefault("passes", torch.empty(nb, dtype=torch.int32, device=dev))
+    out.setdefault("used", torch.empty(nb, dtype=torch.int64, device=dev))
+    need = lib().hs_fit_temperature_workspace(nb, n)
+    if ws is None or ws.numel() < need:
+        ws = torch.empty(need, dtype=torch.uint8, device=dev)
+    ptrs = (ctypes.c_void_p * nb)(*[x.data_ptr() for x in logits])
+    _abi.call("hs_fit_temperature", ptrs, nb, _dtype_code(x0), n, C, int(x0.stride(0)), _p(labels),
+              float(t_lo), float(t_hi), int(max_passes), _p(out["T"]), _p(out["nll"]),
+              _p(out["passes"]), _p(out["used"]), _p(ws), ws.numel(), _p(status), _stream(stream))
     return out
 
 

@@ -46,6 +46,9 @@ SIGNATURES = {
     "hs_calibrate_hist_bytes": (SZ, [I32]),
     "hs_calibrate_histogram": (I32, [P, P, I32, I64, I32, I32, P, P, SZ, P]),
     "hs_calibrate_select": (I32, [I32, I32, I32, P, P, P, P, P, P, SZ, P]),
+    "hs_fit_temperature_workspace": (SZ, [I32, I64]),
+    "hs_fit_temperature": (I32, [P, I32, I32, I64, I64, I64, P, ctypes.c_double, ctypes.c_double, I32,
+                                 P, P, P, P, P, SZ, P, P]),
     "hs_status_string": (ctypes.c_char_p, [I32]),
     "hs_last_error": (ctypes.c_char_p, []),
     "hs_launch_count": (ctypes.c_uint64, []),

@@ -256,6 +256,56 @@ hs_status_t hs_confidence_batched(const void* const* logits, const float* temper
                              (cudaStream_t)stream);
 }
 
+size_t hs_fit_temperature_workspace(int32_t n_batches, int64_t n) {
+  return hs::temp_fit_ws_bytes(n_batches < 1 ? 1 : n_batches, n);
+}
+
+hs_status_t hs_fit_temperature(const void* const* logits, int32_t n_batches, hs_dtype_t dtype,
+                               int64_t n, int64_t n_classes, int64_t row_stride,
+                               const int32_t* labels, double t_lo, double t_hi, int32_t max_passes,
+                               float* d_T, double* d_nll, int32_t* d_passes, int64_t* d_used,
+                               void* ws, size_t ws_bytes, uint32_t* d_status, hs_stream_t stream) {
+  if (!logits) return fail(HS_ERR_INVALID_ARGUMENT, "logits array is required");
+  if (n_batches < 1 || n_batches > hs::kMaxBatch)
+    return fail(HS_ERR_INVALID_ARGUMENT, "n_batches = %d outside 1..%d", n_batches, hs::kMaxBatch);
+  for (int b = 0; b < n_batches; ++b) {
+    hs_status_t st = check_logits(logits[b], dtype, n, 1, n_classes, row_stride, 1.0f,
+                                  HS_CONF_MAXPROB, HS_SEQ_NONE);
+    if (st != HS_OK) return st;
+  }
+  if (!(t_lo > 0.0) || !(t_lo <= t_hi) || !std::isfinite(t_hi))
+    return fail(HS_ERR_INVALID_ARGUMENT, "temperature range must satisfy 0 < t_lo <= t_hi < inf");
+  if (max_passes < 1 || max_passes > 256)
+    return fail(HS_ERR_INVALID_ARGUMENT, "max_passes = %d outside 1..256", max_passes);
+  if (!d_T) return fail(HS_ERR_INVALID_ARGUMENT, "d_T output is required");
+  if (n > 0 && !labels) return fail(HS_ERR_INVALID_ARGUMENT, "labels are required");
+  const size_t need = hs::temp_fit_ws_bytes(n_batches, n);
+  if (ws_bytes < need || !ws) return fail(HS_ERR_WORKSPACE_TOO_SMALL, "workspace %zu < %zu", ws_bytes, need);
+  hs::TfArgs a{};
+  const int eb = dtype == HS_BF16 ? 2 : 4, ve = 16 / eb;
+  for (int b = 0; b < n_batches; ++b) a.bptr[b] = logits[b];
+  a.nbatch = n_batches;
+  a.n = n;
+  a.row_bytes = row_stride * eb;
+  a.C = n_classes;
+  a.nvec = (int)((n_classes + ve - 1) / ve);
+  a.tail = (int)(n_classes % ve);
+  a.labels = labels;
+  a.blo0 = 1.0 / t_hi;
+  a.bhi0 = 1.0 / t_lo;
+  a.t_lo = t_lo;
+  a.t_hi = t_hi;
+  a.tol = 1.0 / (double)(1 << 21);
+  a.max_passes = max_passes;
+  a.T = d_T;
+  a.nll = d_nll;
+  a.passes = d_passes;
+  a.used = d_used;
+  a.status = d_status;
+  return cuda_check(hs::launch_temp_fit(a, dtype == HS_BF16, ws, (cudaStream_t)stream),
+                    "temperature fitting kernel");
+}
+
 size_t hs_route_compact_workspace(int64_t n) { return hs::compact_ws_bytes(n); }
 
 static hs_status_t route_compact_impl(const float* conf, int64_t n, const int64_t* d_n,

@@ -148,4 +148,29 @@ cudaError_t launch_calib_select(int K, int q, int round, int32_t* b_idx, float* 
                                 int64_t* reach, int64_t* handled, int64_t* correct_total,
                                 void* ws, cudaStream_t s);
 
+// ---- NEXT-3: temperature fitting (Eq. 1) ------------------------------------
+constexpr int kTfMaxGrid = 1024;   // CTAs of the persistent launch (partials sized for it)
+struct TfArgs {
+  const void* bptr[kMaxBatch];     // stage b's validation logits
+  int nbatch;                      // stage models fitted together
+  int64_t n;                       // rows per stage
+  int64_t row_bytes;               // row_stride * element size (multiple of 16)
+  int64_t C;                       // classes
+  int nvec, tail;                  // 16-byte vectors per row, C % elements-per-vector
+  const int32_t* labels;           // [n], shared by every stage
+  double blo0, bhi0;               // beta = 1/T range [1/t_hi, 1/t_lo]
+  double t_lo, t_hi;               // clamp range of T (returned exactly at a clamp)
+  double tol;                      // relative Newton-step / bracket tolerance on beta
+  int max_passes;                  // sweeps at a temperature (after the max sweep)
+  float2* rowstat;                 // ws: [nbatch * n] {m, x_y - m}; m = NaN: row unused
+  double* partial;                 // ws: [2][grid][nbatch][3]
+  float* T;                        // [nbatch] fitted temperatures
+  double* nll;                     // [nbatch] mean NLL at the last swept temperature, or NULL
+  int32_t* passes;                 // [nbatch] sweeps used, or NULL
+  int64_t* used;                   // [nbatch] rows in the mean, or NULL
+  uint32_t* status;                // or NULL
+};
+size_t temp_fit_ws_bytes(int nbatch, int64_t n);
+cudaError_t launch_temp_fit(TfArgs a, bool bf16, void* ws, cudaStream_t s);
+
 }  // namespace hs

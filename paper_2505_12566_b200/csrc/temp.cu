@@ -1,0 +1,442 @@
+// temp.cu -- NEXT-3: temperature fitting, Eq. 1.
+//
+// Temperature Scaling learns one T per stage model by minimising
+// the NLL between the temperature-scaled softmax and the labels of the
+// validation set:
+//     NLL(T) = (1/n) sum_i [ LSE_j(x_ij / T) - x_{i,y_i} / T ].
+// With beta = 1/T and d_ij = x_ij - m_i (m_i = row max), per row
+//     nll_i = ln s_i - beta * dy_i,   s_i = sum_j e^{beta d_ij},   dy_i = x_{i,y_i} - m_i
+//     g_i   = dnll_i/dbeta   = E_p[d_i] - dy_i
+//     h_i   = d2nll_i/dbeta2 = Var_p[d_i] >= 0,
+// so NLL is convex in beta and its minimiser over the clamp range
+// [t_lo, t_hi] is where the mean of g changes sign, or a clamp end.
+//
+// Structure exploited here: m_i, dy_i and row validity do not depend on T, so
+// they are computed once (sweep 0, 8 bytes per row to the workspace); every
+// later sweep is ONE pass over the logits at one beta per stage model giving
+// (sum nll, sum g, sum h) -- one MUFU ex2 and ~5 issue slots per logit.  A
+// safeguarded Newton iteration on beta (Newton inside the bracket, probe of an
+// unvisited clamp end, geometric bisection when a step does not halve) needs
+// ~4-6 sweeps.  All sweeps of all stage models run in ONE persistent
+// cooperative launch (one 1024-thread CTA per SM): per sweep every CTA writes
+// its per-stage partial sums, one grid barrier, then EVERY CTA reduces the
+// partials in the same fixed order and runs the identical update (no second
+// barrier, no broadcast; deterministic bitwise).  Per-row sums are fp32
+// (exact x - m, MUFU ex2), cross-row sums fp64.
+#include <cooperative_groups.h>
+
+#include <cmath>
+
+#include "hs_common.cuh"
+#include "hs_internal.h"
+
+namespace hs {
+
+namespace cg = cooperative_groups;
+
+namespace {
+
+constexpr int kTfThreads = 1024;
+constexpr int kTfWarps = kTfThreads / 32;
+constexpr int kTfU = 4;                 // 16-byte vectors per lane per chunk
+
+struct TfState {
+  double lo, hi, beta;      // bracket on beta = 1/T, point of the next sweep
+  double dx, dx_old;        // last two step lengths (bisection safeguard)
+  double nll, swept;        // mean NLL at the last swept beta, and that beta
+  double T;                 // result
+  long long used;           // rows entering the mean
+  int lo_known, hi_known;   // g(lo) < 0 / g(hi) > 0 observed (else: clamp end not yet swept)
+  int done, passes, converged;
+};
+
+__device__ __forceinline__ uint32_t wordq(const uint4& v, int q) {
+  return q == 0 ? v.x : q == 1 ? v.y : q == 2 ? v.z : v.w;
+}
+
+// -inf for elements past C in the row's last 16-byte vector
+template <bool BF16>
+__device__ __forceinline__ uint4 tail_mask(const uint4& v, int tail) {
+  uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    if (BF16) {
+      const uint32_t lo = (2 * q < tail) ? (w[q] & 0xFFFFu) : 0xFF80u;
+      const uint32_t hi = (2 * q + 1 < tail) ? (w[q] & 0xFFFF0000u) : 0xFF800000u;
+      w[q] = lo | hi;
+    } else if (q >= tail) {
+      w[q] = kF32NegInf;
+    }
+  }
+  return make_uint4(w[0], w[1], w[2], w[3]);
+}
+
+// Loads the group's chunk (vectors v0 + k*G + gl); slots past the row hold -inf.
+template <bool BF16, int G>
+__device__ __forceinline__ void load_chunk(uint4 (&v)[kTfU], const uint4* rowp, int v0, int gl,
+                                           int nvec, int tail, bool active) {
+  const uint32_t f = BF16 ? kBf16NegInf2 : kF32NegInf;
+#pragma unroll
+  for (int k = 0; k < kTfU; ++k) {
+    const int vi = v0 + k * G + gl;
+    if (active && vi < nvec) {
+      v[k] = ldg_stream(rowp + vi);
+      if (tail && vi == nvec - 1) v[k] = tail_mask<BF16>(v[k], tail);
+    } else {
+      v[k] = make_uint4(f, f, f, f);
+    }
+  }
+}
+
+template <typename T, int G>
+__device__ __forceinline__ T group_sum(T v) {
+#pragma unroll
+  for (int o = G / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+  return v;
+}
+
+// bf16x2 word L <= m - off with 2^{(L - m) c} < 2^-127 (flushed to 0 by
+// ex2.approx.ftz): clamping x >= L leaves every non-zero term untouched and
+// turns -inf (masked class) into a finite value, so e * d stays 0.  The
+// offset is at least |m| * 2^-7 so that m - off is not absorbed by rounding.
+__device__ __forceinline__ uint32_t clamp_word_bf16(float m, float c) {
+  const float off = fmaxf(128.0f / c, fabsf(m) * 0.0078125f);
+  const uint32_t u = (uint32_t)__bfloat16_as_ushort(__float2bfloat16_rd(m - off));
+  return u | (u << 16);
+}
+
+// One safeguarded Newton update of a stage's state from the means at s.beta.
+__device__ void tf_update(TfState& s, double nll, double g, double h, const TfArgs& a) {
+  const double beta = s.beta;
+  s.passes += 1;
+  s.nll = nll;
+  s.swept = beta;
+  if (beta == a.blo0 && g >= 0.0) {        // NLL non-decreasing over the range: T = t_hi
+    s.T = a.t_hi;
+    s.done = s.converged = 1;
+    return;
+  }
+  if (beta == a.bhi0 && g <= 0.0) {        // non-increasing: T = t_lo
+    s.T = a.t_lo;
+    s.done = s.converged = 1;
+    return;
+  }
+  // g == 0 with h == 0: every used row is saturated in fp32 (all mass on the
+  // label, the other terms below 2^-126); the true derivative is negative
+  // there, so the point is treated as g < 0 (towards lower T)
+  if (g == 0.0 && h > 0.0) {
+    s.T = 1.0 / beta;
+    s.done = s.converged = 1;
+    return;
+  }
+  if (g > 0.0) {
+    s.hi = beta;
+    s.hi_known = 1;
+  } else {
+    s.lo = beta;
+    s.lo_known = 1;
+  }
+  const double step = g / h;
+  const double bn = beta - step;
+  double next;
+  if (h > 0.0 && isfinite(bn) && bn > s.lo && bn < s.hi && fabs(2.0 * step) <= s.dx_old) {
+    if (fabs(step) <= a.tol * beta) {       // converged: report the Newton point
+      s.T = 1.0 / bn;
+      s.done = s.converged = 1;
+      return;
+    }
+    next = bn;
+  } else if (g > 0.0 && !s.lo_known && !(h > 0.0 && bn > s.lo)) {
+    next = s.lo;                            // root may lie below the range: probe t_hi
+  } else if (g <= 0.0 && !s.hi_known && !(h > 0.0 && bn < s.hi)) {
+    next = s.hi;                            // probe t_lo
+  } else {
+    next = sqrt(s.lo * s.hi);               // geometric bisection of the bracket
+  }
+  if (s.lo_known && s.hi_known && (s.hi - s.lo) <= a.tol * s.lo) {
+    s.T = 2.0 / (s.lo + s.hi);
+    s.done = s.converged = 1;
+    return;
+  }
+  s.dx_old = s.dx;
+  s.dx = fabs(next - beta);
+  s.beta = next;
+}
+
+// Fixed-order sum over CTAs of partial[j][b][c] (identical in every CTA).
+__device__ __forceinline__ void reduce_partials(const double* part, int nb, int ncta, double* red,
+                                                const int* skip) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int p = warp; p < nb * 3; p += kTfWarps) {
+    const int b = p / 3;
+    if (skip[b]) continue;
+    double v = 0.0;
+    for (int j = lane; j < ncta; j += 32) v += __ldcg(part + ((size_t)j * nb + b) * 3 + (p % 3));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+    if (lane == 0) red[p] = v;
+  }
+}
+
+template <bool BF16, int G>
+__global__ void __launch_bounds__(kTfThreads, 1) temp_fit_kernel(const TfArgs a) {
+  pdl_start();
+  cg::grid_group grid = cg::this_grid();
+  __shared__ TfState st[kMaxBatch];
+  __shared__ double wacc[kTfWarps][kMaxBatch * 3];
+  __shared__ double red[kMaxBatch * 3];
+  __shared__ int skip[kMaxBatch];
+  constexpr int GPW = 32 / G;
+  constexpr int CH = G * kTfU;                           // vectors per group per chunk
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int gl = lane & (G - 1), grp = lane / G;
+  const int nb = a.nbatch;
+  const int64_t n = a.n;
+  const int64_t wstride = (int64_t)gridDim.x * kTfWarps * GPW;       // rows per warp step
+  const int64_t wbase = ((int64_t)blockIdx.x * kTfWarps + warp) * GPW;
+  double* part0 = a.partial;
+  double* part1 = a.partial + (size_t)gridDim.x * nb * 3;
+
+  // ---- sweep 0: row max m (NaN-propagating), dy = x_y - m, validity
+  for (int b = 0; b < nb; ++b) {
+    const char* base = (const char*)a.bptr[b];
+    double used = 0.0;
+    for (int64_t r0 = wbase; r0 < n; r0 += wstride) {
+      const int64_t row = r0 + grp;
+      const bool active = row < n;
+      const uint4* rowp = reinterpret_cast<const uint4*>(base + (active ? row : 0) * a.row_bytes);
+      int32_t lab = 0;
+      if (active && gl == 0) lab = __ldg(a.labels + row);
+      float m;
+      if (BF16) {
+        uint32_t mw = kBf16NegInf2;
+        for (int v0 = 0; v0 < a.nvec; v0 += CH) {
+          uint4 v[kTfU];
+          load_chunk<BF16, G>(v, rowp, v0, gl, a.nvec, a.tail, active);
+#pragma unroll
+          for (int k = 0; k < kTfU; ++k) mw = bmax2(mw, bmax2(bmax2(v[k].x, v[k].y), bmax2(v[k].z, v[k].w)));
+        }
+        m = fmax_nan(bf_lo(mw), bf_hi(mw));
+      } else {
+        m = -INFINITY;
+        for (int v0 = 0; v0 < a.nvec; v0 += CH) {
+          uint4 v[kTfU];
+          load_chunk<BF16, G>(v, rowp, v0, gl, a.nvec, a.tail, active);
+#pragma unroll
+          for (int k = 0; k < kTfU; ++k)
+            m = fmax_nan(m, fmax3_nan(__uint_as_float(v[k].x), __uint_as_float(v[k].y),
+                                      fmax_nan(__uint_as_float(v[k].z), __uint_as_float(v[k].w))));
+        }
+      }
+#pragma unroll
+      for (int o = G / 2; o > 0; o >>= 1) m = fmax_nan(m, __shfl_xor_sync(0xFFFFFFFFu, m, o));
+      if (active && gl == 0) {
+        const bool valid = (m < INFINITY) && (m > -INFINITY);       // false for NaN too
+        if (!valid && a.status) atomicOr(a.status, HS_STATUS_NONFINITE);
+        float xy = -INFINITY;
+        if (valid && lab >= 0 && (int64_t)lab < a.C) {
+          if (BF16) {
+            const unsigned short u = __ldg(reinterpret_cast<const unsigned short*>(rowp) + lab);
+            xy = __uint_as_float((uint32_t)u << 16);
+          } else {
+            xy = __ldg(reinterpret_cast<const float*>(rowp) + lab);
+          }
+        }
+        const bool use = valid && xy > -INFINITY;
+        a.rowstat[(size_t)b * n + row] = use ? make_float2(m, xy - m) : make_float2(__int_as_float(0x7FC00000), 0.f);
+        used += use ? 1.0 : 0.0;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) used += __shfl_xor_sync(0xFFFFFFFFu, used, o);
+    if (lane == 0) wacc[warp][b * 3] = used;
+  }
+  __syncthreads();
+  if (threadIdx.x < nb) {
+    double u = 0.0;
+    for (int w = 0; w < kTfWarps; ++w) u += wacc[w][threadIdx.x * 3];
+    double* p = part0 + ((size_t)blockIdx.x * nb + threadIdx.x) * 3;
+    p[0] = u;
+    p[1] = 0.0;
+    p[2] = 0.0;
+    skip[threadIdx.x] = 0;
+  }
+  grid.sync();
+  reduce_partials(part0, nb, gridDim.x, red, skip);
+  __syncthreads();
+  if (threadIdx.x < nb) {
+    TfState& s = st[threadIdx.x];
+    s.lo = a.blo0;
+    s.hi = a.bhi0;
+    s.beta = fmin(fmax(1.0, a.blo0), a.bhi0);             // start at T = 1 (clamped)
+    s.dx = s.dx_old = 2.0 * (a.bhi0 - a.blo0) + 1.0;
+    s.nll = __longlong_as_double(0x7FF8000000000000ll);
+    s.T = s.nll;
+    s.used = (long long)red[threadIdx.x * 3];
+    s.lo_known = s.hi_known = 0;
+    s.done = s.used == 0;
+    s.passes = 0;
+    s.converged = 0;
+  }
+  __syncthreads();
+
+  // ---- Newton sweeps: one pass over the logits at st[b].beta per live stage
+  for (int pass = 1; pass <= a.max_passes; ++pass) {
+    bool all = true;
+    for (int b = 0; b < nb; ++b) all &= st[b].done != 0;
+    if (all) break;
+    double* part = (pass & 1) ? part1 : part0;
+    for (int b = 0; b < nb; ++b) {
+      if (st[b].done) continue;
+      const char* base = (const char*)a.bptr[b];
+      const double beta = st[b].beta;
+      const float c = (float)(beta * 1.4426950408889634);   // beta * log2(e)
+      const f2_t c2 = f2(c, c);
+      double acc_nll = 0.0, acc_g = 0.0, acc_h = 0.0;
+      for (int64_t r0 = wbase; r0 < n; r0 += wstride) {
+        const int64_t row = r0 + grp;
+        float2 rs = make_float2(__int_as_float(0x7FC00000), 0.f);
+        if (row < n) rs = __ldcg(a.rowstat + (size_t)b * n + row);
+        const bool active = rs.x == rs.x;                     // used row
+        const uint4* rowp = reinterpret_cast<const uint4*>(base + (row < n ? row : 0) * a.row_bytes);
+        const float m = active ? rs.x : 0.f;
+        const f2_t m2 = f2(m, m);
+        const uint32_t cw = BF16 ? clamp_word_bf16(m, c) : 0u;
+        const float lowf = m - fmaxf(128.0f / c, fabsf(m) * 0.0078125f);
+        f2_t s2 = f2(0.f, 0.f), w12 = f2(0.f, 0.f), w22 = f2(0.f, 0.f);
+        if (__any_sync(0xFFFFFFFFu, active)) {
+          for (int v0 = 0; v0 < a.nvec; v0 += CH) {
+            uint4 v[kTfU];
+            load_chunk<BF16, G>(v, rowp, v0, gl, a.nvec, a.tail, active);
+#pragma unroll
+            for (int k = 0; k < kTfU; ++k) {
+#pragma unroll
+              for (int q = 0; q < (BF16 ? 4 : 2); ++q) {
+                f2_t x;
+                if (BF16) {
+                  const uint32_t u = bmax2_plain(wordq(v[k], q), cw);
+                  x = f2(bf_lo(u), bf_hi(u));
+                } else {
+                  x = f2(fmaxf(__uint_as_float(wordq(v[k], 2 * q)), lowf),
+                         fmaxf(__uint_as_float(wordq(v[k], 2 * q + 1)), lowf));
+                }
+                const f2_t d = f2sub(x, m2);
+                const f2_t z = f2mul(d, c2);
+                const f2_t e = f2(ex2(f2lo(z)), ex2(f2hi(z)));
+                s2 = f2add(s2, e);
+                const f2_t t = f2mul(e, d);
+                w12 = f2add(w12, t);
+                w22 = f2fma(t, d, w22);
+              }
+            }
+          }
+        }
+        float s = group_sum<float, G>(f2lo(s2) + f2hi(s2));
+        float w1 = group_sum<float, G>(f2lo(w12) + f2hi(w12));
+        float w2 = group_sum<float, G>(f2lo(w22) + f2hi(w22));
+        if (active && gl == 0) {
+          const double ds = (double)s, mean = (double)w1 / ds;
+          acc_nll += (double)logf(s) - beta * (double)rs.y;
+          acc_g += mean - (double)rs.y;
+          acc_h += fmax((double)w2 / ds - mean * mean, 0.0);
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        acc_nll += __shfl_xor_sync(0xFFFFFFFFu, acc_nll, o);
+        acc_g += __shfl_xor_sync(0xFFFFFFFFu, acc_g, o);
+        acc_h += __shfl_xor_sync(0xFFFFFFFFu, acc_h, o);
+      }
+      if (lane == 0) {
+        wacc[warp][b * 3 + 0] = acc_nll;
+        wacc[warp][b * 3 + 1] = acc_g;
+        wacc[warp][b * 3 + 2] = acc_h;
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x < nb * 3) {
+      const int b = threadIdx.x / 3;
+      skip[b] = st[b].done;
+      if (!st[b].done) {
+        double v = 0.0;
+        for (int w = 0; w < kTfWarps; ++w) v += wacc[w][threadIdx.x];
+        part[(size_t)blockIdx.x * nb * 3 + threadIdx.x] = v;
+      }
+    }
+    grid.sync();
+    reduce_partials(part, nb, gridDim.x, red, skip);
+    __syncthreads();
+    if (threadIdx.x < nb && !st[threadIdx.x].done) {
+      TfState& s = st[threadIdx.x];
+      const double inv = 1.0 / (double)s.used;
+      tf_update(s, red[threadIdx.x * 3] * inv, red[threadIdx.x * 3 + 1] * inv,
+                red[threadIdx.x * 3 + 2] * inv, a);
+    }
+    __syncthreads();
+  }
+
+  if (blockIdx.x == 0 && threadIdx.x < nb) {
+    TfState& s = st[threadIdx.x];
+    if (!s.done && s.passes > 0) s.T = 1.0 / s.swept;   // pass budget exhausted: last point
+    if (!s.converged && s.used > 0 && a.status) atomicOr(a.status, HS_STATUS_NOT_CONVERGED);
+    a.T[threadIdx.x] = (float)s.T;
+    if (a.nll) a.nll[threadIdx.x] = s.nll;
+    if (a.passes) a.passes[threadIdx.x] = s.passes;
+    if (a.used) a.used[threadIdx.x] = s.used;
+  }
+}
+
+template <bool BF16, int G>
+cudaError_t launch_tf(const TfArgs& a, cudaStream_t s) {
+  auto kern = temp_fit_kernel<BF16, G>;
+  int per_sm = 0;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kTfThreads, 0);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) return cudaErrorLaunchOutOfResources;
+  int grid = num_sms() * per_sm;
+  if (grid > kTfMaxGrid) grid = kTfMaxGrid;
+  TfArgs args = a;
+  void* params[] = {(void*)&args};
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kTfThreads);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
+  e = cudaLaunchKernelExC(&cfg, (const void*)kern, params);
+  count_launch();
+  return e != cudaSuccess ? e : cudaGetLastError();
+}
+
+template <bool BF16>
+cudaError_t launch_tf_dt(const TfArgs& a, cudaStream_t s) {
+  // lanes per row: enough for the row in about one chunk of kTfU vectors per lane
+  const int want = (a.nvec + kTfU - 1) / kTfU;
+  if (want <= 2) return launch_tf<BF16, 2>(a, s);
+  if (want <= 4) return launch_tf<BF16, 4>(a, s);
+  if (want <= 8) return launch_tf<BF16, 8>(a, s);
+  if (want <= 16) return launch_tf<BF16, 16>(a, s);
+  return launch_tf<BF16, 32>(a, s);
+}
+
+}  // namespace
+
+size_t temp_fit_ws_bytes(int nbatch, int64_t n) {
+  const size_t rows = (size_t)nbatch * (size_t)(n > 0 ? n : 0) * sizeof(float2);
+  return (rows + 255) / 256 * 256 + (size_t)2 * kTfMaxGrid * nbatch * 3 * sizeof(double);
+}
+
+cudaError_t launch_temp_fit(TfArgs a, bool bf16, void* ws, cudaStream_t s) {
+  const size_t rows = (size_t)a.nbatch * (size_t)a.n * sizeof(float2);
+  a.rowstat = reinterpret_cast<float2*>(ws);
+  a.partial = reinterpret_cast<double*>(reinterpret_cast<char*>(ws) + (rows + 255) / 256 * 256);
+  return bf16 ? launch_tf_dt<true>(a, s) : launch_tf_dt<false>(a, s);
+}
+
+}  // namespace hs

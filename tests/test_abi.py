@@ -120,3 +120,23 @@ def test_skip_edges_host_helper_matches_oracle(libhs):
             for mode in (hs.SKIP_UNIFORM, hs.SKIP_DECADE):
                 assert np.array_equal(np.array(hs.skip_edges(t32, s_, mode), np.float32),
                                       oracle.skip_edges(t32, s_, mode)), (t, s_, mode)
+
+
+def test_fit_temperature_argument_errors(libhs):
+    """hs_fit_temperature (NEXT-3) validates on the host before any launch."""
+    lib = libhs.lib()
+    ptrs = (ctypes.c_void_p * 1)(256)
+    ws = lib.hs_fit_temperature_workspace(1, 10)
+    assert ws >= 10 * 8
+    assert lib.hs_fit_temperature_workspace(5, 10) > ws
+
+    def call(nb=1, C=1000, lo=0.5, hi=2.0, passes=16, T=512, labels=768, wsb=ws):
+        return lib.hs_fit_temperature(ptrs, nb, 1, 10, C, 1000, labels, lo, hi, passes, T, None,
+                                      None, None, 1024, wsb, None, None)
+    for kw, needle in ((dict(nb=0), "n_batches"), (dict(nb=9), "n_batches"), (dict(C=1), "n_classes"),
+                       (dict(lo=0.0), "range"), (dict(lo=3.0), "range"), (dict(hi=float("inf")), "range"),
+                       (dict(passes=0), "max_passes"), (dict(passes=257), "max_passes"),
+                       (dict(T=None), "d_T"), (dict(labels=None), "labels")):
+        assert call(**kw) == 1, kw
+        assert needle in lib.hs_last_error().decode(), kw
+    assert call(wsb=ws - 1) == 5
