@@ -34,7 +34,9 @@ CONFIG_TEXT = {
     "c4": "3-stage Llama-like next-token cascade, 8,192 requests x 128,256 vocab bf16 per GPU, entropy confidence, 8 KB hidden-state payload gathered",
     "c5": "5-stage ViT streaming cascade, 1,048,576 requests x 1,000 classes bf16 per GPU (8M over 8 GPUs), validation 131,072 per GPU",
     "c3k": "c3 with the Top-K (K = 10) restricted token confidence of P:420-424 (NEXT-2), MIN over 64 tokens",
+    "c2t": "NEXT-3: temperature fitting (Eq. 1, P:384-389) of the 5 C2 ViT stage models on the 50,000-sample validation set per GPU, 1,000 classes bf16, T in [e^-4, e^4]",
 }
+METRIC_TEMP = "temperature fitting (Eq. 1): stage-model validation rows fitted per second"
 
 
 def parse():
@@ -206,11 +208,11 @@ def build_inputs(fam, rank: int, dev):
     return route, val, labels, payload
 
 
-def committed_traffic(config: str):
+def committed_traffic(config: str, name: str = "r01_k1_traffic.json"):
     """DRAM bytes per launch of the roofline kernel from the committed ncu
     capture (profiles/r01_k1_traffic.json, written by tools/ncu_summary.py
     traffic), when it was taken on this config; else None."""
-    path = os.path.join(ROOT, "profiles", "r01_k1_traffic.json")
+    path = os.path.join(ROOT, "profiles", name)
     try:
         rec = json.load(open(path))
     except (OSError, ValueError):
@@ -503,6 +505,145 @@ def run_e2e(args, fam, router, route, val, labels, payload, stream, world):
 
 
 # ---------------------------------------------------------------------------
+# NEXT-3: temperature fitting on the validation set (--config c2t)
+# ---------------------------------------------------------------------------
+def run_temperature(args, world, rank, local):
+    """Step = hs_fit_temperature over the validation shard of every stage model
+    (one persistent launch: a max/label sweep + the Newton sweeps).  N > 1:
+    independent replicas (each rank fits on its own shard; no collective)."""
+    import torch
+    import paper_2505_12566_b200 as hs
+    dev = torch.device("cuda", local)
+    fam = family("c2")
+    _, val, labels, _ = build_inputs(synth_scaled(fam, n=1), rank, dev)
+    K, n = fam.K, fam.n_val
+    ws = torch.empty(hs.lib().hs_fit_temperature_workspace(K, n), dtype=torch.uint8, device=dev)
+    out = {"T": torch.empty(K, dtype=torch.float32, device=dev),
+           "nll": torch.empty(K, dtype=torch.float64, device=dev),
+           "passes": torch.empty(K, dtype=torch.int32, device=dev),
+           "used": torch.empty(K, dtype=torch.int64, device=dev)}
+    status = torch.zeros(1, dtype=torch.int32, device=dev)
+
+    def step():
+        hs.fit_temperature(val, labels, out=out, ws=ws, status=status)
+
+    stream = torch.cuda.Stream(device=dev)
+    with torch.cuda.stream(stream):
+        for _ in range(max(args.warmup, 3)):
+            step()
+    torch.cuda.synchronize()
+    graph = None
+    launches_per_step = 1
+    if not args.no_graph:
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=stream):
+            l0 = hs.launch_count()
+            step()
+            launches_per_step = hs.launch_count() - l0
+        graph.replay()
+        torch.cuda.synchronize()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    barrier(world)
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        with torch.cuda.stream(stream):
+            t0.record(stream)
+            for _ in range(args.steps):
+                graph.replay() if graph is not None else step()
+            t1.record(stream)
+        torch.cuda.synchronize()
+    barrier(world)
+    ms = max_over_ranks(t0.elapsed_time(t1), world) / args.steps
+    passes = out["passes"].cpu().tolist()
+    T = out["T"].cpu().tolist()
+    row_b = fam.row_bytes
+    # algorithmic bytes of one launch: every sweep reads the rows of each model
+    # still fitting (sweep 0 also reads the label and writes 8 B of row state;
+    # later sweeps read it back)
+    # rows of <= 2 KB fold the max/label sweep into the first Newton sweep
+    sweep0 = 0 if row_b <= 2048 else 1
+    k_bytes = sum((sweep0 + p) * n * row_b + n * (4 + 8) + p * n * 8 for p in passes)
+    peak, peak_src = peaks()
+    achieved = k_bytes / (ms / 1e3) / 1e9
+    e2e = None
+    if args.e2e_steps > 0:
+        host_val = [x.cpu().pin_memory() for x in val]
+        host_lab = labels.cpu().pin_memory()
+        host_T = torch.empty(K, dtype=torch.float32).pin_memory()
+        h2d = sum(x.numel() * x.element_size() for x in host_val) + host_lab.numel() * 4
+
+        def once():
+            for d, h in zip(val, host_val):
+                d.copy_(h, non_blocking=True)
+            labels.copy_(host_lab, non_blocking=True)
+            step()
+            host_T.copy_(out["T"], non_blocking=True)
+
+        with torch.cuda.stream(stream):
+            once()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            e0.record(stream)
+            for _ in range(args.e2e_steps):
+                once()
+            e1.record(stream)
+        torch.cuda.synchronize()
+        ems = max_over_ranks(e0.elapsed_time(e1), world) / args.e2e_steps
+        e2e = {"value": K * n * world / (ems / 1e3), "unit": "rows/s", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": K * 4, "ms_per_step": ems, "steps": args.e2e_steps}
+    line = {
+        "metric": METRIC_TEMP, "value": K * n * world / (ms / 1e3), "unit": "rows/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic",
+        "config": {"workload": "c2t_vit5_validation_temperature", "description": CONFIG_TEXT["c2t"],
+                   "validation_per_gpu": n, "K": K, "classes": fam.C, "logits_dtype": fam.dtype,
+                   "parallelism": f"independent replicas x{world} (shard-local fit)",
+                   "l2": "inputs larger than L2 (500 MB of validation logits per sweep)",
+                   "cuda_graph": graph is not None},
+        "temperatures": T, "passes": passes, "status": int(status.item()),
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": committed_traffic("c2t", "r01_tf_traffic.json"),
+                     "kernel": "temp_fit_kernel (the whole step: one persistent cooperative launch)",
+                     "bytes_per_launch": k_bytes, "avg_launch_ms": ms, "peak_source": peak_src},
+        "e2e": e2e, "gpu_launches": launches_per_step * args.steps, "clocks": clk.summary(),
+        "gpu_launches_per_step": launches_per_step,
+    }
+    return line, fam, val, labels
+
+
+def synth_scaled(fam, **kw):
+    from workload import synth
+    return synth.scaled(fam, **kw)
+
+
+def cpu_baseline_temperature(fam, seconds: float, val, labels):
+    """The oracle's fit (fp64, bisection) on a bounded row sample of the same
+    validation logits, repeated for ~`seconds`."""
+    import numpy as np
+    import oracle
+    K = fam.K
+    lab = labels.cpu().numpy()
+    rows_all = [x.view(__import__("torch").int16).cpu().numpy().view(np.uint16) for x in val]
+    m = 256
+    t = time.perf_counter()
+    for k in range(K):
+        oracle.fit_temperature(rows_all[k][:m], lab[:m], n_classes=fam.C)
+    dt = time.perf_counter() - t
+    m = int(min(len(lab), max(m, m * seconds / max(dt, 1e-3))))
+    t = time.perf_counter()
+    for k in range(K):
+        oracle.fit_temperature(rows_all[k][:m], lab[:m], n_classes=fam.C)
+    dt = time.perf_counter() - t
+    return {"value": K * m / dt, "unit": "rows/s", "cores": 1, "kind": "oracle",
+            "sample": f"first {m} of {len(lab)} validation rows of each of the {K} stage models "
+                      f"(same generator), fp64 C oracle (bisection on beta), 1 thread, {dt:.1f} s"}
+
+
+# ---------------------------------------------------------------------------
 # the oracle on the host cores (cpu_baseline leg and --impl reference)
 # ---------------------------------------------------------------------------
 def oracle_inputs(fam, frac_n: int, frac_val: int):
@@ -576,6 +717,8 @@ def run_reference(args, world, rank):
     """--impl reference: the oracle as it stands, on host cores, K bounded steps."""
     if rank != 0:
         return None
+    if args.config == "c2t":
+        return run_reference_temperature(args, world)
     fam = family(args.config)
     budget = 150.0 / max(1, args.steps + args.warmup)
     n, v = cpu_sample_sizes(fam, min(budget, 20.0))
@@ -603,6 +746,48 @@ def run_reference(args, world, rank):
                              "kind": "oracle", "sample": sample},
             "e2e": {"value": value, "unit": "requests/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
+
+
+def run_reference_temperature(args, world):
+    """--impl reference --config c2t: the oracle's fit on a bounded row sample."""
+    import numpy as np
+    import oracle
+    from workload import synth
+    fam = family("c2")
+    budget = min(10.0, 150.0 / max(1, args.steps + args.warmup))
+    vids = np.arange(fam.n_val, dtype=np.int64) + synth.VAL_ID_BASE
+    m = 128
+    while True:
+        lab = synth.labels_np(fam.seed, vids[:m], 1, fam.C).reshape(-1)
+        rows = [synth.logits_np(fam.seed, k, vids[:m], 1, fam.C, fam.thr[k], "bf16") for k in range(fam.K)]
+        t = time.perf_counter()
+        for k in range(fam.K):
+            oracle.fit_temperature(rows[k], lab, n_classes=fam.C)
+        dt = time.perf_counter() - t
+        if dt >= budget / 4 or m >= fam.n_val:
+            break
+        m = min(fam.n_val, int(m * max(2.0, budget / max(dt, 1e-3))))
+    for _ in range(args.warmup):
+        for k in range(fam.K):
+            oracle.fit_temperature(rows[k], lab, n_classes=fam.C)
+    tot = 0.0
+    for _ in range(args.steps):
+        t = time.perf_counter()
+        for k in range(fam.K):
+            oracle.fit_temperature(rows[k], lab, n_classes=fam.C)
+        tot += time.perf_counter() - t
+    value = fam.K * m * args.steps / tot
+    sample = f"first {m} of {fam.n_val} validation rows of each of the {fam.K} stage models per step"
+    return {"impl": "reference", "metric": METRIC_TEMP, "value": value, "unit": "rows/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": tot / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "c2t_vit5_validation_temperature", "description": CONFIG_TEXT["c2t"],
+                       "validation_per_gpu": fam.n_val, "K": fam.K, "classes": fam.C,
+                       "logits_dtype": "bf16", "parallelism": "host core (oracle, 1 thread)"},
+            "cpu_baseline": {"value": value, "unit": "rows/s", "cores": 1, "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": "rows/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
 def _claim_stdout():
@@ -635,6 +820,13 @@ def main():
         os.environ["RANK"] = "0"
         os.environ["LOCAL_RANK"] = "0"
     world, rank, local = init_dist(args, force=args.placement == "balanced" or args.force_dist)
+    if args.config == "c2t":
+        line, fam, val, labels = run_temperature(args, world, rank, local)
+        if rank == 0 and world == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline_temperature(fam, args.cpu_seconds, val, labels)
+        if rank == 0:
+            emit(json.dumps(line))
+        return
     if args.placement == "balanced":
         line, fam = run_balanced(args, world, rank, local)
     else:

@@ -26,6 +26,7 @@
 #include <cooperative_groups.h>
 
 #include <cmath>
+#include <cstdlib>
 
 #include "hs_common.cuh"
 #include "hs_internal.h"
@@ -36,9 +37,12 @@ namespace cg = cooperative_groups;
 
 namespace {
 
-constexpr int kTfThreads = 1024;
+#ifndef HS_TF_THREADS
+#define HS_TF_THREADS 1024
+#endif
+constexpr int kTfThreads = HS_TF_THREADS;
 constexpr int kTfWarps = kTfThreads / 32;
-constexpr int kTfU = 4;                 // 16-byte vectors per lane per chunk
+constexpr int kTfComp = 4;              // partial sums per stage: used, nll, g, h
 
 struct TfState {
   double lo, hi, beta;      // bracket on beta = 1/T, point of the next sweep
@@ -72,12 +76,13 @@ __device__ __forceinline__ uint4 tail_mask(const uint4& v, int tail) {
 }
 
 // Loads the group's chunk (vectors v0 + k*G + gl); slots past the row hold -inf.
-template <bool BF16, int G>
-__device__ __forceinline__ void load_chunk(uint4 (&v)[kTfU], const uint4* rowp, int v0, int gl,
+// Loads the group's chunk (vectors v0 + k*G + gl); slots past the row hold -inf.
+template <bool BF16, int G, int U>
+__device__ __forceinline__ void load_chunk(uint4 (&v)[U], const uint4* rowp, int v0, int gl,
                                            int nvec, int tail, bool active) {
   const uint32_t f = BF16 ? kBf16NegInf2 : kF32NegInf;
 #pragma unroll
-  for (int k = 0; k < kTfU; ++k) {
+  for (int k = 0; k < U; ++k) {
     const int vi = v0 + k * G + gl;
     if (active && vi < nvec) {
       v[k] = ldg_stream(rowp + vi);
@@ -86,6 +91,69 @@ __device__ __forceinline__ void load_chunk(uint4 (&v)[kTfU], const uint4* rowp, 
       v[k] = make_uint4(f, f, f, f);
     }
   }
+}
+
+// NaN-propagating max of a chunk, folded into m
+template <bool BF16, int U>
+__device__ __forceinline__ float chunk_max(const uint4 (&v)[U], float m) {
+  if (BF16) {
+    uint32_t mw = kBf16NegInf2;
+#pragma unroll
+    for (int k = 0; k < U; ++k) mw = bmax2(mw, bmax2(bmax2(v[k].x, v[k].y), bmax2(v[k].z, v[k].w)));
+    return fmax_nan(m, fmax_nan(bf_lo(mw), bf_hi(mw)));
+  }
+#pragma unroll
+  for (int k = 0; k < U; ++k)
+    m = fmax_nan(m, fmax3_nan(__uint_as_float(v[k].x), __uint_as_float(v[k].y),
+                              fmax_nan(__uint_as_float(v[k].z), __uint_as_float(v[k].w))));
+  return m;
+}
+
+// s += e, w1 += e d, w2 += e d^2 over a chunk: d = x - m (exact), e = 2^{d c}
+template <bool BF16, int U>
+__device__ __forceinline__ void accum_chunk(const uint4 (&v)[U], f2_t m2, f2_t c2, uint32_t cw,
+                                            float lowf, f2_t& s2, f2_t& w12, f2_t& w22) {
+#pragma unroll
+  for (int k = 0; k < U; ++k) {
+#pragma unroll
+    for (int q = 0; q < (BF16 ? 4 : 2); ++q) {
+      f2_t x;
+      if (BF16) {
+        const uint32_t u = bmax2_plain(wordq(v[k], q), cw);
+        x = f2(bf_lo(u), bf_hi(u));
+      } else {
+        x = f2(fmaxf(__uint_as_float(wordq(v[k], 2 * q)), lowf),
+               fmaxf(__uint_as_float(wordq(v[k], 2 * q + 1)), lowf));
+      }
+      const f2_t d = f2sub(x, m2);
+      const f2_t z = f2mul(d, c2);
+      const f2_t e = f2(ex2(f2lo(z)), ex2(f2hi(z)));
+      s2 = f2add(s2, e);
+      const f2_t t = f2mul(e, d);
+      w12 = f2add(w12, t);
+      w22 = f2fma(t, d, w22);
+    }
+  }
+}
+
+// The group leader's verdict on a row with max m: used (valid, finite label
+// logit) and dy = x_y - m.  Invalid rows (NaN / +inf / all -inf) flag status.
+template <bool BF16>
+__device__ __forceinline__ bool row_verdict(const TfArgs& a, float m, const uint4* rowp, int32_t lab,
+                                            float* dy) {
+  const bool valid = (m < INFINITY) && (m > -INFINITY);       // false for NaN too
+  if (!valid && a.status) atomicOr(a.status, HS_STATUS_NONFINITE);
+  float xy = -INFINITY;
+  if (valid && lab >= 0 && (int64_t)lab < a.C) {
+    if (BF16) {
+      const unsigned short u = __ldg(reinterpret_cast<const unsigned short*>(rowp) + lab);
+      xy = __uint_as_float((uint32_t)u << 16);
+    } else {
+      xy = __ldg(reinterpret_cast<const float*>(rowp) + lab);
+    }
+  }
+  *dy = xy - m;
+  return valid && xy > -INFINITY;
 }
 
 template <typename T, int G>
@@ -163,31 +231,31 @@ __device__ void tf_update(TfState& s, double nll, double g, double h, const TfAr
   s.beta = next;
 }
 
-// Fixed-order sum over CTAs of partial[j][b][c] (identical in every CTA).
+// Fixed-order sum over CTAs of partial[j][b][c], c < ncomp (identical in every CTA).
 __device__ __forceinline__ void reduce_partials(const double* part, int nb, int ncta, double* red,
-                                                const int* skip) {
+                                                const int* skip, int ncomp) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int p = warp; p < nb * 3; p += kTfWarps) {
-    const int b = p / 3;
-    if (skip[b]) continue;
+  for (int p = warp; p < nb * kTfComp; p += kTfWarps) {
+    const int b = p / kTfComp;
+    if (skip[b] || p % kTfComp >= ncomp) continue;
     double v = 0.0;
-    for (int j = lane; j < ncta; j += 32) v += __ldcg(part + ((size_t)j * nb + b) * 3 + (p % 3));
+    for (int j = lane; j < ncta; j += 32) v += __ldcg(part + ((size_t)j * nb + b) * kTfComp + (p % kTfComp));
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
     if (lane == 0) red[p] = v;
   }
 }
 
-template <bool BF16, int G>
+template <bool BF16, int G, int U>
 __global__ void __launch_bounds__(kTfThreads, 1) temp_fit_kernel(const TfArgs a) {
   pdl_start();
   cg::grid_group grid = cg::this_grid();
   __shared__ TfState st[kMaxBatch];
-  __shared__ double wacc[kTfWarps][kMaxBatch * 3];
-  __shared__ double red[kMaxBatch * 3];
+  __shared__ double wacc[kTfWarps][kMaxBatch * kTfComp];
+  __shared__ double red[kMaxBatch * kTfComp];
   __shared__ int skip[kMaxBatch];
   constexpr int GPW = 32 / G;
-  constexpr int CH = G * kTfU;                           // vectors per group per chunk
+  constexpr int CH = G * U;                              // vectors per group per chunk
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int gl = lane & (G - 1), grp = lane / G;
   const int nb = a.nbatch;
@@ -195,75 +263,12 @@ __global__ void __launch_bounds__(kTfThreads, 1) temp_fit_kernel(const TfArgs a)
   const int64_t wstride = (int64_t)gridDim.x * kTfWarps * GPW;       // rows per warp step
   const int64_t wbase = ((int64_t)blockIdx.x * kTfWarps + warp) * GPW;
   double* part0 = a.partial;
-  double* part1 = a.partial + (size_t)gridDim.x * nb * 3;
+  double* part1 = a.partial + (size_t)gridDim.x * nb * kTfComp;
+  // rows of one chunk: the max / label / validity sweep is folded into the
+  // first Newton sweep (the row is in registers for both)
+  const bool fused = a.nvec <= CH;
+  const float nanf_ = __int_as_float(0x7FC00000);
 
-  // ---- sweep 0: row max m (NaN-propagating), dy = x_y - m, validity
-  for (int b = 0; b < nb; ++b) {
-    const char* base = (const char*)a.bptr[b];
-    double used = 0.0;
-    for (int64_t r0 = wbase; r0 < n; r0 += wstride) {
-      const int64_t row = r0 + grp;
-      const bool active = row < n;
-      const uint4* rowp = reinterpret_cast<const uint4*>(base + (active ? row : 0) * a.row_bytes);
-      int32_t lab = 0;
-      if (active && gl == 0) lab = __ldg(a.labels + row);
-      float m;
-      if (BF16) {
-        uint32_t mw = kBf16NegInf2;
-        for (int v0 = 0; v0 < a.nvec; v0 += CH) {
-          uint4 v[kTfU];
-          load_chunk<BF16, G>(v, rowp, v0, gl, a.nvec, a.tail, active);
-#pragma unroll
-          for (int k = 0; k < kTfU; ++k) mw = bmax2(mw, bmax2(bmax2(v[k].x, v[k].y), bmax2(v[k].z, v[k].w)));
-        }
-        m = fmax_nan(bf_lo(mw), bf_hi(mw));
-      } else {
-        m = -INFINITY;
-        for (int v0 = 0; v0 < a.nvec; v0 += CH) {
-          uint4 v[kTfU];
-          load_chunk<BF16, G>(v, rowp, v0, gl, a.nvec, a.tail, active);
-#pragma unroll
-          for (int k = 0; k < kTfU; ++k)
-            m = fmax_nan(m, fmax3_nan(__uint_as_float(v[k].x), __uint_as_float(v[k].y),
-                                      fmax_nan(__uint_as_float(v[k].z), __uint_as_float(v[k].w))));
-        }
-      }
-#pragma unroll
-      for (int o = G / 2; o > 0; o >>= 1) m = fmax_nan(m, __shfl_xor_sync(0xFFFFFFFFu, m, o));
-      if (active && gl == 0) {
-        const bool valid = (m < INFINITY) && (m > -INFINITY);       // false for NaN too
-        if (!valid && a.status) atomicOr(a.status, HS_STATUS_NONFINITE);
-        float xy = -INFINITY;
-        if (valid && lab >= 0 && (int64_t)lab < a.C) {
-          if (BF16) {
-            const unsigned short u = __ldg(reinterpret_cast<const unsigned short*>(rowp) + lab);
-            xy = __uint_as_float((uint32_t)u << 16);
-          } else {
-            xy = __ldg(reinterpret_cast<const float*>(rowp) + lab);
-          }
-        }
-        const bool use = valid && xy > -INFINITY;
-        a.rowstat[(size_t)b * n + row] = use ? make_float2(m, xy - m) : make_float2(__int_as_float(0x7FC00000), 0.f);
-        used += use ? 1.0 : 0.0;
-      }
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) used += __shfl_xor_sync(0xFFFFFFFFu, used, o);
-    if (lane == 0) wacc[warp][b * 3] = used;
-  }
-  __syncthreads();
-  if (threadIdx.x < nb) {
-    double u = 0.0;
-    for (int w = 0; w < kTfWarps; ++w) u += wacc[w][threadIdx.x * 3];
-    double* p = part0 + ((size_t)blockIdx.x * nb + threadIdx.x) * 3;
-    p[0] = u;
-    p[1] = 0.0;
-    p[2] = 0.0;
-    skip[threadIdx.x] = 0;
-  }
-  grid.sync();
-  reduce_partials(part0, nb, gridDim.x, red, skip);
-  __syncthreads();
   if (threadIdx.x < nb) {
     TfState& s = st[threadIdx.x];
     s.lo = a.blo0;
@@ -271,65 +276,155 @@ __global__ void __launch_bounds__(kTfThreads, 1) temp_fit_kernel(const TfArgs a)
     s.beta = fmin(fmax(1.0, a.blo0), a.bhi0);             // start at T = 1 (clamped)
     s.dx = s.dx_old = 2.0 * (a.bhi0 - a.blo0) + 1.0;
     s.nll = __longlong_as_double(0x7FF8000000000000ll);
+    s.swept = s.nll;
     s.T = s.nll;
-    s.used = (long long)red[threadIdx.x * 3];
+    s.used = -1;
     s.lo_known = s.hi_known = 0;
-    s.done = s.used == 0;
+    s.done = 0;
     s.passes = 0;
     s.converged = 0;
+    skip[threadIdx.x] = 0;
+  }
+
+  if (!fused) {
+    // ---- sweep 0: row max m (NaN-propagating), dy = x_y - m, validity
+    for (int b = 0; b < nb; ++b) {
+      const char* base = (const char*)a.bptr[b];
+      double used = 0.0;
+      for (int64_t r0 = wbase; r0 < n; r0 += wstride) {
+        const int64_t row = r0 + grp;
+        const bool active = row < n;
+        const uint4* rowp = reinterpret_cast<const uint4*>(base + (active ? row : 0) * a.row_bytes);
+        int32_t lab = 0;
+        if (active && gl == 0) lab = __ldg(a.labels + row);
+        float m = -INFINITY;
+        for (int v0 = 0; v0 < a.nvec; v0 += CH) {
+          uint4 v[U];
+          load_chunk<BF16, G, U>(v, rowp, v0, gl, a.nvec, a.tail, active);
+          m = chunk_max<BF16, U>(v, m);
+        }
+#pragma unroll
+        for (int o = G / 2; o > 0; o >>= 1) m = fmax_nan(m, __shfl_xor_sync(0xFFFFFFFFu, m, o));
+        if (active && gl == 0) {
+          float dy;
+          const bool use = row_verdict<BF16>(a, m, rowp, lab, &dy);
+          a.rowstat[(size_t)b * n + row] = use ? make_float2(m, dy) : make_float2(nanf_, 0.f);
+          used += use ? 1.0 : 0.0;
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) used += __shfl_xor_sync(0xFFFFFFFFu, used, o);
+      if (lane == 0) wacc[warp][b * kTfComp] = used;
+    }
+    __syncthreads();
+    if (threadIdx.x < nb) {
+      double u = 0.0;
+      for (int w = 0; w < kTfWarps; ++w) u += wacc[w][threadIdx.x * kTfComp];
+      part0[((size_t)blockIdx.x * nb + threadIdx.x) * kTfComp] = u;
+    }
+    grid.sync();
+    reduce_partials(part0, nb, gridDim.x, red, skip, 1);
+    __syncthreads();
+    if (threadIdx.x < nb) {
+      st[threadIdx.x].used = (long long)red[threadIdx.x * kTfComp];
+      st[threadIdx.x].done = st[threadIdx.x].used == 0;
+    }
   }
   __syncthreads();
 
-  // ---- Newton sweeps: one pass over the logits at st[b].beta per live stage
+  // ---- Newton sweeps: one pass over the logits at st[b].beta per live stage.
+  // The warp-rows (GPW rows) of all live stages form one list dealt round-robin
+  // to the warps, so a pass is balanced to one warp-row across the grid; a
+  // warp visits each stage in one contiguous run and flushes its sums when the
+  // stage changes (warp-uniform).
+  const int64_t gwarp = (int64_t)blockIdx.x * kTfWarps + warp;
+  const int64_t nwarps = (int64_t)gridDim.x * kTfWarps;
+  const int64_t nw = (n + GPW - 1) / GPW;                  // warp-rows per stage
   for (int pass = 1; pass <= a.max_passes; ++pass) {
-    bool all = true;
-    for (int b = 0; b < nb; ++b) all &= st[b].done != 0;
-    if (all) break;
+    int live[kMaxBatch];
+    int nl = 0;
+    for (int b = 0; b < nb; ++b)
+      if (!st[b].done) live[nl++] = b;
+    if (nl == 0) break;
+    const bool first = fused && pass == 1;
     double* part = (pass & 1) ? part1 : part0;
-    for (int b = 0; b < nb; ++b) {
-      if (st[b].done) continue;
-      const char* base = (const char*)a.bptr[b];
-      const double beta = st[b].beta;
-      const float c = (float)(beta * 1.4426950408889634);   // beta * log2(e)
-      const f2_t c2 = f2(c, c);
-      double acc_nll = 0.0, acc_g = 0.0, acc_h = 0.0;
-      for (int64_t r0 = wbase; r0 < n; r0 += wstride) {
-        const int64_t row = r0 + grp;
-        float2 rs = make_float2(__int_as_float(0x7FC00000), 0.f);
-        if (row < n) rs = __ldcg(a.rowstat + (size_t)b * n + row);
+    if (lane < nb * kTfComp) wacc[warp][lane] = 0.0;     // stages this warp does not visit
+    __syncwarp();
+    int li = -1, b = -1;
+    const char* base = nullptr;
+    double beta = 0.0;
+    float c = 0.f;
+    f2_t c2 = 0;
+    double acc_u = 0.0, acc_nll = 0.0, acc_g = 0.0, acc_h = 0.0;
+    auto flush = [&]() {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        acc_u += __shfl_xor_sync(0xFFFFFFFFu, acc_u, o);
+        acc_nll += __shfl_xor_sync(0xFFFFFFFFu, acc_nll, o);
+        acc_g += __shfl_xor_sync(0xFFFFFFFFu, acc_g, o);
+        acc_h += __shfl_xor_sync(0xFFFFFFFFu, acc_h, o);
+      }
+      if (lane == 0) {
+        wacc[warp][b * kTfComp + 0] = acc_u;
+        wacc[warp][b * kTfComp + 1] = acc_nll;
+        wacc[warp][b * kTfComp + 2] = acc_g;
+        wacc[warp][b * kTfComp + 3] = acc_h;
+      }
+      acc_u = acc_nll = acc_g = acc_h = 0.0;
+    };
+    for (int64_t wr = gwarp; wr < (int64_t)nl * nw; wr += nwarps) {
+      int lj = li < 0 ? 0 : li;
+      while (wr >= (int64_t)(lj + 1) * nw) ++lj;            // warp-uniform
+      if (lj != li) {
+        if (li >= 0) flush();
+        li = lj;
+        b = live[li];
+        base = (const char*)a.bptr[b];
+        beta = st[b].beta;
+        c = (float)(beta * 1.4426950408889634);             // beta * log2(e)
+        c2 = f2(c, c);
+      }
+      {
+        const int64_t row = (wr - (int64_t)li * nw) * GPW + grp;
+        const bool inb = row < n;
+        const uint4* rowp = reinterpret_cast<const uint4*>(base + (inb ? row : 0) * a.row_bytes);
+        // the row's first chunk is loaded together with its row state (the
+        // address does not depend on it)
+        uint4 v[U];
+        float2 rs = make_float2(nanf_, 0.f);
+        int32_t lab = 0;
+        if (first) {
+          if (inb && gl == 0) lab = __ldg(a.labels + row);
+        } else if (inb) {
+          rs = __ldcg(a.rowstat + (size_t)b * n + row);
+        }
+        load_chunk<BF16, G, U>(v, rowp, 0, gl, a.nvec, a.tail, inb);
+        if (first) {
+          float m = chunk_max<BF16, U>(v, -INFINITY);
+#pragma unroll
+          for (int o = G / 2; o > 0; o >>= 1) m = fmax_nan(m, __shfl_xor_sync(0xFFFFFFFFu, m, o));
+          float dy = 0.f;
+          bool use = false;
+          if (inb && gl == 0) {
+            use = row_verdict<BF16>(a, m, rowp, lab, &dy);
+            a.rowstat[(size_t)b * n + row] = use ? make_float2(m, dy) : make_float2(nanf_, 0.f);
+            acc_u += use ? 1.0 : 0.0;
+          }
+          const int leader = grp * G;
+          use = __shfl_sync(0xFFFFFFFFu, use, leader);
+          dy = __shfl_sync(0xFFFFFFFFu, dy, leader);
+          rs = use ? make_float2(m, dy) : make_float2(nanf_, 0.f);
+        }
         const bool active = rs.x == rs.x;                     // used row
-        const uint4* rowp = reinterpret_cast<const uint4*>(base + (row < n ? row : 0) * a.row_bytes);
         const float m = active ? rs.x : 0.f;
         const f2_t m2 = f2(m, m);
         const uint32_t cw = BF16 ? clamp_word_bf16(m, c) : 0u;
         const float lowf = m - fmaxf(128.0f / c, fabsf(m) * 0.0078125f);
         f2_t s2 = f2(0.f, 0.f), w12 = f2(0.f, 0.f), w22 = f2(0.f, 0.f);
-        if (__any_sync(0xFFFFFFFFu, active)) {
-          for (int v0 = 0; v0 < a.nvec; v0 += CH) {
-            uint4 v[kTfU];
-            load_chunk<BF16, G>(v, rowp, v0, gl, a.nvec, a.tail, active);
-#pragma unroll
-            for (int k = 0; k < kTfU; ++k) {
-#pragma unroll
-              for (int q = 0; q < (BF16 ? 4 : 2); ++q) {
-                f2_t x;
-                if (BF16) {
-                  const uint32_t u = bmax2_plain(wordq(v[k], q), cw);
-                  x = f2(bf_lo(u), bf_hi(u));
-                } else {
-                  x = f2(fmaxf(__uint_as_float(wordq(v[k], 2 * q)), lowf),
-                         fmaxf(__uint_as_float(wordq(v[k], 2 * q + 1)), lowf));
-                }
-                const f2_t d = f2sub(x, m2);
-                const f2_t z = f2mul(d, c2);
-                const f2_t e = f2(ex2(f2lo(z)), ex2(f2hi(z)));
-                s2 = f2add(s2, e);
-                const f2_t t = f2mul(e, d);
-                w12 = f2add(w12, t);
-                w22 = f2fma(t, d, w22);
-              }
-            }
-          }
+        accum_chunk<BF16, U>(v, m2, c2, cw, lowf, s2, w12, w22);
+        for (int v0 = CH; v0 < a.nvec; v0 += CH) {           // longer rows: further chunks
+          load_chunk<BF16, G, U>(v, rowp, v0, gl, a.nvec, a.tail, inb && active);
+          accum_chunk<BF16, U>(v, m2, c2, cw, lowf, s2, w12, w22);
         }
         float s = group_sum<float, G>(f2lo(s2) + f2hi(s2));
         float w1 = group_sum<float, G>(f2lo(w12) + f2hi(w12));
@@ -341,36 +436,31 @@ __global__ void __launch_bounds__(kTfThreads, 1) temp_fit_kernel(const TfArgs a)
           acc_h += fmax((double)w2 / ds - mean * mean, 0.0);
         }
       }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        acc_nll += __shfl_xor_sync(0xFFFFFFFFu, acc_nll, o);
-        acc_g += __shfl_xor_sync(0xFFFFFFFFu, acc_g, o);
-        acc_h += __shfl_xor_sync(0xFFFFFFFFu, acc_h, o);
-      }
-      if (lane == 0) {
-        wacc[warp][b * 3 + 0] = acc_nll;
-        wacc[warp][b * 3 + 1] = acc_g;
-        wacc[warp][b * 3 + 2] = acc_h;
-      }
     }
+    if (li >= 0) flush();
     __syncthreads();
-    if (threadIdx.x < nb * 3) {
-      const int b = threadIdx.x / 3;
+    if (threadIdx.x < nb * kTfComp) {
+      const int b = threadIdx.x / kTfComp;
       skip[b] = st[b].done;
       if (!st[b].done) {
         double v = 0.0;
         for (int w = 0; w < kTfWarps; ++w) v += wacc[w][threadIdx.x];
-        part[(size_t)blockIdx.x * nb * 3 + threadIdx.x] = v;
+        part[(size_t)blockIdx.x * nb * kTfComp + threadIdx.x] = v;
       }
     }
     grid.sync();
-    reduce_partials(part, nb, gridDim.x, red, skip);
+    reduce_partials(part, nb, gridDim.x, red, skip, kTfComp);
     __syncthreads();
     if (threadIdx.x < nb && !st[threadIdx.x].done) {
       TfState& s = st[threadIdx.x];
-      const double inv = 1.0 / (double)s.used;
-      tf_update(s, red[threadIdx.x * 3] * inv, red[threadIdx.x * 3 + 1] * inv,
-                red[threadIdx.x * 3 + 2] * inv, a);
+      if (first) s.used = (long long)red[threadIdx.x * kTfComp];
+      if (s.used == 0) {
+        s.done = 1;                                       // no usable row: T = NaN
+      } else {
+        const double inv = 1.0 / (double)s.used;
+        tf_update(s, red[threadIdx.x * kTfComp + 1] * inv, red[threadIdx.x * kTfComp + 2] * inv,
+                  red[threadIdx.x * kTfComp + 3] * inv, a);
+      }
     }
     __syncthreads();
   }
@@ -382,13 +472,13 @@ __global__ void __launch_bounds__(kTfThreads, 1) temp_fit_kernel(const TfArgs a)
     a.T[threadIdx.x] = (float)s.T;
     if (a.nll) a.nll[threadIdx.x] = s.nll;
     if (a.passes) a.passes[threadIdx.x] = s.passes;
-    if (a.used) a.used[threadIdx.x] = s.used;
+    if (a.used) a.used[threadIdx.x] = s.used < 0 ? 0 : s.used;
   }
 }
 
-template <bool BF16, int G>
+template <bool BF16, int G, int U>
 cudaError_t launch_tf(const TfArgs& a, cudaStream_t s) {
-  auto kern = temp_fit_kernel<BF16, G>;
+  auto kern = temp_fit_kernel<BF16, G, U>;
   int per_sm = 0;
   cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kTfThreads, 0);
   if (e != cudaSuccess) return e;
@@ -416,20 +506,23 @@ cudaError_t launch_tf(const TfArgs& a, cudaStream_t s) {
 
 template <bool BF16>
 cudaError_t launch_tf_dt(const TfArgs& a, cudaStream_t s) {
-  // lanes per row: enough for the row in about one chunk of kTfU vectors per lane
-  const int want = (a.nvec + kTfU - 1) / kTfU;
-  if (want <= 2) return launch_tf<BF16, 2>(a, s);
-  if (want <= 4) return launch_tf<BF16, 4>(a, s);
-  if (want <= 8) return launch_tf<BF16, 8>(a, s);
-  if (want <= 16) return launch_tf<BF16, 16>(a, s);
-  return launch_tf<BF16, 32>(a, s);
+  // lanes per row: the row in one chunk of 4 vectors per lane where possible
+  // (8 per lane at 16 lanes for 65..128 vectors: two rows per warp, 4 KB of
+  // loads in flight per warp); longer rows stream 32 x 4-vector chunks
+  const int nv = a.nvec;
+  if (nv <= 8) return launch_tf<BF16, 2, 4>(a, s);
+  if (nv <= 16) return launch_tf<BF16, 4, 4>(a, s);
+  if (nv <= 32) return launch_tf<BF16, 8, 4>(a, s);
+  if (nv <= 64) return launch_tf<BF16, 16, 4>(a, s);
+  if (nv <= 128 && !getenv("HS_TF_G32")) return launch_tf<BF16, 16, 8>(a, s);
+  return launch_tf<BF16, 32, 4>(a, s);
 }
 
 }  // namespace
 
 size_t temp_fit_ws_bytes(int nbatch, int64_t n) {
   const size_t rows = (size_t)nbatch * (size_t)(n > 0 ? n : 0) * sizeof(float2);
-  return (rows + 255) / 256 * 256 + (size_t)2 * kTfMaxGrid * nbatch * 3 * sizeof(double);
+  return (rows + 255) / 256 * 256 + (size_t)2 * kTfMaxGrid * nbatch * kTfComp * sizeof(double);
 }
 
 cudaError_t launch_temp_fit(TfArgs a, bool bf16, void* ws, cudaStream_t s) {

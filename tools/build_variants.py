@@ -10,10 +10,12 @@ VARIANTS = {
     "ctrace": ["HS_CALIB_TRACE"],        # globaltimer trace of the calibration kernels
     "noargmax": ["HS_EXP_NOARGMAX"],     # upper bounds: K1 without the argmax ...
     "noexp": ["HS_EXP_NOEXP"],           # ... or without the exponential pass
+    "tf768": ["HS_TF_THREADS=768"],      # temperature fit: 24 warps/SM, 85 registers
 }
 
 if __name__ == "__main__":
     names = sys.argv[1:] or list(VARIANTS)
     for n in names:
         out = os.path.join(ROOT, "build", "exp", f"libhs_{n}.so")
+        os.makedirs(os.path.dirname(out), exist_ok=True)
         print(_build.build_libhs(force=True, defines=VARIANTS[n], out=out))
