@@ -67,6 +67,9 @@ def lib():
             L.hso_fit_temperature.argtypes = [_P, ctypes.c_int, _I64, _I64, _I64, _P,
                                               ctypes.c_double, ctypes.c_double]
             L.hso_fit_temperature.restype = ctypes.c_double
+            L.hso_replay.argtypes = [ctypes.c_int, _I64, _P, _P, ctypes.c_int, _I64, _P, _P, _P,
+                                     _P, _P]
+            L.hso_replay.restype = None
             L.hso_skip_edges.argtypes = [ctypes.c_double, ctypes.c_int, ctypes.c_int, _P]
             L.hso_skip_edges.restype = None
             L.hso_skip_band.argtypes = [ctypes.c_double, _P, ctypes.c_int]
@@ -286,3 +289,93 @@ def bin_index(c, log2_bins: int):
     out = np.clip(out, 0, B)
     out = np.where(np.isnan(c), -1, out)
     return out.astype(np.int64)
+
+
+# --------------------------------------------------------------------------
+# NEXT-4: threshold performance graph, AP and EO (Alg. 1).
+# --------------------------------------------------------------------------
+def grid_size(K: int, log2_bins: int) -> int:
+    """Threshold vectors on the D5 grid: (B+2)^(K-1)."""
+    return ((1 << log2_bins) + 2) ** (K - 1)
+
+
+def grid_vector(s: int, K: int, log2_bins: int) -> list:
+    """Digits of grid vector s, b_0 most significant (itertools.product order)."""
+    R = (1 << log2_bins) + 2
+    b = []
+    for _ in range(K - 1):
+        b.append(s % R)
+        s //= R
+    return b[::-1]
+
+
+def replay(conf: np.ndarray, correct: np.ndarray, log2_bins: int, weights, bvecs=None):
+    """Alg. 1 line 4 for every threshold vector: (correct count, energy, reach[S, K]).
+    conf[K-1, N], correct[K, N]; bvecs[S, K-1] grid indices or None = the whole grid."""
+    c = np.ascontiguousarray(conf, dtype=np.float64)
+    ok = np.ascontiguousarray(correct, dtype=np.uint8)
+    K, N = ok.shape
+    assert c.shape == (K - 1, N)
+    if bvecs is None:
+        S = grid_size(K, log2_bins)
+        bv = None
+    else:
+        bv = np.ascontiguousarray(bvecs, dtype=np.int32).reshape(-1, K - 1)
+        S = bv.shape[0]
+    w = np.ascontiguousarray(weights, dtype=np.int64).reshape(K)
+    oc = np.empty(S, np.int64)
+    oe = np.empty(S, np.int64)
+    orch = np.empty((S, K), np.int64)
+    lib().hso_replay(int(K), int(N), _ptr(c), _ptr(ok), int(log2_bins), int(S),
+                     None if bv is None else _ptr(bv), _ptr(w), _ptr(oc), _ptr(oe), _ptr(orch))
+    return oc, oe, orch
+
+
+def perf_graph(correct_s, energy_s, tau: int, floor: int):
+    """The threshold performance graph's frontier and the AP / EO picks.
+
+    Frontier (Alg. 1 output T, the curve of P:442-444): the Pareto set of the
+    (correct count, energy) points -- for each correct count c the least energy
+    of a vector with exactly c correct (lowest vector index on ties), kept iff
+    strictly below the least energy of every larger count.  Ascending c.
+    AP (G9): the least-energy vector with >= tau correct = the first
+    frontier point with c >= tau.  EO (reading G23): among interior
+    frontier points j with c_j >= floor (a >= a_{m_{n-1}}), the largest second
+    divided difference of e(c),
+        D_j = (e_{j+1} - e_j) / (c_{j+1} - c_j) - (e_j - e_{j-1}) / (c_j - c_{j-1})
+    in fp64 (ties: lowest e); no interior candidate -> EO = AP.
+    Returns dict(front_c, front_e, front_s, ap, eo) (ap / eo: vector index or -1)."""
+    C = np.asarray(correct_s, dtype=np.int64)
+    E = np.asarray(energy_s, dtype=np.int64)
+    best = {}
+    for s in range(C.size):
+        c, e = int(C[s]), int(E[s])
+        if c not in best or e < best[c][0]:
+            best[c] = (e, s)
+    front = []
+    m = None
+    for c in sorted(best, reverse=True):
+        e, s = best[c]
+        if m is None or e < m:
+            front.append((c, e, s))
+            m = e
+    front.reverse()
+    fc = np.array([f[0] for f in front], np.int64)
+    fe = np.array([f[1] for f in front], np.int64)
+    fs = np.array([f[2] for f in front], np.int64)
+    ap = -1
+    for j in range(len(front)):
+        if fc[j] >= tau:
+            ap = int(fs[j])
+            break
+    eo, best_d = -1, None
+    for j in range(1, len(front) - 1):
+        if fc[j] < floor:
+            continue
+        d = (float(fe[j + 1] - fe[j]) / float(fc[j + 1] - fc[j])
+             - float(fe[j] - fe[j - 1]) / float(fc[j] - fc[j - 1]))
+        if best_d is None or d > best_d:
+            best_d, eo = d, int(fs[j])
+    if eo < 0:
+        eo = ap
+    return {"front_c": fc, "front_e": fe, "front_s": fs, "ap": ap, "eo": eo}

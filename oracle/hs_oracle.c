@@ -500,3 +500,53 @@ void hso_cascade_skip(int K, int64_t n, const double* conf, const double* t, int
         visits[r] = v;
     }
 }
+
+/* ------------------------------------------------------------------------- */
+/* NEXT-4. Threshold performance graph (Alg. 1 lines 3-4).        */
+/*   "Compute a on D_v and e = sum_i rho_i e_i" for every threshold set k in */
+/*   K: the cascade statement replayed on the validation set for */
+/*   each threshold vector.  Threshold index b_k on the D5 grid: t_k = b_k/B, */
+/*   b_k = B+1 = +inf (defer all); the test is c >= t_k in fp64 on the fp32  */
+/*   confidence (equivalent to bin(c) >= b_k, reading G10).  rho_i is read as */
+/*   the REACH count (reading G14): energy = sum_k reach_k * w_k with   */
+/*   integer weights w_k (reading G23).  bvec == NULL: the exhaustive grid,   */
+/*   vector s has digits b_0 (most significant) .. b_{K-2} in base B+2, i.e. */
+/*   itertools.product order.  Plain loops, one vector at a time.            */
+/* ------------------------------------------------------------------------- */
+void hso_replay(int K, int64_t N, const double* conf, const uint8_t* correct, int q,
+                int64_t S, const int32_t* bvec, const int64_t* w, int64_t* out_correct,
+                int64_t* out_energy, int64_t* out_reach /* [S*K] or NULL */) {
+    const int64_t B = (int64_t)1 << q, R = B + 2;
+    double t[64];
+    int64_t reach[64];
+    for (int64_t s = 0; s < S; ++s) {
+        int64_t rem = s;
+        for (int k = K - 2; k >= 0; --k) {
+            int64_t b;
+            if (bvec) {
+                b = bvec[s * (K - 1) + k];
+            } else {
+                b = rem % R;
+                rem /= R;
+            }
+            t[k] = (b == B + 1) ? INFINITY : (double)b / (double)B;
+        }
+        for (int k = 0; k < K; ++k) reach[k] = 0;
+        int64_t ok = 0;
+        for (int64_t r = 0; r < N; ++r) {
+            int k = 0;
+            reach[0] += 1;
+            while (k < K - 1 && !(conf[(int64_t)k * N + r] >= t[k])) {
+                ++k;
+                reach[k] += 1;
+            }
+            ok += correct[(int64_t)k * N + r] ? 1 : 0;
+        }
+        int64_t e = 0;
+        for (int k = 0; k < K; ++k) e += reach[k] * w[k];
+        out_correct[s] = ok;
+        out_energy[s] = e;
+        if (out_reach)
+            for (int k = 0; k < K; ++k) out_reach[s * K + k] = reach[k];
+    }
+}
