@@ -318,6 +318,60 @@ hs_status_t hs_fit_temperature(const void* const* logits, int32_t n_batches, hs_
                                void* ws, size_t ws_bytes, uint32_t* d_status, hs_stream_t stream);
 
 /* ------------------------------------------------------------------------ */
+/* Threshold performance graph, AP and EO (NEXT-4; Alg. 1).        */
+/* ------------------------------------------------------------------------ */
+/* hs_threshold_replay -- Alg. 1 line 4 ("Compute a on D_v and e = sum_i rho_i
+ * e_i") for S threshold vectors at once: the cascade statement
+ * replayed on the validation set for each vector.
+ *   conf [(K-1) x N] fp32 and correct [K x N] u8 as for hs_calibrate_thresholds;
+ *   2 <= K <= 8; log2_bins in [1, 14] (the D5 grid: bin(c) = min(B, floor(c*B)),
+ *   NaN never accepted).
+ *   d_bvecs: device int32 [S x (K-1)] threshold indices b_k in 0..B+1 (t_k = b_k/B,
+ *   B+1 = defer all; values outside are clamped by the compare), or NULL = the
+ *   exhaustive grid: S must equal hs_grid_size(K, log2_bins) and vector s has
+ *   the digits hs_grid_vector(s) (b_0 most significant).
+ *   weights: HOST int64 [K] >= 0, energy of one visit of model k (integer
+ *   units, reading G23; rho_k = reach, S:210 / G14).
+ * Outputs (device, per vector s): d_correct[s] = correct answers of the
+ * cascade, d_energy[s] = sum_k reach_k * weights[k], d_reach[s*K + k]
+ * (optional) = requests reaching model k; d_model_correct[k] (optional) = the
+ * correct count of model k alone (tau = [K-1] for AP, the EO floor = [K-2]).
+ * All exact integers (bit-exact vs the oracle).  S < 2^31, N < 2^32, the
+ * energy of a vector < 2^63.  Workspace: hs_threshold_replay_workspace(K, N). */
+int64_t hs_grid_size(int32_t K, int32_t log2_bins);       /* (B+2)^(K-1), or -1 if >= 2^31 / bad args */
+hs_status_t hs_grid_vector(int64_t s, int32_t K, int32_t log2_bins, int32_t* b /* host [K-1] */);
+size_t hs_threshold_replay_workspace(int32_t K, int64_t N);
+hs_status_t hs_threshold_replay(const float* conf, const uint8_t* correct, int32_t K, int64_t N,
+                                int32_t log2_bins, const int32_t* d_bvecs, int64_t S,
+                                const int64_t* weights, int64_t* d_correct, int64_t* d_energy,
+                                int64_t* d_reach, int64_t* d_model_correct, void* ws,
+                                size_t ws_bytes, hs_stream_t stream);
+
+/* hs_perf_graph -- the threshold performance graph (the accuracy-vs-energy
+ * curve of P:442-444) as its Pareto frontier, and the AP / EO picks.
+ *   Input: S points (d_correct[s] in 0..N, d_energy[s] >= 0), e.g. from
+ *   hs_threshold_replay.  Frontier: for each correct count c the least energy
+ *   of a point with exactly c correct (lowest index on ties), kept iff
+ *   strictly below the least energy of every larger count; ascending c (both
+ *   c and energy strictly increase).  d_front_c / d_front_e / d_front_s
+ *   (capacity N+1) and d_front_n[0] = its length.
+ *   AP (G9): d_pick[0] = the least-energy point with >= tau correct
+ *   (-1 if none).  EO (G23): d_pick[1] = the interior frontier point
+ *   j with c_j >= floor maximising (e_{j+1}-e_j)/(c_{j+1}-c_j) -
+ *   (e_j-e_{j-1})/(c_j-c_{j-1}) (fp64, ties to the lowest energy); the AP pick
+ *   when no interior point qualifies.
+ *   tau / floor_ < 0: taken from d_model_correct[K-1] / [K-2] (required then).
+ *   Points with a correct count outside 0..N or a negative energy are ignored
+ *   and set HS_STATUS_NONFINITE in *d_status.
+ * Workspace: hs_perf_graph_workspace(N). */
+size_t hs_perf_graph_workspace(int64_t N);
+hs_status_t hs_perf_graph(const int64_t* d_correct, const int64_t* d_energy, int64_t S, int64_t N,
+                          int64_t tau, int64_t floor_, const int64_t* d_model_correct, int32_t K,
+                          int64_t* d_front_c, int64_t* d_front_e, int64_t* d_front_s,
+                          int64_t* d_front_n, int64_t* d_pick, void* ws, size_t ws_bytes,
+                          uint32_t* d_status, hs_stream_t stream);
+
+/* ------------------------------------------------------------------------ */
 /* Diagnostics.                                                              */
 /* ------------------------------------------------------------------------ */
 const char* hs_status_string(hs_status_t s);

@@ -29,7 +29,8 @@ STATUS_NONFINITE = 1
 STATUS_NOT_CONVERGED = 2
 
 __all__ = ["confidence", "confidence_batched", "route_compact", "cascade_step", "calibrate_thresholds",
-           "calibrate_begin", "calibrate_histogram", "calibrate_select", "fit_temperature", "Cascade", "HsError",
+           "calibrate_begin", "calibrate_histogram", "calibrate_select", "fit_temperature", "threshold_replay", "perf_graph", "grid_size", "grid_vector",
+           "Cascade", "HsError",
            "launch_count", "MAXPROB", "MAXPROB_SQ", "ENTROPY", "SEQ_NONE", "SEQ_MIN", "SEQ_MEAN"]
 
 
@@ -195,6 +196,72 @@ def fit_temperature(logits: list, labels: torch.Tensor, *, n: int | None = None,
     _abi.call("hs_fit_temperature", ptrs, nb, _dtype_code(x0), n, C, int(x0.stride(0)), _p(labels),
               float(t_lo), float(t_hi), int(max_passes), _p(out["T"]), _p(out["nll"]),
               _p(out["passes"]), _p(out["used"]), _p(ws), ws.numel(), _p(status), _stream(stream))
+    return out
+
+
+# ---------------------------------------------------------------------------
+# NEXT-4: threshold performance graph (Alg. 1)
+# ---------------------------------------------------------------------------
+def grid_size(K: int, log2_bins: int) -> int:
+    """(B+2)^(K-1) threshold vectors on the D5 grid (-1 if too many)."""
+    return int(lib().hs_grid_size(int(K), int(log2_bins)))
+
+
+def grid_vector(s: int, K: int, log2_bins: int) -> list:
+    """Threshold indices b_0..b_{K-2} of grid vector s (b_0 most significant)."""
+    import ctypes
+    b = (ctypes.c_int32 * max(1, K - 1))()
+    _abi.call("hs_grid_vector", int(s), int(K), int(log2_bins), b)
+    return list(b)[: K - 1]
+
+
+def threshold_replay(conf: torch.Tensor, correct: torch.Tensor, weights, *, log2_bins: int = 12,
+                     bvecs: torch.Tensor | None = None, want_reach: bool = False,
+                     out: dict | None = None, ws: torch.Tensor | None = None, stream=None) -> dict:
+    """Replay the cascade for S threshold vectors (``bvecs`` [S, K-1] int32, or
+    None = the whole grid): ``correct`` i64[S], ``energy`` i64[S] (sum_k reach_k
+    * weights[k]), optional ``reach`` i64[S, K], ``model_correct`` i64[K]."""
+    import ctypes
+    _check_cuda(conf, correct, bvecs)
+    K, N = int(correct.shape[0]), int(correct.shape[1])
+    S = grid_size(K, log2_bins) if bvecs is None else int(bvecs.shape[0])
+    dev = conf.device
+    out = dict(out or {})
+    out.setdefault("correct", torch.empty(S, dtype=torch.int64, device=dev))
+    out.setdefault("energy", torch.empty(S, dtype=torch.int64, device=dev))
+    out.setdefault("model_correct", torch.empty(K, dtype=torch.int64, device=dev))
+    if want_reach:
+        out.setdefault("reach", torch.empty(S, K, dtype=torch.int64, device=dev))
+    need = lib().hs_threshold_replay_workspace(K, N)
+    if ws is None or ws.numel() < need:
+        ws = torch.empty(need, dtype=torch.uint8, device=dev)
+    w = (ctypes.c_int64 * K)(*[int(x) for x in weights])
+    _abi.call("hs_threshold_replay", _p(conf), _p(correct), K, N, int(log2_bins), _p(bvecs), S, w,
+              _p(out["correct"]), _p(out["energy"]), _p(out.get("reach")), _p(out["model_correct"]),
+              _p(ws), ws.numel(), _stream(stream))
+    return out
+
+
+def perf_graph(correct: torch.Tensor, energy: torch.Tensor, N: int, *, tau: int = -1, floor: int = -1,
+               model_correct: torch.Tensor | None = None, K: int = 0, status: torch.Tensor | None = None,
+               out: dict | None = None, ws: torch.Tensor | None = None, stream=None) -> dict:
+    """Pareto frontier of the (correct, energy) points and the AP / EO picks:
+    ``front_c``/``front_e``/``front_s`` i64[N+1] (first ``front_n`` valid),
+    ``pick`` i64[2] = (AP vector, EO vector)."""
+    _check_cuda(correct, energy, model_correct, status)
+    S = int(correct.numel())
+    dev = correct.device
+    out = dict(out or {})
+    for k in ("front_c", "front_e", "front_s"):
+        out.setdefault(k, torch.empty(N + 1, dtype=torch.int64, device=dev))
+    out.setdefault("front_n", torch.empty(1, dtype=torch.int64, device=dev))
+    out.setdefault("pick", torch.empty(2, dtype=torch.int64, device=dev))
+    need = lib().hs_perf_graph_workspace(N)
+    if ws is None or ws.numel() < need:
+        ws = torch.empty(need, dtype=torch.uint8, device=dev)
+    _abi.call("hs_perf_graph", _p(correct), _p(energy), S, int(N), int(tau), int(floor),
+              _p(model_correct), int(K), _p(out["front_c"]), _p(out["front_e"]), _p(out["front_s"]),
+              _p(out["front_n"]), _p(out["pick"]), _p(ws), ws.numel(), _p(status), _stream(stream))
     return out
 
 

@@ -306,6 +306,92 @@ hs_status_t hs_fit_temperature(const void* const* logits, int32_t n_batches, hs_
                     "temperature fitting kernel");
 }
 
+int64_t hs_grid_size(int32_t K, int32_t log2_bins) {
+  if (K < 2 || K > hs::kReplayMaxK || log2_bins < 1 || log2_bins > 14) return -1;
+  const int64_t R = ((int64_t)1 << log2_bins) + 2;
+  int64_t S = 1;
+  for (int k = 0; k < K - 1; ++k) {
+    S *= R;
+    if (S >= ((int64_t)1 << 31)) return -1;
+  }
+  return S;
+}
+
+hs_status_t hs_grid_vector(int64_t s, int32_t K, int32_t log2_bins, int32_t* b) {
+  const int64_t S = hs_grid_size(K, log2_bins);
+  if (S < 0 || s < 0 || s >= S || !b) return fail(HS_ERR_INVALID_ARGUMENT, "bad grid vector query");
+  const int64_t R = ((int64_t)1 << log2_bins) + 2;
+  for (int k = K - 2; k >= 0; --k) {
+    b[k] = (int32_t)(s % R);
+    s /= R;
+  }
+  return HS_OK;
+}
+
+size_t hs_threshold_replay_workspace(int32_t K, int64_t N) {
+  return hs::replay_ws_bytes(K < 2 ? 2 : K, N < 0 ? 0 : N);
+}
+
+hs_status_t hs_threshold_replay(const float* conf, const uint8_t* correct, int32_t K, int64_t N,
+                                int32_t log2_bins, const int32_t* d_bvecs, int64_t S,
+                                const int64_t* weights, int64_t* d_correct, int64_t* d_energy,
+                                int64_t* d_reach, int64_t* d_model_correct, void* ws,
+                                size_t ws_bytes, hs_stream_t stream) {
+  if (K < 2 || K > hs::kReplayMaxK) return fail(HS_ERR_INVALID_ARGUMENT, "K = %d outside 2..%d", K, hs::kReplayMaxK);
+  if (log2_bins < 1 || log2_bins > 14) return fail(HS_ERR_INVALID_ARGUMENT, "log2_bins = %d outside 1..14", log2_bins);
+  if (N < 1 || N >= ((int64_t)1 << 32)) return fail(HS_ERR_INVALID_ARGUMENT, "N = %lld outside 1..2^32-1 (empty trace)", (long long)N);
+  if (S < 0 || S >= ((int64_t)1 << 31)) return fail(HS_ERR_INVALID_ARGUMENT, "S = %lld outside 0..2^31-1", (long long)S);
+  if (!d_bvecs && S != hs_grid_size(K, log2_bins))
+    return fail(HS_ERR_INVALID_ARGUMENT, "d_bvecs == NULL requires S == hs_grid_size(K, log2_bins)");
+  if (!conf || !correct || !weights || (S > 0 && (!d_correct || !d_energy)))
+    return fail(HS_ERR_INVALID_ARGUMENT, "conf, correct, weights, d_correct and d_energy are required");
+  hs::ReplayArgs a{};
+  unsigned long long cum = 0;
+  for (int k = 0; k < K; ++k) {
+    if (weights[k] < 0) return fail(HS_ERR_INVALID_ARGUMENT, "weights must be >= 0");
+    const unsigned long long add = (unsigned long long)weights[k];
+    if (cum + add < cum || (cum + add) > (~0ull >> 1) / (unsigned long long)N)
+      return fail(HS_ERR_INVALID_ARGUMENT, "energy would overflow int64");
+    cum += add;
+    a.w.cum[k] = cum;
+  }
+  const size_t need = hs::replay_ws_bytes(K, N);
+  if (ws_bytes < need || !ws) return fail(HS_ERR_WORKSPACE_TOO_SMALL, "workspace %zu < %zu", ws_bytes, need);
+  a.K = K;
+  a.N = N;
+  a.q = log2_bins;
+  a.bvecs = d_bvecs;
+  a.S = S;
+  a.out_c = d_correct;
+  a.out_e = d_energy;
+  a.reach = d_reach;
+  return cuda_check(hs::launch_replay(a, conf, correct, reinterpret_cast<unsigned long long*>(d_model_correct),
+                                      ws, (cudaStream_t)stream),
+                    "threshold replay kernels");
+}
+
+size_t hs_perf_graph_workspace(int64_t N) { return hs::graph_ws_bytes(N < 0 ? 0 : N); }
+
+hs_status_t hs_perf_graph(const int64_t* d_correct, const int64_t* d_energy, int64_t S, int64_t N,
+                          int64_t tau, int64_t floor_, const int64_t* d_model_correct, int32_t K,
+                          int64_t* d_front_c, int64_t* d_front_e, int64_t* d_front_s,
+                          int64_t* d_front_n, int64_t* d_pick, void* ws, size_t ws_bytes,
+                          uint32_t* d_status, hs_stream_t stream) {
+  if (S < 0 || N < 0) return fail(HS_ERR_INVALID_ARGUMENT, "S and N must be >= 0");
+  if (S > 0 && (!d_correct || !d_energy)) return fail(HS_ERR_INVALID_ARGUMENT, "d_correct / d_energy are required");
+  if (!d_front_c || !d_front_e || !d_front_s || !d_front_n || !d_pick)
+    return fail(HS_ERR_INVALID_ARGUMENT, "frontier outputs and d_pick are required");
+  if ((tau < 0 || floor_ < 0) && (!d_model_correct || K < 2 || K > hs::kReplayMaxK))
+    return fail(HS_ERR_INVALID_ARGUMENT, "tau / floor < 0 need d_model_correct and 2 <= K <= %d", hs::kReplayMaxK);
+  const size_t need = hs::graph_ws_bytes(N);
+  if (ws_bytes < need || !ws) return fail(HS_ERR_WORKSPACE_TOO_SMALL, "workspace %zu < %zu", ws_bytes, need);
+  return cuda_check(hs::launch_graph(d_correct, d_energy, S, N, tau, floor_,
+                                     reinterpret_cast<const unsigned long long*>(d_model_correct), K,
+                                     d_front_c, d_front_e, d_front_s, d_front_n, d_pick, d_status, ws,
+                                     (cudaStream_t)stream),
+                    "performance graph kernels");
+}
+
 size_t hs_route_compact_workspace(int64_t n) { return hs::compact_ws_bytes(n); }
 
 static hs_status_t route_compact_impl(const float* conf, int64_t n, const int64_t* d_n,

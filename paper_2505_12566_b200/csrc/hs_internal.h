@@ -173,4 +173,32 @@ struct TfArgs {
 size_t temp_fit_ws_bytes(int nbatch, int64_t n);
 cudaError_t launch_temp_fit(TfArgs a, bool bf16, void* ws, cudaStream_t s);
 
+// ---- NEXT-4: threshold performance graph (Alg. 1) ---------------------------
+constexpr int kReplayMaxK = 8;
+struct ReplayWeights {
+  unsigned long long cum[kReplayMaxK];   // cum[j] = sum_{k <= j} w_k: energy of a request answered by m_j
+};
+struct ReplayArgs {
+  int K;                    // models (2..kReplayMaxK)
+  int64_t N;                // validation samples
+  int64_t Np;               // N rounded up to 4 (set by launch_replay)
+  int q;                    // log2 bins
+  const int32_t* bvecs;     // [S x (K-1)] grid indices, or NULL = the exhaustive grid
+  int64_t S;                // threshold vectors
+  ReplayWeights w;
+  int32_t* bins;            // ws: [(K-1) x Np]
+  uint32_t* bits;           // ws: [Np] correct bits
+  int64_t* out_c;           // [S] correct counts
+  int64_t* out_e;           // [S] energies
+  int64_t* reach;           // [S x K] or NULL
+};
+size_t replay_ws_bytes(int K, int64_t N);
+cudaError_t launch_replay(ReplayArgs a, const float* conf, const uint8_t* correct,
+                          unsigned long long* model_correct, void* ws, cudaStream_t s);
+size_t graph_ws_bytes(int64_t N);
+cudaError_t launch_graph(const int64_t* C, const int64_t* E, int64_t S, int64_t N, int64_t tau,
+                         int64_t floor_, const unsigned long long* model_correct, int K,
+                         int64_t* front_c, int64_t* front_e, int64_t* front_s, int64_t* front_n,
+                         int64_t* pick, uint32_t* status, void* ws, cudaStream_t s);
+
 }  // namespace hs

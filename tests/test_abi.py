@@ -140,3 +140,40 @@ def test_fit_temperature_argument_errors(libhs):
         assert call(**kw) == 1, kw
         assert needle in lib.hs_last_error().decode(), kw
     assert call(wsb=ws - 1) == 5
+
+
+def test_grid_helpers_match_oracle(libhs):
+    """hs_grid_size / hs_grid_vector are host arithmetic (no device work)."""
+    import oracle
+    import paper_2505_12566_b200 as hs
+    for K, q in ((2, 1), (3, 2), (5, 4), (8, 1)):
+        S = hs.grid_size(K, q)
+        assert S == oracle.grid_size(K, q)
+        for s in (0, 1, S // 3, S - 1):
+            assert hs.grid_vector(s, K, q) == oracle.grid_vector(s, K, q)
+    assert hs.grid_size(5, 14) == -1 and hs.grid_size(9, 1) == -1 and hs.grid_size(1, 4) == -1
+
+
+def test_replay_and_graph_argument_errors(libhs):
+    lib = libhs.lib()
+    w = (ctypes.c_int64 * 3)(1, 2, 3)
+    ws = lib.hs_threshold_replay_workspace(3, 100)
+    def rp(K=3, N=100, q=4, bv=None, S=None, wt=w, wsb=ws):
+        S = lib.hs_grid_size(K, q) if S is None else S
+        return lib.hs_threshold_replay(256, 512, K, N, q, bv, S, wt, 1024, 2048, None, None, 4096, wsb, None)
+    assert rp(K=1) == 1 and "K" in lib.hs_last_error().decode()
+    assert rp(K=9) == 1
+    assert rp(q=0) == 1 and "log2_bins" in lib.hs_last_error().decode()
+    assert rp(N=0) == 1 and "empty" in lib.hs_last_error().decode()
+    assert rp(S=7) == 1 and "hs_grid_size" in lib.hs_last_error().decode()
+    neg = (ctypes.c_int64 * 3)(1, -2, 3)
+    assert rp(wt=neg) == 1 and "weights" in lib.hs_last_error().decode()
+    big = (ctypes.c_int64 * 3)(1, 1 << 62, 3)
+    assert rp(wt=big) == 1 and "overflow" in lib.hs_last_error().decode()
+    assert rp(wsb=ws - 1) == 5
+    gws = lib.hs_perf_graph_workspace(100)
+    assert gws >= 101 * 16
+    rc = lib.hs_perf_graph(256, 512, 10, 100, -1, 5, None, 3, 1, 2, 3, 4, 5, 4096, gws, None, None)
+    assert rc == 1 and "d_model_correct" in lib.hs_last_error().decode()
+    rc = lib.hs_perf_graph(256, 512, 10, 100, 5, 5, None, 3, 1, 2, 3, 4, 5, 4096, gws - 1, None, None)
+    assert rc == 5
