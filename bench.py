@@ -34,9 +34,11 @@ CONFIG_TEXT = {
     "c4": "3-stage Llama-like next-token cascade, 8,192 requests x 128,256 vocab bf16 per GPU, entropy confidence, 8 KB hidden-state payload gathered",
     "c5": "5-stage ViT streaming cascade, 1,048,576 requests x 1,000 classes bf16 per GPU (8M over 8 GPUs), validation 131,072 per GPU",
     "c3k": "c3 with the Top-K (K = 10) restricted token confidence of P:420-424 (NEXT-2), MIN over 64 tokens",
+    "c2g": "NEXT-4: threshold performance graph of the 5 C2 ViT stage models: the exhaustive q = 4 grid (18^4 = 104,976 threshold vectors) replayed on the 50,000-sample validation set per GPU, Pareto frontier, AP and EO picks",
     "c2t": "NEXT-3: temperature fitting (Eq. 1, P:384-389) of the 5 C2 ViT stage models on the 50,000-sample validation set per GPU, 1,000 classes bf16, T in [e^-4, e^4]",
 }
 METRIC_TEMP = "temperature fitting (Eq. 1): stage-model validation rows fitted per second"
+METRIC_GRAPH = "threshold performance graph (Alg. 1): threshold-vector x validation-sample cascade replays per second"
 
 
 def parse():
@@ -615,6 +617,147 @@ def run_temperature(args, world, rank, local):
     return line, fam, val, labels
 
 
+GRAPH_Q = 4
+GRAPH_W = (1, 2, 4, 8, 16)     # integer energy per visit, ViT-XS .. ViT-L (synthetic ratios)
+
+
+def graph_inputs(fam, rank, dev):
+    """The validation confidences / correct bits of every stage model (the input
+    of Alg. 1), computed once on the GPU before timing."""
+    import paper_2505_12566_b200 as hs
+    _, val, labels, _ = build_inputs(synth_scaled(fam, n=1), rank, dev)
+    r = hs.confidence_batched(val, fam.temps, labels=labels)
+    K, n = fam.K, fam.n_val
+    conf = r["conf"].view(K, n)[: K - 1].contiguous()
+    ok = r["correct"].view(K, n).contiguous()
+    return conf, ok
+
+
+def run_graph(args, world, rank, local):
+    """Step = hs_threshold_replay over the whole q = 4 grid + hs_perf_graph
+    (frontier, AP, EO).  N > 1: independent replicas on shard-local samples."""
+    import torch
+    import paper_2505_12566_b200 as hs
+    dev = torch.device("cuda", local)
+    fam = family("c2")
+    conf, ok = graph_inputs(fam, rank, dev)
+    K, n = fam.K, fam.n_val
+    S = hs.grid_size(K, GRAPH_Q)
+    rws = torch.empty(hs.lib().hs_threshold_replay_workspace(K, n), dtype=torch.uint8, device=dev)
+    gws = torch.empty(hs.lib().hs_perf_graph_workspace(n), dtype=torch.uint8, device=dev)
+    rout, gout = {}, {}
+
+    def step():
+        r = hs.threshold_replay(conf, ok, GRAPH_W, log2_bins=GRAPH_Q, out=rout, ws=rws)
+        rout.update(r)
+        g = hs.perf_graph(r["correct"], r["energy"], n, model_correct=r["model_correct"], K=K,
+                          out=gout, ws=gws)
+        gout.update(g)
+
+    stream = torch.cuda.Stream(device=dev)
+    with torch.cuda.stream(stream):
+        for _ in range(max(args.warmup, 3)):
+            step()
+    torch.cuda.synchronize()
+    graph = None
+    launches_per_step = None
+    if not args.no_graph:
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=stream):
+            l0 = hs.launch_count()
+            step()
+            launches_per_step = hs.launch_count() - l0
+        graph.replay()
+        torch.cuda.synchronize()
+    ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    barrier(world)
+    torch.cuda.synchronize()
+    l_before = hs.launch_count()
+    with ClockSampler(local) as clk:
+        with torch.cuda.stream(stream):
+            t0.record(stream)
+            for _ in range(args.steps):
+                graph.replay() if graph is not None else step()
+            t1.record(stream)
+        torch.cuda.synchronize()
+    barrier(world)
+    ms = max_over_ranks(t0.elapsed_time(t1), world) / args.steps
+    if launches_per_step is None:
+        launches_per_step = (hs.launch_count() - l_before) / args.steps
+    # the replay kernel alone (eager, CUDA events on its stream)
+    rk = []
+    with torch.cuda.stream(stream):
+        for _ in range(10):
+            ev[0].record(stream)
+            hs.threshold_replay(conf, ok, GRAPH_W, log2_bins=GRAPH_Q, out=rout, ws=rws)
+            ev[1].record(stream)
+            stream.synchronize()
+            rk.append(ev[0].elapsed_time(ev[1]))
+    replay_ms = sorted(rk)[len(rk) // 2]
+    evals = S * n
+    # per (vector, sample): K-1 compares + K-1 selects + 2 (correct bit) + 1 (add)
+    # + 2 (64-bit energy add) thread instructions, the algorithm's minimum
+    ops_per_eval = 2 * (K - 1) + 5
+    clocks = clk.summary()
+    mhz = clocks.get("sm_max_mhz") or 1965
+    # the compares / selects / shifts / integer adds all issue to the ALU pipe:
+    # reciprocal throughput 2 cycles per warp instruction per SMSP (B300_MICROARCH.md
+    # "fma vs alu split", same SM design) = 16 lanes/clk/SMSP, 64/clk/SM
+    peak = 148 * 4 * 16 * mhz * 1e6 / 1e12
+    achieved = ops_per_eval * evals / (replay_ms / 1e3) / 1e12
+    pick = gout["pick"].cpu().tolist()
+    fn = int(gout["front_n"].item())
+    line = {
+        "metric": METRIC_GRAPH, "value": evals * world / (ms / 1e3), "unit": "replays/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
+        "data": "synthetic",
+        "config": {"workload": "c2g_vit5_grid_q4", "description": CONFIG_TEXT["c2g"],
+                   "validation_per_gpu": n, "K": K, "log2_bins": GRAPH_Q, "vectors": S,
+                   "energy_weights": list(GRAPH_W),
+                   "parallelism": f"independent replicas x{world} (shard-local graph)",
+                   "l2": "samples re-read from L2 by every CTA (2.5 MB working set, by design)",
+                   "cuda_graph": graph is not None},
+        "frontier_points": fn, "ap_vector": hs.grid_vector(pick[0], K, GRAPH_Q) if pick[0] >= 0 else None,
+        "eo_vector": hs.grid_vector(pick[1], K, GRAPH_Q) if pick[1] >= 0 else None,
+        "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Tinstr/s",
+                     "frac": achieved / peak, "traffic": None,
+                     "kernel": f"replay_kernel<{K - 1}> ({S} vectors x {n} samples, {ops_per_eval} "
+                               "algorithmic thread-instructions per replay)",
+                     "avg_launch_ms": replay_ms,
+                     "peak_source": "derived: ALU pipe 148 SMs x 4 SMSPs x 16 lanes/clk (rt 2 clk/warp-instr, B300_MICROARCH.md) x max SM clock"},
+        "e2e": None, "gpu_launches": launches_per_step * args.steps, "clocks": clocks,
+        "gpu_launches_per_step": launches_per_step,
+    }
+    return line, fam, conf, ok
+
+
+def cpu_baseline_graph(fam, seconds, conf, ok):
+    """The oracle's replay (plain C loops, one thread) on a bounded sample of
+    the grid's vectors over the same validation set."""
+    import numpy as np
+    import oracle
+    c = conf.cpu().numpy()
+    o = ok.cpu().numpy()
+    K, n = o.shape
+    S = oracle.grid_size(K, GRAPH_Q)
+    m = 4
+    while True:
+        idx = np.linspace(0, S - 1, m).astype(np.int64)
+        bv = np.array([oracle.grid_vector(int(s), K, GRAPH_Q) for s in idx], np.int32)
+        t = time.perf_counter()
+        oracle.replay(c, o, GRAPH_Q, GRAPH_W, bvecs=bv)
+        dt = time.perf_counter() - t
+        if dt >= seconds / 3 or m >= S:
+            break
+        m = min(S, int(m * max(2.0, seconds / max(dt, 1e-3))))
+    return {"value": m * n / dt, "unit": "replays/s", "cores": 1, "kind": "oracle",
+            "sample": f"{m} of the {S} grid vectors (evenly spaced) x all {n} validation samples, "
+                      f"fp64 C oracle (hso_replay), 1 thread, {dt:.1f} s"}
+
+
 def synth_scaled(fam, **kw):
     from workload import synth
     return synth.scaled(fam, **kw)
@@ -719,6 +862,8 @@ def run_reference(args, world, rank):
         return None
     if args.config == "c2t":
         return run_reference_temperature(args, world)
+    if args.config == "c2g":
+        return run_reference_graph(args, world)
     fam = family(args.config)
     budget = 150.0 / max(1, args.steps + args.warmup)
     n, v = cpu_sample_sizes(fam, min(budget, 20.0))
@@ -790,6 +935,57 @@ def run_reference_temperature(args, world):
             "e2e": {"value": value, "unit": "rows/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
+def run_reference_graph(args, world):
+    """--impl reference --config c2g: the oracle's replay of a bounded vector
+    sample per step, on oracle confidences of the same validation set."""
+    import numpy as np
+    import oracle
+    from workload import synth
+    fam = family("c2")
+    K, n = fam.K, fam.n_val
+    vids = np.arange(n, dtype=np.int64) + synth.VAL_ID_BASE
+    lab = synth.labels_np(fam.seed, vids, 1, fam.C).reshape(-1)
+    conf = np.empty((K - 1, n))
+    ok = np.empty((K, n), np.uint8)
+    for k in range(K):
+        bits = synth.logits_np(fam.seed, k, vids, 1, fam.C, fam.thr[k], "bf16")
+        r = oracle.confidence(bits, n, 1, fam.C, fam.C, fam.temps[k], labels=lab)
+        ok[k] = r["correct"]
+        if k < K - 1:
+            conf[k] = r["conf"]
+    S = oracle.grid_size(K, GRAPH_Q)
+    budget = min(10.0, 150.0 / max(1, args.steps + args.warmup))
+    m = 4
+    while True:
+        bv = np.array([oracle.grid_vector(int(s), K, GRAPH_Q)
+                       for s in np.linspace(0, S - 1, m).astype(np.int64)], np.int32)
+        t = time.perf_counter()
+        oracle.replay(conf, ok, GRAPH_Q, GRAPH_W, bvecs=bv)
+        dt = time.perf_counter() - t
+        if dt >= budget / 3 or m >= S:
+            break
+        m = min(S, int(m * max(2.0, budget / max(dt, 1e-3))))
+    for _ in range(args.warmup):
+        oracle.replay(conf, ok, GRAPH_Q, GRAPH_W, bvecs=bv)
+    tot = 0.0
+    for _ in range(args.steps):
+        t = time.perf_counter()
+        oracle.replay(conf, ok, GRAPH_Q, GRAPH_W, bvecs=bv)
+        tot += time.perf_counter() - t
+    value = m * n * args.steps / tot
+    sample = f"{m} of the {S} grid vectors x all {n} validation samples per step"
+    return {"impl": "reference", "metric": METRIC_GRAPH, "value": value, "unit": "replays/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": tot / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "c2g_vit5_grid_q4", "description": CONFIG_TEXT["c2g"],
+                       "validation_per_gpu": n, "K": K, "log2_bins": GRAPH_Q,
+                       "parallelism": "host core (oracle, 1 thread)"},
+            "cpu_baseline": {"value": value, "unit": "replays/s", "cores": 1, "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": "replays/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
 def _claim_stdout():
     """Route C-level stdout (NCCL's version banner, library prints) to stderr for
     the whole run; return a writer for the one JSON line on the real stdout."""
@@ -820,6 +1016,13 @@ def main():
         os.environ["RANK"] = "0"
         os.environ["LOCAL_RANK"] = "0"
     world, rank, local = init_dist(args, force=args.placement == "balanced" or args.force_dist)
+    if args.config == "c2g":
+        line, fam, conf, ok = run_graph(args, world, rank, local)
+        if rank == 0 and world == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline_graph(fam, args.cpu_seconds, conf, ok)
+        if rank == 0:
+            emit(json.dumps(line))
+        return
     if args.config == "c2t":
         line, fam, val, labels = run_temperature(args, world, rank, local)
         if rank == 0 and world == 1 and not args.no_cpu_baseline:
