@@ -643,7 +643,7 @@ def run_graph(args, world, rank, local):
     conf, ok = graph_inputs(fam, rank, dev)
     K, n = fam.K, fam.n_val
     S = hs.grid_size(K, GRAPH_Q)
-    rws = torch.empty(hs.lib().hs_threshold_replay_workspace(K, n), dtype=torch.uint8, device=dev)
+    rws = torch.empty(hs.lib().hs_threshold_replay_workspace(K, n, GRAPH_Q), dtype=torch.uint8, device=dev)
     gws = torch.empty(hs.lib().hs_perf_graph_workspace(n), dtype=torch.uint8, device=dev)
     rout, gout = {}, {}
 
@@ -697,16 +697,20 @@ def run_graph(args, world, rank, local):
             rk.append(ev[0].elapsed_time(ev[1]))
     replay_ms = sorted(rk)[len(rk) // 2]
     evals = S * n
-    # per (vector, sample): K-1 compares + K-1 selects + 2 (correct bit) + 1 (add)
-    # + 2 (64-bit energy add) thread instructions, the algorithm's minimum
-    ops_per_eval = 2 * (K - 1) + 5
+    # the exhaustive grid runs through the prefix histograms (q <= 5): one visit
+    # per (prefix b_0..b_{K-3}, sample); its ALU work per visit is K-2 compares +
+    # K-2 selects (answering model), 2 (correct bit), 2(K-2) (reach counts) and
+    # 4 (histogram address + 64-bit add) thread instructions
+    R = (1 << GRAPH_Q) + 2
+    visits = (S // R) * n
+    ops_per_visit = 4 * (K - 2) + 6
     clocks = clk.summary()
     mhz = clocks.get("sm_max_mhz") or 1965
     # the compares / selects / shifts / integer adds all issue to the ALU pipe:
     # reciprocal throughput 2 cycles per warp instruction per SMSP (B300_MICROARCH.md
     # "fma vs alu split", same SM design) = 16 lanes/clk/SMSP, 64/clk/SM
     peak = 148 * 4 * 16 * mhz * 1e6 / 1e12
-    achieved = ops_per_eval * evals / (replay_ms / 1e3) / 1e12
+    achieved = ops_per_visit * visits / (replay_ms / 1e3) / 1e12
     pick = gout["pick"].cpu().tolist()
     fn = int(gout["front_n"].item())
     line = {
@@ -724,8 +728,9 @@ def run_graph(args, world, rank, local):
         "eo_vector": hs.grid_vector(pick[1], K, GRAPH_Q) if pick[1] >= 0 else None,
         "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Tinstr/s",
                      "frac": achieved / peak, "traffic": None,
-                     "kernel": f"replay_kernel<{K - 1}> ({S} vectors x {n} samples, {ops_per_eval} "
-                               "algorithmic thread-instructions per replay)",
+                     "kernel": f"hs_threshold_replay: replay_hist_kernel<{K - 1}> + prep / finish "
+                               f"({S // R} prefixes x {n} samples = {visits} visits, {ops_per_visit} "
+                               "algorithmic ALU instructions per visit; timed as the whole call)",
                      "avg_launch_ms": replay_ms,
                      "peak_source": "derived: ALU pipe 148 SMs x 4 SMSPs x 16 lanes/clk (rt 2 clk/warp-instr, B300_MICROARCH.md) x max SM clock"},
         "e2e": None, "gpu_launches": launches_per_step * args.steps, "clocks": clocks,

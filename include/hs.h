@@ -337,10 +337,13 @@ hs_status_t hs_fit_temperature(const void* const* logits, int32_t n_batches, hs_
  * (optional) = requests reaching model k; d_model_correct[k] (optional) = the
  * correct count of model k alone (tau = [K-1] for AP, the EO floor = [K-2]).
  * All exact integers (bit-exact vs the oracle).  S < 2^31, N < 2^32, the
- * energy of a vector < 2^63.  Workspace: hs_threshold_replay_workspace(K, N). */
+ * energy of a vector < 2^63.  Workspace: hs_threshold_replay_workspace(K, N, log2_bins)
+ * (0 for bad K / log2_bins).  The exhaustive grid with B+2 <= 48 (log2_bins <= 5)
+ * and N < 2^21 is evaluated through per-prefix histograms of the last
+ * threshold's bins ((B+2)x fewer sample visits); results are identical. */
 int64_t hs_grid_size(int32_t K, int32_t log2_bins);       /* (B+2)^(K-1), or -1 if >= 2^31 / bad args */
 hs_status_t hs_grid_vector(int64_t s, int32_t K, int32_t log2_bins, int32_t* b /* host [K-1] */);
-size_t hs_threshold_replay_workspace(int32_t K, int64_t N);
+size_t hs_threshold_replay_workspace(int32_t K, int64_t N, int32_t log2_bins);
 hs_status_t hs_threshold_replay(const float* conf, const uint8_t* correct, int32_t K, int64_t N,
                                 int32_t log2_bins, const int32_t* d_bvecs, int64_t S,
                                 const int64_t* weights, int64_t* d_correct, int64_t* d_energy,

@@ -232,7 +232,7 @@ def threshold_replay(conf: torch.Tensor, correct: torch.Tensor, weights, *, log2
     out.setdefault("model_correct", torch.empty(K, dtype=torch.int64, device=dev))
     if want_reach:
         out.setdefault("reach", torch.empty(S, K, dtype=torch.int64, device=dev))
-    need = lib().hs_threshold_replay_workspace(K, N)
+    need = lib().hs_threshold_replay_workspace(K, N, int(log2_bins))
     if ws is None or ws.numel() < need:
         ws = torch.empty(need, dtype=torch.uint8, device=dev)
     w = (ctypes.c_int64 * K)(*[int(x) for x in weights])

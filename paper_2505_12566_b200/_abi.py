@@ -51,7 +51,7 @@ SIGNATURES = {
                                  P, P, P, P, P, SZ, P, P]),
     "hs_grid_size": (I64, [I32, I32]),
     "hs_grid_vector": (I32, [I64, I32, I32, P]),
-    "hs_threshold_replay_workspace": (SZ, [I32, I64]),
+    "hs_threshold_replay_workspace": (SZ, [I32, I64, I32]),
     "hs_threshold_replay": (I32, [P, P, I32, I64, I32, P, I64, P, P, P, P, P, P, SZ, P]),
     "hs_perf_graph_workspace": (SZ, [I64]),
     "hs_perf_graph": (I32, [P, P, I64, I64, I64, I64, P, I32, P, P, P, P, P, P, SZ, P, P]),

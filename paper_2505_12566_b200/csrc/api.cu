@@ -328,8 +328,9 @@ hs_status_t hs_grid_vector(int64_t s, int32_t K, int32_t log2_bins, int32_t* b) 
   return HS_OK;
 }
 
-size_t hs_threshold_replay_workspace(int32_t K, int64_t N) {
-  return hs::replay_ws_bytes(K < 2 ? 2 : K, N < 0 ? 0 : N);
+size_t hs_threshold_replay_workspace(int32_t K, int64_t N, int32_t log2_bins) {
+  if (K < 2 || K > hs::kReplayMaxK || log2_bins < 1 || log2_bins > 14) return 0;
+  return hs::replay_ws_bytes(K, N < 0 ? 0 : N, log2_bins);
 }
 
 hs_status_t hs_threshold_replay(const float* conf, const uint8_t* correct, int32_t K, int64_t N,
@@ -355,7 +356,7 @@ hs_status_t hs_threshold_replay(const float* conf, const uint8_t* correct, int32
     cum += add;
     a.w.cum[k] = cum;
   }
-  const size_t need = hs::replay_ws_bytes(K, N);
+  const size_t need = hs::replay_ws_bytes(K, N, log2_bins);
   if (ws_bytes < need || !ws) return fail(HS_ERR_WORKSPACE_TOO_SMALL, "workspace %zu < %zu", ws_bytes, need);
   a.K = K;
   a.N = N;

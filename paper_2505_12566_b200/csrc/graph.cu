@@ -18,12 +18,23 @@
 //     per sample: K-1 compares -> answering stage (predicated select chain),
 //     correct += bit, energy += cumulative weight of the stage (smem table).
 //     ALU-bound: ~15 issue slots per (vector, sample).
+// K9b' replay_hist_kernel / replay_finish_kernel (the exhaustive grid, B+2 <= 48):
+//     vectors sharing the prefix (b_0..b_{K-3}) see the same requests reach
+//     model K-2, so per prefix ONE walk over the samples builds a histogram of
+//     bin_{K-2} (count, correct_{K-2}, correct_{K-1} packed in a u64, private
+//     per thread in shared memory, [bin][thread] so lanes never conflict) plus
+//     the correct / energy of the requests answered earlier; the B+2 vectors
+//     of the prefix then follow from prefix sums over the histogram (the
+//     "joint-histogram prefix table" of SURVEY 8(f) NEXT-4).  (B+2)x fewer
+//     sample visits than the direct replay; samples split over CTAs, partial
+//     histograms summed with integer atomics (exact).
 // K9c graph_*: per correct count c the least energy (64-bit atomicMin) and the
 //     lowest vector index achieving it; one CTA then sweeps c downwards
 //     (suffix minimum), compacts the Pareto points in ascending c and picks
 //     AP (first point with c >= tau) and EO (largest second divided difference
 //     of e(c) among interior points with c >= floor, ties to the lowest e).
 #include <climits>
+#include <cstdlib>
 
 #include "hs_common.cuh"
 #include "hs_internal.h"
@@ -35,6 +46,7 @@ namespace {
 constexpr int kReplayThreads = 256;
 // samples per shared-memory tile: (K-1) bins + one bit word per sample, <= 40 KB
 __host__ __device__ constexpr int replay_tile(int km1) { return km1 <= 4 ? 2048 : 1024; }
+__host__ __device__ constexpr int hist_tile(int) { return 1024; }
 constexpr int kFrontThreads = 1024;
 
 __device__ __forceinline__ int32_t bin_of(float c, int q) {
@@ -173,6 +185,197 @@ __global__ void __launch_bounds__(kReplayThreads) replay_kernel(
       for (int k = 1; k < K; ++k) out_reach[s * K + k] = (int64_t)reach[k];
     }
   }
+}
+
+// ---- K9b': prefix histograms for the exhaustive grid -------------------------
+constexpr int kHistThreads = 256;
+constexpr int kHistMaxR = 48;                  // B + 2 <= 48: q <= 5
+constexpr int kPackBits = 21;                  // N < 2^21 per (prefix, bin) counter field
+
+// hist[p][v] (v = bin_{K-2} + 1 in 0..R-1) packed count | correct_{K-2} << 21 |
+// correct_{K-1} << 42; pre[p] = {correct, energy} of the requests answered by
+// models 0..K-3; preach[p][k-1] = requests reaching model k (1 <= k <= K-2)
+template <int KM1>
+__global__ void __launch_bounds__(kHistThreads) replay_hist_kernel(
+    const int32_t* __restrict__ bins, const uint32_t* __restrict__ bits, int64_t N, int64_t Np, int q,
+    int64_t P, int64_t chunk, const __grid_constant__ ReplayWeights cw,
+    unsigned long long* hist, unsigned long long* pre, unsigned long long* preach) {
+  pdl_start();
+  constexpr int KP = KM1 - 1;                               // compares before the last threshold
+  constexpr int kTile = hist_tile(KM1);
+  extern __shared__ __align__(16) unsigned char smraw[];
+  int32_t* sb = reinterpret_cast<int32_t*>(smraw);           // [KM1][kTile]
+  uint32_t* sk = reinterpret_cast<uint32_t*>(sb + (size_t)KM1 * kTile);
+  unsigned long long* sh = reinterpret_cast<unsigned long long*>(sk + kTile);   // [R][kHistThreads]
+  const int R = (1 << q) + 2;
+  const int tid = threadIdx.x;
+  const int64_t p = (int64_t)blockIdx.x * kHistThreads + tid;
+  const bool valid = p < P;
+  int32_t t[KP > 0 ? KP : 1];
+  {
+    int64_t rem = valid ? p : 0;
+#pragma unroll
+    for (int k = KP - 1; k >= 0; --k) {
+      t[k] = (int32_t)(rem % R);
+      rem /= R;
+    }
+  }
+  for (int v = 0; v < R; ++v) sh[(size_t)v * kHistThreads + tid] = 0ull;
+  unsigned long long a = 0ull;
+  uint32_t reach[KP > 0 ? KP : 1];
+#pragma unroll
+  for (int k = 0; k < (KP > 0 ? KP : 1); ++k) reach[k] = 0;
+  const int64_t s0 = (int64_t)blockIdx.y * chunk, s1 = min(N, s0 + chunk);
+  for (int64_t r0 = s0; r0 < s1; r0 += kTile) {
+    const int m = (int)min((int64_t)kTile, (s1 - r0 + 3) & ~(int64_t)3);
+    __syncthreads();
+    for (int i = tid * 4; i < m; i += kHistThreads * 4) {
+#pragma unroll
+      for (int k = 0; k < KM1; ++k)
+        *reinterpret_cast<int4*>(&sb[(size_t)k * kTile + i]) =
+            __ldg(reinterpret_cast<const int4*>(bins + (int64_t)k * Np + r0 + i));
+      *reinterpret_cast<uint4*>(&sk[i]) = __ldg(reinterpret_cast<const uint4*>(bits + r0 + i));
+    }
+    __syncthreads();
+    const int mr = (int)min((int64_t)m, s1 - r0);
+    // one request: answering model among 0..K-3 (st < KP) or alive at K-2 (st == KP);
+    // a counts correct_st for every request (the alive ones' correct_{K-2} total is
+    // the histogram's, subtracted in the finish kernel), reach[k] = #(st > k)
+    auto visit = [&](const int32_t (&bk)[KM1], uint32_t kb) {
+      int st = KP;
+#pragma unroll
+      for (int k = KP - 1; k >= 0; --k)
+        if (bk[k] >= t[k]) st = k;
+      a += (kb >> st) & 1u;
+#pragma unroll
+      for (int k = 0; k < KP; ++k) reach[k] += st > k ? 1u : 0u;
+      if (st == KP) {
+        unsigned long long* h = sh + (size_t)(bk[KP] + 1) * kHistThreads + tid;   // bin + 1: 0 = NaN
+        *h += 1ull | ((unsigned long long)((kb >> KP) & 1u) << kPackBits) |
+              ((unsigned long long)((kb >> KM1) & 1u) << (2 * kPackBits));
+      }
+    };
+    int i = 0;
+    for (; i + 4 <= mr; i += 4) {
+      int4 b4[KM1];
+#pragma unroll
+      for (int k = 0; k < KM1; ++k) b4[k] = *reinterpret_cast<const int4*>(&sb[(size_t)k * kTile + i]);
+      const uint4 k4 = *reinterpret_cast<const uint4*>(&sk[i]);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        int32_t bk[KM1];
+#pragma unroll
+        for (int k = 0; k < KM1; ++k) bk[k] = j == 0 ? b4[k].x : j == 1 ? b4[k].y : j == 2 ? b4[k].z : b4[k].w;
+        visit(bk, j == 0 ? k4.x : j == 1 ? k4.y : j == 2 ? k4.z : k4.w);
+      }
+    }
+    for (; i < mr; ++i) {
+      int32_t bk[KM1];
+#pragma unroll
+      for (int k = 0; k < KM1; ++k) bk[k] = sb[(size_t)k * kTile + i];
+      visit(bk, sk[i]);
+    }
+  }
+  if (!valid) return;
+  for (int v = 0; v < R; ++v) {
+    const unsigned long long h = sh[(size_t)v * kHistThreads + tid];
+    if (h) atomicAdd(hist + p * R + v, h);
+  }
+  if (a) atomicAdd(pre + 2 * p, a);
+#pragma unroll
+  for (int k = 0; k < KP; ++k)
+    if (reach[k]) atomicAdd(preach + p * (KP > 0 ? KP : 1) + k, (unsigned long long)reach[k]);
+}
+
+// one thread per prefix: the R vectors (prefix, b) from prefix sums over its histogram
+template <int KM1>
+__global__ void __launch_bounds__(256) replay_finish_kernel(
+    const unsigned long long* __restrict__ hist, const unsigned long long* __restrict__ pre,
+    const unsigned long long* __restrict__ preach, int64_t N, int q, int64_t P,
+    const __grid_constant__ ReplayWeights cw, int64_t* out_c, int64_t* out_e, int64_t* out_reach) {
+  pdl_start();
+  constexpr int KP = KM1 - 1;
+  constexpr int K = KM1 + 1;
+  const int R = (1 << q) + 2;
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= P) return;
+  const unsigned long long mask = (1ull << kPackBits) - 1ull;
+  unsigned long long tn = 0, ta = 0, tz = 0;
+  for (int v = 0; v < R; ++v) {
+    const unsigned long long h = hist[p * R + v];
+    tn += h & mask;
+    ta += (h >> kPackBits) & mask;
+    tz += h >> (2 * kPackBits);
+  }
+  // requests answered by models 0..K-3: correct = a_all - (correct_{K-2} of the alive ones);
+  // energy = sum_{k<K-2} w_k * (reach_k - alive), reach_0 = N
+  const unsigned long long A = pre[2 * p] - ta;
+  unsigned long long E = 0ull;
+#pragma unroll
+  for (int k = 0; k < KP; ++k) {
+    const unsigned long long rk = k == 0 ? (unsigned long long)N : preach[p * (KP > 0 ? KP : 1) + k - 1];
+    E += (cw.cum[k] - (k ? cw.cum[k - 1] : 0ull)) * (rk - tn);
+  }
+  const unsigned long long wa = cw.cum[KP], wz = cw.cum[KM1];
+  unsigned long long dn = 0, da = 0, dz = 0;               // bins < b: deferred to the last model
+  for (int b = 0; b < R; ++b) {
+    const unsigned long long h = hist[p * R + b];           // v = b  <=>  bin = b - 1 < b
+    dn += h & mask;
+    da += (h >> kPackBits) & mask;
+    dz += h >> (2 * kPackBits);
+    const int64_t s = p * R + b;
+    out_c[s] = (int64_t)(A + (ta - da) + dz);
+    out_e[s] = (int64_t)(E + (tn - dn) * wa + dn * wz);
+    if (out_reach) {
+      out_reach[s * K] = N;
+#pragma unroll
+      for (int k = 0; k < KP; ++k) out_reach[s * K + 1 + k] = (int64_t)preach[p * (KP > 0 ? KP : 1) + k];
+      out_reach[s * K + KM1] = (int64_t)dn;
+    }
+  }
+}
+
+__global__ void zero_u64_kernel(unsigned long long* p, int64_t n) {
+  pdl_start();
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = 0ull;
+}
+
+template <int KM1>
+cudaError_t launch_replay_hist_k(const ReplayArgs& a, unsigned long long* hws, cudaStream_t s) {
+  constexpr int KP = KM1 - 1;
+  const int R = (1 << a.q) + 2;
+  const int64_t P = a.S / R;
+  unsigned long long* hist = hws;
+  unsigned long long* pre = hist + (size_t)P * R;
+  unsigned long long* preach = pre + 2 * (size_t)P;
+  const int64_t nz = (int64_t)P * R + 2 * P + P * (KP > 0 ? KP : 1);
+  cudaError_t e = launch_pdl(zero_u64_kernel, dim3((unsigned)min((int64_t)num_sms() * 4, (nz + 255) / 256)),
+                             dim3(256), 0, s, hws, nz);
+  if (e != cudaSuccess) return e;
+  auto kern = replay_hist_kernel<KM1>;
+  const size_t smem = ((size_t)KM1 * hist_tile(KM1) + hist_tile(KM1)) * 4 +
+                      (size_t)R * kHistThreads * 8;
+  static bool attr[8] = {};
+  if (!attr[KM1]) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr[KM1] = true;
+  }
+  const int64_t pb = (P + kHistThreads - 1) / kHistThreads;
+  int per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kHistThreads, smem);
+  // split the samples so that the grid fills the GPU about twice (>= 1024 samples per CTA)
+  int64_t chunks = max((int64_t)1, (int64_t)num_sms() * max(per_sm, 1) * 2 / pb);
+  chunks = min(chunks, max((int64_t)1, a.N / 1024));
+  int64_t chunk = (a.N + chunks - 1) / chunks;
+  chunk = (chunk + 3) / 4 * 4;
+  chunks = (a.N + chunk - 1) / chunk;
+  e = launch_pdl(kern, dim3((unsigned)pb, (unsigned)chunks), dim3(kHistThreads), smem, s, a.bins, a.bits,
+                 a.N, a.Np, a.q, P, chunk, a.w, hist, pre, preach);
+  if (e != cudaSuccess) return e;
+  return launch_pdl(replay_finish_kernel<KM1>, dim3((unsigned)((P + 255) / 256)), dim3(256), 0, s,
+                    (const unsigned long long*)hist, (const unsigned long long*)pre,
+                    (const unsigned long long*)preach, a.N, a.q, P, a.w, a.out_c, a.out_e, a.reach);
 }
 
 // ---- K9c: frontier -------------------------------------------------------------
@@ -357,9 +560,23 @@ cudaError_t launch_replay_k(const ReplayArgs& a, cudaStream_t s) {
 
 }  // namespace
 
-size_t replay_ws_bytes(int K, int64_t N) {
+// the exhaustive grid goes through the prefix histograms when they fit
+static bool use_hist(int K, int q, int64_t N) {
+  static const bool direct = getenv("HS_REPLAY_DIRECT") && getenv("HS_REPLAY_DIRECT")[0] == '1';
+  return !direct && (1 << q) + 2 <= kHistMaxR && N < (int64_t(1) << kPackBits) && K >= 2;
+}
+static size_t hist_ws_bytes(int K, int q) {
+  const int64_t R = (1 << q) + 2;
+  int64_t P = 1;
+  for (int k = 0; k < K - 2; ++k) P *= R;
+  return (size_t)(P * R + 2 * P + P * (K > 2 ? K - 2 : 1)) * 8u;
+}
+
+size_t replay_ws_bytes(int K, int64_t N, int q) {
   const int64_t Np = (N + 3) / 4 * 4;
-  return (size_t)Np * (size_t)K * 4u + 256u;
+  size_t b = ((size_t)Np * (size_t)K * 4u + 255u) / 256u * 256u + 256u;
+  if (use_hist(K, q, N)) b += hist_ws_bytes(K, q);
+  return b;
 }
 
 cudaError_t launch_replay(ReplayArgs a, const float* conf, const uint8_t* correct,
@@ -377,6 +594,20 @@ cudaError_t launch_replay(ReplayArgs a, const float* conf, const uint8_t* correc
   e = launch_pdl(replay_prep_kernel, dim3(blocks), dim3(256), 0, s, conf, correct, a.K, a.N, a.Np,
                  a.q, a.bins, a.bits, model_correct);
   if (e != cudaSuccess || a.S == 0) return e;
+  if (!a.bvecs && use_hist(a.K, a.q, a.N)) {
+    unsigned long long* hws = reinterpret_cast<unsigned long long*>(
+        reinterpret_cast<char*>(ws) + ((size_t)a.Np * (size_t)a.K * 4u + 255u) / 256u * 256u + 256u);
+    switch (a.K - 1) {
+      case 1: return launch_replay_hist_k<1>(a, hws, s);
+      case 2: return launch_replay_hist_k<2>(a, hws, s);
+      case 3: return launch_replay_hist_k<3>(a, hws, s);
+      case 4: return launch_replay_hist_k<4>(a, hws, s);
+      case 5: return launch_replay_hist_k<5>(a, hws, s);
+      case 6: return launch_replay_hist_k<6>(a, hws, s);
+      case 7: return launch_replay_hist_k<7>(a, hws, s);
+      default: return cudaErrorInvalidValue;
+    }
+  }
   switch (a.K - 1) {
     case 1: return launch_replay_k<1>(a, s);
     case 2: return launch_replay_k<2>(a, s);

@@ -192,7 +192,7 @@ struct ReplayArgs {
   int64_t* out_e;           // [S] energies
   int64_t* reach;           // [S x K] or NULL
 };
-size_t replay_ws_bytes(int K, int64_t N);
+size_t replay_ws_bytes(int K, int64_t N, int q);
 cudaError_t launch_replay(ReplayArgs a, const float* conf, const uint8_t* correct,
                           unsigned long long* model_correct, void* ws, cudaStream_t s);
 size_t graph_ws_bytes(int64_t N);

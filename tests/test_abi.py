@@ -157,7 +157,7 @@ def test_grid_helpers_match_oracle(libhs):
 def test_replay_and_graph_argument_errors(libhs):
     lib = libhs.lib()
     w = (ctypes.c_int64 * 3)(1, 2, 3)
-    ws = lib.hs_threshold_replay_workspace(3, 100)
+    ws = lib.hs_threshold_replay_workspace(3, 100, 4)
     def rp(K=3, N=100, q=4, bv=None, S=None, wt=w, wsb=ws):
         S = lib.hs_grid_size(K, q) if S is None else S
         return lib.hs_threshold_replay(256, 512, K, N, q, bv, S, wt, 1024, 2048, None, None, 4096, wsb, None)

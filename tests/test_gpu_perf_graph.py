@@ -81,7 +81,7 @@ def _case(rng, K, N, nan=True):
 
 
 @pytest.mark.parametrize("K,q,N", [(2, 4, 1), (2, 6, 2049), (3, 3, 4097), (4, 2, 1000), (5, 2, 3001),
-                                   (6, 1, 777), (8, 1, 300)])
+                                   (6, 1, 777), (8, 1, 300), (3, 5, 9001), (4, 4, 2500)])
 def test_whole_grid_vs_oracle(hs, K, q, N):
     rng = np.random.default_rng(100 + K * 10 + q)
     conf, ok, w = _case(rng, K, N)
@@ -126,6 +126,11 @@ def test_c2_validation_exhaustive_grid_sampled(hs):
     bv = np.array([oracle.grid_vector(int(s), fam.K, q) for s in idx], np.int32)
     c, e, _ = oracle.replay(conf, ok, q, w, bvecs=bv)
     check(g, c, e, None, int(ok[-1].sum()), int(ok[-2].sum()), idx=idx)
+    # the prefix-histogram path (whole grid) equals the direct replay of the same
+    # vectors passed explicitly (two independent GPU paths)
+    allv = np.array([oracle.grid_vector(int(s), fam.K, q) for s in range(S)], np.int32)
+    gd = gpu_graph(hs, conf, ok, q, w, bvecs=allv, reach=False)
+    assert np.array_equal(gd["correct"], g["correct"]) and np.array_equal(gd["energy"], g["energy"])
     # the exhaustive AP optimum never costs more than the greedy calibration (D5)
     cal = oracle.calibrate(conf, ok, q)
     cg, eg, _ = oracle.replay(conf, ok, q, w, bvecs=cal["b"][None, :])
