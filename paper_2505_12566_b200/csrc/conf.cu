@@ -1137,6 +1137,126 @@ __global__ void __launch_bounds__(NT) conf_cta_kernel(const ConfArgs a) {
 }
 
 // ---------------------------------------------------------------------------
+// K1d: one WARP per vocabulary-sized row (persistent over rows), the same
+// per-lane online (max, sum, weighted sum) over chunks of 32 x NV vectors as
+// K1b, the next (row, chunk) item in flight; the row merge is a warp merge
+// (shuffles), so no CTA barrier ever stalls the other rows' streams (K1b's top
+// stall on T5 rows: barrier 1.5 warps per issue).
+// ---------------------------------------------------------------------------
+template <bool BF16, bool ENTROPY, int NV>
+__global__ void __launch_bounds__(256, 2) conf_stream_kernel(const ConfArgs a) {
+  pdl_start();
+  constexpr int VE = BF16 ? 8 : 4;
+  constexpr int CH = 32 * NV;                  // vectors per chunk
+  const int lane = threadIdx.x & 31;
+  const int64_t rows = live_rows(a);
+  const int nvec = a.nvec;
+  const int nch = (nvec + CH - 1) / CH;
+  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  int64_t rowA = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (rowA >= rows) return;
+  int chA = 0;
+  RowSrc rsA = locate(a, rowA), rsB = rsA;
+  const uint4* pB = reinterpret_cast<const uint4*>(rsA.base + rsA.src * a.row_bytes);
+  uint4 A[NV], B[NV];
+  cta_load_chunk<BF16, NV, 32>(A, pB, 0, lane, nvec, a.tail, CH <= nvec);
+  int32_t labA = (a.labels && lane == 0) ? __ldg(a.labels + rsA.src) : 0, labB = 0;
+
+  float m = -INFINITY;
+  int mch = -1;                                // chunk where the lane's running max was set
+  f2_t s2 = f2(0.f, 0.f), w2 = f2(0.f, 0.f);
+  while (true) {
+    int64_t rowB = rowA;
+    int chB = chA + 1;
+    if (chB == nch) {
+      chB = 0;
+      rowB = rowA + nwarps;
+    }
+    const bool more = rowB < rows;
+    if (more) {
+      if (chB == 0) {
+        rsB = locate(a, rowB);
+        pB = reinterpret_cast<const uint4*>(rsB.base + rsB.src * a.row_bytes);
+        if (a.labels && lane == 0) labB = __ldg(a.labels + rsB.src);
+      }
+      cta_load_chunk<BF16, NV, 32>(B, pB, chB * CH, lane, nvec, a.tail, (chB + 1) * CH <= nvec);
+    }
+    const float c = rsA.c;
+    const f2_t c2 = f2(c, c);
+    float cm = -INFINITY;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) cm = fmax_nan(cm, vec_max<BF16>(A[k]));
+    if (!(cm <= m)) {
+      const float nm = fmax_nan(m, cm);
+      if (m > -INFINITY) {
+        const float d = (m - nm) * c;
+        const float f = ex2(d);
+        const f2_t f2v = f2(f, f);
+        if (ENTROPY) w2 = f2mul(f2v, f2fma(f2(d, d), s2, w2));
+        s2 = f2mul(f2v, s2);
+      }
+      m = nm;
+      mch = chA;
+    }
+    if (m > -INFINITY) {
+      // the chunk's terms are summed apart and then added to the row's running
+      // sums: each lane adds ~4,000 terms on a Llama row, a single running fp32
+      // sum would exceed the 1e-5 tolerance
+      const f2_t m2 = f2(m, m);
+      const uint32_t cw = ENTROPY && BF16 ? entropy_clamp_word(m, c) : 0u;
+      f2_t cs = f2(0.f, 0.f), cwv = f2(0.f, 0.f);
+#pragma unroll
+      for (int k = 0; k < NV; ++k) vec_accum<BF16, ENTROPY>(A[k], m2, c2, cw, cs, cwv);
+      s2 = f2add(s2, cs);
+      if (ENTROPY) w2 = f2add(w2, cwv);
+    }
+    if (chA == nch - 1) {
+      // ---- warp merge: max, rescale to it, fixed-order sums, min index among maxima
+      float M = m;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) M = fmax_nan(M, __shfl_xor_sync(0xFFFFFFFFu, M, o));
+      float sv = 0.f, wv = 0.f;
+      if (m > -INFINITY) {
+        const float d = (m - M) * c;
+        const float f = ex2(d);
+        const float ls = f2lo(s2) + f2hi(s2);
+        sv = f * ls;
+        if (ENTROPY && f > 0.f) wv = f * ((f2lo(w2) + f2hi(w2)) + d * ls);
+      }
+      sv = warp_sum(sv);
+      if (ENTROPY) wv = warp_sum(wv);
+      unsigned mine = 0xFFFFFFFFu;
+      if (m == M && mch >= 0) {      // re-read the lane's vectors of the chunk that set its max (L2-hot)
+        uint4 R[NV];
+        const uint4* pr = reinterpret_cast<const uint4*>(rsA.base + rsA.src * a.row_bytes);
+        cta_load_chunk<BF16, NV, 32>(R, pr, mch * CH, lane, nvec, a.tail, (mch + 1) * CH <= nvec);
+#pragma unroll
+        for (int k = NV - 1; k >= 0; --k) {
+          const int e = vec_first_eq<BF16>(R[k], M);
+          if (e < VE) mine = (unsigned)((mch * CH + k * 32 + lane) * VE + e);
+        }
+      }
+      const unsigned am = __reduce_min_sync(0xFFFFFFFFu, mine);
+      if (lane == 0) {
+        RowOut r{M, sv, wv, am, 1.0f};
+        write_row(a, rowA, labA, r);
+      }
+      m = -INFINITY;
+      mch = -1;
+      s2 = f2(0.f, 0.f);
+      w2 = f2(0.f, 0.f);
+      labA = labB;
+    }
+    if (!more) break;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) A[k] = B[k];
+    rowA = rowB;
+    chA = chB;
+    rsA = rsB;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // K2: token -> sequence reduce, fixed order (P:423 MIN; MEAN), all-L correctness.
 // ---------------------------------------------------------------------------
 __global__ void seq_reduce_kernel(const float* tok_conf, const uint8_t* tok_ok, int64_t n,
@@ -1238,6 +1358,16 @@ cudaError_t launch_cta(const ConfArgs& a, int64_t rows, cudaStream_t s) {
   return launch_pdl(k, dim3(grid), dim3(NT), 0, s, a);
 }
 
+template <bool BF16, bool ENTROPY>
+cudaError_t launch_stream(const ConfArgs& a, int64_t rows, cudaStream_t s) {
+  auto k = conf_stream_kernel<BF16, ENTROPY, 8>;
+  static const int occ = occupancy(k, 256);
+  const int64_t want = (rows + 7) / 8;
+  const int64_t cap = (int64_t)num_sms() * occ;
+  const int grid = (int)(want < cap ? (want > 0 ? want : 1) : cap);
+  return launch_pdl(k, dim3(grid), dim3(256), 0, s, a);
+}
+
 template <bool BF16, bool ENTROPY, int NV, int G, int NCW, int S, bool L1>
 cudaError_t launch_tma_l(const ConfArgs& a, int64_t rows, cudaStream_t s) {
   auto k = conf_tma_kernel<BF16, ENTROPY, NV, G, NCW, S, L1>;
@@ -1270,6 +1400,7 @@ int conf_impl() {
     const char* e = getenv("HS_CONF_IMPL");
     if (e && strcmp(e, "tma") == 0) return 1;
     if (e && strcmp(e, "ldg") == 0) return 0;
+    if (e && strcmp(e, "cta") == 0) return 3;     // vocabulary rows: K1b instead of K1d
     return 2;
   }();
   return v;
@@ -1294,15 +1425,16 @@ cudaError_t dispatch(const ConfArgs& a, int64_t rows, cudaStream_t s) {
   if (nvec <= 128) return launch_warp<BF16, ENTROPY, 8, 16>(a, rows, s);
   if (nvec <= 256) return launch_warp<BF16, ENTROPY, 16, 16>(a, rows, s);
   if (nvec <= 512) return launch_warp<BF16, ENTROPY, 16, 32>(a, rows, s);
-  // 256-thread CTAs, two per SM: one streams while the other merges a row
-  return launch_cta<BF16, ENTROPY, 256>(a, rows, s);
+  // vocabulary rows: a warp per row (K1d), or (HS_CONF_IMPL=cta) K1b's CTA per row
+  if (conf_impl() == 3) return launch_cta<BF16, ENTROPY, 256>(a, rows, s);
+  return launch_stream<BF16, ENTROPY>(a, rows, s);
 }
 
 }  // namespace
 
 const char* confidence_path(int64_t nvec) {
   if (nvec <= 512) return "warp-per-row";
-  return "cta-per-row";
+  return conf_impl() == 3 ? "cta-per-row" : "warp-per-row-stream";
 }
 
 template <bool BF16, bool ENTROPY>
