@@ -11,6 +11,7 @@ VARIANTS = {
     "noargmax": ["HS_EXP_NOARGMAX"],     # upper bounds: K1 without the argmax ...
     "noexp": ["HS_EXP_NOEXP"],           # ... or without the exponential pass
     "tf768": ["HS_TF_THREADS=768"],      # temperature fit: 24 warps/SM, 85 registers
+    "tf1024": ["HS_TF_THREADS=1024"],    # temperature fit: 32 warps/SM, 64 registers
 }
 
 if __name__ == "__main__":

@@ -1,0 +1,3 @@
+timeout 900 python -m pytest tests/test_gpu_temperature.py -x -q 2>&1 | tail -3 > gpurun_out/pytest62.txt
+timeout 600 python bench.py --config c2t --steps 30 --no-cpu-baseline --e2e-steps 0 2>/dev/null | tail -1 > gpurun_out/bench62_c2t.json
+git stash -q 2>/dev/null; true
