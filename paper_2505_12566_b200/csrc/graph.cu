@@ -48,6 +48,8 @@ constexpr int kReplayThreads = 256;
 __host__ __device__ constexpr int replay_tile(int km1) { return km1 <= 4 ? 2048 : 1024; }
 __host__ __device__ constexpr int hist_tile(int) { return 1024; }
 constexpr int kFrontThreads = 1024;
+constexpr int kFrontTE = 4;                               // counts per thread per tile
+constexpr int kFrontTile = kFrontThreads * kFrontTE;
 
 __device__ __forceinline__ int32_t bin_of(float c, int q) {
   if (c != c) return -1;                                  // NaN: never accepted (G20)
@@ -452,58 +454,80 @@ __global__ void __launch_bounds__(kFrontThreads) graph_front_kernel(
   __shared__ long long s_ap, s_n;
   const int tid = threadIdx.x;
   const int T = kFrontThreads;
-  const int64_t chunk = (n1 + T - 1) / T;
-  const int64_t lo = min(n1, (int64_t)tid * chunk), hi = min(n1, lo + chunk);
   if (tau < 0) tau = model_correct ? (int64_t)model_correct[K - 1] : 0;
   if (floor_ < 0) floor_ = model_correct ? (int64_t)model_correct[K - 2] : 0;
-  // 1. suffix minimum from above: scan in reversed thread order
-  unsigned long long cm = ~0ull;
-  for (int64_t c = lo; c < hi; ++c) cm = min(cm, minE[c]);
-  // chunk minima, then a suffix minimum over them (Hillis-Steele, 10 steps)
+  // Tiles of kFrontTile counts from the top down (coalesced loads into shared
+  // memory; thread t owns kFrontTE consecutive counts of the tile).  Kept(c) <=>
+  // minE[c] < min over every larger count; kept points are written in
+  // DESCENDING c first (their positions are known from the top), then reversed.
+  __shared__ unsigned long long tv[kFrontTile];
   __shared__ unsigned long long cmin[kFrontThreads];
-  cmin[tid] = cm;
-  __syncthreads();
-  for (int o = 1; o < T; o <<= 1) {
-    const unsigned long long v = (tid + o < T) ? cmin[tid + o] : ~0ull;
+  unsigned long long carry = ~0ull;                         // min over the tiles above
+  long long J = 0;
+  for (int64_t t0 = ((n1 - 1) / kFrontTile) * kFrontTile; n1 > 0 && t0 >= 0; t0 -= kFrontTile) {
+    for (int i = tid; i < kFrontTile; i += T) tv[i] = (t0 + i < n1) ? minE[t0 + i] : ~0ull;
     __syncthreads();
-    cmin[tid] = min(cmin[tid], v);
+    unsigned long long cm = ~0ull;
+#pragma unroll
+    for (int j = 0; j < kFrontTE; ++j) cm = min(cm, tv[tid * kFrontTE + j]);
+    cmin[tid] = cm;
     __syncthreads();
-  }
-  unsigned long long above = (tid + 1 < T) ? cmin[tid + 1] : ~0ull;
-  __syncthreads();
-  // 2. count kept points of this chunk (descending c)
-  long long kept = 0;
-  {
-    unsigned long long run = above;
-    for (int64_t c = hi - 1; c >= lo; --c) {
-      const unsigned long long v = minE[c];
-      if (v < run) {
-        ++kept;
-        run = v;
+    for (int o = 1; o < T; o <<= 1) {                       // suffix minimum over the threads
+      const unsigned long long v = (tid + o < T) ? cmin[tid + o] : ~0ull;
+      __syncthreads();
+      cmin[tid] = min(cmin[tid], v);
+      __syncthreads();
+    }
+    const unsigned long long above = min(carry, (tid + 1 < T) ? cmin[tid + 1] : ~0ull);
+    unsigned kmask = 0;
+    long long kept = 0;
+    {
+      unsigned long long run = above;
+#pragma unroll
+      for (int j = kFrontTE - 1; j >= 0; --j) {
+        const unsigned long long v = tv[tid * kFrontTE + j];
+        if (v < run) {
+          kmask |= 1u << j;
+          ++kept;
+          run = v;
+        }
       }
     }
-  }
-  const long long incl = block_scan_incl<long long>(kept, shl, AddOp());
-  const long long start = incl - kept;                      // ascending-c position of the chunk
-  if (tid == T - 1) s_n = incl;
-  // 3. write the chunk's kept points in ascending c
-  {
-    unsigned long long run = above;
-    long long pos = start + kept - 1;
-    for (int64_t c = hi - 1; c >= lo; --c) {
-      const unsigned long long v = minE[c];
-      if (v < run) {
+    const long long incl = block_scan_incl<long long>(kept, shl, AddOp());
+    if (tid == T - 1) s_n = incl;                           // kept in this tile
+    __syncthreads();
+    const long long tile_kept = s_n;
+    long long pos = J + (tile_kept - incl);                 // kept points of higher threads come first
+#pragma unroll
+    for (int j = kFrontTE - 1; j >= 0; --j) {
+      if (kmask & (1u << j)) {
+        const int64_t c = t0 + tid * kFrontTE + j;
         front_c[pos] = c;
-        front_e[pos] = (int64_t)v;
+        front_e[pos] = (int64_t)tv[tid * kFrontTE + j];
         front_s[pos] = (int64_t)minS[c];
-        --pos;
-        run = v;
+        ++pos;
       }
     }
+    J += tile_kept;
+    carry = min(carry, cmin[0]);
+    __syncthreads();
   }
-  if (tid == 0) s_ap = -1;
+  // ascending c: reverse the J points in place (disjoint pairs)
+  for (long long i = tid; i < J / 2; i += T) {
+    const long long k = J - 1 - i;
+    const int64_t c0 = front_c[i], e0 = front_e[i], s0 = front_s[i];
+    front_c[i] = front_c[k];
+    front_e[i] = front_e[k];
+    front_s[i] = front_s[k];
+    front_c[k] = c0;
+    front_e[k] = e0;
+    front_s[k] = s0;
+  }
+  if (tid == 0) {
+    s_ap = -1;
+    s_n = J;
+  }
   __syncthreads();
-  const long long J = s_n;
   // 4. AP: the first frontier point with c >= tau
   for (long long j = tid; j < J; j += T) {
     if (front_c[j] >= tau && (j == 0 || front_c[j - 1] < tau)) s_ap = front_s[j];
