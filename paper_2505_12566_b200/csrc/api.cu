@@ -526,7 +526,7 @@ hs_status_t hs_skip_route(const float* conf, int64_t n, const int64_t* d_n, floa
 
 // cascade-step workspace: [compact ws][conf f32 n][argmax i32 n*L][def_pos i64 n][conf ws]
 static size_t step_layout(int64_t n, int32_t L, size_t* o_conf, size_t* o_am, size_t* o_pos,
-                          size_t* o_cws, size_t* o_tick = nullptr) {
+                          size_t* o_cws, size_t* o_tick = nullptr, size_t* o_split = nullptr) {
   size_t off = align_up(hs::compact_ws_bytes(n), 256);
   if (o_tick) *o_tick = off;           // K1 row-group ticket + finished-CTA count
   off += 256;
@@ -538,6 +538,8 @@ static size_t step_layout(int64_t n, int32_t L, size_t* o_conf, size_t* o_am, si
   off = align_up(off + (size_t)n * sizeof(int64_t), 256);
   *o_cws = off;
   off = align_up(off + conf_ws(n, L), 256);
+  if (o_split) *o_split = off;         // K1e split-row partials (small batches), zero-filled once
+  off = align_up(off + hs::split_ws_bytes(n * (int64_t)L), 256);
   return off;
 }
 
@@ -587,8 +589,8 @@ hs_status_t hs_cascade_step_ex(int32_t stage, int32_t n_stages, const void* logi
   if (next_payload && (!payload || payload_row_bytes <= 0 || (payload_row_bytes & 15) ||
                        !aligned16(payload) || !aligned16(next_payload)))
     return fail(HS_ERR_INVALID_ARGUMENT, "payload rows must be 16-byte aligned multiples of 16 bytes");
-  size_t o_conf, o_am, o_pos, o_cws, o_tick;
-  const size_t need = step_layout(n, seq_len, &o_conf, &o_am, &o_pos, &o_cws, &o_tick);
+  size_t o_conf, o_am, o_pos, o_cws, o_tick, o_split;
+  const size_t need = step_layout(n, seq_len, &o_conf, &o_am, &o_pos, &o_cws, &o_tick, &o_split);
   if (!ws || ws_bytes < need) return fail(HS_ERR_WORKSPACE_TOO_SMALL, "workspace %zu < %zu", ws_bytes, need);
   cudaStream_t s = (cudaStream_t)stream;
   char* w = reinterpret_cast<char*>(ws);
@@ -603,6 +605,7 @@ hs_status_t hs_cascade_step_ex(int32_t stage, int32_t n_stages, const void* logi
     hs::ConfArgs a = make_conf_args(logits, dtype, n, seq_len, n_classes, row_stride, row_index, d_n,
                                     temperature, kind);
     a.top_k = top_k;
+    if (hs::split_ws_bytes(n * (int64_t)seq_len)) a.split_ws = w + o_split;
     if (flags & HS_STEP_OVERLAP_PREVIOUS) {
       // CTAs that start late (SMs held by the previous kernel) take fewer rows
       a.ticket = reinterpret_cast<unsigned int*>(w + o_tick);

@@ -1257,6 +1257,157 @@ __global__ void __launch_bounds__(256, 2) conf_stream_kernel(const ConfArgs a) {
 }
 
 // ---------------------------------------------------------------------------
+// K1e: split rows for small batches of long rows (routing latency, Fig. 8
+// P:1039-1040).  Row r is cut into S contiguous segments of whole chunks, one
+// warp each (K1d's per-lane online reduction); each warp publishes its
+// segment's (max, sum, weighted sum, first argmax) and the LAST warp of the row
+// to arrive (per-row arrival counter) merges the S partials in segment order
+// (fixed tree: deterministic) and writes the row; it re-arms the counter.
+// ---------------------------------------------------------------------------
+struct SplitPart {
+  float m, s, w;
+  uint32_t am;
+};
+
+// (m, s, w) relative to m (base-2 exponents scaled by c), folded into the running
+// (M, S, W, AM) -- the same rescale as K1b/K1d's row merge
+__device__ __forceinline__ void fold_part(float& M, float& S, float& W, uint32_t& AM, const SplitPart& q,
+                                          float c, bool ent) {
+  const float nm = fmax_nan(M, q.m);
+  float s0 = 0.f, w0 = 0.f, s1 = 0.f, w1 = 0.f;
+  if (M > -INFINITY && nm == nm) {
+    const float d = (M - nm) * c, f = ex2(d);
+    s0 = f * S;
+    if (ent && f > 0.f) w0 = f * (W + d * S);
+  }
+  if (q.m > -INFINITY && nm == nm) {
+    const float d = (q.m - nm) * c, f = ex2(d);
+    s1 = f * q.s;
+    if (ent && f > 0.f) w1 = f * (q.w + d * q.s);
+  }
+  AM = (M == nm ? AM : 0xFFFFFFFFu);
+  if (q.m == nm) AM = min(AM, q.am);
+  M = nm;
+  S = s0 + s1;
+  W = w0 + w1;
+}
+
+template <bool BF16, bool ENTROPY, int NV>
+__global__ void __launch_bounds__(256) conf_split_kernel(const ConfArgs a, int nseg, int segch,
+                                                         SplitPart* parts, unsigned* arrive) {
+  pdl_start();
+  constexpr int VE = BF16 ? 8 : 4;
+  constexpr int CH = 32 * NV;
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int64_t row = gw / nseg;
+  const int seg = (int)(gw - row * nseg);
+  if (row >= live_rows(a)) return;
+  const int nvec = a.nvec;
+  const int nch = (nvec + CH - 1) / CH;
+  const int c0 = seg * segch, c1 = min(nch, c0 + segch);
+  const RowSrc rs = locate(a, row);
+  const uint4* p = reinterpret_cast<const uint4*>(rs.base + rs.src * a.row_bytes);
+  const float c = rs.c;
+  const f2_t c2 = f2(c, c);
+  float m = -INFINITY;
+  int mch = -1;
+  f2_t s2 = f2(0.f, 0.f), w2 = f2(0.f, 0.f);
+  uint4 A[NV], B[NV];
+  cta_load_chunk<BF16, NV, 32>(A, p, c0 * CH, lane, nvec, a.tail, (c0 + 1) * CH <= nvec);
+  for (int ch = c0; ch < c1; ++ch) {
+    const bool more = ch + 1 < c1;
+    if (more) cta_load_chunk<BF16, NV, 32>(B, p, (ch + 1) * CH, lane, nvec, a.tail, (ch + 2) * CH <= nvec);
+    float cm = -INFINITY;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) cm = fmax_nan(cm, vec_max<BF16>(A[k]));
+    if (!(cm <= m)) {
+      const float nm = fmax_nan(m, cm);
+      if (m > -INFINITY) {
+        const float d = (m - nm) * c;
+        const float f = ex2(d);
+        const f2_t f2v = f2(f, f);
+        if (ENTROPY) w2 = f2mul(f2v, f2fma(f2(d, d), s2, w2));
+        s2 = f2mul(f2v, s2);
+      }
+      m = nm;
+      mch = ch;
+    }
+    if (m > -INFINITY) {
+      const f2_t m2 = f2(m, m);
+      const uint32_t cw = ENTROPY && BF16 ? entropy_clamp_word(m, c) : 0u;
+      f2_t cs = f2(0.f, 0.f), cwv = f2(0.f, 0.f);
+#pragma unroll
+      for (int k = 0; k < NV; ++k) vec_accum<BF16, ENTROPY>(A[k], m2, c2, cw, cs, cwv);
+      s2 = f2add(s2, cs);
+      if (ENTROPY) w2 = f2add(w2, cwv);
+    }
+    if (more) {
+#pragma unroll
+      for (int k = 0; k < NV; ++k) A[k] = B[k];
+    }
+  }
+  // ---- the segment's partial: warp merge (as K1d's row merge)
+  float M = m;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) M = fmax_nan(M, __shfl_xor_sync(0xFFFFFFFFu, M, o));
+  float sv = 0.f, wv = 0.f;
+  if (m > -INFINITY) {
+    const float d = (m - M) * c;
+    const float f = ex2(d);
+    const float ls = f2lo(s2) + f2hi(s2);
+    sv = f * ls;
+    if (ENTROPY && f > 0.f) wv = f * ((f2lo(w2) + f2hi(w2)) + d * ls);
+  }
+  sv = warp_sum(sv);
+  if (ENTROPY) wv = warp_sum(wv);
+  unsigned mine = 0xFFFFFFFFu;
+  if (m == M && mch >= 0) {
+    uint4 R[NV];
+    cta_load_chunk<BF16, NV, 32>(R, p, mch * CH, lane, nvec, a.tail, (mch + 1) * CH <= nvec);
+#pragma unroll
+    for (int k = NV - 1; k >= 0; --k) {
+      const int e = vec_first_eq<BF16>(R[k], M);
+      if (e < VE) mine = (unsigned)((mch * CH + k * 32 + lane) * VE + e);
+    }
+  }
+  const unsigned am = __reduce_min_sync(0xFFFFFFFFu, mine);
+  unsigned last = 0;
+  if (lane == 0) {
+    parts[row * nseg + seg] = SplitPart{M, sv, wv, am};
+    __threadfence();
+    last = atomicAdd(arrive + row, 1u) == (unsigned)(nseg - 1);
+  }
+  if (!__shfl_sync(0xFFFFFFFFu, last, 0)) return;
+  // ---- last arrival: merge the row's partials in segment order
+  __threadfence();
+  float RM = -INFINITY, RS = 0.f, RW = 0.f;
+  uint32_t RA = 0xFFFFFFFFu;
+  for (int j = lane; j < nseg; j += 32) {
+    const float4 q4 = __ldcg(reinterpret_cast<const float4*>(parts + row * nseg + j));
+    fold_part(RM, RS, RW, RA, SplitPart{q4.x, q4.y, q4.z, __float_as_uint(q4.w)}, c, ENTROPY);
+  }
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {        // fixed tree over the lanes
+    SplitPart q{__shfl_xor_sync(0xFFFFFFFFu, RM, o), __shfl_xor_sync(0xFFFFFFFFu, RS, o),
+                __shfl_xor_sync(0xFFFFFFFFu, RW, o), __shfl_xor_sync(0xFFFFFFFFu, RA, o)};
+    // both lanes of a pair must combine in the same order to stay identical
+    if (lane & o) {
+      const SplitPart mineq{RM, RS, RW, RA};
+      RM = q.m; RS = q.s; RW = q.w; RA = q.am;
+      fold_part(RM, RS, RW, RA, mineq, c, ENTROPY);
+    } else {
+      fold_part(RM, RS, RW, RA, q, c, ENTROPY);
+    }
+  }
+  if (lane == 0) {
+    RowOut r{RM, RS, RW, RA, 1.0f};
+    write_row(a, row, a.labels ? __ldg(a.labels + rs.src) : 0, r);
+    arrive[row] = 0u;                        // re-armed for the next launch (stream order)
+  }
+}
+
+// ---------------------------------------------------------------------------
 // K2: token -> sequence reduce, fixed order (P:423 MIN; MEAN), all-L correctness.
 // ---------------------------------------------------------------------------
 __global__ void seq_reduce_kernel(const float* tok_conf, const uint8_t* tok_ok, int64_t n,
@@ -1368,6 +1519,35 @@ cudaError_t launch_stream(const ConfArgs& a, int64_t rows, cudaStream_t s) {
   return launch_pdl(k, dim3(grid), dim3(256), 0, s, a);
 }
 
+// K1e when the batch is too small to fill the GPU with one warp per row
+template <bool BF16, bool ENTROPY>
+bool launch_split(const ConfArgs& a, int64_t rows, cudaStream_t s, cudaError_t* err) {
+  constexpr int NV = 8, CH = 32 * NV;
+  if (!a.split_ws || a.top_k || a.ticket || rows > kSplitMaxRows || rows < 1) return false;
+  static const bool off = getenv("HS_NO_SPLIT") && getenv("HS_NO_SPLIT")[0] == '1';
+  if (off) return false;
+  const int nch = (a.nvec + CH - 1) / CH;
+  const int64_t target = (int64_t)num_sms() * 16;          // K1d's resident warps
+  // measured (tools/fig8_sweep.py): splitting pays when every row gets >= 4
+  // segments and rows are >= 8 chunks (>= 32 KB); below that the extra merge
+  // costs more than the parallelism gains
+  if (rows * 4 > target || nch < 8) return false;
+  int64_t want = (target + rows - 1) / rows;
+  if (want > kSplitMaxSeg) want = kSplitMaxSeg;
+  if (want > nch) want = nch;
+  if (want < 2) return false;
+  const int segch = (int)((nch + want - 1) / want);
+  const int nseg = (nch + segch - 1) / segch;
+  if (nseg < 2) return false;
+  SplitPart* parts = reinterpret_cast<SplitPart*>(reinterpret_cast<char*>(a.split_ws) +
+                                                  (size_t)kSplitMaxRows * sizeof(unsigned));
+  unsigned* arrive = reinterpret_cast<unsigned*>(a.split_ws);
+  const int64_t warps = rows * nseg;
+  *err = launch_pdl(conf_split_kernel<BF16, ENTROPY, NV>, dim3((unsigned)((warps + 7) / 8)), dim3(256), 0,
+                    s, a, nseg, segch, parts, arrive);
+  return true;
+}
+
 template <bool BF16, bool ENTROPY, int NV, int G, int NCW, int S, bool L1>
 cudaError_t launch_tma_l(const ConfArgs& a, int64_t rows, cudaStream_t s) {
   auto k = conf_tma_kernel<BF16, ENTROPY, NV, G, NCW, S, L1>;
@@ -1425,12 +1605,20 @@ cudaError_t dispatch(const ConfArgs& a, int64_t rows, cudaStream_t s) {
   if (nvec <= 128) return launch_warp<BF16, ENTROPY, 8, 16>(a, rows, s);
   if (nvec <= 256) return launch_warp<BF16, ENTROPY, 16, 16>(a, rows, s);
   if (nvec <= 512) return launch_warp<BF16, ENTROPY, 16, 32>(a, rows, s);
-  // vocabulary rows: a warp per row (K1d), or (HS_CONF_IMPL=cta) K1b's CTA per row
+  // vocabulary rows: a warp per row (K1d), split rows for small batches (K1e),
+  // or (HS_CONF_IMPL=cta) K1b's CTA per row
   if (conf_impl() == 3) return launch_cta<BF16, ENTROPY, 256>(a, rows, s);
+  cudaError_t e = cudaSuccess;
+  if (launch_split<BF16, ENTROPY>(a, rows, s, &e)) return e;
   return launch_stream<BF16, ENTROPY>(a, rows, s);
 }
 
 }  // namespace
+
+size_t split_ws_bytes(int64_t rows) {
+  if (rows <= 0 || rows > kSplitMaxRows) return 0;
+  return (size_t)kSplitMaxRows * sizeof(unsigned) + (size_t)rows * kSplitMaxSeg * sizeof(SplitPart);
+}
 
 const char* confidence_path(int64_t nvec) {
   if (nvec <= 512) return "warp-per-row";

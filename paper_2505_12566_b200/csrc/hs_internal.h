@@ -70,7 +70,13 @@ struct ConfArgs {
   int late_wait;
   // NEXT-2: softmax restricted to the top_k largest logits (0 = full row)
   int top_k;
+  // K1e split rows (small batches of long rows): zero-filled-once workspace of
+  // split_ws_bytes(rows) bytes, or NULL (no split)
+  void* split_ws;
 };
+constexpr int kSplitMaxRows = 2048;     // the split path serves batches up to this many rows
+constexpr int kSplitMaxSeg = 64;        // segments per row
+size_t split_ws_bytes(int64_t rows);
 constexpr int kTopkMax = 32;
 cudaError_t launch_confidence(const ConfArgs& a, bool bf16, cudaStream_t s);
 cudaError_t launch_seq_reduce(const float* tok_conf, const uint8_t* tok_ok, int64_t n,
