@@ -375,6 +375,56 @@ hs_status_t hs_perf_graph(const int64_t* d_correct, const int64_t* d_energy, int
                           uint32_t* d_status, hs_stream_t stream);
 
 /* ------------------------------------------------------------------------ */
+/* Multi-GPU forwarding of deferred requests over peer memory.    */
+/* ------------------------------------------------------------------------ */
+/* After a stage every rank g (0 <= g < world <= 8) holds D_g deferred ids in
+ * increasing global order (next_ids of hs_cascade_step, count d_count).  The
+ * next stage's batch is the global rank-major list, split into contiguous
+ * blocks over the destination ranks dest_ranks[0..n_dest) (distinct): block d
+ * = global positions [floor(d*D/n_dest), floor((d+1)*D/n_dest)), D = sum_g D_g.
+ * Receiver dest_ranks[d] gets its block, in global order, at recv_ids[0..) (and
+ * payload rows at recv_payload) -- exactly dist.forward_deferred's result, but
+ * moved by the kernels through peer-mapped memory (CUDA IPC over NVLink /
+ * NVSwitch) with no host round trip and no NCCL:
+ *   hs_forward_publish: store {epoch, D_g} into slot g of every rank's count
+ *     array (peer_counts[h] = rank h's u64[world] array, mapped here).
+ *   hs_forward_scatter: wait until this rank's count array (my_counts) holds
+ *     every rank's count of this epoch, write each local deferred id (+ payload
+ *     row) into the receive buffer of its destination (peer_recv_ids[h],
+ *     peer_recv_payload[h] or NULL), write this rank's receive count to
+ *     *d_recv_count, then store {epoch} into slot g of every rank's done array
+ *     (peer_done[h]).
+ *   hs_forward_wait: wait until this rank's done array (my_done) holds the
+ *     epoch from every rank: the receive buffer is complete for later kernels.
+ * Rules: epoch > 0 and strictly increasing per forward on a group; count and
+ * done arrays zero-filled once; the receive buffers hold world * cap rows and
+ * alternate between two sets on consecutive stages (a rank may scatter stage
+ * k+1 while a peer still reads stage k's buffer); ws >= 256 bytes zero-filled
+ * once (completion counter, re-armed by the kernel).  Payload rows: multiples
+ * of 16 bytes, 16-byte aligned.  All calls stream-ordered, graph-capturable.
+ * hs_ipc_alloc / hs_ipc_free: the one explicit device allocation of the library
+ * (a whole cudaMalloc allocation, zero-filled synchronously, so that its IPC
+ * handle maps exactly this buffer on the peers).
+ * hs_ipc_handle / hs_ipc_open / hs_ipc_close wrap cudaIpcGetMemHandle /
+ * cudaIpcOpenMemHandle (lazy peer access) / cudaIpcCloseMemHandle: a 64-byte
+ * host handle per device buffer, exchanged by the caller (e.g. torch.distributed). */
+#define HS_FWD_MAX_WORLD 8
+hs_status_t hs_forward_publish(const int64_t* d_count, int64_t cap, int32_t rank, int32_t world,
+                               uint64_t* const* peer_counts, uint32_t epoch, hs_stream_t stream);
+hs_status_t hs_forward_scatter(const int64_t* ids, const void* payload, int64_t payload_row_bytes,
+                               int64_t cap, int32_t rank, int32_t world, const uint64_t* my_counts,
+                               uint64_t* const* peer_done, int64_t* const* peer_recv_ids,
+                               void* const* peer_recv_payload, const int32_t* dest_ranks,
+                               int32_t n_dest, uint32_t epoch, int64_t* d_recv_count, void* ws,
+                               size_t ws_bytes, hs_stream_t stream);
+hs_status_t hs_forward_wait(const uint64_t* my_done, int32_t world, uint32_t epoch, hs_stream_t stream);
+hs_status_t hs_ipc_alloc(size_t bytes, void** dptr);   /* cudaMalloc + zero fill: exportable whole allocation */
+hs_status_t hs_ipc_free(void* dptr);
+hs_status_t hs_ipc_handle(const void* dptr, void* handle /* host, 64 bytes */);
+hs_status_t hs_ipc_open(const void* handle /* host, 64 bytes */, void** dptr);
+hs_status_t hs_ipc_close(void* dptr);
+
+/* ------------------------------------------------------------------------ */
 /* Diagnostics.                                                              */
 /* ------------------------------------------------------------------------ */
 const char* hs_status_string(hs_status_t s);

@@ -266,6 +266,44 @@ def perf_graph(correct: torch.Tensor, energy: torch.Tensor, N: int, *, tau: int 
 
 
 # ---------------------------------------------------------------------------
+# Peer-memory forwarding of deferred requests (hs_forward_*)
+# ---------------------------------------------------------------------------
+def _ptr_array(ptrs):
+    import ctypes
+    return (ctypes.c_void_p * len(ptrs))(*[int(p) if p else None for p in ptrs])
+
+
+def forward_publish(d_count: torch.Tensor, cap: int, rank: int, peer_counts: list, epoch: int,
+                    stream=None):
+    """Store {epoch, D_rank} into slot ``rank`` of every rank's count array
+    (``peer_counts[h]``: device address of rank h's u64[world] array, mapped here)."""
+    _abi.call("hs_forward_publish", _p(d_count), int(cap), int(rank), len(peer_counts),
+              _ptr_array(peer_counts), int(epoch), _stream(stream))
+
+
+def forward_scatter(ids: torch.Tensor, cap: int, rank: int, my_counts: torch.Tensor | int,
+                    peer_done: list, peer_recv_ids: list, dest_ranks: list, epoch: int,
+                    recv_count: torch.Tensor, ws: torch.Tensor, *, payload: torch.Tensor | None = None,
+                    payload_row_bytes: int = 0, peer_recv_payload: list | None = None, stream=None):
+    """Write this rank's deferred ids (+ payload rows) into their destination
+    ranks' receive buffers at their global positions; ``recv_count`` gets this
+    rank's receive count."""
+    import ctypes
+    mc = my_counts if isinstance(my_counts, int) else my_counts.data_ptr()
+    dr = (ctypes.c_int32 * len(dest_ranks))(*[int(d) for d in dest_ranks])
+    _abi.call("hs_forward_scatter", _p(ids), _p(payload), int(payload_row_bytes), int(cap), int(rank),
+              len(peer_done), mc, _ptr_array(peer_done), _ptr_array(peer_recv_ids),
+              _ptr_array(peer_recv_payload) if peer_recv_payload else None, dr, len(dest_ranks),
+              int(epoch), _p(recv_count), _p(ws), ws.numel(), _stream(stream))
+
+
+def forward_wait(my_done: torch.Tensor | int, world: int, epoch: int, stream=None):
+    """Wait until every rank's done flag of ``epoch`` is in this rank's array."""
+    md = my_done if isinstance(my_done, int) else my_done.data_ptr()
+    _abi.call("hs_forward_wait", md, int(world), int(epoch), _stream(stream))
+
+
+# ---------------------------------------------------------------------------
 # hs_route_compact
 # ---------------------------------------------------------------------------
 def route_compact(conf: torch.Tensor, threshold: float | torch.Tensor, *, is_last: bool = False,

@@ -55,6 +55,15 @@ SIGNATURES = {
     "hs_threshold_replay": (I32, [P, P, I32, I64, I32, P, I64, P, P, P, P, P, P, SZ, P]),
     "hs_perf_graph_workspace": (SZ, [I64]),
     "hs_perf_graph": (I32, [P, P, I64, I64, I64, I64, P, I32, P, P, P, P, P, P, SZ, P, P]),
+    "hs_forward_publish": (I32, [P, I64, I32, I32, P, ctypes.c_uint32, P]),
+    "hs_forward_scatter": (I32, [P, P, I64, I64, I32, I32, P, P, P, P, P, I32, ctypes.c_uint32, P, P,
+                                 SZ, P]),
+    "hs_forward_wait": (I32, [P, I32, ctypes.c_uint32, P]),
+    "hs_ipc_alloc": (I32, [SZ, P]),
+    "hs_ipc_free": (I32, [P]),
+    "hs_ipc_handle": (I32, [P, P]),
+    "hs_ipc_open": (I32, [P, P]),
+    "hs_ipc_close": (I32, [P]),
     "hs_status_string": (ctypes.c_char_p, [I32]),
     "hs_last_error": (ctypes.c_char_p, []),
     "hs_launch_count": (ctypes.c_uint64, []),

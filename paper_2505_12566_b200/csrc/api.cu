@@ -393,6 +393,105 @@ hs_status_t hs_perf_graph(const int64_t* d_correct, const int64_t* d_energy, int
                     "performance graph kernels");
 }
 
+hs_status_t hs_forward_publish(const int64_t* d_count, int64_t cap, int32_t rank, int32_t world,
+                               uint64_t* const* peer_counts, uint32_t epoch, hs_stream_t stream) {
+  if (world < 1 || world > hs::kFwdMaxWorld || rank < 0 || rank >= world)
+    return fail(HS_ERR_INVALID_ARGUMENT, "rank %d / world %d out of range", rank, world);
+  if (!d_count || !peer_counts || cap < 0 || cap >= ((int64_t)1 << 32) || epoch == 0)
+    return fail(HS_ERR_INVALID_ARGUMENT, "d_count, peer_counts, 0 <= cap < 2^32 and epoch > 0 are required");
+  hs::FwdPeers p{};
+  p.world = world;
+  for (int h = 0; h < world; ++h) {
+    if (!peer_counts[h]) return fail(HS_ERR_INVALID_ARGUMENT, "peer_counts[%d] is NULL", h);
+    p.counts[h] = reinterpret_cast<unsigned long long*>(peer_counts[h]);
+  }
+  return cuda_check(hs::launch_fwd_publish(d_count, cap, rank, p, epoch, (cudaStream_t)stream),
+                    "forward publish kernel");
+}
+
+hs_status_t hs_forward_scatter(const int64_t* ids, const void* payload, int64_t payload_row_bytes,
+                               int64_t cap, int32_t rank, int32_t world, const uint64_t* my_counts,
+                               uint64_t* const* peer_done, int64_t* const* peer_recv_ids,
+                               void* const* peer_recv_payload, const int32_t* dest_ranks,
+                               int32_t n_dest, uint32_t epoch, int64_t* d_recv_count, void* ws,
+                               size_t ws_bytes, hs_stream_t stream) {
+  if (world < 1 || world > hs::kFwdMaxWorld || rank < 0 || rank >= world)
+    return fail(HS_ERR_INVALID_ARGUMENT, "rank %d / world %d out of range", rank, world);
+  if (!ids || !my_counts || !peer_done || !peer_recv_ids || !d_recv_count || epoch == 0 || cap < 0)
+    return fail(HS_ERR_INVALID_ARGUMENT, "ids, my_counts, peer_done, peer_recv_ids, d_recv_count and epoch > 0 are required");
+  if (payload_row_bytes < 0 || (payload_row_bytes % 16) != 0 || (payload_row_bytes && (!payload || !peer_recv_payload || !aligned16(payload))))
+    return fail(HS_ERR_INVALID_ARGUMENT, "payload rows must be 16-byte aligned multiples of 16 bytes");
+  if (!dest_ranks || n_dest < 1 || n_dest > world)
+    return fail(HS_ERR_INVALID_ARGUMENT, "1 <= n_dest <= world destination ranks are required");
+  if (!ws || ws_bytes < 256) return fail(HS_ERR_WORKSPACE_TOO_SMALL, "workspace %zu < 256", ws_bytes);
+  hs::FwdPeers p{};
+  p.world = world;
+  p.my_counts = reinterpret_cast<const unsigned long long*>(my_counts);
+  for (int h = 0; h < world; ++h) {
+    if (!peer_done[h] || !peer_recv_ids[h] || (payload_row_bytes && !peer_recv_payload[h]))
+      return fail(HS_ERR_INVALID_ARGUMENT, "peer buffers of rank %d are NULL", h);
+    p.done[h] = reinterpret_cast<unsigned long long*>(peer_done[h]);
+    p.recv_ids[h] = peer_recv_ids[h];
+    p.recv_payload[h] = payload_row_bytes ? peer_recv_payload[h] : nullptr;
+  }
+  hs::FwdDest d{};
+  d.n = n_dest;
+  unsigned seen = 0;
+  for (int i = 0; i < n_dest; ++i) {
+    if (dest_ranks[i] < 0 || dest_ranks[i] >= world || (seen >> dest_ranks[i]) & 1u)
+      return fail(HS_ERR_INVALID_ARGUMENT, "dest_ranks must be distinct ranks of the group");
+    seen |= 1u << dest_ranks[i];
+    d.ranks[i] = dest_ranks[i];
+  }
+  return cuda_check(hs::launch_fwd_scatter(ids, payload, payload_row_bytes, cap, rank, p, epoch, d,
+                                           d_recv_count, reinterpret_cast<unsigned*>(ws),
+                                           (cudaStream_t)stream),
+                    "forward scatter kernel");
+}
+
+hs_status_t hs_forward_wait(const uint64_t* my_done, int32_t world, uint32_t epoch, hs_stream_t stream) {
+  if (!my_done || world < 1 || world > hs::kFwdMaxWorld || epoch == 0)
+    return fail(HS_ERR_INVALID_ARGUMENT, "my_done, 1 <= world <= %d and epoch > 0 are required", hs::kFwdMaxWorld);
+  return cuda_check(hs::launch_fwd_wait(reinterpret_cast<const unsigned long long*>(my_done), world, epoch,
+                                        (cudaStream_t)stream),
+                    "forward wait kernel");
+}
+
+hs_status_t hs_ipc_alloc(size_t bytes, void** dptr) {
+  if (!dptr || bytes == 0) return fail(HS_ERR_INVALID_ARGUMENT, "dptr and bytes > 0 are required");
+  hs_status_t st = cuda_check(cudaMalloc(dptr, bytes), "cudaMalloc");
+  if (st != HS_OK) return st;
+  st = cuda_check(cudaMemset(*dptr, 0, bytes), "cudaMemset");
+  if (st == HS_OK) st = cuda_check(cudaDeviceSynchronize(), "cudaDeviceSynchronize");
+  return st;
+}
+
+hs_status_t hs_ipc_free(void* dptr) {
+  if (!dptr) return fail(HS_ERR_INVALID_ARGUMENT, "dptr is required");
+  return cuda_check(cudaFree(dptr), "cudaFree");
+}
+
+hs_status_t hs_ipc_handle(const void* dptr, void* handle) {
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+  if (!dptr || !handle) return fail(HS_ERR_INVALID_ARGUMENT, "dptr and handle are required");
+  cudaIpcMemHandle_t h;
+  hs_status_t st = cuda_check(cudaIpcGetMemHandle(&h, const_cast<void*>(dptr)), "cudaIpcGetMemHandle");
+  if (st == HS_OK) memcpy(handle, &h, sizeof h);
+  return st;
+}
+
+hs_status_t hs_ipc_open(const void* handle, void** dptr) {
+  if (!handle || !dptr) return fail(HS_ERR_INVALID_ARGUMENT, "handle and dptr are required");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof h);
+  return cuda_check(cudaIpcOpenMemHandle(dptr, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+}
+
+hs_status_t hs_ipc_close(void* dptr) {
+  if (!dptr) return fail(HS_ERR_INVALID_ARGUMENT, "dptr is required");
+  return cuda_check(cudaIpcCloseMemHandle(dptr), "cudaIpcCloseMemHandle");
+}
+
 size_t hs_route_compact_workspace(int64_t n) { return hs::compact_ws_bytes(n); }
 
 static hs_status_t route_compact_impl(const float* conf, int64_t n, const int64_t* d_n,

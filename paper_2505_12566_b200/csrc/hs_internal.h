@@ -207,4 +207,25 @@ cudaError_t launch_graph(const int64_t* C, const int64_t* E, int64_t S, int64_t 
                          int64_t* front_c, int64_t* front_e, int64_t* front_s, int64_t* front_n,
                          int64_t* pick, uint32_t* status, void* ws, cudaStream_t s);
 
+// ---- multi-GPU forwarding over peer memory (forward.cu) -----------------------
+constexpr int kFwdMaxWorld = 8;
+struct FwdPeers {
+  int world;
+  unsigned long long* counts[kFwdMaxWorld];   // rank h's count array (u64[world]), peer-mapped
+  unsigned long long* done[kFwdMaxWorld];     // rank h's done array (u64[world]), peer-mapped
+  const unsigned long long* my_counts;        // this rank's count array
+  int64_t* recv_ids[kFwdMaxWorld];            // rank h's receive buffer for ids
+  void* recv_payload[kFwdMaxWorld];           // rank h's receive buffer for payload rows (or NULL)
+};
+struct FwdDest {
+  int n;                                      // destination ranks of the next stage
+  int ranks[kFwdMaxWorld];
+};
+cudaError_t launch_fwd_publish(const int64_t* d_count, int64_t cap, int rank, const FwdPeers& p,
+                               unsigned epoch, cudaStream_t s);
+cudaError_t launch_fwd_scatter(const int64_t* ids, const void* payload, int64_t row_bytes, int64_t cap,
+                               int rank, const FwdPeers& p, unsigned epoch, const FwdDest& dest,
+                               int64_t* d_recv_count, unsigned* done_ctr, cudaStream_t s);
+cudaError_t launch_fwd_wait(const unsigned long long* my_done, int world, unsigned epoch, cudaStream_t s);
+
 }  // namespace hs
