@@ -56,10 +56,12 @@ def parse():
                     help="run routing stage 1 strictly after the calibration (no PDL overlap)")
     ap.add_argument("--force-dist", action="store_true",
                     help="initialise NCCL even at one GPU (exercises the sharded calibration path)")
-    ap.add_argument("--placement", default="local", choices=["local", "balanced"],
+    ap.add_argument("--placement", default="local", choices=["local", "balanced", "p2p"],
                     help="local: every rank serves every stage (no data-path collective); "
                          "balanced: deferred requests are re-spread over all ranks after "
-                         "every stage with an NCCL all-to-all (dist.forward_deferred)")
+                         "every stage with an NCCL all-to-all (dist.forward_deferred); "
+                         "p2p: the same re-spread by the hs_forward_* kernels over peer "
+                         "memory (dist.PeerForwarder), graph-captured")
     return ap.parse_args()
 
 
@@ -452,6 +454,109 @@ def run_balanced(args, world, rank, local):
         "gpu_launches": launches, "clocks": clk.summary(), "e2e": None,
         "thresholds": router.cal["t"].cpu().tolist(),
     }
+    return line, fam
+
+
+def run_p2p(args, world, rank, local):
+    """BALANCED placement with the deferred requests moved by the hs_forward_*
+    kernels over peer memory (CUDA IPC mappings, dist.PeerForwarder): counts and
+    data never touch the host.  World size 1: the whole step is captured in one
+    CUDA graph; > 1: eager (the calibration's NCCL all-reduce stays)."""
+    import torch
+    import torch.distributed as dist
+    import workload
+    import paper_2505_12566_b200 as hs
+    from paper_2505_12566_b200 import dist as hsd
+    from workload import synth
+
+    dev = torch.device("cuda", local)
+    fam = family(args.config)
+    K, n, P = fam.K, fam.n, fam.payload_bytes
+    tdt = torch.bfloat16 if fam.dtype == "bf16" else torch.float32
+    logits = []
+    for k in range(K):
+        rows = n if k == 0 else world * n
+        x = torch.empty(rows * fam.L, fam.C, dtype=tdt, device=dev)
+        workload.gpu_logits(x, fam, k, id_base=rank * n if k == 0 else 0, n=rows)
+        logits.append(x)
+    _, val, labels, _ = build_inputs(synth.scaled(fam, n=1), rank, dev)
+    group = dist.group.WORLD if dist.is_initialized() else None
+    router = make_router(fam, dev, group if world > 1 else None)
+    cap = world * n
+    fwd = hsd.PeerForwarder(n, P, group=group, device=dev)
+    ws = hs.workspace(hs.lib().hs_cascade_step_workspace(cap, fam.L), dev)
+    ids0 = torch.arange(rank * n, (rank + 1) * n, dtype=torch.int64, device=dev)
+    rows0 = torch.arange(n, dtype=torch.int64, device=dev)
+    pay0 = (torch.randint(0, 255, (n, P), dtype=torch.uint8, device=dev) if P else None)
+    outs = [{"acc_ids": torch.empty(cap, dtype=torch.int64, device=dev),
+             "acc_conf": torch.empty(cap, dtype=torch.float32, device=dev),
+             "acc_pred": torch.empty(cap * fam.L, dtype=torch.int32, device=dev),
+             "next_ids": torch.empty(cap, dtype=torch.int64, device=dev),
+             "counts": torch.zeros(2, dtype=torch.int64, device=dev)} for _ in range(K)]
+    if P:
+        for o in outs:
+            o["next_payload"] = torch.empty(cap * P, dtype=torch.uint8, device=dev)
+
+    def step():
+        cal = router.calibrate(val, labels)
+        ids, pay, d_n, nb, row_index = ids0, pay0, None, n, rows0
+        for k in range(K):
+            o = outs[k]
+            hs.cascade_step(k, K, logits[k], cal["t"][k:k + 1], n=nb, d_n=d_n, seq_len=fam.L,
+                            n_classes=fam.C, temperature=fam.temps[k], kind=fam.kind,
+                            reduce=fam.reduce, row_index=row_index, ids=ids, payload=pay,
+                            payload_row_bytes=P, out=o, ws=ws)
+            if k == K - 1:
+                break
+            ids, pay, d_n = fwd.forward(o["next_ids"], o["counts"][1:2],
+                                        payload=o["next_payload"][: n * P].view(n, P) if P else None)
+            nb, row_index = cap, ids
+
+    stream = torch.cuda.Stream(device=dev)
+    with torch.cuda.stream(stream):
+        for _ in range(max(args.warmup, 3)):
+            step()
+    torch.cuda.synchronize()
+    graph = None
+    per_step = 0
+    if world == 1 and not args.no_graph:
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=stream):
+            l0 = hs.launch_count()
+            step()
+            per_step = hs.launch_count() - l0
+        graph.replay()
+        torch.cuda.synchronize()
+    l0 = hs.launch_count()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    barrier(world)
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        with torch.cuda.stream(stream):
+            t0.record(stream)
+            for _ in range(args.steps):
+                graph.replay() if graph is not None else step()
+            t1.record(stream)
+        torch.cuda.synchronize()
+    barrier(world)
+    ms = max_over_ranks(t0.elapsed_time(t1), world) / args.steps
+    launches = per_step * args.steps if graph is not None else hs.launch_count() - l0
+    reach = [int(o["counts"].sum().item()) for o in outs]
+    line = {
+        "metric": METRIC, "value": world * n / (ms / 1e3), "unit": "requests/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": fam.name, "description": CONFIG_TEXT[args.config],
+                   "requests_per_gpu": n, "validation_per_gpu": fam.n_val, "K": K,
+                   "classes": fam.C, "seq_len": fam.L, "logits_dtype": fam.dtype,
+                   "parallelism": f"request-sharded dp{world}, balanced forwarding over peer memory "
+                                  "(hs_forward_* kernels, CUDA IPC)",
+                   "l2": "inputs larger than L2", "cuda_graph": graph is not None},
+        "reach_this_rank": reach, "gpu_launches": launches, "clocks": clk.summary(), "e2e": None,
+        "thresholds": router.cal["t"].cpu().tolist(),
+    }
+    fwd.close()
     return line, fam
 
 
@@ -1014,13 +1119,13 @@ def main():
         if line is not None:
             emit(json.dumps(line))
         return
-    if (args.placement == "balanced" or args.force_dist) and int(os.environ.get("WORLD_SIZE", "1")) == 1:
+    if (args.placement in ("balanced", "p2p") or args.force_dist) and int(os.environ.get("WORLD_SIZE", "1")) == 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         os.environ.setdefault("MASTER_PORT", "29533")
         os.environ["WORLD_SIZE"] = "1"
         os.environ["RANK"] = "0"
         os.environ["LOCAL_RANK"] = "0"
-    world, rank, local = init_dist(args, force=args.placement == "balanced" or args.force_dist)
+    world, rank, local = init_dist(args, force=args.placement in ("balanced", "p2p") or args.force_dist)
     if args.config == "c2g":
         line, fam, conf, ok = run_graph(args, world, rank, local)
         if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -1037,6 +1142,8 @@ def main():
         return
     if args.placement == "balanced":
         line, fam = run_balanced(args, world, rank, local)
+    elif args.placement == "p2p":
+        line, fam = run_p2p(args, world, rank, local)
     else:
         line, fam, *_ = run_ours(args, world, rank, local)
     if rank == 0:

@@ -83,3 +83,106 @@ def global_order_offsets(counts: list[int]) -> list[int]:
         off.append(acc)
         acc += d
     return off
+
+
+class _DevArray:
+    """A torch view of a raw device allocation (``__cuda_array_interface__``)."""
+
+    def __init__(self, ptr: int, shape, typestr: str):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr,
+                                         "data": (int(ptr), False), "version": 3, "strides": None}
+
+
+class PeerForwarder:
+    """Forwarding of deferred requests over peer memory (hs_forward_*): the
+    same result as :func:`forward_deferred` -- this rank's block of the global
+    stable deferred list -- moved by the kernels through CUDA IPC mappings of
+    the peers' buffers (NVLink / NVSwitch), with no host round trip and no NCCL
+    on the data path.  The IPC handles are exchanged once, at construction,
+    with ``all_gather_object`` over the process group.
+
+    Buffers per rank (one exportable allocation each, hs_ipc_alloc): the count
+    and done flag arrays (u64[world]) and two receive sets (ids [world*cap],
+    payload [world*cap*P]) used on alternate stages."""
+
+    def __init__(self, cap: int, payload_row_bytes: int = 0, group=None, device=None):
+        import ctypes
+        from . import lib, _abi
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.cap, self.P = int(cap), int(payload_row_bytes)
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        W = self.world
+        sizes = {"counts": 8 * W, "done": 8 * W,
+                 "ids0": 8 * W * self.cap, "ids1": 8 * W * self.cap}
+        if self.P:
+            sizes.update(pay0=W * self.cap * self.P, pay1=W * self.cap * self.P)
+        self._own = {}
+        for k, b in sizes.items():
+            p = ctypes.c_void_p()
+            _abi.call("hs_ipc_alloc", max(int(b), 16), ctypes.byref(p))
+            self._own[k] = int(p.value)
+        handles = {}
+        for k, p in self._own.items():
+            h = ctypes.create_string_buffer(64)
+            if W > 1:
+                _abi.call("hs_ipc_handle", p, h)
+            handles[k] = bytes(h.raw)
+        allh = [None] * W
+        if W > 1:
+            dist.all_gather_object(allh, handles, group=group)
+        else:
+            allh = [handles]
+        self._opened = []
+        self.peer = {k: [0] * W for k in self._own}
+        for h in range(W):
+            for k in self._own:
+                if h == self.rank:
+                    self.peer[k][h] = self._own[k]
+                else:
+                    p = ctypes.c_void_p()
+                    hb = ctypes.create_string_buffer(allh[h][k], 64)
+                    _abi.call("hs_ipc_open", hb, ctypes.byref(p))
+                    self.peer[k][h] = int(p.value)
+                    self._opened.append(int(p.value))
+        self.ws = torch.zeros(256, dtype=torch.uint8, device=self.device)
+        self.recv_count = torch.zeros(1, dtype=torch.int64, device=self.device)
+        self.epoch = 0
+        self._lib = lib
+
+    def recv_ids(self, parity: int) -> torch.Tensor:
+        return torch.as_tensor(_DevArray(self._own[f"ids{parity}"], (self.world * self.cap,), "<i8"),
+                               device=self.device)
+
+    def recv_payload(self, parity: int) -> torch.Tensor | None:
+        if not self.P:
+            return None
+        return torch.as_tensor(_DevArray(self._own[f"pay{parity}"], (self.world * self.cap, self.P), "|u1"),
+                               device=self.device)
+
+    def forward(self, ids: torch.Tensor, count: torch.Tensor, *, dest_ranks: list[int] | None = None,
+                payload: torch.Tensor | None = None, stream=None):
+        """Forward this rank's compacted deferred list ``ids[:count]`` (``count``:
+        device int64[1], e.g. d_counts[1:2]).  Returns (recv_ids, recv_payload,
+        recv_count) -- device tensors of this forward's receive set (alternating),
+        recv_count a device int64[1]; nothing is read back to the host."""
+        from . import forward_publish, forward_scatter, forward_wait
+        self.epoch += 1
+        par = self.epoch & 1
+        dest = list(range(self.world)) if dest_ranks is None else list(dest_ranks)
+        forward_publish(count, self.cap, self.rank, self.peer["counts"], self.epoch, stream=stream)
+        forward_scatter(ids, self.cap, self.rank, self._own["counts"], self.peer["done"],
+                        self.peer[f"ids{par}"], dest, self.epoch, self.recv_count, self.ws,
+                        payload=payload, payload_row_bytes=self.P if payload is not None else 0,
+                        peer_recv_payload=self.peer.get(f"pay{par}"), stream=stream)
+        forward_wait(self._own["done"], self.world, self.epoch, stream=stream)
+        return self.recv_ids(par), self.recv_payload(par), self.recv_count
+
+    def close(self):
+        from . import _abi
+        torch.cuda.synchronize(self.device)
+        for p in self._opened:
+            _abi.call("hs_ipc_close", p)
+        for p in self._own.values():
+            _abi.call("hs_ipc_free", p)
+        self._opened, self._own = [], {}
