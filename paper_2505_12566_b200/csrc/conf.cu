@@ -507,8 +507,11 @@ __global__ void __launch_bounds__(256, (NV <= 8 ? 2 : 1)) conf_warp_kernel(const
 //   wt seen later) -- at least K elements are >= wt, so elements <= wt can be
 //   replaced by copies of wt.  Exact for ties (multisets of values).
 // ---------------------------------------------------------------------------
-constexpr int kTopkU = 4;                  // vectors per lane per chunk
-constexpr int kTopkPB = 40;                // candidate slots per lane (>= 32 per chunk + slack)
+#ifndef HS_TOPK_U
+#define HS_TOPK_U 4
+#endif
+constexpr int kTopkU = HS_TOPK_U;          // vectors per lane per chunk
+constexpr int kTopkPB = 8 * kTopkU + 8;    // candidate slots per lane (>= one chunk's elements + slack)
 
 __device__ __forceinline__ uint32_t f_order(float f) {   // monotone float -> u32
   const uint32_t u = __float_as_uint(f);
@@ -555,12 +558,12 @@ __device__ __noinline__ float topk_merge(float lst, float* col, int pn, int K, i
 }
 
 template <bool BF16, bool ENTROPY>
-__global__ void __launch_bounds__(256, 3) conf_topk_kernel(const ConfArgs a) {
+__global__ void __launch_bounds__(256, kTopkU <= 4 ? 3 : 2) conf_topk_kernel(const ConfArgs a) {
   pdl_start();
   constexpr int VE = BF16 ? 8 : 4, U = kTopkU;
-  __shared__ float s_col[8][kTopkPB][32];
+  extern __shared__ __align__(16) float s_col[];          // [8 warps][kTopkPB][32 lanes]
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  float* col = &s_col[warp][0][lane];
+  float* col = s_col + (size_t)warp * kTopkPB * 32 + lane;
   const int64_t rows = live_rows(a);
   const int nvec = a.nvec, K = a.top_k;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -641,7 +644,7 @@ __global__ void __launch_bounds__(256, 3) conf_topk_kernel(const ConfArgs a) {
       // merge as soon as K candidates are buffered (raises wt early, so later
       // chunks rarely have any) or when a column could overflow in the next chunk
       if (__reduce_add_sync(0xFFFFFFFFu, (unsigned)pn) >= (unsigned)K ||
-          __any_sync(0xFFFFFFFFu, pn > kTopkPB - 32)) {
+          __any_sync(0xFFFFFFFFu, pn > kTopkPB - 8 * kTopkU)) {
         __syncwarp();
         lst = topk_merge(lst, col, pn, K, lane);
         wt = __shfl_sync(0xFFFFFFFFu, lst, K - 1);
@@ -1628,11 +1631,17 @@ const char* confidence_path(int64_t nvec) {
 template <bool BF16, bool ENTROPY>
 cudaError_t launch_topk(const ConfArgs& a, int64_t rows, cudaStream_t s) {
   auto k = conf_topk_kernel<BF16, ENTROPY>;
-  static const int occ = occupancy(k, 256);
+  constexpr size_t smem = (size_t)8 * kTopkPB * 32 * sizeof(float);
+  static const int occ = [&] {
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int b = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k, 256, smem);
+    return b > 0 ? b : 1;
+  }();
   const int64_t want = (rows + 7) / 8;
   const int64_t cap = (int64_t)num_sms() * occ;
   const int grid = (int)(want < cap ? (want > 0 ? want : 1) : cap);
-  return launch_pdl(k, dim3(grid), dim3(256), 0, s, a);
+  return launch_pdl(k, dim3(grid), dim3(256), smem, s, a);
 }
 
 cudaError_t launch_confidence(const ConfArgs& a, bool bf16, cudaStream_t s) {

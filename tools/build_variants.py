@@ -12,6 +12,7 @@ VARIANTS = {
     "noexp": ["HS_EXP_NOEXP"],           # ... or without the exponential pass
     "tf768": ["HS_TF_THREADS=768"],      # temperature fit: 24 warps/SM, 85 registers
     "tf1024": ["HS_TF_THREADS=1024"],    # temperature fit: 32 warps/SM, 64 registers
+    "topk8": ["HS_TOPK_U=8"],            # Top-K confidence: 8 vectors per lane per chunk
 }
 
 if __name__ == "__main__":
