@@ -304,16 +304,25 @@ def run_ours(args, world, rank, local):
     clocks = clk.summary()
     gpu_launches = (launches_per_step * args.steps) if graph is not None else (hs.launch_count() - l_before)
     # per-launch duration of the dominant kernel: one more timed pass, recording each step's events
-    k_ms = []
+    k_ms, s_ms = [], []
+    s0 = torch.cuda.Event(enable_timing=True)
+    s1 = torch.cuda.Event(enable_timing=True)
     with torch.cuda.stream(stream):
         for _ in range(min(args.steps, 50)):
+            s0.record(stream)
             if graph is not None:
                 graph.replay()
             else:
                 step()
+            s1.record(stream)
             stream.synchronize()
             k_ms.append(ev[0].elapsed_time(ev[1]))
+            s_ms.append(s0.elapsed_time(s1))
     kernel_ms = sum(k_ms) / len(k_ms)
+    s_ms.sort()
+    step_pct = {"p10": s_ms[len(s_ms) // 10], "p50": s_ms[len(s_ms) // 2],
+                "p90": s_ms[(9 * len(s_ms)) // 10], "n": len(s_ms),
+                "note": "per-step CUDA-event times of a second, individually synchronised pass"}
     ms = max_over_ranks(total_ms, world) / args.steps
     # cascade statistics (identical every step): reach per stage
     counts = router.cascade.counts.cpu().tolist()
@@ -361,6 +370,7 @@ def run_ours(args, world, rank, local):
                      "peak_source": peak_src},
         "e2e": e2e, "gpu_launches": gpu_launches, "clocks": clocks,
         "gpu_launches_per_step": gpu_launches / args.steps,
+        "step_ms_percentiles": step_pct,
     }
     return line, fam, route, val, labels
 
