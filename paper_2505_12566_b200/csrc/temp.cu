@@ -52,6 +52,7 @@ struct TfState {
   long long used;           // rows entering the mean
   int lo_known, hi_known;   // g(lo) < 0 / g(hi) > 0 observed (else: clamp end not yet swept)
   int done, passes, converged;
+  int newton_prev;          // the last move was a Newton step
 };
 
 __device__ __forceinline__ uint32_t wordq(const uint4& v, int q) {
@@ -213,6 +214,17 @@ __device__ void tf_update(TfState& s, double nll, double g, double h, const TfAr
       s.done = s.converged = 1;
       return;
     }
+    // quadratic regime (two Newton steps in a row): the error left after this
+    // step is ~ step^3 / prev_step^2; finish without a confirming sweep when it
+    // is 10x below the tolerance
+    if (s.newton_prev && s.dx > 0.0) {
+      const double st = fabs(step);
+      if (st * st * st <= 0.1 * a.tol * beta * s.dx * s.dx) {
+        s.T = 1.0 / bn;
+        s.done = s.converged = 1;
+        return;
+      }
+    }
     next = bn;
   } else if (g > 0.0 && !s.lo_known && !(h > 0.0 && bn > s.lo)) {
     next = s.lo;                            // root may lie below the range: probe t_hi
@@ -226,6 +238,7 @@ __device__ void tf_update(TfState& s, double nll, double g, double h, const TfAr
     s.done = s.converged = 1;
     return;
   }
+  s.newton_prev = next == bn ? 1 : 0;
   s.dx_old = s.dx;
   s.dx = fabs(next - beta);
   s.beta = next;
@@ -280,6 +293,7 @@ __global__ void __launch_bounds__(kTfThreads, 1) temp_fit_kernel(const TfArgs a)
     s.T = s.nll;
     s.used = -1;
     s.lo_known = s.hi_known = 0;
+    s.newton_prev = 0;
     s.done = 0;
     s.passes = 0;
     s.converged = 0;
