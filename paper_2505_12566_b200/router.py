@@ -12,9 +12,12 @@ from __future__ import annotations
 
 import torch
 
+import dataclasses
+
 from . import (Cascade, StageSpec, _calib_out, calibrate_begin, calibrate_hist_view,
                calibrate_histogram, calibrate_select, calibrate_thresholds,
-               calibrate_workspace, confidence, confidence_batched, cascade_step, route_compact)
+               calibrate_workspace, confidence, confidence_batched, cascade_step, fit_temperature,
+               perf_graph, route_compact, threshold_replay)
 
 
 class Router:
@@ -89,6 +92,50 @@ class Router:
                 calibrate_select(self.K, k, self.cal, log2_bins=self.q, ws=self.cal_ws,
                                  stream=stream)
         return self.cal
+
+    # ---- offline: temperature scaling (Eq. 1) ---------------------
+    def fit_temperatures(self, val_logits: list, labels: torch.Tensor, *, t_lo: float | None = None,
+                         t_hi: float | None = None, stream=None) -> list:
+        """Fit one temperature per stage model on its validation logits (all
+        models in one hs_fit_temperature launch; token rows of generation models
+        are samples) and use them from now on (the confidence kernels take T as
+        a host value, so this reads the K temperatures back: offline step)."""
+        L = max(s.seq_len for s in self.stages)
+        kw = {} if t_lo is None else {"t_lo": t_lo, "t_hi": t_hi}
+        r = fit_temperature(val_logits, labels, n=self.n_val * L,
+                            n_classes=self.stages[0].n_classes, stream=stream, **kw)
+        temps = [float(t) for t in r["T"].cpu().tolist()]
+        self.stages = [dataclasses.replace(s, temperature=t) for s, t in zip(self.stages, temps)]
+        self.cascade.stages = self.stages
+        self.temperature_fit = r
+        return temps
+
+    # ---- offline: threshold performance graph, AP / EO (Alg. 1) -------------
+    def performance_graph(self, weights, *, log2_bins: int = 4, bvecs: torch.Tensor | None = None,
+                          stream=None) -> dict:
+        """Replay the cascade on the last calibrated validation confidences for
+        every vector of the (B+2)^(K-1) grid (or ``bvecs``) with integer energy
+        weights per model visit; returns the frontier, and the AP / EO vectors'
+        threshold indices and thresholds (host lists)."""
+        from . import grid_vector
+        r = threshold_replay(self.vconf, self.vok, weights, log2_bins=log2_bins, bvecs=bvecs,
+                             stream=stream)
+        g = perf_graph(r["correct"], r["energy"], self.n_val, model_correct=r["model_correct"],
+                       K=self.K, stream=stream)
+        n = int(g["front_n"].item())
+        pick = g["pick"].cpu().tolist()
+        B = 1 << log2_bins
+
+        def vec(s):
+            if s < 0:
+                return None
+            b = grid_vector(s, self.K, log2_bins) if bvecs is None else bvecs[s].cpu().tolist()
+            return {"b": b, "t": [float("inf") if x == B + 1 else x / B for x in b] + [0.0],
+                    "correct": int(r["correct"][s]), "energy": int(r["energy"][s])}
+
+        return {"front_c": g["front_c"][:n].cpu(), "front_e": g["front_e"][:n].cpu(),
+                "front_s": g["front_s"][:n].cpu(), "ap": vec(pick[0]), "eo": vec(pick[1]),
+                "replay": r}
 
     # ---- online: the cascade (P:443-446) ------------------------------------
     def route(self, logits: list, *, n: int | None = None, ids=None, payload=None,

@@ -164,3 +164,46 @@ def test_graph_closed_forms_and_edges(hs):
                       status=st)
     torch.cuda.synchronize()
     assert int(st.item()) & 1 and int(g["front_n"].item()) == 1 and g["pick"].tolist() == [0, 0]
+
+
+def test_router_offline_flow(hs):
+    """The offline 'dataflow construction' through the Router: fit temperatures
+    (Eq. 1), calibrate AP thresholds with them (Alg. 1 AP), build the threshold
+    performance graph (AP / EO), then route -- each step checked against the oracle."""
+    from paper_2505_12566_b200.router import Router
+    fam = synth.scaled(synth.FAMILIES["c2"], n=4000, n_val=3000)
+    dev_ = dev()
+    vids = np.arange(fam.n_val, dtype=np.int64) + synth.VAL_ID_BASE
+    lab = synth.labels_np(fam.seed, vids, 1, fam.C).reshape(-1)
+    vbits = [synth.logits_np(fam.seed, k, vids, 1, fam.C, fam.thr[k], "bf16") for k in range(fam.K)]
+    val = [torch.from_numpy(b.view(np.int16)).to(dev_).view(torch.bfloat16) for b in vbits]
+    labels = torch.from_numpy(lab).to(dev_)
+    router = Router([hs.StageSpec(fam.C, 1.0) for _ in range(fam.K)], fam.n, fam.n_val, dev_,
+                    log2_bins=fam.log2_bins)
+    temps = router.fit_temperatures(val, labels)
+    for k in range(fam.K):
+        t_o = oracle.fit_temperature(vbits[k], lab, n_classes=fam.C)
+        assert abs(temps[k] - t_o) <= 1e-5 * t_o
+    cal = router.calibrate(val, labels)
+    torch.cuda.synchronize()
+    vconf = router.vconf.cpu().numpy()
+    vok = router.vok.cpu().numpy()
+    for k in range(fam.K - 1):                   # the fitted T are the ones used
+        ref = oracle.confidence(vbits[k], fam.n_val, 1, fam.C, fam.C, temps[k], labels=lab)
+        assert np.max(np.abs(vconf[k] - ref["conf"]) / ref["conf"]) <= 1e-5
+    assert cal["b"].cpu().numpy().tolist() == oracle.calibrate(vconf, vok, fam.log2_bins)["b"].tolist()
+    w = [1, 2, 4, 8, 16]
+    g = router.performance_graph(w, log2_bins=3)
+    c, e, _ = oracle.replay(vconf, vok, 3, w)
+    ref = oracle.perf_graph(c, e, int(vok[-1].sum()), int(vok[-2].sum()))
+    assert g["front_s"].numpy().tolist() == ref["front_s"].tolist()
+    assert g["ap"]["b"] == oracle.grid_vector(ref["ap"], fam.K, 3)
+    assert g["eo"]["b"] == oracle.grid_vector(ref["eo"], fam.K, 3)
+    assert g["ap"]["correct"] >= int(vok[-1].sum())
+    # route with the AP thresholds of the graph (host list) and with the calibrated ones
+    ids = np.arange(fam.n, dtype=np.int64)
+    logits = [torch.from_numpy(synth.logits_np(fam.seed, k, ids, 1, fam.C, fam.thr[k], "bf16")
+                               .view(np.int16)).to(dev_).view(torch.bfloat16) for k in range(fam.K)]
+    router.route(logits, thresholds=g["ap"]["t"])
+    res = router.cascade.results()
+    assert sum(r["n_acc"] for r in res) == fam.n
