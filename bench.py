@@ -56,6 +56,11 @@ def parse():
                     help="run routing stage 1 strictly after the calibration (no PDL overlap)")
     ap.add_argument("--force-dist", action="store_true",
                     help="initialise NCCL even at one GPU (exercises the sharded calibration path)")
+    ap.add_argument("--layout", default="dense", choices=["by_id", "dense"],
+                    help="by_id: stage k's logits exist for every request id and the batch "
+                         "gathers its rows; dense: stage k's logits are the dense batch of "
+                         "the requests that reach model k, in order (the model ran on that "
+                         "batch only, P:320-322)")
     ap.add_argument("--placement", default="local", choices=["local", "balanced", "p2p"],
                     help="local: every rank serves every stage (no data-path collective); "
                          "balanced: deferred requests are re-spread over all ranks after "
@@ -224,6 +229,34 @@ def committed_traffic(config: str, name: str = "r01_k1_traffic.json"):
     return rec.get("dram_bytes_per_launch") if rec.get("config") == config else None
 
 
+def dense_stage_logits(fam, router, route, val, labels, payload, rank, dev):
+    """--layout dense: run the step once (untimed) to learn which requests reach
+    each model, then regenerate stage k's logits (same keyed generator, so the
+    same values per request) as the dense batch of exactly those requests in
+    order -- what model m_k produces when it runs on its batch only.  The
+    cascade is deterministic, so every timed step routes the same batches."""
+    import torch
+    import workload
+    router.calibrate(val, labels)
+    router.route(route, payload=payload)
+    torch.cuda.synchronize()
+    counts = router.cascade.counts.cpu().tolist()
+    tdt = torch.bfloat16 if fam.dtype == "bf16" else torch.float32
+    out = [route[0]]
+    for k in range(1, fam.K):
+        nk = int(counts[k - 1][1])
+        ids = router.cascade.outs[k - 1]["next_ids"][:nk].clone() + rank * fam.n
+        x = torch.empty(max(nk, 1) * fam.L, fam.C, dtype=tdt, device=dev)
+        if nk:
+            workload.gpu_logits(x, fam, k, ids=ids, n=nk)
+        out.append(x)
+    for k in range(1, fam.K):
+        route[k] = None                    # the full-population tensors are not needed
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    return out, counts
+
+
 def make_router(fam, dev, group):
     import paper_2505_12566_b200 as hs
     from paper_2505_12566_b200.router import Router
@@ -254,12 +287,15 @@ def run_ours(args, world, rank, local):
     route, val, labels, payload = build_inputs(fam, rank, dev)
     router = make_router(fam, dev, group)
     ev = (timing_event(), timing_event())
+    dense = args.layout == "dense"
+    if dense:
+        route, dense_counts = dense_stage_logits(fam, router, route, val, labels, payload, rank, dev)
 
     def step():
         # K1 on the validation shard is the timed launch (events around it); the
         # routing stage-1 K1 then runs next to the latency-bound calibration
         router.calibrate(val, labels, time_val=ev)
-        router.route(route, payload=payload, overlap_first=not args.no_overlap)
+        router.route(route, payload=payload, overlap_first=not args.no_overlap, by_id=not dense)
 
     stream = torch.cuda.Stream(device=dev)
     torch.cuda.synchronize()
@@ -326,6 +362,8 @@ def run_ours(args, world, rank, local):
     ms = max_over_ranks(total_ms, world) / args.steps
     # cascade statistics (identical every step): reach per stage
     counts = router.cascade.counts.cpu().tolist()
+    if dense:   # the dense batches were generated for exactly these deferred sets
+        assert counts == dense_counts, "dense layout: the cascade changed between steps"
     reach = [fam.n] + [c[1] for c in counts[:-1]]
     st = int(router.status.item())
     # algorithmic bytes of one step (logits dominate): validation sweep + reach-weighted routing
@@ -355,6 +393,7 @@ def run_ours(args, world, rank, local):
                    + (f" over the top {fam.top_k} logits" if fam.top_k else ""),
                    "log2_bins": fam.log2_bins, "parallelism": f"request-sharded dp{world}",
                    "l2": "inputs larger than L2 (per-step logits working set >> 126 MB)",
+                   "logits_layout": args.layout,
                    "cuda_graph": graph is not None},
         "logits_GBps": step_bytes_all / (ms / 1e3) / 1e9,
         "logits_frac_of_peak": step_bytes_all / world / (ms / 1e3) / 1e9 / peak,
@@ -596,7 +635,7 @@ def run_e2e(args, fam, router, route, val, labels, payload, stream, world):
         if payload is not None:
             payload.copy_(host_pay, non_blocking=True)
         router.calibrate(val, labels)
-        router.route(route, payload=payload)
+        router.route(route, payload=payload, by_id=args.layout != "dense")
         cnt_host.copy_(router.cascade.counts, non_blocking=True)
         # accepted ids of every stage (the answers' request ids)
         for o, h in zip(outs, res_host):
