@@ -70,6 +70,7 @@ typedef enum { HS_SEQ_NONE = 0, HS_SEQ_MIN = 1, HS_SEQ_MEAN = 2 } hs_seq_reduce_
 
 #define HS_STATUS_NONFINITE 1u
 #define HS_STATUS_NOT_CONVERGED 2u   /* hs_fit_temperature: pass budget exhausted */
+#define HS_STATUS_TIMEOUT 4u         /* hs_forward_*: a peer did not publish within 10 s */
 
 /* ------------------------------------------------------------------------ */
 /* Confidence.                                        */
@@ -400,7 +401,9 @@ hs_status_t hs_perf_graph(const int64_t* d_correct, const int64_t* d_energy, int
  * done arrays zero-filled once; the receive buffers hold world * cap rows and
  * alternate between two sets on consecutive stages (a rank may scatter stage
  * k+1 while a peer still reads stage k's buffer); ws >= 256 bytes zero-filled
- * once (completion counter, re-armed by the kernel).  Payload rows: multiples
+ * once (completion counter, re-armed by the kernel).  The waits give up after
+ * 10 s (a peer that never publishes), OR HS_STATUS_TIMEOUT into *d_status
+ * (optional) and skip their writes, instead of hanging the GPU.  Payload rows: multiples
  * of 16 bytes, 16-byte aligned.  All calls stream-ordered, graph-capturable.
  * hs_ipc_alloc / hs_ipc_free: the one explicit device allocation of the library
  * (a whole cudaMalloc allocation, zero-filled synchronously, so that its IPC
@@ -416,8 +419,9 @@ hs_status_t hs_forward_scatter(const int64_t* ids, const void* payload, int64_t 
                                uint64_t* const* peer_done, int64_t* const* peer_recv_ids,
                                void* const* peer_recv_payload, const int32_t* dest_ranks,
                                int32_t n_dest, uint32_t epoch, int64_t* d_recv_count, void* ws,
-                               size_t ws_bytes, hs_stream_t stream);
-hs_status_t hs_forward_wait(const uint64_t* my_done, int32_t world, uint32_t epoch, hs_stream_t stream);
+                               size_t ws_bytes, uint32_t* d_status, hs_stream_t stream);
+hs_status_t hs_forward_wait(const uint64_t* my_done, int32_t world, uint32_t epoch, uint32_t* d_status,
+                            hs_stream_t stream);
 hs_status_t hs_ipc_alloc(size_t bytes, void** dptr);   /* cudaMalloc + zero fill: exportable whole allocation */
 hs_status_t hs_ipc_free(void* dptr);
 hs_status_t hs_ipc_handle(const void* dptr, void* handle /* host, 64 bytes */);

@@ -27,6 +27,7 @@ _KINDS = {"maxprob": MAXPROB, "maxprob_sq": MAXPROB_SQ, "entropy": ENTROPY}
 _REDUCES = {"none": SEQ_NONE, "min": SEQ_MIN, "mean": SEQ_MEAN}
 STATUS_NONFINITE = 1
 STATUS_NOT_CONVERGED = 2
+STATUS_TIMEOUT = 4
 
 __all__ = ["confidence", "confidence_batched", "route_compact", "cascade_step", "calibrate_thresholds",
            "calibrate_begin", "calibrate_histogram", "calibrate_select", "fit_temperature", "threshold_replay", "perf_graph", "grid_size", "grid_vector",
@@ -284,7 +285,8 @@ def forward_publish(d_count: torch.Tensor, cap: int, rank: int, peer_counts: lis
 def forward_scatter(ids: torch.Tensor, cap: int, rank: int, my_counts: torch.Tensor | int,
                     peer_done: list, peer_recv_ids: list, dest_ranks: list, epoch: int,
                     recv_count: torch.Tensor, ws: torch.Tensor, *, payload: torch.Tensor | None = None,
-                    payload_row_bytes: int = 0, peer_recv_payload: list | None = None, stream=None):
+                    payload_row_bytes: int = 0, peer_recv_payload: list | None = None,
+                    status: torch.Tensor | None = None, stream=None):
     """Write this rank's deferred ids (+ payload rows) into their destination
     ranks' receive buffers at their global positions; ``recv_count`` gets this
     rank's receive count."""
@@ -294,13 +296,15 @@ def forward_scatter(ids: torch.Tensor, cap: int, rank: int, my_counts: torch.Ten
     _abi.call("hs_forward_scatter", _p(ids), _p(payload), int(payload_row_bytes), int(cap), int(rank),
               len(peer_done), mc, _ptr_array(peer_done), _ptr_array(peer_recv_ids),
               _ptr_array(peer_recv_payload) if peer_recv_payload else None, dr, len(dest_ranks),
-              int(epoch), _p(recv_count), _p(ws), ws.numel(), _stream(stream))
+              int(epoch), _p(recv_count), _p(ws), ws.numel(), _p(status), _stream(stream))
 
 
-def forward_wait(my_done: torch.Tensor | int, world: int, epoch: int, stream=None):
-    """Wait until every rank's done flag of ``epoch`` is in this rank's array."""
+def forward_wait(my_done: torch.Tensor | int, world: int, epoch: int,
+                 status: torch.Tensor | None = None, stream=None):
+    """Wait until every rank's done flag of ``epoch`` is in this rank's array
+    (gives up after 10 s with STATUS_TIMEOUT in ``status``)."""
     md = my_done if isinstance(my_done, int) else my_done.data_ptr()
-    _abi.call("hs_forward_wait", md, int(world), int(epoch), _stream(stream))
+    _abi.call("hs_forward_wait", md, int(world), int(epoch), _p(status), _stream(stream))
 
 
 # ---------------------------------------------------------------------------

@@ -57,8 +57,8 @@ SIGNATURES = {
     "hs_perf_graph": (I32, [P, P, I64, I64, I64, I64, P, I32, P, P, P, P, P, P, SZ, P, P]),
     "hs_forward_publish": (I32, [P, I64, I32, I32, P, ctypes.c_uint32, P]),
     "hs_forward_scatter": (I32, [P, P, I64, I64, I32, I32, P, P, P, P, P, I32, ctypes.c_uint32, P, P,
-                                 SZ, P]),
-    "hs_forward_wait": (I32, [P, I32, ctypes.c_uint32, P]),
+                                 SZ, P, P]),
+    "hs_forward_wait": (I32, [P, I32, ctypes.c_uint32, P, P]),
     "hs_ipc_alloc": (I32, [SZ, P]),
     "hs_ipc_free": (I32, [P]),
     "hs_ipc_handle": (I32, [P, P]),

@@ -414,7 +414,7 @@ hs_status_t hs_forward_scatter(const int64_t* ids, const void* payload, int64_t 
                                uint64_t* const* peer_done, int64_t* const* peer_recv_ids,
                                void* const* peer_recv_payload, const int32_t* dest_ranks,
                                int32_t n_dest, uint32_t epoch, int64_t* d_recv_count, void* ws,
-                               size_t ws_bytes, hs_stream_t stream) {
+                               size_t ws_bytes, uint32_t* d_status, hs_stream_t stream) {
   if (world < 1 || world > hs::kFwdMaxWorld || rank < 0 || rank >= world)
     return fail(HS_ERR_INVALID_ARGUMENT, "rank %d / world %d out of range", rank, world);
   if (!ids || !my_counts || !peer_done || !peer_recv_ids || !d_recv_count || epoch == 0 || cap < 0)
@@ -444,16 +444,17 @@ hs_status_t hs_forward_scatter(const int64_t* ids, const void* payload, int64_t 
     d.ranks[i] = dest_ranks[i];
   }
   return cuda_check(hs::launch_fwd_scatter(ids, payload, payload_row_bytes, cap, rank, p, epoch, d,
-                                           d_recv_count, reinterpret_cast<unsigned*>(ws),
+                                           d_recv_count, reinterpret_cast<unsigned*>(ws), d_status,
                                            (cudaStream_t)stream),
                     "forward scatter kernel");
 }
 
-hs_status_t hs_forward_wait(const uint64_t* my_done, int32_t world, uint32_t epoch, hs_stream_t stream) {
+hs_status_t hs_forward_wait(const uint64_t* my_done, int32_t world, uint32_t epoch, uint32_t* d_status,
+                            hs_stream_t stream) {
   if (!my_done || world < 1 || world > hs::kFwdMaxWorld || epoch == 0)
     return fail(HS_ERR_INVALID_ARGUMENT, "my_done, 1 <= world <= %d and epoch > 0 are required", hs::kFwdMaxWorld);
   return cuda_check(hs::launch_fwd_wait(reinterpret_cast<const unsigned long long*>(my_done), world, epoch,
-                                        (cudaStream_t)stream),
+                                        d_status, (cudaStream_t)stream),
                     "forward wait kernel");
 }
 

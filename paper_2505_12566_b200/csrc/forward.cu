@@ -37,6 +37,30 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long
   asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// Spin until (flag word `p`, shifted) == epoch; gives up after kFwdTimeoutNs
+// (a peer that never publishes would otherwise hang the GPU), ORs
+// HS_STATUS_TIMEOUT into *status and returns false.
+constexpr unsigned long long kFwdTimeoutNs = 10ull * 1000 * 1000 * 1000;
+__device__ __forceinline__ bool wait_epoch(const unsigned long long* p, int shift, unsigned epoch,
+                                           unsigned long long* out, uint32_t* status) {
+  unsigned long long v = ld_acquire_sys(p);
+  const unsigned long long t0 = globaltimer_ns();
+  while ((unsigned)(v >> shift) != epoch) {
+    if (globaltimer_ns() - t0 > kFwdTimeoutNs) {
+      if (status) atomicOr(status, HS_STATUS_TIMEOUT);
+      return false;
+    }
+    __nanosleep(64);
+    v = ld_acquire_sys(p);
+  }
+  *out = v;
+  return true;
+}
 
 __global__ void fwd_publish_kernel(const int64_t* d_count, int64_t cap, int rank, const __grid_constant__ FwdPeers peers,
                                    unsigned epoch) {
@@ -56,21 +80,22 @@ __global__ void __launch_bounds__(256) fwd_scatter_kernel(const int64_t* __restr
                                                           int64_t row_vec, int rank,
                                                           const __grid_constant__ FwdPeers peers,
                                                           unsigned epoch, const __grid_constant__ FwdDest dest,
-                                                          int64_t* d_recv_count, unsigned* done_ctr) {
+                                                          int64_t* d_recv_count, unsigned* done_ctr,
+                                                          uint32_t* status) {
   pdl_start();
   __shared__ long long cnt[kFwdMaxWorld];
   __shared__ long long s_off, s_D;
+  __shared__ int s_ok;
   const int W = peers.world;
+  if (threadIdx.x == 0) s_ok = 1;
+  __syncthreads();
   if (threadIdx.x < W) {
-    const unsigned long long* f = peers.my_counts + threadIdx.x;
-    unsigned long long v = ld_acquire_sys(f);
-    while ((unsigned)(v >> 32) != epoch) {
-      __nanosleep(64);
-      v = ld_acquire_sys(f);
-    }
+    unsigned long long v = 0;
+    if (!wait_epoch(peers.my_counts + threadIdx.x, 32, epoch, &v, status)) s_ok = 0;
     cnt[threadIdx.x] = (long long)(v & 0xFFFFFFFFull);
   }
   __syncthreads();
+  if (!s_ok) return;      // timed out: nothing is written, the flag is raised
   if (threadIdx.x == 0) {
     long long off = 0, D = 0;
     for (int h = 0; h < W; ++h) {
@@ -115,11 +140,13 @@ __global__ void __launch_bounds__(256) fwd_scatter_kernel(const int64_t* __restr
   }
 }
 
-__global__ void fwd_wait_kernel(const unsigned long long* my_done, int world, unsigned epoch) {
+__global__ void fwd_wait_kernel(const unsigned long long* my_done, int world, unsigned epoch,
+                                uint32_t* status) {
   pdl_start();
   const int h = threadIdx.x;
   if (h >= world) return;
-  while ((unsigned)ld_acquire_sys(my_done + h) != epoch) __nanosleep(64);
+  unsigned long long v;
+  wait_epoch(my_done + h, 0, epoch, &v, status);
 }
 
 }  // namespace
@@ -131,17 +158,19 @@ cudaError_t launch_fwd_publish(const int64_t* d_count, int64_t cap, int rank, co
 
 cudaError_t launch_fwd_scatter(const int64_t* ids, const void* payload, int64_t row_bytes, int64_t cap,
                                int rank, const FwdPeers& p, unsigned epoch, const FwdDest& dest,
-                               int64_t* d_recv_count, unsigned* done_ctr, cudaStream_t s) {
+                               int64_t* d_recv_count, unsigned* done_ctr, uint32_t* status,
+                               cudaStream_t s) {
   const int64_t want = (cap * 32 + 255) / 256;
   int grid = (int)(want < (int64_t)num_sms() * 8 ? want : (int64_t)num_sms() * 8);
   if (grid < 1) grid = 1;
   return launch_pdl(fwd_scatter_kernel, dim3(grid), dim3(256), 0, s, ids,
                     reinterpret_cast<const uint4*>(payload), row_bytes / 16, rank, p, epoch, dest,
-                    d_recv_count, done_ctr);
+                    d_recv_count, done_ctr, status);
 }
 
-cudaError_t launch_fwd_wait(const unsigned long long* my_done, int world, unsigned epoch, cudaStream_t s) {
-  return launch_pdl(fwd_wait_kernel, dim3(1), dim3(32), 0, s, my_done, world, epoch);
+cudaError_t launch_fwd_wait(const unsigned long long* my_done, int world, unsigned epoch, uint32_t* status,
+                            cudaStream_t s) {
+  return launch_pdl(fwd_wait_kernel, dim3(1), dim3(32), 0, s, my_done, world, epoch, status);
 }
 
 }  // namespace hs

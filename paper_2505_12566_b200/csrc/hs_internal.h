@@ -225,7 +225,9 @@ cudaError_t launch_fwd_publish(const int64_t* d_count, int64_t cap, int rank, co
                                unsigned epoch, cudaStream_t s);
 cudaError_t launch_fwd_scatter(const int64_t* ids, const void* payload, int64_t row_bytes, int64_t cap,
                                int rank, const FwdPeers& p, unsigned epoch, const FwdDest& dest,
-                               int64_t* d_recv_count, unsigned* done_ctr, cudaStream_t s);
-cudaError_t launch_fwd_wait(const unsigned long long* my_done, int world, unsigned epoch, cudaStream_t s);
+                               int64_t* d_recv_count, unsigned* done_ctr, uint32_t* status,
+                               cudaStream_t s);
+cudaError_t launch_fwd_wait(const unsigned long long* my_done, int world, unsigned epoch, uint32_t* status,
+                            cudaStream_t s);
 
 }  // namespace hs

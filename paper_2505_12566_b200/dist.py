@@ -147,6 +147,7 @@ class PeerForwarder:
                     self._opened.append(int(p.value))
         self.ws = torch.zeros(256, dtype=torch.uint8, device=self.device)
         self.recv_count = torch.zeros(1, dtype=torch.int64, device=self.device)
+        self.status = torch.zeros(1, dtype=torch.int32, device=self.device)   # STATUS_TIMEOUT
         self.epoch = 0
         self._lib = lib
 
@@ -174,8 +175,9 @@ class PeerForwarder:
         forward_scatter(ids, self.cap, self.rank, self._own["counts"], self.peer["done"],
                         self.peer[f"ids{par}"], dest, self.epoch, self.recv_count, self.ws,
                         payload=payload, payload_row_bytes=self.P if payload is not None else 0,
-                        peer_recv_payload=self.peer.get(f"pay{par}"), stream=stream)
-        forward_wait(self._own["done"], self.world, self.epoch, stream=stream)
+                        peer_recv_payload=self.peer.get(f"pay{par}"), status=self.status,
+                        stream=stream)
+        forward_wait(self._own["done"], self.world, self.epoch, status=self.status, stream=stream)
         return self.recv_ids(par), self.recv_payload(par), self.recv_count
 
     def close(self):

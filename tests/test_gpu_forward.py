@@ -86,3 +86,25 @@ def test_forward_argument_errors(hs):
         hs.forward_scatter(c, 10, 0, c, [c.data_ptr()] * 2, [c.data_ptr()] * 2, [1, 1], 1, c[:1], ws)
     with pytest.raises(hs.HsError):
         hs.forward_wait(c, 9, 1)
+
+
+def test_forward_times_out_instead_of_hanging(hs):
+    """A peer that never publishes: the scatter and wait kernels give up after
+    10 s, flag STATUS_TIMEOUT and write nothing (the GPU is not hung)."""
+    dev = torch.device("cuda:0")
+    W = 2
+    counts = [torch.zeros(W, dtype=torch.int64, device=dev) for _ in range(W)]
+    done = [torch.zeros(W, dtype=torch.int64, device=dev) for _ in range(W)]
+    recv = [torch.full((8,), -7, dtype=torch.int64, device=dev) for _ in range(W)]
+    ws = torch.zeros(256, dtype=torch.uint8, device=dev)
+    st = torch.zeros(1, dtype=torch.int32, device=dev)
+    rc = torch.zeros(1, dtype=torch.int64, device=dev)
+    ids = torch.arange(4, dtype=torch.int64, device=dev)
+    cnt = torch.tensor([4], dtype=torch.int64, device=dev)
+    hs.forward_publish(cnt, 4, 0, [c.data_ptr() for c in counts], 1)      # rank 1 never publishes
+    hs.forward_scatter(ids, 4, 0, counts[0], [d.data_ptr() for d in done], [r.data_ptr() for r in recv],
+                       [0, 1], 1, rc, ws, status=st)
+    hs.forward_wait(done[0], W, 1, status=st)
+    torch.cuda.synchronize()
+    assert int(st.item()) & hs.STATUS_TIMEOUT
+    assert (recv[0] == -7).all() and (recv[1] == -7).all()
