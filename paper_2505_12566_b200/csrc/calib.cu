@@ -463,7 +463,7 @@ constexpr unsigned long long kPackMask = (1ull << kPackBits) - 1;
 
 // select_core's three passes (same arithmetic, same tie rules) on a packed
 // global histogram whose bins [lo, lo + n) sit in this thread's registers.
-template <int NT, int PMAX>
+template <int NT, int PMAX, bool SMEM = false>
 __device__ __forceinline__ void select_packed(const unsigned long long* __restrict__ g, int K,
                                               int q, int round, SelState* ss) {
   constexpr int NW = NT / 32;
@@ -478,8 +478,8 @@ __device__ __forceinline__ void select_packed(const unsigned long long* __restri
   const int lo = min(tid * per, B + 1), n = min(per, B + 1 - lo);
   unsigned long long v[PMAX];
 #pragma unroll
-  for (int i = 0; i < PMAX; ++i) v[i] = i < n ? __ldcg(g + lo + i + 1) : 0ull;
-  const unsigned long long v0 = tid == 0 ? __ldcg(g) : 0ull;   // NaN bin: never accepted
+  for (int i = 0; i < PMAX; ++i) v[i] = i < n ? (SMEM ? g[lo + i + 1] : __ldcg(g + lo + i + 1)) : 0ull;
+  const unsigned long long v0 = tid == 0 ? (SMEM ? g[0] : __ldcg(g)) : 0ull;   // NaN bin: never accepted
 #define HS_CNT(x) ((int)((x) & kPackMask))
 #define HS_CK(x) ((int)(((x) >> kPackBits) & kPackMask))
 #define HS_CKK(x) ((int)((x) >> (2 * kPackBits)))
@@ -642,6 +642,11 @@ __global__ void __launch_bounds__(kResidentThreads, 1) calib_resident_kernel(
   HS_TR("init");
   const int mup = (m + 31) & ~31;
   const bool aggregate = q < 8;      // block-uniform
+  // one CTA (small validation sets, e.g. C1): the packed bins stay in shared
+  // memory and the round needs no grid barrier and no global atomics
+  const bool solo = gridDim.x == 1;
+  unsigned long long* spk = reinterpret_cast<unsigned long long*>(
+      reinterpret_cast<unsigned char*>(sok + per_cta) + (16 - (reinterpret_cast<uintptr_t>(sok + per_cta) & 15)));
   for (int k = 0; k < K - 1; ++k) {
     unsigned long long* cur = hist3 + (size_t)(k % 3) * nb;
     unsigned long long* nxt = hist3 + (size_t)((k + 1) % 3) * nb;
@@ -682,7 +687,13 @@ __global__ void __launch_bounds__(kResidentThreads, 1) calib_resident_kernel(
     HS_TR("local");
     for (int i = tid; i < nb; i += blockDim.x) {
       const unsigned c = sh[i];
-      if (c) {       // correct counts are only taken on counted samples
+      if (solo) {
+        const unsigned long long ck = sh[nb + i], cK = sh[2 * nb + i];
+        sh[i] = 0u;
+        sh[nb + i] = 0u;
+        sh[2 * nb + i] = 0u;
+        spk[i] = (unsigned long long)c | (ck << kPackBits) | (cK << (2 * kPackBits));
+      } else if (c) {       // correct counts are only taken on counted samples
         const unsigned long long ck = sh[nb + i], cK = sh[2 * nb + i];
         sh[i] = 0u;
         sh[nb + i] = 0u;
@@ -691,6 +702,12 @@ __global__ void __launch_bounds__(kResidentThreads, 1) calib_resident_kernel(
       }
     }
     HS_TR("flush");
+    if (solo) {
+      __syncthreads();
+      select_packed<kResidentThreads, PMAX, true>(spk, K, q, k, ss);
+      HS_TR("select");
+      continue;
+    }
     grid.sync();
     HS_TR("sync");
     // every CTA selects from the summed histogram (identical results)
@@ -871,7 +888,8 @@ static cudaError_t launch_calib_resident(const float* conf, const uint8_t* corre
   if (grid > num_sms()) grid = num_sms();
   if (grid < 1) grid = 1;
   const int64_t per = (N + grid - 1) / grid;
-  const size_t smem = head + (size_t)per * (2 * (size_t)(K - 1) + 2) + 16;
+  size_t smem = head + (size_t)per * (2 * (size_t)(K - 1) + 2) + 16;
+  if (grid == 1) smem += (size_t)((1 << q) + 2) * sizeof(unsigned long long) + 16;   // packed bins (solo)
   // packed u64 bins need N < 2^21; K <= 16 correct bits per sample
   if (K > 16 || N >= (int64_t(1) << kPackBits) || q > 14 || smem > cap) return cudaSuccess;
   const int pm = q <= 9 ? 1 : q <= 11 ? 3 : q == 12 ? 5 : q == 13 ? 9 : 17;
