@@ -297,13 +297,15 @@ hs_status_t hs_calibrate_select(int32_t K, int32_t log2_bins, int32_t round, int
  * finite with 0 <= label < n_classes; -inf entries are masked classes.  Rows
  * with NaN / +inf (or all -inf) also set HS_STATUS_NONFINITE in *d_status.
  * NLL is convex in beta = 1/T; the minimiser is found by a safeguarded Newton
- * iteration on beta (one pass over the logits per iterate; ~4-6 passes),
+ * iteration on beta (one pass over the logits per iterate; with n >= 32,768
+ * rows of <= 2 KB, up to 2 warm-start Newton sweeps over every 16th row come
+ * first; then ~2-4 full passes),
  * converged when a Newton step or the bracket is below 2^-21 relative; a
  * clamp end is returned exactly.  All passes of all stage models run in ONE
  * persistent cooperative kernel launch (one CTA per SM).
  * Outputs (device): d_T[b] fp32 (NaN if no row is used), and optionally
  * d_nll[b] (fp64 mean NLL at the last temperature swept, within the
- * tolerance of d_T[b]), d_passes[b] (passes at a temperature), d_used[b].
+ * tolerance of d_T[b]), d_passes[b] (full passes at a temperature), d_used[b].
  * max_passes (1..256) bounds the passes; when a model has not converged within
  * it, d_T[b] is the last swept temperature and HS_STATUS_NOT_CONVERGED is ORed
  * into *d_status.  Requires 0 < t_lo <= t_hi < inf.  Workspace:

@@ -43,6 +43,12 @@ namespace {
 constexpr int kTfThreads = HS_TF_THREADS;
 constexpr int kTfWarps = kTfThreads / 32;
 constexpr int kTfComp = 4;              // partial sums per stage: used, nll, g, h
+// warm start: up to kTfSubPasses Newton sweeps over every kTfSubStride-th row
+// (same objective on a 1/16 sample) before the first full sweep, for stages
+// with >= kTfSubMin rows whose rows fit one chunk
+constexpr int kTfSubStride = 16;
+constexpr int kTfSubPasses = 2;
+constexpr int64_t kTfSubMin = 32768;
 
 struct TfState {
   double lo, hi, beta;      // bracket on beta = 1/T, point of the next sweep
@@ -53,6 +59,8 @@ struct TfState {
   int lo_known, hi_known;   // g(lo) < 0 / g(hi) > 0 observed (else: clamp end not yet swept)
   int done, passes, converged;
   int newton_prev;          // the last move was a Newton step
+  int mode;                 // 0: subsample warm-start sweeps, 1: first full sweep, 2: full sweeps
+  int subpasses;
 };
 
 __device__ __forceinline__ uint32_t wordq(const uint4& v, int q) {
@@ -267,6 +275,8 @@ __global__ void __launch_bounds__(kTfThreads, 1) temp_fit_kernel(const TfArgs a)
   __shared__ double wacc[kTfWarps][kMaxBatch * kTfComp];
   __shared__ double red[kMaxBatch * kTfComp];
   __shared__ int skip[kMaxBatch];
+  __shared__ int s_live[kMaxBatch], s_nl;
+  __shared__ long long s_cum[kMaxBatch + 1];
   constexpr int GPW = 32 / G;
   constexpr int CH = G * U;                              // vectors per group per chunk
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -294,6 +304,8 @@ __global__ void __launch_bounds__(kTfThreads, 1) temp_fit_kernel(const TfArgs a)
     s.used = -1;
     s.lo_known = s.hi_known = 0;
     s.newton_prev = 0;
+    s.mode = !fused ? 2 : (n >= kTfSubMin ? 0 : 1);
+    s.subpasses = 0;
     s.done = 0;
     s.passes = 0;
     s.converged = 0;
@@ -354,14 +366,29 @@ __global__ void __launch_bounds__(kTfThreads, 1) temp_fit_kernel(const TfArgs a)
   const int64_t gwarp = (int64_t)blockIdx.x * kTfWarps + warp;
   const int64_t nwarps = (int64_t)gridDim.x * kTfWarps;
   const int64_t nw = (n + GPW - 1) / GPW;                  // warp-rows per stage
-  for (int pass = 1; pass <= a.max_passes; ++pass) {
-    int live[kMaxBatch];
-    int nl = 0;
-    for (int b = 0; b < nb; ++b)
-      if (!st[b].done) live[nl++] = b;
+  const int64_t n_sub = (n + kTfSubStride - 1) / kTfSubStride;
+  const int64_t nw_sub = (n_sub + GPW - 1) / GPW;          // warp-rows of a subsample sweep
+  for (int pass = 1; pass <= a.max_passes + kTfSubPasses; ++pass) {
+    // the live stages and their warp-row offsets (identical in every thread; in
+    // shared memory to keep the lookup out of registers / local memory)
+    if (threadIdx.x == 0) {
+      int k = 0;
+      s_cum[0] = 0;
+      for (int b = 0; b < nb; ++b)
+        if (!st[b].done) {
+          s_live[k] = b;
+          s_cum[k + 1] = s_cum[k] + (st[b].mode == 0 ? nw_sub : nw);
+          ++k;
+        }
+      s_nl = k;
+    }
+    __syncthreads();
+    const int nl = s_nl;
+    const int* live = s_live;
+    const long long* cum = s_cum;
     if (nl == 0) break;
-    const bool first = fused && pass == 1;
     double* part = (pass & 1) ? part1 : part0;
+    int mode = 2;                                          // of the stage being swept
     if (lane < nb * kTfComp) wacc[warp][lane] = 0.0;     // stages this warp does not visit
     __syncwarp();
     int li = -1, b = -1;
@@ -386,9 +413,9 @@ __global__ void __launch_bounds__(kTfThreads, 1) temp_fit_kernel(const TfArgs a)
       }
       acc_u = acc_nll = acc_g = acc_h = 0.0;
     };
-    for (int64_t wr = gwarp; wr < (int64_t)nl * nw; wr += nwarps) {
+    for (int64_t wr = gwarp; wr < cum[nl]; wr += nwarps) {
       int lj = li < 0 ? 0 : li;
-      while (wr >= (int64_t)(lj + 1) * nw) ++lj;            // warp-uniform
+      while (wr >= cum[lj + 1]) ++lj;                        // warp-uniform
       if (lj != li) {
         if (li >= 0) flush();
         li = lj;
@@ -397,10 +424,13 @@ __global__ void __launch_bounds__(kTfThreads, 1) temp_fit_kernel(const TfArgs a)
         beta = st[b].beta;
         c = (float)(beta * 1.4426950408889634);             // beta * log2(e)
         c2 = f2(c, c);
+        mode = st[b].mode;
       }
+      const bool first = mode <= 1;                         // m, dy from registers
       {
-        const int64_t row = (wr - (int64_t)li * nw) * GPW + grp;
-        const bool inb = row < n;
+        const int64_t rl = (wr - cum[li]) * GPW + grp;
+        const int64_t row = mode == 0 ? rl * kTfSubStride : rl;
+        const bool inb = mode == 0 ? rl < n_sub : row < n;
         const uint4* rowp = reinterpret_cast<const uint4*>(base + (inb ? row : 0) * a.row_bytes);
         // the row's first chunk is loaded together with its row state (the
         // address does not depend on it)
@@ -421,7 +451,7 @@ __global__ void __launch_bounds__(kTfThreads, 1) temp_fit_kernel(const TfArgs a)
           bool use = false;
           if (inb && gl == 0) {
             use = row_verdict<BF16>(a, m, rowp, lab, &dy);
-            a.rowstat[(size_t)b * n + row] = use ? make_float2(m, dy) : make_float2(nanf_, 0.f);
+            if (mode == 1) a.rowstat[(size_t)b * n + row] = use ? make_float2(m, dy) : make_float2(nanf_, 0.f);
             acc_u += use ? 1.0 : 0.0;
           }
           const int leader = grp * G;
@@ -467,13 +497,31 @@ __global__ void __launch_bounds__(kTfThreads, 1) temp_fit_kernel(const TfArgs a)
     __syncthreads();
     if (threadIdx.x < nb && !st[threadIdx.x].done) {
       TfState& s = st[threadIdx.x];
-      if (first) s.used = (long long)red[threadIdx.x * kTfComp];
-      if (s.used == 0) {
-        s.done = 1;                                       // no usable row: T = NaN
+      const double* r = red + threadIdx.x * kTfComp;
+      if (s.mode == 0) {
+        // warm start on the subsample: plain Newton, clamped to the range; no
+        // convergence decision is taken on a sample
+        const double u = r[0];
+        double step = 0.0;
+        if (u > 0.0) {
+          const double g = r[2] / u, h = r[3] / u;
+          step = (h > 0.0 && isfinite(g / h)) ? g / h : 0.0;
+          s.beta = fmin(fmax(s.beta - step, a.blo0), a.bhi0);
+        }
+        if (u == 0.0 || ++s.subpasses >= kTfSubPasses || fabs(step) <= 1e-3 * s.beta) s.mode = 1;
       } else {
-        const double inv = 1.0 / (double)s.used;
-        tf_update(s, red[threadIdx.x * kTfComp + 1] * inv, red[threadIdx.x * kTfComp + 2] * inv,
-                  red[threadIdx.x * kTfComp + 3] * inv, a);
+        if (s.mode == 1) s.used = (long long)r[0];
+        s.mode = 2;
+        if (s.used == 0) {
+          s.done = 1;                                     // no usable row: T = NaN
+        } else {
+          const double inv = 1.0 / (double)s.used;
+          tf_update(s, r[1] * inv, r[2] * inv, r[3] * inv, a);
+          if (!s.done && s.passes >= a.max_passes) {      // full-sweep budget spent
+            s.T = 1.0 / s.swept;
+            s.done = 1;                                   // converged stays 0: flagged below
+          }
+        }
       }
     }
     __syncthreads();
@@ -481,7 +529,7 @@ __global__ void __launch_bounds__(kTfThreads, 1) temp_fit_kernel(const TfArgs a)
 
   if (blockIdx.x == 0 && threadIdx.x < nb) {
     TfState& s = st[threadIdx.x];
-    if (!s.done && s.passes > 0) s.T = 1.0 / s.swept;   // pass budget exhausted: last point
+    if (!s.done && s.passes > 0) s.T = 1.0 / s.swept;   // (defensive) last swept point
     if (!s.converged && s.used > 0 && a.status) atomicOr(a.status, HS_STATUS_NOT_CONVERGED);
     a.T[threadIdx.x] = (float)s.T;
     if (a.nll) a.nll[threadIdx.x] = s.nll;

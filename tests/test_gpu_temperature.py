@@ -198,3 +198,21 @@ def test_fit_pass_budget(hs):
     assert g["passes"][0] == 1 and g["status"] & 2 and g["T"][0] == 1.0
     nll1, _ = oracle.nll(x, y, 1.0)
     assert abs(g["nll"][0] - nll1) <= NLL_REL * nll1
+
+
+@pytest.mark.parametrize("dtype,C", [("bf16", 128), ("fp32", 64)])
+def test_fit_warm_start_path(hs, dtype, C):
+    """n >= 32,768 rows of <= 2 KB: the fit starts with Newton sweeps over every
+    16th row before the full sweeps; the result is still the full objective's
+    minimiser (same tolerances), for three models with different optima."""
+    n = 40000
+    xs, ys = [], None
+    for k in range(3):
+        x, y = _gauss_rows(200 + k, n, C, margin=1.0 + 1.5 * k, scale=0.4 + 0.6 * k)
+        if ys is None:
+            ys = y
+        if dtype == "bf16":
+            x = _bf16_bits(x).view(np.uint16)
+        xs.append(to_dev(x, dtype))
+    g = check_against_oracle(hs, xs, ys, C)
+    assert (g["passes"] <= 4).all(), g["passes"]
