@@ -34,6 +34,7 @@ CONFIG_TEXT = {
     "c4": "3-stage Llama-like next-token cascade, 8,192 requests x 128,256 vocab bf16 per GPU, entropy confidence, 8 KB hidden-state payload gathered",
     "c5": "5-stage ViT streaming cascade, 1,048,576 requests x 1,000 classes bf16 per GPU (8M over 8 GPUs), validation 131,072 per GPU",
     "c3k": "c3 with the Top-K (K = 10) restricted token confidence of P:420-424 (NEXT-2), MIN over 64 tokens",
+    "c3m": "c3 with the MEAN of the 64 token confidences as the sequence confidence (north_star; the paper's is MIN, P:423)",
     "c2g": "NEXT-4: threshold performance graph of the 5 C2 ViT stage models: the exhaustive q = 4 grid (18^4 = 104,976 threshold vectors) replayed on the 50,000-sample validation set per GPU, Pareto frontier, AP and EO picks",
     "c2t": "NEXT-3: temperature fitting (Eq. 1, P:384-389) of the 5 C2 ViT stage models on the 50,000-sample validation set per GPU, 1,000 classes bf16, T in [e^-4, e^4]",
 }
@@ -186,6 +187,10 @@ def family(config: str):
                                 name="c3k_t5x4_top10_bf16", top_k=10)
     if config == "c3":      # per-GPU shard of the 8-GPU T5 config
         f = synth.scaled(f, n=2048, n_val=512)
+    if config == "c3m":     # the same shard, MEAN sequence confidence
+        import dataclasses
+        f = dataclasses.replace(synth.scaled(synth.FAMILIES["c3"], n=2048, n_val=512),
+                                name="c3m_t5x4_mean_bf16", reduce=2)
     return f
 
 
@@ -391,6 +396,7 @@ def run_ours(args, world, rank, local):
                    "classes": fam.C, "seq_len": fam.L, "logits_dtype": fam.dtype,
                    "confidence": ["maxprob", "maxprob_sq", "entropy"][fam.kind]
                    + (f" over the top {fam.top_k} logits" if fam.top_k else ""),
+                   "sequence_reduce": ["none", "min", "mean"][fam.reduce],
                    "log2_bins": fam.log2_bins, "parallelism": f"request-sharded dp{world}",
                    "l2": "inputs larger than L2 (per-step logits working set >> 126 MB)",
                    "logits_layout": args.layout,
