@@ -105,3 +105,22 @@ def test_split_repeatable_and_rearmed(hs):
     for seed in (10, 11, 12):
         y = np.random.default_rng(seed).normal(size=(5, C)).astype(np.float32) * 3
         check(hs, y, "bf16", C, 1.0, 2, ws)
+
+
+@pytest.mark.parametrize("reduce", [1, 2])
+def test_split_rows_in_sequences(hs, reduce):
+    """Token rows of a few T5-like sequences (4 x 64 tokens of 32,128 classes:
+    256 rows, split path) reduced to sequence confidences (MIN / MEAN)
+    with their argmaxes, through a last-stage cascade step, vs the oracle."""
+    n, L, C = 4, 64, 32128
+    rng = np.random.default_rng(31 + reduce)
+    x = (rng.normal(size=(n * L, C)) * 1.5).astype(np.float32)
+    x[np.arange(n * L), rng.integers(0, C, size=n * L)] += 7.0
+    bits = _bf16_bits(x)
+    xt = torch.from_numpy(bits.view(np.int16)).to(dev()).view(torch.bfloat16)
+    out = hs.cascade_step(0, 1, xt, 0.0, n=n, seq_len=L, n_classes=C, temperature=1.0, reduce=reduce)
+    torch.cuda.synchronize()
+    ref = oracle.confidence(bits, n, L, C, C, 1.0, reduce=reduce)
+    conf = out["acc_conf"][:n].cpu().numpy()
+    assert np.max(np.abs(conf - ref["conf"]) / ref["conf"]) <= REL
+    assert np.array_equal(out["acc_pred"][: n * L].cpu().numpy(), ref["argmax"])
