@@ -55,6 +55,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-overlap", action="store_true",
                     help="run routing stage 1 strictly after the calibration (no PDL overlap)")
+    ap.add_argument("--native-comm", action="store_true",
+                    help="calibration all-reduce inside libhs on its own NCCL communicator "
+                         "(hs_calibrate_thresholds_comm) instead of torch.distributed")
     ap.add_argument("--force-dist", action="store_true",
                     help="initialise NCCL even at one GPU (exercises the sharded calibration path)")
     ap.add_argument("--layout", default="dense", choices=["by_id", "dense"],
@@ -262,13 +265,13 @@ def dense_stage_logits(fam, router, route, val, labels, payload, rank, dev):
     return out, counts
 
 
-def make_router(fam, dev, group):
+def make_router(fam, dev, group, native_comm: bool = False):
     import paper_2505_12566_b200 as hs
     from paper_2505_12566_b200.router import Router
     stages = [hs.StageSpec(fam.C, fam.temps[k], fam.L, fam.kind, fam.reduce, fam.top_k)
               for k in range(fam.K)]
     return Router(stages, fam.n, fam.n_val, dev, log2_bins=fam.log2_bins,
-                  payload_row_bytes=fam.payload_bytes, group=group)
+                  payload_row_bytes=fam.payload_bytes, group=group, native_comm=native_comm)
 
 
 def timing_event():
@@ -290,7 +293,7 @@ def run_ours(args, world, rank, local):
     fam = family(args.config)
     group = dist.group.WORLD if dist.is_initialized() else None
     route, val, labels, payload = build_inputs(fam, rank, dev)
-    router = make_router(fam, dev, group)
+    router = make_router(fam, dev, group, native_comm=args.native_comm)
     ev = (timing_event(), timing_event())
     dense = args.layout == "dense"
     if dense:

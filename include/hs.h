@@ -431,6 +431,36 @@ hs_status_t hs_ipc_open(const void* handle /* host, 64 bytes */, void** dptr);
 hs_status_t hs_ipc_close(void* dptr);
 
 /* ------------------------------------------------------------------------ */
+/* Request-sharded calibration across GPUs with the library's own NCCL        */
+/* communicator.                                          */
+/* ------------------------------------------------------------------------ */
+/* hs_comm_unique_id: rank 0 creates a 128-byte NCCL unique id (host) and
+ *   shares it with the other ranks (e.g. over torch.distributed).
+ * hs_comm_create: every rank joins with the shared id (collective over the
+ *   group; blocks until all ranks joined).  The library owns the handle.
+ * hs_calibrate_thresholds_comm: hs_calibrate_thresholds where conf / correct
+ *   hold THIS rank's shard of the validation set (N = local samples): per round
+ *   every rank histograms its shard, the int32 histograms are summed with an
+ *   NCCL all-reduce on `stream`, and every rank selects the identical b_k from
+ *   the global histogram (integer counts: order-independent, deterministic).
+ *   target_correct < 0: AP, tau = the GLOBAL correct count of m_K.  comm ==
+ *   NULL: single GPU (the same sweep without the all-reduce).  Outputs as
+ *   hs_calibrate_thresholds (refinement passes are not available here).
+ * NCCL is loaded with dlopen("libnccl.so.2") on the first of these calls;
+ * HS_ERR_UNSUPPORTED when it cannot be loaded. */
+typedef struct hs_comm_s* hs_comm_t;
+hs_status_t hs_comm_unique_id(void* id /* host, 128 bytes */);
+hs_status_t hs_comm_create(const void* id /* host, 128 bytes */, int32_t rank, int32_t world,
+                           int32_t device, hs_comm_t* out);
+hs_status_t hs_comm_destroy(hs_comm_t comm);
+hs_status_t hs_calibrate_thresholds_comm(const float* conf, const uint8_t* correct, int32_t K,
+                                         int64_t N, int32_t log2_bins, int64_t target_correct,
+                                         int32_t* d_bin_idx, float* d_thresholds, int64_t* d_reach,
+                                         int64_t* d_handled, int64_t* d_correct_total,
+                                         hs_comm_t comm, void* ws, size_t ws_bytes,
+                                         hs_stream_t stream);
+
+/* ------------------------------------------------------------------------ */
 /* Diagnostics.                                                              */
 /* ------------------------------------------------------------------------ */
 const char* hs_status_string(hs_status_t s);

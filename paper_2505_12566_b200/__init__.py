@@ -308,6 +308,46 @@ def forward_wait(my_done: torch.Tensor | int, world: int, epoch: int,
 
 
 # ---------------------------------------------------------------------------
+# The library's NCCL communicator and request-sharded calibration (hs_comm_*)
+# ---------------------------------------------------------------------------
+def comm_unique_id() -> bytes:
+    """A 128-byte NCCL unique id (create on rank 0, share with the group)."""
+    import ctypes
+    buf = ctypes.create_string_buffer(128)
+    _abi.call("hs_comm_unique_id", buf)
+    return bytes(buf.raw)
+
+
+def comm_create(uid: bytes, rank: int, world: int, device: int) -> int:
+    """Join the group (collective); returns the library-owned handle."""
+    import ctypes
+    h = ctypes.c_void_p()
+    _abi.call("hs_comm_create", ctypes.create_string_buffer(uid, 128), int(rank), int(world),
+              int(device), ctypes.byref(h))
+    return int(h.value)
+
+
+def comm_destroy(comm: int):
+    _abi.call("hs_comm_destroy", comm)
+
+
+def calibrate_thresholds_comm(conf: torch.Tensor, correct: torch.Tensor, comm: int | None, *,
+                              log2_bins: int = 12, target: int = -1, out: dict | None = None,
+                              ws: torch.Tensor | None = None, stream=None) -> dict:
+    """hs_calibrate_thresholds over a validation set sharded across the ranks
+    of ``comm`` (this rank's shard in conf / correct); identical b_k on every rank."""
+    _check_cuda(conf, correct)
+    K, N = int(correct.shape[0]), int(correct.shape[1])
+    out = _calib_out(K, conf.device, out)
+    if ws is None:
+        ws = calibrate_workspace(K, log2_bins, conf.device)
+    _abi.call("hs_calibrate_thresholds_comm", _p(conf), _p(correct), K, N, int(log2_bins), int(target),
+              _p(out["b"]), _p(out["t"]), _p(out["reach"]), _p(out["handled"]),
+              _p(out["correct_total"]), comm, _p(ws), ws.numel(), _stream(stream))
+    return out
+
+
+# ---------------------------------------------------------------------------
 # hs_route_compact
 # ---------------------------------------------------------------------------
 def route_compact(conf: torch.Tensor, threshold: float | torch.Tensor, *, is_last: bool = False,

@@ -493,6 +493,53 @@ hs_status_t hs_ipc_close(void* dptr) {
   return cuda_check(cudaIpcCloseMemHandle(dptr), "cudaIpcCloseMemHandle");
 }
 
+hs_status_t hs_comm_unique_id(void* id) {
+  if (!id) return fail(HS_ERR_INVALID_ARGUMENT, "id is required");
+  if (!hs::nccl_available()) return fail(HS_ERR_UNSUPPORTED, "libnccl.so.2 could not be loaded");
+  const int r = hs::nccl_unique_id(id);
+  return r ? fail(HS_ERR_CUDA, "ncclGetUniqueId: %s", hs::nccl_error(r)) : HS_OK;
+}
+
+hs_status_t hs_comm_create(const void* id, int32_t rank, int32_t world, int32_t device, hs_comm_t* out) {
+  if (!id || !out || world < 1 || rank < 0 || rank >= world || device < 0)
+    return fail(HS_ERR_INVALID_ARGUMENT, "id, out, 0 <= rank < world and device >= 0 are required");
+  if (!hs::nccl_available()) return fail(HS_ERR_UNSUPPORTED, "libnccl.so.2 could not be loaded");
+  const int r = hs::nccl_comm_create(id, rank, world, device, out);
+  return r ? fail(HS_ERR_CUDA, "ncclCommInitRank: %s", hs::nccl_error(r)) : HS_OK;
+}
+
+hs_status_t hs_comm_destroy(hs_comm_t comm) {
+  if (!comm) return fail(HS_ERR_INVALID_ARGUMENT, "comm is required");
+  const int r = hs::nccl_comm_destroy(comm);
+  return r ? fail(HS_ERR_CUDA, "ncclCommDestroy: %s", hs::nccl_error(r)) : HS_OK;
+}
+
+hs_status_t hs_calibrate_thresholds_comm(const float* conf, const uint8_t* correct, int32_t K,
+                                         int64_t N, int32_t log2_bins, int64_t target_correct,
+                                         int32_t* d_bin_idx, float* d_thresholds, int64_t* d_reach,
+                                         int64_t* d_handled, int64_t* d_correct_total,
+                                         hs_comm_t comm, void* ws, size_t ws_bytes,
+                                         hs_stream_t stream) {
+  if (!d_bin_idx || !d_thresholds || !d_reach || !d_handled || !d_correct_total)
+    return fail(HS_ERR_INVALID_ARGUMENT, "all calibration outputs are required");
+  hs_status_t st = hs_calibrate_begin(K, log2_bins, target_correct, ws, ws_bytes, stream);
+  if (st != HS_OK) return st;
+  int32_t* hist = hs_calibrate_hist_ptr(ws);
+  const size_t words = hs_calibrate_hist_bytes(log2_bins) / sizeof(int32_t);
+  for (int32_t k = 0; k < K - 1; ++k) {
+    st = hs_calibrate_histogram(conf, correct, K, N, log2_bins, k, d_bin_idx, ws, ws_bytes, stream);
+    if (st != HS_OK) return st;
+    if (comm) {
+      const int r = hs::nccl_allreduce_i32_sum(hist, words, comm, (cudaStream_t)stream);
+      if (r) return fail(HS_ERR_CUDA, "ncclAllReduce: %s", hs::nccl_error(r));
+    }
+    st = hs_calibrate_select(K, log2_bins, k, d_bin_idx, d_thresholds, d_reach, d_handled,
+                             d_correct_total, ws, ws_bytes, stream);
+    if (st != HS_OK) return st;
+  }
+  return HS_OK;
+}
+
 size_t hs_route_compact_workspace(int64_t n) { return hs::compact_ws_bytes(n); }
 
 static hs_status_t route_compact_impl(const float* conf, int64_t n, const int64_t* d_n,

@@ -8,6 +8,8 @@
 
 #include "../../include/hs.h"
 
+struct hs_comm_s;
+
 namespace hs {
 
 int num_sms();          // SM count of the current device (cached per device)
@@ -229,5 +231,13 @@ cudaError_t launch_fwd_scatter(const int64_t* ids, const void* payload, int64_t 
                                cudaStream_t s);
 cudaError_t launch_fwd_wait(const unsigned long long* my_done, int world, unsigned epoch, uint32_t* status,
                             cudaStream_t s);
+
+// ---- NCCL communicator (comm.cu; NCCL is dlopen-ed on first use) ---------------
+bool nccl_available();
+const char* nccl_error(int r);
+int nccl_unique_id(void* out128);
+int nccl_comm_create(const void* id128, int rank, int world, int device, hs_comm_s** out);
+int nccl_comm_destroy(hs_comm_s* c);
+int nccl_allreduce_i32_sum(int32_t* buf, size_t count, hs_comm_s* c, cudaStream_t s);
 
 }  // namespace hs

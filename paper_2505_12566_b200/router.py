@@ -15,14 +15,15 @@ import torch
 import dataclasses
 
 from . import (Cascade, StageSpec, _calib_out, calibrate_begin, calibrate_hist_view,
-               calibrate_histogram, calibrate_select, calibrate_thresholds,
+               calibrate_histogram, calibrate_select, calibrate_thresholds, calibrate_thresholds_comm,
                calibrate_workspace, confidence, confidence_batched, cascade_step, fit_temperature,
                perf_graph, route_compact, threshold_replay)
 
 
 class Router:
     def __init__(self, stages: list[StageSpec], n_cap: int, n_val: int, device, *,
-                 log2_bins: int = 12, payload_row_bytes: int = 0, group=None):
+                 log2_bins: int = 12, payload_row_bytes: int = 0, group=None,
+                 native_comm: bool = False):
         self.stages = stages
         self.K = len(stages)
         self.n_cap = int(n_cap)
@@ -50,6 +51,19 @@ class Router:
         self.status = torch.zeros(1, dtype=torch.int32, device=dev)
         self.cascade = Cascade(self.n_cap, stages, dev, payload_row_bytes)
         self.cascade.status = self.status
+        # native_comm: the calibration all-reduce runs inside the library on its
+        # own NCCL communicator (hs_calibrate_thresholds_comm); the unique id is
+        # shared once over the torch.distributed group
+        self.hs_comm = None
+        if native_comm:
+            from . import comm_create, comm_unique_id
+            import torch.distributed as dist
+            world = dist.get_world_size(group) if group is not None else 1
+            rank = dist.get_rank(group) if group is not None else 0
+            uid = [comm_unique_id() if rank == 0 else None]
+            if group is not None:
+                dist.broadcast_object_list(uid, src=dist.get_global_rank(group, 0), group=group)
+            self.hs_comm = comm_create(uid[0], rank, world, self.device.index or 0)
 
     # ---- offline: Alg. 1 / AP thresholds -----------------------
     def calibrate(self, val_logits: list, labels: torch.Tensor, *, target: int = -1,
@@ -78,7 +92,10 @@ class Router:
                            stream=stream)
         if time_val is not None:
             time_val[1].record()
-        if self.group is None:
+        if self.hs_comm is not None:
+            calibrate_thresholds_comm(self.vconf, self.vok, self.hs_comm, log2_bins=self.q,
+                                      target=target, out=self.cal, ws=self.cal_ws, stream=stream)
+        elif self.group is None:
             calibrate_thresholds(self.vconf, self.vok, log2_bins=self.q, target=target,
                                  out=self.cal, ws=self.cal_ws, stream=stream)
         else:

@@ -1,0 +1,62 @@
+"""The library's NCCL communicator (hs_comm_*) and the request-sharded
+calibration built on it (hs_calibrate_thresholds_comm), at world size 1 on one
+B200 (the all-reduce runs; with one rank it is the identity): bit-exact with
+the single-GPU calibration and the oracle (integer algorithm, D5)."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from workload import synth
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def hs(libhs):
+    return libhs
+
+
+@pytest.mark.parametrize("K,N,q", [(2, 4096, 12), (5, 50000, 12), (3, 777, 4)])
+def test_calibrate_comm_world1_bit_exact(hs, K, N, q):
+    dev = torch.device("cuda:0")
+    rng = np.random.default_rng(K * 1000 + N)
+    conf = rng.random((K - 1, N)).astype(np.float32)
+    conf[0, :5] = np.nan
+    ok = (rng.random((K, N)) < np.linspace(0.6, 0.9, K)[:, None]).astype(np.uint8)
+    c = torch.from_numpy(conf).to(dev)
+    o = torch.from_numpy(ok).to(dev)
+    comm = hs.comm_create(hs.comm_unique_id(), 0, 1, 0)
+    try:
+        a = hs.calibrate_thresholds_comm(c, o, comm, log2_bins=q)
+        b = hs.calibrate_thresholds_comm(c, o, None, log2_bins=q)
+        r = hs.calibrate_thresholds(c, o, log2_bins=q)
+        torch.cuda.synchronize()
+    finally:
+        hs.comm_destroy(comm)
+    ref = oracle.calibrate(conf, ok, q)
+    for out in (a, b, r):
+        assert out["b"].cpu().numpy().tolist() == ref["b"].tolist()
+        assert out["reach"].cpu().numpy().tolist() == ref["reach"].tolist()
+        assert out["handled"].cpu().numpy().tolist() == ref["handled"].tolist()
+        assert int(out["correct_total"].item()) == ref["correct_total"]
+        assert np.array_equal(out["t"].cpu().numpy(), r["t"].cpu().numpy())
+
+
+def test_router_native_comm(hs):
+    from paper_2505_12566_b200.router import Router
+    dev = torch.device("cuda:0")
+    fam = synth.scaled(synth.FAMILIES["c2"], n=2000, n_val=5000)
+    vids = np.arange(fam.n_val, dtype=np.int64) + synth.VAL_ID_BASE
+    labels = torch.from_numpy(synth.labels_np(fam.seed, vids, 1, fam.C).reshape(-1)).to(dev)
+    val = [torch.from_numpy(synth.logits_np(fam.seed, k, vids, 1, fam.C, fam.thr[k], "bf16").view(np.int16))
+           .to(dev).view(torch.bfloat16) for k in range(fam.K)]
+    stages = [hs.StageSpec(fam.C, fam.temps[k]) for k in range(fam.K)]
+    r1 = Router(stages, fam.n, fam.n_val, dev, log2_bins=fam.log2_bins)
+    r2 = Router(stages, fam.n, fam.n_val, dev, log2_bins=fam.log2_bins, native_comm=True)
+    a = r1.calibrate(val, labels)
+    b = r2.calibrate(val, labels)
+    torch.cuda.synchronize()
+    assert a["b"].cpu().tolist() == b["b"].cpu().tolist()
+    assert a["t"].cpu().tolist() == b["t"].cpu().tolist()
+    hs.comm_destroy(r2.hs_comm)
