@@ -449,6 +449,21 @@ hs_status_t hs_ipc_close(void* dptr);
  * NCCL is loaded with dlopen("libnccl.so.2") on the first of these calls;
  * HS_ERR_UNSUPPORTED when it cannot be loaded. */
 typedef struct hs_comm_s* hs_comm_t;
+/* hs_forward_nccl -- the NCCL path of the forwarding step (
+ * hs_forward_* is the peer-memory path): after hs_cascade_step on every rank,
+ * move this rank's deferred ids[0..*d_count) (+ payload rows of
+ * payload_row_bytes) so that dest_ranks[d] (distinct) receives block d of the
+ * global rank-major deferred list (as hs_forward_scatter / dist.forward_deferred).
+ * One all-gather of the counts, ONE device->host read of them (NCCL sizes are
+ * host values: this call synchronises `stream`), then grouped ncclSend/ncclRecv.
+ * recv_ids / recv_payload hold recv_cap rows; *h_recv_count (host) = rows
+ * received.  ws: hs_forward_nccl_workspace(world) bytes of device memory. */
+size_t hs_forward_nccl_workspace(int32_t world);
+hs_status_t hs_forward_nccl(const int64_t* ids, const void* payload, int64_t payload_row_bytes,
+                            const int64_t* d_count, const int32_t* dest_ranks, int32_t n_dest,
+                            int64_t* recv_ids, void* recv_payload, int64_t recv_cap,
+                            int64_t* h_recv_count, hs_comm_t comm, void* ws, size_t ws_bytes,
+                            hs_stream_t stream);
 hs_status_t hs_comm_unique_id(void* id /* host, 128 bytes */);
 hs_status_t hs_comm_create(const void* id /* host, 128 bytes */, int32_t rank, int32_t world,
                            int32_t device, hs_comm_t* out);

@@ -331,6 +331,32 @@ def comm_destroy(comm: int):
     _abi.call("hs_comm_destroy", comm)
 
 
+def forward_nccl(ids: torch.Tensor, d_count: torch.Tensor, comm: int, world: int, *,
+                 dest_ranks: list | None = None, payload: torch.Tensor | None = None,
+                 payload_row_bytes: int = 0, recv_cap: int | None = None, out: dict | None = None,
+                 ws: torch.Tensor | None = None, stream=None):
+    """NCCL forwarding of this rank's deferred list (hs_forward_nccl): returns
+    (recv_ids, recv_payload, n_recv) with n_recv read back to the host."""
+    import ctypes
+    dev = ids.device
+    dest = list(range(world)) if dest_ranks is None else list(dest_ranks)
+    cap = int(recv_cap if recv_cap is not None else world * ids.numel())
+    out = dict(out or {})
+    out.setdefault("recv_ids", torch.empty(max(cap, 1), dtype=torch.int64, device=dev))
+    if payload_row_bytes:
+        out.setdefault("recv_payload", torch.empty(max(cap, 1) * payload_row_bytes, dtype=torch.uint8, device=dev))
+    need = lib().hs_forward_nccl_workspace(world)
+    if ws is None or ws.numel() < need:
+        ws = torch.empty(need, dtype=torch.uint8, device=dev)
+    dr = (ctypes.c_int32 * len(dest))(*dest)
+    n = ctypes.c_int64()
+    _abi.call("hs_forward_nccl", _p(ids), _p(payload), int(payload_row_bytes), _p(d_count), dr, len(dest),
+              _p(out["recv_ids"]), _p(out.get("recv_payload")), cap, ctypes.byref(n), comm, _p(ws),
+              ws.numel(), _stream(stream))
+    return out["recv_ids"][: n.value], (out["recv_payload"][: n.value * payload_row_bytes]
+                                         if payload_row_bytes else None), n.value
+
+
 def calibrate_thresholds_comm(conf: torch.Tensor, correct: torch.Tensor, comm: int | None, *,
                               log2_bins: int = 12, target: int = -1, out: dict | None = None,
                               ws: torch.Tensor | None = None, stream=None) -> dict:

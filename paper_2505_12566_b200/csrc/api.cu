@@ -2,6 +2,7 @@
 //
 // Host side only: synchronous argument validation, workspace carving, variant
 // selection and stream-ordered launches.  No allocation, no synchronisation.
+#include <algorithm>
 #include <atomic>
 #include <cstdarg>
 #include <cmath>
@@ -537,6 +538,73 @@ hs_status_t hs_calibrate_thresholds_comm(const float* conf, const uint8_t* corre
                              d_correct_total, ws, ws_bytes, stream);
     if (st != HS_OK) return st;
   }
+  return HS_OK;
+}
+
+size_t hs_forward_nccl_workspace(int32_t world) { return (size_t)(world < 1 ? 1 : world) * sizeof(int64_t) + 256; }
+
+hs_status_t hs_forward_nccl(const int64_t* ids, const void* payload, int64_t payload_row_bytes,
+                            const int64_t* d_count, const int32_t* dest_ranks, int32_t n_dest,
+                            int64_t* recv_ids, void* recv_payload, int64_t recv_cap,
+                            int64_t* h_recv_count, hs_comm_t comm, void* ws, size_t ws_bytes,
+                            hs_stream_t stream) {
+  if (!comm) return fail(HS_ERR_INVALID_ARGUMENT, "comm is required");
+  const int W = hs::nccl_world(comm), rank = hs::nccl_rank(comm);
+  if (!ids || !d_count || !recv_ids || !h_recv_count || recv_cap < 0)
+    return fail(HS_ERR_INVALID_ARGUMENT, "ids, d_count, recv_ids and h_recv_count are required");
+  if (payload_row_bytes < 0 || (payload_row_bytes && (!payload || !recv_payload)))
+    return fail(HS_ERR_INVALID_ARGUMENT, "payload buffers are required when payload_row_bytes > 0");
+  if (!dest_ranks || n_dest < 1 || n_dest > W) return fail(HS_ERR_INVALID_ARGUMENT, "1 <= n_dest <= world");
+  std::vector<int> is_dest(W, -1);
+  for (int i = 0; i < n_dest; ++i) {
+    if (dest_ranks[i] < 0 || dest_ranks[i] >= W || is_dest[dest_ranks[i]] >= 0)
+      return fail(HS_ERR_INVALID_ARGUMENT, "dest_ranks must be distinct ranks of the group");
+    is_dest[dest_ranks[i]] = i;
+  }
+  if (!ws || ws_bytes < hs_forward_nccl_workspace(W))
+    return fail(HS_ERR_WORKSPACE_TOO_SMALL, "workspace %zu < %zu", ws_bytes, hs_forward_nccl_workspace(W));
+  cudaStream_t s = (cudaStream_t)stream;
+  int64_t* d_all = reinterpret_cast<int64_t*>(ws);
+  int r = hs::nccl_allgather_i64(d_count, d_all, comm, s);
+  if (r) return fail(HS_ERR_CUDA, "ncclAllGather: %s", hs::nccl_error(r));
+  std::vector<int64_t> cnt(W);
+  hs_status_t st = cuda_check(cudaMemcpyAsync(cnt.data(), d_all, W * sizeof(int64_t), cudaMemcpyDeviceToHost, s),
+                              "count read-back");
+  if (st == HS_OK) st = cuda_check(cudaStreamSynchronize(s), "count read-back");
+  if (st != HS_OK) return st;
+  int64_t D = 0;
+  for (int h = 0; h < W; ++h) D += cnt[h];
+  const int64_t R = n_dest;
+  auto lo = [&](int64_t d) { return d * D / R; };
+  // send[g][h]: rank g's global slice [off_g, off_g + D_g) intersected with rank h's block
+  auto plan = [&](int g, int h) -> int64_t {
+    if (is_dest[h] < 0) return 0;
+    int64_t off = 0;
+    for (int x = 0; x < g; ++x) off += cnt[x];
+    const int64_t d = is_dest[h], a = std::max(off, lo(d)), b = std::min(off + cnt[g], lo(d + 1));
+    return b > a ? b - a : 0;
+  };
+  std::vector<int64_t> scnt(W), soff(W), rcnt(W), roff(W);
+  int64_t so = 0, ro = 0;
+  for (int h = 0; h < W; ++h) {
+    scnt[h] = plan(rank, h);
+    soff[h] = so;
+    so += scnt[h];
+    rcnt[h] = plan(h, rank);
+    roff[h] = ro;
+    ro += rcnt[h];
+  }
+  if (ro > recv_cap) return fail(HS_ERR_INVALID_ARGUMENT, "recv_cap %lld < %lld rows to receive", (long long)recv_cap, (long long)ro);
+  r = hs::nccl_exchange(reinterpret_cast<const char*>(ids), soff.data(), scnt.data(),
+                        reinterpret_cast<char*>(recv_ids), roff.data(), rcnt.data(), 8, comm, s);
+  if (r) return fail(HS_ERR_CUDA, "NCCL send/recv (ids): %s", hs::nccl_error(r));
+  if (payload_row_bytes) {
+    r = hs::nccl_exchange(reinterpret_cast<const char*>(payload), soff.data(), scnt.data(),
+                          reinterpret_cast<char*>(recv_payload), roff.data(), rcnt.data(),
+                          payload_row_bytes, comm, s);
+    if (r) return fail(HS_ERR_CUDA, "NCCL send/recv (payload): %s", hs::nccl_error(r));
+  }
+  *h_recv_count = ro;
   return HS_OK;
 }
 

@@ -30,6 +30,11 @@ struct NcclApi {
   ncclResult_t (*all_reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                              cudaStream_t) = nullptr;
   const char* (*error_string)(ncclResult_t) = nullptr;
+  ncclResult_t (*all_gather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*group_start)() = nullptr;
+  ncclResult_t (*group_end)() = nullptr;
   bool ok = false;
 };
 
@@ -45,7 +50,13 @@ const NcclApi& nccl() {
     api.comm_destroy = reinterpret_cast<decltype(api.comm_destroy)>(dlsym(h, "ncclCommDestroy"));
     api.all_reduce = reinterpret_cast<decltype(api.all_reduce)>(dlsym(h, "ncclAllReduce"));
     api.error_string = reinterpret_cast<decltype(api.error_string)>(dlsym(h, "ncclGetErrorString"));
-    api.ok = api.get_unique_id && api.comm_init_rank && api.comm_destroy && api.all_reduce;
+    api.all_gather = reinterpret_cast<decltype(api.all_gather)>(dlsym(h, "ncclAllGather"));
+    api.send = reinterpret_cast<decltype(api.send)>(dlsym(h, "ncclSend"));
+    api.recv = reinterpret_cast<decltype(api.recv)>(dlsym(h, "ncclRecv"));
+    api.group_start = reinterpret_cast<decltype(api.group_start)>(dlsym(h, "ncclGroupStart"));
+    api.group_end = reinterpret_cast<decltype(api.group_end)>(dlsym(h, "ncclGroupEnd"));
+    api.ok = api.get_unique_id && api.comm_init_rank && api.comm_destroy && api.all_reduce &&
+             api.all_gather && api.send && api.recv && api.group_start && api.group_end;
   });
   return api;
 }
@@ -90,6 +101,32 @@ int nccl_comm_destroy(hs_comm_s* c) {
   if (a.ok && c->nc) r = (int)a.comm_destroy(c->nc);
   delete c;
   return r;
+}
+
+int nccl_world(const hs_comm_s* c) { return c->world; }
+int nccl_rank(const hs_comm_s* c) { return c->rank; }
+
+int nccl_allgather_i64(const int64_t* one, int64_t* all, hs_comm_s* c, cudaStream_t s) {
+  const NcclApi& a = nccl();
+  if (!a.ok) return -1;
+  return (int)a.all_gather(one, all, 1, ncclInt64, c->nc, s);
+}
+
+// grouped point-to-point exchange: send[h] elements from sbuf + soff[h] to rank h,
+// recv[h] elements into rbuf + roff[h] from rank h (bytes, ncclUint8)
+int nccl_exchange(const char* sbuf, const int64_t* soff, const int64_t* scnt, char* rbuf,
+                  const int64_t* roff, const int64_t* rcnt, int64_t elem_bytes, hs_comm_s* c,
+                  cudaStream_t s) {
+  const NcclApi& a = nccl();
+  if (!a.ok) return -1;
+  ncclResult_t r = a.group_start();
+  for (int h = 0; h < c->world && r == ncclSuccess; ++h) {
+    if (scnt[h]) r = a.send(sbuf + soff[h] * elem_bytes, (size_t)(scnt[h] * elem_bytes), ncclUint8, h, c->nc, s);
+    if (r == ncclSuccess && rcnt[h])
+      r = a.recv(rbuf + roff[h] * elem_bytes, (size_t)(rcnt[h] * elem_bytes), ncclUint8, h, c->nc, s);
+  }
+  const ncclResult_t e = a.group_end();
+  return (int)(r != ncclSuccess ? r : e);
 }
 
 int nccl_allreduce_i32_sum(int32_t* buf, size_t count, hs_comm_s* c, cudaStream_t s) {

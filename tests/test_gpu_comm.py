@@ -60,3 +60,25 @@ def test_router_native_comm(hs):
     assert a["b"].cpu().tolist() == b["b"].cpu().tolist()
     assert a["t"].cpu().tolist() == b["t"].cpu().tolist()
     hs.comm_destroy(r2.hs_comm)
+
+
+def test_forward_nccl_world1(hs):
+    """hs_forward_nccl at world size 1 (self send / receive through NCCL): the
+    receiver gets the whole deferred list, with payload, in order."""
+    dev = torch.device("cuda:0")
+    rng = np.random.default_rng(3)
+    conf = torch.from_numpy(rng.random(5000).astype(np.float32)).to(dev)
+    ids = torch.arange(100, 5100, dtype=torch.int64, device=dev)
+    pay = torch.from_numpy(rng.integers(0, 255, (5000, 32)).astype(np.uint8)).to(dev)
+    o = hs.route_compact(conf, 0.6, ids=ids, payload=pay)
+    comm = hs.comm_create(hs.comm_unique_id(), 0, 1, 0)
+    try:
+        rid, rpay, n = hs.forward_nccl(o["def_ids"], o["counts"][1:2], comm, 1, payload=o["def_payload"],
+                                       payload_row_bytes=32)
+        torch.cuda.synchronize()
+    finally:
+        hs.comm_destroy(comm)
+    c = conf.cpu().numpy()
+    want = np.flatnonzero(~(c >= np.float32(0.6))) + 100
+    assert n == len(want) and np.array_equal(rid.cpu().numpy(), want)
+    assert np.array_equal(rpay.cpu().numpy().reshape(n, 32), pay.cpu().numpy()[want - 100])
