@@ -41,7 +41,7 @@ def test_peer_forward_virtual_ranks(hs, world, dest, P):
     recv_pay = [torch.zeros(world * cap * max(P, 16), dtype=torch.uint8, device=dev) for _ in range(world)]
     wss = [torch.zeros(256, dtype=torch.uint8, device=dev) for _ in range(world)]
     rcnt = [torch.zeros(1, dtype=torch.int64, device=dev) for _ in range(world)]
-    for epoch, t in ((1, 0.6), (2, 0.25), (3, 0.97)):
+    for epoch, t in ((1, 0.6), (2, 0.25), (3, 0.97), (4, 0.0), (5, 0.5)):
         outs = []
         for g in range(world):
             lo, hi = bounds[g], bounds[g + 1]
