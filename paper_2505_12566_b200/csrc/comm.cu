@@ -84,9 +84,12 @@ int nccl_comm_create(const void* id_bytes, int rank, int world, int device, hs_c
   if (!a.ok) return -1;
   ncclUniqueId id;
   memcpy(&id, id_bytes, sizeof id);
+  int prev = 0;
+  cudaGetDevice(&prev);                      // NCCL binds the communicator to the current device
   cudaSetDevice(device);
   hs_comm_s* c = new hs_comm_s{nullptr, rank, world, device};
   const ncclResult_t r = a.comm_init_rank(&c->nc, world, id, rank);
+  cudaSetDevice(prev);                       // the caller's current device is unchanged
   if (r != ncclSuccess) {
     delete c;
     return (int)r;
