@@ -181,7 +181,12 @@ const char* hs_build_info(void) {
   return "libhs: sm_100a (compute_100a), nvcc " HS_STR(__CUDACC_VER_MAJOR__) "." HS_STR(__CUDACC_VER_MINOR__);
 }
 
-size_t hs_confidence_workspace(int64_t n, int32_t seq_len) { return conf_ws(n, seq_len); }
+// mandatory part (token rows of sequences) + the optional split-row region
+size_t hs_confidence_workspace(int64_t n, int32_t seq_len) {
+  if (n < 0) n = 0;
+  const size_t split = hs::split_ws_bytes(n * (int64_t)(seq_len < 1 ? 1 : seq_len));
+  return split ? align_up(conf_ws(n, seq_len), 256) + split : conf_ws(n, seq_len);
+}
 
 hs_status_t hs_confidence(const void* logits, hs_dtype_t dtype, int64_t n, int32_t seq_len,
                           int64_t n_classes, int64_t row_stride, const int64_t* row_index,
@@ -212,6 +217,15 @@ hs_status_t hs_confidence_topk(const void* logits, hs_dtype_t dtype, int64_t n, 
   hs::ConfArgs a = make_conf_args(logits, dtype, n, seq_len, n_classes, row_stride, row_index, d_n,
                                   temperature, kind);
   a.top_k = top_k;
+  {  // optional split-row region: used when the caller's workspace has room for it;
+     // its arrival counters are zeroed by the launcher (no zero-fill contract here)
+    const size_t base = align_up(conf_ws(n, seq_len), 256);
+    const size_t split = hs::split_ws_bytes(n * (int64_t)seq_len);
+    if (split && ws && ws_bytes >= base + split) {
+      a.split_ws = reinterpret_cast<char*>(ws) + base;
+      a.split_zero = 1;
+    }
+  }
   return run_confidence_args(a, dtype, reduce, conf, argmax, labels, correct, ws, d_status,
                              (cudaStream_t)stream);
 }

@@ -1546,6 +1546,10 @@ bool launch_split(const ConfArgs& a, int64_t rows, cudaStream_t s, cudaError_t* 
                                                   (size_t)kSplitMaxRows * sizeof(unsigned));
   unsigned* arrive = reinterpret_cast<unsigned*>(a.split_ws);
   const int64_t warps = rows * nseg;
+  if (a.split_zero) {
+    *err = cudaMemsetAsync(arrive, 0, (size_t)rows * sizeof(unsigned), s);
+    if (*err != cudaSuccess) return true;
+  }
   *err = launch_pdl(conf_split_kernel<BF16, ENTROPY, NV>, dim3((unsigned)((warps + 7) / 8)), dim3(256), 0,
                     s, a, nseg, segch, parts, arrive);
   return true;

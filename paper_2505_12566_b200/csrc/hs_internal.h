@@ -75,6 +75,7 @@ struct ConfArgs {
   // K1e split rows (small batches of long rows): zero-filled-once workspace of
   // split_ws_bytes(rows) bytes, or NULL (no split)
   void* split_ws;
+  int split_zero;          // 1: zero the arrival counters before the launch
 };
 constexpr int kSplitMaxRows = 2048;     // the split path serves batches up to this many rows
 constexpr int kSplitMaxSeg = 64;        // segments per row

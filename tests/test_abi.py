@@ -40,7 +40,8 @@ def test_workspace_queries_are_pure(libhs):
     # one 8-byte look-back descriptor per 2,048-item tile
     assert lib.hs_route_compact_workspace(2048) == lib.hs_route_compact_workspace(1)
     assert lib.hs_route_compact_workspace(2049) == lib.hs_route_compact_workspace(2048) + 8
-    assert lib.hs_confidence_workspace(100, 1) == 0
+    assert lib.hs_confidence_workspace(3000, 1) == 0         # no token rows, no split region
+    assert lib.hs_confidence_workspace(100, 1) > 0           # optional split-row region (<= 2,048 rows)
     assert lib.hs_confidence_workspace(100, 64) >= 100 * 64 * 5
     assert lib.hs_calibrate_workspace(5, 12) >= 3 * (4096 + 2) * 4
     assert lib.hs_calibrate_workspace(5, 15) == 0

@@ -585,7 +585,11 @@ def test_confidence_batched_equals_per_stage(hs, key, n_val):
                             reduce=fam.reduce, labels=lab_d)
         torch.cuda.synchronize()
         sl = slice(k * n_val, (k + 1) * n_val)
-        assert torch.equal(got["conf"][sl], one["conf"])
+        # one launch per stage may take the split-row path for a few long rows
+        # (another reduction order): equal within the K1 tolerance, not bitwise
+        g1, o1 = got["conf"][sl].cpu().numpy(), one["conf"].cpu().numpy()
+        assert np.array_equal(np.isnan(g1), np.isnan(o1))
+        assert np.allclose(g1, o1, rtol=REL, atol=0, equal_nan=True)
         assert torch.equal(got["correct"][sl], one["correct"])
         assert torch.equal(got["argmax"][k * n_val * fam.L:(k + 1) * n_val * fam.L], one["argmax"])
         ref = oracle.confidence(bits[k], n_val, fam.L, fam.C, fam.C, fam.temps[k], kind=fam.kind,

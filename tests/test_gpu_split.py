@@ -124,3 +124,21 @@ def test_split_rows_in_sequences(hs, reduce):
     conf = out["acc_conf"][:n].cpu().numpy()
     assert np.max(np.abs(conf - ref["conf"]) / ref["conf"]) <= REL
     assert np.array_equal(out["acc_pred"][: n * L].cpu().numpy(), ref["argmax"])
+
+
+def test_split_through_hs_confidence(hs):
+    """hs_confidence with its full workspace (not zero-filled: torch.empty) takes
+    the split-row path for a few long rows; results vs the oracle, repeatable."""
+    C = 128256
+    rng = np.random.default_rng(41)
+    for n, kind in ((1, 2), (3, 0), (17, 1)):
+        x = rng.normal(size=(n, C)).astype(np.float32) * 2
+        bits = _bf16_bits(x)
+        xt = torch.from_numpy(bits.view(np.int16)).to(dev()).view(torch.bfloat16)
+        ws = torch.full((hs.lib().hs_confidence_workspace(n, 1),), 0xAB, dtype=torch.uint8, device=dev())
+        for _ in range(2):
+            r = hs.confidence(xt, temperature=1.3, kind=kind, ws=ws)
+            torch.cuda.synchronize()
+            ref = oracle.confidence(bits, n, 1, C, C, 1.3, kind=kind)
+            assert np.max(np.abs(r["conf"].cpu().numpy() - ref["conf"]) / ref["conf"]) <= REL
+            assert np.array_equal(r["argmax"].cpu().numpy(), ref["argmax"])
