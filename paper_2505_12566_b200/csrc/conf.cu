@@ -511,7 +511,10 @@ __global__ void __launch_bounds__(256, (NV <= 8 ? 2 : 1)) conf_warp_kernel(const
 #define HS_TOPK_U 4
 #endif
 constexpr int kTopkU = HS_TOPK_U;          // vectors per lane per chunk
-constexpr int kTopkPB = 8 * kTopkU + 8;    // candidate slots per lane (>= one chunk's elements + slack)
+#ifndef HS_TOPK_SLACK
+#define HS_TOPK_SLACK 8
+#endif
+constexpr int kTopkPB = 8 * kTopkU + HS_TOPK_SLACK;   // candidate slots per lane (>= one chunk's elements + slack)
 
 __device__ __forceinline__ uint32_t f_order(float f) {   // monotone float -> u32
   const uint32_t u = __float_as_uint(f);
@@ -628,7 +631,11 @@ __global__ void __launch_bounds__(256, kTopkU <= 4 ? 3 : 2) conf_topk_kernel(con
         }
         lst = wt;
       }
+#ifdef HS_EXP_TOPK_NOCAND
+      if (false) {                        // timing experiment only: no candidates (wrong results)
+#else
       if (lmx > wt) {                     // rare: append this lane's elements > wt
+#endif
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           const float vm = BF16 ? fmaxf(bf_lo(wv[u]), bf_hi(wv[u])) : __uint_as_float(wv[u]);
@@ -643,7 +650,10 @@ __global__ void __launch_bounds__(256, kTopkU <= 4 ? 3 : 2) conf_topk_kernel(con
       }
       // merge as soon as K candidates are buffered (raises wt early, so later
       // chunks rarely have any) or when a column could overflow in the next chunk
-      if (__reduce_add_sync(0xFFFFFFFFu, (unsigned)pn) >= (unsigned)K ||
+#ifndef HS_TOPK_MERGE_AT
+#define HS_TOPK_MERGE_AT 8     // merge once 8K candidates are buffered (A/B: 1 -> 0.72, 4 -> 0.80, 8 -> 0.80 of peak, fastest step)
+#endif
+      if (__reduce_add_sync(0xFFFFFFFFu, (unsigned)pn) >= (unsigned)(HS_TOPK_MERGE_AT * K) ||
           __any_sync(0xFFFFFFFFu, pn > kTopkPB - 8 * kTopkU)) {
         __syncwarp();
         lst = topk_merge(lst, col, pn, K, lane);

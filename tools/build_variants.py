@@ -13,6 +13,12 @@ VARIANTS = {
     "tf768": ["HS_TF_THREADS=768"],      # temperature fit: 24 warps/SM, 85 registers
     "tf1024": ["HS_TF_THREADS=1024"],    # temperature fit: 32 warps/SM, 64 registers
     "topk8": ["HS_TOPK_U=8"],            # Top-K confidence: 8 vectors per lane per chunk
+    "topknocand": ["HS_EXP_TOPK_NOCAND"],  # Top-K timing bound without candidate handling
+    "topkm2": ["HS_TOPK_MERGE_AT=2"],    # Top-K: merge when 2K candidates are buffered
+    "topkm4": ["HS_TOPK_MERGE_AT=4"],    # ... 4K
+    "topkm8": ["HS_TOPK_MERGE_AT=8"],
+    "topkm4s40": ["HS_TOPK_MERGE_AT=4", "HS_TOPK_SLACK=40"],   # + 40 more buffered slots per lane
+    "topkm8s40": ["HS_TOPK_MERGE_AT=8", "HS_TOPK_SLACK=40"],
 }
 
 if __name__ == "__main__":
