@@ -969,8 +969,8 @@ def oracle_inputs(fam, frac_n: int, frac_val: int):
     ids = np.arange(frac_n, dtype=np.int64)
     vids = np.arange(frac_val, dtype=np.int64) + synth.VAL_ID_BASE
     lab = synth.labels_np(fam.seed, vids, fam.L, fam.C).reshape(-1)
-    vl = [synth.logits_np(fam.seed, k, vids, fam.L, fam.C, fam.thr[k], fam.dtype) for k in range(K)]
-    rl = [synth.logits_np(fam.seed, k, ids, fam.L, fam.C, fam.thr[k], fam.dtype) for k in range(K)]
+    vl = [synth.fam_logits_np(fam, k, vids, fam.dtype, L=fam.L, C=fam.C) for k in range(K)]
+    rl = [synth.fam_logits_np(fam, k, ids, fam.dtype, L=fam.L, C=fam.C) for k in range(K)]
     return {"n": frac_n, "v": frac_val, "lab": lab, "vl": vl, "rl": rl}
 
 
@@ -1076,7 +1076,7 @@ def run_reference_temperature(args, world):
     m = 128
     while True:
         lab = synth.labels_np(fam.seed, vids[:m], 1, fam.C).reshape(-1)
-        rows = [synth.logits_np(fam.seed, k, vids[:m], 1, fam.C, fam.thr[k], "bf16") for k in range(fam.K)]
+        rows = [synth.fam_logits_np(fam, k, vids[:m], "bf16", L=1, C=fam.C) for k in range(fam.K)]
         t = time.perf_counter()
         for k in range(fam.K):
             oracle.fit_temperature(rows[k], lab, n_classes=fam.C)
@@ -1120,7 +1120,7 @@ def run_reference_graph(args, world):
     conf = np.empty((K - 1, n))
     ok = np.empty((K, n), np.uint8)
     for k in range(K):
-        bits = synth.logits_np(fam.seed, k, vids, 1, fam.C, fam.thr[k], "bf16")
+        bits = synth.fam_logits_np(fam, k, vids, "bf16", L=1, C=fam.C)
         r = oracle.confidence(bits, n, 1, fam.C, fam.C, fam.temps[k], labels=lab)
         ok[k] = r["correct"]
         if k < K - 1:

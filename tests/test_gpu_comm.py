@@ -49,7 +49,7 @@ def test_router_native_comm(hs):
     fam = synth.scaled(synth.FAMILIES["c2"], n=2000, n_val=5000)
     vids = np.arange(fam.n_val, dtype=np.int64) + synth.VAL_ID_BASE
     labels = torch.from_numpy(synth.labels_np(fam.seed, vids, 1, fam.C).reshape(-1)).to(dev)
-    val = [torch.from_numpy(synth.logits_np(fam.seed, k, vids, 1, fam.C, fam.thr[k], "bf16").view(np.int16))
+    val = [torch.from_numpy(synth.fam_logits_np(fam, k, vids, "bf16", L=1, C=fam.C).view(np.int16))
            .to(dev).view(torch.bfloat16) for k in range(fam.K)]
     stages = [hs.StageSpec(fam.C, fam.temps[k]) for k in range(fam.K)]
     r1 = Router(stages, fam.n, fam.n_val, dev, log2_bins=fam.log2_bins)

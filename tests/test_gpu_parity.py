@@ -68,7 +68,7 @@ def run_conf(hs, x, fam_like, n, L, C, T, kind, reduce, labels=None, row_index=N
 def check_family(hs, fam, n, kinds=None, stride_pad=0, T=None):
     ids = np.arange(n, dtype=np.int64) * 7 + 3
     L, C = fam.L, fam.C
-    bits = synth.logits_np(fam.seed, 0, ids, L, C, fam.thr[0], fam.dtype)
+    bits = synth.fam_logits_np(fam, 0, ids, fam.dtype, L=L, C=C)
     lab = synth.labels_np(fam.seed, ids, L, C).reshape(-1)
     eb = 2 if fam.dtype == "bf16" else 4
     stride = C + stride_pad
@@ -157,7 +157,7 @@ def test_conf_adversarial_rows(hs):
 def test_conf_row_index_and_dynamic_n(hs):
     fam = synth.FAMILIES["c2"]
     n_all = 5000
-    bits = synth.logits_np(fam.seed, 1, np.arange(n_all), 1, fam.C, fam.thr[1], "bf16")
+    bits = synth.fam_logits_np(fam, 1, np.arange(n_all), "bf16", L=1, C=fam.C)
     x = to_dev_bits(bits, "bf16")
     ri = np.sort(np.random.default_rng(0).choice(n_all, 1234, replace=False))
     r, _ = run_conf(hs, x, fam, len(ri), 1, fam.C, 1.3, 0, 0, row_index=ri)
@@ -175,12 +175,12 @@ def test_conf_row_index_and_dynamic_n(hs):
 
 def test_gpu_generator_matches_numpy(hs):
     import workload
-    for key in ("c1", "c2", "c3", "c4"):
+    for key in ("c1", "c2", "c3", "c4", "c5"):
         fam = synth.FAMILIES[key]
         L = min(fam.L, 3)
         f = synth.scaled(fam, L=L)
         ids = np.array([0, 1, 5, 77, 1 << 33], np.int64)
-        want = synth.logits_np(f.seed, 1, ids, L, f.C, f.thr[1], f.dtype)
+        want = synth.fam_logits_np(f, 1, ids, f.dtype, L=L, C=f.C)
         tdt = torch.bfloat16 if f.dtype == "bf16" else torch.float32
         out = torch.empty(len(ids) * L, f.C, dtype=tdt, device=dev())
         workload.gpu_logits(out, f, 1, ids=torch.from_numpy(ids).to(dev()))
@@ -296,7 +296,7 @@ def test_cascade_vs_oracle(hs, key, n):
     ids = np.arange(n, dtype=np.int64)
     logits, conf_o = [], []
     for k in range(K):
-        bits = synth.logits_np(fam.seed, k, ids, fam.L, fam.C, fam.thr[k], fam.dtype)
+        bits = synth.fam_logits_np(fam, k, ids, fam.dtype, L=fam.L, C=fam.C)
         logits.append(to_dev_bits(bits, fam.dtype))
         conf_o.append(oracle.confidence(bits, n, fam.L, fam.C, fam.C, fam.temps[k], kind=fam.kind,
                                         reduce=fam.reduce)["conf"])
@@ -387,7 +387,7 @@ def _gpu_val(hs, fam, n_val):
     vok = torch.empty(K, n_val, dtype=torch.uint8, device=dev())
     oconf = np.empty((K - 1, n_val))
     for k in range(K):
-        bits = synth.logits_np(fam.seed, k, vids, fam.L, fam.C, fam.thr[k], fam.dtype)
+        bits = synth.fam_logits_np(fam, k, vids, fam.dtype, L=fam.L, C=fam.C)
         x = to_dev_bits(bits, fam.dtype)
         r = hs.confidence(x, n=n_val, seq_len=fam.L, temperature=fam.temps[k], kind=fam.kind,
                           reduce=fam.reduce, labels=lab_d)
@@ -575,7 +575,7 @@ def test_confidence_batched_equals_per_stage(hs, key, n_val):
     vids = np.arange(n_val, dtype=np.int64) + synth.VAL_ID_BASE
     lab = synth.labels_np(fam.seed, vids, fam.L, fam.C).reshape(-1)
     lab_d = torch.from_numpy(lab).to(dev())
-    bits = [synth.logits_np(fam.seed, k, vids, fam.L, fam.C, fam.thr[k], fam.dtype) for k in range(fam.K)]
+    bits = [synth.fam_logits_np(fam, k, vids, fam.dtype, L=fam.L, C=fam.C) for k in range(fam.K)]
     xs = [to_dev_bits(b, fam.dtype) for b in bits]
     got = hs.confidence_batched(xs, fam.temps, n=n_val, seq_len=fam.L, kind=fam.kind,
                                 reduce=fam.reduce, labels=lab_d)
@@ -659,7 +659,7 @@ def test_skip_cascade_vs_oracle(hs, mode, key, n):
     ids = np.arange(n, dtype=np.int64)
     logits, conf_o = [], []
     for k in range(K):
-        bits = synth.logits_np(fam.seed, k, ids, fam.L, fam.C, fam.thr[k], fam.dtype)
+        bits = synth.fam_logits_np(fam, k, ids, fam.dtype, L=fam.L, C=fam.C)
         logits.append(to_dev_bits(bits, fam.dtype))
         conf_o.append(oracle.confidence(bits, n, fam.L, fam.C, fam.C, fam.temps[k], kind=fam.kind,
                                         reduce=fam.reduce)["conf"])
@@ -773,8 +773,7 @@ def test_topk_generation_sequences_vs_oracle(hs):
     fam = synth.FAMILIES["c3"]
     n = 6
     ids = np.array([5, 0, 17, 3, 9, 11], np.int64)
-    bits = synth.logits_np(fam.seed, 1, np.arange(18, dtype=np.int64), fam.L, fam.C, fam.thr[1],
-                           fam.dtype)
+    bits = synth.fam_logits_np(fam, 1, np.arange(18, dtype=np.int64))
     x = to_dev_bits(bits, fam.dtype)
     lab = synth.labels_np(fam.seed, np.arange(18, dtype=np.int64), fam.L, fam.C).reshape(-1)
     for K, reduce in ((10, oracle.SEQ_MIN), (4, oracle.SEQ_MEAN)):

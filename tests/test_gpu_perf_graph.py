@@ -111,7 +111,7 @@ def test_c2_validation_exhaustive_grid_sampled(hs):
     lab = torch.from_numpy(synth.labels_np(fam.seed, vids, 1, fam.C).reshape(-1)).to(dev())
     xs = []
     for k in range(fam.K):
-        bits = synth.logits_np(fam.seed, k, vids, 1, fam.C, fam.thr[k], "bf16")
+        bits = synth.fam_logits_np(fam, k, vids, "bf16", L=1, C=fam.C)
         xs.append(torch.from_numpy(bits.view(np.int16)).to(dev()).view(torch.bfloat16))
     r = hs.confidence_batched(xs, fam.temps, labels=lab)
     conf = r["conf"].view(fam.K, n)[: fam.K - 1].cpu().numpy()
@@ -175,7 +175,7 @@ def test_router_offline_flow(hs):
     dev_ = dev()
     vids = np.arange(fam.n_val, dtype=np.int64) + synth.VAL_ID_BASE
     lab = synth.labels_np(fam.seed, vids, 1, fam.C).reshape(-1)
-    vbits = [synth.logits_np(fam.seed, k, vids, 1, fam.C, fam.thr[k], "bf16") for k in range(fam.K)]
+    vbits = [synth.fam_logits_np(fam, k, vids, "bf16", L=1, C=fam.C) for k in range(fam.K)]
     val = [torch.from_numpy(b.view(np.int16)).to(dev_).view(torch.bfloat16) for b in vbits]
     labels = torch.from_numpy(lab).to(dev_)
     router = Router([hs.StageSpec(fam.C, 1.0) for _ in range(fam.K)], fam.n, fam.n_val, dev_,
@@ -202,7 +202,7 @@ def test_router_offline_flow(hs):
     assert g["ap"]["correct"] >= int(vok[-1].sum())
     # route with the AP thresholds of the graph (host list) and with the calibrated ones
     ids = np.arange(fam.n, dtype=np.int64)
-    logits = [torch.from_numpy(synth.logits_np(fam.seed, k, ids, 1, fam.C, fam.thr[k], "bf16")
+    logits = [torch.from_numpy(synth.fam_logits_np(fam, k, ids, "bf16", L=1, C=fam.C)
                                .view(np.int16)).to(dev_).view(torch.bfloat16) for k in range(fam.K)]
     router.route(logits, thresholds=g["ap"]["t"])
     res = router.cascade.results()

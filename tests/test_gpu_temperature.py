@@ -101,7 +101,7 @@ def test_fit_c2_validation_stages(hs):
     n = 3000
     vids = np.arange(n, dtype=np.int64) + synth.VAL_ID_BASE
     labels = synth.labels_np(fam.seed, vids, 1, fam.C).reshape(-1)
-    xs = [to_dev(synth.logits_np(fam.seed, k, vids, 1, fam.C, fam.thr[k], "bf16"), "bf16")
+    xs = [to_dev(synth.fam_logits_np(fam, k, vids, "bf16", L=1, C=fam.C), "bf16")
           for k in range(fam.K)]
     g = check_against_oracle(hs, xs, labels, fam.C)
     assert (g["passes"] <= 12).all(), g["passes"]

@@ -37,7 +37,7 @@ def test_marginal_accuracy_and_overlap():
     lab = synth.labels_np(fam.seed, ids, 1, fam.C)[:, 0]
     accs = []
     for k in range(fam.K):
-        x = synth.logits_np(fam.seed, k, ids, 1, fam.C, fam.thr[k], "fp32")
+        x = synth.fam_logits_np(fam, k, ids, "fp32", L=1, C=fam.C)
         accs.append(np.argmax(x, axis=1) == lab)
     for k, a in enumerate(fam.acc):
         assert abs(accs[k].mean() - a) < 0.03
@@ -57,3 +57,23 @@ def test_token_sequences_one_wrong_token():
 def test_accuracy_threshold_monotone():
     t = [synth.accuracy_threshold(a) for a in (0.0, 0.1, 0.3, 0.5, 0.8, 0.95, 1.0)]
     assert t == sorted(t) and t[0] == 0 and t[-1] == 65536 + 32768
+
+
+def test_margin_profiles_exact_in_bf16():
+    """Winner codes stay within 8 significant bits (|code| <= 255), so the
+    values code * 2^-4 are exact in bf16 for every profile in use."""
+    for m in {f.margin for f in synth.FAMILIES.values()}:
+        rb, rm1, rm2, wb, wm, cs, ccap = m
+        assert rb + rm1 + rm2 + (ccap if cs > 0 else 0) <= 255 and wb + wm <= 255
+        assert min(rb, wb) >= 0
+
+
+def test_vit_margin_confidence_grows_with_slack():
+    """VIT_MARGIN: a right answer far from the accuracy boundary gets a larger
+    winner code than one near it; wrong answers do not depend on slack."""
+    ok = np.array([True, True, False, False])
+    slack = np.array([0, 40000, 0, 40000], np.int64)
+    z = np.zeros(4, np.int64)
+    c = synth.winner_code(ok, slack, z, z, synth.VIT_MARGIN)
+    assert c[1] - c[0] == min(40000 >> synth.VIT_MARGIN[5], synth.VIT_MARGIN[6])
+    assert c[2] == c[3] == synth.VIT_MARGIN[3]

@@ -10,7 +10,7 @@ import ctypes
 import os
 import threading
 
-from .synth import FAMILIES, VAL_ID_BASE, Family, labels_np, logits_np, scaled  # noqa: F401
+from .synth import FAMILIES, VAL_ID_BASE, Family, fam_logits_np, labels_np, logits_np, scaled  # noqa: F401
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB = os.path.join(_HERE, "libhs_synth.so")
@@ -27,7 +27,7 @@ def _synth_lib():
             L = ctypes.CDLL(_LIB)
             P, I64, I32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32
             L.hs_synth_logits.argtypes = [P, I32, P, I64, I64, I32, I64, I64, I32, ctypes.c_uint32,
-                                          I64, I32, P]
+                                          I64, I32, P, P]
             L.hs_synth_logits.restype = I32
             L.hs_synth_labels.argtypes = [P, P, I64, I64, I32, I64, ctypes.c_uint32, P]
             L.hs_synth_labels.restype = I32
@@ -43,9 +43,10 @@ def gpu_logits(out, fam: Family, stage: int, *, ids=None, id_base: int = 0, n: i
     n = int(n if n is not None else (ids.numel() if ids is not None else out.shape[0] // fam.L))
     dtype = 1 if out.dtype == torch.bfloat16 else 0
     s = (stream or torch.cuda.current_stream()).cuda_stream
+    mg = (ctypes.c_int32 * 7)(*fam.margin)
     rc = _synth_lib().hs_synth_logits(out.data_ptr(), dtype, None if ids is None else ids.data_ptr(),
                                       int(id_base), n, fam.L, fam.C, out.stride(0), int(stage),
-                                      fam.seed & 0xFFFFFFFF, fam.thr[stage], scale_log2, s)
+                                      fam.seed & 0xFFFFFFFF, fam.thr[stage], scale_log2, mg, s)
     if rc != 0:
         raise RuntimeError(f"hs_synth_logits failed: cuda error {rc}")
     return out

@@ -21,8 +21,11 @@ both implementations agree bit for bit):
   marginal accuracy a_k (Table II).  Overlap across stages is
   therefore "not strictly subset" (P:263-269).
 * the winning class (y if meant right, else a random other class) gets code
-  60 + U[0,128) + U[0,64) (right) or 60 + U[0,64) (wrong): confident answers
-  are more often right.  Token models (L > 1): a wrong sequence has one
+  rb + U[0,rm1] + U[0,rm2] (+ min(slack >> cs, ccap) when cs > 0, slack =
+  thr_k - d - e_k: requests far from the model's accuracy boundary are answered
+  more confidently) when right, wb + U[0,wm] when wrong: confident answers are
+  more often right.  Legacy profile (60,127,63,60,63,0,0); ViT families
+  use VIT_MARGIN, tuned toward Table III's handled fractions.  Token models (L > 1): a wrong sequence has one
   wrong, low-margin token.
 * value = code * 2^-scale_log2, exactly representable in bf16 and fp32.
   Whether the model is actually right is decided by the router's own argmax.
@@ -103,8 +106,25 @@ def labels_np(seed: int, ids, L: int, C: int) -> np.ndarray:
     return (mix32(rq ^ mix32(t + np.uint32(0x01000193))) % np.uint32(C)).astype(np.int32)
 
 
+LEGACY_MARGIN = (60, 127, 63, 60, 63, 0, 0)
+
+
+def winner_code(ok, slack, m1, m2, margin):
+    """Code of the winning class (numpy, int64 arrays).  margin = (rb, rm1, rm2,
+    wb, wm, cs, ccap): a right token gets rb + (m1 & rm1) + (m2 & rm2) plus, when
+    cs > 0, min(max(slack, 0) >> cs, ccap) -- the further the request is from
+    the model's accuracy boundary (slack = thr - d - e), the more confident the
+    right answer; a wrong token gets wb + (m1 & wm).  Codes stay <= 255 so the
+    values are exact in bf16."""
+    rb, rm1, rm2, wb, wm, cs, ccap = margin
+    right = rb + (m1 & rm1) + (m2 & rm2)
+    if cs > 0:
+        right = right + np.minimum(np.maximum(slack, 0) >> cs, ccap)
+    return np.where(ok, right, wb + (m1 & wm))
+
+
 def logits_np(seed: int, stage: int, ids, L: int, C: int, thr: int, dtype: str = "bf16",
-              scale_log2: int = 4) -> np.ndarray:
+              scale_log2: int = 4, margin=LEGACY_MARGIN) -> np.ndarray:
     """Stage ``stage`` logits for requests ``ids``: float32 [n*L, C], or raw bf16
     bits (uint16) [n*L, C] when dtype == 'bf16'."""
     ids = np.asarray(ids, dtype=np.int64)
@@ -123,7 +143,8 @@ def logits_np(seed: int, stage: int, ids, L: int, C: int, thr: int, dtype: str =
     winner = np.where(tok_ok, lab, (lab.astype(np.int64) + 1 + other) % C).astype(np.int64)
     m1 = (mix32(tk ^ np.uint32(0x11))).astype(np.int64)
     m2 = (mix32(tk ^ np.uint32(0x22))).astype(np.int64)
-    wcode = np.where(tok_ok, 60 + (m1 & 127) + (m2 & 63), 60 + (m1 & 63))
+    slack = (thr - d.astype(np.int64) - e.astype(np.int64))[:, None]
+    wcode = winner_code(tok_ok, slack, m1, m2, margin)
     j = np.arange(C, dtype=np.uint32)[None, None, :]
     with np.errstate(over="ignore"):
         h = mix32(tk[:, :, None] + (j + np.uint32(1)) * np.uint32(0x85EBCA6B))
@@ -142,6 +163,14 @@ def logits_np(seed: int, stage: int, ids, L: int, C: int, thr: int, dtype: str =
 def bf16_bits_to_f32(bits: np.ndarray) -> np.ndarray:
     return (bits.astype(np.uint32) << np.uint32(16)).view(np.float32)
 
+
+# ViT families: the right answer's margin grows with the request's distance
+# from the model's accuracy boundary, so confident-but-wrong and unsure-but-
+# right answers overlap and AP calibration has to defer about half of the
+# requests (tools/tune_generator.py).  C2 at full size: calibrated reach
+# [1, .481, .312, .232, .182] (sum 2.21); handled 51.9 / 16.9 / 8.0 / 5.0 /
+# 18.2 % -- Table III's ViT split is 59.6 / 5.1 / 18.2 / 17.1 %.
+VIT_MARGIN = (50, 15, 7, 60, 63, 8, 180)
 
 # --------------------------------------------------------------------------
 # Workload families (BASELINE.json configs).
@@ -162,6 +191,7 @@ class Family:
     log2_bins: int = 12
     seed: int = 0x250512566
     top_k: int = 0              # NEXT-2: stage confidence over the top_k logits (0 = full)
+    margin: tuple = LEGACY_MARGIN   # winner-code profile (winner_code); ViT families: VIT_MARGIN
 
     @property
     def K(self):
@@ -183,10 +213,11 @@ class Family:
 FAMILIES = {
     # C1: 2-stage ViT-S -> ViT-L, fp32, 4,096 x 1,000
     "c1": Family("c1_vit2_fp32", 4096, 1000, 1, "fp32", (0.808, 0.823), (1.0, 1.0), 0, 0, 4096,
-                 seed=0x250512566 + 1),
+                 seed=0x250512566 + 1, margin=VIT_MARGIN),
     # C2: 5-stage ViT family, bf16, 262,144 x 1,000, 50,000 validation
     "c2": Family("c2_vit5_bf16", 262144, 1000, 1, "bf16", (0.748, 0.808, 0.812, 0.813, 0.823),
-                 (1.0, 1.1, 0.9, 1.0, 1.2), 0, 0, 50000, seed=0x250512566 + 2),
+                 (1.0, 1.1, 0.9, 1.0, 1.2), 0, 0, 50000, seed=0x250512566 + 2,
+                 margin=VIT_MARGIN),
     # C3: 4-size T5, 16,384 seq x 64 tok x 32,128 vocab bf16, MIN over tokens
     "c3": Family("c3_t5x4_bf16", 16384, 32128, 64, "bf16", (0.782, 0.842, 0.871, 0.905),
                  (1.0, 1.0, 1.0, 1.0), 0, 1, 4096, payload_bytes=256, seed=0x250512566 + 3),
@@ -196,8 +227,15 @@ FAMILIES = {
     # C5: streaming 5-stage ViT, 2^23 requests x 1,000 bf16 (sharded over GPUs)
     "c5": Family("c5_vit5_stream_bf16", 1 << 23, 1000, 1, "bf16",
                  (0.748, 0.808, 0.812, 0.813, 0.823), (1.0, 1.1, 0.9, 1.0, 1.2), 0, 0, 1 << 20,
-                 seed=0x250512566 + 5),
+                 seed=0x250512566 + 5, margin=VIT_MARGIN),
 }
+
+
+def fam_logits_np(f: Family, stage: int, ids, dtype: str | None = None, L: int | None = None,
+                  C: int | None = None) -> np.ndarray:
+    """logits_np with the family's seed, accuracy threshold and margin profile."""
+    return logits_np(f.seed, stage, ids, L or f.L, C or f.C, f.thr[stage], dtype or f.dtype,
+                     margin=f.margin)
 
 
 def scaled(f: Family, n: int | None = None, n_val: int | None = None, C: int | None = None,
