@@ -50,6 +50,7 @@ typedef enum {
   HS_ERR_INVALID_ARGUMENT = 1,
   HS_ERR_NONFINITE_INPUT = 2, /* reserved for host-side checks of d_status */
   HS_ERR_CUDA = 3,
+  HS_ERR_NCCL = 4,            /* an NCCL call of the hs_comm_* paths failed (hs_last_error: detail) */
   HS_ERR_WORKSPACE_TOO_SMALL = 5,
   HS_ERR_UNSUPPORTED = 6
 } hs_status_t;
@@ -450,6 +451,10 @@ hs_status_t hs_ipc_close(void* dptr);
  *   target_correct < 0: AP, tau = the GLOBAL correct count of m_K.  comm ==
  *   NULL: single GPU (the same sweep without the all-reduce).  Outputs as
  *   hs_calibrate_thresholds (refinement passes are not available here).
+ *   Every argument is validated before the first collective, so an argument
+ *   error returns on the failing rank before any rank has entered a round
+ *   (the arguments that decide the collectives -- K, log2_bins -- must agree
+ *   across ranks).  NCCL failures: HS_ERR_NCCL.
  * NCCL is loaded with dlopen("libnccl.so.2") on the first of these calls;
  * HS_ERR_UNSUPPORTED when it cannot be loaded. */
 typedef struct hs_comm_s* hs_comm_t;
@@ -458,10 +463,14 @@ typedef struct hs_comm_s* hs_comm_t;
  * move this rank's deferred ids[0..*d_count) (+ payload rows of
  * payload_row_bytes) so that dest_ranks[d] (distinct) receives block d of the
  * global rank-major deferred list (as hs_forward_scatter / dist.forward_deferred).
- * One all-gather of the counts, ONE device->host read of them (NCCL sizes are
- * host values: this call synchronises `stream`), then grouped ncclSend/ncclRecv.
- * recv_ids / recv_payload hold recv_cap rows; *h_recv_count (host) = rows
- * received.  ws: hs_forward_nccl_workspace(world) bytes of device memory. */
+ * One all-gather of every rank's (count, recv_cap), ONE device->host read of
+ * them (NCCL sizes are host values: this call synchronises `stream`), then
+ * grouped ncclSend/ncclRecv.  recv_ids / recv_payload hold recv_cap rows;
+ * *h_recv_count (host) = rows received.  When ANY rank's block exceeds that
+ * rank's recv_cap, EVERY rank returns HS_ERR_INVALID_ARGUMENT after the
+ * all-gather and none posts a send or receive (the decision is taken on the
+ * gathered values, so no rank is left waiting).  NCCL failures: HS_ERR_NCCL.
+ * ws: hs_forward_nccl_workspace(world) bytes of device memory. */
 size_t hs_forward_nccl_workspace(int32_t world);
 hs_status_t hs_forward_nccl(const int64_t* ids, const void* payload, int64_t payload_row_bytes,
                             const int64_t* d_count, const int32_t* dest_ranks, int32_t n_dest,

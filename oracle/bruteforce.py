@@ -56,6 +56,35 @@ def greedy_by_simulation(conf, correct, log2_bins: int, target: int = -1):
     return {"b": b, "correct_total": total, "handled": handled, "reach": reach, "tau": tau}
 
 
+def refine_by_simulation(conf, correct, log2_bins: int, passes: int, target: int = -1):
+    """D5's refinement by coordinate descent on the simulated cascade: starting
+    from the greedy thresholds, each pass visits k = 1..K-1 in order and sets
+    b_k = the smallest b whose cascade (b_k = b, every other threshold as it
+    stands) still keeps >= tau correct answers -- Alg. 1's local search "Repeat
+    line 3-4 on search space [k - eps, k + eps]" taken to its exact
+    per-coordinate minimum.  Stops after ``passes`` passes or at a fixpoint."""
+    B = 1 << log2_bins
+    K = len(correct)
+    N = len(correct[0])
+    bins = [[_bin(float(conf[k][r]), B) for r in range(N)] for k in range(K - 1)]
+    g = greedy_by_simulation(conf, correct, log2_bins, target)
+    tau, b = g["tau"], list(g["b"])
+    for _ in range(passes):
+        changed = False
+        for k in range(K - 1):
+            for cand in range(B + 2):
+                trial = b[:k] + [cand] + b[k + 1:]
+                if simulate(bins, correct, trial)[0] >= tau:
+                    if cand != b[k]:
+                        b[k] = cand
+                        changed = True
+                    break
+        if not changed:
+            break
+    total, handled, reach = simulate(bins, correct, b)
+    return {"b": b, "correct_total": total, "handled": handled, "reach": reach, "tau": tau}
+
+
 def exhaustive_min_energy(conf, correct, log2_bins: int, energy, target: int = -1):
     """Exhaustive grid search over all (B+2)^(K-1) threshold vectors: the AP
     point of minimal energy e = sum_k reach_k * e_k (reach reading of

@@ -75,6 +75,16 @@ def build_info() -> str:
     return lib().hs_build_info().decode()
 
 
+def _temp_workspace(nbytes: int, device, stream=None) -> torch.Tensor:
+    """A call-local workspace; when the call runs on another stream than torch's
+    current one, the caching allocator is told so (record_stream) and does not
+    hand the memory out again before that stream is done with it."""
+    t = torch.empty(max(int(nbytes), 16), dtype=torch.uint8, device=device)
+    if stream is not None and stream != torch.cuda.current_stream(device):
+        t.record_stream(stream)
+    return t
+
+
 def workspace(nbytes: int, device) -> torch.Tensor:
     """A zero-filled workspace (the compaction descriptors must start zeroed)."""
     return torch.zeros(max(int(nbytes), 16), dtype=torch.uint8, device=device)
@@ -112,9 +122,13 @@ def confidence(logits: torch.Tensor, *, n: int | None = None, seq_len: int = 1,
         out["argmax"] = torch.empty(n * seq_len, dtype=torch.int32, device=dev)
     if labels is not None and "correct" not in out:
         out["correct"] = torch.empty(n, dtype=torch.uint8, device=dev)
-    need = lib().hs_confidence_workspace(n, seq_len)
-    if need and (ws is None or ws.numel() < need):
-        ws = torch.empty(need, dtype=torch.uint8, device=dev)
+    # required: the token-row part (hs_confidence_batched_workspace(1, ..)); a
+    # caller workspace of at least that size is used as is (the optional
+    # split-row region only when it fits).  A temporary gets the full size.
+    need = lib().hs_confidence_batched_workspace(1, n, seq_len)
+    if ws is None or ws.numel() < need:
+        full = lib().hs_confidence_workspace(n, seq_len)
+        ws = _temp_workspace(full, dev, stream) if full else None
     _abi.call("hs_confidence_topk", _p(logits), _dtype_code(logits), n, seq_len, C, stride,
               _p(row_index), _p(d_n), float(temperature), _kind(kind), _reduce(reduce), int(top_k),
               _p(out["conf"]), _p(out.get("argmax")), _p(labels), _p(out.get("correct")),
@@ -151,7 +165,7 @@ def confidence_batched(logits: list, temperatures, *, n: int | None = None, seq_
         out["correct"] = torch.empty(nb * n, dtype=torch.uint8, device=dev)
     need = lib().hs_confidence_batched_workspace(nb, n, seq_len)
     if need and (ws is None or ws.numel() < need):
-        ws = torch.empty(need, dtype=torch.uint8, device=dev)
+        ws = _temp_workspace(need, dev, stream)
     ptrs = (ctypes.c_void_p * nb)(*[x.data_ptr() for x in logits])
     temps = (ctypes.c_float * nb)(*[float(t) for t in temperatures])
     _abi.call("hs_confidence_batched", ptrs, temps, nb, _dtype_code(x0), n, seq_len, C,
@@ -192,7 +206,7 @@ def fit_temperature(logits: list, labels: torch.Tensor, *, n: int | None = None,
     out.setdefault("used", torch.empty(nb, dtype=torch.int64, device=dev))
     need = lib().hs_fit_temperature_workspace(nb, n)
     if ws is None or ws.numel() < need:
-        ws = torch.empty(need, dtype=torch.uint8, device=dev)
+        ws = _temp_workspace(need, dev, stream)
     ptrs = (ctypes.c_void_p * nb)(*[x.data_ptr() for x in logits])
     _abi.call("hs_fit_temperature", ptrs, nb, _dtype_code(x0), n, C, int(x0.stride(0)), _p(labels),
               float(t_lo), float(t_hi), int(max_passes), _p(out["T"]), _p(out["nll"]),
@@ -235,7 +249,7 @@ def threshold_replay(conf: torch.Tensor, correct: torch.Tensor, weights, *, log2
         out.setdefault("reach", torch.empty(S, K, dtype=torch.int64, device=dev))
     need = lib().hs_threshold_replay_workspace(K, N, int(log2_bins))
     if ws is None or ws.numel() < need:
-        ws = torch.empty(need, dtype=torch.uint8, device=dev)
+        ws = _temp_workspace(need, dev, stream)
     w = (ctypes.c_int64 * K)(*[int(x) for x in weights])
     _abi.call("hs_threshold_replay", _p(conf), _p(correct), K, N, int(log2_bins), _p(bvecs), S, w,
               _p(out["correct"]), _p(out["energy"]), _p(out.get("reach")), _p(out["model_correct"]),
@@ -259,7 +273,7 @@ def perf_graph(correct: torch.Tensor, energy: torch.Tensor, N: int, *, tau: int 
     out.setdefault("pick", torch.empty(2, dtype=torch.int64, device=dev))
     need = lib().hs_perf_graph_workspace(N)
     if ws is None or ws.numel() < need:
-        ws = torch.empty(need, dtype=torch.uint8, device=dev)
+        ws = _temp_workspace(need, dev, stream)
     _abi.call("hs_perf_graph", _p(correct), _p(energy), S, int(N), int(tau), int(floor),
               _p(model_correct), int(K), _p(out["front_c"]), _p(out["front_e"]), _p(out["front_s"]),
               _p(out["front_n"]), _p(out["pick"]), _p(ws), ws.numel(), _p(status), _stream(stream))
@@ -347,7 +361,7 @@ def forward_nccl(ids: torch.Tensor, d_count: torch.Tensor, comm: int, world: int
         out.setdefault("recv_payload", torch.empty(max(cap, 1) * payload_row_bytes, dtype=torch.uint8, device=dev))
     need = lib().hs_forward_nccl_workspace(world)
     if ws is None or ws.numel() < need:
-        ws = torch.empty(need, dtype=torch.uint8, device=dev)
+        ws = _temp_workspace(need, dev, stream)
     dr = (ctypes.c_int32 * len(dest))(*dest)
     n = ctypes.c_int64()
     _abi.call("hs_forward_nccl", _p(ids), _p(payload), int(payload_row_bytes), _p(d_count), dr, len(dest),
@@ -500,7 +514,7 @@ def calibrate_thresholds(conf: torch.Tensor, correct: torch.Tensor, *, log2_bins
     out = _calib_out(K, dev, out)
     need = lib().hs_calibrate_workspace(K, log2_bins)
     if ws is None or ws.numel() < need:
-        ws = torch.empty(max(need, 16), dtype=torch.uint8, device=dev)
+        ws = _temp_workspace(need, dev, stream)
     _abi.call("hs_calibrate_thresholds", _p(conf), _p(correct), K, N, int(log2_bins), int(target),
               int(refine_passes), _p(out["b"]), _p(out["t"]), _p(out["reach"]),
               _p(out["handled"]), _p(out["correct_total"]), _p(ws), ws.numel(), _stream(stream))

@@ -17,7 +17,7 @@ SZ = ctypes.c_size_t
 
 HS_OK = 0
 STATUS_NAMES = {0: "HS_OK", 1: "HS_ERR_INVALID_ARGUMENT", 2: "HS_ERR_NONFINITE_INPUT",
-                3: "HS_ERR_CUDA", 5: "HS_ERR_WORKSPACE_TOO_SMALL", 6: "HS_ERR_UNSUPPORTED"}
+                3: "HS_ERR_CUDA", 4: "HS_ERR_NCCL", 5: "HS_ERR_WORKSPACE_TOO_SMALL", 6: "HS_ERR_UNSUPPORTED"}
 
 # every symbol include/hs.h declares: name -> (restype, argtypes)
 SIGNATURES = {
@@ -99,6 +99,9 @@ def lib():
                 f = getattr(L, name)
                 f.restype = res
                 f.argtypes = args
+            if b"EXPERIMENT" in L.hs_build_info() and os.environ.get("HS_ALLOW_EXPERIMENT") != "1":
+                raise ImportError(f"{LIB_PATH} is a timing-bound experiment build (wrong results); "
+                                  "set HS_ALLOW_EXPERIMENT=1 to load it for A/B timing")
             _lib = L
     return _lib
 

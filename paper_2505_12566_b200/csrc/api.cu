@@ -167,6 +167,7 @@ const char* hs_status_string(hs_status_t s) {
     case HS_ERR_INVALID_ARGUMENT: return "HS_ERR_INVALID_ARGUMENT";
     case HS_ERR_NONFINITE_INPUT: return "HS_ERR_NONFINITE_INPUT";
     case HS_ERR_CUDA: return "HS_ERR_CUDA";
+    case HS_ERR_NCCL: return "HS_ERR_NCCL";
     case HS_ERR_WORKSPACE_TOO_SMALL: return "HS_ERR_WORKSPACE_TOO_SMALL";
     case HS_ERR_UNSUPPORTED: return "HS_ERR_UNSUPPORTED";
   }
@@ -178,7 +179,14 @@ uint64_t hs_launch_count(void) { return hs::g_launches.load(); }
 const char* hs_build_info(void) {
 #define HS_STR2(x) #x
 #define HS_STR(x) HS_STR2(x)
+#if defined(HS_EXP_NOARGMAX) || defined(HS_EXP_NOEXP) || defined(HS_EXP_TOPK_NOCAND)
+  // timing-bound experiment build (tools/build_variants.py): results are WRONG;
+  // the Python loader refuses it unless HS_ALLOW_EXPERIMENT=1
+  return "libhs: sm_100a (compute_100a), nvcc " HS_STR(__CUDACC_VER_MAJOR__) "." HS_STR(__CUDACC_VER_MINOR__)
+         " EXPERIMENT-WRONG-RESULTS";
+#else
   return "libhs: sm_100a (compute_100a), nvcc " HS_STR(__CUDACC_VER_MAJOR__) "." HS_STR(__CUDACC_VER_MINOR__);
+#endif
 }
 
 // mandatory part (token rows of sequences) + the optional split-row region
@@ -512,7 +520,7 @@ hs_status_t hs_comm_unique_id(void* id) {
   if (!id) return fail(HS_ERR_INVALID_ARGUMENT, "id is required");
   if (!hs::nccl_available()) return fail(HS_ERR_UNSUPPORTED, "libnccl.so.2 could not be loaded");
   const int r = hs::nccl_unique_id(id);
-  return r ? fail(HS_ERR_CUDA, "ncclGetUniqueId: %s", hs::nccl_error(r)) : HS_OK;
+  return r ? fail(HS_ERR_NCCL, "ncclGetUniqueId: %s", hs::nccl_error(r)) : HS_OK;
 }
 
 hs_status_t hs_comm_create(const void* id, int32_t rank, int32_t world, int32_t device, hs_comm_t* out) {
@@ -520,14 +528,16 @@ hs_status_t hs_comm_create(const void* id, int32_t rank, int32_t world, int32_t 
     return fail(HS_ERR_INVALID_ARGUMENT, "id, out, 0 <= rank < world and device >= 0 are required");
   if (!hs::nccl_available()) return fail(HS_ERR_UNSUPPORTED, "libnccl.so.2 could not be loaded");
   const int r = hs::nccl_comm_create(id, rank, world, device, out);
-  return r ? fail(HS_ERR_CUDA, "ncclCommInitRank: %s", hs::nccl_error(r)) : HS_OK;
+  return r ? fail(HS_ERR_NCCL, "ncclCommInitRank: %s", hs::nccl_error(r)) : HS_OK;
 }
 
 hs_status_t hs_comm_destroy(hs_comm_t comm) {
   if (!comm) return fail(HS_ERR_INVALID_ARGUMENT, "comm is required");
   const int r = hs::nccl_comm_destroy(comm);
-  return r ? fail(HS_ERR_CUDA, "ncclCommDestroy: %s", hs::nccl_error(r)) : HS_OK;
+  return r ? fail(HS_ERR_NCCL, "ncclCommDestroy: %s", hs::nccl_error(r)) : HS_OK;
 }
+
+static hs_status_t check_calib(int32_t K, int32_t q, void* ws, size_t ws_bytes);
 
 hs_status_t hs_calibrate_thresholds_comm(const float* conf, const uint8_t* correct, int32_t K,
                                          int64_t N, int32_t log2_bins, int64_t target_correct,
@@ -537,7 +547,12 @@ hs_status_t hs_calibrate_thresholds_comm(const float* conf, const uint8_t* corre
                                          hs_stream_t stream) {
   if (!d_bin_idx || !d_thresholds || !d_reach || !d_handled || !d_correct_total)
     return fail(HS_ERR_INVALID_ARGUMENT, "all calibration outputs are required");
-  hs_status_t st = hs_calibrate_begin(K, log2_bins, target_correct, ws, ws_bytes, stream);
+  // validate everything the rounds will check before any collective is posted
+  hs_status_t st = check_calib(K, log2_bins, ws, ws_bytes);
+  if (st != HS_OK) return st;
+  if (N < 0) return fail(HS_ERR_INVALID_ARGUMENT, "N < 0");
+  if (N > 0 && (!conf || !correct)) return fail(HS_ERR_INVALID_ARGUMENT, "NULL input");
+  st = hs_calibrate_begin(K, log2_bins, target_correct, ws, ws_bytes, stream);
   if (st != HS_OK) return st;
   int32_t* hist = hs_calibrate_hist_ptr(ws);
   const size_t words = hs_calibrate_hist_bytes(log2_bins) / sizeof(int32_t);
@@ -546,7 +561,7 @@ hs_status_t hs_calibrate_thresholds_comm(const float* conf, const uint8_t* corre
     if (st != HS_OK) return st;
     if (comm) {
       const int r = hs::nccl_allreduce_i32_sum(hist, words, comm, (cudaStream_t)stream);
-      if (r) return fail(HS_ERR_CUDA, "ncclAllReduce: %s", hs::nccl_error(r));
+      if (r) return fail(HS_ERR_NCCL, "ncclAllReduce: %s", hs::nccl_error(r));
     }
     st = hs_calibrate_select(K, log2_bins, k, d_bin_idx, d_thresholds, d_reach, d_handled,
                              d_correct_total, ws, ws_bytes, stream);
@@ -555,7 +570,8 @@ hs_status_t hs_calibrate_thresholds_comm(const float* conf, const uint8_t* corre
   return HS_OK;
 }
 
-size_t hs_forward_nccl_workspace(int32_t world) { return (size_t)(world < 1 ? 1 : world) * sizeof(int64_t) + 256; }
+// ws: this rank's (count, recv_cap) pair, then every rank's pairs
+size_t hs_forward_nccl_workspace(int32_t world) { return (size_t)(2 + 2 * (world < 1 ? 1 : world)) * sizeof(int64_t) + 256; }
 
 hs_status_t hs_forward_nccl(const int64_t* ids, const void* payload, int64_t payload_row_bytes,
                             const int64_t* d_count, const int32_t* dest_ranks, int32_t n_dest,
@@ -578,14 +594,27 @@ hs_status_t hs_forward_nccl(const int64_t* ids, const void* payload, int64_t pay
   if (!ws || ws_bytes < hs_forward_nccl_workspace(W))
     return fail(HS_ERR_WORKSPACE_TOO_SMALL, "workspace %zu < %zu", ws_bytes, hs_forward_nccl_workspace(W));
   cudaStream_t s = (cudaStream_t)stream;
-  int64_t* d_all = reinterpret_cast<int64_t*>(ws);
-  int r = hs::nccl_allgather_i64(d_count, d_all, comm, s);
-  if (r) return fail(HS_ERR_CUDA, "ncclAllGather: %s", hs::nccl_error(r));
-  std::vector<int64_t> cnt(W);
-  hs_status_t st = cuda_check(cudaMemcpyAsync(cnt.data(), d_all, W * sizeof(int64_t), cudaMemcpyDeviceToHost, s),
-                              "count read-back");
+  int64_t* d_mine = reinterpret_cast<int64_t*>(ws);
+  int64_t* d_all = d_mine + 2;
+  // every rank learns every rank's (count, recv_cap): the capacity check below
+  // is then the same decision on all ranks, taken before any send/recv is posted
+  hs_status_t st = cuda_check(cudaMemcpyAsync(d_mine, d_count, sizeof(int64_t), cudaMemcpyDeviceToDevice, s),
+                              "count copy");
+  if (st == HS_OK)
+    st = cuda_check(cudaMemcpyAsync(d_mine + 1, &recv_cap, sizeof(int64_t), cudaMemcpyHostToDevice, s),
+                    "capacity copy");
+  if (st != HS_OK) return st;
+  int r = hs::nccl_allgather_i64(d_mine, d_all, 2, comm, s);
+  if (r) return fail(HS_ERR_NCCL, "ncclAllGather: %s", hs::nccl_error(r));
+  std::vector<int64_t> pairs(2 * W), cnt(W), caps(W);
+  st = cuda_check(cudaMemcpyAsync(pairs.data(), d_all, 2 * W * sizeof(int64_t), cudaMemcpyDeviceToHost, s),
+                  "count read-back");
   if (st == HS_OK) st = cuda_check(cudaStreamSynchronize(s), "count read-back");
   if (st != HS_OK) return st;
+  for (int h = 0; h < W; ++h) {
+    cnt[h] = pairs[2 * h] < 0 ? 0 : pairs[2 * h];
+    caps[h] = pairs[2 * h + 1];
+  }
   int64_t D = 0;
   for (int h = 0; h < W; ++h) D += cnt[h];
   const int64_t R = n_dest;
@@ -598,6 +627,13 @@ hs_status_t hs_forward_nccl(const int64_t* ids, const void* payload, int64_t pay
     const int64_t d = is_dest[h], a = std::max(off, lo(d)), b = std::min(off + cnt[g], lo(d + 1));
     return b > a ? b - a : 0;
   };
+  // the same decision on every rank: does any receiver's block exceed its capacity?
+  for (int h = 0; h < W; ++h) {
+    const int64_t blk = is_dest[h] < 0 ? 0 : lo(is_dest[h] + 1) - lo(is_dest[h]);
+    if (blk > caps[h])
+      return fail(HS_ERR_INVALID_ARGUMENT, "rank %d: recv_cap %lld < %lld rows to receive (no rank exchanged)",
+                  h, (long long)caps[h], (long long)blk);
+  }
   std::vector<int64_t> scnt(W), soff(W), rcnt(W), roff(W);
   int64_t so = 0, ro = 0;
   for (int h = 0; h < W; ++h) {
@@ -608,15 +644,14 @@ hs_status_t hs_forward_nccl(const int64_t* ids, const void* payload, int64_t pay
     roff[h] = ro;
     ro += rcnt[h];
   }
-  if (ro > recv_cap) return fail(HS_ERR_INVALID_ARGUMENT, "recv_cap %lld < %lld rows to receive", (long long)recv_cap, (long long)ro);
   r = hs::nccl_exchange(reinterpret_cast<const char*>(ids), soff.data(), scnt.data(),
                         reinterpret_cast<char*>(recv_ids), roff.data(), rcnt.data(), 8, comm, s);
-  if (r) return fail(HS_ERR_CUDA, "NCCL send/recv (ids): %s", hs::nccl_error(r));
+  if (r) return fail(HS_ERR_NCCL, "NCCL send/recv (ids): %s", hs::nccl_error(r));
   if (payload_row_bytes) {
     r = hs::nccl_exchange(reinterpret_cast<const char*>(payload), soff.data(), scnt.data(),
                           reinterpret_cast<char*>(recv_payload), roff.data(), rcnt.data(),
                           payload_row_bytes, comm, s);
-    if (r) return fail(HS_ERR_CUDA, "NCCL send/recv (payload): %s", hs::nccl_error(r));
+    if (r) return fail(HS_ERR_NCCL, "NCCL send/recv (payload): %s", hs::nccl_error(r));
   }
   *h_recv_count = ro;
   return HS_OK;

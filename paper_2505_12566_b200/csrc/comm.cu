@@ -109,10 +109,10 @@ int nccl_comm_destroy(hs_comm_s* c) {
 int nccl_world(const hs_comm_s* c) { return c->world; }
 int nccl_rank(const hs_comm_s* c) { return c->rank; }
 
-int nccl_allgather_i64(const int64_t* one, int64_t* all, hs_comm_s* c, cudaStream_t s) {
+int nccl_allgather_i64(const int64_t* mine, int64_t* all, int64_t count, hs_comm_s* c, cudaStream_t s) {
   const NcclApi& a = nccl();
   if (!a.ok) return -1;
-  return (int)a.all_gather(one, all, 1, ncclInt64, c->nc, s);
+  return (int)a.all_gather(mine, all, (size_t)count, ncclInt64, c->nc, s);
 }
 
 // grouped point-to-point exchange: send[h] elements from sbuf + soff[h] to rank h,

@@ -242,7 +242,7 @@ int nccl_comm_destroy(hs_comm_s* c);
 int nccl_allreduce_i32_sum(int32_t* buf, size_t count, hs_comm_s* c, cudaStream_t s);
 int nccl_world(const hs_comm_s* c);
 int nccl_rank(const hs_comm_s* c);
-int nccl_allgather_i64(const int64_t* one, int64_t* all, hs_comm_s* c, cudaStream_t s);
+int nccl_allgather_i64(const int64_t* mine, int64_t* all, int64_t count, hs_comm_s* c, cudaStream_t s);
 int nccl_exchange(const char* sbuf, const int64_t* soff, const int64_t* scnt, char* rbuf,
                   const int64_t* roff, const int64_t* rcnt, int64_t elem_bytes, hs_comm_s* c,
                   cudaStream_t s);

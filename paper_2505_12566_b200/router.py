@@ -99,15 +99,19 @@ class Router:
             calibrate_thresholds(self.vconf, self.vok, log2_bins=self.q, target=target,
                                  out=self.cal, ws=self.cal_ws, stream=stream)
         else:
+            import contextlib
             import torch.distributed as dist
             hist = calibrate_hist_view(self.cal_ws, self.q)
-            calibrate_begin(self.K, self.q, target, self.cal_ws, stream=stream)
-            for k in range(self.K - 1):
-                calibrate_histogram(self.vconf, self.vok, k, self.cal["b"], log2_bins=self.q,
-                                    ws=self.cal_ws, stream=stream)
-                dist.all_reduce(hist, op=dist.ReduceOp.SUM, group=self.group)
-                calibrate_select(self.K, k, self.cal, log2_bins=self.q, ws=self.cal_ws,
-                                 stream=stream)
+            # dist.all_reduce runs on torch's current stream: make it the
+            # caller's, so histogram -> all-reduce -> select stay ordered
+            ctx = torch.cuda.stream(stream) if stream is not None else contextlib.nullcontext()
+            with ctx:
+                calibrate_begin(self.K, self.q, target, self.cal_ws)
+                for k in range(self.K - 1):
+                    calibrate_histogram(self.vconf, self.vok, k, self.cal["b"], log2_bins=self.q,
+                                        ws=self.cal_ws)
+                    dist.all_reduce(hist, op=dist.ReduceOp.SUM, group=self.group)
+                    calibrate_select(self.K, k, self.cal, log2_bins=self.q, ws=self.cal_ws)
         return self.cal
 
     # ---- offline: temperature scaling (Eq. 1) ---------------------

@@ -96,6 +96,7 @@ def test_status_strings(libhs):
     lib = libhs.lib()
     assert lib.hs_status_string(0) == b"HS_OK"
     assert lib.hs_status_string(5) == b"HS_ERR_WORKSPACE_TOO_SMALL"
+    assert lib.hs_status_string(4) == b"HS_ERR_NCCL"
     assert b"sm_100a" in lib.hs_build_info()
 
 

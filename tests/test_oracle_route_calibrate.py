@@ -149,6 +149,53 @@ def test_refinement_never_raises_and_stays_feasible():
         assert bruteforce.simulate(bins, ok, list(r["b"]))[0] == r["correct_total"]
 
 
+def test_refinement_equals_simulation_coordinate_descent():
+    """Pin for the oracle's refinement passes (D5, the analogue of Alg. 1's
+    "Repeat line 3-4 on search space [k-eps, k+eps]", P:467): bruteforce.py
+    re-picks each b_k as the smallest b whose SIMULATED cascade keeps >= tau
+    correct (independent code: no histograms, no suffix sums).  The cases are
+    drawn so that refinement moves at least one threshold in many of them, so a
+    refinement that does nothing (or moves the wrong coordinate) fails."""
+    rng = np.random.default_rng(11)
+    moved = 0
+    for case in range(300):
+        K = int(rng.integers(3, 6))
+        N = int(rng.integers(2, 24))
+        q = int(rng.integers(1, 4))
+        conf, ok = _random_case(rng, K, N, correlated=True)
+        if case % 9 == 0:
+            conf[1, 0] = np.nan
+        passes = int(rng.integers(1, 4))
+        r = oracle.calibrate(conf, ok, q, refine_passes=passes)
+        bf = bruteforce.refine_by_simulation(conf, ok, q, passes)
+        assert list(r["b"]) == bf["b"], (case, passes, conf, ok)
+        assert r["correct_total"] == bf["correct_total"] >= r["tau"]
+        assert list(r["handled"]) == bf["handled"] and list(r["reach"]) == bf["reach"]
+        moved += list(r["b"]) != list(oracle.calibrate(conf, ok, q)["b"])
+    assert moved >= 20, moved
+
+
+def test_refinement_hand_example():
+    """Hand-worked K = 3, B = 2 (q = 1) case where refinement lowers b_1.
+    c_1 = (.1, .9, .9) -> bins (0, 1, 1); c_2 = (.9, .9, .6) -> bins (1, 1, 1);
+    correct m_1 = (0, 0, 0), m_2 = (1, 1, 0), m_3 = (0, 1, 0); tau = 1 (m_3).
+    Greedy, k = 1 (later models defer all, so m_3 answers the rest): A = 0,
+    G = 1, H = (0, -1, 0) over bins 0..2, S(0) = S(1) = -1, S(2) = 0, so
+    b_1 = 2 (nobody is answered by m_1).  k = 2: G = 1, H[1] = 1, S(0) = 1 ->
+    b_2 = 0 (m_2 answers all: 2 correct).  Refinement, k = 1, now that m_2
+    answers whatever m_1 defers: b_1 = 0 answers everyone at m_1 (0 < tau);
+    b_1 = 1 answers r1, r2 at m_1 and r0 at m_2 (1 >= tau): b_1 = 2 -> 1, and
+    m_2's reach drops from 3 to 1."""
+    conf = np.array([[0.1, 0.9, 0.9], [0.9, 0.9, 0.6]])
+    ok = np.array([[0, 0, 0], [1, 1, 0], [0, 1, 0]], np.uint8)
+    g = oracle.calibrate(conf, ok, 1)
+    assert list(g["b"]) == [2, 0] and g["tau"] == 1 and g["correct_total"] == 2
+    assert list(g["reach"]) == [3, 3, 0]
+    r = oracle.calibrate(conf, ok, 1, refine_passes=1)
+    assert list(r["b"]) == [1, 0] and r["correct_total"] == 1
+    assert list(r["reach"]) == [3, 1, 0] and list(r["handled"]) == [2, 1, 0]
+
+
 def test_explicit_target_and_defer_all():
     conf = np.array([[1.0, 1.0, 0.5]])
     ok = np.array([[0, 0, 1], [1, 1, 1]], np.uint8)
