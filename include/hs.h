@@ -71,7 +71,8 @@ typedef enum { HS_SEQ_NONE = 0, HS_SEQ_MIN = 1, HS_SEQ_MEAN = 2 } hs_seq_reduce_
 
 #define HS_STATUS_NONFINITE 1u
 #define HS_STATUS_NOT_CONVERGED 2u   /* hs_fit_temperature: pass budget exhausted */
-#define HS_STATUS_TIMEOUT 4u         /* hs_forward_*: a peer did not publish within 10 s */
+#define HS_STATUS_TIMEOUT 4u         /* hs_peer_* / *_peer: a peer did not publish within 10 s */
+#define HS_STATUS_OVERFLOW 8u        /* hs_peer_forward*: a rank deferred more than the group's cap */
 
 /* ------------------------------------------------------------------------ */
 /* Confidence.                                        */
@@ -383,52 +384,101 @@ hs_status_t hs_perf_graph(const int64_t* d_correct, const int64_t* d_energy, int
                           uint32_t* d_status, hs_stream_t stream);
 
 /* ------------------------------------------------------------------------ */
-/* Multi-GPU forwarding of deferred requests over peer memory.    */
+/* Multi-GPU cascade over peer memory (§V-A; P:561 DMA, P:617-619   */
+/* zero-copy): a group of ranks (one process per GPU) that exchange through   */
+/* each other's memory over NVLink / NVSwitch, with no host round trip and no */
+/* NCCL on the data path.                                                    */
 /* ------------------------------------------------------------------------ */
-/* After a stage every rank g (0 <= g < world <= 8) holds D_g deferred ids in
- * increasing global order (next_ids of hs_cascade_step, count d_count).  The
+/* Every rank g owns one PEER REGION of hs_peer_region_bytes(world, cap, P, q)
+ * bytes, allocated with hs_ipc_alloc (zero-filled, exportable); the 64-byte
+ * hs_ipc_handle of every region is exchanged once by the caller (e.g.
+ * torch.distributed all_gather_object) and opened with hs_ipc_open, so that
+ * hs_peer_t.region[h] is rank h's region as mapped in this process
+ * (region[rank] = this rank's own allocation).  The region holds the forward
+ * flags, two receive sets of world*cap ids (+ payload rows of P bytes) and two
+ * calibration slot sets of world x (2^q + 2) packed bins.
+ *   cap: the largest batch any rank routes in any stage (every rank's deferred
+ *        count must stay <= cap; more sets HS_STATUS_OVERFLOW and is clamped).
+ *   All ranks must call the same sequence of hs_peer_* / *_peer operations
+ *   (the flags carry per-rank epochs kept on the device).
+ *
+ * hs_peer_forward -- after a stage every rank g holds D_g deferred ids in
+ * increasing global order (next_ids of hs_cascade_step, count *d_count).  The
  * next stage's batch is the global rank-major list, split into contiguous
- * blocks over the destination ranks dest_ranks[0..n_dest) (distinct): block d
- * = global positions [floor(d*D/n_dest), floor((d+1)*D/n_dest)), D = sum_g D_g.
- * Receiver dest_ranks[d] gets its block, in global order, at recv_ids[0..) (and
- * payload rows at recv_payload) -- exactly dist.forward_deferred's result, but
- * moved by the kernels through peer-mapped memory (CUDA IPC over NVLink /
- * NVSwitch) with no host round trip and no NCCL:
- *   hs_forward_publish: store {epoch, D_g} into slot g of every rank's count
- *     array (peer_counts[h] = rank h's u64[world] array, mapped here).
- *   hs_forward_scatter: wait until this rank's count array (my_counts) holds
- *     every rank's count of this epoch, write each local deferred id (+ payload
- *     row) into the receive buffer of its destination (peer_recv_ids[h],
- *     peer_recv_payload[h] or NULL), write this rank's receive count to
- *     *d_recv_count, then store {epoch} into slot g of every rank's done array
- *     (peer_done[h]).
- *   hs_forward_wait: wait until this rank's done array (my_done) holds the
- *     epoch from every rank: the receive buffer is complete for later kernels.
- * Rules: epoch > 0 and strictly increasing per forward on a group; count and
- * done arrays zero-filled once; the receive buffers hold world * cap rows and
- * alternate between two sets on consecutive stages (a rank may scatter stage
- * k+1 while a peer still reads stage k's buffer); ws >= 256 bytes zero-filled
- * once (completion counter, re-armed by the kernel).  The waits give up after
- * 10 s (a peer that never publishes), OR HS_STATUS_TIMEOUT into *d_status
- * (optional) and skip their writes, instead of hanging the GPU.  Payload rows: multiples
- * of 16 bytes, 16-byte aligned.  All calls stream-ordered, graph-capturable.
+ * blocks over the destination ranks dest_ranks[0..n_dest) (distinct; NULL =
+ * all ranks in order, the balanced placement): block d = global positions
+ * [floor(d*D/n_dest), floor((d+1)*D/n_dest)), D = sum_g D_g.  Receiver
+ * dest_ranks[d] gets its block, in global order, at hs_peer_recv_ids(g, set)
+ * [0 .. *d_recv_count) (and its payload rows at hs_peer_recv_payload(g, set);
+ * payload may be NULL).  Three stream-ordered kernels, graph-capturable:
+ *   publish: {epoch, D_g} into slot g of every rank's count array;
+ *   scatter: wait for every rank's count of the epoch, write each local id
+ *            (one thread per item: coalesced peer stores) and payload row at
+ *            its final position in the destination's receive set, then (last
+ *            CTA) this rank's receive count and a "done" flag to every rank;
+ *   wait:    until every rank's done flag carries the epoch.
+ *   set (0/1): the receive set written; alternate it between consecutive
+ *   forwards (stage parity) -- a rank may scatter stage k+1 while a peer still
+ *   reads stage k's set.  The phases are also exported separately (publish all
+ *   ranks, then scatter, then wait) for several ranks driven by one process.
+ * Waits give up after 10 s (a peer that never publishes): HS_STATUS_TIMEOUT is
+ * ORed into *d_status (optional), the receive count is 0, nothing hangs.
+ *
+ * hs_calibrate_thresholds_peer -- hs_calibrate_thresholds where conf / correct
+ * hold THIS rank's shard (N >= 0 samples, may be 0): every round, each rank's
+ * packed histogram is pushed into every rank's region inside the one
+ * cooperative calibration kernel (system-scope release counter), and every
+ * rank selects the identical b_k from the sum of the W histograms (integer
+ * counts: order-independent, deterministic).  AP: tau = the GLOBAL correct
+ * count of m_K.  Needs q = the group's log2_bins, K <= 16, N * world < 2^21
+ * and a shard that fits the resident kernel (else HS_ERR_UNSUPPORTED, before
+ * any launch).  No refinement passes on this path.
+ *
+ * hs_cascade_step_peer -- hs_cascade_step_ex, then (stage < n_stages-1)
+ * hs_peer_forward of its next_ids / next_payload / d_counts[1] to
+ * next_stage_ranks (SURVEY 8(b)'s comm-aware cascade step).  n must be <= cap.
+ *
  * hs_ipc_alloc / hs_ipc_free: the one explicit device allocation of the library
  * (a whole cudaMalloc allocation, zero-filled synchronously, so that its IPC
  * handle maps exactly this buffer on the peers).
  * hs_ipc_handle / hs_ipc_open / hs_ipc_close wrap cudaIpcGetMemHandle /
- * cudaIpcOpenMemHandle (lazy peer access) / cudaIpcCloseMemHandle: a 64-byte
- * host handle per device buffer, exchanged by the caller (e.g. torch.distributed). */
-#define HS_FWD_MAX_WORLD 8
-hs_status_t hs_forward_publish(const int64_t* d_count, int64_t cap, int32_t rank, int32_t world,
-                               uint64_t* const* peer_counts, uint32_t epoch, hs_stream_t stream);
-hs_status_t hs_forward_scatter(const int64_t* ids, const void* payload, int64_t payload_row_bytes,
-                               int64_t cap, int32_t rank, int32_t world, const uint64_t* my_counts,
-                               uint64_t* const* peer_done, int64_t* const* peer_recv_ids,
-                               void* const* peer_recv_payload, const int32_t* dest_ranks,
-                               int32_t n_dest, uint32_t epoch, int64_t* d_recv_count, void* ws,
-                               size_t ws_bytes, uint32_t* d_status, hs_stream_t stream);
-hs_status_t hs_forward_wait(const uint64_t* my_done, int32_t world, uint32_t epoch, uint32_t* d_status,
-                            hs_stream_t stream);
+ * cudaIpcOpenMemHandle (lazy peer access) / cudaIpcCloseMemHandle. */
+#define HS_PEER_MAX_WORLD 8
+typedef struct {
+  int32_t rank, world;                /* 0 <= rank < world <= 8 */
+  int64_t cap;                        /* max items per rank per stage (< 2^32) */
+  int64_t payload_row_bytes;          /* 0 or a multiple of 16 */
+  int32_t log2_bins;                  /* calibration grid the regions are sized for (1..14) */
+  void* region[HS_PEER_MAX_WORLD];    /* region[h]: rank h's region, mapped in this process */
+} hs_peer_t;
+size_t hs_peer_region_bytes(int32_t world, int64_t cap, int64_t payload_row_bytes, int32_t log2_bins);
+int64_t* hs_peer_recv_ids(const hs_peer_t* g, int32_t set);     /* this rank's receive set (device) */
+void* hs_peer_recv_payload(const hs_peer_t* g, int32_t set);    /* NULL without payload rows */
+hs_status_t hs_peer_forward(const hs_peer_t* g, int32_t set, const int64_t* ids, const void* payload,
+                            const int64_t* d_count, const int32_t* dest_ranks, int32_t n_dest,
+                            int64_t* d_recv_count, uint32_t* d_status, hs_stream_t stream);
+hs_status_t hs_peer_forward_publish(const hs_peer_t* g, const int64_t* d_count, uint32_t* d_status,
+                                    hs_stream_t stream);
+hs_status_t hs_peer_forward_scatter(const hs_peer_t* g, int32_t set, const int64_t* ids, const void* payload,
+                                    const int32_t* dest_ranks, int32_t n_dest, int64_t* d_recv_count,
+                                    uint32_t* d_status, hs_stream_t stream);
+hs_status_t hs_peer_forward_wait(const hs_peer_t* g, uint32_t* d_status, hs_stream_t stream);
+hs_status_t hs_calibrate_thresholds_peer(const float* conf, const uint8_t* correct, int32_t K, int64_t N,
+                                         int32_t log2_bins, int64_t target_correct, int32_t* d_bin_idx,
+                                         float* d_thresholds, int64_t* d_reach, int64_t* d_handled,
+                                         int64_t* d_correct_total, const hs_peer_t* g, void* ws,
+                                         size_t ws_bytes, uint32_t* d_status, hs_stream_t stream);
+hs_status_t hs_cascade_step_peer(int32_t stage, int32_t n_stages, const void* logits, hs_dtype_t dtype,
+                                 int64_t n, int32_t seq_len, int64_t n_classes, int64_t row_stride,
+                                 const int64_t* row_index, const int64_t* d_n, float temperature,
+                                 hs_conf_kind_t kind, hs_seq_reduce_t reduce, float threshold,
+                                 const float* d_threshold, const int64_t* ids, const void* payload,
+                                 int64_t payload_row_bytes, int64_t* acc_ids, float* acc_conf,
+                                 int32_t* acc_pred, int64_t* next_ids, void* next_payload,
+                                 int64_t* d_counts, void* ws, size_t ws_bytes, uint32_t* d_status,
+                                 int32_t top_k, uint32_t flags, const hs_peer_t* g, int32_t set,
+                                 const int32_t* next_stage_ranks, int32_t n_next_ranks,
+                                 int64_t* d_recv_count, hs_stream_t stream);
 hs_status_t hs_ipc_alloc(size_t bytes, void** dptr);   /* cudaMalloc + zero fill: exportable whole allocation */
 hs_status_t hs_ipc_free(void* dptr);
 hs_status_t hs_ipc_handle(const void* dptr, void* handle /* host, 64 bytes */);

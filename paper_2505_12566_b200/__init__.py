@@ -288,37 +288,69 @@ def _ptr_array(ptrs):
     return (ctypes.c_void_p * len(ptrs))(*[int(p) if p else None for p in ptrs])
 
 
-def forward_publish(d_count: torch.Tensor, cap: int, rank: int, peer_counts: list, epoch: int,
-                    stream=None):
-    """Store {epoch, D_rank} into slot ``rank`` of every rank's count array
-    (``peer_counts[h]``: device address of rank h's u64[world] array, mapped here)."""
-    _abi.call("hs_forward_publish", _p(d_count), int(cap), int(rank), len(peer_counts),
-              _ptr_array(peer_counts), int(epoch), _stream(stream))
+# ---------------------------------------------------------------------------
+# Multi-GPU group over peer memory (hs_peer_*; dist.PeerGroup builds the group)
+# ---------------------------------------------------------------------------
+def peer_region_bytes(world: int, cap: int, payload_row_bytes: int = 0, log2_bins: int = 12) -> int:
+    return int(lib().hs_peer_region_bytes(int(world), int(cap), int(payload_row_bytes), int(log2_bins)))
 
 
-def forward_scatter(ids: torch.Tensor, cap: int, rank: int, my_counts: torch.Tensor | int,
-                    peer_done: list, peer_recv_ids: list, dest_ranks: list, epoch: int,
-                    recv_count: torch.Tensor, ws: torch.Tensor, *, payload: torch.Tensor | None = None,
-                    payload_row_bytes: int = 0, peer_recv_payload: list | None = None,
-                    status: torch.Tensor | None = None, stream=None):
-    """Write this rank's deferred ids (+ payload rows) into their destination
-    ranks' receive buffers at their global positions; ``recv_count`` gets this
-    rank's receive count."""
+def _dest_array(dest_ranks):
     import ctypes
-    mc = my_counts if isinstance(my_counts, int) else my_counts.data_ptr()
-    dr = (ctypes.c_int32 * len(dest_ranks))(*[int(d) for d in dest_ranks])
-    _abi.call("hs_forward_scatter", _p(ids), _p(payload), int(payload_row_bytes), int(cap), int(rank),
-              len(peer_done), mc, _ptr_array(peer_done), _ptr_array(peer_recv_ids),
-              _ptr_array(peer_recv_payload) if peer_recv_payload else None, dr, len(dest_ranks),
-              int(epoch), _p(recv_count), _p(ws), ws.numel(), _p(status), _stream(stream))
+    if dest_ranks is None:
+        return None, 0
+    return (ctypes.c_int32 * len(dest_ranks))(*[int(d) for d in dest_ranks]), len(dest_ranks)
 
 
-def forward_wait(my_done: torch.Tensor | int, world: int, epoch: int,
-                 status: torch.Tensor | None = None, stream=None):
-    """Wait until every rank's done flag of ``epoch`` is in this rank's array
-    (gives up after 10 s with STATUS_TIMEOUT in ``status``)."""
-    md = my_done if isinstance(my_done, int) else my_done.data_ptr()
-    _abi.call("hs_forward_wait", md, int(world), int(epoch), _p(status), _stream(stream))
+def peer_forward(g, set_: int, ids: torch.Tensor, d_count: torch.Tensor, recv_count: torch.Tensor, *,
+                 payload: torch.Tensor | None = None, dest_ranks=None, status: torch.Tensor | None = None,
+                 stream=None):
+    """hs_peer_forward: this rank's deferred ids[:*d_count] (+ payload rows) to
+    their blocks of the global stable list on ``dest_ranks`` (None = all ranks);
+    this rank's block lands in receive set ``set_`` (count -> recv_count)."""
+    import ctypes
+    dr, nd = _dest_array(dest_ranks)
+    _abi.call("hs_peer_forward", ctypes.byref(g), int(set_), _p(ids), _p(payload), _p(d_count), dr, nd,
+              _p(recv_count), _p(status), _stream(stream))
+
+
+def peer_forward_publish(g, d_count: torch.Tensor, status: torch.Tensor | None = None, stream=None):
+    import ctypes
+    _abi.call("hs_peer_forward_publish", ctypes.byref(g), _p(d_count), _p(status), _stream(stream))
+
+
+def peer_forward_scatter(g, set_: int, ids: torch.Tensor, recv_count: torch.Tensor, *,
+                         payload: torch.Tensor | None = None, dest_ranks=None,
+                         status: torch.Tensor | None = None, stream=None):
+    import ctypes
+    dr, nd = _dest_array(dest_ranks)
+    _abi.call("hs_peer_forward_scatter", ctypes.byref(g), int(set_), _p(ids), _p(payload), dr, nd,
+              _p(recv_count), _p(status), _stream(stream))
+
+
+def peer_forward_wait(g, status: torch.Tensor | None = None, stream=None):
+    import ctypes
+    _abi.call("hs_peer_forward_wait", ctypes.byref(g), _p(status), _stream(stream))
+
+
+def calibrate_thresholds_peer(conf: torch.Tensor, correct: torch.Tensor, g, *, log2_bins: int = 12,
+                              target: int = -1, out: dict | None = None, ws: torch.Tensor | None = None,
+                              status: torch.Tensor | None = None, stream=None) -> dict:
+    """AP calibration over a request-sharded validation set: this rank's shard
+    (conf f32 [K-1, N], correct u8 [K, N]); the per-round histograms are summed
+    across the group inside the calibration kernel (hs_calibrate_thresholds_peer)."""
+    import ctypes
+    _check_cuda(conf, correct)
+    K, N = int(correct.shape[0]), int(correct.shape[1])
+    dev = correct.device
+    out = _calib_out(K, dev, out)
+    need = lib().hs_calibrate_workspace(K, log2_bins)
+    if ws is None or ws.numel() < need:
+        ws = _temp_workspace(need, dev, stream)
+    _abi.call("hs_calibrate_thresholds_peer", _p(conf), _p(correct), K, N, int(log2_bins), int(target),
+              _p(out["b"]), _p(out["t"]), _p(out["reach"]), _p(out["handled"]), _p(out["correct_total"]),
+              ctypes.byref(g), _p(ws), ws.numel(), _p(status), _stream(stream))
+    return out
 
 
 # ---------------------------------------------------------------------------
@@ -443,8 +475,13 @@ def cascade_step(stage: int, n_stages: int, logits: torch.Tensor, threshold, *, 
                  payload: torch.Tensor | None = None, payload_row_bytes: int = 0,
                  out: dict | None = None, ws: torch.Tensor | None = None,
                  status: torch.Tensor | None = None, overlap_previous: bool = False,
-                 top_k: int = 0, stream=None) -> dict:
+                 top_k: int = 0, peer=None, peer_set: int = 0, next_ranks=None,
+                 recv_count: torch.Tensor | None = None, stream=None) -> dict:
     """One model m_k of the cascade: confidence -> threshold -> compaction/gather.
+
+    ``peer`` (a dist.PeerGroup's ``g``): hs_cascade_step_peer -- the deferred
+    list is then forwarded to ``next_ranks`` (None = all ranks) into receive
+    set ``peer_set`` of the group (count -> ``recv_count``).
 
     ``overlap_previous`` (HS_STEP_OVERLAP_PREVIOUS): the confidence kernel runs
     next to the previous libhs kernel on the stream; the caller guarantees that
@@ -471,6 +508,17 @@ def cascade_step(stage: int, n_stages: int, logits: torch.Tensor, threshold, *, 
         ws = workspace(need, dev)
     d_thr = threshold if isinstance(threshold, torch.Tensor) else None
     thr = 0.0 if d_thr is not None else float(threshold)
+    if peer is not None:
+        import ctypes
+        dr, nd = _dest_array(next_ranks)
+        _abi.call("hs_cascade_step_peer", int(stage), int(n_stages), _p(logits), _dtype_code(logits),
+                  int(n), int(seq_len), C, int(logits.stride(0)), _p(row_index), _p(d_n),
+                  float(temperature), _kind(kind), _reduce(reduce), thr, _p(d_thr), _p(ids), _p(payload),
+                  int(payload_row_bytes), _p(out["acc_ids"]), _p(out["acc_conf"]), _p(out["acc_pred"]),
+                  _p(out["next_ids"]), _p(out.get("next_payload")), _p(out["counts"]), _p(ws),
+                  ws.numel(), _p(status), int(top_k), HS_STEP_OVERLAP_PREVIOUS if overlap_previous else 0,
+                  ctypes.byref(peer), int(peer_set), dr, nd, _p(recv_count), _stream(stream))
+        return out
     _abi.call("hs_cascade_step_ex", int(stage), int(n_stages), _p(logits), _dtype_code(logits),
               int(n), int(seq_len), C, int(logits.stride(0)), _p(row_index), _p(d_n),
               float(temperature), _kind(kind), _reduce(reduce), thr, _p(d_thr), _p(ids), _p(payload),
@@ -600,27 +648,46 @@ class Cascade:
         self.ws = workspace(lib().hs_cascade_step_workspace(n_cap, L), dev)
 
     def route(self, logits: list, thresholds, *, n: int | None = None, ids=None, payload=None,
-              by_id: bool = True, overlap_first: bool = False, stream=None):
+              by_id: bool = True, overlap_first: bool = False, peer=None, next_ranks=None,
+              stream=None):
         """Run the K stages.  ``overlap_first``: stage 1's confidence kernel runs
         next to the previous libhs kernel (e.g. the calibration it does not
-        depend on); see hs_cascade_step_ex / HS_STEP_OVERLAP_PREVIOUS."""
+        depend on); see hs_cascade_step_ex / HS_STEP_OVERLAP_PREVIOUS.
+
+        ``peer`` (a dist.PeerGroup): request-sharded cascade over a group of
+        GPUs -- after every stage the deferred list is forwarded over peer
+        memory (hs_cascade_step_peer) to ``next_ranks[k]`` (None = all ranks:
+        the balanced placement), and stage k+1 routes the block this rank
+        received (receive set k % 2, count ``peer.recv_count[k]``).  With
+        ``by_id`` the stage logits are indexed by request id; otherwise they are
+        the dense batch of the block this rank receives."""
         n = self.n_cap if n is None else int(n)
         d_thr = thresholds if isinstance(thresholds, torch.Tensor) else None
         for k, s in enumerate(self.stages):
             prev = self.outs[k - 1] if k else None
-            cur_ids = prev["next_ids"] if k else ids
-            cur_payload = prev.get("next_payload") if k else payload
+            if k and peer is not None:
+                cur_ids = peer.recv_ids((k - 1) % 2)
+                cur_payload = peer.recv_payload((k - 1) % 2) if self.P else None
+                d_n = peer.recv_count[k - 1: k]
+            else:
+                cur_ids = prev["next_ids"] if k else ids
+                cur_payload = prev.get("next_payload") if k else payload
+                d_n = prev["counts"][1:2] if k else None
             thr = d_thr[k:k + 1] if d_thr is not None else float(thresholds[k] if k < self.K - 1 else 0.0)
             row_index = cur_ids if by_id else None
             if by_id and cur_ids is None:
                 row_index = None   # stage 1 with identity ids: row = id = position
+            kw = {}
+            if peer is not None and k < self.K - 1:
+                kw = {"peer": peer.g, "peer_set": k % 2, "recv_count": peer.recv_count[k:k + 1],
+                      "next_ranks": None if next_ranks is None else next_ranks[k]}
             cascade_step(k, self.K, logits[k], thr, n=n, seq_len=s.seq_len, n_classes=s.n_classes,
                          temperature=s.temperature, kind=s.kind, reduce=s.reduce,
-                         row_index=row_index, d_n=prev["counts"][1:2] if k else None,
+                         row_index=row_index, d_n=d_n,
                          ids=cur_ids, payload=cur_payload, payload_row_bytes=self.P,
                          out=self.outs[k], ws=self.ws, status=self.status,
                          overlap_previous=overlap_first and k == 0, top_k=s.top_k,
-                         stream=stream)
+                         stream=stream, **kw)
         return self
 
     def results(self):

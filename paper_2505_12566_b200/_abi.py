@@ -55,10 +55,17 @@ SIGNATURES = {
     "hs_threshold_replay": (I32, [P, P, I32, I64, I32, P, I64, P, P, P, P, P, P, SZ, P]),
     "hs_perf_graph_workspace": (SZ, [I64]),
     "hs_perf_graph": (I32, [P, P, I64, I64, I64, I64, P, I32, P, P, P, P, P, P, SZ, P, P]),
-    "hs_forward_publish": (I32, [P, I64, I32, I32, P, ctypes.c_uint32, P]),
-    "hs_forward_scatter": (I32, [P, P, I64, I64, I32, I32, P, P, P, P, P, I32, ctypes.c_uint32, P, P,
-                                 SZ, P, P]),
-    "hs_forward_wait": (I32, [P, I32, ctypes.c_uint32, P, P]),
+    "hs_peer_region_bytes": (SZ, [I32, I64, I64, I32]),
+    "hs_peer_recv_ids": (P, [P, I32]),
+    "hs_peer_recv_payload": (P, [P, I32]),
+    "hs_peer_forward": (I32, [P, I32, P, P, P, P, I32, P, P, P]),
+    "hs_peer_forward_publish": (I32, [P, P, P, P]),
+    "hs_peer_forward_scatter": (I32, [P, I32, P, P, P, I32, P, P, P]),
+    "hs_peer_forward_wait": (I32, [P, P, P]),
+    "hs_calibrate_thresholds_peer": (I32, [P, P, I32, I64, I32, I64, P, P, P, P, P, P, P, SZ, P, P]),
+    "hs_cascade_step_peer": (I32, [I32, I32, P, I32, I64, I32, I64, I64, P, P, F32, I32, I32, F32, P, P,
+                                   P, I64, P, P, P, P, P, P, P, SZ, P, I32, ctypes.c_uint32, P, I32, P,
+                                   I32, P, P]),
     "hs_ipc_alloc": (I32, [SZ, P]),
     "hs_ipc_free": (I32, [P]),
     "hs_ipc_handle": (I32, [P, P]),
@@ -75,6 +82,16 @@ SIGNATURES = {
     "hs_launch_count": (ctypes.c_uint64, []),
     "hs_build_info": (ctypes.c_char_p, []),
 }
+
+PEER_MAX_WORLD = 8
+
+
+class PeerGroup(ctypes.Structure):
+    """hs_peer_t (include/hs.h): the peer-memory group as seen by this process."""
+    _fields_ = [("rank", ctypes.c_int32), ("world", ctypes.c_int32), ("cap", ctypes.c_int64),
+                ("payload_row_bytes", ctypes.c_int64), ("log2_bins", ctypes.c_int32),
+                ("region", ctypes.c_void_p * PEER_MAX_WORLD)]
+
 
 _lock = threading.Lock()
 _lib = None

@@ -416,69 +416,121 @@ hs_status_t hs_perf_graph(const int64_t* d_correct, const int64_t* d_energy, int
                     "performance graph kernels");
 }
 
-hs_status_t hs_forward_publish(const int64_t* d_count, int64_t cap, int32_t rank, int32_t world,
-                               uint64_t* const* peer_counts, uint32_t epoch, hs_stream_t stream) {
-  if (world < 1 || world > hs::kFwdMaxWorld || rank < 0 || rank >= world)
-    return fail(HS_ERR_INVALID_ARGUMENT, "rank %d / world %d out of range", rank, world);
-  if (!d_count || !peer_counts || cap < 0 || cap >= ((int64_t)1 << 32) || epoch == 0)
-    return fail(HS_ERR_INVALID_ARGUMENT, "d_count, peer_counts, 0 <= cap < 2^32 and epoch > 0 are required");
-  hs::FwdPeers p{};
-  p.world = world;
-  for (int h = 0; h < world; ++h) {
-    if (!peer_counts[h]) return fail(HS_ERR_INVALID_ARGUMENT, "peer_counts[%d] is NULL", h);
-    p.counts[h] = reinterpret_cast<unsigned long long*>(peer_counts[h]);
+// ---- multi-GPU group over peer memory (peer.cu) -------------------------------
+static hs_status_t peer_args(const hs_peer_t* g, bool need_pay, hs::PeerArgs* out, hs::PeerLayout* lay) {
+  if (!g) return fail(HS_ERR_INVALID_ARGUMENT, "peer group is required");
+  if (g->world < 1 || g->world > hs::kPeerMaxWorld || g->rank < 0 || g->rank >= g->world)
+    return fail(HS_ERR_INVALID_ARGUMENT, "rank %d / world %d out of range", g->rank, g->world);
+  if (g->cap < 0 || g->cap >= ((int64_t)1 << 32) || g->payload_row_bytes < 0 || (g->payload_row_bytes % 16) ||
+      g->log2_bins < 1 || g->log2_bins > 14)
+    return fail(HS_ERR_INVALID_ARGUMENT, "0 <= cap < 2^32, payload_row_bytes %% 16 == 0 and 1 <= log2_bins <= 14");
+  if (need_pay && g->payload_row_bytes == 0)
+    return fail(HS_ERR_INVALID_ARGUMENT, "the group's regions were sized without payload rows");
+  const hs::PeerLayout L = hs::peer_layout(g->world, g->cap, g->payload_row_bytes, g->log2_bins);
+  hs::PeerArgs A{};
+  A.world = g->world;
+  A.rank = g->rank;
+  A.recv_stride = (int64_t)L.recv_stride;
+  for (int h = 0; h < g->world; ++h) {
+    char* r = reinterpret_cast<char*>(g->region[h]);
+    if (!r || !aligned16(r)) return fail(HS_ERR_INVALID_ARGUMENT, "region[%d] is NULL or misaligned", h);
+    A.hdr[h] = reinterpret_cast<hs::PeerHeader*>(r);
+    A.recv_ids[h] = reinterpret_cast<int64_t*>(r + L.recv_off);
+    A.recv_payload[h] = g->payload_row_bytes ? r + L.pay_off : nullptr;
   }
-  return cuda_check(hs::launch_fwd_publish(d_count, cap, rank, p, epoch, (cudaStream_t)stream),
-                    "forward publish kernel");
+  *out = A;
+  if (lay) *lay = L;
+  return HS_OK;
 }
 
-hs_status_t hs_forward_scatter(const int64_t* ids, const void* payload, int64_t payload_row_bytes,
-                               int64_t cap, int32_t rank, int32_t world, const uint64_t* my_counts,
-                               uint64_t* const* peer_done, int64_t* const* peer_recv_ids,
-                               void* const* peer_recv_payload, const int32_t* dest_ranks,
-                               int32_t n_dest, uint32_t epoch, int64_t* d_recv_count, void* ws,
-                               size_t ws_bytes, uint32_t* d_status, hs_stream_t stream) {
-  if (world < 1 || world > hs::kFwdMaxWorld || rank < 0 || rank >= world)
-    return fail(HS_ERR_INVALID_ARGUMENT, "rank %d / world %d out of range", rank, world);
-  if (!ids || !my_counts || !peer_done || !peer_recv_ids || !d_recv_count || epoch == 0 || cap < 0)
-    return fail(HS_ERR_INVALID_ARGUMENT, "ids, my_counts, peer_done, peer_recv_ids, d_recv_count and epoch > 0 are required");
-  if (payload_row_bytes < 0 || (payload_row_bytes % 16) != 0 || (payload_row_bytes && (!payload || !peer_recv_payload || !aligned16(payload))))
-    return fail(HS_ERR_INVALID_ARGUMENT, "payload rows must be 16-byte aligned multiples of 16 bytes");
-  if (!dest_ranks || n_dest < 1 || n_dest > world)
-    return fail(HS_ERR_INVALID_ARGUMENT, "1 <= n_dest <= world destination ranks are required");
-  if (!ws || ws_bytes < 256) return fail(HS_ERR_WORKSPACE_TOO_SMALL, "workspace %zu < 256", ws_bytes);
-  hs::FwdPeers p{};
-  p.world = world;
-  p.my_counts = reinterpret_cast<const unsigned long long*>(my_counts);
-  for (int h = 0; h < world; ++h) {
-    if (!peer_done[h] || !peer_recv_ids[h] || (payload_row_bytes && !peer_recv_payload[h]))
-      return fail(HS_ERR_INVALID_ARGUMENT, "peer buffers of rank %d are NULL", h);
-    p.done[h] = reinterpret_cast<unsigned long long*>(peer_done[h]);
-    p.recv_ids[h] = peer_recv_ids[h];
-    p.recv_payload[h] = payload_row_bytes ? peer_recv_payload[h] : nullptr;
+static hs_status_t peer_dest(const hs_peer_t* g, const int32_t* dest_ranks, int32_t n_dest, hs::PeerDest* d) {
+  if (!dest_ranks) {     // NULL: every rank, in rank order (the balanced placement)
+    d->n = g->world;
+    for (int i = 0; i < g->world; ++i) d->ranks[i] = i;
+    return HS_OK;
   }
-  hs::FwdDest d{};
-  d.n = n_dest;
+  if (n_dest < 1 || n_dest > g->world) return fail(HS_ERR_INVALID_ARGUMENT, "1 <= n_dest <= world");
+  d->n = n_dest;
   unsigned seen = 0;
   for (int i = 0; i < n_dest; ++i) {
-    if (dest_ranks[i] < 0 || dest_ranks[i] >= world || (seen >> dest_ranks[i]) & 1u)
+    if (dest_ranks[i] < 0 || dest_ranks[i] >= g->world || (seen >> dest_ranks[i]) & 1u)
       return fail(HS_ERR_INVALID_ARGUMENT, "dest_ranks must be distinct ranks of the group");
     seen |= 1u << dest_ranks[i];
-    d.ranks[i] = dest_ranks[i];
+    d->ranks[i] = dest_ranks[i];
   }
-  return cuda_check(hs::launch_fwd_scatter(ids, payload, payload_row_bytes, cap, rank, p, epoch, d,
-                                           d_recv_count, reinterpret_cast<unsigned*>(ws), d_status,
-                                           (cudaStream_t)stream),
-                    "forward scatter kernel");
+  return HS_OK;
 }
 
-hs_status_t hs_forward_wait(const uint64_t* my_done, int32_t world, uint32_t epoch, uint32_t* d_status,
-                            hs_stream_t stream) {
-  if (!my_done || world < 1 || world > hs::kFwdMaxWorld || epoch == 0)
-    return fail(HS_ERR_INVALID_ARGUMENT, "my_done, 1 <= world <= %d and epoch > 0 are required", hs::kFwdMaxWorld);
-  return cuda_check(hs::launch_fwd_wait(reinterpret_cast<const unsigned long long*>(my_done), world, epoch,
-                                        d_status, (cudaStream_t)stream),
-                    "forward wait kernel");
+size_t hs_peer_region_bytes(int32_t world, int64_t cap, int64_t payload_row_bytes, int32_t log2_bins) {
+  if (world < 1 || world > hs::kPeerMaxWorld || cap < 0 || payload_row_bytes < 0 || log2_bins < 1 ||
+      log2_bins > 14)
+    return 0;
+  return hs::peer_layout(world, cap, payload_row_bytes, log2_bins).bytes;
+}
+
+int64_t* hs_peer_recv_ids(const hs_peer_t* g, int32_t set) {
+  hs::PeerArgs A;
+  if (set < 0 || set > 1 || peer_args(g, false, &A, nullptr) != HS_OK) return nullptr;
+  return A.recv_ids[g->rank] + (int64_t)set * A.recv_stride;
+}
+
+void* hs_peer_recv_payload(const hs_peer_t* g, int32_t set) {
+  hs::PeerArgs A;
+  if (set < 0 || set > 1 || peer_args(g, false, &A, nullptr) != HS_OK || !g->payload_row_bytes) return nullptr;
+  return reinterpret_cast<char*>(A.recv_payload[g->rank]) + (int64_t)set * A.recv_stride * g->payload_row_bytes;
+}
+
+hs_status_t hs_peer_forward_publish(const hs_peer_t* g, const int64_t* d_count, uint32_t* d_status,
+                                    hs_stream_t stream) {
+  hs::PeerArgs A;
+  hs_status_t st = peer_args(g, false, &A, nullptr);
+  if (st != HS_OK) return st;
+  if (!d_count) return fail(HS_ERR_INVALID_ARGUMENT, "d_count is required");
+  return cuda_check(hs::launch_peer_publish(d_count, g->cap, A, d_status, (cudaStream_t)stream),
+                    "peer publish kernel");
+}
+
+hs_status_t hs_peer_forward_scatter(const hs_peer_t* g, int32_t set, const int64_t* ids, const void* payload,
+                                    const int32_t* dest_ranks, int32_t n_dest, int64_t* d_recv_count,
+                                    uint32_t* d_status, hs_stream_t stream) {
+  hs::PeerArgs A;
+  hs_status_t st = peer_args(g, payload != nullptr, &A, nullptr);
+  if (st != HS_OK) return st;
+  if (set < 0 || set > 1) return fail(HS_ERR_INVALID_ARGUMENT, "set must be 0 or 1");
+  if (!ids || !d_recv_count) return fail(HS_ERR_INVALID_ARGUMENT, "ids and d_recv_count are required");
+  if (payload && !aligned16(payload)) return fail(HS_ERR_INVALID_ARGUMENT, "payload must be 16-byte aligned");
+  hs::PeerDest d{};
+  st = peer_dest(g, dest_ranks, n_dest, &d);
+  if (st != HS_OK) return st;
+  return cuda_check(hs::launch_peer_scatter(ids, payload, payload ? g->payload_row_bytes : 0, g->cap, set, A,
+                                            d, d_recv_count, d_status, (cudaStream_t)stream),
+                    "peer scatter kernel");
+}
+
+hs_status_t hs_peer_forward_wait(const hs_peer_t* g, uint32_t* d_status, hs_stream_t stream) {
+  hs::PeerArgs A;
+  hs_status_t st = peer_args(g, false, &A, nullptr);
+  if (st != HS_OK) return st;
+  return cuda_check(hs::launch_peer_wait(A, d_status, (cudaStream_t)stream), "peer wait kernel");
+}
+
+hs_status_t hs_peer_forward(const hs_peer_t* g, int32_t set, const int64_t* ids, const void* payload,
+                            const int64_t* d_count, const int32_t* dest_ranks, int32_t n_dest,
+                            int64_t* d_recv_count, uint32_t* d_status, hs_stream_t stream) {
+  // validate everything first: a rank that fails after publishing would leave
+  // its peers waiting (they time out instead of hanging, but still)
+  hs::PeerArgs A;
+  hs_status_t st = peer_args(g, payload != nullptr, &A, nullptr);
+  if (st != HS_OK) return st;
+  hs::PeerDest d{};
+  st = peer_dest(g, dest_ranks, n_dest, &d);
+  if (st != HS_OK) return st;
+  if (set < 0 || set > 1 || !ids || !d_count || !d_recv_count || (payload && !aligned16(payload)))
+    return fail(HS_ERR_INVALID_ARGUMENT, "set in {0,1}, ids, d_count, d_recv_count (aligned payload) required");
+  st = hs_peer_forward_publish(g, d_count, d_status, stream);
+  if (st == HS_OK) st = hs_peer_forward_scatter(g, set, ids, payload, dest_ranks, n_dest, d_recv_count, d_status, stream);
+  if (st == HS_OK) st = hs_peer_forward_wait(g, d_status, stream);
+  return st;
 }
 
 hs_status_t hs_ipc_alloc(size_t bytes, void** dptr) {
@@ -988,6 +1040,74 @@ hs_status_t hs_calibrate_thresholds(const float* conf, const uint8_t* correct, i
                                             d_thresholds, d_reach, d_handled, d_correct_total, ws,
                                             (cudaStream_t)stream),
                     "calib refinement");
+}
+
+hs_status_t hs_calibrate_thresholds_peer(const float* conf, const uint8_t* correct, int32_t K, int64_t N,
+                                         int32_t log2_bins, int64_t target_correct, int32_t* d_bin_idx,
+                                         float* d_thresholds, int64_t* d_reach, int64_t* d_handled,
+                                         int64_t* d_correct_total, const hs_peer_t* g, void* ws,
+                                         size_t ws_bytes, uint32_t* d_status, hs_stream_t stream) {
+  hs_status_t st = check_calib(K, log2_bins, ws, ws_bytes);
+  if (st != HS_OK) return st;
+  hs::PeerArgs A;
+  hs::PeerLayout L;
+  st = peer_args(g, false, &A, &L);
+  if (st != HS_OK) return st;
+  if (g->log2_bins != log2_bins)
+    return fail(HS_ERR_INVALID_ARGUMENT, "the group's regions were sized for log2_bins = %d", g->log2_bins);
+  if (N < 0 || (N > 0 && (!conf || !correct))) return fail(HS_ERR_INVALID_ARGUMENT, "N >= 0 and inputs required");
+  if (K > 16) return fail(HS_ERR_UNSUPPORTED, "K = %d > 16 on the peer path", K);
+  if (N * (int64_t)g->world >= ((int64_t)1 << 21))
+    return fail(HS_ERR_UNSUPPORTED, "N * world must be < 2^21 on the peer path (packed bins)");
+  if (!d_bin_idx || !d_thresholds || !d_reach || !d_handled || !d_correct_total)
+    return fail(HS_ERR_INVALID_ARGUMENT, "NULL output");
+  hs::PeerCal pc{};
+  pc.world = g->world;
+  pc.rank = g->rank;
+  for (int h = 0; h < g->world; ++h) {
+    pc.slots[h] = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(g->region[h]) + L.cal_off);
+    pc.arrive[h] = A.hdr[h]->cal_arrive;
+  }
+  pc.round_ctr = &A.hdr[g->rank]->cal_round;
+  pc.status = d_status;
+  const cudaError_t e = hs::launch_calib_peer(conf, correct, K, N, log2_bins, target_correct, d_bin_idx,
+                                              d_thresholds, d_reach, d_handled, d_correct_total, ws, pc,
+                                              (cudaStream_t)stream);
+  if (e == cudaErrorNotSupported)
+    return fail(HS_ERR_UNSUPPORTED, "the shard does not fit the resident calibration kernel");
+  return cuda_check(e, "peer calibration kernel");
+}
+
+hs_status_t hs_cascade_step_peer(int32_t stage, int32_t n_stages, const void* logits, hs_dtype_t dtype,
+                                 int64_t n, int32_t seq_len, int64_t n_classes, int64_t row_stride,
+                                 const int64_t* row_index, const int64_t* d_n, float temperature,
+                                 hs_conf_kind_t kind, hs_seq_reduce_t reduce, float threshold,
+                                 const float* d_threshold, const int64_t* ids, const void* payload,
+                                 int64_t payload_row_bytes, int64_t* acc_ids, float* acc_conf,
+                                 int32_t* acc_pred, int64_t* next_ids, void* next_payload,
+                                 int64_t* d_counts, void* ws, size_t ws_bytes, uint32_t* d_status,
+                                 int32_t top_k, uint32_t flags, const hs_peer_t* g, int32_t set,
+                                 const int32_t* next_stage_ranks, int32_t n_next_ranks,
+                                 int64_t* d_recv_count, hs_stream_t stream) {
+  const int is_last = stage == n_stages - 1;
+  if (!is_last) {     // validate the forward before anything is launched
+    hs::PeerArgs A;
+    hs_status_t st = peer_args(g, next_payload != nullptr, &A, nullptr);
+    if (st != HS_OK) return st;
+    hs::PeerDest d{};
+    st = peer_dest(g, next_stage_ranks, n_next_ranks, &d);
+    if (st != HS_OK) return st;
+    if (set < 0 || set > 1 || !next_ids || !d_recv_count)
+      return fail(HS_ERR_INVALID_ARGUMENT, "set in {0,1}, next_ids and d_recv_count are required");
+    if (n > g->cap) return fail(HS_ERR_INVALID_ARGUMENT, "n = %lld exceeds the group's cap", (long long)n);
+  }
+  hs_status_t st = hs_cascade_step_ex(stage, n_stages, logits, dtype, n, seq_len, n_classes, row_stride,
+                                      row_index, d_n, temperature, kind, reduce, threshold, d_threshold, ids,
+                                      payload, payload_row_bytes, acc_ids, acc_conf, acc_pred, next_ids,
+                                      next_payload, d_counts, ws, ws_bytes, d_status, top_k, flags, stream);
+  if (st != HS_OK || is_last) return st;
+  return hs_peer_forward(g, set, next_ids, next_payload, d_counts + 1, next_stage_ranks, n_next_ranks,
+                         d_recv_count, d_status, stream);
 }
 
 }  // extern "C"

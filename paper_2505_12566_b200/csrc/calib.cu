@@ -465,7 +465,8 @@ constexpr unsigned long long kPackMask = (1ull << kPackBits) - 1;
 // global histogram whose bins [lo, lo + n) sit in this thread's registers.
 template <int NT, int PMAX, bool SMEM = false>
 __device__ __forceinline__ void select_packed(const unsigned long long* __restrict__ g, int K,
-                                              int q, int round, SelState* ss) {
+                                              int q, int round, SelState* ss, int nsum = 1,
+                                              int sum_stride = 0) {
   constexpr int NW = NT / 32;
   static_assert(NW <= 32, "one warp scans the warp totals");
   __shared__ int sh_x[NW], sh_y[NW], sh_z[NW], sh_u[NW];
@@ -479,7 +480,15 @@ __device__ __forceinline__ void select_packed(const unsigned long long* __restri
   unsigned long long v[PMAX];
 #pragma unroll
   for (int i = 0; i < PMAX; ++i) v[i] = i < n ? (SMEM ? g[lo + i + 1] : __ldcg(g + lo + i + 1)) : 0ull;
-  const unsigned long long v0 = tid == 0 ? (SMEM ? g[0] : __ldcg(g)) : 0ull;   // NaN bin: never accepted
+  unsigned long long v0 = tid == 0 ? (SMEM ? g[0] : __ldcg(g)) : 0ull;   // NaN bin: never accepted
+  // multi-GPU: the W ranks' packed histograms (pushed into this rank's peer
+  // region) are summed here; packed fields cannot carry (global N < 2^21)
+  for (int w = 1; w < nsum; ++w) {
+    const unsigned long long* gw = g + (size_t)w * sum_stride;
+#pragma unroll
+    for (int i = 0; i < PMAX; ++i) v[i] += i < n ? __ldcg(gw + lo + i + 1) : 0ull;
+    if (tid == 0) v0 += __ldcg(gw);
+  }
 #define HS_CNT(x) ((int)((x) & kPackMask))
 #define HS_CK(x) ((int)(((x) >> kPackBits) & kPackMask))
 #define HS_CKK(x) ((int)((x) >> (2 * kPackBits)))
@@ -602,12 +611,61 @@ constexpr int kResidentThreads = 1024;
 
 // PMAX = bins per thread in the select, ceil((2^q + 1) / 1024): one
 // instantiation per range of q keeps the bins in registers.
-template <int PMAX>
+// Multi-GPU round exchange over peer memory (peer.cu layout): this rank's
+// packed histogram of round r (global round index, parity p = r & 1) is pushed
+// into slot [p][rank] of every rank's region (CTA c serves ranks c, c + grid,
+// ...), each push followed by a system-scope release increment of that rank's
+// arrival counter p; every CTA then waits until its own counter p reached
+// (r/2 + 1) * W and the select sums the W slots.  A slot of parity p is
+// rewritten two rounds later, by a rank that has seen every peer's push of
+// the round in between -- pushed after that peer's CTAs finished reading it.
+__device__ __forceinline__ void red_release_sys_add(unsigned long long* p, unsigned long long v) {
+  asm volatile("red.release.sys.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void peer_push_wait(const PeerCal& pc, const unsigned long long* hist,
+                                               bool hist_smem, int nb, unsigned long long r) {
+  const int par = (int)(r & 1), W = pc.world;
+  for (int h = blockIdx.x; h < W; h += gridDim.x) {
+    unsigned long long* dst = pc.slots[h] + ((size_t)par * W + pc.rank) * nb;
+    for (int i = threadIdx.x; i < nb; i += blockDim.x) dst[i] = hist_smem ? hist[i] : __ldcg(hist + i);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence_system();
+      red_release_sys_add(pc.arrive[h] + par, 1ull);
+    }
+  }
+  if (threadIdx.x == 0) {
+    const unsigned long long want = ((r >> 1) + 1) * (unsigned long long)W;
+    const unsigned long long* a = pc.arrive[pc.rank] + par;
+    unsigned long long t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    while (ld_acquire_sys_u64(a) < want) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (t - t0 > 10ull * 1000 * 1000 * 1000) {      // a peer never pushed: give up, flag it
+        if (pc.status) atomicOr(pc.status, HS_STATUS_TIMEOUT);
+        break;
+      }
+      __nanosleep(128);
+    }
+  }
+  __syncthreads();
+}
+
+template <int PMAX, bool PEER>
 __global__ void __launch_bounds__(kResidentThreads, 1) calib_resident_kernel(
     const float* __restrict__ conf, const uint8_t* __restrict__ correct, int K, int64_t N, int q,
     long long target, int32_t* b_idx, float* thr, int64_t* reach, int64_t* handled,
-    int64_t* correct_total, CalibState* st_out, unsigned long long* hist3, int per_cta) {
+    int64_t* correct_total, CalibState* st_out, unsigned long long* hist3, int per_cta,
+    const __grid_constant__ PeerCal pc) {
   pdl_start();
+  const unsigned long long rbase = PEER ? *pc.round_ctr : 0ull;   // read before the first grid barrier
 #ifdef HS_CALIB_TRACE
   int tr = 0;
 #endif
@@ -704,16 +762,31 @@ __global__ void __launch_bounds__(kResidentThreads, 1) calib_resident_kernel(
     HS_TR("flush");
     if (solo) {
       __syncthreads();
-      select_packed<kResidentThreads, PMAX, true>(spk, K, q, k, ss);
+      if (PEER) {
+        const unsigned long long r = rbase + k;
+        peer_push_wait(pc, spk, true, nb, r);
+        select_packed<kResidentThreads, PMAX>(pc.slots[pc.rank] + (size_t)(r & 1) * pc.world * nb, K, q,
+                                              k, ss, pc.world, nb);
+      } else {
+        select_packed<kResidentThreads, PMAX, true>(spk, K, q, k, ss);
+      }
       HS_TR("select");
       continue;
     }
     grid.sync();
     HS_TR("sync");
-    // every CTA selects from the summed histogram (identical results)
-    select_packed<kResidentThreads, PMAX>(cur, K, q, k, ss);
+    if (PEER) {
+      const unsigned long long r = rbase + k;
+      peer_push_wait(pc, cur, false, nb, r);
+      select_packed<kResidentThreads, PMAX>(pc.slots[pc.rank] + (size_t)(r & 1) * pc.world * nb, K, q, k,
+                                            ss, pc.world, nb);
+    } else {
+      // every CTA selects from the summed histogram (identical results)
+      select_packed<kResidentThreads, PMAX>(cur, K, q, k, ss);
+    }
     HS_TR("select");
   }
+  if (PEER && blockIdx.x == 0 && threadIdx.x == 0) *pc.round_ctr = rbase + (unsigned long long)(K - 1);
   if (blockIdx.x == 0) {
     for (int k = tid; k < K; k += blockDim.x) {
       if (k < K - 1) b_idx[k] = ss->b[k];
@@ -879,7 +952,7 @@ static cudaError_t launch_calib_resident(const float* conf, const uint8_t* corre
                                         int64_t N, int q, long long target, int32_t* b_idx,
                                         float* thr, int64_t* reach, int64_t* handled,
                                         int64_t* correct_total, void* ws, cudaStream_t s,
-                                        bool* launched) {
+                                        bool* launched, const PeerCal* peer = nullptr) {
   *launched = false;
   const size_t hbytes = (size_t)3 * ((1 << q) + 2) * sizeof(unsigned);
   const size_t head = hbytes + 16 - hbytes % 16 + sizeof(SelState);
@@ -891,19 +964,28 @@ static cudaError_t launch_calib_resident(const float* conf, const uint8_t* corre
   size_t smem = head + (size_t)per * (2 * (size_t)(K - 1) + 2) + 16;
   if (grid == 1) smem += (size_t)((1 << q) + 2) * sizeof(unsigned long long) + 16;   // packed bins (solo)
   // packed u64 bins need N < 2^21; K <= 16 correct bits per sample
-  if (K > 16 || N >= (int64_t(1) << kPackBits) || q > 14 || smem > cap) return cudaSuccess;
+  // (multi-GPU: the packed fields hold sums over every rank's shard; shards of
+  // equal size assumed, N * world < 2^21)
+  const int64_t n_glob = N * (peer ? (int64_t)peer->world : 1);
+  if (K > 16 || n_glob >= (int64_t(1) << kPackBits) || q > 14 || smem > cap) return cudaSuccess;
   const int pm = q <= 9 ? 1 : q <= 11 ? 3 : q == 12 ? 5 : q == 13 ? 9 : 17;
-  void (*kern)(const float*, const uint8_t*, int, int64_t, int, long long, int32_t*, float*,
-               int64_t*, int64_t*, int64_t*, CalibState*, unsigned long long*, int) =
-      pm == 1 ? calib_resident_kernel<1> : pm == 3 ? calib_resident_kernel<3>
-      : pm == 5 ? calib_resident_kernel<5> : pm == 9 ? calib_resident_kernel<9>
-                                                     : calib_resident_kernel<17>;
-  static bool attr[5] = {false, false, false, false, false};
+  using Kern = void (*)(const float*, const uint8_t*, int, int64_t, int, long long, int32_t*, float*,
+                        int64_t*, int64_t*, int64_t*, CalibState*, unsigned long long*, int, PeerCal);
+  static const Kern kerns[2][5] = {
+      {calib_resident_kernel<1, false>, calib_resident_kernel<3, false>, calib_resident_kernel<5, false>,
+       calib_resident_kernel<9, false>, calib_resident_kernel<17, false>},
+      {calib_resident_kernel<1, true>, calib_resident_kernel<3, true>, calib_resident_kernel<5, true>,
+       calib_resident_kernel<9, true>, calib_resident_kernel<17, true>}};
   const int slot = pm == 1 ? 0 : pm == 3 ? 1 : pm == 5 ? 2 : pm == 9 ? 3 : 4;
-  if (!attr[slot]) {
+  const int pe = peer ? 1 : 0;
+  Kern kern = kerns[pe][slot];
+  static bool attr[2][5] = {};
+  if (!attr[pe][slot]) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cap);
-    attr[slot] = true;
+    attr[pe][slot] = true;
   }
+  PeerCal pc{};
+  if (peer) pc = *peer;
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kResidentThreads, smem);
   if (per_sm < 1 || grid > per_sm * num_sms()) return cudaSuccess;
@@ -913,7 +995,7 @@ static cudaError_t launch_calib_resident(const float* conf, const uint8_t* corre
   int per_cta = (int)per;
   void* args[] = {(void*)&conf, (void*)&correct, (void*)&K, (void*)&N, (void*)&q, (void*)&target,
                   (void*)&b_idx, (void*)&thr, (void*)&reach, (void*)&handled,
-                  (void*)&correct_total, (void*)&st, (void*)&hist3, (void*)&per_cta};
+                  (void*)&correct_total, (void*)&st, (void*)&hist3, (void*)&per_cta, (void*)&pc};
   // cooperative (grid barriers) + programmatic dependent launch: the CTAs are
   // placed as the previous kernel's CTAs retire and wait in griddepcontrol.wait
   cudaLaunchConfig_t cfg = {};
@@ -969,6 +1051,20 @@ cudaError_t launch_calib_fused(const float* conf, const uint8_t* correct, int K,
                                               args, smem, s);
   count_launch();
   return e != cudaSuccess ? e : cudaGetLastError();
+}
+
+// Multi-GPU calibration over peer memory: the resident kernel only (the
+// samples of this rank's shard must fit its shared memory, N * world < 2^21);
+// returns cudaErrorNotSupported when it cannot be used.
+cudaError_t launch_calib_peer(const float* conf, const uint8_t* correct, int K, int64_t N, int q,
+                              long long target, int32_t* b_idx, float* thr, int64_t* reach,
+                              int64_t* handled, int64_t* correct_total, void* ws, const PeerCal& pc,
+                              cudaStream_t s) {
+  bool launched = false;
+  const cudaError_t e = launch_calib_resident(conf, correct, K, N, q, target, b_idx, thr, reach, handled,
+                                              correct_total, ws, s, &launched, &pc);
+  if (e != cudaSuccess) return e;
+  return launched ? cudaSuccess : cudaErrorNotSupported;
 }
 
 cudaError_t launch_calib_refine(const float* conf, const uint8_t* correct, int K, int64_t N, int q,

@@ -210,28 +210,48 @@ cudaError_t launch_graph(const int64_t* C, const int64_t* E, int64_t S, int64_t 
                          int64_t* front_c, int64_t* front_e, int64_t* front_s, int64_t* front_n,
                          int64_t* pick, uint32_t* status, void* ws, cudaStream_t s);
 
-// ---- multi-GPU forwarding over peer memory (forward.cu) -----------------------
-constexpr int kFwdMaxWorld = 8;
-struct FwdPeers {
-  int world;
-  unsigned long long* counts[kFwdMaxWorld];   // rank h's count array (u64[world]), peer-mapped
-  unsigned long long* done[kFwdMaxWorld];     // rank h's done array (u64[world]), peer-mapped
-  const unsigned long long* my_counts;        // this rank's count array
-  int64_t* recv_ids[kFwdMaxWorld];            // rank h's receive buffer for ids
-  void* recv_payload[kFwdMaxWorld];           // rank h's receive buffer for payload rows (or NULL)
+// ---- multi-GPU exchange over peer memory (peer.cu; calib.cu's resident kernel) --
+constexpr int kPeerMaxWorld = 8;
+struct PeerHeader {                 // start of every rank's peer region
+  unsigned long long fwd_counts[kPeerMaxWorld];   // slot g: {epoch:32 | count:32} from rank g
+  unsigned long long fwd_done[kPeerMaxWorld];     // slot g: epoch from rank g
+  unsigned long long cal_arrive[2];               // calibration pushes received, per round parity
+  unsigned fwd_epoch, fwd_ctr, fwd_failed, pad0;  // local: forward epoch, completion counter, timeout flag
+  unsigned long long cal_round;                   // local: calibration rounds run so far
+  unsigned long long pad[10];
 };
-struct FwdDest {
-  int n;                                      // destination ranks of the next stage
-  int ranks[kFwdMaxWorld];
+struct PeerLayout {                 // byte offsets inside a region (identical on every rank)
+  size_t cal_off, cal_words, recv_off, recv_stride, pay_off, bytes;
 };
-cudaError_t launch_fwd_publish(const int64_t* d_count, int64_t cap, int rank, const FwdPeers& p,
-                               unsigned epoch, cudaStream_t s);
-cudaError_t launch_fwd_scatter(const int64_t* ids, const void* payload, int64_t row_bytes, int64_t cap,
-                               int rank, const FwdPeers& p, unsigned epoch, const FwdDest& dest,
-                               int64_t* d_recv_count, unsigned* done_ctr, uint32_t* status,
-                               cudaStream_t s);
-cudaError_t launch_fwd_wait(const unsigned long long* my_done, int world, unsigned epoch, uint32_t* status,
-                            cudaStream_t s);
+PeerLayout peer_layout(int world, int64_t cap, int64_t payload_row_bytes, int q);
+struct PeerArgs {                   // the group as seen by this process
+  int world, rank;
+  int64_t recv_stride;                            // rows per receive set (world * cap)
+  PeerHeader* hdr[kPeerMaxWorld];                 // rank h's region header
+  int64_t* recv_ids[kPeerMaxWorld];               // rank h's receive sets [2][recv_stride]
+  void* recv_payload[kPeerMaxWorld];              // rank h's payload sets [2][recv_stride][P] (or NULL)
+};
+struct PeerDest {
+  int n;                                          // destination ranks of the next stage
+  int ranks[kPeerMaxWorld];
+};
+struct PeerCal {                    // calibration exchange of calib_resident_kernel
+  int world, rank;
+  unsigned long long* slots[kPeerMaxWorld];       // rank h's cal slots [2][world][2^q + 2]
+  unsigned long long* arrive[kPeerMaxWorld];      // rank h's cal_arrive[2]
+  unsigned long long* round_ctr;                  // this rank's cal_round
+  uint32_t* status;
+};
+cudaError_t launch_peer_publish(const int64_t* d_count, int64_t cap, const PeerArgs& g, uint32_t* status,
+                                cudaStream_t s);
+cudaError_t launch_peer_scatter(const int64_t* ids, const void* payload, int64_t row_bytes, int64_t cap,
+                                int set, const PeerArgs& g, const PeerDest& dest, int64_t* d_recv_count,
+                                uint32_t* status, cudaStream_t s);
+cudaError_t launch_peer_wait(const PeerArgs& g, uint32_t* status, cudaStream_t s);
+cudaError_t launch_calib_peer(const float* conf, const uint8_t* correct, int K, int64_t N, int q,
+                              long long target, int32_t* b_idx, float* thr, int64_t* reach,
+                              int64_t* handled, int64_t* correct_total, void* ws, const PeerCal& pc,
+                              cudaStream_t s);
 
 // ---- NCCL communicator (comm.cu; NCCL is dlopen-ed on first use) ---------------
 bool nccl_available();

@@ -93,98 +93,105 @@ class _DevArray:
                                          "data": (int(ptr), False), "version": 3, "strides": None}
 
 
-class PeerForwarder:
-    """Forwarding of deferred requests over peer memory (hs_forward_*): the
-    same result as :func:`forward_deferred` -- this rank's block of the global
-    stable deferred list -- moved by the kernels through CUDA IPC mappings of
-    the peers' buffers (NVLink / NVSwitch), with no host round trip and no NCCL
-    on the data path.  The IPC handles are exchanged once, at construction,
-    with ``all_gather_object`` over the process group.
+class PeerGroup:
+    """The multi-GPU group of the cascade over peer memory (hs_peer_t): one
+    region per rank (hs_ipc_alloc), mapped into every rank's process with CUDA
+    IPC -- handles exchanged once with ``all_gather_object`` over the process
+    group -- so that the library's kernels forward deferred requests
+    (hs_peer_forward, hs_cascade_step_peer) and sum the calibration histograms
+    (hs_calibrate_thresholds_peer) through NVLink / NVSwitch with no host round
+    trip and no NCCL on the data path.  ``cap``: the largest batch any rank
+    routes in a stage; ``K``: stages (one receive count per forward)."""
 
-    Buffers per rank (one exportable allocation each, hs_ipc_alloc): the count
-    and done flag arrays (u64[world]) and two receive sets (ids [world*cap],
-    payload [world*cap*P]) used on alternate stages."""
-
-    def __init__(self, cap: int, payload_row_bytes: int = 0, group=None, device=None):
+    def __init__(self, cap: int, payload_row_bytes: int = 0, log2_bins: int = 12, K: int = 8,
+                 group=None, device=None, *, _local=None):
         import ctypes
-        from . import lib, _abi
-        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
-        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
-        self.cap, self.P = int(cap), int(payload_row_bytes)
+        from . import _abi, peer_region_bytes
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
-        W = self.world
-        sizes = {"counts": 8 * W, "done": 8 * W,
-                 "ids0": 8 * W * self.cap, "ids1": 8 * W * self.cap}
-        if self.P:
-            sizes.update(pay0=W * self.cap * self.P, pay1=W * self.cap * self.P)
-        self._own = {}
-        for k, b in sizes.items():
-            p = ctypes.c_void_p()
-            _abi.call("hs_ipc_alloc", max(int(b), 16), ctypes.byref(p))
-            self._own[k] = int(p.value)
-        handles = {}
-        for k, p in self._own.items():
-            h = ctypes.create_string_buffer(64)
-            if W > 1:
-                _abi.call("hs_ipc_handle", p, h)
-            handles[k] = bytes(h.raw)
-        allh = [None] * W
-        if W > 1:
-            dist.all_gather_object(allh, handles, group=group)
+        if _local is not None:                      # one process driving several ranks (tests)
+            self.rank, self.world, regions = _local
+            self._own, self._opened = None, []
         else:
-            allh = [handles]
-        self._opened = []
-        self.peer = {k: [0] * W for k in self._own}
-        for h in range(W):
-            for k in self._own:
-                if h == self.rank:
-                    self.peer[k][h] = self._own[k]
-                else:
-                    p = ctypes.c_void_p()
-                    hb = ctypes.create_string_buffer(allh[h][k], 64)
-                    _abi.call("hs_ipc_open", hb, ctypes.byref(p))
-                    self.peer[k][h] = int(p.value)
-                    self._opened.append(int(p.value))
-        self.ws = torch.zeros(256, dtype=torch.uint8, device=self.device)
-        self.recv_count = torch.zeros(1, dtype=torch.int64, device=self.device)
-        self.status = torch.zeros(1, dtype=torch.int32, device=self.device)   # STATUS_TIMEOUT
-        self.epoch = 0
-        self._lib = lib
+            self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+            self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+            nbytes = peer_region_bytes(self.world, cap, payload_row_bytes, log2_bins)
+            p = ctypes.c_void_p()
+            _abi.call("hs_ipc_alloc", max(nbytes, 256), ctypes.byref(p))
+            self._own = int(p.value)
+            self._opened = []
+            regions = [0] * self.world
+            regions[self.rank] = self._own
+            if self.world > 1:
+                h = ctypes.create_string_buffer(64)
+                _abi.call("hs_ipc_handle", self._own, h)
+                allh = [None] * self.world
+                dist.all_gather_object(allh, bytes(h.raw), group=group)
+                for r in range(self.world):
+                    if r == self.rank:
+                        continue
+                    q = ctypes.c_void_p()
+                    _abi.call("hs_ipc_open", ctypes.create_string_buffer(allh[r], 64), ctypes.byref(q))
+                    regions[r] = int(q.value)
+                    self._opened.append(int(q.value))
+        g = _abi.PeerGroup()
+        g.rank, g.world, g.cap = self.rank, self.world, int(cap)
+        g.payload_row_bytes, g.log2_bins = int(payload_row_bytes), int(log2_bins)
+        for r in range(self.world):
+            g.region[r] = regions[r]
+        self.g = g
+        self.cap, self.P, self.q = int(cap), int(payload_row_bytes), int(log2_bins)
+        self.recv_count = torch.zeros(max(K - 1, 1), dtype=torch.int64, device=self.device)
+        self.status = torch.zeros(1, dtype=torch.int32, device=self.device)
 
-    def recv_ids(self, parity: int) -> torch.Tensor:
-        return torch.as_tensor(_DevArray(self._own[f"ids{parity}"], (self.world * self.cap,), "<i8"),
-                               device=self.device)
+    @classmethod
+    def local_group(cls, world: int, cap: int, payload_row_bytes: int = 0, log2_bins: int = 12,
+                    K: int = 8, device=None):
+        """``world`` ranks driven by ONE process on one GPU (virtual ranks, for
+        tests): the regions are plain allocations shared by pointer."""
+        import ctypes
+        from . import _abi, peer_region_bytes
+        nbytes = peer_region_bytes(world, cap, payload_row_bytes, log2_bins)
+        regions = []
+        for _ in range(world):
+            p = ctypes.c_void_p()
+            _abi.call("hs_ipc_alloc", max(nbytes, 256), ctypes.byref(p))
+            regions.append(int(p.value))
+        ranks = [cls(cap, payload_row_bytes, log2_bins, K, device=device, _local=(r, world, regions))
+                 for r in range(world)]
+        ranks[0]._owned_local = regions
+        return ranks
 
-    def recv_payload(self, parity: int) -> torch.Tensor | None:
+    def recv_ids(self, set_: int) -> torch.Tensor:
+        from . import lib
+        import ctypes
+        ptr = lib().hs_peer_recv_ids(ctypes.byref(self.g), int(set_))
+        return torch.as_tensor(_DevArray(ptr, (self.world * self.cap,), "<i8"), device=self.device)
+
+    def recv_payload(self, set_: int):
+        from . import lib
+        import ctypes
         if not self.P:
             return None
-        return torch.as_tensor(_DevArray(self._own[f"pay{parity}"], (self.world * self.cap, self.P), "|u1"),
-                               device=self.device)
+        ptr = lib().hs_peer_recv_payload(ctypes.byref(self.g), int(set_))
+        return torch.as_tensor(_DevArray(ptr, (self.world * self.cap, self.P), "|u1"), device=self.device)
 
-    def forward(self, ids: torch.Tensor, count: torch.Tensor, *, dest_ranks: list[int] | None = None,
-                payload: torch.Tensor | None = None, stream=None):
-        """Forward this rank's compacted deferred list ``ids[:count]`` (``count``:
-        device int64[1], e.g. d_counts[1:2]).  Returns (recv_ids, recv_payload,
-        recv_count) -- device tensors of this forward's receive set (alternating),
-        recv_count a device int64[1]; nothing is read back to the host."""
-        from . import forward_publish, forward_scatter, forward_wait
-        self.epoch += 1
-        par = self.epoch & 1
-        dest = list(range(self.world)) if dest_ranks is None else list(dest_ranks)
-        forward_publish(count, self.cap, self.rank, self.peer["counts"], self.epoch, stream=stream)
-        forward_scatter(ids, self.cap, self.rank, self._own["counts"], self.peer["done"],
-                        self.peer[f"ids{par}"], dest, self.epoch, self.recv_count, self.ws,
-                        payload=payload, payload_row_bytes=self.P if payload is not None else 0,
-                        peer_recv_payload=self.peer.get(f"pay{par}"), status=self.status,
-                        stream=stream)
-        forward_wait(self._own["done"], self.world, self.epoch, status=self.status, stream=stream)
-        return self.recv_ids(par), self.recv_payload(par), self.recv_count
+    def forward(self, stage: int, ids: torch.Tensor, count: torch.Tensor, *, payload=None,
+                dest_ranks=None, stream=None):
+        """Forward this rank's deferred list ``ids[:count]`` after stage
+        ``stage`` (receive set stage % 2).  Returns (recv_ids, recv_payload,
+        recv_count) -- device tensors; nothing is read back to the host."""
+        from . import peer_forward
+        peer_forward(self.g, stage % 2, ids, count, self.recv_count[stage:stage + 1], payload=payload,
+                     dest_ranks=dest_ranks, status=self.status, stream=stream)
+        return self.recv_ids(stage % 2), self.recv_payload(stage % 2), self.recv_count[stage:stage + 1]
 
     def close(self):
         from . import _abi
         torch.cuda.synchronize(self.device)
         for p in self._opened:
             _abi.call("hs_ipc_close", p)
-        for p in self._own.values():
+        if self._own:
+            _abi.call("hs_ipc_free", self._own)
+        for p in getattr(self, "_owned_local", []):
             _abi.call("hs_ipc_free", p)
-        self._opened, self._own = [], {}
+        self._opened, self._own, self._owned_local = [], None, []

@@ -1,12 +1,16 @@
 """The user-facing router: calibrate thresholds on a validation set, then route
 batches through the cascade -- a sequence of C-ABI calls, nothing else.
 
-One ``Router`` per GPU.  With a ``torch.distributed`` process group the
-validation set and the request stream are sharded over the ranks: the only
-exchange is the integer calibration histogram, summed with an all-reduce
-between ``hs_calibrate_histogram`` and ``hs_calibrate_select`` (order-independent
-count merging), so every rank selects identical thresholds.  Forwarding
-deferred requests to other ranks is in ``dist.py``.
+One ``Router`` per GPU.  With a ``dist.PeerGroup`` (``peer=``) the validation
+set and the request stream are sharded over the ranks and every exchange runs
+inside the library over peer memory: the integer calibration histograms are
+summed inside the calibration kernel (hs_calibrate_thresholds_peer), and the
+deferred requests of every stage are forwarded to the next stage's ranks
+(hs_cascade_step_peer) -- the whole calibrate + K-stage step is one CUDA graph
+with no host round trip.  With a ``torch.distributed`` process group instead,
+the histograms are summed with an all-reduce between ``hs_calibrate_histogram``
+and ``hs_calibrate_select`` (order-independent count merging), or by the
+library's own NCCL communicator (``native_comm``).
 """
 from __future__ import annotations
 
@@ -16,6 +20,7 @@ import dataclasses
 
 from . import (Cascade, StageSpec, _calib_out, calibrate_begin, calibrate_hist_view,
                calibrate_histogram, calibrate_select, calibrate_thresholds, calibrate_thresholds_comm,
+               calibrate_thresholds_peer,
                calibrate_workspace, confidence, confidence_batched, cascade_step, fit_temperature,
                perf_graph, route_compact, threshold_replay)
 
@@ -23,7 +28,7 @@ from . import (Cascade, StageSpec, _calib_out, calibrate_begin, calibrate_hist_v
 class Router:
     def __init__(self, stages: list[StageSpec], n_cap: int, n_val: int, device, *,
                  log2_bins: int = 12, payload_row_bytes: int = 0, group=None,
-                 native_comm: bool = False):
+                 native_comm: bool = False, peer=None):
         self.stages = stages
         self.K = len(stages)
         self.n_cap = int(n_cap)
@@ -31,6 +36,7 @@ class Router:
         self.q = int(log2_bins)
         self.device = torch.device(device)
         self.group = group
+        self.peer = peer
         dev = self.device
         K = self.K
         # validation confidences of all K stages: rows 0..K-2 are the calibration input
@@ -92,7 +98,11 @@ class Router:
                            stream=stream)
         if time_val is not None:
             time_val[1].record()
-        if self.hs_comm is not None:
+        if self.peer is not None:
+            calibrate_thresholds_peer(self.vconf, self.vok, self.peer.g, log2_bins=self.q, target=target,
+                                      out=self.cal, ws=self.cal_ws, status=self.peer.status,
+                                      stream=stream)
+        elif self.hs_comm is not None:
             calibrate_thresholds_comm(self.vconf, self.vok, self.hs_comm, log2_bins=self.q,
                                       target=target, out=self.cal, ws=self.cal_ws, stream=stream)
         elif self.group is None:
@@ -160,12 +170,14 @@ class Router:
 
     # ---- online: the cascade ------------------------------------
     def route(self, logits: list, *, n: int | None = None, ids=None, payload=None,
-              by_id: bool = True, thresholds=None, overlap_first: bool = False, stream=None):
+              by_id: bool = True, thresholds=None, overlap_first: bool = False, next_ranks=None,
+              stream=None):
         """Route a batch; thresholds default to the calibrated device vector.
         ``overlap_first``: stage 1's confidence runs next to the calibration
         (HS_STEP_OVERLAP_PREVIOUS; it reads neither the calibration's buffers nor
         is read by it -- only the threshold test waits for the thresholds)."""
         thr = self.cal["t"] if thresholds is None else thresholds
         self.cascade.route(logits, thr, n=n, ids=ids, payload=payload, by_id=by_id,
-                           overlap_first=overlap_first, stream=stream)
+                           overlap_first=overlap_first, peer=self.peer, next_ranks=next_ranks,
+                           stream=stream)
         return self.cascade

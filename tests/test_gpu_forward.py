@@ -1,11 +1,19 @@
-"""GPU check of the peer-memory forwarding of deferred requests (hs_forward_*,
-SURVEY 8(e) v2): W virtual ranks on ONE GPU, each with its own count / done
-arrays and receive buffers, addressed through the same pointer tables a real
-multi-GPU group builds from CUDA IPC mappings.  After publish -> scatter ->
-wait, every destination rank must hold exactly its contiguous block of the
-GLOBAL stable deferred list (rank-major concatenation of the per-rank lists
-given by the oracle's stable split), with its payload rows; the same
-buffers are reused for a second forward (epochs, re-armed counter)."""
+"""GPU checks of the multi-GPU exchange over peer memory (hs_peer_*, SURVEY
+8(e)): W virtual ranks on ONE GPU, each with its own peer region,
+addressed through the same hs_peer_t pointer tables a real multi-GPU group
+builds from CUDA IPC mappings (dist.PeerGroup.local_group).
+
+* forwarding: after publish -> scatter -> wait, every destination rank holds
+  exactly its contiguous block of the GLOBAL stable deferred list (rank-major
+  concatenation of the per-rank lists given by the oracle's stable split,
+  P:443-444), with its payload rows; the regions are reused over several
+  forwards (device epochs, re-armed completion counter, alternating sets).
+* calibration: every virtual rank runs hs_calibrate_thresholds_peer on its
+  shard of a validation set (one stream per rank, so the W cooperative kernels
+  run side by side) and must select exactly the thresholds the oracle selects
+  on the WHOLE set (the pushed histograms are summed inside the kernel).
+* the comm-aware cascade step (hs_cascade_step_peer) over W virtual ranks
+  equals the oracle's cascade of the whole batch."""
 import numpy as np
 import pytest
 import torch
@@ -25,86 +33,178 @@ def _payload_of(ids: np.ndarray, P: int) -> np.ndarray:
     return ((ids[:, None] * 7 + np.arange(P)[None, :]) % 251).astype(np.uint8)
 
 
+def _expected_blocks(conf_all, bounds, t, dest, world):
+    glob = np.concatenate([bounds[g] + oracle.route(conf_all[bounds[g]:bounds[g + 1]], t, False)[1]
+                           for g in range(world)]).astype(np.int64)
+    lo_b = hsd.block_bounds(len(glob), len(dest))
+    return [np.concatenate([glob[lo_b[i]:lo_b[i + 1]] for i, h in enumerate(dest) if h == g] or
+                           [np.zeros(0, np.int64)]) for g in range(world)]
+
+
 @pytest.mark.parametrize("world,dest,P", [(1, None, 16), (2, None, 0), (3, None, 32), (3, [2], 16),
-                                          (4, [0, 2], 0), (8, [7, 1, 4], 48)])
-def test_peer_forward_virtual_ranks(hs, world, dest, P):
+                                          (4, [0, 2], 0), (8, [7, 1, 4], 48), (8, None, 0)])
+@pytest.mark.parametrize("fused", [False, True])
+def test_peer_forward_virtual_ranks(hs, world, dest, P, fused):
+    """fused=False: the three phases for all ranks in turn on one stream;
+    fused=True: hs_peer_forward per rank on its own stream (the kernels of the
+    ranks run side by side and synchronise through the flags)."""
     dev = torch.device("cuda:0")
     n = 6001
     rng = np.random.default_rng(world * 10 + P)
     conf_all = rng.random(n).astype(np.float32)
-    dest = list(range(world)) if dest is None else dest
+    destl = list(range(world)) if dest is None else dest
     bounds = [g * n // world for g in range(world + 1)]
     cap = max(bounds[g + 1] - bounds[g] for g in range(world))
-    counts = [torch.zeros(world, dtype=torch.int64, device=dev) for _ in range(world)]
-    done = [torch.zeros(world, dtype=torch.int64, device=dev) for _ in range(world)]
-    recv_ids = [torch.full((world * cap,), -1, dtype=torch.int64, device=dev) for _ in range(world)]
-    recv_pay = [torch.zeros(world * cap * max(P, 16), dtype=torch.uint8, device=dev) for _ in range(world)]
-    wss = [torch.zeros(256, dtype=torch.uint8, device=dev) for _ in range(world)]
-    rcnt = [torch.zeros(1, dtype=torch.int64, device=dev) for _ in range(world)]
-    for epoch, t in ((1, 0.6), (2, 0.25), (3, 0.97), (4, 0.0), (5, 0.5)):
+    if dest is not None:
+        cap = n      # placed blocks can exceed a rank's shard
+    grp = hsd.PeerGroup.local_group(world, cap, P, 12, K=8, device=dev)
+    streams = [torch.cuda.Stream(device=dev) for _ in range(world)]
+    for it, t in enumerate((0.6, 0.25, 0.97, 0.0, 0.5, 1.0)):
         outs = []
         for g in range(world):
             lo, hi = bounds[g], bounds[g + 1]
             ids = torch.arange(lo, hi, dtype=torch.int64, device=dev)
             pay = torch.from_numpy(_payload_of(np.arange(lo, hi), P)).to(dev) if P else None
-            o = hs.route_compact(torch.from_numpy(conf_all[lo:hi]).to(dev), t, ids=ids, payload=pay)
-            outs.append(o)
-        for g in range(world):
-            hs.forward_publish(outs[g]["counts"][1:2], cap, g, [c.data_ptr() for c in counts], epoch)
-        for g in range(world):
-            hs.forward_scatter(outs[g]["def_ids"], cap, g, counts[g], [d.data_ptr() for d in done],
-                               [r.data_ptr() for r in recv_ids], dest, epoch, rcnt[g], wss[g],
-                               payload=outs[g].get("def_payload"), payload_row_bytes=P,
-                               peer_recv_payload=[r.data_ptr() for r in recv_pay] if P else None)
-        for g in range(world):
-            hs.forward_wait(done[g], world, epoch)
+            outs.append(hs.route_compact(torch.from_numpy(conf_all[lo:hi]).to(dev), t, ids=ids, payload=pay))
         torch.cuda.synchronize()
-        # expected: the oracle's per-rank stable deferred lists, concatenated, split into blocks
-        glob = np.concatenate([bounds[g] + oracle.route(conf_all[bounds[g]:bounds[g + 1]], t, False)[1]
-                               for g in range(world)]).astype(np.int64)
-        lo_b = hsd.block_bounds(len(glob), len(dest))
+        st = it % 2
+        rc = [grp[g].recv_count[it:it + 1] for g in range(world)]
+        if fused:
+            for g in range(world):
+                hs.peer_forward(grp[g].g, st, outs[g]["def_ids"], outs[g]["counts"][1:2], rc[g],
+                                payload=outs[g].get("def_payload"), dest_ranks=dest,
+                                status=grp[g].status, stream=streams[g])
+        else:
+            for g in range(world):
+                hs.peer_forward_publish(grp[g].g, outs[g]["counts"][1:2], status=grp[g].status)
+            for g in range(world):
+                hs.peer_forward_scatter(grp[g].g, st, outs[g]["def_ids"], rc[g],
+                                        payload=outs[g].get("def_payload"), dest_ranks=dest,
+                                        status=grp[g].status)
+            for g in range(world):
+                hs.peer_forward_wait(grp[g].g, status=grp[g].status)
+        torch.cuda.synchronize()
+        want = _expected_blocks(conf_all, bounds, t, destl, world)
         for g in range(world):
-            want = np.concatenate([glob[lo_b[i]:lo_b[i + 1]] for i, h in enumerate(dest) if h == g] or
-                                  [np.zeros(0, np.int64)])
-            got_n = int(rcnt[g].item())
-            assert got_n == len(want), (epoch, g)
-            assert np.array_equal(recv_ids[g][:got_n].cpu().numpy(), want), (epoch, g)
+            assert int(grp[g].status.item()) == 0
+            got_n = int(rc[g].item())
+            assert got_n == len(want[g]), (it, g)
+            assert np.array_equal(grp[g].recv_ids(st)[:got_n].cpu().numpy(), want[g]), (it, g)
             if P:
-                got_p = recv_pay[g][: got_n * P].cpu().numpy().reshape(got_n, P)
-                assert np.array_equal(got_p, _payload_of(want, P)), (epoch, g)
-        assert all(int(w.sum()) == 0 for w in wss)              # completion counters re-armed
-        assert all((c.cpu().numpy() >> 32 == epoch).all() for c in counts)
+                got_p = grp[g].recv_payload(st)[:got_n].cpu().numpy()
+                assert np.array_equal(got_p, _payload_of(want[g], P)), (it, g)
+    grp[0].close()
 
 
-def test_forward_argument_errors(hs):
+def test_peer_forward_argument_errors(hs):
     dev = torch.device("cuda:0")
+    grp = hsd.PeerGroup.local_group(2, 16, 0, 12, device=dev)
     c = torch.zeros(2, dtype=torch.int64, device=dev)
-    ws = torch.zeros(256, dtype=torch.uint8, device=dev)
     with pytest.raises(hs.HsError):
-        hs.forward_publish(c[:1], 10, 0, [c.data_ptr()] * 2, 0)          # epoch 0
+        hs.peer_forward(grp[0].g, 2, c, c[:1], c[1:])                     # set outside {0, 1}
     with pytest.raises(hs.HsError):
-        hs.forward_scatter(c, 10, 0, c, [c.data_ptr()] * 2, [c.data_ptr()] * 2, [1, 1], 1, c[:1], ws)
+        hs.peer_forward(grp[0].g, 0, c, c[:1], c[1:], dest_ranks=[1, 1])  # repeated destination
     with pytest.raises(hs.HsError):
-        hs.forward_wait(c, 9, 1)
+        hs.peer_forward(grp[0].g, 0, c, c[:1], c[1:], payload=c)          # regions sized without payload
+    bad = hsd.PeerGroup.local_group(2, 16, 0, 12, device=dev)[0].g
+    bad.world = 9
+    with pytest.raises(hs.HsError):
+        hs.peer_forward(bad, 0, c, c[:1], c[1:])
+    grp[0].close()
 
 
-def test_forward_times_out_instead_of_hanging(hs):
+def test_peer_forward_times_out_instead_of_hanging(hs):
     """A peer that never publishes: the scatter and wait kernels give up after
-    10 s, flag STATUS_TIMEOUT and write nothing (the GPU is not hung)."""
+    10 s, flag STATUS_TIMEOUT, receive nothing (the GPU is not hung); the
+    completion counter is re-armed, so a later forward works."""
     dev = torch.device("cuda:0")
-    W = 2
-    counts = [torch.zeros(W, dtype=torch.int64, device=dev) for _ in range(W)]
-    done = [torch.zeros(W, dtype=torch.int64, device=dev) for _ in range(W)]
-    recv = [torch.full((8,), -7, dtype=torch.int64, device=dev) for _ in range(W)]
-    ws = torch.zeros(256, dtype=torch.uint8, device=dev)
-    st = torch.zeros(1, dtype=torch.int32, device=dev)
-    rc = torch.zeros(1, dtype=torch.int64, device=dev)
+    grp = hsd.PeerGroup.local_group(2, 8, 0, 12, device=dev)
     ids = torch.arange(4, dtype=torch.int64, device=dev)
     cnt = torch.tensor([4], dtype=torch.int64, device=dev)
-    hs.forward_publish(cnt, 4, 0, [c.data_ptr() for c in counts], 1)      # rank 1 never publishes
-    hs.forward_scatter(ids, 4, 0, counts[0], [d.data_ptr() for d in done], [r.data_ptr() for r in recv],
-                       [0, 1], 1, rc, ws, status=st)
-    hs.forward_wait(done[0], W, 1, status=st)
+    rc = grp[0].recv_count[:1]
+    hs.peer_forward(grp[0].g, 0, ids, cnt, rc, status=grp[0].status)      # rank 1 never publishes
     torch.cuda.synchronize()
-    assert int(st.item()) & hs.STATUS_TIMEOUT
-    assert (recv[0] == -7).all() and (recv[1] == -7).all()
+    assert int(grp[0].status.item()) & hs.STATUS_TIMEOUT
+    assert int(rc.item()) == 0
+
+
+def _calib_case(seed, n, K):
+    rng = np.random.default_rng(seed)
+    d = rng.uniform(size=n)
+    ok = np.stack([(d + 0.3 * rng.normal(size=n) < 0.5 + 0.08 * k) for k in range(K)]).astype(np.uint8)
+    conf = np.clip(np.where(ok[:K - 1] == 1, rng.beta(5, 2, (K - 1, n)), rng.beta(2, 3, (K - 1, n))),
+                   0, 1).astype(np.float32)
+    conf[0, :: 97] = 1.0
+    return conf, ok
+
+
+@pytest.mark.parametrize("world,n,q,K", [(1, 3000, 12, 5), (2, 7000, 12, 5), (3, 9001, 10, 4),
+                                         (4, 20000, 12, 5), (8, 16000, 8, 3), (2, 1, 4, 2)])
+def test_peer_calibration_equals_oracle_on_the_whole_set(hs, world, n, q, K):
+    dev = torch.device("cuda:0")
+    conf, ok = _calib_case(world * 100 + n, n, K)
+    ref = oracle.calibrate(conf.astype(np.float64), ok, q)
+    grp = hsd.PeerGroup.local_group(world, 16, 0, q, device=dev)
+    bounds = [g * n // world for g in range(world + 1)]
+    streams = [torch.cuda.Stream(device=dev) for _ in range(world)]
+    outs = []
+    for rep in range(3):                 # regions reused: round counters advance
+        outs = []
+        for g in range(world):
+            lo, hi = bounds[g], bounds[g + 1]
+            c = torch.from_numpy(np.ascontiguousarray(conf[:, lo:hi])).to(dev)
+            o = torch.from_numpy(np.ascontiguousarray(ok[:, lo:hi])).to(dev)
+            outs.append((c, o))
+        torch.cuda.synchronize()
+        res = [hs.calibrate_thresholds_peer(outs[g][0], outs[g][1], grp[g].g, log2_bins=q,
+                                            status=grp[g].status, stream=streams[g])
+               for g in range(world)]
+        torch.cuda.synchronize()
+        for g in range(world):
+            assert int(grp[g].status.item()) == 0
+            assert np.array_equal(res[g]["b"].cpu().numpy(), ref["b"]), (rep, g)
+            assert int(res[g]["correct_total"].item()) == ref["correct_total"]
+            assert np.array_equal(res[g]["reach"].cpu().numpy(), ref["reach"])
+            assert np.array_equal(res[g]["handled"].cpu().numpy(), ref["handled"])
+    grp[0].close()
+
+
+@pytest.mark.parametrize("world", [1, 2, 4])
+def test_peer_cascade_step_equals_oracle_cascade(hs, world):
+    """The comm-aware cascade step over W virtual ranks (balanced placement):
+    the union of the accepted lists of stage k over all ranks equals the
+    oracle's stage-k list of the whole batch (a request's stage does not
+    depend on where it was routed)."""
+    from workload import synth
+    dev = torch.device("cuda:0")
+    fam = synth.scaled(synth.FAMILIES["c2"], n=3000)
+    K, n, C = fam.K, fam.n, fam.C
+    ids_all = np.arange(n, dtype=np.int64)
+    logits = [torch.from_numpy(synth.fam_logits_np(fam, k, ids_all).view(np.int16)).to(dev).view(torch.bfloat16)
+              for k in range(K)]
+    t = [float(np.float32(x)) for x in (0.55, 0.3, 0.6, 0.45, 0.0)]
+    conf = np.stack([oracle.confidence(logits[k].view(torch.int16).cpu().numpy().view(np.uint16), n, 1, C, C,
+                                       fam.temps[k])["conf"] for k in range(K)])
+    stage_of = oracle.cascade(conf, np.array(t, np.float64))
+    near = np.zeros(n, bool)
+    for k in range(K - 1):
+        near |= np.abs(conf[k] - t[k]) <= 1e-5 * t[k]
+    bounds = [g * n // world for g in range(world + 1)]
+    cap = max(bounds[g + 1] - bounds[g] for g in range(world))
+    grp = hsd.PeerGroup.local_group(world, cap, 0, 12, K=K, device=dev)
+    casc = [__import__("paper_2505_12566_b200").Cascade(cap, [
+        __import__("paper_2505_12566_b200").StageSpec(C, fam.temps[k]) for k in range(K)], dev)
+        for _ in range(world)]
+    streams = [torch.cuda.Stream(device=dev) for _ in range(world)]
+    thr = torch.tensor(t, dtype=torch.float32, device=dev)
+    for g in range(world):
+        ids = torch.arange(bounds[g], bounds[g + 1], dtype=torch.int64, device=dev)
+        casc[g].route(logits, thr, n=bounds[g + 1] - bounds[g], ids=ids, by_id=True, peer=grp[g],
+                      stream=streams[g])
+    torch.cuda.synchronize()
+    for k in range(K):
+        got = np.sort(np.concatenate([casc[g].results()[k]["ids"].numpy() for g in range(world)]))
+        want = np.flatnonzero(stage_of == k)
+        assert np.array_equal(got[~near[got]], want[~near[want]]), k
+    assert all(int(grp[g].status.item()) == 0 for g in range(world))
+    grp[0].close()
