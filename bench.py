@@ -65,12 +65,22 @@ def parse():
                          "gathers its rows; dense: stage k's logits are the dense batch of "
                          "the requests that reach model k, in order (the model ran on that "
                          "batch only, P:320-322)")
-    ap.add_argument("--placement", default="local", choices=["local", "balanced", "p2p"],
-                    help="local: every rank serves every stage (no data-path collective); "
-                         "balanced: deferred requests are re-spread over all ranks after "
-                         "every stage with an NCCL all-to-all (dist.forward_deferred); "
-                         "p2p: the same re-spread by the hs_forward_* kernels over peer "
-                         "memory (dist.PeerForwarder), graph-captured")
+    ap.add_argument("--placement", default="balanced", choices=["balanced", "local", "nccl"],
+                    help="balanced (default): after every stage the global stable deferred list is "
+                         "re-spread in contiguous blocks over all ranks by the library's kernels over "
+                         "peer memory (hs_cascade_step_peer; calibration histograms summed inside the "
+                         "calibration kernel, hs_calibrate_thresholds_peer) -- one CUDA graph per "
+                         "step, no host round trip; at one GPU the exchange is the identity. "
+                         "local: every rank serves every stage of its own shard (replicas, no "
+                         "exchange).  nccl: the balanced re-spread with torch.distributed NCCL "
+                         "(count all-gather + all-to-all, host split sizes, eager) -- the baseline")
+    ap.add_argument("--plumbing-check", action="store_true",
+                    help="CPU self-test of the multi-rank launcher (no GPU): every rank joins a gloo "
+                         "group, exchanges a handle with all_gather_object and reduces with the "
+                         "bench's max/sum helpers; rank 0 prints one JSON line")
+    ap.add_argument("--share-gpu", action="store_true",
+                    help="test mode: every rank uses cuda:0 (several processes time-slice one GPU; "
+                         "plumbing over gloo) -- exercises the multi-process peer path on one GPU")
     return ap.parse_args()
 
 
@@ -137,17 +147,34 @@ class ClockSampler:
 # distributed plumbing
 # ---------------------------------------------------------------------------
 def init_dist(args, force: bool = False):
+    """One process per GPU (torchrun env).  torch.distributed is plumbing only
+    (barriers, max-over-ranks timing, the one-time IPC handle exchange); the
+    data path of the balanced placement runs in libhs over peer memory.
+    --share-gpu: every rank on cuda:0 with gloo plumbing (test mode)."""
     import torch
     import torch.distributed as dist
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.share_gpu:
+        local = 0
+    if world > 1 and not args.share_gpu and torch.cuda.device_count() < world:
+        raise SystemExit(f"bench: {world} ranks need {world} visible GPUs, found {torch.cuda.device_count()}")
+    torch.cuda.set_device(local)
     if world > 1 or force:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    else:
-        torch.cuda.set_device(0)
+        if args.share_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     return world, rank, local
+
+
+def _dist_tensor(x, dtype):
+    """A tensor on the device the process group's backend reduces on."""
+    import torch
+    import torch.distributed as dist
+    dev = "cpu" if dist.get_backend() == "gloo" else "cuda"
+    return torch.tensor(x, dtype=dtype, device=dev)
 
 
 def barrier(world):
@@ -156,14 +183,15 @@ def barrier(world):
         dist.barrier()
 
 
-def max_over_ranks(x: float, world: int) -> float:
+def max_over_ranks(x, world: int):
+    """Element-wise max over ranks of a float or a list of floats."""
     if world == 1:
         return x
     import torch
     import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    t = _dist_tensor(x if isinstance(x, list) else [x], torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    return float(t.item())
+    return t.tolist() if isinstance(x, list) else float(t[0].item())
 
 
 def sum_over_ranks(x, world: int):
@@ -171,7 +199,7 @@ def sum_over_ranks(x, world: int):
         return x
     import torch
     import torch.distributed as dist
-    t = torch.tensor(x, dtype=torch.float64, device="cuda")
+    t = _dist_tensor(x, torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.SUM)
     return t.tolist()
 
@@ -237,23 +265,32 @@ def committed_traffic(config: str, name: str = "r01_k1_traffic.json"):
     return rec.get("dram_bytes_per_launch") if rec.get("config") == config else None
 
 
-def dense_stage_logits(fam, router, route, val, labels, payload, rank, dev):
+def dense_stage_logits(fam, router, route, val, labels, payload, rank, dev, ids0=None):
     """--layout dense: run the step once (untimed) to learn which requests reach
-    each model, then regenerate stage k's logits (same keyed generator, so the
-    same values per request) as the dense batch of exactly those requests in
-    order -- what model m_k produces when it runs on its batch only.  The
-    cascade is deterministic, so every timed step routes the same batches."""
+    each model (on this rank), then regenerate stage k's logits (same keyed
+    generator, so the same values per request) as the dense batch of exactly
+    those requests in order -- what model m_k produces when it runs on its
+    batch only.  The cascade is deterministic, so every timed step routes the
+    same batches.  With a peer group the batch of stage k >= 2 on this rank is
+    the block it RECEIVED from the forward after stage k-1."""
     import torch
     import workload
     router.calibrate(val, labels)
-    router.route(route, payload=payload)
+    router.route(route, ids=ids0, payload=payload, by_id=False)
     torch.cuda.synchronize()
     counts = router.cascade.counts.cpu().tolist()
     tdt = torch.bfloat16 if fam.dtype == "bf16" else torch.float32
     out = [route[0]]
+    batch = []
+    peer = router.peer
     for k in range(1, fam.K):
-        nk = int(counts[k - 1][1])
-        ids = router.cascade.outs[k - 1]["next_ids"][:nk].clone() + rank * fam.n
+        if peer is not None:
+            nk = int(peer.recv_count[k - 1].item())
+            ids = peer.recv_ids((k - 1) % 2)[:nk].clone()
+        else:
+            nk = int(counts[k - 1][1])
+            ids = router.cascade.outs[k - 1]["next_ids"][:nk].clone() + rank * fam.n
+        batch.append(nk)
         x = torch.empty(max(nk, 1) * fam.L, fam.C, dtype=tdt, device=dev)
         if nk:
             workload.gpu_logits(x, fam, k, ids=ids, n=nk)
@@ -262,16 +299,27 @@ def dense_stage_logits(fam, router, route, val, labels, payload, rank, dev):
         route[k] = None                    # the full-population tensors are not needed
     torch.cuda.synchronize()
     torch.cuda.empty_cache()
-    return out, counts
+    return out, (counts, batch)
 
 
-def make_router(fam, dev, group, native_comm: bool = False):
+def dense_signature(router, fam):
+    import torch
+    counts = router.cascade.counts.cpu().tolist()
+    batch = []
+    if router.peer is not None:
+        batch = [int(x) for x in router.peer.recv_count[: fam.K - 1].cpu().tolist()]
+    else:
+        batch = [int(c[1]) for c in counts[:-1]]
+    return counts, batch
+
+
+def make_router(fam, dev, group, native_comm: bool = False, peer=None):
     import paper_2505_12566_b200 as hs
     from paper_2505_12566_b200.router import Router
     stages = [hs.StageSpec(fam.C, fam.temps[k], fam.L, fam.kind, fam.reduce, fam.top_k)
               for k in range(fam.K)]
     return Router(stages, fam.n, fam.n_val, dev, log2_bins=fam.log2_bins,
-                  payload_row_bytes=fam.payload_bytes, group=group, native_comm=native_comm)
+                  payload_row_bytes=fam.payload_bytes, group=group, native_comm=native_comm, peer=peer)
 
 
 def timing_event():
@@ -285,25 +333,44 @@ def timing_event():
 
 
 def run_ours(args, world, rank, local):
+    """The step of every config but c2g / c2t: calibration + K-stage routing.
+    world > 1 with the balanced placement: a dist.PeerGroup -- the calibration
+    histograms are summed inside the calibration kernel and every stage's
+    deferred list is forwarded to its global block over peer memory, all inside
+    one CUDA graph (hs_calibrate_thresholds_peer, hs_cascade_step_peer)."""
     import torch
     import torch.distributed as dist
     import paper_2505_12566_b200 as hs
+    from paper_2505_12566_b200 import dist as hsd
 
     dev = torch.device("cuda", local)
     fam = family(args.config)
     group = dist.group.WORLD if dist.is_initialized() else None
     route, val, labels, payload = build_inputs(fam, rank, dev)
-    router = make_router(fam, dev, group, native_comm=args.native_comm)
+    peer = None
+    if world > 1 and args.placement == "balanced":
+        peer = hsd.PeerGroup(fam.n, fam.payload_bytes, fam.log2_bins, K=fam.K, group=group, device=dev)
+    router = make_router(fam, dev, None if peer is not None else group, native_comm=args.native_comm,
+                         peer=peer)
+    ids0 = (torch.arange(rank * fam.n, (rank + 1) * fam.n, dtype=torch.int64, device=dev)
+            if peer is not None else None)
     ev = (timing_event(), timing_event())
     dense = args.layout == "dense"
+    if peer is not None and not dense:
+        raise SystemExit("bench: the balanced placement routes dense stage batches (--layout dense)")
     if dense:
-        route, dense_counts = dense_stage_logits(fam, router, route, val, labels, payload, rank, dev)
+        route, dense_sig = dense_stage_logits(fam, router, route, val, labels, payload, rank, dev, ids0)
+    K = fam.K
+    sev = [timing_event() for _ in range(2 * K)] + [timing_event()]
 
-    def step():
+    def step(events=None):
         # K1 on the validation shard is the timed launch (events around it); the
         # routing stage-1 K1 then runs next to the latency-bound calibration
         router.calibrate(val, labels, time_val=ev)
-        router.route(route, payload=payload, overlap_first=not args.no_overlap, by_id=not dense)
+        router.route(route, ids=ids0, payload=payload, overlap_first=not args.no_overlap,
+                     by_id=not dense, events=events)
+        if events is not None:
+            sev[2 * K].record()
 
     stream = torch.cuda.Stream(device=dev)
     torch.cuda.synchronize()
@@ -368,17 +435,32 @@ def run_ours(args, world, rank, local):
                 "p90": s_ms[(9 * len(s_ms)) // 10], "n": len(s_ms),
                 "note": "per-step CUDA-event times of a second, individually synchronised pass"}
     ms = max_over_ranks(total_ms, world) / args.steps
-    # cascade statistics (identical every step): reach per stage
+    # per-stage breakdown (an eager, event-instrumented pass: the forward is
+    # launched as its own call between the events), max over ranks
+    barrier(world)
+    with torch.cuda.stream(stream):
+        for _ in range(3):
+            step(events=sev)
+        stream.synchronize()
+    stage_ms = [sev[2 * k].elapsed_time(sev[2 * k + 1]) for k in range(K)]
+    fwd_ms = [sev[2 * k + 1].elapsed_time(sev[2 * k + 2]) for k in range(K - 1)]
+    stage_ms = max_over_ranks(stage_ms, world)
+    fwd_ms = max_over_ranks(fwd_ms, world) if K > 1 else []
+    # cascade statistics (identical every step): reach per stage (summed over ranks)
+    if dense:
+        assert dense_signature(router, fam) == dense_sig, "dense layout: the cascade changed between steps"
     counts = router.cascade.counts.cpu().tolist()
-    if dense:   # the dense batches were generated for exactly these deferred sets
-        assert counts == dense_counts, "dense layout: the cascade changed between steps"
-    reach = [fam.n] + [c[1] for c in counts[:-1]]
-    st = int(router.status.item())
-    # algorithmic bytes of one step (logits dominate): validation sweep + reach-weighted routing
+    if peer is not None:
+        batch_local = [fam.n] + [int(x) for x in peer.recv_count[: K - 1].cpu().tolist()]
+    else:
+        batch_local = [fam.n] + [c[1] for c in counts[:-1]]
+    deferred_local = [c[1] for c in counts[:-1]]
+    reach = [int(x) for x in sum_over_ranks([float(b) for b in batch_local], world)]
+    st = int(router.status.item()) | (int(peer.status.item()) if peer is not None else 0)
+    # algorithmic bytes of one step (logits dominate): validation sweep + routing of each stage batch
     row_b = fam.row_bytes
-    val_bytes = fam.K * fam.n_val * row_b
-    route_bytes = sum(reach) * row_b
-    step_bytes = val_bytes + route_bytes
+    val_bytes = K * fam.n_val * row_b
+    step_bytes = val_bytes + sum(batch_local) * row_b
     step_bytes_all = sum_over_ranks([float(step_bytes)], world)[0]
     n_all = fam.n * world
     value = n_all / (ms / 1e3)
@@ -386,33 +468,39 @@ def run_ours(args, world, rank, local):
     # dominant kernel: K1 over the validation shard, all K stages in one launch:
     # per item, its L token rows of logits (row_b) + per token conf (4 B),
     # argmax (4 B), label (4 B) and correct bit (1 B)
-    k_bytes = fam.K * fam.n_val * (row_b + 13 * fam.L)
+    k_bytes = K * fam.n_val * (row_b + 13 * fam.L)
     achieved = k_bytes / (kernel_ms / 1e3) / 1e9
     traffic = committed_traffic(args.config)
-    e2e = run_e2e(args, fam, router, route, val, labels, payload, stream, world) if args.e2e_steps > 0 else None
+    e2e = (run_e2e(args, fam, router, route, val, labels, payload, stream, world, ids0)
+           if args.e2e_steps > 0 else None)
     line = {
         "metric": METRIC, "value": value, "unit": "requests/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": fam.name, "description": CONFIG_TEXT[args.config],
-                   "requests_per_gpu": fam.n, "validation_per_gpu": fam.n_val, "K": fam.K,
+                   "requests_per_gpu": fam.n, "validation_per_gpu": fam.n_val, "K": K,
                    "classes": fam.C, "seq_len": fam.L, "logits_dtype": fam.dtype,
                    "confidence": ["maxprob", "maxprob_sq", "entropy"][fam.kind]
                    + (f" over the top {fam.top_k} logits" if fam.top_k else ""),
                    "sequence_reduce": ["none", "min", "mean"][fam.reduce],
-                   "log2_bins": fam.log2_bins, "parallelism": f"request-sharded dp{world}",
+                   "log2_bins": fam.log2_bins,
+                   "parallelism": f"request-sharded dp{world}"
+                   + (", balanced forwarding + calibration exchange over peer memory (hs_peer_*)"
+                      if peer is not None else ", replicas (no exchange)" if world > 1 else ""),
+                   "placement": args.placement if world > 1 else "single GPU",
                    "l2": "inputs larger than L2 (per-step logits working set >> 126 MB)",
                    "logits_layout": args.layout,
                    "cuda_graph": graph is not None},
         "logits_GBps": step_bytes_all / (ms / 1e3) / 1e9,
         "logits_frac_of_peak": step_bytes_all / world / (ms / 1e3) / 1e9 / peak,
         "reach": reach, "thresholds": router.cal["t"].cpu().tolist(), "status": st,
+        "stage_ms_max_over_ranks": stage_ms,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "kernel": ("conf_topk_kernel" if fam.top_k else
                                 "conf_async_kernel" if fam.C * fam.elt_bytes <= 2048 else
-                                "conf_warp_kernel" if fam.C * fam.elt_bytes <= 8192 else "conf_cta_kernel")
-                     + f" (K1 on the validation shard: {fam.K} stages x {fam.n_val} items in one launch"
+                                "conf_warp_kernel" if fam.C * fam.elt_bytes <= 8192 else "conf_stream_kernel")
+                     + f" (K1 on the validation shard: {K} stages x {fam.n_val} items in one launch"
                      + (", + K2 sequence reduce" if fam.L > 1 else "") + ")",
                      "bytes_per_launch": k_bytes, "avg_launch_ms": kernel_ms,
                      "peak_source": peak_src},
@@ -420,11 +508,24 @@ def run_ours(args, world, rank, local):
         "gpu_launches_per_step": gpu_launches / args.steps,
         "step_ms_percentiles": step_pct,
     }
+    if peer is not None:
+        # forwarded ids (+ payload rows) per stage, NVLink bytes sent per rank
+        fwd_items = [int(x) for x in sum_over_ranks([float(d) for d in deferred_local], world)]
+        per_rank_bytes = max_over_ranks([float(d * (8 + fam.payload_bytes)) for d in deferred_local], world)
+        line["comm"] = {
+            "kind": "peer memory (CUDA IPC mappings; hs_peer_forward + in-kernel histogram exchange)",
+            "world": world, "forwarded_items_per_stage": fwd_items,
+            "bytes_sent_per_rank_max": per_rank_bytes,
+            "forward_ms_max_over_ranks": fwd_ms,
+            "nvlink_GBps_per_rank": [b / (t / 1e3) / 1e9 if t > 0 else None
+                                     for b, t in zip(per_rank_bytes, fwd_ms)],
+            "nvlink_peak_GBps_per_direction": 900.0,
+            "note": "ids-only forwarding is latency-bound (flag round trip ~ us); the fraction of "
+                    "NVLink peak is reported, not targeted"}
     return line, fam, route, val, labels
-
-
-def run_balanced(args, world, rank, local):
-    """Request-sharded cascade with the BALANCED placement: after
+def run_nccl(args, world, rank, local):
+    """Request-sharded cascade with the BALANCED placement done by
+    torch.distributed NCCL -- the baseline of the peer-memory path: after
     every stage the global stable deferred list is re-spread in contiguous blocks
     over all ranks (count all-gather + one NCCL all-to-all of ids and payload),
     and each rank routes the block it received.  Calibration sums the per-rank
@@ -507,7 +608,8 @@ def run_balanced(args, world, rank, local):
         "config": {"workload": fam.name, "description": CONFIG_TEXT[args.config],
                    "requests_per_gpu": n, "validation_per_gpu": fam.n_val, "K": K,
                    "classes": fam.C, "seq_len": fam.L, "logits_dtype": fam.dtype,
-                   "parallelism": f"request-sharded dp{world}, balanced all-to-all forwarding",
+                   "parallelism": f"request-sharded dp{world}, balanced all-to-all forwarding "
+                                  "(torch.distributed NCCL, host split sizes, eager)",
                    "l2": "inputs larger than L2", "cuda_graph": False},
         "gpu_launches": launches, "clocks": clk.summary(), "e2e": None,
         "thresholds": router.cal["t"].cpu().tolist(),
@@ -515,110 +617,7 @@ def run_balanced(args, world, rank, local):
     return line, fam
 
 
-def run_p2p(args, world, rank, local):
-    """BALANCED placement with the deferred requests moved by the hs_forward_*
-    kernels over peer memory (CUDA IPC mappings, dist.PeerForwarder): counts and
-    data never touch the host.  World size 1: the whole step is captured in one
-    CUDA graph; > 1: eager (the calibration's NCCL all-reduce stays)."""
-    import torch
-    import torch.distributed as dist
-    import workload
-    import paper_2505_12566_b200 as hs
-    from paper_2505_12566_b200 import dist as hsd
-    from workload import synth
-
-    dev = torch.device("cuda", local)
-    fam = family(args.config)
-    K, n, P = fam.K, fam.n, fam.payload_bytes
-    tdt = torch.bfloat16 if fam.dtype == "bf16" else torch.float32
-    logits = []
-    for k in range(K):
-        rows = n if k == 0 else world * n
-        x = torch.empty(rows * fam.L, fam.C, dtype=tdt, device=dev)
-        workload.gpu_logits(x, fam, k, id_base=rank * n if k == 0 else 0, n=rows)
-        logits.append(x)
-    _, val, labels, _ = build_inputs(synth.scaled(fam, n=1), rank, dev)
-    group = dist.group.WORLD if dist.is_initialized() else None
-    router = make_router(fam, dev, group if world > 1 else None)
-    cap = world * n
-    fwd = hsd.PeerForwarder(n, P, group=group, device=dev)
-    ws = hs.workspace(hs.lib().hs_cascade_step_workspace(cap, fam.L), dev)
-    ids0 = torch.arange(rank * n, (rank + 1) * n, dtype=torch.int64, device=dev)
-    rows0 = torch.arange(n, dtype=torch.int64, device=dev)
-    pay0 = (torch.randint(0, 255, (n, P), dtype=torch.uint8, device=dev) if P else None)
-    outs = [{"acc_ids": torch.empty(cap, dtype=torch.int64, device=dev),
-             "acc_conf": torch.empty(cap, dtype=torch.float32, device=dev),
-             "acc_pred": torch.empty(cap * fam.L, dtype=torch.int32, device=dev),
-             "next_ids": torch.empty(cap, dtype=torch.int64, device=dev),
-             "counts": torch.zeros(2, dtype=torch.int64, device=dev)} for _ in range(K)]
-    if P:
-        for o in outs:
-            o["next_payload"] = torch.empty(cap * P, dtype=torch.uint8, device=dev)
-
-    def step():
-        cal = router.calibrate(val, labels)
-        ids, pay, d_n, nb, row_index = ids0, pay0, None, n, rows0
-        for k in range(K):
-            o = outs[k]
-            hs.cascade_step(k, K, logits[k], cal["t"][k:k + 1], n=nb, d_n=d_n, seq_len=fam.L,
-                            n_classes=fam.C, temperature=fam.temps[k], kind=fam.kind,
-                            reduce=fam.reduce, row_index=row_index, ids=ids, payload=pay,
-                            payload_row_bytes=P, out=o, ws=ws)
-            if k == K - 1:
-                break
-            ids, pay, d_n = fwd.forward(o["next_ids"], o["counts"][1:2],
-                                        payload=o["next_payload"][: n * P].view(n, P) if P else None)
-            nb, row_index = cap, ids
-
-    stream = torch.cuda.Stream(device=dev)
-    with torch.cuda.stream(stream):
-        for _ in range(max(args.warmup, 3)):
-            step()
-    torch.cuda.synchronize()
-    graph = None
-    per_step = 0
-    if world == 1 and not args.no_graph:
-        graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(graph, stream=stream):
-            l0 = hs.launch_count()
-            step()
-            per_step = hs.launch_count() - l0
-        graph.replay()
-        torch.cuda.synchronize()
-    l0 = hs.launch_count()
-    t0 = torch.cuda.Event(enable_timing=True)
-    t1 = torch.cuda.Event(enable_timing=True)
-    barrier(world)
-    torch.cuda.synchronize()
-    with ClockSampler(local) as clk:
-        with torch.cuda.stream(stream):
-            t0.record(stream)
-            for _ in range(args.steps):
-                graph.replay() if graph is not None else step()
-            t1.record(stream)
-        torch.cuda.synchronize()
-    barrier(world)
-    ms = max_over_ranks(t0.elapsed_time(t1), world) / args.steps
-    launches = per_step * args.steps if graph is not None else hs.launch_count() - l0
-    reach = [int(o["counts"].sum().item()) for o in outs]
-    line = {
-        "metric": METRIC, "value": world * n / (ms / 1e3), "unit": "requests/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": fam.name, "description": CONFIG_TEXT[args.config],
-                   "requests_per_gpu": n, "validation_per_gpu": fam.n_val, "K": K,
-                   "classes": fam.C, "seq_len": fam.L, "logits_dtype": fam.dtype,
-                   "parallelism": f"request-sharded dp{world}, balanced forwarding over peer memory "
-                                  "(hs_forward_* kernels, CUDA IPC)",
-                   "l2": "inputs larger than L2", "cuda_graph": graph is not None},
-        "reach_this_rank": reach, "gpu_launches": launches, "clocks": clk.summary(), "e2e": None,
-        "thresholds": router.cal["t"].cpu().tolist(),
-    }
-    fwd.close()
-    return line, fam
-
-
-def run_e2e(args, fam, router, route, val, labels, payload, stream, world):
+def run_e2e(args, fam, router, route, val, labels, payload, stream, world, ids0=None):
     """Same metric through the public API from pinned HOST buffers: every step copies
     its inputs host->device and reads the per-request results back."""
     import torch
@@ -644,7 +643,7 @@ def run_e2e(args, fam, router, route, val, labels, payload, stream, world):
         if payload is not None:
             payload.copy_(host_pay, non_blocking=True)
         router.calibrate(val, labels)
-        router.route(route, payload=payload, by_id=args.layout != "dense")
+        router.route(route, ids=ids0, payload=payload, by_id=args.layout != "dense")
         cnt_host.copy_(router.cascade.counts, non_blocking=True)
         # accepted ids of every stage (the answers' request ids)
         for o, h in zip(outs, res_host):
@@ -1171,23 +1170,76 @@ def _claim_stdout():
     return emit
 
 
+def spawn_ranks(args) -> int:
+    """--gpus N > 1 without a torchrun environment: re-launch this script as N
+    ranks (torch.distributed.run, one process per GPU, rendezvous on
+    127.0.0.1); rank 0's JSON line is the output."""
+    import socket
+    import subprocess
+    import torch
+    if not (args.share_gpu or args.plumbing_check) and torch.cuda.device_count() < args.gpus:
+        raise SystemExit(f"bench: --gpus {args.gpus} needs {args.gpus} visible GPUs, "
+                         f"found {torch.cuda.device_count()}")
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def plumbing_check(world: int, rank: int):
+    """--plumbing-check: the launcher and the host-side helpers of the
+    multi-rank bench on CPU (gloo): what a peer group does once at set-up
+    (all_gather_object of a 64-byte handle) and the max / sum over ranks the
+    timing uses."""
+    import torch.distributed as dist
+    if world > 1:
+        dist.init_process_group("gloo")
+    handles = [None] * world
+    mine = bytes([rank]) * 64
+    if world > 1:
+        dist.all_gather_object(handles, mine)
+    else:
+        handles = [mine]
+    mx = max_over_ranks([float(rank), 10.0 - rank], world)
+    sm = sum_over_ranks([float(rank + 1)], world)
+    ok = all(h == bytes([r]) * 64 for r, h in enumerate(handles))
+    if world > 1:
+        barrier(world)
+        dist.destroy_process_group()
+    if rank != 0:
+        return None
+    return {"plumbing_check": True, "world": world, "handles_ok": ok, "max": mx, "sum": sm}
+
+
 def main():
-    emit = _claim_stdout()
     args = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args))
+    emit = _claim_stdout()
+    if world > 1 and args.gpus not in (1, world):
+        print(f"[bench] --gpus {args.gpus} but WORLD_SIZE {world}: using {world}", file=sys.stderr)
     rank = int(os.environ.get("RANK", "0"))
+    if args.plumbing_check:
+        line = plumbing_check(world, rank)
+        if line is not None:
+            emit(json.dumps(line))
+        return
     if args.impl == "reference":
         line = run_reference(args, world, rank)
         if line is not None:
             emit(json.dumps(line))
         return
-    if (args.placement in ("balanced", "p2p") or args.force_dist) and int(os.environ.get("WORLD_SIZE", "1")) == 1:
+    if (args.placement == "nccl" or args.force_dist) and world == 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         os.environ.setdefault("MASTER_PORT", "29533")
         os.environ["WORLD_SIZE"] = "1"
         os.environ["RANK"] = "0"
         os.environ["LOCAL_RANK"] = "0"
-    world, rank, local = init_dist(args, force=args.placement in ("balanced", "p2p") or args.force_dist)
+    world, rank, local = init_dist(args, force=args.placement == "nccl" or args.force_dist)
     if args.config == "c2g":
         line, fam, conf, ok = run_graph(args, world, rank, local)
         if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -1202,10 +1254,8 @@ def main():
         if rank == 0:
             emit(json.dumps(line))
         return
-    if args.placement == "balanced":
-        line, fam = run_balanced(args, world, rank, local)
-    elif args.placement == "p2p":
-        line, fam = run_p2p(args, world, rank, local)
+    if args.placement == "nccl":
+        line, fam = run_nccl(args, world, rank, local)
     else:
         line, fam, *_ = run_ours(args, world, rank, local)
     if rank == 0:

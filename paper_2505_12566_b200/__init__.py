@@ -649,7 +649,7 @@ class Cascade:
 
     def route(self, logits: list, thresholds, *, n: int | None = None, ids=None, payload=None,
               by_id: bool = True, overlap_first: bool = False, peer=None, next_ranks=None,
-              stream=None):
+              events=None, stream=None):
         """Run the K stages.  ``overlap_first``: stage 1's confidence kernel runs
         next to the previous libhs kernel (e.g. the calibration it does not
         depend on); see hs_cascade_step_ex / HS_STEP_OVERLAP_PREVIOUS.
@@ -660,7 +660,11 @@ class Cascade:
         the balanced placement), and stage k+1 routes the block this rank
         received (receive set k % 2, count ``peer.recv_count[k]``).  With
         ``by_id`` the stage logits are indexed by request id; otherwise they are
-        the dense batch of the block this rank receives."""
+        the dense batch of the block this rank receives.
+
+        ``events`` (timing): a list of 2K CUDA events; events[2k] is recorded
+        before stage k and events[2k+1] between its compaction and its forward
+        (the forward is then launched as its own call, same kernels)."""
         n = self.n_cap if n is None else int(n)
         d_thr = thresholds if isinstance(thresholds, torch.Tensor) else None
         for k, s in enumerate(self.stages):
@@ -678,9 +682,12 @@ class Cascade:
             if by_id and cur_ids is None:
                 row_index = None   # stage 1 with identity ids: row = id = position
             kw = {}
-            if peer is not None and k < self.K - 1:
+            fwd = peer is not None and k < self.K - 1
+            if fwd and events is None:
                 kw = {"peer": peer.g, "peer_set": k % 2, "recv_count": peer.recv_count[k:k + 1],
                       "next_ranks": None if next_ranks is None else next_ranks[k]}
+            if events is not None:
+                events[2 * k].record(stream)
             cascade_step(k, self.K, logits[k], thr, n=n, seq_len=s.seq_len, n_classes=s.n_classes,
                          temperature=s.temperature, kind=s.kind, reduce=s.reduce,
                          row_index=row_index, d_n=d_n,
@@ -688,6 +695,13 @@ class Cascade:
                          out=self.outs[k], ws=self.ws, status=self.status,
                          overlap_previous=overlap_first and k == 0, top_k=s.top_k,
                          stream=stream, **kw)
+            if events is not None:
+                events[2 * k + 1].record(stream)
+                if fwd:
+                    peer_forward(peer.g, k % 2, self.outs[k]["next_ids"], self.outs[k]["counts"][1:2],
+                                 peer.recv_count[k:k + 1], payload=self.outs[k].get("next_payload"),
+                                 dest_ranks=None if next_ranks is None else next_ranks[k],
+                                 status=peer.status, stream=stream)
         return self
 
     def results(self):

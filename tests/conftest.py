@@ -8,6 +8,12 @@ if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
 
+# several virtual ranks on one GPU drive their peer kernels from separate streams:
+# enough hardware work queues that no two of those streams share one (a
+# spinning kernel would otherwise block the kernel queued behind it)
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
+
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200, sm_100a)")
 

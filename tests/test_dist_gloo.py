@@ -87,3 +87,21 @@ def test_forward_deferred_matches_global_order(world, dest):
     for h in range(world):
         if h not in dest_ranks:
             assert got[h][2] == 0
+
+
+def test_bench_spawns_ranks_and_reduces():
+    """bench.py --gpus 2 without a torchrun environment re-launches itself as
+    two ranks (torch.distributed.run, 127.0.0.1 rendezvous); the ranks join a
+    gloo group, exchange handles once and reduce with max / sum over ranks --
+    the host side of the multi-GPU bench, on CPU."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--plumbing-check"],
+                       capture_output=True, text=True, timeout=300, env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    assert line == {"plumbing_check": True, "world": 2, "handles_ok": True, "max": [1.0, 10.0],
+                    "sum": [3.0]}
