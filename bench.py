@@ -266,40 +266,41 @@ def committed_traffic(config: str, name: str = "r01_k1_traffic.json"):
 
 
 def dense_stage_logits(fam, router, route, val, labels, payload, rank, dev, ids0=None):
-    """--layout dense: run the step once (untimed) to learn which requests reach
-    each model (on this rank), then regenerate stage k's logits (same keyed
+    """--layout dense: learn, stage by stage (untimed), which requests reach
+    each model on this rank and generate stage k's logits (same keyed
     generator, so the same values per request) as the dense batch of exactly
     those requests in order -- what model m_k produces when it runs on its
-    batch only.  The cascade is deterministic, so every timed step routes the
-    same batches.  With a peer group the batch of stage k >= 2 on this rank is
-    the block it RECEIVED from the forward after stage k-1."""
+    batch only.  With a peer group the batch of stage k >= 2 on this rank is
+    the block it RECEIVED from the forward after stage k-1 (requests of any
+    rank).  The cascade is deterministic, so every timed step routes the same
+    batches (asserted after timing)."""
     import torch
     import workload
     router.calibrate(val, labels)
-    router.route(route, ids=ids0, payload=payload, by_id=False)
-    torch.cuda.synchronize()
-    counts = router.cascade.counts.cpu().tolist()
     tdt = torch.bfloat16 if fam.dtype == "bf16" else torch.float32
-    out = [route[0]]
-    batch = []
+    out = [route[0]] + [None] * (fam.K - 1)
     peer = router.peer
     for k in range(1, fam.K):
+        # stages 0..k-1 on the batches known so far (every rank in lockstep)
+        router.route(out, ids=ids0, payload=payload, by_id=False, upto=k - 1)
+        torch.cuda.synchronize()
         if peer is not None:
             nk = int(peer.recv_count[k - 1].item())
             ids = peer.recv_ids((k - 1) % 2)[:nk].clone()
         else:
-            nk = int(counts[k - 1][1])
-            ids = router.cascade.outs[k - 1]["next_ids"][:nk].clone() + rank * fam.n
-        batch.append(nk)
+            nk = int(router.cascade.counts[k - 1][1].item())
+            ids = router.cascade.outs[k - 1]["next_ids"][:nk].clone()
+            if ids0 is None:
+                ids += rank * fam.n
         x = torch.empty(max(nk, 1) * fam.L, fam.C, dtype=tdt, device=dev)
         if nk:
             workload.gpu_logits(x, fam, k, ids=ids, n=nk)
-        out.append(x)
-    for k in range(1, fam.K):
-        route[k] = None                    # the full-population tensors are not needed
+        out[k] = x
+        route[k] = None                    # the full-population tensor is not needed
+    router.route(out, ids=ids0, payload=payload, by_id=False)
     torch.cuda.synchronize()
     torch.cuda.empty_cache()
-    return out, (counts, batch)
+    return out, dense_signature(router, fam)
 
 
 def dense_signature(router, fam):
@@ -522,7 +523,7 @@ def run_ours(args, world, rank, local):
             "nvlink_peak_GBps_per_direction": 900.0,
             "note": "ids-only forwarding is latency-bound (flag round trip ~ us); the fraction of "
                     "NVLink peak is reported, not targeted"}
-    return line, fam, route, val, labels
+    return line, fam, route, val, labels, router
 def run_nccl(args, world, rank, local):
     """Request-sharded cascade with the BALANCED placement done by
     torch.distributed NCCL -- the baseline of the peer-memory path: after
@@ -996,7 +997,63 @@ def oracle_step(fam, inp):
                               kind=fam.kind, reduce=fam.reduce, row_index=batch, top_k=fam.top_k)
         acc, dfr = oracle.route(r["conf"], float(np.float32(cal["t"][k])), k == K - 1)
         batch = batch[dfr]
+    inp["last"] = {"vconf": conf, "vok": ok, "cal": cal}
     return time.perf_counter() - t, n
+
+
+def cpu_parity(fam, inp, router):
+    """Part of the cpu_baseline leg: the oracle's outputs of the timed sample
+    against the GPU's outputs of the same requests (SURVEY 8(c) protocol).
+      * validation confidences of the sample (1e-5 relative) and correct bits;
+      * calibration (i): the oracle's D5 sweep on the GPU's confidences of the
+        WHOLE validation shard must give the GPU's b bit-exactly; (ii) on its
+        own confidences (when the sample is the whole shard): equal, or the
+        samples that changed bin are counted;
+      * routing: every sampled request's answering model under the GPU's
+        thresholds equals the oracle cascade's, except near-threshold
+        requests (|c - t_k| <= 1e-5 t_k at a stage they reach), counted per stage."""
+    import numpy as np
+    import oracle
+    K, nv, n = fam.K, inp["v"], inp["n"]
+    last = inp["last"]
+    gv = router.vconf_all.view(K, fam.n_val).cpu().numpy().astype(np.float64)
+    gok = router.vok.view(K, fam.n_val).cpu().numpy()
+    oc = last["vconf"]
+    err = np.abs(gv[: K - 1, :nv] - oc) / np.maximum(np.abs(oc), 1e-300)
+    b_gpu = router.cal["b"].cpu().numpy()
+    cal_i = oracle.calibrate(gv[: K - 1].astype(np.float32), gok, fam.log2_bins)
+    out = {"validation_conf_max_rel_err": float(np.nanmax(err)) if err.size else 0.0,
+           "validation_correct_bits_equal": bool(np.array_equal(gok[:, :nv], last["vok"])),
+           "calibration_i_bit_exact": bool(np.array_equal(cal_i["b"], b_gpu))}
+    if nv == fam.n_val:
+        B = 1 << fam.log2_bins
+        ob = np.where(np.isnan(oc), -1, np.minimum(B, np.floor(oc * B)))
+        gb = np.where(np.isnan(gv[: K - 1]), -1, np.minimum(B, np.floor(gv[: K - 1] * B)))
+        out["calibration_ii_equal"] = bool(np.array_equal(last["cal"]["b"], b_gpu))
+        out["calibration_ii_samples_changed_bin"] = int((ob != gb).sum())
+    # routing of the sampled requests (ids 0..n-1 of this shard)
+    t = router.cal["t"].cpu().numpy().astype(np.float64)
+    conf = np.stack([oracle.confidence(inp["rl"][k], n, fam.L, fam.C, fam.C, fam.temps[k], kind=fam.kind,
+                                       reduce=fam.reduce, top_k=fam.top_k)["conf"] for k in range(K)])
+    st_o = oracle.cascade(conf, t)
+    st_g = np.full(n, -1, np.int64)
+    counts = router.cascade.counts.cpu().numpy()
+    for k in range(K):
+        ids = router.cascade.outs[k]["acc_ids"][: int(counts[k][0])].cpu().numpy()
+        ids = ids[ids < n]
+        st_g[ids] = k
+    near = np.zeros(n, bool)
+    per = []
+    for k in range(K - 1):
+        nk = (st_o >= k) & (np.abs(conf[k] - t[k]) <= 1e-5 * t[k]) if np.isfinite(t[k]) else np.zeros(n, bool)
+        per.append(int(nk.sum()))
+        near |= nk
+    out.update({"requests_checked": n, "near_threshold_per_stage": per,
+                "routing_mismatches_excluding_near": int((st_o[~near] != st_g[~near]).sum()),
+                "routing_mismatches_near": int((st_o[near] != st_g[near]).sum())})
+    out["green"] = (out["validation_conf_max_rel_err"] <= 1e-5 and out["validation_correct_bits_equal"]
+                    and out["calibration_i_bit_exact"] and out["routing_mismatches_excluding_near"] == 0)
+    return out
 
 
 def cpu_sample_sizes(fam, seconds: float):
@@ -1011,8 +1068,10 @@ def cpu_sample_sizes(fam, seconds: float):
     return n, v
 
 
-def cpu_baseline(fam, seconds: float):
-    """The oracle on the host cores, repeated over a bounded sample for ~`seconds`."""
+def cpu_baseline(fam, seconds: float, router=None):
+    """The oracle on the host cores, repeated over a bounded sample for ~`seconds`;
+    with the GPU's router, the oracle's outputs of that sample are also checked
+    against the GPU's (``parity``)."""
     n, v = cpu_sample_sizes(fam, seconds)
     inp = oracle_inputs(fam, n, v)
     tot, routed, reps = 0.0, 0, 0
@@ -1021,10 +1080,13 @@ def cpu_baseline(fam, seconds: float):
         tot += dt
         routed += r
         reps += 1
-    return {"value": routed / tot, "unit": "requests/s", "cores": os.cpu_count(), "kind": "oracle",
-            "sample": f"{reps} x ({n} of {fam.n} requests + {v} of {fam.n_val} validation samples "
-                      f"of {fam.name}, same generator), fp64 C oracle on {os.cpu_count()} threads, "
-                      f"{tot:.1f} s"}
+    out = {"value": routed / tot, "unit": "requests/s", "cores": os.cpu_count(), "kind": "oracle",
+           "sample": f"{reps} x ({n} of {fam.n} requests + {v} of {fam.n_val} validation samples "
+                     f"of {fam.name}, same generator), fp64 C oracle on {os.cpu_count()} threads, "
+                     f"{tot:.1f} s"}
+    if router is not None and fam.top_k == 0 and fam.L == 1:
+        out["parity"] = cpu_parity(fam, inp, router)
+    return out
 
 
 def run_reference(args, world, rank):
@@ -1254,13 +1316,15 @@ def main():
         if rank == 0:
             emit(json.dumps(line))
         return
+    router = None
     if args.placement == "nccl":
         line, fam = run_nccl(args, world, rank, local)
     else:
-        line, fam, *_ = run_ours(args, world, rank, local)
+        line, fam, *_, router = run_ours(args, world, rank, local)
     if rank == 0:
         if world == 1 and not args.no_cpu_baseline:
-            line["cpu_baseline"] = cpu_baseline(fam, args.cpu_seconds)
+            line["cpu_baseline"] = cpu_baseline(fam, args.cpu_seconds,
+                                                router if args.layout == "dense" else None)
         emit(json.dumps(line))
     import torch.distributed as dist
     if dist.is_initialized():

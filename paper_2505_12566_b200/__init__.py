@@ -649,7 +649,7 @@ class Cascade:
 
     def route(self, logits: list, thresholds, *, n: int | None = None, ids=None, payload=None,
               by_id: bool = True, overlap_first: bool = False, peer=None, next_ranks=None,
-              events=None, stream=None):
+              events=None, upto: int | None = None, stream=None):
         """Run the K stages.  ``overlap_first``: stage 1's confidence kernel runs
         next to the previous libhs kernel (e.g. the calibration it does not
         depend on); see hs_cascade_step_ex / HS_STEP_OVERLAP_PREVIOUS.
@@ -664,10 +664,13 @@ class Cascade:
 
         ``events`` (timing): a list of 2K CUDA events; events[2k] is recorded
         before stage k and events[2k+1] between its compaction and its forward
-        (the forward is then launched as its own call, same kernels)."""
+        (the forward is then launched as its own call, same kernels).
+        ``upto``: run stages 0..upto only (and their forwards)."""
         n = self.n_cap if n is None else int(n)
         d_thr = thresholds if isinstance(thresholds, torch.Tensor) else None
         for k, s in enumerate(self.stages):
+            if upto is not None and k > upto:
+                break
             prev = self.outs[k - 1] if k else None
             if k and peer is not None:
                 cur_ids = peer.recv_ids((k - 1) % 2)

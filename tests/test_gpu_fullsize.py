@@ -92,3 +92,76 @@ def test_bench_step_full_size(hs, config):
     st_o = oracle.cascade(conf_o, t)
     assert np.array_equal(st_o[~near], stage_of[req][~near])
     assert near.sum() <= 5
+
+
+@pytest.mark.parametrize("config", ["c2", "c4"])
+def test_bench_dense_step_full_size_every_request(hs, config):
+    """The TIMED configuration of bench.py (--layout dense, the default): stage
+    k's logits are the dense batch of the requests that reach model k; the
+    step (batched validation confidence, resident calibration, stage 1
+    overlapping it, K stages with device-resident counts) is captured in one
+    CUDA graph and replayed.  Every request of every stage batch is checked:
+    the oracle's confidence of each dense row decides accept / defer at t_k,
+    and the GPU's accepted and deferred lists must equal the oracle's split of
+    the same batch, with the near-threshold requests (G18) removed and counted;
+    accepted confidences within 1e-5 and predictions bit-exact."""
+    import argparse
+    import bench
+    dev = torch.device("cuda:0")
+    fam = bench.family(config)
+    route, val, labels, payload = bench.build_inputs(fam, 0, dev)
+    router = bench.make_router(fam, dev, None)
+    route, _ = bench.dense_stage_logits(fam, router, route, val, labels, payload, 0, dev)
+    stream = torch.cuda.Stream(device=dev)
+
+    def step():
+        router.calibrate(val, labels)
+        router.route(route, payload=payload, overlap_first=True, by_id=False)
+
+    with torch.cuda.stream(stream):
+        step()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=stream):
+        step()
+    for _ in range(3):
+        g.replay()
+    torch.cuda.synchronize()
+    K, n = fam.K, fam.n
+    assert int(router.status.item()) == 0
+    vconf = router.vconf_all.view(K, fam.n_val).cpu().numpy()
+    vok = router.vok.view(K, fam.n_val).cpu().numpy()
+    cal = oracle.calibrate(vconf[: K - 1], vok, fam.log2_bins)
+    assert router.cal["b"].cpu().numpy().tolist() == cal["b"].tolist()
+    t = router.cal["t"].cpu().numpy().astype(np.float64)
+    counts = router.cascade.counts.cpu().numpy()
+    batch_ids = np.arange(n, dtype=np.int64)
+    near_counts = []
+    for k in range(K):
+        nb = len(batch_ids)
+        if k:
+            assert nb == counts[k - 1][1]
+        bits = host_bits(route[k][:nb]) if nb else np.zeros((0, fam.C), np.uint16)
+        ref = oracle.confidence(bits, nb, 1, fam.C, fam.C, fam.temps[k], kind=fam.kind)
+        last = k == K - 1
+        acc_o = np.ones(nb, bool) if last else ref["conf"] >= t[k]
+        near = np.zeros(nb, bool) if last else np.abs(ref["conf"] - t[k]) <= REL * t[k]
+        near_counts.append(int(near.sum()))
+        o = router.cascade.outs[k]
+        na, nd = int(counts[k][0]), int(counts[k][1])
+        assert na + nd == nb
+        acc_ids = o["acc_ids"][:na].cpu().numpy()
+        nxt = o["next_ids"][:nd].cpu().numpy() if not last else np.zeros(0, np.int64)
+        near_ids = set(batch_ids[near].tolist())
+        keep_a = np.array([i not in near_ids for i in acc_ids], bool)
+        keep_d = np.array([i not in near_ids for i in nxt], bool)
+        assert np.array_equal(acc_ids[keep_a], batch_ids[acc_o & ~near]), k
+        assert np.array_equal(nxt[keep_d], batch_ids[~acc_o & ~near]), k
+        # accepted confidences and predictions, matched by position in the batch
+        pos = np.searchsorted(batch_ids, acc_ids)
+        ac = o["acc_conf"][:na].cpu().numpy().astype(np.float64)
+        assert (np.abs(ac - ref["conf"][pos]) <= REL * ref["conf"][pos]).all()
+        assert np.array_equal(o["acc_pred"][:na].cpu().numpy(), ref["argmax"][pos])
+        batch_ids = nxt
+    print(f"{config}: near-threshold requests per stage {near_counts}")
+    assert sum(near_counts) <= max(5, n // 10000)
