@@ -118,6 +118,18 @@ hs_status_t hs_confidence_topk(const void* logits, hs_dtype_t dtype, int64_t n, 
                                const int32_t* labels, uint8_t* correct, void* ws, size_t ws_bytes,
                                uint32_t* d_status, hs_stream_t stream);
 
+/* hs_confidence_ex: hs_confidence_topk plus conf_entropy (optional, [n]
+ * fp32): exp(-H) of every row written alongside conf in the same pass
+ * (north_star "max-probability (and entropy) confidence"; reading G3), e.g.
+ * MAXPROB in conf and the entropy confidence in conf_entropy.  NaN for an
+ * invalid row.  Requires seq_len == 1 (INVALID_ARGUMENT otherwise). */
+hs_status_t hs_confidence_ex(const void* logits, hs_dtype_t dtype, int64_t n, int32_t seq_len,
+                             int64_t n_classes, int64_t row_stride, const int64_t* row_index,
+                             const int64_t* d_n, float temperature, hs_conf_kind_t kind,
+                             hs_seq_reduce_t reduce, int32_t top_k, float* conf, float* conf_entropy,
+                             int32_t* argmax, const int32_t* labels, uint8_t* correct, void* ws,
+                             size_t ws_bytes, uint32_t* d_status, hs_stream_t stream);
+
 /* Every stage model's confidence on the SAME item set in one launch (the
  * calibration input of Alg. 1: "Compute a on D_v" for every model m_1..m_K,
  * P:458-464).  Batch b (0 <= b < n_batches <= 8) reads logits[b] (host array

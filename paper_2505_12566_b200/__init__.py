@@ -99,14 +99,16 @@ def confidence(logits: torch.Tensor, *, n: int | None = None, seq_len: int = 1,
                d_n: torch.Tensor | None = None, labels: torch.Tensor | None = None,
                want_argmax: bool = True, status: torch.Tensor | None = None,
                out: dict | None = None, ws: torch.Tensor | None = None, top_k: int = 0,
-               stream=None) -> dict:
+               want_entropy: bool = False, stream=None) -> dict:
     """Per-item confidence of a batch of logits rows.
 
     ``logits``: [rows, row_stride] bf16/fp32 on the GPU (row-major; the first
     ``n_classes`` entries of a row are the prediction vector).  Returns dict of
     ``conf`` f32[n], ``argmax`` i32[n*seq_len] and ``correct`` u8[n] (when
     ``labels`` is given).  ``top_k`` > 0: softmax restricted to each row's
-    top_k logits (NEXT-2; hs_confidence_topk)."""
+    top_k logits (NEXT-2; hs_confidence_topk).  ``want_entropy``:
+    also ``conf_entropy`` f32[n] = exp(-H) of every row, in the same pass
+    (hs_confidence_ex; seq_len 1)."""
     _check_cuda(logits, row_index, d_n, labels, status)
     if logits.dim() != 2 or logits.stride(1) != 1:
         raise ValueError("logits must be a 2-D row-major tensor")
@@ -122,6 +124,8 @@ def confidence(logits: torch.Tensor, *, n: int | None = None, seq_len: int = 1,
         out["argmax"] = torch.empty(n * seq_len, dtype=torch.int32, device=dev)
     if labels is not None and "correct" not in out:
         out["correct"] = torch.empty(n, dtype=torch.uint8, device=dev)
+    if want_entropy and "conf_entropy" not in out:
+        out["conf_entropy"] = torch.empty(n, dtype=torch.float32, device=dev)
     # required: the token-row part (hs_confidence_batched_workspace(1, ..)); a
     # caller workspace of at least that size is used as is (the optional
     # split-row region only when it fits).  A temporary gets the full size.
@@ -129,10 +133,11 @@ def confidence(logits: torch.Tensor, *, n: int | None = None, seq_len: int = 1,
     if ws is None or ws.numel() < need:
         full = lib().hs_confidence_workspace(n, seq_len)
         ws = _temp_workspace(full, dev, stream) if full else None
-    _abi.call("hs_confidence_topk", _p(logits), _dtype_code(logits), n, seq_len, C, stride,
+    _abi.call("hs_confidence_ex", _p(logits), _dtype_code(logits), n, seq_len, C, stride,
               _p(row_index), _p(d_n), float(temperature), _kind(kind), _reduce(reduce), int(top_k),
-              _p(out["conf"]), _p(out.get("argmax")), _p(labels), _p(out.get("correct")),
-              _p(ws), 0 if ws is None else ws.numel(), _p(status), _stream(stream))
+              _p(out["conf"]), _p(out.get("conf_entropy")), _p(out.get("argmax")), _p(labels),
+              _p(out.get("correct")), _p(ws), 0 if ws is None else ws.numel(), _p(status),
+              _stream(stream))
     return out
 
 

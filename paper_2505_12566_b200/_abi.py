@@ -25,6 +25,8 @@ SIGNATURES = {
     "hs_confidence": (I32, [P, I32, I64, I32, I64, I64, P, P, F32, I32, I32, P, P, P, P, P, SZ, P, P]),
     "hs_confidence_topk": (I32, [P, I32, I64, I32, I64, I64, P, P, F32, I32, I32, I32, P, P, P, P, P, SZ,
                                  P, P]),
+    "hs_confidence_ex": (I32, [P, I32, I64, I32, I64, I64, P, P, F32, I32, I32, I32, P, P, P, P, P, P,
+                               SZ, P, P]),
     "hs_confidence_batched_workspace": (SZ, [I32, I64, I32]),
     "hs_confidence_batched": (I32, [P, P, I32, I32, I64, I32, I64, I64, P, I32, I32, P, P, P, P, P,
                                     SZ, P, P]),

@@ -213,7 +213,20 @@ hs_status_t hs_confidence_topk(const void* logits, hs_dtype_t dtype, int64_t n, 
                                hs_seq_reduce_t reduce, int32_t top_k, float* conf, int32_t* argmax,
                                const int32_t* labels, uint8_t* correct, void* ws, size_t ws_bytes,
                                uint32_t* d_status, hs_stream_t stream) {
+  return hs_confidence_ex(logits, dtype, n, seq_len, n_classes, row_stride, row_index, d_n, temperature,
+                          kind, reduce, top_k, conf, nullptr, argmax, labels, correct, ws, ws_bytes,
+                          d_status, stream);
+}
+
+hs_status_t hs_confidence_ex(const void* logits, hs_dtype_t dtype, int64_t n, int32_t seq_len,
+                             int64_t n_classes, int64_t row_stride, const int64_t* row_index,
+                             const int64_t* d_n, float temperature, hs_conf_kind_t kind,
+                             hs_seq_reduce_t reduce, int32_t top_k, float* conf, float* conf_entropy,
+                             int32_t* argmax, const int32_t* labels, uint8_t* correct, void* ws,
+                             size_t ws_bytes, uint32_t* d_status, hs_stream_t stream) {
   hs_status_t st = check_logits(logits, dtype, n, seq_len, n_classes, row_stride, temperature, kind, reduce);
+  if (st == HS_OK && conf_entropy && seq_len != 1)
+    st = fail(HS_ERR_INVALID_ARGUMENT, "conf_entropy requires seq_len == 1");
   if (st != HS_OK) return st;
   if (top_k < 0 || top_k > hs::kTopkMax)
     return fail(HS_ERR_INVALID_ARGUMENT, "top_k = %d outside 0..%d", top_k, hs::kTopkMax);
@@ -225,6 +238,7 @@ hs_status_t hs_confidence_topk(const void* logits, hs_dtype_t dtype, int64_t n, 
   hs::ConfArgs a = make_conf_args(logits, dtype, n, seq_len, n_classes, row_stride, row_index, d_n,
                                   temperature, kind);
   a.top_k = top_k;
+  a.conf2 = conf_entropy;
   {  // optional split-row region: used when the caller's workspace has room for it;
      // its arrival counters are zeroed by the launcher (no zero-fill contract here)
     const size_t base = align_up(conf_ws(n, seq_len), 256);

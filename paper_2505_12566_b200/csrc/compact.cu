@@ -8,6 +8,11 @@
 // the 4,096-item tile b (blocks are dispatched in index order, as in CUB's
 // single-pass scan), ranks its items with warp ballots, publishes its deferred
 // count, and walks back over predecessor descriptors for its exclusive prefix.
+// Tiles are taken from a TICKET (an atomic counter in the workspace) rather
+// than from blockIdx: a CTA only ever waits on tiles whose CTAs started before
+// it, so the look-back makes progress whatever order the hardware dispatches
+// CTAs in and however many are resident (the CTA drawing the last ticket
+// re-arms the counter for the next launch).
 // Descriptors are 64-bit {epoch:32 | flag:2 | count:30}, written with
 // st.release and read with ld.acquire at gpu scope; the epoch (bumped by the
 // last tile of every launch) makes stale descriptors from earlier launches
@@ -26,6 +31,19 @@ constexpr unsigned long long kValMask = (1ull << 30) - 1;
 __device__ __forceinline__ unsigned long long* tile_status(void* ws) {
   return reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(ws) + sizeof(CompactWs));
 }
+// Tile of this CTA: the next ticket.  Thread 0 draws it; the CTA that draws
+// the last one (every CTA of the grid has drawn) re-arms the counter.
+__device__ __forceinline__ int64_t draw_tile(CompactWs* ws) {
+  __shared__ unsigned s_t;
+  if (threadIdx.x == 0) {
+    const unsigned t = atomicAdd(&ws->ticket, 1u);
+    if (t == gridDim.x - 1) ws->ticket = 0u;
+    s_t = t;
+  }
+  __syncthreads();
+  return (int64_t)s_t;
+}
+
 __device__ __forceinline__ unsigned desc_flag(unsigned long long d, unsigned epoch) {
   return (unsigned)(d >> 32) == epoch ? (unsigned)((d >> 30) & 3u) : 0u;   // 0 = not ready
 }
@@ -41,10 +59,10 @@ __global__ void __launch_bounds__(kCompactThreads) route_compact_kernel(const Co
   unsigned long long* st = tile_status(a.ws);
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
 
+  const int64_t tile = draw_tile(ws);
   int64_t n = a.n;
   if (a.d_n) n = min(*a.d_n, a.n);
   const int64_t ntiles = (n + kCompactTile - 1) / kCompactTile;
-  const int64_t tile = blockIdx.x;
   if (ntiles == 0) {
     if (tile == 0 && tid == 0) {
       a.counts[0] = 0;
@@ -228,7 +246,7 @@ __global__ void __launch_bounds__(kCompactThreads) route_compact_fast_kernel(con
   CompactWs* ws = reinterpret_cast<CompactWs*>(a.ws);
   unsigned long long* st = tile_status(a.ws);
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int64_t tile = blockIdx.x;
+  const int64_t tile = draw_tile(ws);
   const int64_t base = tile * TILE;
   const int64_t i0 = base + (int64_t)tid * I;
   const bool pred1 = a.acc_pred && a.pred_len == 1;

@@ -55,7 +55,7 @@ __device__ __forceinline__ void write_row(const ConfArgs& a, int64_t row, int32_
     am = -1;
     if (a.status) atomicOr(a.status, HS_STATUS_NONFINITE);
   } else {
-    const float p = r.e0 / r.s;
+    const float p = __fdividef(r.e0, r.s);   // s in [1, C]: MUFU.RCP + FMUL, <= 2 ulp
     if (a.kind == HS_CONF_MAXPROB_SQ) {
       c = p * p;
     } else if (a.kind == HS_CONF_ENTROPY) {
@@ -67,6 +67,7 @@ __device__ __forceinline__ void write_row(const ConfArgs& a, int64_t row, int32_
     }
   }
   a.conf[row] = c;
+  if (a.conf2) a.conf2[row] = bad ? __int_as_float(0x7FC00000) : exp2f(r.w / r.s - log2f(r.s));
   if (a.argmax) a.argmax[row] = am;
   if (a.ok) a.ok[row] = (uint8_t)(a.labels ? (!bad && lab == am) : 0);
 }
@@ -306,31 +307,66 @@ __device__ __forceinline__ int vec_first_eq_bf16n(const uint4& x, uint32_t mb2) 
   return r;
 }
 
+// does the packed bf16x2 word w hold the NORMAL bf16 value whose bits are
+// mb2 = (mb, mb) in either half?  (one packed compare; exact for normal m)
+__device__ __forceinline__ bool bf2_has(uint32_t w, uint32_t mb2) {
+  uint32_t r;
+  asm("{\n\t.reg .pred p, h;\n\t"
+      "setp.eq.bf16x2 p|h, %1, %2;\n\t"
+      "or.pred p, p, h;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(r)
+      : "r"(w), "r"(mb2));
+  return r != 0u;
+}
+
+// Lowest k in [0, 8) whose vector max vmw[k] holds m (some vmw[k] does): a
+// descent of the pairwise max tree -- 3 packed compares and 4 selects instead
+// of one compare and two selects per vector.
+__device__ __forceinline__ int tree_first8(const uint32_t (&v)[8], uint32_t mb2) {
+  const uint32_t p0 = bmax2(v[0], v[1]), p2 = bmax2(v[4], v[5]);
+  const uint32_t q0 = bmax2(p0, bmax2(v[2], v[3]));
+  const bool l1 = bf2_has(q0, mb2);                 // in vectors 0..3?
+  const bool l2 = bf2_has(l1 ? p0 : p2, mb2);        // in the first pair of that half?
+  const uint32_t w = l1 ? (l2 ? v[0] : v[2]) : (l2 ? v[4] : v[6]);
+  const bool l3 = bf2_has(w, mb2);                  // in the first vector of that pair?
+  return (l1 ? 0 : 4) + (l2 ? 0 : 2) + (l3 ? 0 : 1);
+}
+
+// `srow`: shared-memory address of the row's vector 0 when the row is staged
+// there (cp.async / TMA kernels; 0xFFFFFFFF: not staged, re-read from L2).
 template <bool BF16, bool ENTROPY, int NV, int G>
 __device__ __forceinline__ void group_reduce_row(const ConfArgs& a, const uint4 (&v)[NV],
                                                  bool active, int64_t row, int gl,
-                                                 float c, const uint4* rowp, int32_t lab) {
+                                                 float c, const uint4* rowp, int32_t lab,
+                                                 uint32_t srow = 0xFFFFFFFFu) {
   constexpr int VE = BF16 ? 8 : 4;
   const f2_t c2 = f2(c, c);
   // 1. row max (exact, NaN-propagating): packed per-vector maxima, then the group
   uint32_t vmw[NV];
-  uint32_t lw = vec_maxw<BF16>(v[0]);
-  vmw[0] = lw;
 #pragma unroll
-  for (int k = 1; k < NV; ++k) {
-    vmw[k] = vec_maxw<BF16>(v[k]);
-    lw = BF16 ? bmax2(lw, vmw[k]) : __float_as_uint(fmax_nan(__uint_as_float(lw), __uint_as_float(vmw[k])));
+  for (int k = 0; k < NV; ++k) vmw[k] = vec_maxw<BF16>(v[k]);
+  uint32_t lw;
+  if constexpr (BF16 && NV == 8) {   // pairwise tree: shared with the argmax descent
+    lw = bmax2(bmax2(bmax2(vmw[0], vmw[1]), bmax2(vmw[2], vmw[3])),
+               bmax2(bmax2(vmw[4], vmw[5]), bmax2(vmw[6], vmw[7])));
+  } else {
+    lw = vmw[0];
+#pragma unroll
+    for (int k = 1; k < NV; ++k)
+      lw = BF16 ? bmax2(lw, vmw[k]) : __float_as_uint(fmax_nan(__uint_as_float(lw), __uint_as_float(vmw[k])));
   }
   float m = BF16 ? fmax_nan(bf_lo(lw), bf_hi(lw)) : __uint_as_float(lw);
 #pragma unroll
   for (int o = G / 2; o > 0; o >>= 1) m = fmax_nan(m, __shfl_xor_sync(0xFFFFFFFFu, m, o));
 
   // 2. argmax = lowest index holding m.  (i) each lane: lowest of its vectors
-  //    whose packed max contains m; (ii) group min -> vector vi; (iii) lane 0
-  //    re-reads that one 16-byte vector (an L2 hit: the row was just streamed)
-  //    and finds the first element equal to m after the exponential pass has
-  //    hidden the load.  A normal bf16 m is matched with one packed compare per
-  //    vector; a zero/subnormal m (or fp32) takes the exact fp32 compares.
+  //    whose packed max contains m -- bf16: one packed compare of the lane max,
+  //    then a descent of the max tree (log2 NV compares); (ii) group min -> vector
+  //    vi; (iii) the group reads that one 16-byte vector -- from the shared-memory
+  //    stage when the row is staged there (no dependent L2 round trip), else from
+  //    L2 -- and finds the first element equal to m after the exponential pass.
+  //    A zero/subnormal m (or fp32) takes the exact fp32 compares.
 #ifdef HS_EXP_NOARGMAX
   const unsigned am = 0;
 #else
@@ -339,19 +375,21 @@ __device__ __forceinline__ void group_reduce_row(const ConfArgs& a, const uint4 
   const bool slow = BF16 && (m == m) && !(fabsf(m) >= 1.17549435e-38f);
   const bool anyslow = BF16 && __any_sync(0xFFFFFFFFu, slow);
   const uint32_t mb2 = (__float_as_uint(m) >> 16) * 0x10001u;
+  if (BF16) {
+#ifndef HS_AB_LINEAR_ARGMAX
+    if constexpr (NV == 8) {
+      if (bf2_has(lw, mb2)) vi = (unsigned)(tree_first8(vmw, mb2) * G + gl);
+    } else
+#endif
+    {
 #pragma unroll
-  for (int k = NV - 1; k >= 0; --k) {
-    const unsigned idx = (unsigned)(k * G + gl);
-    if (BF16) {
-      asm("{\n\t.reg .pred p, h;\n\t"
-          "setp.eq.bf16x2 p|h, %1, %2;\n\t"
-          "@h mov.u32 %0, %3;\n\t"
-          "@p mov.u32 %0, %3;\n\t}"
-          : "+r"(vi)
-          : "r"(vmw[k]), "r"(mb2), "r"(idx));
-    } else if (__uint_as_float(vmw[k]) == m) {
-      vi = idx;
+      for (int k = NV - 1; k >= 0; --k)
+        if (bf2_has(vmw[k], mb2)) vi = (unsigned)(k * G + gl);
     }
+  } else {
+#pragma unroll
+    for (int k = NV - 1; k >= 0; --k)
+      if (__uint_as_float(vmw[k]) == m) vi = (unsigned)(k * G + gl);
   }
   if (anyslow) {
     if (slow) {
@@ -365,7 +403,18 @@ __device__ __forceinline__ void group_reduce_row(const ConfArgs& a, const uint4 
   for (int o = G / 2; o > 0; o >>= 1) vi = min(vi, (unsigned)__shfl_xor_sync(0xFFFFFFFFu, vi, o));
   // every lane of the group reads the same vector (one broadcast transaction);
   // an invalid row (no match) reads vector 0 and is discarded by write_row
-  const uint4 xv = __ldg(rowp + (vi < (unsigned)a.nvec ? vi : 0u));
+  const unsigned vr = vi < (unsigned)a.nvec ? vi : 0u;
+  uint4 xv;
+#ifdef HS_AB_L2_REREAD
+  srow = 0xFFFFFFFFu;
+#endif
+  if (srow != 0xFFFFFFFFu) {
+    __syncwarp();                    // the other lanes' staged vectors are visible
+    asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(xv.x), "=r"(xv.y), "=r"(xv.z), "=r"(xv.w) : "r"(srow + vr * 16u));
+  } else {
+    xv = __ldg(rowp + vr);
+  }
 #endif
 
   // 3. exponentials with the common max: a = (x - m) * c, x - m formed exactly
@@ -859,7 +908,8 @@ __global__ void __launch_bounds__(kAsyncThreads, 3) conf_async_kernel(const Conf
       cp_async_wait<1>();        // this lane's copies of row A have landed
       group_lds_row<BF16, NV, G, FULL>(A, sbase + (uint32_t)(it & 1) * STAGEB, gl, nvec);
       if (a.tail) group_mask_tail<BF16, NV, G>(A, gl, nvec, a.tail);
-      group_reduce_row<BF16, ENTROPY, NV, G>(a, A, actA, rowA, gl, cA, pA, labA);
+      group_reduce_row<BF16, ENTROPY, NV, G>(a, A, actA, rowA, gl, cA, pA, labA,
+                                             sbase + (uint32_t)(it & 1) * STAGEB - (uint32_t)gl * 16u);
       if (!anyB) break;
       rowA = rowB;
       actA = actB;
@@ -1660,7 +1710,7 @@ cudaError_t launch_topk(const ConfArgs& a, int64_t rows, cudaStream_t s) {
 
 cudaError_t launch_confidence(const ConfArgs& a, bool bf16, cudaStream_t s) {
   const int64_t rows = a.n * a.L * a.nbatch;
-  const bool ent = a.kind == HS_CONF_ENTROPY;
+  const bool ent = a.kind == HS_CONF_ENTROPY || a.conf2 != nullptr;
   if (a.top_k > 0 && (int64_t)a.top_k < a.C) {
     if (bf16) return ent ? launch_topk<true, true>(a, rows, s) : launch_topk<true, false>(a, rows, s);
     return ent ? launch_topk<false, true>(a, rows, s) : launch_topk<false, false>(a, rows, s);

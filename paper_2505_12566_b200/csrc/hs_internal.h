@@ -76,6 +76,9 @@ struct ConfArgs {
   // split_ws_bytes(rows) bytes, or NULL (no split)
   void* split_ws;
   int split_zero;          // 1: zero the arrival counters before the launch
+  // optional second output: exp(-H) of every row alongside `conf` (north_star
+  // "max-probability (and entropy) confidence"); forces the entropy sums
+  float* conf2;
 };
 constexpr int kSplitMaxRows = 2048;     // the split path serves batches up to this many rows
 constexpr int kSplitMaxSeg = 64;        // segments per row
@@ -94,7 +97,7 @@ constexpr int kCompactTile = kCompactThreads * kCompactItems;   // 2048 items pe
 
 struct CompactWs {          // zero-filled before first use; then self-maintaining
   unsigned int epoch;       // launch counter tagging the tile descriptors
-  unsigned int pad0;
+  unsigned int ticket;      // tile tickets: CTAs take tiles in the order they START
   unsigned long long pad[3];
   // unsigned long long status[n_tiles] follows (32-byte header)
 };

@@ -910,3 +910,27 @@ def test_topk_cascade_step_vs_oracle(hs):
     for k in range(3):
         got, want = res[k]["ids"].numpy(), lists[k][1]
         assert np.array_equal(got[~near[got]], want[~near[want]])
+
+
+@pytest.mark.parametrize("C,dtype,kind", [(1000, "bf16", 0), (1000, "fp32", 1), (32128, "bf16", 0),
+                                          (128256, "bf16", 2), (17, "fp32", 0)])
+def test_conf_entropy_alongside(hs, C, dtype, kind):
+    """hs_confidence_ex: the entropy confidence exp(-H) written next to the
+    requested kind in the same pass (north_star "max-probability (and
+    entropy) confidence"), both within 1e-5 of the oracle, on random and
+    adversarial rows (invalid rows: NaN in both)."""
+    rng = np.random.default_rng(C + kind)
+    x32 = _adversarial_rows(C, rng)
+    bits = x32 if dtype == "fp32" else \
+        torch.from_numpy(x32).to(torch.bfloat16).view(torch.int16).numpy().view(np.uint16)
+    n = bits.shape[0]
+    x = to_dev_bits(bits, dtype)
+    for ws in (None, torch.zeros(16, dtype=torch.uint8, device=dev())):
+        r = hs.confidence(x, n_classes=C, temperature=0.7, kind=kind, want_entropy=True, ws=ws)
+        torch.cuda.synchronize()
+        ref = oracle.confidence(host_bits(x), n, 1, C, C, 0.7, kind=kind)
+        ent = oracle.confidence(host_bits(x), n, 1, C, C, 0.7, kind=2)
+        assert_conf_close(r["conf"].cpu().numpy(), ref["conf"])
+        assert_conf_close(r["conf_entropy"].cpu().numpy(), ent["conf"])
+    with pytest.raises(hs.HsError):
+        hs.confidence(x, n=n // 2, seq_len=2, n_classes=C, reduce=1, want_entropy=True)
