@@ -55,6 +55,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-overlap", action="store_true",
                     help="run routing stage 1 strictly after the calibration (no PDL overlap)")
+    ap.add_argument("--no-split", action="store_true",
+                    help="run each stage's compaction on the critical path (hs_cascade_step) instead of "
+                         "on a side stream next to the next stage's confidence")
     ap.add_argument("--native-comm", action="store_true",
                     help="calibration all-reduce inside libhs on its own NCCL communicator "
                          "(hs_calibrate_thresholds_comm) instead of torch.distributed")
@@ -369,7 +372,7 @@ def run_ours(args, world, rank, local):
         # routing stage-1 K1 then runs next to the latency-bound calibration
         router.calibrate(val, labels, time_val=ev)
         router.route(route, ids=ids0, payload=payload, overlap_first=not args.no_overlap,
-                     by_id=not dense, events=events)
+                     by_id=not dense, events=events, split=dense and peer is None and not args.no_split)
         if events is not None:
             sev[2 * K].record()
 

@@ -250,6 +250,34 @@ hs_status_t hs_cascade_step_ex(int32_t stage, int32_t n_stages, const void* logi
                                int64_t* d_counts, void* ws, size_t ws_bytes, uint32_t* d_status,
                                int32_t top_k, uint32_t flags, hs_stream_t stream);
 
+/* The two halves of hs_cascade_step_ex, for callers that take the compaction
+ * off the critical path (the next stage's confidence needs only the COUNT of
+ * deferred items when its logits are the dense batch of those items):
+ *   hs_cascade_confidence: the stage's confidence (K1, + K2 for sequences) into
+ *     the step workspace `ws`; with d_defer_count != NULL also ADDS the number
+ *     of items the threshold test will defer (0 at the last stage) to
+ *     *d_defer_count (caller zero-fills it; same fp32 test as the compaction,
+ *     so it equals d_counts[1]).
+ *   hs_cascade_compact: the threshold test + stable compaction (+ gather) of
+ *     the confidences a previous hs_cascade_confidence left in `ws` (same n,
+ *     seq_len, d_n, threshold).  May run on another stream than the next
+ *     stage's confidence, ordered after this stage's hs_cascade_confidence; a
+ *     workspace is then needed per stage in flight.
+ * Arguments as for hs_cascade_step_ex. */
+hs_status_t hs_cascade_confidence(int32_t stage, int32_t n_stages, const void* logits, hs_dtype_t dtype,
+                                  int64_t n, int32_t seq_len, int64_t n_classes, int64_t row_stride,
+                                  const int64_t* row_index, const int64_t* d_n, float temperature,
+                                  hs_conf_kind_t kind, hs_seq_reduce_t reduce, float threshold,
+                                  const float* d_threshold, uint64_t* d_defer_count, void* ws,
+                                  size_t ws_bytes, uint32_t* d_status, int32_t top_k, uint32_t flags,
+                                  hs_stream_t stream);
+hs_status_t hs_cascade_compact(int32_t stage, int32_t n_stages, int64_t n, int32_t seq_len,
+                               const int64_t* d_n, float threshold, const float* d_threshold,
+                               const int64_t* ids, const void* payload, int64_t payload_row_bytes,
+                               int64_t* acc_ids, float* acc_conf, int32_t* acc_pred, int64_t* next_ids,
+                               void* next_payload, int64_t* d_counts, void* ws, size_t ws_bytes,
+                               hs_stream_t stream);
+
 /* ------------------------------------------------------------------------ */
 /* Offline Accuracy-Preserving threshold calibration (Alg. 1, AP).  */
 /* ------------------------------------------------------------------------ */

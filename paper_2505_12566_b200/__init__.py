@@ -654,7 +654,7 @@ class Cascade:
 
     def route(self, logits: list, thresholds, *, n: int | None = None, ids=None, payload=None,
               by_id: bool = True, overlap_first: bool = False, peer=None, next_ranks=None,
-              events=None, upto: int | None = None, stream=None):
+              events=None, upto: int | None = None, split: bool = False, stream=None):
         """Run the K stages.  ``overlap_first``: stage 1's confidence kernel runs
         next to the previous libhs kernel (e.g. the calibration it does not
         depend on); see hs_cascade_step_ex / HS_STEP_OVERLAP_PREVIOUS.
@@ -670,7 +670,15 @@ class Cascade:
         ``events`` (timing): a list of 2K CUDA events; events[2k] is recorded
         before stage k and events[2k+1] between its compaction and its forward
         (the forward is then launched as its own call, same kernels).
-        ``upto``: run stages 0..upto only (and their forwards)."""
+        ``upto``: run stages 0..upto only (and their forwards).
+        ``split``: single GPU, dense stage batches (``by_id=False``): each
+        stage's confidence also counts its deferred items
+        (hs_cascade_confidence), the next stage's confidence starts from that
+        count, and every compaction (hs_cascade_compact) runs on a side stream
+        off the critical path (joined before returning)."""
+        if split and peer is None and not by_id and events is None:
+            return self._route_split(logits, thresholds, n=n, ids=ids, payload=payload,
+                                     overlap_first=overlap_first, upto=upto, stream=stream)
         n = self.n_cap if n is None else int(n)
         d_thr = thresholds if isinstance(thresholds, torch.Tensor) else None
         for k, s in enumerate(self.stages):
@@ -710,6 +718,48 @@ class Cascade:
                                  peer.recv_count[k:k + 1], payload=self.outs[k].get("next_payload"),
                                  dest_ranks=None if next_ranks is None else next_ranks[k],
                                  status=peer.status, stream=stream)
+        return self
+
+    def _route_split(self, logits, thresholds, *, n, ids, payload, overlap_first, upto, stream):
+        import ctypes
+        n = self.n_cap if n is None else int(n)
+        main = stream if stream is not None else torch.cuda.current_stream(self.device)
+        if not hasattr(self, "_side"):
+            L = max(s.seq_len for s in self.stages)
+            self._side = torch.cuda.Stream(device=self.device)
+            self._stage_ws = [workspace(lib().hs_cascade_step_workspace(self.n_cap, L), self.device)
+                              for _ in range(self.K)]
+            self._defer = torch.zeros(self.K, dtype=torch.int64, device=self.device)
+            self._ev = [torch.cuda.Event() for _ in range(self.K)]
+        d_thr = thresholds if isinstance(thresholds, torch.Tensor) else None
+        side = self._side
+        with torch.cuda.stream(main):
+            self._defer.zero_()
+        for k, s in enumerate(self.stages):
+            if upto is not None and k > upto:
+                break
+            thr = d_thr[k:k + 1] if d_thr is not None else float(thresholds[k] if k < self.K - 1 else 0.0)
+            dt, th = (_p(thr), 0.0) if isinstance(thr, torch.Tensor) else (None, float(thr))
+            d_n = self._defer[k - 1:k] if k else None
+            x = logits[k]
+            ws = self._stage_ws[k]
+            last = k == self.K - 1
+            _abi.call("hs_cascade_confidence", k, self.K, _p(x), _dtype_code(x), n, int(s.seq_len),
+                      int(s.n_classes), int(x.stride(0)), None, _p(d_n), float(s.temperature),
+                      _kind(s.kind), _reduce(s.reduce), th, dt,
+                      None if last else _p(self._defer[k:k + 1]), _p(ws), ws.numel(), _p(self.status),
+                      int(s.top_k), HS_STEP_OVERLAP_PREVIOUS if (overlap_first and k == 0) else 0,
+                      main.cuda_stream)
+            self._ev[k].record(main)
+            side.wait_event(self._ev[k])
+            prev = self.outs[k - 1] if k else None
+            o = self.outs[k]
+            _abi.call("hs_cascade_compact", k, self.K, n, int(s.seq_len), _p(d_n), th, dt,
+                      _p(prev["next_ids"] if k else ids),
+                      _p(prev.get("next_payload") if k else payload), self.P,
+                      _p(o["acc_ids"]), _p(o["acc_conf"]), _p(o["acc_pred"]), _p(o["next_ids"]),
+                      _p(o.get("next_payload")), _p(o["counts"]), _p(ws), ws.numel(), side.cuda_stream)
+        main.wait_stream(side)
         return self
 
     def results(self):

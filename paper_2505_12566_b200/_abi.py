@@ -41,6 +41,9 @@ SIGNATURES = {
                               P, I64, P, P, P, P, P, P, P, SZ, P, P]),
     "hs_cascade_step_ex": (I32, [I32, I32, P, I32, I64, I32, I64, I64, P, P, F32, I32, I32, F32, P, P,
                                  P, I64, P, P, P, P, P, P, P, SZ, P, I32, ctypes.c_uint32, P]),
+    "hs_cascade_confidence": (I32, [I32, I32, P, I32, I64, I32, I64, I64, P, P, F32, I32, I32, F32, P, P,
+                                    P, SZ, P, I32, ctypes.c_uint32, P]),
+    "hs_cascade_compact": (I32, [I32, I32, I64, I32, P, F32, P, P, P, I64, P, P, P, P, P, P, P, SZ, P]),
     "hs_calibrate_workspace": (SZ, [I32, I32]),
     "hs_calibrate_thresholds": (I32, [P, P, I32, I64, I32, I64, I32, P, P, P, P, P, P, SZ, P]),
     "hs_calibrate_begin": (I32, [I32, I32, I64, P, SZ, P]),

@@ -892,6 +892,81 @@ hs_status_t hs_cascade_step(int32_t stage, int32_t n_stages, const void* logits,
                             next_payload, d_counts, ws, ws_bytes, d_status, 0, 0u, stream);
 }
 
+static hs_status_t step_common_checks(int32_t stage, int32_t n_stages, int64_t n, float threshold,
+                                      const float* d_threshold, int32_t top_k) {
+  if (top_k < 0 || top_k > hs::kTopkMax)
+    return fail(HS_ERR_INVALID_ARGUMENT, "top_k = %d outside 0..%d", top_k, hs::kTopkMax);
+  if (n_stages < 1 || stage < 0 || stage >= n_stages)
+    return fail(HS_ERR_INVALID_ARGUMENT, "stage %d outside 0..n_stages-1 (%d)", stage, n_stages);
+  if (n < 0 || n >= (int64_t(1) << 30)) return fail(HS_ERR_INVALID_ARGUMENT, "n must be in 0..2^30-1 per call");
+  if (stage != n_stages - 1 && !d_threshold) return check_threshold(threshold);
+  return HS_OK;
+}
+
+hs_status_t hs_cascade_confidence(int32_t stage, int32_t n_stages, const void* logits, hs_dtype_t dtype,
+                                  int64_t n, int32_t seq_len, int64_t n_classes, int64_t row_stride,
+                                  const int64_t* row_index, const int64_t* d_n, float temperature,
+                                  hs_conf_kind_t kind, hs_seq_reduce_t reduce, float threshold,
+                                  const float* d_threshold, uint64_t* d_defer_count, void* ws,
+                                  size_t ws_bytes, uint32_t* d_status, int32_t top_k, uint32_t flags,
+                                  hs_stream_t stream) {
+  if (flags & ~(uint32_t)HS_STEP_OVERLAP_PREVIOUS)
+    return fail(HS_ERR_INVALID_ARGUMENT, "unknown flags 0x%x", flags);
+  hs_status_t st = step_common_checks(stage, n_stages, n, threshold, d_threshold, top_k);
+  if (st != HS_OK) return st;
+  st = check_logits(logits, dtype, n, seq_len, n_classes, row_stride, temperature, kind, reduce);
+  if (st != HS_OK) return st;
+  size_t o_conf, o_am, o_pos, o_cws, o_tick, o_split;
+  const size_t need = step_layout(n, seq_len, &o_conf, &o_am, &o_pos, &o_cws, &o_tick, &o_split);
+  if (!ws || ws_bytes < need) return fail(HS_ERR_WORKSPACE_TOO_SMALL, "workspace %zu < %zu", ws_bytes, need);
+  if (n == 0) return HS_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  char* w = reinterpret_cast<char*>(ws);
+  float* conf = reinterpret_cast<float*>(w + o_conf);
+  int32_t* am = reinterpret_cast<int32_t*>(w + o_am);
+  hs::ConfArgs a = make_conf_args(logits, dtype, n, seq_len, n_classes, row_stride, row_index, d_n,
+                                  temperature, kind);
+  a.top_k = top_k;
+  if (hs::split_ws_bytes(n * (int64_t)seq_len)) a.split_ws = w + o_split;
+  if (flags & HS_STEP_OVERLAP_PREVIOUS) {
+    // CTAs that start late (SMs held by the previous kernel) take fewer rows
+    a.ticket = reinterpret_cast<unsigned int*>(w + o_tick);
+    a.late_wait = 1;
+  }
+  st = run_confidence_args(a, dtype, reduce, conf, am, nullptr, nullptr, w + o_cws, d_status, s);
+  if (st != HS_OK || !d_defer_count) return st;
+  return cuda_check(hs::launch_count_deferred(conf, n, d_n, threshold, d_threshold, stage == n_stages - 1,
+                                              reinterpret_cast<unsigned long long*>(d_defer_count), s),
+                    "count kernel");
+}
+
+hs_status_t hs_cascade_compact(int32_t stage, int32_t n_stages, int64_t n, int32_t seq_len,
+                               const int64_t* d_n, float threshold, const float* d_threshold,
+                               const int64_t* ids, const void* payload, int64_t payload_row_bytes,
+                               int64_t* acc_ids, float* acc_conf, int32_t* acc_pred, int64_t* next_ids,
+                               void* next_payload, int64_t* d_counts, void* ws, size_t ws_bytes,
+                               hs_stream_t stream) {
+  hs_status_t st = step_common_checks(stage, n_stages, n, threshold, d_threshold, 0);
+  if (st != HS_OK) return st;
+  if (seq_len < 1) return fail(HS_ERR_INVALID_ARGUMENT, "seq_len = %d < 1", seq_len);
+  if (!d_counts) return fail(HS_ERR_INVALID_ARGUMENT, "d_counts is required");
+  if (next_payload && (!payload || payload_row_bytes <= 0 || (payload_row_bytes & 15) ||
+                       !aligned16(payload) || !aligned16(next_payload)))
+    return fail(HS_ERR_INVALID_ARGUMENT, "payload rows must be 16-byte aligned multiples of 16 bytes");
+  size_t o_conf, o_am, o_pos, o_cws, o_tick, o_split;
+  const size_t need = step_layout(n, seq_len, &o_conf, &o_am, &o_pos, &o_cws, &o_tick, &o_split);
+  if (!ws || ws_bytes < need) return fail(HS_ERR_WORKSPACE_TOO_SMALL, "workspace %zu < %zu", ws_bytes, need);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (n == 0) return cuda_check(cudaMemsetAsync(d_counts, 0, 2 * sizeof(int64_t), s), "memset counts");
+  char* w = reinterpret_cast<char*>(ws);
+  const float* conf = reinterpret_cast<const float*>(w + o_conf);
+  const int32_t* am = reinterpret_cast<const int32_t*>(w + o_am);
+  int64_t* pos = reinterpret_cast<int64_t*>(w + o_pos);
+  return route_compact_impl(conf, n, d_n, threshold, d_threshold, stage == n_stages - 1, ids, am, seq_len,
+                            acc_ids, acc_conf, acc_pred, next_ids, next_payload ? pos : nullptr, payload,
+                            payload_row_bytes, next_payload, d_counts, ws, s);
+}
+
 hs_status_t hs_cascade_step_ex(int32_t stage, int32_t n_stages, const void* logits, hs_dtype_t dtype,
                                int64_t n, int32_t seq_len, int64_t n_classes, int64_t row_stride,
                                const int64_t* row_index, const int64_t* d_n, float temperature,
@@ -901,52 +976,20 @@ hs_status_t hs_cascade_step_ex(int32_t stage, int32_t n_stages, const void* logi
                                int32_t* acc_pred, int64_t* next_ids, void* next_payload,
                                int64_t* d_counts, void* ws, size_t ws_bytes, uint32_t* d_status,
                                int32_t top_k, uint32_t flags, hs_stream_t stream) {
-  if (flags & ~(uint32_t)HS_STEP_OVERLAP_PREVIOUS)
-    return fail(HS_ERR_INVALID_ARGUMENT, "unknown flags 0x%x", flags);
-  if (top_k < 0 || top_k > hs::kTopkMax)
-    return fail(HS_ERR_INVALID_ARGUMENT, "top_k = %d outside 0..%d", top_k, hs::kTopkMax);
-  if (n_stages < 1 || stage < 0 || stage >= n_stages)
-    return fail(HS_ERR_INVALID_ARGUMENT, "stage %d outside 0..n_stages-1 (%d)", stage, n_stages);
-  if (n >= (int64_t(1) << 30)) return fail(HS_ERR_INVALID_ARGUMENT, "n must be < 2^30 per call");
-  const int is_last = stage == n_stages - 1;
-  hs_status_t st = check_logits(logits, dtype, n, seq_len, n_classes, row_stride, temperature, kind, reduce);
+  // validate both halves before launching either
+  hs_status_t st = step_common_checks(stage, n_stages, n, threshold, d_threshold, top_k);
   if (st != HS_OK) return st;
-  if (!is_last && !d_threshold) {
-    st = check_threshold(threshold);
-    if (st != HS_OK) return st;
-  }
   if (!d_counts) return fail(HS_ERR_INVALID_ARGUMENT, "d_counts is required");
   if (next_payload && (!payload || payload_row_bytes <= 0 || (payload_row_bytes & 15) ||
                        !aligned16(payload) || !aligned16(next_payload)))
     return fail(HS_ERR_INVALID_ARGUMENT, "payload rows must be 16-byte aligned multiples of 16 bytes");
-  size_t o_conf, o_am, o_pos, o_cws, o_tick, o_split;
-  const size_t need = step_layout(n, seq_len, &o_conf, &o_am, &o_pos, &o_cws, &o_tick, &o_split);
-  if (!ws || ws_bytes < need) return fail(HS_ERR_WORKSPACE_TOO_SMALL, "workspace %zu < %zu", ws_bytes, need);
-  cudaStream_t s = (cudaStream_t)stream;
-  char* w = reinterpret_cast<char*>(ws);
-  float* conf = reinterpret_cast<float*>(w + o_conf);
-  int32_t* am = reinterpret_cast<int32_t*>(w + o_am);
-  int64_t* pos = reinterpret_cast<int64_t*>(w + o_pos);
-  if (n == 0) {
-    st = cuda_check(cudaMemsetAsync(d_counts, 0, 2 * sizeof(int64_t), s), "memset counts");
-    return st;
-  }
-  {
-    hs::ConfArgs a = make_conf_args(logits, dtype, n, seq_len, n_classes, row_stride, row_index, d_n,
-                                    temperature, kind);
-    a.top_k = top_k;
-    if (hs::split_ws_bytes(n * (int64_t)seq_len)) a.split_ws = w + o_split;
-    if (flags & HS_STEP_OVERLAP_PREVIOUS) {
-      // CTAs that start late (SMs held by the previous kernel) take fewer rows
-      a.ticket = reinterpret_cast<unsigned int*>(w + o_tick);
-      a.late_wait = 1;
-    }
-    st = run_confidence_args(a, dtype, reduce, conf, am, nullptr, nullptr, w + o_cws, d_status, s);
-  }
+  st = hs_cascade_confidence(stage, n_stages, logits, dtype, n, seq_len, n_classes, row_stride, row_index, d_n,
+                             temperature, kind, reduce, threshold, d_threshold, nullptr, ws, ws_bytes, d_status,
+                             top_k, flags, stream);
   if (st != HS_OK) return st;
-  return route_compact_impl(conf, n, d_n, threshold, d_threshold, is_last, ids, am, seq_len, acc_ids, acc_conf,
-                            acc_pred, next_ids, next_payload ? pos : nullptr, payload,
-                            payload_row_bytes, next_payload, d_counts, ws, s);
+  return hs_cascade_compact(stage, n_stages, n, seq_len, d_n, threshold, d_threshold, ids, payload,
+                            payload_row_bytes, acc_ids, acc_conf, acc_pred, next_ids, next_payload, d_counts,
+                            ws, ws_bytes, stream);
 }
 
 size_t hs_calibrate_workspace(int32_t K, int32_t log2_bins) {

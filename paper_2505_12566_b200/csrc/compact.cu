@@ -428,7 +428,52 @@ __global__ void __launch_bounds__(256) gather_rows_kernel(const int64_t* __restr
   }
 }
 
+// Count of the items the threshold test defers (the next stage's batch size),
+// without the compaction: lets the next stage's confidence start while the
+// compaction of this stage runs off the critical path.  One atomic per CTA into
+// *out (zero-filled by the caller).
+__global__ void __launch_bounds__(256) count_deferred_kernel(const float* __restrict__ conf, int64_t cap,
+                                                             const int64_t* d_n, float threshold,
+                                                             const float* d_threshold, int is_last,
+                                                             unsigned long long* out) {
+  pdl_start();
+  __shared__ unsigned s_c[8];
+  int64_t n = cap;
+  if (d_n) n = min(*d_n, cap);
+  const float thr = d_threshold ? *d_threshold : threshold;
+  unsigned c = 0;
+  if (!is_last) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x * 4;
+    for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4; i < n; i += stride) {
+      if (i + 4 <= n) {
+        const float4 v = __ldg(reinterpret_cast<const float4*>(conf + i));
+        c += !(v.x >= thr) + !(v.y >= thr) + !(v.z >= thr) + !(v.w >= thr);
+      } else {
+        for (int64_t j = i; j < n; ++j) c += !(__ldg(conf + j) >= thr);
+      }
+    }
+  }
+  c = __reduce_add_sync(0xFFFFFFFFu, c);
+  if ((threadIdx.x & 31) == 0) s_c[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned t = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += s_c[w];
+    if (t) atomicAdd(out, (unsigned long long)t);
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_count_deferred(const float* conf, int64_t cap, const int64_t* d_n, float threshold,
+                                  const float* d_threshold, int is_last, unsigned long long* out,
+                                  cudaStream_t s) {
+  const int64_t want = (cap + 1023) / 1024;
+  const int64_t lim = (int64_t)num_sms() * 2;
+  const int grid = (int)(want < 1 ? 1 : (want < lim ? want : lim));
+  return launch_pdl(count_deferred_kernel, dim3(grid), dim3(256), 0, s, conf, cap, d_n, threshold,
+                    d_threshold, is_last, out);
+}
 
 size_t compact_ws_bytes(int64_t n) {
   const int64_t tiles = (n + kCompactTile - 1) / kCompactTile;

@@ -333,13 +333,10 @@ __device__ __forceinline__ int tree_first8(const uint32_t (&v)[8], uint32_t mb2)
   return (l1 ? 0 : 4) + (l2 ? 0 : 2) + (l3 ? 0 : 1);
 }
 
-// `srow`: shared-memory address of the row's vector 0 when the row is staged
-// there (cp.async / TMA kernels; 0xFFFFFFFF: not staged, re-read from L2).
 template <bool BF16, bool ENTROPY, int NV, int G>
 __device__ __forceinline__ void group_reduce_row(const ConfArgs& a, const uint4 (&v)[NV],
                                                  bool active, int64_t row, int gl,
-                                                 float c, const uint4* rowp, int32_t lab,
-                                                 uint32_t srow = 0xFFFFFFFFu) {
+                                                 float c, const uint4* rowp, int32_t lab) {
   constexpr int VE = BF16 ? 8 : 4;
   const f2_t c2 = f2(c, c);
   // 1. row max (exact, NaN-propagating): packed per-vector maxima, then the group
@@ -363,9 +360,9 @@ __device__ __forceinline__ void group_reduce_row(const ConfArgs& a, const uint4 
   // 2. argmax = lowest index holding m.  (i) each lane: lowest of its vectors
   //    whose packed max contains m -- bf16: one packed compare of the lane max,
   //    then a descent of the max tree (log2 NV compares); (ii) group min -> vector
-  //    vi; (iii) the group reads that one 16-byte vector -- from the shared-memory
-  //    stage when the row is staged there (no dependent L2 round trip), else from
-  //    L2 -- and finds the first element equal to m after the exponential pass.
+  //    vi; (iii) the group re-reads that one 16-byte vector (an L2 hit: the row
+  //    was just streamed) and finds the first element equal to m after the
+  //    exponential pass has hidden the load.
   //    A zero/subnormal m (or fp32) takes the exact fp32 compares.
 #ifdef HS_EXP_NOARGMAX
   const unsigned am = 0;
@@ -403,18 +400,9 @@ __device__ __forceinline__ void group_reduce_row(const ConfArgs& a, const uint4 
   for (int o = G / 2; o > 0; o >>= 1) vi = min(vi, (unsigned)__shfl_xor_sync(0xFFFFFFFFu, vi, o));
   // every lane of the group reads the same vector (one broadcast transaction);
   // an invalid row (no match) reads vector 0 and is discarded by write_row
-  const unsigned vr = vi < (unsigned)a.nvec ? vi : 0u;
-  uint4 xv;
-#ifdef HS_AB_L2_REREAD
-  srow = 0xFFFFFFFFu;
-#endif
-  if (srow != 0xFFFFFFFFu) {
-    __syncwarp();                    // the other lanes' staged vectors are visible
-    asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(xv.x), "=r"(xv.y), "=r"(xv.z), "=r"(xv.w) : "r"(srow + vr * 16u));
-  } else {
-    xv = __ldg(rowp + vr);
-  }
+  // (A/B: reading it from the shared-memory stage instead, behind a
+  // __syncwarp, was 4 % slower than this L2 hit)
+  const uint4 xv = __ldg(rowp + (vi < (unsigned)a.nvec ? vi : 0u));
 #endif
 
   // 3. exponentials with the common max: a = (x - m) * c, x - m formed exactly
@@ -908,8 +896,7 @@ __global__ void __launch_bounds__(kAsyncThreads, 3) conf_async_kernel(const Conf
       cp_async_wait<1>();        // this lane's copies of row A have landed
       group_lds_row<BF16, NV, G, FULL>(A, sbase + (uint32_t)(it & 1) * STAGEB, gl, nvec);
       if (a.tail) group_mask_tail<BF16, NV, G>(A, gl, nvec, a.tail);
-      group_reduce_row<BF16, ENTROPY, NV, G>(a, A, actA, rowA, gl, cA, pA, labA,
-                                             sbase + (uint32_t)(it & 1) * STAGEB - (uint32_t)gl * 16u);
+      group_reduce_row<BF16, ENTROPY, NV, G>(a, A, actA, rowA, gl, cA, pA, labA);
       if (!anyB) break;
       rowA = rowB;
       actA = actB;

@@ -102,6 +102,9 @@ struct CompactWs {          // zero-filled before first use; then self-maintaini
   // unsigned long long status[n_tiles] follows (32-byte header)
 };
 size_t compact_ws_bytes(int64_t n);
+cudaError_t launch_count_deferred(const float* conf, int64_t cap, const int64_t* d_n, float threshold,
+                                  const float* d_threshold, int is_last, unsigned long long* out,
+                                  cudaStream_t s);
 
 struct CompactArgs {
   const float* conf;

@@ -171,7 +171,7 @@ class Router:
     # ---- online: the cascade ------------------------------------
     def route(self, logits: list, *, n: int | None = None, ids=None, payload=None,
               by_id: bool = True, thresholds=None, overlap_first: bool = False, next_ranks=None,
-              events=None, upto: int | None = None, stream=None):
+              events=None, upto: int | None = None, split: bool = False, stream=None):
         """Route a batch; thresholds default to the calibrated device vector.
         ``overlap_first``: stage 1's confidence runs next to the calibration
         (HS_STEP_OVERLAP_PREVIOUS; it reads neither the calibration's buffers nor
@@ -179,5 +179,5 @@ class Router:
         thr = self.cal["t"] if thresholds is None else thresholds
         self.cascade.route(logits, thr, n=n, ids=ids, payload=payload, by_id=by_id,
                            overlap_first=overlap_first, peer=self.peer, next_ranks=next_ranks,
-                           events=events, upto=upto, stream=stream)
+                           events=events, upto=upto, split=split, stream=stream)
         return self.cascade

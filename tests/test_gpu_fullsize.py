@@ -94,8 +94,8 @@ def test_bench_step_full_size(hs, config):
     assert near.sum() <= 5
 
 
-@pytest.mark.parametrize("config", ["c2", "c4"])
-def test_bench_dense_step_full_size_every_request(hs, config):
+@pytest.mark.parametrize("config,split", [("c2", True), ("c2", False), ("c4", True)])
+def test_bench_dense_step_full_size_every_request(hs, config, split):
     """The TIMED configuration of bench.py (--layout dense, the default): stage
     k's logits are the dense batch of the requests that reach model k; the
     step (batched validation confidence, resident calibration, stage 1
@@ -105,7 +105,6 @@ def test_bench_dense_step_full_size_every_request(hs, config):
     and the GPU's accepted and deferred lists must equal the oracle's split of
     the same batch, with the near-threshold requests (G18) removed and counted;
     accepted confidences within 1e-5 and predictions bit-exact."""
-    import argparse
     import bench
     dev = torch.device("cuda:0")
     fam = bench.family(config)
@@ -116,7 +115,7 @@ def test_bench_dense_step_full_size_every_request(hs, config):
 
     def step():
         router.calibrate(val, labels)
-        router.route(route, payload=payload, overlap_first=True, by_id=False)
+        router.route(route, payload=payload, overlap_first=True, by_id=False, split=split)
 
     with torch.cuda.stream(stream):
         step()

@@ -934,3 +934,44 @@ def test_conf_entropy_alongside(hs, C, dtype, kind):
         assert_conf_close(r["conf_entropy"].cpu().numpy(), ent["conf"])
     with pytest.raises(hs.HsError):
         hs.confidence(x, n=n // 2, seq_len=2, n_classes=C, reduce=1, want_entropy=True)
+
+
+@pytest.mark.parametrize("graph", [False, True])
+def test_split_compaction_equals_step(hs, graph):
+    """hs_cascade_confidence (+ deferred count) / hs_cascade_compact on a side
+    stream -- the compaction off the critical path -- gives the cascade of
+    hs_cascade_step bit for bit (dense stage batches, stage 1 overlapping the
+    calibration), eagerly and replayed from a CUDA graph, over repeated steps."""
+    import bench
+    fam = synth.scaled(synth.FAMILIES["c2"], n=65536, n_val=20000)
+    route, val, labels, payload = bench.build_inputs(fam, 0, dev())
+    base = bench.make_router(fam, dev(), None)
+    dense, _ = bench.dense_stage_logits(fam, base, route, val, labels, payload, 0, dev())
+
+    def run(split):
+        r = bench.make_router(fam, dev(), None)
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            def step():
+                r.calibrate(val, labels)
+                r.route(dense, overlap_first=True, by_id=False, split=split)
+            step()
+            if graph:
+                s.synchronize()
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=s):
+                    step()
+                for _ in range(3):
+                    g.replay()
+            else:
+                for _ in range(3):
+                    step()
+        torch.cuda.synchronize()
+        return r.cascade.counts.cpu(), r.cascade.results()
+
+    c0, res0 = run(False)
+    c1, res1 = run(True)
+    assert torch.equal(c0, c1)
+    for a, b in zip(res0, res1):
+        for key in ("ids", "conf", "pred"):
+            assert torch.equal(a[key], b[key]), key

@@ -8,8 +8,6 @@ from paper_2505_12566_b200 import _build  # noqa: E402
 
 VARIANTS = {
     "linargmax": ["HS_AB_LINEAR_ARGMAX"],             # K1a argmax: one compare per vector (round 1)
-    "l2reread": ["HS_AB_L2_REREAD"],                  # K1a argmax: winning vector re-read from L2 (round 1)
-    "r1argmax": ["HS_AB_LINEAR_ARGMAX", "HS_AB_L2_REREAD"],
     "ctrace": ["HS_CALIB_TRACE"],        # globaltimer trace of the calibration kernels
     "noargmax": ["HS_EXP_NOARGMAX"],     # upper bounds: K1 without the argmax ...
     "noexp": ["HS_EXP_NOEXP"],           # ... or without the exponential pass
