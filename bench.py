@@ -55,9 +55,10 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-overlap", action="store_true",
                     help="run routing stage 1 strictly after the calibration (no PDL overlap)")
-    ap.add_argument("--no-split", action="store_true",
-                    help="run each stage's compaction on the critical path (hs_cascade_step) instead of "
-                         "on a side stream next to the next stage's confidence")
+    ap.add_argument("--split", action="store_true",
+                    help="run each stage's compaction on a side stream next to the next stage's "
+                         "confidence (hs_cascade_confidence + count / hs_cascade_compact); A/B on one "
+                         "B200: 0.415 ms vs 0.396 ms per C2 step for the default single-stream step")
     ap.add_argument("--native-comm", action="store_true",
                     help="calibration all-reduce inside libhs on its own NCCL communicator "
                          "(hs_calibrate_thresholds_comm) instead of torch.distributed")
@@ -68,12 +69,14 @@ def parse():
                          "gathers its rows; dense: stage k's logits are the dense batch of "
                          "the requests that reach model k, in order (the model ran on that "
                          "batch only, P:320-322)")
-    ap.add_argument("--placement", default="balanced", choices=["balanced", "local", "nccl"],
+    ap.add_argument("--placement", default="balanced", choices=["balanced", "placed", "local", "nccl"],
                     help="balanced (default): after every stage the global stable deferred list is "
                          "re-spread in contiguous blocks over all ranks by the library's kernels over "
                          "peer memory (hs_cascade_step_peer; calibration histograms summed inside the "
                          "calibration kernel, hs_calibrate_thresholds_peer) -- one CUDA graph per "
                          "step, no host round trip; at one GPU the exchange is the identity. "
+                         "placed: the same exchange, but stage k's batch goes only to the ranks holding "
+                         "model k's replicas, R_m proportional to reach_m x cost_m (P:627-640). "
                          "local: every rank serves every stage of its own shard (replicas, no "
                          "exchange).  nccl: the balanced re-spread with torch.distributed NCCL "
                          "(count all-gather + all-to-all, host split sizes, eager) -- the baseline")
@@ -268,7 +271,7 @@ def committed_traffic(config: str, name: str = "r01_k1_traffic.json"):
     return rec.get("dram_bytes_per_launch") if rec.get("config") == config else None
 
 
-def dense_stage_logits(fam, router, route, val, labels, payload, rank, dev, ids0=None):
+def dense_stage_logits(fam, router, route, val, labels, payload, rank, dev, ids0=None, next_ranks=None):
     """--layout dense: learn, stage by stage (untimed), which requests reach
     each model on this rank and generate stage k's logits (same keyed
     generator, so the same values per request) as the dense batch of exactly
@@ -285,7 +288,7 @@ def dense_stage_logits(fam, router, route, val, labels, payload, rank, dev, ids0
     peer = router.peer
     for k in range(1, fam.K):
         # stages 0..k-1 on the batches known so far (every rank in lockstep)
-        router.route(out, ids=ids0, payload=payload, by_id=False, upto=k - 1)
+        router.route(out, ids=ids0, payload=payload, by_id=False, upto=k - 1, next_ranks=next_ranks)
         torch.cuda.synchronize()
         if peer is not None:
             nk = int(peer.recv_count[k - 1].item())
@@ -300,7 +303,7 @@ def dense_stage_logits(fam, router, route, val, labels, payload, rank, dev, ids0
             workload.gpu_logits(x, fam, k, ids=ids, n=nk)
         out[k] = x
         route[k] = None                    # the full-population tensor is not needed
-    router.route(out, ids=ids0, payload=payload, by_id=False)
+    router.route(out, ids=ids0, payload=payload, by_id=False, next_ranks=next_ranks)
     torch.cuda.synchronize()
     torch.cuda.empty_cache()
     return out, dense_signature(router, fam)
@@ -317,12 +320,12 @@ def dense_signature(router, fam):
     return counts, batch
 
 
-def make_router(fam, dev, group, native_comm: bool = False, peer=None):
+def make_router(fam, dev, group, native_comm: bool = False, peer=None, n_cap=None):
     import paper_2505_12566_b200 as hs
     from paper_2505_12566_b200.router import Router
     stages = [hs.StageSpec(fam.C, fam.temps[k], fam.L, fam.kind, fam.reduce, fam.top_k)
               for k in range(fam.K)]
-    return Router(stages, fam.n, fam.n_val, dev, log2_bins=fam.log2_bins,
+    return Router(stages, n_cap or fam.n, fam.n_val, dev, log2_bins=fam.log2_bins,
                   payload_row_bytes=fam.payload_bytes, group=group, native_comm=native_comm, peer=peer)
 
 
@@ -352,10 +355,23 @@ def run_ours(args, world, rank, local):
     group = dist.group.WORLD if dist.is_initialized() else None
     route, val, labels, payload = build_inputs(fam, rank, dev)
     peer = None
-    if world > 1 and args.placement == "balanced":
-        peer = hsd.PeerGroup(fam.n, fam.payload_bytes, fam.log2_bins, K=fam.K, group=group, device=dev)
+    placed = args.placement == "placed" and world > 1
+    # placed: a rank holding a model's replica can receive up to world x its shard
+    cap = fam.n * (world if placed else 1)
+    if world > 1 and args.placement in ("balanced", "placed"):
+        peer = hsd.PeerGroup(cap, fam.payload_bytes, fam.log2_bins, K=fam.K, group=group, device=dev)
     router = make_router(fam, dev, None if peer is not None else group, native_comm=args.native_comm,
-                         peer=peer)
+                         peer=peer, n_cap=cap)
+    next_ranks = None
+    if placed:
+        # replicas from the calibrated validation reach (global, summed inside the
+        # calibration kernel) and per-visit costs (GRAPH_W: synthetic ViT ratios)
+        router.calibrate(val, labels)
+        reach = [float(x) for x in router.cal["reach"].cpu().tolist()]
+        replicas = hsd.replica_counts(world, [r / max(reach[0], 1.0) for r in reach], list(GRAPH_W[:fam.K]))
+        ranks = hsd.placed_ranks(world, replicas)
+        next_ranks = ranks[1:]
+        router.next_ranks = next_ranks
     ids0 = (torch.arange(rank * fam.n, (rank + 1) * fam.n, dtype=torch.int64, device=dev)
             if peer is not None else None)
     ev = (timing_event(), timing_event())
@@ -363,7 +379,8 @@ def run_ours(args, world, rank, local):
     if peer is not None and not dense:
         raise SystemExit("bench: the balanced placement routes dense stage batches (--layout dense)")
     if dense:
-        route, dense_sig = dense_stage_logits(fam, router, route, val, labels, payload, rank, dev, ids0)
+        route, dense_sig = dense_stage_logits(fam, router, route, val, labels, payload, rank, dev, ids0,
+                                              next_ranks=next_ranks)
     K = fam.K
     sev = [timing_event() for _ in range(2 * K)] + [timing_event()]
 
@@ -372,7 +389,8 @@ def run_ours(args, world, rank, local):
         # routing stage-1 K1 then runs next to the latency-bound calibration
         router.calibrate(val, labels, time_val=ev)
         router.route(route, ids=ids0, payload=payload, overlap_first=not args.no_overlap,
-                     by_id=not dense, events=events, split=dense and peer is None and not args.no_split)
+                     by_id=not dense, events=events, split=dense and peer is None and args.split,
+                     next_ranks=next_ranks)
         if events is not None:
             sev[2 * K].record()
 
@@ -489,8 +507,9 @@ def run_ours(args, world, rank, local):
                    "sequence_reduce": ["none", "min", "mean"][fam.reduce],
                    "log2_bins": fam.log2_bins,
                    "parallelism": f"request-sharded dp{world}"
-                   + (", balanced forwarding + calibration exchange over peer memory (hs_peer_*)"
-                      if peer is not None else ", replicas (no exchange)" if world > 1 else ""),
+                   + (f", {'placed' if placed else 'balanced'} forwarding + calibration exchange over "
+                      "peer memory (hs_peer_*)" if peer is not None else ", replicas (no exchange)"
+                      if world > 1 else ""),
                    "placement": args.placement if world > 1 else "single GPU",
                    "l2": "inputs larger than L2 (per-step logits working set >> 126 MB)",
                    "logits_layout": args.layout,
@@ -512,6 +531,9 @@ def run_ours(args, world, rank, local):
         "gpu_launches_per_step": gpu_launches / args.steps,
         "step_ms_percentiles": step_pct,
     }
+    if placed:
+        line["config"]["replicas_per_model"] = replicas
+        line["config"]["model_ranks"] = ranks
     if peer is not None:
         # forwarded ids (+ payload rows) per stage, NVLink bytes sent per rank
         fwd_items = [int(x) for x in sum_over_ranks([float(d) for d in deferred_local], world)]

@@ -697,6 +697,9 @@ class Cascade:
             row_index = cur_ids if by_id else None
             if by_id and cur_ids is None:
                 row_index = None   # stage 1 with identity ids: row = id = position
+            # stages after the first: capacity-sized (a placed rank may receive
+            # more than its own shard), the live count comes from d_n
+            nk = n if (k == 0 or peer is None) else self.n_cap
             kw = {}
             fwd = peer is not None and k < self.K - 1
             if fwd and events is None:
@@ -704,7 +707,7 @@ class Cascade:
                       "next_ranks": None if next_ranks is None else next_ranks[k]}
             if events is not None:
                 events[2 * k].record(stream)
-            cascade_step(k, self.K, logits[k], thr, n=n, seq_len=s.seq_len, n_classes=s.n_classes,
+            cascade_step(k, self.K, logits[k], thr, n=nk, seq_len=s.seq_len, n_classes=s.n_classes,
                          temperature=s.temperature, kind=s.kind, reduce=s.reduce,
                          row_index=row_index, d_n=d_n,
                          ids=cur_ids, payload=cur_payload, payload_row_bytes=self.P,

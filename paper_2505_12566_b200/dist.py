@@ -76,6 +76,44 @@ def forward_deferred(ids: torch.Tensor, count: torch.Tensor, *, dest_ranks: list
     return out_ids, out_payload, n_recv
 
 
+def replica_counts(world: int, reach: list[float], cost: list[float]) -> list[int]:
+    """Replicas per model for the PLACED placement, from the
+    zero-queuing rule of P:627-640 (§V-C): R_m S_m proportional to rho_m l_m
+    ("the replications (R_1..R_n) should be (rho_1 l_1, .., rho_n l_n)/R_m ...
+    round the real number to the nearest positive integer"), with
+    rho_m the fraction of requests reaching model m, l_m its per-request cost
+    and S_m = 1 (no model partitioning).  The world's GPUs are shared out:
+    R_m = max(1, round(world * rho_m l_m / sum_j rho_j l_j)), then trimmed
+    (largest first) or topped up (largest remainder first) until sum R_m ==
+    world when the models fit, else each model keeps one replica."""
+    w = [max(0.0, float(r)) * max(0.0, float(c)) for r, c in zip(reach, cost)]
+    K = len(w)
+    tot = sum(w)
+    if tot <= 0:
+        return [1] * K
+    exact = [world * x / tot for x in w]
+    R = [max(1, int(round(x))) for x in exact]
+    if K > world:
+        return [1] * K
+    while sum(R) > world:
+        i = max((i for i in range(K) if R[i] > 1), key=lambda i: R[i] - exact[i])
+        R[i] -= 1
+    while sum(R) < world:
+        i = max(range(K), key=lambda i: exact[i] - R[i])
+        R[i] += 1
+    return R
+
+
+def placed_ranks(world: int, replicas: list[int]) -> list[list[int]]:
+    """Ranks hosting each model's replicas: consecutive blocks of the rank
+    range, wrapping around (models share GPUs when sum R_m > world)."""
+    out, start = [], 0
+    for r in replicas:
+        out.append([(start + i) % world for i in range(r)])
+        start = (start + r) % world
+    return out
+
+
 def global_order_offsets(counts: list[int]) -> list[int]:
     """off_g = sum_{h<g} D_h: where rank g's deferred list starts in the global order."""
     off, acc = [], 0

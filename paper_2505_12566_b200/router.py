@@ -37,6 +37,7 @@ class Router:
         self.device = torch.device(device)
         self.group = group
         self.peer = peer
+        self.next_ranks = None      # placed placement: destination ranks per forward
         dev = self.device
         K = self.K
         # validation confidences of all K stages: rows 0..K-2 are the calibration input
@@ -178,6 +179,7 @@ class Router:
         is read by it -- only the threshold test waits for the thresholds)."""
         thr = self.cal["t"] if thresholds is None else thresholds
         self.cascade.route(logits, thr, n=n, ids=ids, payload=payload, by_id=by_id,
-                           overlap_first=overlap_first, peer=self.peer, next_ranks=next_ranks,
+                           overlap_first=overlap_first, peer=self.peer,
+                           next_ranks=next_ranks if next_ranks is not None else self.next_ranks,
                            events=events, upto=upto, split=split, stream=stream)
         return self.cascade

@@ -179,3 +179,38 @@ def test_replay_and_graph_argument_errors(libhs):
     assert rc == 1 and "d_model_correct" in lib.hs_last_error().decode()
     rc = lib.hs_perf_graph(256, 512, 10, 100, 5, 5, None, 3, 1, 2, 3, 4, 5, 4096, gws - 1, None, None)
     assert rc == 5
+
+
+def _build_c_client(tmp_path):
+    import shutil
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    pkg = os.path.join(root, "paper_2505_12566_b200")
+    cc = shutil.which("gcc") or shutil.which("cc")
+    if cc is None:
+        pytest.skip("no C compiler")
+    exe = str(tmp_path / "hs_c_client")
+    r = subprocess.run([cc, "-std=c11", "-Wall", "-Werror", "-I", os.path.join(root, "include"),
+                        "-I", "/usr/local/cuda/include", os.path.join(root, "examples", "c_client.c"),
+                        "-L", pkg, "-lhs", f"-Wl,-rpath,{pkg}", "-L", "/usr/local/cuda/lib64", "-lcudart",
+                        "-lm", "-o", exe], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    return exe
+
+
+def test_c_program_links_libhs(libhs, tmp_path):
+    """A plain C program built against include/hs.h and linked with -lhs (no
+    Python): host-only calls and the synchronous argument checks."""
+    import subprocess
+    r = subprocess.run([_build_c_client(tmp_path)], capture_output=True, text=True, timeout=60)
+    assert r.returncode == 0 and "c client ok" in r.stdout, r.stdout + r.stderr
+
+
+@pytest.mark.gpu
+def test_c_program_routes_a_cascade_on_the_gpu(libhs, tmp_path):
+    """The same C program with --gpu: one 6-request, 3-stage cascade through
+    hs_cascade_step with cudaMalloc'd buffers, checked against the hand-worked
+    stages (P:443-444)."""
+    import subprocess
+    r = subprocess.run([_build_c_client(tmp_path), "--gpu"], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0 and "c client ok" in r.stdout, r.stdout + r.stderr

@@ -105,3 +105,21 @@ def test_bench_spawns_ranks_and_reduces():
     line = json.loads(r.stdout.strip().splitlines()[-1])
     assert line == {"plumbing_check": True, "world": 2, "handles_ok": True, "max": [1.0, 10.0],
                     "sum": [3.0]}
+
+
+def test_replica_counts_follow_the_zero_queuing_rule():
+    """R_m proportional to rho_m l_m, rounded to positive integers,
+    and the world's GPUs shared out exactly."""
+    R = hsd.replica_counts(8, [1.0, 0.5, 0.3, 0.2, 0.18], [1, 2, 4, 8, 16])
+    assert sum(R) == 8 and min(R) >= 1
+    w = [1.0 * 1, 0.5 * 2, 0.3 * 4, 0.2 * 8, 0.18 * 16]
+    assert R[4] == max(R) and R[4] >= R[0]          # the giant model carries the most load
+    # exact proportions are reproduced when they are integers
+    assert hsd.replica_counts(6, [1, 1, 1], [1, 2, 3]) == [1, 2, 3]
+    assert hsd.replica_counts(4, [1, 0, 0], [1, 1, 1]) == [2, 1, 1]     # every model keeps a replica
+    assert hsd.replica_counts(2, [1, 1, 1], [1, 1, 1]) == [1, 1, 1]     # more models than GPUs
+    assert hsd.replica_counts(8, [0, 0], [1, 1]) == [1, 1]
+    ranks = hsd.placed_ranks(8, R)
+    assert [len(r) for r in ranks] == R
+    assert sorted(x for r in ranks for x in r) == list(range(8))       # every GPU used once
+    assert hsd.placed_ranks(3, [2, 2]) == [[0, 1], [2, 0]]
