@@ -33,6 +33,10 @@ CONFIG_TEXT = {
     "c3": "4-size T5 cascade, 2,048 sequences x 64 tokens x 32,128 vocab bf16 per GPU (16,384 over 8 GPUs), MIN token confidence, 256 B payload gathered, 512 validation sequences per GPU",
     "c4": "3-stage Llama-like next-token cascade, 8,192 requests x 128,256 vocab bf16 per GPU, entropy confidence, 8 KB hidden-state payload gathered",
     "c5": "5-stage ViT streaming cascade, 1,048,576 requests x 1,000 classes bf16 per GPU (8M over 8 GPUs), validation 131,072 per GPU",
+    "c5s": "5-stage ViT streaming cascade, STRONG scaling: 8,388,608 requests x 1,000 classes bf16 in total, "
+           "2^23 / N per GPU (validation 2^20 / N per GPU)",
+    "c5p": "5-stage ViT cascade, 16,384 requests x 1,000 classes bf16 per GPU, each request carrying its "
+           "3 x 224 x 224 u8 image (150,528 B payload) that is gathered / forwarded with every deferral",
     "c3k": "c3 with the Top-K (K = 10) restricted token confidence of P:420-424 (NEXT-2), MIN over 64 tokens",
     "c3m": "c3 with the MEAN of the 64 token confidences as the sequence confidence (north_star; the paper's is MIN, P:423)",
     "c2g": "NEXT-4: threshold performance graph of the 5 C2 ViT stage models: the exhaustive q = 4 grid (18^4 = 104,976 threshold vectors) replayed on the 50,000-sample validation set per GPU, Pareto frontier, AP and EO picks",
@@ -213,11 +217,18 @@ def sum_over_ranks(x, world: int):
 # ---------------------------------------------------------------------------
 # workload (per rank): weak scaling -- every rank routes its own shard
 # ---------------------------------------------------------------------------
-def family(config: str):
+def family(config: str, world: int = 1):
+    import dataclasses
     from workload import synth
     f = synth.FAMILIES.get(config)
     if config == "c5":      # per-GPU shard of the 8-GPU streaming config
         f = synth.scaled(f, n=1 << 20, n_val=1 << 17)
+    if config == "c5s":     # strong scaling: the whole 2^23-request job split over the GPUs
+        f = dataclasses.replace(synth.scaled(synth.FAMILIES["c5"], n=(1 << 23) // world,
+                                             n_val=(1 << 20) // world), name="c5s_vit5_strong_bf16")
+    if config == "c5p":     # the NVLink-roofline variant: a 3x224x224 u8 image forwarded with each request
+        f = dataclasses.replace(synth.scaled(synth.FAMILIES["c5"], n=16384, n_val=1 << 17),
+                                name="c5p_vit5_image_payload_bf16", payload_bytes=150528)
     if config == "c3k":     # NEXT-2: the T5 shard with Top-K token confidence
         import dataclasses
         f = dataclasses.replace(synth.scaled(synth.FAMILIES["c3"], n=2048, n_val=512),
@@ -351,7 +362,7 @@ def run_ours(args, world, rank, local):
     from paper_2505_12566_b200 import dist as hsd
 
     dev = torch.device("cuda", local)
-    fam = family(args.config)
+    fam = family(args.config, world)
     group = dist.group.WORLD if dist.is_initialized() else None
     route, val, labels, payload = build_inputs(fam, rank, dev)
     peer = None
@@ -498,7 +509,8 @@ def run_ours(args, world, rank, local):
     line = {
         "metric": METRIC, "value": value, "unit": "requests/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "scaling": "strong" if args.config == "c5s" else "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic",
         "config": {"workload": fam.name, "description": CONFIG_TEXT[args.config],
                    "requests_per_gpu": fam.n, "validation_per_gpu": fam.n_val, "K": K,
                    "classes": fam.C, "seq_len": fam.L, "logits_dtype": fam.dtype,
@@ -531,6 +543,13 @@ def run_ours(args, world, rank, local):
         "gpu_launches_per_step": gpu_launches / args.steps,
         "step_ms_percentiles": step_pct,
     }
+    if fam.payload_bytes:
+        # deferred requests carry their payload rows: gathered (read + write) at
+        # every deferral on a single GPU, forwarded over NVLink at N > 1
+        moved = sum_over_ranks([float(sum(deferred_local) * 2 * fam.payload_bytes)], world)[0]
+        line["payload"] = {"row_bytes": fam.payload_bytes, "bytes_moved_per_step": moved,
+                           "GBps_step": moved / (ms / 1e3) / 1e9,
+                           "note": "gather K4 / peer scatter of the deferred rows; step-level rate"}
     if placed:
         line["config"]["replicas_per_model"] = replicas
         line["config"]["model_ranks"] = ranks

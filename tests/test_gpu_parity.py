@@ -924,12 +924,14 @@ def test_conf_entropy_alongside(hs, C, dtype, kind):
     bits = x32 if dtype == "fp32" else \
         torch.from_numpy(x32).to(torch.bfloat16).view(torch.int16).numpy().view(np.uint16)
     n = bits.shape[0]
-    x = to_dev_bits(bits, dtype)
+    ve = 8 if dtype == "bf16" else 4
+    x = to_dev_bits(bits, dtype, C + (-C) % ve)       # rows padded to 16 bytes
     for ws in (None, torch.zeros(16, dtype=torch.uint8, device=dev())):
         r = hs.confidence(x, n_classes=C, temperature=0.7, kind=kind, want_entropy=True, ws=ws)
         torch.cuda.synchronize()
-        ref = oracle.confidence(host_bits(x), n, 1, C, C, 0.7, kind=kind)
-        ent = oracle.confidence(host_bits(x), n, 1, C, C, 0.7, kind=2)
+        st = x.shape[1]
+        ref = oracle.confidence(host_bits(x), n, 1, C, st, 0.7, kind=kind)
+        ent = oracle.confidence(host_bits(x), n, 1, C, st, 0.7, kind=2)
         assert_conf_close(r["conf"].cpu().numpy(), ref["conf"])
         assert_conf_close(r["conf_entropy"].cpu().numpy(), ent["conf"])
     with pytest.raises(hs.HsError):
