@@ -540,7 +540,7 @@ hs_status_t hs_ipc_close(void* dptr);
  *   the global histogram (integer counts: order-independent, deterministic).
  *   target_correct < 0: AP, tau = the GLOBAL correct count of m_K.  comm ==
  *   NULL: single GPU (the same sweep without the all-reduce).  Outputs as
- *   hs_calibrate_thresholds (refinement passes are not available here).
+ *   hs_calibrate_thresholds (refinement passes: hs_calibrate_thresholds_comm_ex).
  *   Every argument is validated before the first collective, so an argument
  *   error returns on the failing rank before any rank has entered a round
  *   (the arguments that decide the collectives -- K, log2_bins -- must agree
@@ -577,6 +577,15 @@ hs_status_t hs_calibrate_thresholds_comm(const float* conf, const uint8_t* corre
                                          int64_t* d_handled, int64_t* d_correct_total,
                                          hs_comm_t comm, void* ws, size_t ws_bytes,
                                          hs_stream_t stream);
+/* hs_calibrate_thresholds_comm_ex: the same plus refine_passes (0..64) D5
+ * refinement passes on the sharded set (as hs_calibrate_thresholds): per pass
+ * and stage the refinement histogram and A_k are summed across ranks, and the
+ * final replay's reach / handled / correct_total are summed too. */
+hs_status_t hs_calibrate_thresholds_comm_ex(const float* conf, const uint8_t* correct, int32_t K,
+                                            int64_t N, int32_t log2_bins, int64_t target_correct,
+                                            int32_t refine_passes, int32_t* d_bin_idx, float* d_thresholds,
+                                            int64_t* d_reach, int64_t* d_handled, int64_t* d_correct_total,
+                                            hs_comm_t comm, void* ws, size_t ws_bytes, hs_stream_t stream);
 
 /* ------------------------------------------------------------------------ */
 /* Diagnostics.                                                              */

@@ -409,17 +409,19 @@ def forward_nccl(ids: torch.Tensor, d_count: torch.Tensor, comm: int, world: int
 
 
 def calibrate_thresholds_comm(conf: torch.Tensor, correct: torch.Tensor, comm: int | None, *,
-                              log2_bins: int = 12, target: int = -1, out: dict | None = None,
-                              ws: torch.Tensor | None = None, stream=None) -> dict:
+                              log2_bins: int = 12, target: int = -1, refine_passes: int = 0,
+                              out: dict | None = None, ws: torch.Tensor | None = None,
+                              stream=None) -> dict:
     """hs_calibrate_thresholds over a validation set sharded across the ranks
-    of ``comm`` (this rank's shard in conf / correct); identical b_k on every rank."""
+    of ``comm`` (this rank's shard in conf / correct); identical b_k on every
+    rank (hs_calibrate_thresholds_comm_ex; refinement passes summed across ranks)."""
     _check_cuda(conf, correct)
     K, N = int(correct.shape[0]), int(correct.shape[1])
     out = _calib_out(K, conf.device, out)
     if ws is None:
         ws = calibrate_workspace(K, log2_bins, conf.device)
-    _abi.call("hs_calibrate_thresholds_comm", _p(conf), _p(correct), K, N, int(log2_bins), int(target),
-              _p(out["b"]), _p(out["t"]), _p(out["reach"]), _p(out["handled"]),
+    _abi.call("hs_calibrate_thresholds_comm_ex", _p(conf), _p(correct), K, N, int(log2_bins), int(target),
+              int(refine_passes), _p(out["b"]), _p(out["t"]), _p(out["reach"]), _p(out["handled"]),
               _p(out["correct_total"]), comm, _p(ws), ws.numel(), _stream(stream))
     return out
 

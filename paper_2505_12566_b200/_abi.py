@@ -80,6 +80,7 @@ SIGNATURES = {
     "hs_comm_create": (I32, [P, I32, I32, I32, P]),
     "hs_comm_destroy": (I32, [P]),
     "hs_calibrate_thresholds_comm": (I32, [P, P, I32, I64, I32, I64, P, P, P, P, P, P, P, SZ, P]),
+    "hs_calibrate_thresholds_comm_ex": (I32, [P, P, I32, I64, I32, I64, I32, P, P, P, P, P, P, P, SZ, P]),
     "hs_forward_nccl_workspace": (SZ, [I32]),
     "hs_forward_nccl": (I32, [P, P, I64, P, P, I32, P, P, I64, P, P, P, SZ, P]),
     "hs_status_string": (ctypes.c_char_p, [I32]),

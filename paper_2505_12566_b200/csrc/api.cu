@@ -611,6 +611,18 @@ hs_status_t hs_calibrate_thresholds_comm(const float* conf, const uint8_t* corre
                                          int64_t* d_handled, int64_t* d_correct_total,
                                          hs_comm_t comm, void* ws, size_t ws_bytes,
                                          hs_stream_t stream) {
+  return hs_calibrate_thresholds_comm_ex(conf, correct, K, N, log2_bins, target_correct, 0, d_bin_idx,
+                                         d_thresholds, d_reach, d_handled, d_correct_total, comm, ws,
+                                         ws_bytes, stream);
+}
+
+hs_status_t hs_calibrate_thresholds_comm_ex(const float* conf, const uint8_t* correct, int32_t K,
+                                            int64_t N, int32_t log2_bins, int64_t target_correct,
+                                            int32_t refine_passes, int32_t* d_bin_idx, float* d_thresholds,
+                                            int64_t* d_reach, int64_t* d_handled, int64_t* d_correct_total,
+                                            hs_comm_t comm, void* ws, size_t ws_bytes, hs_stream_t stream) {
+  if (refine_passes < 0 || refine_passes > 64)
+    return fail(HS_ERR_INVALID_ARGUMENT, "refine_passes = %d outside 0..64", refine_passes);
   if (!d_bin_idx || !d_thresholds || !d_reach || !d_handled || !d_correct_total)
     return fail(HS_ERR_INVALID_ARGUMENT, "all calibration outputs are required");
   // validate everything the rounds will check before any collective is posted
@@ -633,7 +645,36 @@ hs_status_t hs_calibrate_thresholds_comm(const float* conf, const uint8_t* corre
                              d_correct_total, ws, ws_bytes, stream);
     if (st != HS_OK) return st;
   }
-  return HS_OK;
+  if (refine_passes == 0) return HS_OK;
+  // D5 refinement on the sharded set: per pass and stage, each rank histograms
+  // its samples that reach k (downstream correctness as third channel) and adds
+  // A_k (answers given before k); histogram and A_k are summed across ranks,
+  // every rank selects the same b_k; a final replay's counts are summed too.
+  cudaStream_t s = (cudaStream_t)stream;
+  int64_t* d_A = reinterpret_cast<int64_t*>(ws);     // CalibState::A (first field)
+  for (int32_t p = 0; p < refine_passes; ++p) {
+    for (int32_t k = 0; k < K - 1; ++k) {
+      st = cuda_check(hs::launch_calib_refine_round(conf, correct, K, N, log2_bins, k, d_bin_idx, ws, p == 0 && k == 0, s),
+                      "calib refinement histogram");
+      if (st != HS_OK) return st;
+      if (comm) {
+        int r = hs::nccl_allreduce_i32_sum(hist, words, comm, s);
+        if (!r) r = hs::nccl_allreduce_i64_sum(d_A, 1, comm, s);
+        if (r) return fail(HS_ERR_NCCL, "ncclAllReduce (refinement): %s", hs::nccl_error(r));
+      }
+      st = hs_calibrate_select(K, log2_bins, k, d_bin_idx, d_thresholds, d_reach, d_handled, d_correct_total,
+                               ws, ws_bytes, stream);
+      if (st != HS_OK) return st;
+    }
+  }
+  st = cuda_check(hs::launch_calib_replay(conf, correct, K, N, log2_bins, d_bin_idx, d_reach, d_handled,
+                                          d_correct_total, s),
+                  "calib replay");
+  if (st != HS_OK || !comm) return st;
+  int r = hs::nccl_allreduce_i64_sum(d_reach, K, comm, s);
+  if (!r) r = hs::nccl_allreduce_i64_sum(d_handled, K, comm, s);
+  if (!r) r = hs::nccl_allreduce_i64_sum(d_correct_total, 1, comm, s);
+  return r ? fail(HS_ERR_NCCL, "ncclAllReduce (replay): %s", hs::nccl_error(r)) : HS_OK;
 }
 
 // ws: this rank's (count, recv_cap) pair, then every rank's pairs

@@ -1067,6 +1067,43 @@ cudaError_t launch_calib_peer(const float* conf, const uint8_t* correct, int K, 
   return launched ? cudaSuccess : cudaErrorNotSupported;
 }
 
+// Building blocks of the refinement for a sharded validation set (the caller
+// sums the histogram + A, and the replay counts, across ranks in between).
+cudaError_t launch_calib_refine_round(const float* conf, const uint8_t* correct, int K, int64_t N, int q,
+                                      int k, const int32_t* b_idx, void* ws, bool zero_hist, cudaStream_t s) {
+  CalibState* st = reinterpret_cast<CalibState*>(ws);
+  int32_t* hist = hist_of(ws);
+  const size_t smem = (size_t)3 * ((1 << q) + 2) * sizeof(unsigned);
+  static const bool attr = [] {
+    cudaFuncSetAttribute(calib_refine_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(3 * ((1 << 14) + 2) * sizeof(unsigned)));
+    return true;
+  }();
+  (void)attr;
+  int64_t grid = (N + 4095) / 4096;
+  if (grid > num_sms()) grid = num_sms();
+  if (grid < 1) grid = 1;
+  cudaError_t e = zero_hist ? cudaMemsetAsync(hist, 0, calib_hist_bytes(q), s) : cudaSuccess;
+  if (e == cudaSuccess) e = launch_pdl(calib_refine_begin_kernel, dim3(1), dim3(32), 0, s, st);
+  if (e == cudaSuccess && N > 0)
+    e = launch_pdl(calib_refine_hist_kernel, dim3((int)grid), dim3(512), smem, s, conf, correct, K, N, q, k,
+                   b_idx, hist, st);
+  return e;
+}
+
+cudaError_t launch_calib_replay(const float* conf, const uint8_t* correct, int K, int64_t N, int q,
+                                const int32_t* b_idx, int64_t* reach, int64_t* handled, int64_t* correct_total,
+                                cudaStream_t s) {
+  int64_t grid = (N + 4095) / 4096;
+  if (grid > num_sms()) grid = num_sms();
+  if (grid < 1) grid = 1;
+  cudaError_t e = launch_pdl(calib_replay_zero_kernel, dim3(1), dim3(32), 0, s, K, reach, handled, correct_total);
+  if (e == cudaSuccess && N > 0)
+    e = launch_pdl(calib_replay_kernel, dim3((int)grid), dim3(512), 0, s, conf, correct, K, N, q, b_idx, reach,
+                   handled, correct_total);
+  return e;
+}
+
 cudaError_t launch_calib_refine(const float* conf, const uint8_t* correct, int K, int64_t N, int q,
                                 int passes, int32_t* b_idx, float* thr, int64_t* reach,
                                 int64_t* handled, int64_t* correct_total, void* ws,

@@ -138,4 +138,10 @@ int nccl_allreduce_i32_sum(int32_t* buf, size_t count, hs_comm_s* c, cudaStream_
   return (int)a.all_reduce(buf, buf, count, ncclInt32, ncclSum, c->nc, s);
 }
 
+int nccl_allreduce_i64_sum(int64_t* buf, size_t count, hs_comm_s* c, cudaStream_t s) {
+  const NcclApi& a = nccl();
+  if (!a.ok) return -1;
+  return (int)a.all_reduce(buf, buf, count, ncclInt64, ncclSum, c->nc, s);
+}
+
 }  // namespace hs

@@ -17,6 +17,8 @@
 // st.release and read with ld.acquire at gpu scope; the epoch (bumped by the
 // last tile of every launch) makes stale descriptors from earlier launches
 // read as "not ready", so there is no reset pass and no memset between calls.
+#include <cstdlib>
+
 #include "hs_common.cuh"
 #include "hs_internal.h"
 
@@ -236,12 +238,18 @@ __global__ void __launch_bounds__(kCompactThreads) route_compact_kernel(const Co
 constexpr int kFastItems = 8;
 static_assert(kFastItems * kCompactThreads == kCompactTile, "one tile per CTA");
 
-__global__ void __launch_bounds__(kCompactThreads) route_compact_fast_kernel(const CompactArgs a,
-                                                                             int vec) {
+// T threads x 8 items per tile: 256 (2,048-item tiles, small batches) or 1,024
+// (8,192-item tiles: 4x fewer tiles, so the look-back that decides the
+// kernel's latency crosses 4x fewer descriptors; the split is staged in
+// dynamic shared memory, 16 B per item).
+template <int T>
+__global__ void __launch_bounds__(T) route_compact_fast_kernel(const CompactArgs a, int vec) {
   pdl_start();
-  constexpr int T = kCompactThreads, I = kFastItems, NW = T / 32, TILE = kCompactTile;
-  __shared__ long long s_id[TILE];     // accepted ids [0, A_t), deferred ids [A_t, tn)
-  __shared__ long long s_aux[TILE];    // accepted: pred << 32 | conf bits; deferred: position
+  constexpr int I = kFastItems, NW = T / 32, TILE = T * kFastItems;
+  static_assert(NW <= 32, "one warp scans the warp offsets");
+  extern __shared__ __align__(16) long long s_dyn[];
+  long long* s_id = s_dyn;             // accepted ids [0, A_t), deferred ids [A_t, tn)
+  long long* s_aux = s_dyn + TILE;     // accepted: pred << 32 | conf bits; deferred: position
   __shared__ int s_woff[NW];
   __shared__ long long s_excl;
   __shared__ int s_agg;
@@ -491,7 +499,18 @@ cudaError_t launch_route_compact(const CompactArgs& a, cudaStream_t s) {
   const bool fast = !a.sel_dest && !a.skip_dest && (!a.acc_pred || a.pred_len == 1);
   if (fast) {
     const int vec = aligned16(a.conf) && aligned16(a.ids) && (!a.acc_pred || aligned16(a.pred));
-    return launch_pdl(route_compact_fast_kernel, dim3(grid), dim3(kCompactThreads), 0, s, a, vec);
+    static const bool big_ok = [] {
+      return cudaFuncSetAttribute(route_compact_fast_kernel<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  1024 * kFastItems * 16) == cudaSuccess;
+    }();
+    static const bool off = getenv("HS_COMPACT_SMALL_TILES") && getenv("HS_COMPACT_SMALL_TILES")[0] == '1';
+    if (big_ok && !off && a.n >= 4 * 1024 * kFastItems) {   // >= 4 big tiles
+      const int64_t bt = (a.n + 1024 * kFastItems - 1) / (1024 * kFastItems);
+      return launch_pdl(route_compact_fast_kernel<1024>, dim3((unsigned)bt), dim3(1024),
+                        (size_t)1024 * kFastItems * 16, s, a, vec);
+    }
+    return launch_pdl(route_compact_fast_kernel<256>, dim3(grid), dim3(256), (size_t)256 * kFastItems * 16, s,
+                      a, vec);
   }
   return launch_pdl(route_compact_kernel, dim3(grid), dim3(kCompactThreads), 0, s, a);
 }

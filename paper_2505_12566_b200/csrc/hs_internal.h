@@ -147,6 +147,11 @@ struct CalibState {         // lives at the start of the calibration workspace
 size_t calib_hist_bytes(int q);
 size_t calib_ws_bytes(int K, int q);
 cudaError_t launch_calib_init(void* ws, int q, long long target, cudaStream_t s);
+cudaError_t launch_calib_refine_round(const float* conf, const uint8_t* correct, int K, int64_t N, int q,
+                                      int k, const int32_t* b_idx, void* ws, bool zero_hist, cudaStream_t s);
+cudaError_t launch_calib_replay(const float* conf, const uint8_t* correct, int K, int64_t N, int q,
+                                const int32_t* b_idx, int64_t* reach, int64_t* handled, int64_t* correct_total,
+                                cudaStream_t s);
 cudaError_t launch_calib_hist(const float* conf, const uint8_t* correct, int K, int64_t N, int q,
                               int round, const int32_t* b_idx, int32_t* hist, cudaStream_t s);
 cudaError_t launch_calib_fused(const float* conf, const uint8_t* correct, int K, int64_t N, int q,
@@ -266,6 +271,7 @@ int nccl_unique_id(void* out128);
 int nccl_comm_create(const void* id128, int rank, int world, int device, hs_comm_s** out);
 int nccl_comm_destroy(hs_comm_s* c);
 int nccl_allreduce_i32_sum(int32_t* buf, size_t count, hs_comm_s* c, cudaStream_t s);
+int nccl_allreduce_i64_sum(int64_t* buf, size_t count, hs_comm_s* c, cudaStream_t s);
 int nccl_world(const hs_comm_s* c);
 int nccl_rank(const hs_comm_s* c);
 int nccl_allgather_i64(const int64_t* mine, int64_t* all, int64_t count, hs_comm_s* c, cudaStream_t s);

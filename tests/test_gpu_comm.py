@@ -82,3 +82,33 @@ def test_forward_nccl_world1(hs):
     want = np.flatnonzero(~(c >= np.float32(0.6))) + 100
     assert n == len(want) and np.array_equal(rid.cpu().numpy(), want)
     assert np.array_equal(rpay.cpu().numpy().reshape(n, 32), pay.cpu().numpy()[want - 100])
+
+
+@pytest.mark.parametrize("K,N,q,passes", [(3, 4000, 6, 2), (5, 20000, 12, 1), (4, 999, 3, 3)])
+def test_calibrate_comm_refinement_world1(hs, K, N, q, passes):
+    """hs_calibrate_thresholds_comm_ex with refinement passes (the histogram and
+    A_k all-reduced per pass and stage, the replay counts all-reduced) equals
+    the oracle's refinement at world size 1 -- with the communicator and
+    without -- and the single-GPU call."""
+    dev = torch.device("cuda:0")
+    rng = np.random.default_rng(K * 77 + N)
+    d = rng.random(N)
+    ok = np.stack([(d + 0.3 * rng.normal(size=N) < 0.5 + 0.1 * k) for k in range(K)]).astype(np.uint8)
+    conf = np.clip(np.where(ok[:K - 1] == 1, rng.beta(5, 2, (K - 1, N)), rng.beta(2, 3, (K - 1, N))),
+                   0, 1).astype(np.float32)
+    c = torch.from_numpy(conf).to(dev)
+    o = torch.from_numpy(ok).to(dev)
+    comm = hs.comm_create(hs.comm_unique_id(), 0, 1, 0)
+    try:
+        a = hs.calibrate_thresholds_comm(c, o, comm, log2_bins=q, refine_passes=passes)
+        b = hs.calibrate_thresholds_comm(c, o, None, log2_bins=q, refine_passes=passes)
+        r = hs.calibrate_thresholds(c, o, log2_bins=q, refine_passes=passes)
+        torch.cuda.synchronize()
+    finally:
+        hs.comm_destroy(comm)
+    ref = oracle.calibrate(conf.astype(np.float64), ok, q, refine_passes=passes)
+    for out in (a, b, r):
+        assert out["b"].cpu().numpy().tolist() == ref["b"].tolist()
+        assert out["reach"].cpu().numpy().tolist() == ref["reach"].tolist()
+        assert out["handled"].cpu().numpy().tolist() == ref["handled"].tolist()
+        assert int(out["correct_total"].item()) == ref["correct_total"]
