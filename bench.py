@@ -39,6 +39,10 @@ CONFIG_TEXT = {
            "3 x 224 x 224 u8 image (150,528 B payload) that is gathered / forwarded with every deferral",
     "c3k": "c3 with the Top-K (K = 10) restricted token confidence of P:420-424 (NEXT-2), MIN over 64 tokens",
     "c3m": "c3 with the MEAN of the 64 token confidences as the sequence confidence (north_star; the paper's is MIN, P:423)",
+    "c2skip": "NEXT-1: the C2 cascade (262,144 requests x 1,000 bf16, 5 ViT models, calibrated on 50,000) with "
+              "skip connections -- a deferred request jumps to model k+1+j by the band of [0, t_k) its "
+              "confidence falls in (uniform bands, P:497-541); logits indexed by request id; the plain "
+              "cascade on the same logits is timed in the same run",
     "c2g": "NEXT-4: threshold performance graph of the 5 C2 ViT stage models: the exhaustive q = 4 grid (18^4 = 104,976 threshold vectors) replayed on the 50,000-sample validation set per GPU, Pareto frontier, AP and EO picks",
     "c2t": "NEXT-3: temperature fitting (Eq. 1, P:384-389) of the 5 C2 ViT stage models on the 50,000-sample validation set per GPU, 1,000 classes bf16, T in [e^-4, e^4]",
 }
@@ -406,6 +410,7 @@ def run_ours(args, world, rank, local):
             sev[2 * K].record()
 
     stream = torch.cuda.Stream(device=dev)
+    stream.wait_stream(torch.cuda.current_stream())   # after the set-up queued so far
     torch.cuda.synchronize()
     with torch.cuda.stream(stream):
         for _ in range(max(args.warmup, 3)):
@@ -714,6 +719,88 @@ def run_e2e(args, fam, router, route, val, labels, payload, stream, world, ids0=
 
 
 # ---------------------------------------------------------------------------
+# NEXT-1: skip connections (--config c2skip)
+# ---------------------------------------------------------------------------
+def run_skip(args, world, rank, local):
+    """Step = calibration + routing through the SKIP cascade (hs_skip_select /
+    hs_confidence / hs_skip_route per model; uniform bands); the plain
+    cascade (by-id layout) on the same logits and thresholds is timed in the
+    same run for the comparison the paper draws (tail latency).  N > 1:
+    independent replicas on shard-local requests."""
+    import torch
+    import paper_2505_12566_b200 as hs
+    dev = torch.device("cuda", local)
+    fam = family("c2")
+    route, val, labels, _ = build_inputs(fam, rank, dev)
+    router = make_router(fam, dev, None)
+    stages = [hs.StageSpec(fam.C, fam.temps[k]) for k in range(fam.K)]
+    sc = hs.SkipCascade(fam.n, stages, dev, mode=hs.SKIP_UNIFORM)
+
+    def step_skip():
+        router.calibrate(val, labels)
+        sc.route(route, router.cal["t"])
+
+    def step_plain():
+        router.calibrate(val, labels)
+        router.route(route, by_id=True, overlap_first=not args.no_overlap)
+
+    stream = torch.cuda.Stream(device=dev)
+    stream.wait_stream(torch.cuda.current_stream())   # after the set-up queued so far
+    graphs = {}
+    for name, fn in (("skip", step_skip), ("plain", step_plain)):
+        with torch.cuda.stream(stream):
+            for _ in range(max(args.warmup, 3)):
+                fn()
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        l0 = hs.launch_count()
+        with torch.cuda.graph(g, stream=stream):
+            fn()
+        graphs[name] = (g, hs.launch_count() - l0)
+        g.replay()
+        torch.cuda.synchronize()
+    times = {}
+    barrier(world)
+    with ClockSampler(local) as clk:
+        for name in ("skip", "plain", "skip"):
+            g = graphs[name][0]
+            t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            with torch.cuda.stream(stream):
+                t0.record(stream)
+                for _ in range(args.steps):
+                    g.replay()
+                t1.record(stream)
+            torch.cuda.synchronize()
+            times[name] = t0.elapsed_time(t1) / args.steps      # skip: the second pass
+    ms = max_over_ranks(times["skip"], world)
+    ms_plain = max_over_ranks(times["plain"], world)
+    sel = sc.sel_counts.cpu().tolist()
+    visits_skip = [fam.n] + [int(c[1]) for c in sel[1:]]
+    counts = router.cascade.counts.cpu().tolist()
+    visits_plain = [fam.n] + [int(c[1]) for c in counts[:-1]]
+    answered_skip = [int(c[0]) for c in sc.counts.cpu().tolist()]
+    line = {
+        "metric": METRIC, "value": fam.n * world / (ms / 1e3), "unit": "requests/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": "c2skip_vit5_uniform_bands", "description": CONFIG_TEXT["c2skip"],
+                   "requests_per_gpu": fam.n, "validation_per_gpu": fam.n_val, "K": fam.K,
+                   "classes": fam.C, "logits_dtype": fam.dtype, "logits_layout": "by_id",
+                   "parallelism": f"independent replicas x{world}",
+                   "l2": "inputs larger than L2", "cuda_graph": True},
+        "thresholds": router.cal["t"].cpu().tolist(),
+        "model_visits_skip": visits_skip, "answered_per_model_skip": answered_skip,
+        "model_visits_plain": visits_plain,
+        "plain_cascade_ms_per_step": ms_plain,
+        "skip_vs_plain_logits_bytes": sum(visits_skip) / max(sum(visits_plain), 1),
+        "gpu_launches": graphs["skip"][1] * args.steps, "gpu_launches_per_step": graphs["skip"][1],
+        "clocks": clk.summary(), "e2e": None,
+    }
+    return line
+
+
+# ---------------------------------------------------------------------------
 # NEXT-3: temperature fitting on the validation set (--config c2t)
 # ---------------------------------------------------------------------------
 def run_temperature(args, world, rank, local):
@@ -737,6 +824,7 @@ def run_temperature(args, world, rank, local):
         hs.fit_temperature(val, labels, out=out, ws=ws, status=status)
 
     stream = torch.cuda.Stream(device=dev)
+    stream.wait_stream(torch.cuda.current_stream())   # after the set-up queued so far
     with torch.cuda.stream(stream):
         for _ in range(max(args.warmup, 3)):
             step()
@@ -866,6 +954,7 @@ def run_graph(args, world, rank, local):
         gout.update(g)
 
     stream = torch.cuda.Stream(device=dev)
+    stream.wait_stream(torch.cuda.current_stream())   # after the set-up queued so far
     with torch.cuda.stream(stream):
         for _ in range(max(args.warmup, 3)):
             step()
@@ -1350,6 +1439,11 @@ def main():
         line, fam, conf, ok = run_graph(args, world, rank, local)
         if rank == 0 and world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline_graph(fam, args.cpu_seconds, conf, ok)
+        if rank == 0:
+            emit(json.dumps(line))
+        return
+    if args.config == "c2skip":
+        line = run_skip(args, world, rank, local)
         if rank == 0:
             emit(json.dumps(line))
         return

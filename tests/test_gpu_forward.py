@@ -63,6 +63,8 @@ def test_peer_forward_virtual_ranks(hs, world, dest, P, fused):
         cap = n      # placed blocks can exceed a rank's shard
     grp = hsd.PeerGroup.local_group(world, cap, P, 12, K=8, device=dev)
     streams = [torch.cuda.Stream(device=dev) for _ in range(world)]
+    for st_ in streams:
+        st_.wait_stream(torch.cuda.current_stream())   # after the set-up queued so far
     for it, t in enumerate((0.6, 0.25, 0.97, 0.0, 0.5, 1.0)):
         outs = []
         for g in range(world):
@@ -151,6 +153,8 @@ def test_peer_calibration_equals_oracle_on_the_whole_set(hs, world, n, q, K):
     grp = hsd.PeerGroup.local_group(world, 16, 0, q, device=dev)
     bounds = [g * n // world for g in range(world + 1)]
     streams = [torch.cuda.Stream(device=dev) for _ in range(world)]
+    for st_ in streams:
+        st_.wait_stream(torch.cuda.current_stream())   # after the set-up queued so far
     outs = []
     for rep in range(3):                 # regions reused: round counters advance
         outs = []
@@ -200,6 +204,8 @@ def test_peer_cascade_step_equals_oracle_cascade(hs, world):
         __import__("paper_2505_12566_b200").StageSpec(C, fam.temps[k]) for k in range(K)], dev)
         for _ in range(world)]
     streams = [torch.cuda.Stream(device=dev) for _ in range(world)]
+    for st_ in streams:
+        st_.wait_stream(torch.cuda.current_stream())   # after the set-up queued so far
     thr = torch.tensor(t, dtype=torch.float32, device=dev)
     for g in range(world):
         ids = torch.arange(bounds[g], bounds[g + 1], dtype=torch.int64, device=dev)

@@ -34,6 +34,7 @@ def test_bench_step_full_size(hs, config):
     route, val, labels, payload = bench.build_inputs(fam, 0, dev)
     router = bench.make_router(fam, dev, None)
     stream = torch.cuda.Stream(device=dev)
+    stream.wait_stream(torch.cuda.current_stream())   # after the set-up queued so far
 
     def step():
         router.calibrate(val, labels)
@@ -112,6 +113,7 @@ def test_bench_dense_step_full_size_every_request(hs, config, split):
     router = bench.make_router(fam, dev, None)
     route, _ = bench.dense_stage_logits(fam, router, route, val, labels, payload, 0, dev)
     stream = torch.cuda.Stream(device=dev)
+    stream.wait_stream(torch.cuda.current_stream())   # after the set-up queued so far
 
     def step():
         router.calibrate(val, labels)

@@ -73,6 +73,7 @@ def _worker(rank, world, port, n, n_val, graph, q):
                 workload.gpu_logits(x, fam, k, ids=peer.recv_ids((k - 1) % 2)[:nk].clone(), n=nk)
             logits[k] = x
         s = torch.cuda.Stream(device=dev)
+        s.wait_stream(torch.cuda.current_stream())   # after the set-up queued so far
 
         def step():
             router.calibrate(val, lab)

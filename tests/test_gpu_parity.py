@@ -422,6 +422,7 @@ def test_router_overlap_first_equals_serial(hs, graph):
     def run(overlap):
         r = Router(stages, n, n_val, dev(), log2_bins=fam.log2_bins)
         s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())   # after the set-up queued so far
         with torch.cuda.stream(s):
             def step():
                 r.calibrate(val, lab)
@@ -953,6 +954,7 @@ def test_split_compaction_equals_step(hs, graph):
     def run(split):
         r = bench.make_router(fam, dev(), None)
         s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())   # after the set-up queued so far
         with torch.cuda.stream(s):
             def step():
                 r.calibrate(val, labels)

@@ -59,6 +59,7 @@ def main():
         return run
 
     s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())   # after the set-up queued so far
     res = {}
     prev_t = 0.0
     names = ["val K1", "+ calibration"] + [f"+ stage {k + 1}" for k in range(K)]

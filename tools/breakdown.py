@@ -79,6 +79,7 @@ def main():
             mark(f"route_compact[{k}]")
 
     stream = torch.cuda.Stream()
+    stream.wait_stream(torch.cuda.current_stream())   # after the set-up queued so far
     with torch.cuda.stream(stream):
         for _ in range(3):
             step()

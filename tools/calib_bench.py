@@ -29,6 +29,7 @@ def main():
                     out = hs._calib_out(K, dev, None)
                     ws = hs.calibrate_workspace(K, q, dev)
                     s = torch.cuda.Stream()
+                    s.wait_stream(torch.cuda.current_stream())   # after the set-up queued so far
                     with torch.cuda.stream(s):
                         for _ in range(3):
                             hs.calibrate_thresholds(conf, ok, log2_bins=q, out=out, ws=ws)
@@ -54,6 +55,7 @@ def main():
     o = hs.route_compact(c, 0.5, ws=ws)
     gr = torch.cuda.CUDAGraph()
     s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())   # after the set-up queued so far
     with torch.cuda.graph(gr, stream=s):
         for _ in range(20):
             hs.route_compact(c, 0.5, ws=ws, out=o)

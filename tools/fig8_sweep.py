@@ -48,6 +48,7 @@ def main():
                 thr = torch.tensor([float("inf")] * (K - 1) + [0.0], dtype=torch.float32, device=dev)
                 logits = [x] * K
                 s = torch.cuda.Stream(device=dev)
+                s.wait_stream(torch.cuda.current_stream())   # after the set-up queued so far
                 with torch.cuda.stream(s):
                     for _ in range(3):
                         casc.route(logits, thr)
