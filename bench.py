@@ -88,6 +88,9 @@ def parse():
                          "local: every rank serves every stage of its own shard (replicas, no "
                          "exchange).  nccl: the balanced re-spread with torch.distributed NCCL "
                          "(count all-gather + all-to-all, host split sizes, eager) -- the baseline")
+    ap.add_argument("--requests", type=int, default=0,
+                    help="override the requests per GPU of the config (debugging / scaled runs; the "
+                         "workload name then carries the count)")
     ap.add_argument("--plumbing-check", action="store_true",
                     help="CPU self-test of the multi-rank launcher (no GPU): every rank joins a gloo "
                          "group, exchanges a handle with all_gather_object and reduces with the "
@@ -367,6 +370,9 @@ def run_ours(args, world, rank, local):
 
     dev = torch.device("cuda", local)
     fam = family(args.config, world)
+    if args.requests:
+        import dataclasses
+        fam = dataclasses.replace(fam, n=args.requests, name=f"{fam.name}_n{args.requests}")
     group = dist.group.WORLD if dist.is_initialized() else None
     route, val, labels, payload = build_inputs(fam, rank, dev)
     peer = None
@@ -672,6 +678,10 @@ def run_e2e(args, fam, router, route, val, labels, payload, stream, world, ids0=
     its inputs host->device and reads the per-request results back."""
     import torch
     steps = args.e2e_steps
+    in_bytes = sum(x.numel() * x.element_size() for x in list(route) + list(val) if x is not None)
+    if in_bytes > (8 << 30):   # pinned host copies of > 8 GB per rank: not run (c5s at few GPUs)
+        return {"skipped": f"{in_bytes / 1e9:.1f} GB of inputs per step per rank exceed the 8 GB "
+                           "pinned-host budget of the e2e leg"}
     host_route = [x.cpu().pin_memory() for x in route]
     host_val = [x.cpu().pin_memory() for x in val]
     host_lab = labels.cpu().pin_memory()

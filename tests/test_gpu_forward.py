@@ -177,8 +177,8 @@ def test_peer_calibration_equals_oracle_on_the_whole_set(hs, world, n, q, K):
     grp[0].close()
 
 
-@pytest.mark.parametrize("world", [1, 2, 4])
-def test_peer_cascade_step_equals_oracle_cascade(hs, world):
+@pytest.mark.parametrize("world,placed", [(1, False), (2, False), (4, False), (2, True), (3, True)])
+def test_peer_cascade_step_equals_oracle_cascade(hs, world, placed):
     """The comm-aware cascade step over W virtual ranks (balanced placement):
     the union of the accepted lists of stage k over all ranks equals the
     oracle's stage-k list of the whole batch (a request's stage does not
@@ -199,6 +199,11 @@ def test_peer_cascade_step_equals_oracle_cascade(hs, world):
         near |= np.abs(conf[k] - t[k]) <= 1e-5 * t[k]
     bounds = [g * n // world for g in range(world + 1)]
     cap = max(bounds[g + 1] - bounds[g] for g in range(world))
+    next_ranks = None
+    if placed:       # replicas by the zero-queuing rule: a rank may receive every deferral
+        ranks = hsd.placed_ranks(world, hsd.replica_counts(world, [1, .5, .3, .2, .2], [1, 2, 4, 8, 16]))
+        next_ranks = ranks[1:]
+        cap = world * cap
     grp = hsd.PeerGroup.local_group(world, cap, 0, 12, K=K, device=dev)
     casc = [__import__("paper_2505_12566_b200").Cascade(cap, [
         __import__("paper_2505_12566_b200").StageSpec(C, fam.temps[k]) for k in range(K)], dev)
@@ -210,7 +215,7 @@ def test_peer_cascade_step_equals_oracle_cascade(hs, world):
     for g in range(world):
         ids = torch.arange(bounds[g], bounds[g + 1], dtype=torch.int64, device=dev)
         casc[g].route(logits, thr, n=bounds[g + 1] - bounds[g], ids=ids, by_id=True, peer=grp[g],
-                      stream=streams[g])
+                      next_ranks=next_ranks, stream=streams[g])
     torch.cuda.synchronize()
     for k in range(K):
         got = np.sort(np.concatenate([casc[g].results()[k]["ids"].numpy() for g in range(world)]))
