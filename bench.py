@@ -306,7 +306,7 @@ def dense_stage_logits(fam, router, route, val, labels, payload, rank, dev, ids0
     peer = router.peer
     for k in range(1, fam.K):
         # stages 0..k-1 on the batches known so far (every rank in lockstep)
-        router.route(out, ids=ids0, payload=payload, by_id=False, upto=k - 1, next_ranks=next_ranks)
+        router.route(out, n=fam.n, ids=ids0, payload=payload, by_id=False, upto=k - 1, next_ranks=next_ranks)
         torch.cuda.synchronize()
         if peer is not None:
             nk = int(peer.recv_count[k - 1].item())
@@ -321,7 +321,7 @@ def dense_stage_logits(fam, router, route, val, labels, payload, rank, dev, ids0
             workload.gpu_logits(x, fam, k, ids=ids, n=nk)
         out[k] = x
         route[k] = None                    # the full-population tensor is not needed
-    router.route(out, ids=ids0, payload=payload, by_id=False, next_ranks=next_ranks)
+    router.route(out, n=fam.n, ids=ids0, payload=payload, by_id=False, next_ranks=next_ranks)
     torch.cuda.synchronize()
     torch.cuda.empty_cache()
     return out, dense_signature(router, fam)
@@ -409,7 +409,7 @@ def run_ours(args, world, rank, local):
         # K1 on the validation shard is the timed launch (events around it); the
         # routing stage-1 K1 then runs next to the latency-bound calibration
         router.calibrate(val, labels, time_val=ev)
-        router.route(route, ids=ids0, payload=payload, overlap_first=not args.no_overlap,
+        router.route(route, n=fam.n, ids=ids0, payload=payload, overlap_first=not args.no_overlap,
                      by_id=not dense, events=events, split=dense and peer is None and args.split,
                      next_ranks=next_ranks)
         if events is not None:
@@ -703,7 +703,7 @@ def run_e2e(args, fam, router, route, val, labels, payload, stream, world, ids0=
         if payload is not None:
             payload.copy_(host_pay, non_blocking=True)
         router.calibrate(val, labels)
-        router.route(route, ids=ids0, payload=payload, by_id=args.layout != "dense")
+        router.route(route, n=fam.n, ids=ids0, payload=payload, by_id=args.layout != "dense")
         cnt_host.copy_(router.cascade.counts, non_blocking=True)
         # accepted ids of every stage (the answers' request ids)
         for o, h in zip(outs, res_host):

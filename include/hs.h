@@ -217,7 +217,8 @@ hs_status_t hs_skip_route(const float* conf, int64_t n, const int64_t* d_n, floa
  * argmaxes); deferred items become the next stage's batch: next_ids,
  * next_payload (optional).  d_counts = {#accepted, #deferred}.  d_threshold as
  * for hs_route_compact.
- * Workspace: hs_cascade_step_workspace(n, seq_len) bytes, zero-filled before
+ * Workspace: hs_cascade_step_workspace(n, seq_len) bytes (non-decreasing in n: a
+ * workspace sized for a capacity serves every smaller batch), zero-filled before
  * first use (then reused as is).  n < 2^30.  Same errors as the two calls above. */
 size_t hs_cascade_step_workspace(int64_t n, int32_t seq_len);
 hs_status_t hs_cascade_step(int32_t stage, int32_t n_stages, const void* logits, hs_dtype_t dtype,

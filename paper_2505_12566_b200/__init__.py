@@ -494,6 +494,8 @@ def cascade_step(stage: int, n_stages: int, logits: torch.Tensor, threshold, *, 
     next to the previous libhs kernel on the stream; the caller guarantees that
     kernel does not touch this step's inputs or workspace."""
     _check_cuda(logits, row_index, d_n, ids, payload, status)
+    if row_index is None and d_n is None and logits.shape[0] < n * seq_len:
+        raise ValueError(f"cascade_step: {n} items x {seq_len} tokens but logits has {logits.shape[0]} rows")
     C = int(n_classes or logits.shape[1])
     dev = logits.device
     out = dict(out or {})

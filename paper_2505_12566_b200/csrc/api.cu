@@ -910,7 +910,11 @@ static size_t step_layout(int64_t n, int32_t L, size_t* o_conf, size_t* o_am, si
   *o_cws = off;
   off = align_up(off + conf_ws(n, L), 256);
   if (o_split) *o_split = off;         // K1e split-row partials (small batches), zero-filled once
-  off = align_up(off + hs::split_ws_bytes(n * (int64_t)L), 256);
+  // the split-row region is reserved for min(n*L, kSplitMaxRows) rows, so the
+  // workspace size never shrinks as n grows (a workspace sized for a capacity
+  // serves every smaller batch, including those that take the split path)
+  const int64_t srows = n * (int64_t)L < hs::kSplitMaxRows ? n * (int64_t)L : hs::kSplitMaxRows;
+  off = align_up(off + hs::split_ws_bytes(srows), 256);
   return off;
 }
 
