@@ -46,7 +46,6 @@ class Router:
         self.vconf_last = self.vconf_all[K - 1]
         self.vok = torch.empty(K, self.n_val, dtype=torch.uint8, device=dev)
         L = max(s.seq_len for s in stages)
-        self.vargmax = torch.empty(K * self.n_val * L, dtype=torch.int32, device=dev)
         self.conf_ws = torch.empty(max(1, K * self.n_val * L * 5 + 1024), dtype=torch.uint8, device=dev)
         # one launch for every stage when the stages share a prediction shape
         s0 = stages[0]
@@ -86,17 +85,16 @@ class Router:
             confidence_batched(val_logits, [t.temperature for t in self.stages], n=self.n_val,
                                seq_len=s.seq_len, n_classes=s.n_classes, kind=s.kind,
                                reduce=s.reduce, labels=labels,
-                               out={"conf": self.vconf_all.view(-1), "argmax": self.vargmax,
-                                    "correct": self.vok.view(-1)},
+                               out={"conf": self.vconf_all.view(-1), "correct": self.vok.view(-1)},
+                               want_argmax=False,
                                ws=self.conf_ws, status=self.status, stream=stream)
         else:
             for k, s in enumerate(self.stages):
-                out = {"conf": self.vconf_all[k],
-                       "argmax": self.vargmax[: self.n_val * s.seq_len], "correct": self.vok[k]}
+                out = {"conf": self.vconf_all[k], "correct": self.vok[k]}
                 confidence(val_logits[k], n=self.n_val, seq_len=s.seq_len, n_classes=s.n_classes,
                            temperature=s.temperature, kind=s.kind, reduce=s.reduce, labels=labels,
                            out=out, ws=self.conf_ws, status=self.status, top_k=s.top_k,
-                           stream=stream)
+                           want_argmax=False, stream=stream)
         if time_val is not None:
             time_val[1].record()
         if self.peer is not None:

@@ -208,13 +208,13 @@ def test_peer_cascade_step_equals_oracle_cascade(hs, world, placed):
     casc = [__import__("paper_2505_12566_b200").Cascade(cap, [
         __import__("paper_2505_12566_b200").StageSpec(C, fam.temps[k]) for k in range(K)], dev)
         for _ in range(world)]
+    thr = torch.tensor(t, dtype=torch.float32, device=dev)
+    ids = [torch.arange(bounds[g], bounds[g + 1], dtype=torch.int64, device=dev) for g in range(world)]
     streams = [torch.cuda.Stream(device=dev) for _ in range(world)]
     for st_ in streams:
         st_.wait_stream(torch.cuda.current_stream())   # after the set-up queued so far
-    thr = torch.tensor(t, dtype=torch.float32, device=dev)
     for g in range(world):
-        ids = torch.arange(bounds[g], bounds[g + 1], dtype=torch.int64, device=dev)
-        casc[g].route(logits, thr, n=bounds[g + 1] - bounds[g], ids=ids, by_id=True, peer=grp[g],
+        casc[g].route(logits, thr, n=bounds[g + 1] - bounds[g], ids=ids[g], by_id=True, peer=grp[g],
                       next_ranks=next_ranks, stream=streams[g])
     torch.cuda.synchronize()
     for k in range(K):

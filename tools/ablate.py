@@ -42,7 +42,7 @@ def main():
                 hs.confidence_batched(val, [t.temperature for t in router.stages], n=router.n_val,
                                       seq_len=s0.seq_len, n_classes=s0.n_classes, kind=s0.kind,
                                       reduce=s0.reduce, labels=labels,
-                                      out={"conf": router.vconf_all.view(-1), "argmax": router.vargmax,
+                                      want_argmax=False, out={"conf": router.vconf_all.view(-1),
                                            "correct": router.vok.view(-1)}, ws=router.conf_ws)
             thr = router.cal["t"]
             for k in range(0, max(0, upto - 1)):

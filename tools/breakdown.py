@@ -53,7 +53,7 @@ def main():
         hs.confidence_batched(val, [t.temperature for t in router.stages], n=router.n_val,
                               seq_len=s0.seq_len, n_classes=s0.n_classes, kind=s0.kind,
                               reduce=s0.reduce, labels=labels,
-                              out={"conf": router.vconf_all.view(-1), "argmax": router.vargmax,
+                              want_argmax=False, out={"conf": router.vconf_all.view(-1),
                                    "correct": router.vok.view(-1)}, ws=router.conf_ws)
         mark("val_conf(all stages, one launch)")
         hs.calibrate_thresholds(router.vconf, router.vok, log2_bins=router.q, out=router.cal,
