@@ -277,9 +277,9 @@ def build_inputs(fam, rank: int, dev):
     return route, val, labels, payload
 
 
-def committed_traffic(config: str, name: str = "r01_k1_traffic.json"):
+def committed_traffic(config: str, name: str = "r02_k1_traffic.json"):
     """DRAM bytes per launch of the roofline kernel from the committed ncu
-    capture (profiles/r01_k1_traffic.json, written by tools/ncu_summary.py
+    capture (profiles/r02_k1_traffic.json, written by tools/ncu_summary.py
     traffic), when it was taken on this config; else None."""
     path = os.path.join(ROOT, "profiles", name)
     try:

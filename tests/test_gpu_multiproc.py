@@ -33,7 +33,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, n, n_val, graph, q):
+def _worker(rank, world, port, n, n_val, graph, q, placed=False):
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -55,9 +55,13 @@ def _worker(rank, world, port, n, n_val, graph, q):
             val.append(v)
         lab = torch.empty(n_val, dtype=torch.int32, device=dev)
         workload.gpu_labels(lab, fam, id_base=synth.VAL_ID_BASE + rank * n_val, n=n_val)
-        peer = hsd.PeerGroup(n, 0, fam.log2_bins, K=K, device=dev)
+        cap = n * (world if placed else 1)
+        peer = hsd.PeerGroup(cap, 0, fam.log2_bins, K=K, device=dev)
         stages = [hs.StageSpec(fam.C, fam.temps[k]) for k in range(K)]
-        router = Router(stages, n, n_val, dev, log2_bins=fam.log2_bins, peer=peer)
+        router = Router(stages, cap, n_val, dev, log2_bins=fam.log2_bins, peer=peer)
+        if placed:      # model m's replicas on placed ranks: every deferral to one rank
+            router.next_ranks = hsd.placed_ranks(world, hsd.replica_counts(
+                world, [1, .5, .3, .2, .2], [1, 2, 4, 8, 16]))[1:]
         ids0 = torch.arange(rank * n, (rank + 1) * n, dtype=torch.int64, device=dev)
         x0 = torch.empty(n, fam.C, dtype=torch.bfloat16, device=dev)
         workload.gpu_logits(x0, fam, 0, id_base=rank * n, n=n)
@@ -65,7 +69,7 @@ def _worker(rank, world, port, n, n_val, graph, q):
         router.calibrate(val, lab)
         logits = [x0] + [None] * (K - 1)
         for k in range(1, K):
-            router.route(logits, ids=ids0, by_id=False, upto=k - 1)
+            router.route(logits, n=n, ids=ids0, by_id=False, upto=k - 1)
             torch.cuda.synchronize()
             nk = int(peer.recv_count[k - 1].item())
             x = torch.empty(max(nk, 1), fam.C, dtype=torch.bfloat16, device=dev)
@@ -77,7 +81,7 @@ def _worker(rank, world, port, n, n_val, graph, q):
 
         def step():
             router.calibrate(val, lab)
-            router.route(logits, ids=ids0, by_id=False, overlap_first=True)
+            router.route(logits, n=n, ids=ids0, by_id=False, overlap_first=True)
 
         with torch.cuda.stream(s):
             step()
@@ -102,8 +106,9 @@ def _worker(rank, world, port, n, n_val, graph, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,graph", [(2, False), (2, True), (3, True)])
-def test_peer_group_across_processes_equals_oracle(libhs, world, graph):
+@pytest.mark.parametrize("world,graph,placed", [(2, False, False), (2, True, False), (3, True, False),
+                                                (3, True, True)])
+def test_peer_group_across_processes_equals_oracle(libhs, world, graph, placed):
     import torch.multiprocessing as mp
     import oracle
     from paper_2505_12566_b200 import dist as hsd
@@ -112,7 +117,8 @@ def test_peer_group_across_processes_equals_oracle(libhs, world, graph):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, n, n_val, graph, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n, n_val, graph, q, placed))
+             for r in range(world)]
     for p in procs:
         p.start()
     outs = [q.get(timeout=600) for _ in range(world)]
@@ -147,7 +153,7 @@ def test_peer_group_across_processes_equals_oracle(libhs, world, graph):
         want = np.flatnonzero(stage_of == k)
         assert np.array_equal(got[~near[got]], want[~near[want]]), k
     # balanced placement: rank g received block g of the global deferred list
-    for k in range(K - 1):
+    for k in range(K - 1 if not placed else 0):
         D = int((stage_of > k).sum())
         lo = hsd.block_bounds(D, world)
         if not near.any():

@@ -31,7 +31,7 @@ def main():
             xs.append(xk)
         lab = torch.randint(0, fam.C, (args.rows * fam.L,), dtype=torch.int32, device="cuda")
         for _ in range(args.reps):
-            hs.confidence_batched(xs, fam.temps[:args.batched], n=args.rows, seq_len=fam.L,
+            hs.confidence_batched(xs, fam.temps[:args.batched], n=args.rows, seq_len=fam.L, want_argmax=False,
                                   kind=fam.kind, reduce=fam.reduce, labels=lab)
         torch.cuda.synchronize()
         print("ok")
