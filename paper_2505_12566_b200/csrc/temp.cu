@@ -474,10 +474,21 @@ __global__ void __launch_bounds__(kTfThreads, 1) temp_fit_kernel(const TfArgs a)
         float w1 = group_sum<float, G>(f2lo(w12) + f2hi(w12));
         float w2 = group_sum<float, G>(f2lo(w22) + f2hi(w22));
         if (active && gl == 0) {
+          // per-row moments in fp32 (one MUFU.RCP; s in [1, C]), row sums in fp64:
+          // g_i and h_i only steer the Newton iteration, whose stop (2^-21 in beta)
+          // is far above their fp32 rounding; the fp64 divisions cost ~10 % of a
+          // sweep's instructions on the warp's critical path
+#ifdef HS_AB_TF_FP64_ROW
           const double ds = (double)s, mean = (double)w1 / ds;
           acc_nll += (double)logf(s) - beta * (double)rs.y;
           acc_g += mean - (double)rs.y;
           acc_h += fmax((double)w2 / ds - mean * mean, 0.0);
+#else
+          const float inv = __fdividef(1.0f, s), mean = w1 * inv;
+          acc_nll += (double)logf(s) - beta * (double)rs.y;
+          acc_g += (double)(mean - rs.y);
+          acc_h += (double)fmaxf(fmaf(w2, inv, -mean * mean), 0.0f);
+#endif
         }
       }
     }

@@ -7,6 +7,7 @@ sys.path.insert(0, ROOT)
 from paper_2505_12566_b200 import _build  # noqa: E402
 
 VARIANTS = {
+    "tffp64": ["HS_AB_TF_FP64_ROW"],                  # temperature fit: per-row moments in fp64 (round 1)
     "noticket": ["HS_AB_NO_TICKET"],                  # K3 tiles by blockIdx (round 1)
     "linargmax": ["HS_AB_LINEAR_ARGMAX"],             # K1a argmax: one compare per vector (round 1)
     "ctrace": ["HS_CALIB_TRACE"],        # globaltimer trace of the calibration kernels
