@@ -110,6 +110,11 @@ __device__ __forceinline__ int64_t fetch_index(const ConfArgs& a, int64_t row) {
   const int64_t local = batch_local(a, row, &b);
   return a.L == 1 ? a.row_index[local] : a.row_index[local / a.L];
 }
+template <bool RIDX>
+__device__ __forceinline__ int64_t fetch_index_t(const ConfArgs& a, int64_t row) {
+  if constexpr (!RIDX) return 0;
+  else return fetch_index(a, row);
+}
 __device__ __forceinline__ RowSrc locate_with(const ConfArgs& a, int64_t row, int64_t fetched) {
   int b;
   const int64_t local = batch_local(a, row, &b);
@@ -132,6 +137,7 @@ struct BatchCur {
 __device__ __forceinline__ BatchCur cur_init(const ConfArgs& a) {
   return BatchCur{0u, a.nbatch > 1 ? 0u : 0xFFFFFFFFu, (const char*)a.logits, a.c};
 }
+template <bool RIDX = true>
 __device__ __forceinline__ RowSrc locate_cur(const ConfArgs& a, BatchCur& k, int64_t row,
                                              int64_t fetched) {
   if ((uint32_t)row < k.start || (uint32_t)row >= k.end) {
@@ -144,7 +150,7 @@ __device__ __forceinline__ RowSrc locate_cur(const ConfArgs& a, BatchCur& k, int
   }
   const int64_t local = row - (int64_t)k.start;
   RowSrc r{k.base, k.c, local};
-  if (a.row_index) r.src = a.L == 1 ? fetched : fetched * a.L + local % a.L;
+  if (RIDX && a.row_index) r.src = a.L == 1 ? fetched : fetched * a.L + local % a.L;
   return r;
 }
 __device__ __forceinline__ RowSrc locate(const ConfArgs& a, int64_t row) {
@@ -816,7 +822,9 @@ constexpr int kAsyncThreads = 256;
 template <int NV, int G>
 constexpr int async_smem_bytes() { return (kAsyncThreads / 32) * 2 * (32 / G) * G * NV * 16; }
 
-template <bool BF16, bool ENTROPY, int NV, int G, bool FULL, bool DYN>
+// RIDX: the launch reads rows through row_index (gathered batch); false for
+// dense batches -- the row-index lookups and checks compile away.
+template <bool BF16, bool ENTROPY, int NV, int G, bool FULL, bool DYN, bool RIDX>
 __global__ void __launch_bounds__(kAsyncThreads, 3) conf_async_kernel(const ConfArgs a) {
   if (a.late_wait) pdl_trigger(); else pdl_start();
   extern __shared__ __align__(16) unsigned char smem[];
@@ -848,7 +856,7 @@ __global__ void __launch_bounds__(kAsyncThreads, 3) conf_async_kernel(const Conf
     return cnext++;
   };
   const int64_t g0 = dyn ? next_group(0) : ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t fA = fetch_index(a, g0 * RPW + grp < cap ? g0 * RPW + grp : 0);
+  const int64_t fA = fetch_index_t<RIDX>(a, g0 * RPW + grp < cap ? g0 * RPW + grp : 0);
   const int64_t rows = live_rows(a);
   if (g0 * RPW < rows) {
     // lane gl's vector k of stage st sits at base + st*STAGEB + grp*ROWB + k*G*16 + gl*16:
@@ -864,7 +872,7 @@ __global__ void __launch_bounds__(kAsyncThreads, 3) conf_async_kernel(const Conf
     float cA;
     int32_t labA;
     {
-      const RowSrc r = locate_cur(a, cur, actA ? rowA : 0, actA ? fA : fetch_index(a, 0));
+      const RowSrc r = locate_cur<RIDX>(a, cur, actA ? rowA : 0, actA ? fA : fetch_index_t<RIDX>(a, 0));
       pA = reinterpret_cast<const uint4*>(r.base + r.src * a.row_bytes);
       cA = r.c;
       labA = fetch_label(a, r);
@@ -872,7 +880,7 @@ __global__ void __launch_bounds__(kAsyncThreads, 3) conf_async_kernel(const Conf
     group_prefetch_row<NV, G, FULL>(sbase, pA, gl, nvec);
     cp_async_commit();
     int64_t gB = next_group(g0);
-    int64_t fB = fetch_index(a, gB * RPW + grp < cap ? gB * RPW + grp : 0);
+    int64_t fB = fetch_index_t<RIDX>(a, gB * RPW + grp < cap ? gB * RPW + grp : 0);
     uint4 A[NV];
     for (int it = 0;; ++it) {
       const int64_t rowB = gB * RPW + grp;
@@ -883,14 +891,14 @@ __global__ void __launch_bounds__(kAsyncThreads, 3) conf_async_kernel(const Conf
       float cB = cA;
       int32_t labB = 0;
       if (anyB) {
-        const RowSrc r = locate_cur(a, cur, actB ? rowB : 0, actB ? fB : fetch_index(a, 0));
+        const RowSrc r = locate_cur<RIDX>(a, cur, actB ? rowB : 0, actB ? fB : fetch_index_t<RIDX>(a, 0));
         pB = reinterpret_cast<const uint4*>(r.base + r.src * a.row_bytes);
         cB = r.c;
         group_prefetch_row<NV, G, FULL>(sbase + (uint32_t)((it + 1) & 1) * STAGEB, pB, gl, nvec);
         labB = fetch_label(a, r);
         gC = next_group(gB);
         const int64_t rowC = gC * RPW + grp;
-        fC = fetch_index(a, rowC < cap ? rowC : 0);
+        fC = fetch_index_t<RIDX>(a, rowC < cap ? rowC : 0);
       }
       cp_async_commit();
       cp_async_wait<1>();        // this lane's copies of row A have landed
@@ -1511,9 +1519,9 @@ cudaError_t launch_warp_l(const ConfArgs& a, int64_t rows, cudaStream_t s) {
   return launch_pdl(k, dim3(grid), dim3(256), 0, s, a);
 }
 
-template <bool BF16, bool ENTROPY, int NV, int G, bool FULL, bool DYN>
+template <bool BF16, bool ENTROPY, int NV, int G, bool FULL, bool DYN, bool RIDX>
 cudaError_t launch_async_d(const ConfArgs& a, int64_t rows, cudaStream_t s) {
-  auto k = conf_async_kernel<BF16, ENTROPY, NV, G, FULL, DYN>;
+  auto k = conf_async_kernel<BF16, ENTROPY, NV, G, FULL, DYN, RIDX>;
   constexpr int smem = async_smem_bytes<NV, G>();
   static const int occ = [&] {
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -1530,8 +1538,15 @@ cudaError_t launch_async_d(const ConfArgs& a, int64_t rows, cudaStream_t s) {
 
 template <bool BF16, bool ENTROPY, int NV, int G, bool FULL>
 cudaError_t launch_async_l(const ConfArgs& a, int64_t rows, cudaStream_t s) {
-  return a.ticket ? launch_async_d<BF16, ENTROPY, NV, G, FULL, true>(a, rows, s)
-                  : launch_async_d<BF16, ENTROPY, NV, G, FULL, false>(a, rows, s);
+#ifdef HS_AB_K1_RIDX_ALWAYS
+  if (true)
+#else
+  if (a.row_index)
+#endif
+    return a.ticket ? launch_async_d<BF16, ENTROPY, NV, G, FULL, true, true>(a, rows, s)
+                    : launch_async_d<BF16, ENTROPY, NV, G, FULL, false, true>(a, rows, s);
+  return a.ticket ? launch_async_d<BF16, ENTROPY, NV, G, FULL, true, false>(a, rows, s)
+                  : launch_async_d<BF16, ENTROPY, NV, G, FULL, false, false>(a, rows, s);
 }
 
 int conf_impl();

@@ -46,7 +46,10 @@ constexpr int kTfComp = 4;              // partial sums per stage: used, nll, g,
 // warm start: up to kTfSubPasses Newton sweeps over every kTfSubStride-th row
 // (same objective on a 1/16 sample) before the first full sweep, for stages
 // with >= kTfSubMin rows whose rows fit one chunk
-constexpr int kTfSubStride = 16;
+#ifndef HS_TF_SUB_STRIDE
+#define HS_TF_SUB_STRIDE 16
+#endif
+constexpr int kTfSubStride = HS_TF_SUB_STRIDE;
 constexpr int kTfSubPasses = 2;
 constexpr int64_t kTfSubMin = 32768;
 
