@@ -250,41 +250,6 @@ __device__ __forceinline__ void vec_accum(const uint4& v, f2_t m2, f2_t c2, uint
   }
 }
 
-// The same sums with the exponent folded into one FFMA2: a' = x*c - mc with
-// mc = fl(m*c), i.e. a' = (x - m)*c - delta rounded ONCE (delta = mc - m*c,
-// common to every element; the fma's single rounding error is relative to the
-// small |a'| near the max).  s' = 2^-delta s and w' = 2^-delta (w - delta s):
-// p_max = e0 / s' with e0 = 2^-delta computed from the exact residual
-// fma(m, c, -mc), and exp(-H) = 2^{w/s - log2 s} is invariant to the shift.
-template <bool BF16, bool ENTROPY>
-__device__ __forceinline__ void vec_accum_fold(const uint4& v, f2_t nmc2, f2_t c2, uint32_t clampw,
-                                               f2_t& s2, f2_t& w2) {
-  if (BF16) {
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      uint32_t u = ENTROPY ? bmax2_plain(word(v, q), clampw) : word(v, q);
-      f2_t a = f2fma(f2(bf_lo(u), bf_hi(u)), c2, nmc2);
-      f2_t e = f2(ex2(f2lo(a)), ex2(f2hi(a)));
-      s2 = f2add(s2, e);
-      if (ENTROPY) w2 = f2fma(e, a, w2);
-    }
-  } else {
-#pragma unroll
-    for (int q = 0; q < 2; ++q) {
-      f2_t a = f2fma(f2(__uint_as_float(word(v, 2 * q)), __uint_as_float(word(v, 2 * q + 1))), c2, nmc2);
-      float a0 = f2lo(a), a1 = f2hi(a);
-      if (ENTROPY) {
-        a0 = fmaxf(a0, -128.f);
-        a1 = fmaxf(a1, -128.f);
-        a = f2(a0, a1);
-      }
-      f2_t e = f2(ex2(a0), ex2(a1));
-      s2 = f2add(s2, e);
-      if (ENTROPY) w2 = f2fma(e, a, w2);
-    }
-  }
-}
-
 // bf16x2 word holding a lower bound L <= m - 128/c (rounded down): clamping
 // x >= L leaves every term with 2^a >= 2^-128 untouched and turns -inf into a
 // finite value whose 2^a flushes to 0, so 2^a * a stays 0 (masked classes).
@@ -457,16 +422,9 @@ __device__ __forceinline__ void group_reduce_row(const ConfArgs& a, const uint4 
   {   // unconditional: an invalid row's sums are discarded by write_row
 #endif
     const uint32_t cw = ENTROPY && BF16 ? entropy_clamp_word(m, c) : 0u;
-#ifndef HS_AB_NO_FOLD
-    const float mc = m * c;
-    const f2_t nmc2 = f2(-mc, -mc);
-#pragma unroll
-    for (int k = 0; k < NV; ++k) vec_accum_fold<BF16, ENTROPY>(v[k], nmc2, c2, cw, s2, w2);
-#else
     const f2_t m2 = f2(m, m);
 #pragma unroll
     for (int k = 0; k < NV; ++k) vec_accum<BF16, ENTROPY>(v[k], m2, c2, cw, s2, w2);
-#endif
   }
   float s = f2lo(s2) + f2hi(s2);
   float w = ENTROPY ? f2lo(w2) + f2hi(w2) : 0.f;
@@ -483,13 +441,7 @@ __device__ __forceinline__ void group_reduce_row(const ConfArgs& a, const uint4 
   const unsigned am = vi * VE + (unsigned)e;
 #endif
   if (active && gl == 0) {
-#ifndef HS_AB_NO_FOLD
-    // 2^{a'} of the max element: a' = m*c - fl(m*c), the exact residual (fma)
-    const float e0 = (m < INFINITY && m > -INFINITY) ? ex2(fmaf(m, c, -(m * c))) : 1.0f;
-#else
-    const float e0 = 1.0f;
-#endif
-    RowOut r{m, s, w, am, e0};
+    RowOut r{m, s, w, am, 1.0f};
     write_row(a, row, lab, r);
   }
 }

@@ -148,36 +148,6 @@ __device__ __forceinline__ void accum_chunk(const uint4 (&v)[U], f2_t m2, f2_t c
   }
 }
 
-// The same sums with the exponent folded into one FFMA2: z = x c - mc, mc =
-// fl(m c), i.e. z = (x - m) c - delta rounded once (delta = mc - m c, common to
-// the row): s' = 2^-delta s, and with t = e z the moments are those of z; the
-// caller converts them back (E[d] = (E[z] + delta) / c, Var[d] = Var[z] / c^2,
-// ln s = ln s' + delta ln 2).
-template <bool BF16, int U>
-__device__ __forceinline__ void accum_chunk_fold(const uint4 (&v)[U], f2_t nmc2, f2_t c2, uint32_t cw,
-                                                 float lowf, f2_t& s2, f2_t& w12, f2_t& w22) {
-#pragma unroll
-  for (int k = 0; k < U; ++k) {
-#pragma unroll
-    for (int q = 0; q < (BF16 ? 4 : 2); ++q) {
-      f2_t x;
-      if (BF16) {
-        const uint32_t u = bmax2_plain(wordq(v[k], q), cw);
-        x = f2(bf_lo(u), bf_hi(u));
-      } else {
-        x = f2(fmaxf(__uint_as_float(wordq(v[k], 2 * q)), lowf),
-               fmaxf(__uint_as_float(wordq(v[k], 2 * q + 1)), lowf));
-      }
-      const f2_t z = f2fma(x, c2, nmc2);
-      const f2_t e = f2(ex2(f2lo(z)), ex2(f2hi(z)));
-      s2 = f2add(s2, e);
-      const f2_t t = f2mul(e, z);
-      w12 = f2add(w12, t);
-      w22 = f2fma(t, z, w22);
-    }
-  }
-}
-
 // The group leader's verdict on a row with max m: used (valid, finite label
 // logit) and dy = x_y - m.  Invalid rows (NaN / +inf / all -inf) flag status.
 template <bool BF16>
@@ -498,41 +468,24 @@ __global__ void __launch_bounds__(kTfThreads, 1) temp_fit_kernel(const TfArgs a)
         const uint32_t cw = BF16 ? clamp_word_bf16(m, c) : 0u;
         const float lowf = m - fmaxf(128.0f / c, fabsf(m) * 0.0078125f);
         f2_t s2 = f2(0.f, 0.f), w12 = f2(0.f, 0.f), w22 = f2(0.f, 0.f);
-#ifndef HS_AB_TF_NO_FOLD
-        const float mc = m * c;
-        const f2_t nmc2 = f2(-mc, -mc);
-        accum_chunk_fold<BF16, U>(v, nmc2, c2, cw, lowf, s2, w12, w22);
-        for (int v0 = CH; v0 < a.nvec; v0 += CH) {           // longer rows: further chunks
-          load_chunk<BF16, G, U>(v, rowp, v0, gl, a.nvec, a.tail, inb && active);
-          accum_chunk_fold<BF16, U>(v, nmc2, c2, cw, lowf, s2, w12, w22);
-        }
-#else
         accum_chunk<BF16, U>(v, m2, c2, cw, lowf, s2, w12, w22);
         for (int v0 = CH; v0 < a.nvec; v0 += CH) {           // longer rows: further chunks
           load_chunk<BF16, G, U>(v, rowp, v0, gl, a.nvec, a.tail, inb && active);
           accum_chunk<BF16, U>(v, m2, c2, cw, lowf, s2, w12, w22);
         }
-#endif
         float s = group_sum<float, G>(f2lo(s2) + f2hi(s2));
         float w1 = group_sum<float, G>(f2lo(w12) + f2hi(w12));
         float w2 = group_sum<float, G>(f2lo(w22) + f2hi(w22));
-#ifndef HS_AB_TF_NO_FOLD
-        // back from the moments of z = (x - m) c - delta to those of d = x - m
-        const float delta = -fmaf(m, c, -mc);               // mc - m c, exact
-        const float rc = 1.0f / c;
-        const float lnfix = delta * 0.6931471805599453f;    // ln s = ln s' + delta ln 2
-#endif
         if (active && gl == 0) {
           // per-row moments in fp32 (one MUFU.RCP; s in [1, C]), row sums in fp64:
           // g_i and h_i only steer the Newton iteration, whose stop (2^-21 in beta)
           // is far above their fp32 rounding; the fp64 divisions cost ~10 % of a
           // sweep's instructions on the warp's critical path
-#if !defined(HS_AB_TF_NO_FOLD)
-          const float inv = __fdividef(1.0f, s), mz = w1 * inv;
-          const float mean = (mz + delta) * rc;
-          acc_nll += (double)logf(s) + (double)lnfix - beta * (double)rs.y;
-          acc_g += (double)(mean - rs.y);
-          acc_h += (double)(fmaxf(fmaf(w2, inv, -mz * mz), 0.0f) * (rc * rc));
+#ifdef HS_AB_TF_FP64_ROW
+          const double ds = (double)s, mean = (double)w1 / ds;
+          acc_nll += (double)logf(s) - beta * (double)rs.y;
+          acc_g += mean - (double)rs.y;
+          acc_h += fmax((double)w2 / ds - mean * mean, 0.0);
 #else
           const float inv = __fdividef(1.0f, s), mean = w1 * inv;
           acc_nll += (double)logf(s) - beta * (double)rs.y;

@@ -7,11 +7,10 @@ sys.path.insert(0, ROOT)
 from paper_2505_12566_b200 import _build  # noqa: E402
 
 VARIANTS = {
-    "tfnofold": ["HS_AB_TF_NO_FOLD"],                 # temperature fit: (x - m) then x c instead of one FFMA2
-    "nofold": ["HS_AB_NO_FOLD"],                      # K1a: (x - m) then x c (FADD2 + FMUL2) instead of one FFMA2
     "ridxall": ["HS_AB_K1_RIDX_ALWAYS"],              # K1a: one instantiation for dense and gathered rows
     "tfsub8": ["HS_TF_SUB_STRIDE=8"],                 # temperature fit: warm start on every 8th row
     "tfsub4": ["HS_TF_SUB_STRIDE=4"],                 # ... every 4th row
+    "tffp64": ["HS_AB_TF_FP64_ROW"],                  # temperature fit: per-row moments in fp64 (round 1)
     "noticket": ["HS_AB_NO_TICKET"],                  # K3 tiles by blockIdx (round 1)
     "linargmax": ["HS_AB_LINEAR_ARGMAX"],             # K1a argmax: one compare per vector (round 1)
     "ctrace": ["HS_CALIB_TRACE"],        # globaltimer trace of the calibration kernels
