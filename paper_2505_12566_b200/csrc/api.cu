@@ -179,7 +179,8 @@ uint64_t hs_launch_count(void) { return hs::g_launches.load(); }
 const char* hs_build_info(void) {
 #define HS_STR2(x) #x
 #define HS_STR(x) HS_STR2(x)
-#if defined(HS_EXP_NOARGMAX) || defined(HS_EXP_NOEXP) || defined(HS_EXP_TOPK_NOCAND)
+#if defined(HS_EXP_NOARGMAX) || defined(HS_EXP_NOEXP) || defined(HS_EXP_TOPK_NOCAND) || \
+    defined(HS_EXP_FZ_NOSCATTER) || defined(HS_EXP_FZ_NOSEQ) || defined(HS_EXP_FZ_RELAXED)
   // timing-bound experiment build (tools/build_variants.py): results are WRONG;
   // the Python loader refuses it unless HS_ALLOW_EXPERIMENT=1
   return "libhs: sm_100a (compute_100a), nvcc " HS_STR(__CUDACC_VER_MAJOR__) "." HS_STR(__CUDACC_VER_MINOR__)
@@ -897,10 +898,13 @@ hs_status_t hs_skip_route(const float* conf, int64_t n, const int64_t* d_n, floa
 
 // cascade-step workspace: [compact ws][conf f32 n][argmax i32 n*L][def_pos i64 n][conf ws]
 static size_t step_layout(int64_t n, int32_t L, size_t* o_conf, size_t* o_am, size_t* o_pos,
-                          size_t* o_cws, size_t* o_tick = nullptr, size_t* o_split = nullptr) {
+                          size_t* o_cws, size_t* o_tick = nullptr, size_t* o_split = nullptr,
+                          size_t* o_fuse = nullptr) {
   size_t off = align_up(hs::compact_ws_bytes(n), 256);
   if (o_tick) *o_tick = off;           // K1 row-group ticket + finished-CTA count
   off += 256;
+  if (o_fuse) *o_fuse = off;           // fused K1+K3 tiles (descriptors, counters), zero-filled once
+  off = align_up(off + hs::fuse_ws_bytes(), 256);
   *o_conf = off;
   off = align_up(off + (size_t)n * sizeof(float), 256);
   *o_am = off;
@@ -935,6 +939,14 @@ hs_status_t hs_cascade_step(int32_t stage, int32_t n_stages, const void* logits,
                             row_index, d_n, temperature, kind, reduce, threshold, d_threshold, ids,
                             payload, payload_row_bytes, acc_ids, acc_conf, acc_pred, next_ids,
                             next_payload, d_counts, ws, ws_bytes, d_status, 0, 0u, stream);
+}
+
+// HS_FUSE=1: hs_cascade_step runs K1 with the threshold test and the stable
+// compaction fused into it (one launch per stage).  Opt-in: measured slower
+// than K1 then K3 on C2.
+static bool fuse_enabled() {
+  const char* e = getenv("HS_FUSE");
+  return e && e[0] == '1';
 }
 
 static hs_status_t step_common_checks(int32_t stage, int32_t n_stages, int64_t n, float threshold,
@@ -1028,6 +1040,45 @@ hs_status_t hs_cascade_step_ex(int32_t stage, int32_t n_stages, const void* logi
   if (next_payload && (!payload || payload_row_bytes <= 0 || (payload_row_bytes & 15) ||
                        !aligned16(payload) || !aligned16(next_payload)))
     return fail(HS_ERR_INVALID_ARGUMENT, "payload rows must be 16-byte aligned multiples of 16 bytes");
+  // HS_FUSE=1: one launch, K1 with the threshold test and the stable
+  // compaction in its row epilogue, when the rows take the cp.async kernel
+  if (!(flags & HS_STEP_OVERLAP_PREVIOUS) && fuse_enabled()) {
+    st = check_logits(logits, dtype, n, seq_len, n_classes, row_stride, temperature, kind, reduce);
+    if (st != HS_OK) return st;
+    size_t o_conf, o_am, o_pos, o_cws, o_tick, o_split, o_fuse;
+    const size_t need = step_layout(n, seq_len, &o_conf, &o_am, &o_pos, &o_cws, &o_tick, &o_split, &o_fuse);
+    if (!ws || ws_bytes < need) return fail(HS_ERR_WORKSPACE_TOO_SMALL, "workspace %zu < %zu", ws_bytes, need);
+    char* w = reinterpret_cast<char*>(ws);
+    hs::ConfArgs a = make_conf_args(logits, dtype, n, seq_len, n_classes, row_stride, row_index, d_n,
+                                    temperature, kind);
+    a.top_k = top_k;
+    a.ticket = reinterpret_cast<unsigned int*>(w + o_tick);
+    if (hs::confidence_fusable(a)) {
+      cudaStream_t s = (cudaStream_t)stream;
+      if (n == 0) return cuda_check(cudaMemsetAsync(d_counts, 0, 2 * sizeof(int64_t), s), "memset counts");
+      const int is_last = stage == n_stages - 1;
+      int64_t* pos = reinterpret_cast<int64_t*>(w + o_pos);
+      a.fz.on = 1;
+      a.fz.is_last = is_last;
+      a.fz.threshold = threshold;
+      a.fz.d_threshold = d_threshold;
+      a.fz.ids = ids;
+      a.fz.acc_ids = acc_ids;
+      a.fz.acc_conf = acc_conf;
+      a.fz.acc_pred = acc_pred;
+      a.fz.def_ids = next_ids;
+      a.fz.def_pos = (next_payload && !is_last) ? pos : nullptr;
+      a.fz.counts = d_counts;
+      a.fz.tiles = w + o_fuse;
+      st = run_confidence_args(a, dtype, reduce, reinterpret_cast<float*>(w + o_conf),
+                               reinterpret_cast<int32_t*>(w + o_am), nullptr, nullptr, w + o_cws, d_status, s);
+      if (st != HS_OK) return st;
+      if (next_payload && payload_row_bytes > 0 && !is_last)
+        st = cuda_check(hs::launch_gather_rows(pos, d_counts + 1, n, payload, payload_row_bytes, next_payload, s),
+                        "gather kernel");
+      return st;
+    }
+  }
   st = hs_cascade_confidence(stage, n_stages, logits, dtype, n, seq_len, n_classes, row_stride, row_index, d_n,
                              temperature, kind, reduce, threshold, d_threshold, nullptr, ws, ws_bytes, d_status,
                              top_k, flags, stream);

@@ -45,8 +45,8 @@ struct RowOut {
 };
 
 // `lab`: the row's label, loaded by the caller ahead of time (a.labels only)
-__device__ __forceinline__ void write_row(const ConfArgs& a, int64_t row, int32_t lab,
-                                          const RowOut& r) {
+__device__ __forceinline__ float write_row(const ConfArgs& a, int64_t row, int32_t lab,
+                                           const RowOut& r) {
   const bool bad = !(r.m < INFINITY) || (r.m == -INFINITY);
   float c;
   int32_t am = (int32_t)r.am;
@@ -70,6 +70,7 @@ __device__ __forceinline__ void write_row(const ConfArgs& a, int64_t row, int32_
   if (a.conf2) a.conf2[row] = bad ? __int_as_float(0x7FC00000) : exp2f(r.w / r.s - log2f(r.s));
   if (a.argmax) a.argmax[row] = am;
   if (a.ok) a.ok[row] = (uint8_t)(a.labels ? (!bad && lab == am) : 0);
+  return c;
 }
 
 
@@ -339,10 +340,12 @@ __device__ __forceinline__ int tree_first8(const uint32_t (&v)[8], uint32_t mb2)
   return (l1 ? 0 : 4) + (l2 ? 0 : 2) + (l3 ? 0 : 1);
 }
 
+// Returns the row's confidence on its group's lane 0 (0 on the other lanes and
+// for an inactive group).
 template <bool BF16, bool ENTROPY, int NV, int G>
-__device__ __forceinline__ void group_reduce_row(const ConfArgs& a, const uint4 (&v)[NV],
-                                                 bool active, int64_t row, int gl,
-                                                 float c, const uint4* rowp, int32_t lab) {
+__device__ __forceinline__ float group_reduce_row(const ConfArgs& a, const uint4 (&v)[NV],
+                                                  bool active, int64_t row, int gl,
+                                                  float c, const uint4* rowp, int32_t lab) {
   constexpr int VE = BF16 ? 8 : 4;
   const f2_t c2 = f2(c, c);
   // 1. row max (exact, NaN-propagating): packed per-vector maxima, then the group
@@ -440,10 +443,12 @@ __device__ __forceinline__ void group_reduce_row(const ConfArgs& a, const uint4 
   }
   const unsigned am = vi * VE + (unsigned)e;
 #endif
+  float conf = 0.f;
   if (active && gl == 0) {
     RowOut r{m, s, w, am, 1.0f};
-    write_row(a, row, lab, r);
+    conf = write_row(a, row, lab, r);
   }
+  return conf;
 }
 
 template <bool L1>
@@ -818,14 +823,300 @@ __device__ __forceinline__ void group_lds_row(uint4 (&v)[NV], uint32_t ssrc, int
   }
 }
 
+// ---- fused threshold test + stable compaction (K1+K3, FuseArgs) ------------
+// Rows are claimed in chunks (in row order, from the ticket) and grouped into
+// at most kFuseTiles tiles of whole chunks.  Per tile:
+//   * every chunk adds {rows, deferred} to the tile counter with a release
+//     reduction (fire and forget: its rows' outputs are published with it);
+//   * one SEQUENCER warp (warp 0 of CTA 0, which claims no rows) reads the
+//     counters in tile order, 256 per L2 round trip (acquire), and as soon as
+//     every earlier tile is complete publishes each tile's exclusive deferred
+//     prefix (release) and re-arms its counter; after the last tile it writes
+//     the counts;
+//   * the warp that processed the tile's FIRST chunk owns the tile: it checks
+//     for the prefix at its next chunk boundaries (or waits once it has no
+//     rows left) and then writes the tile's accepted / deferred lists in row
+//     order.
+// No warp that holds unprocessed rows waits on another tile (at most one
+// pending tile per warp; a second one waits for the first, whose prefix is a
+// whole chunk of rows old by then).  Descriptors are {epoch:32 | flag:2 |
+// value:30}, epoch-tagged: no reset pass between launches.
+constexpr unsigned long long kFzFlagP = 2ull << 30;   // exclusive deferred prefix available
+constexpr unsigned long long kFzValMask = (1ull << 30) - 1;
+
+struct FuseTiles {
+  unsigned* epoch;
+  unsigned long long* desc;
+  unsigned long long* acc;
+};
+__device__ __forceinline__ FuseTiles fuse_tiles(void* w) {
+  char* b = reinterpret_cast<char*>(w);
+  return {reinterpret_cast<unsigned*>(b), reinterpret_cast<unsigned long long*>(b + 32),
+          reinterpret_cast<unsigned long long*>(b + 32 + 8 * kFuseTiles)};
+}
+#ifdef HS_FZ_TRACE
+// timing trace of the fused step (experiment build): first CTA start, last
+// tile completion seen by the sequencer, sequencer done, last scatter done, warps
+__device__ unsigned long long g_fz_trace[8];
+__device__ __forceinline__ unsigned long long fz_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#endif
+// Spin-waits of the fused step give up after 2 s (a corrupted workspace would
+// otherwise hang the device): HS_STATUS_TIMEOUT is ORed into the status word.
+constexpr unsigned long long kFzTimeoutNs = 2000ull * 1000 * 1000;
+__device__ __forceinline__ unsigned long long fz_clock() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void red_add_release(unsigned long long* p, unsigned long long v) {
+  asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_relaxed(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ bool fz_ready(unsigned long long d, unsigned epoch) {
+  return (unsigned)(d >> 32) == epoch && ((d >> 30) & 3u) == 2u;
+}
+// Tiles of whole claimed chunks: at most kFuseTiles of them.
+__device__ __forceinline__ int64_t fuse_tile_chunks(int64_t rows, int CR) {
+  const int64_t nch = (rows + CR - 1) / CR;
+  const int64_t sc = (nch + kFuseTiles - 1) / kFuseTiles;
+  return sc < 1 ? 1 : sc;
+}
+
+// The sequencer.
+__device__ __noinline__ void fuse_sequencer(const ConfArgs& a, int64_t rows, int CR, unsigned epoch) {
+  constexpr int U = 8;
+  const int lane = threadIdx.x & 31;
+  const FuseTiles t = fuse_tiles(a.fz.tiles);
+  const unsigned long long etag = (unsigned long long)epoch << 32;
+  const int64_t R = fuse_tile_chunks(rows, CR) * CR;
+  const int64_t NT = (rows + R - 1) / R;
+  long long run = 0;                               // deferred rows before tile j
+  unsigned long long t_prog = fz_clock();
+  for (int64_t j = 0; j < NT;) {
+    unsigned long long d[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t idx = j + 32 * u + lane;
+      d[u] = idx < NT ? ld_relaxed(&t.acc[idx]) : 0ull;   // polled relaxed (an acquire
+                                                          // load invalidates the SM's L1)
+    }
+    int ready = 0;
+    bool fenced = false;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (ready == 32 * u) {                       // warp-uniform: every earlier slot was complete
+        const int64_t idx = j + 32 * u + lane;
+        const int64_t trows = idx < NT ? (R < rows - idx * R ? R : rows - idx * R) : -1;
+        const unsigned nr = __ballot_sync(0xFFFFFFFFu, (int64_t)(d[u] >> 32) != trows);
+        const int r = nr ? __ffs(nr) - 1 : 32;
+        const long long own = lane < r ? (long long)(d[u] & 0xFFFFFFFFull) : 0ll;
+        long long v = own;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const long long y = __shfl_up_sync(0xFFFFFFFFu, v, o);
+          if (lane >= o) v += y;
+        }
+        if (r && !fenced) {
+          __threadfence();                         // acquire the counters read, release the prefixes
+          fenced = true;
+        }
+        if (lane < r) {
+          t.acc[idx] = 0ull;                       // re-armed for the next launch
+          st_relaxed(&t.desc[idx], etag | kFzFlagP | (unsigned long long)(run + v - own));
+        }
+        run += __shfl_sync(0xFFFFFFFFu, v, 31);
+        ready += r;
+      }
+    }
+    if (ready == 0) {
+      __nanosleep(64);
+      if (fz_clock() - t_prog > kFzTimeoutNs) {   // warp-uniform (lane 0's clock)
+        if (lane == 0 && a.status) atomicOr(a.status, HS_STATUS_TIMEOUT);
+        break;
+      }
+    } else {
+      t_prog = fz_clock();
+    }
+#ifdef HS_FZ_TRACE
+    else if (lane == 0) g_fz_trace[1] = fz_now();
+    if (lane == 0) g_fz_trace[6] += 1;             // probes
+#endif
+    j += ready;
+  }
+  if (lane == 0) {
+#ifdef HS_FZ_TRACE
+    g_fz_trace[2] = fz_now();
+#endif
+    a.fz.counts[0] = rows - run;
+    a.fz.counts[1] = run;
+    *(volatile unsigned*)t.epoch = epoch + 1u;     // retires this launch's descriptors
+  }
+}
+
+// The owner of tile j, once its exclusive deferred prefix `excl` is known:
+// D3 per row (accept iff c >= t; NaN defers; the last stage accepts all), the
+// accepted list and the deferred list (the next stage's batch) in row order.
+// The rows' outputs were published by their warps' release reductions, which
+// the sequencer acquired before its release of the prefix this warp acquired.
+__device__ __noinline__ void fuse_scatter_tile(const ConfArgs& a, int64_t j, int64_t R, int64_t rows,
+                                               long long excl, float thr) {
+  const int lane = threadIdx.x & 31;
+  const FuseArgs& z = a.fz;
+  const int64_t base = j * R;
+  const int tn = (int)(R < rows - base ? R : rows - base);
+  const int64_t acc_base = base - excl;            // accepted rows before this tile
+  const unsigned lt = lanemask_lt();
+  int dsum = 0;                                    // deferred rows of the tile so far
+  for (int p0 = 0; p0 < tn; p0 += 128) {
+    float cv[4];
+    int64_t idv[4];
+    int32_t pv[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int p = p0 + u * 32 + lane;
+      const int64_t i = base + p;
+      const bool in = p < tn;
+      cv[u] = in ? __ldcg(a.conf + i) : 0.f;
+      idv[u] = (in && z.ids) ? __ldg(z.ids + i) : i;
+      pv[u] = (in && z.acc_pred) ? __ldcg(a.argmax + i) : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int p = p0 + u * 32 + lane;
+      const bool in = p < tn;
+      const bool d = in && !(z.is_last || cv[u] >= thr);
+      const unsigned bd = __ballot_sync(0xFFFFFFFFu, d);
+      const int r = __popc(bd & lt);
+      if (d) {
+        const int64_t pos = excl + dsum + r;
+        if (z.def_ids) z.def_ids[pos] = idv[u];
+        if (z.def_pos) z.def_pos[pos] = base + p;
+      } else if (in) {
+        const int64_t pos = acc_base + p - (dsum + r);
+        if (z.acc_ids) z.acc_ids[pos] = idv[u];
+        if (z.acc_conf) z.acc_conf[pos] = cv[u];
+        if (z.acc_pred) z.acc_pred[pos] = pv[u];
+      }
+      dsum += __popc(bd);
+    }
+  }
+}
+
+// Per-warp state of the fused compaction in shared memory (kept out of the
+// row loop's registers).
+constexpr int kFusePend = 4;
+struct FusePend {
+  int tile[kFusePend];   // owned tiles waiting for their prefixes, in tile order (ring)
+  int head, count;
+  unsigned epoch;        // this launch's descriptor epoch (read at the start: the
+                         // sequencer retires it once every prefix is published)
+  unsigned pad;
+};
+
+// The owned tiles' lists, oldest first, while their prefixes are published
+// (`wait`: until every owned tile is done).
+__device__ __noinline__ void fuse_try_pending(const ConfArgs& a, FusePend* fp, int64_t rows, int CR,
+                                              float thr, bool wait) {
+  const int lane = threadIdx.x & 31;
+  while (fp->count > 0) {
+    const int j = fp->tile[fp->head];
+    const unsigned long long* dp = &fuse_tiles(a.fz.tiles).desc[j];
+    const unsigned epoch = fp->epoch;
+    unsigned long long d = 0;
+    bool late = false;
+    if (lane == 0) {
+      d = ld_relaxed(dp);
+      const unsigned long long t0 = wait ? fz_clock() : 0ull;
+      while (wait && !fz_ready(d, epoch)) {
+        __nanosleep(64);
+        d = ld_relaxed(dp);
+        if (fz_clock() - t0 > kFzTimeoutNs) {
+          late = true;
+          if (a.status) atomicOr(a.status, HS_STATUS_TIMEOUT);
+          break;
+        }
+      }
+    }
+    d = __shfl_sync(0xFFFFFFFFu, d, 0);
+    if (__shfl_sync(0xFFFFFFFFu, late, 0)) {       // give the tile up
+      if (lane == 0) fp->count = 0;
+      __syncwarp();
+      return;
+    }
+    if (!fz_ready(d, epoch)) return;
+    __syncwarp();
+    __threadfence();                               // acquire: the prefix, then the rows' outputs
+    const int64_t R = fuse_tile_chunks(rows, CR) * CR;
+    fuse_scatter_tile(a, j, R, rows, (long long)(d & kFzValMask), thr);
+    __syncwarp();
+#ifdef HS_FZ_TRACE
+    if (lane == 0) atomicMax(&g_fz_trace[3], fz_now());
+#endif
+    if (lane == 0) {
+      fp->head = (fp->head + 1) % kFusePend;
+      fp->count -= 1;
+    }
+    __syncwarp();
+  }
+}
+
+// End of claimed chunk c (`cdef` deferred rows): release-add to the tile
+// counter; the warp of the tile's first chunk becomes its owner (queued; the
+// warp waits only when kFusePend owned tiles are still unpublished).
+__device__ __noinline__ void fuse_chunk_end(const ConfArgs& a, FusePend* fp, int64_t c, unsigned cdef,
+                                            int64_t rows, int CR, float thr) {
+  const int lane = threadIdx.x & 31;
+  const int64_t sc = fuse_tile_chunks(rows, CR);
+  const int64_t c0 = c * CR;
+  const unsigned crow = (unsigned)(rows - c0 < CR ? rows - c0 : CR);
+  __syncwarp();                                    // both groups' row outputs before the release
+#ifdef HS_FZ_TRACE
+  if (lane == 0) atomicMax(&g_fz_trace[5], fz_now());
+#endif
+#ifdef HS_EXP_FZ_RELAXED
+  if (lane == 0) atomicAdd(&fuse_tiles(a.fz.tiles).acc[c / sc], ((unsigned long long)crow << 32) | cdef);
+#else
+  if (lane == 0)
+    red_add_release(&fuse_tiles(a.fz.tiles).acc[c / sc], ((unsigned long long)crow << 32) | cdef);
+#endif
+#ifdef HS_EXP_FZ_NOSCATTER
+  return;
+#endif
+  fuse_try_pending(a, fp, rows, CR, thr, false);
+  if (c % sc == 0) {
+    if (fp->count == kFusePend) {                  // rare: wait for the oldest
+      fuse_try_pending(a, fp, rows, CR, thr, true);
+    }
+    if (lane == 0) {
+      fp->tile[(fp->head + fp->count) % kFusePend] = (int)(c / sc);
+      fp->count += 1;
+    }
+    __syncwarp();
+  }
+}
+
 constexpr int kAsyncThreads = 256;
 template <int NV, int G>
 constexpr int async_smem_bytes() { return (kAsyncThreads / 32) * 2 * (32 / G) * G * NV * 16; }
 
 // RIDX: the launch reads rows through row_index (gathered batch); false for
 // dense batches -- the row-index lookups and checks compile away.
-template <bool BF16, bool ENTROPY, int NV, int G, bool FULL, bool DYN, bool RIDX>
-__global__ void __launch_bounds__(kAsyncThreads, 3) conf_async_kernel(const ConfArgs a) {
+// FUSE: the threshold test + stable compaction of hs_cascade_step in the row
+// epilogue (a.fz; requires DYN and no late wait).
+template <bool BF16, bool ENTROPY, int NV, int G, bool FULL, bool DYN, bool RIDX, bool FUSE>
+__global__ void __launch_bounds__(kAsyncThreads, 3) conf_async_kernel(const __grid_constant__ ConfArgs a) {
+  static_assert(!FUSE || DYN, "the fused compaction needs rows claimed in order");
   if (a.late_wait) pdl_trigger(); else pdl_start();
   extern __shared__ __align__(16) unsigned char smem[];
   constexpr int RPW = 32 / G;
@@ -843,21 +1134,55 @@ __global__ void __launch_bounds__(kAsyncThreads, 3) conf_async_kernel(const Conf
   // the previous kernel) just take fewer groups
   // dynamic claims come in chunks of kChunk groups per warp (one atomic per
   // kChunk * RPW rows keeps the single ticket word off the critical path)
-  constexpr int kChunk = 8;
+  // The next chunk is claimed when the current chunk's last group is handed
+  // out and taken when that group has been reduced: the ticket atomic's
+  // latency hides behind a row group, and a warp holds at most one group
+  // beyond its current chunk (tail balance).
+  // chunks of 8 row groups (A/B: chunks of 1-4 groups for small batches are
+  // slower -- the single ticket word's atomics serialise)
+  constexpr int kShift = 3;
+  constexpr int kChunk = 1 << kShift;
   int64_t cnext = 0, cend = 0;
+  unsigned cpre = 0;                                  // lane 0: the chunk claimed ahead
+  auto claim = [&]() {
+    if (lane == 0) cpre = atomicAdd(a.ticket, (unsigned)kChunk);
+  };
   auto next_group = [&](int64_t g) -> int64_t {
     if (!dyn) return g + nwarps;
     if (cnext == cend) {
-      unsigned t = 0;
-      if (lane == 0) t = atomicAdd(a.ticket, (unsigned)kChunk);
-      cnext = (int64_t)__shfl_sync(0xFFFFFFFFu, t, 0);
+      cnext = (int64_t)__shfl_sync(0xFFFFFFFFu, cpre, 0);
       cend = cnext + kChunk;
     }
+    if (cnext == cend - 1) claim();
     return cnext++;
   };
-  const int64_t g0 = dyn ? next_group(0) : ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  // fused compaction: warp 0 of CTA 0 is the sequencer and claims no rows
+  const bool seq = FUSE && blockIdx.x == 0 && warp == 0;
+  if (dyn && !seq) claim();
+  const int64_t g0 = seq ? (int64_t(1) << 56) / RPW
+                         : dyn ? next_group(0) : ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t fA = fetch_index_t<RIDX>(a, g0 * RPW + grp < cap ? g0 * RPW + grp : 0);
   const int64_t rows = live_rows(a);
+  // fused compaction: the chunk's deferred rows (registers); the warp's pending
+  // tile in shared memory
+  constexpr int CR = kChunk * RPW;                    // rows per claimed chunk
+  float thr = 0.f;
+  unsigned cdef = 0;
+  __shared__ FusePend s_pend[FUSE ? kAsyncThreads / 32 : 1];
+  FusePend* fp = &s_pend[FUSE ? warp : 0];
+  if constexpr (FUSE) {
+    thr = a.fz.d_threshold ? *a.fz.d_threshold : a.fz.threshold;
+    if (lane == 0) {
+      fp->head = 0;
+      fp->count = 0;
+      fp->epoch = *(volatile unsigned*)fuse_tiles(a.fz.tiles).epoch;
+#ifdef HS_FZ_TRACE
+      atomicMin(&g_fz_trace[0], fz_now());
+      atomicAdd(&g_fz_trace[4], 1ull);
+#endif
+    }
+    __syncwarp();
+  }
   if (g0 * RPW < rows) {
     // lane gl's vector k of stage st sits at base + st*STAGEB + grp*ROWB + k*G*16 + gl*16:
     // a quarter-warp reads 128 contiguous bytes (conflict-free LDS.128)
@@ -879,6 +1204,7 @@ __global__ void __launch_bounds__(kAsyncThreads, 3) conf_async_kernel(const Conf
     }
     group_prefetch_row<NV, G, FULL>(sbase, pA, gl, nvec);
     cp_async_commit();
+    int64_t gA = g0;
     int64_t gB = next_group(g0);
     int64_t fB = fetch_index_t<RIDX>(a, gB * RPW + grp < cap ? gB * RPW + grp : 0);
     uint4 A[NV];
@@ -904,8 +1230,17 @@ __global__ void __launch_bounds__(kAsyncThreads, 3) conf_async_kernel(const Conf
       cp_async_wait<1>();        // this lane's copies of row A have landed
       group_lds_row<BF16, NV, G, FULL>(A, sbase + (uint32_t)(it & 1) * STAGEB, gl, nvec);
       if (a.tail) group_mask_tail<BF16, NV, G>(A, gl, nvec, a.tail);
-      group_reduce_row<BF16, ENTROPY, NV, G>(a, A, actA, rowA, gl, cA, pA, labA);
+      const float crA = group_reduce_row<BF16, ENTROPY, NV, G>(a, A, actA, rowA, gl, cA, pA, labA);
+      if constexpr (FUSE) {
+        // D3 per row (accept iff c >= t, NaN defers; the last stage accepts all)
+        cdef += (unsigned)__popc(__ballot_sync(0xFFFFFFFFu, actA && gl == 0 && !(a.fz.is_last || crA >= thr)));
+        if (((gA + 1) & (kChunk - 1)) == 0 || !anyB) {
+          fuse_chunk_end(a, fp, gA >> kShift, cdef, rows, CR, thr);
+          cdef = 0;
+        }
+      }
       if (!anyB) break;
+      gA = gB;
       rowA = rowB;
       actA = actB;
       pA = pB;
@@ -915,8 +1250,21 @@ __global__ void __launch_bounds__(kAsyncThreads, 3) conf_async_kernel(const Conf
       fB = fC;
     }
     cp_async_wait<0>();
+#ifndef HS_EXP_FZ_NOSCATTER
+    if constexpr (FUSE) fuse_try_pending(a, fp, rows, CR, thr, true);
+#endif
+  }
+  if constexpr (FUSE) {
+#ifndef HS_EXP_FZ_NOSEQ
+    if (seq) fuse_sequencer(a, rows, CR, fp->epoch);
+#endif
   }
   if (dyn) {
+    // the claim issued ahead must have landed before the last CTA re-arms the
+    // ticket: consume its result (the store below never executes -- ticket
+    // values are multiples of kChunk -- but keeps the wait from being elided)
+    cpre = __shfl_sync(0xFFFFFFFFu, cpre, 0);
+    if (cpre == 0xFFFFFFFFu) a.ticket[2] = 0u;
     __syncthreads();                 // every warp of this CTA is done claiming
     if (threadIdx.x == 0) {
       const unsigned done = atomicAdd(a.ticket + 1, 1u);
@@ -1519,9 +1867,9 @@ cudaError_t launch_warp_l(const ConfArgs& a, int64_t rows, cudaStream_t s) {
   return launch_pdl(k, dim3(grid), dim3(256), 0, s, a);
 }
 
-template <bool BF16, bool ENTROPY, int NV, int G, bool FULL, bool DYN, bool RIDX>
+template <bool BF16, bool ENTROPY, int NV, int G, bool FULL, bool DYN, bool RIDX, bool FUSE = false>
 cudaError_t launch_async_d(const ConfArgs& a, int64_t rows, cudaStream_t s) {
-  auto k = conf_async_kernel<BF16, ENTROPY, NV, G, FULL, DYN, RIDX>;
+  auto k = conf_async_kernel<BF16, ENTROPY, NV, G, FULL, DYN, RIDX, FUSE>;
   constexpr int smem = async_smem_bytes<NV, G>();
   static const int occ = [&] {
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -1543,8 +1891,12 @@ cudaError_t launch_async_l(const ConfArgs& a, int64_t rows, cudaStream_t s) {
 #else
   if (a.row_index)
 #endif
+  {
+    if (a.fz.on) return launch_async_d<BF16, ENTROPY, NV, G, FULL, true, true, true>(a, rows, s);
     return a.ticket ? launch_async_d<BF16, ENTROPY, NV, G, FULL, true, true>(a, rows, s)
                     : launch_async_d<BF16, ENTROPY, NV, G, FULL, false, true>(a, rows, s);
+  }
+  if (a.fz.on) return launch_async_d<BF16, ENTROPY, NV, G, FULL, true, false, true>(a, rows, s);
   return a.ticket ? launch_async_d<BF16, ENTROPY, NV, G, FULL, true, false>(a, rows, s)
                   : launch_async_d<BF16, ENTROPY, NV, G, FULL, false, false>(a, rows, s);
 }
@@ -1683,6 +2035,24 @@ cudaError_t dispatch(const ConfArgs& a, int64_t rows, cudaStream_t s) {
 }
 
 }  // namespace
+
+#ifdef HS_FZ_TRACE
+}  // namespace hs
+extern "C" int hs_fz_trace(unsigned long long* host8, int reset) {
+  unsigned long long z[8] = {~0ull, 0, 0, 0, 0, 0, 0, 0};
+  cudaDeviceSynchronize();
+  if (host8 && cudaMemcpyFromSymbol(host8, hs::g_fz_trace, sizeof(z)) != cudaSuccess) return 1;
+  if (reset && cudaMemcpyToSymbol(hs::g_fz_trace, z, sizeof(z)) != cudaSuccess) return 1;
+  return 0;
+}
+namespace hs {
+#endif
+
+bool confidence_fusable(const ConfArgs& a) {
+  // the dispatch below: rows of <= 128 x 16 B take the cp.async kernel (K1a)
+  return a.L == 1 && a.nbatch == 1 && !a.late_wait && (a.top_k == 0 || (int64_t)a.top_k >= a.C) &&
+         a.nvec <= 128 && conf_impl() == 2;
+}
 
 size_t split_ws_bytes(int64_t rows) {
   if (rows <= 0 || rows > kSplitMaxRows) return 0;

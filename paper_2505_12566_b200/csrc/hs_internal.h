@@ -39,6 +39,28 @@ cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t s
 
 // ---- K1 / K2 ---------------------------------------------------------------
 constexpr int kMaxBatch = 8;
+// K1 with the stage's threshold test and stable compaction (K3) fused into its
+// row epilogue (hs_cascade_step, single-token rows on the cp.async kernel).
+// Rows are cut into at most kFuseTiles contiguous tiles of whole claimed
+// chunks; the warp whose chunk completes a tile publishes the tile's deferred
+// count, looks back over the tile descriptors for its exclusive prefix and
+// scatters the tile's accepted / deferred lists.
+constexpr int kFuseTiles = 1024;
+struct FuseArgs {
+  int on;                         // 0: plain K1
+  int is_last;                    // the last stage accepts every row
+  float threshold;
+  const float* d_threshold;       // overrides threshold when non-NULL
+  const int64_t* ids;             // request id of row i, or NULL (= i)
+  int64_t* acc_ids;               // accepted: id, confidence, argmax (stable order)
+  float* acc_conf;
+  int32_t* acc_pred;
+  int64_t* def_ids;               // deferred: id (the next stage's batch), stable order
+  int64_t* def_pos;               // deferred: row position (payload gather), or NULL
+  int64_t* counts;                // {n_acc, n_def}
+  void* tiles;                    // fuse_ws_bytes(): header, descriptors, tile counters
+};
+constexpr size_t fuse_ws_bytes() { return 32 + (size_t)kFuseTiles * 16; }
 struct ConfArgs {
   const void* logits;
   int64_t row_bytes;       // row_stride * element size (multiple of 16)
@@ -79,7 +101,12 @@ struct ConfArgs {
   // optional second output: exp(-H) of every row alongside `conf` (north_star
   // "max-probability (and entropy) confidence"); forces the entropy sums
   float* conf2;
+  // K1+K3 fused (async kernel with a ticket, L = 1, nbatch = 1, no late wait)
+  FuseArgs fz;
 };
+// true when launch_confidence(a) takes the cp.async kernel, which is the one
+// that can run the fused threshold test + compaction
+bool confidence_fusable(const ConfArgs& a);
 constexpr int kSplitMaxRows = 2048;     // the split path serves batches up to this many rows
 constexpr int kSplitMaxSeg = 64;        // segments per row
 size_t split_ws_bytes(int64_t rows);
