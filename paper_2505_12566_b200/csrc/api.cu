@@ -180,7 +180,7 @@ const char* hs_build_info(void) {
 #define HS_STR2(x) #x
 #define HS_STR(x) HS_STR2(x)
 #if defined(HS_EXP_NOARGMAX) || defined(HS_EXP_NOEXP) || defined(HS_EXP_TOPK_NOCAND) || \
-    defined(HS_EXP_FZ_NOSCATTER) || defined(HS_EXP_FZ_NOSEQ) || defined(HS_EXP_FZ_RELAXED)
+    defined(HS_EXP_FZ_NOSYNC) || defined(HS_EXP_FZ_NOFINISH)
   // timing-bound experiment build (tools/build_variants.py): results are WRONG;
   // the Python loader refuses it unless HS_ALLOW_EXPERIMENT=1
   return "libhs: sm_100a (compute_100a), nvcc " HS_STR(__CUDACC_VER_MAJOR__) "." HS_STR(__CUDACC_VER_MINOR__)
@@ -903,7 +903,7 @@ static size_t step_layout(int64_t n, int32_t L, size_t* o_conf, size_t* o_am, si
   size_t off = align_up(hs::compact_ws_bytes(n), 256);
   if (o_tick) *o_tick = off;           // K1 row-group ticket + finished-CTA count
   off += 256;
-  if (o_fuse) *o_fuse = off;           // fused K1+K3 tiles (descriptors, counters), zero-filled once
+  if (o_fuse) *o_fuse = off;           // fused K1+K3: epoch + two banks of tile counters
   off = align_up(off + hs::fuse_ws_bytes(), 256);
   *o_conf = off;
   off = align_up(off + (size_t)n * sizeof(float), 256);
@@ -1052,7 +1052,6 @@ hs_status_t hs_cascade_step_ex(int32_t stage, int32_t n_stages, const void* logi
     hs::ConfArgs a = make_conf_args(logits, dtype, n, seq_len, n_classes, row_stride, row_index, d_n,
                                     temperature, kind);
     a.top_k = top_k;
-    a.ticket = reinterpret_cast<unsigned int*>(w + o_tick);
     if (hs::confidence_fusable(a)) {
       cudaStream_t s = (cudaStream_t)stream;
       if (n == 0) return cuda_check(cudaMemsetAsync(d_counts, 0, 2 * sizeof(int64_t), s), "memset counts");

@@ -25,6 +25,7 @@
 //   * conf_cta_kernel   -- one CTA per row, persistent over rows, per-thread
 //     online (max, sum, weighted sum) over 8-vector chunks, block merge
 //     (vocabulary-sized rows: T5 32,128, Llama 128,256).
+#include <cooperative_groups.h>
 #include <cuda_bf16.h>
 #include <cstdlib>
 #include <cstring>
@@ -824,151 +825,35 @@ __device__ __forceinline__ void group_lds_row(uint4 (&v)[NV], uint32_t ssrc, int
 }
 
 // ---- fused threshold test + stable compaction (K1+K3, FuseArgs) ------------
-// Rows are claimed in chunks (in row order, from the ticket) and grouped into
-// at most kFuseTiles tiles of whole chunks.  Per tile:
-//   * every chunk adds {rows, deferred} to the tile counter with a release
-//     reduction (fire and forget: its rows' outputs are published with it);
-//   * one SEQUENCER warp (warp 0 of CTA 0, which claims no rows) reads the
-//     counters in tile order, 256 per L2 round trip (acquire), and as soon as
-//     every earlier tile is complete publishes each tile's exclusive deferred
-//     prefix (release) and re-arms its counter; after the last tile it writes
-//     the counts;
-//   * the warp that processed the tile's FIRST chunk owns the tile: it checks
-//     for the prefix at its next chunk boundaries (or waits once it has no
-//     rows left) and then writes the tile's accepted / deferred lists in row
-//     order.
-// No warp that holds unprocessed rows waits on another tile (at most one
-// pending tile per warp; a second one waits for the first, whose prefix is a
-// whole chunk of rows old by then).  Descriptors are {epoch:32 | flag:2 |
-// value:30}, epoch-tagged: no reset pass between launches.
-constexpr unsigned long long kFzFlagP = 2ull << 30;   // exclusive deferred prefix available
-constexpr unsigned long long kFzValMask = (1ull << 30) - 1;
-
+// One cooperative launch (all CTAs co-resident).  Row groups are cut into at
+// most kFuseTiles tiles of 2^s consecutive groups.  While streaming its rows a
+// warp adds each group's deferred count to the group's tile counter (one
+// relaxed reduction; no fence).  After the last row, ONE grid barrier; then
+// every CTA scans the tile counters into exclusive deferred prefixes (shared
+// memory, the same in every CTA) and each warp writes the accepted / deferred
+// lists of its tiles in row order, reading the rows' confidences and
+// argmaxes that the barrier made visible.  The counters alternate between two
+// banks by launch (the launch epoch's parity): a launch zeroes the bank the
+// next one uses.
 struct FuseTiles {
   unsigned* epoch;
-  unsigned long long* desc;
-  unsigned long long* acc;
+  unsigned* acc;          // [2][kFuseTiles]
 };
 __device__ __forceinline__ FuseTiles fuse_tiles(void* w) {
   char* b = reinterpret_cast<char*>(w);
-  return {reinterpret_cast<unsigned*>(b), reinterpret_cast<unsigned long long*>(b + 32),
-          reinterpret_cast<unsigned long long*>(b + 32 + 8 * kFuseTiles)};
+  return {reinterpret_cast<unsigned*>(b), reinterpret_cast<unsigned*>(b + 32)};
 }
-#ifdef HS_FZ_TRACE
-// timing trace of the fused step (experiment build): first CTA start, last
-// tile completion seen by the sequencer, sequencer done, last scatter done, warps
-__device__ unsigned long long g_fz_trace[8];
-__device__ __forceinline__ unsigned long long fz_now() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
-#endif
-// Spin-waits of the fused step give up after 2 s (a corrupted workspace would
-// otherwise hang the device): HS_STATUS_TIMEOUT is ORed into the status word.
-constexpr unsigned long long kFzTimeoutNs = 2000ull * 1000 * 1000;
-__device__ __forceinline__ unsigned long long fz_clock() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
-__device__ __forceinline__ void red_add_release(unsigned long long* p, unsigned long long v) {
-  asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ unsigned long long ld_relaxed(const unsigned long long* p) {
-  unsigned long long v;
-  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_relaxed(unsigned long long* p, unsigned long long v) {
-  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ bool fz_ready(unsigned long long d, unsigned epoch) {
-  return (unsigned)(d >> 32) == epoch && ((d >> 30) & 3u) == 2u;
-}
-// Tiles of whole claimed chunks: at most kFuseTiles of them.
-__device__ __forceinline__ int64_t fuse_tile_chunks(int64_t rows, int CR) {
-  const int64_t nch = (rows + CR - 1) / CR;
-  const int64_t sc = (nch + kFuseTiles - 1) / kFuseTiles;
-  return sc < 1 ? 1 : sc;
+// Tiles of 2^s row groups (RPW rows each), s the least with <= kFuseTiles tiles.
+__device__ __forceinline__ int fuse_tshift(int64_t rows, int RPW) {
+  const int64_t ng = (rows + RPW - 1) / RPW;
+  int sh = 0;
+  while (((ng + (int64_t(1) << sh) - 1) >> sh) > kFuseTiles) ++sh;
+  return sh;
 }
 
-// The sequencer.
-__device__ __noinline__ void fuse_sequencer(const ConfArgs& a, int64_t rows, int CR, unsigned epoch) {
-  constexpr int U = 8;
-  const int lane = threadIdx.x & 31;
-  const FuseTiles t = fuse_tiles(a.fz.tiles);
-  const unsigned long long etag = (unsigned long long)epoch << 32;
-  const int64_t R = fuse_tile_chunks(rows, CR) * CR;
-  const int64_t NT = (rows + R - 1) / R;
-  long long run = 0;                               // deferred rows before tile j
-  unsigned long long t_prog = fz_clock();
-  for (int64_t j = 0; j < NT;) {
-    unsigned long long d[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t idx = j + 32 * u + lane;
-      d[u] = idx < NT ? ld_relaxed(&t.acc[idx]) : 0ull;   // polled relaxed (an acquire
-                                                          // load invalidates the SM's L1)
-    }
-    int ready = 0;
-    bool fenced = false;
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      if (ready == 32 * u) {                       // warp-uniform: every earlier slot was complete
-        const int64_t idx = j + 32 * u + lane;
-        const int64_t trows = idx < NT ? (R < rows - idx * R ? R : rows - idx * R) : -1;
-        const unsigned nr = __ballot_sync(0xFFFFFFFFu, (int64_t)(d[u] >> 32) != trows);
-        const int r = nr ? __ffs(nr) - 1 : 32;
-        const long long own = lane < r ? (long long)(d[u] & 0xFFFFFFFFull) : 0ll;
-        long long v = own;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const long long y = __shfl_up_sync(0xFFFFFFFFu, v, o);
-          if (lane >= o) v += y;
-        }
-        if (r && !fenced) {
-          __threadfence();                         // acquire the counters read, release the prefixes
-          fenced = true;
-        }
-        if (lane < r) {
-          t.acc[idx] = 0ull;                       // re-armed for the next launch
-          st_relaxed(&t.desc[idx], etag | kFzFlagP | (unsigned long long)(run + v - own));
-        }
-        run += __shfl_sync(0xFFFFFFFFu, v, 31);
-        ready += r;
-      }
-    }
-    if (ready == 0) {
-      __nanosleep(64);
-      if (fz_clock() - t_prog > kFzTimeoutNs) {   // warp-uniform (lane 0's clock)
-        if (lane == 0 && a.status) atomicOr(a.status, HS_STATUS_TIMEOUT);
-        break;
-      }
-    } else {
-      t_prog = fz_clock();
-    }
-#ifdef HS_FZ_TRACE
-    else if (lane == 0) g_fz_trace[1] = fz_now();
-    if (lane == 0) g_fz_trace[6] += 1;             // probes
-#endif
-    j += ready;
-  }
-  if (lane == 0) {
-#ifdef HS_FZ_TRACE
-    g_fz_trace[2] = fz_now();
-#endif
-    a.fz.counts[0] = rows - run;
-    a.fz.counts[1] = run;
-    *(volatile unsigned*)t.epoch = epoch + 1u;     // retires this launch's descriptors
-  }
-}
-
-// The owner of tile j, once its exclusive deferred prefix `excl` is known:
-// D3 per row (accept iff c >= t; NaN defers; the last stage accepts all), the
-// accepted list and the deferred list (the next stage's batch) in row order.
-// The rows' outputs were published by their warps' release reductions, which
-// the sequencer acquired before its release of the prefix this warp acquired.
+// Tile j of R rows, its exclusive deferred prefix `excl` known: D3 per row
+// (accept iff c >= t; NaN defers; the last stage accepts all), the accepted
+// list and the deferred list (the next stage's batch) in row order.
 __device__ __noinline__ void fuse_scatter_tile(const ConfArgs& a, int64_t j, int64_t R, int64_t rows,
                                                long long excl, float thr) {
   const int lane = threadIdx.x & 31;
@@ -1013,96 +898,53 @@ __device__ __noinline__ void fuse_scatter_tile(const ConfArgs& a, int64_t j, int
   }
 }
 
-// Per-warp state of the fused compaction in shared memory (kept out of the
-// row loop's registers).
-constexpr int kFusePend = 4;
-struct FusePend {
-  int tile[kFusePend];   // owned tiles waiting for their prefixes, in tile order (ring)
-  int head, count;
-  unsigned epoch;        // this launch's descriptor epoch (read at the start: the
-                         // sequencer retires it once every prefix is published)
-  unsigned pad;
-};
-
-// The owned tiles' lists, oldest first, while their prefixes are published
-// (`wait`: until every owned tile is done).
-__device__ __noinline__ void fuse_try_pending(const ConfArgs& a, FusePend* fp, int64_t rows, int CR,
-                                              float thr, bool wait) {
-  const int lane = threadIdx.x & 31;
-  while (fp->count > 0) {
-    const int j = fp->tile[fp->head];
-    const unsigned long long* dp = &fuse_tiles(a.fz.tiles).desc[j];
-    const unsigned epoch = fp->epoch;
-    unsigned long long d = 0;
-    bool late = false;
-    if (lane == 0) {
-      d = ld_relaxed(dp);
-      const unsigned long long t0 = wait ? fz_clock() : 0ull;
-      while (wait && !fz_ready(d, epoch)) {
-        __nanosleep(64);
-        d = ld_relaxed(dp);
-        if (fz_clock() - t0 > kFzTimeoutNs) {
-          late = true;
-          if (a.status) atomicOr(a.status, HS_STATUS_TIMEOUT);
-          break;
-        }
-      }
-    }
-    d = __shfl_sync(0xFFFFFFFFu, d, 0);
-    if (__shfl_sync(0xFFFFFFFFu, late, 0)) {       // give the tile up
-      if (lane == 0) fp->count = 0;
-      __syncwarp();
-      return;
-    }
-    if (!fz_ready(d, epoch)) return;
-    __syncwarp();
-    __threadfence();                               // acquire: the prefix, then the rows' outputs
-    const int64_t R = fuse_tile_chunks(rows, CR) * CR;
-    fuse_scatter_tile(a, j, R, rows, (long long)(d & kFzValMask), thr);
-    __syncwarp();
-#ifdef HS_FZ_TRACE
-    if (lane == 0) atomicMax(&g_fz_trace[3], fz_now());
-#endif
-    if (lane == 0) {
-      fp->head = (fp->head + 1) % kFusePend;
-      fp->count -= 1;
-    }
-    __syncwarp();
+// After the grid barrier: the prefixes (every CTA), the lists (warp per tile),
+// the counts and the epoch (CTA 0).  `spre`: >= kFuseTiles + 32 words of
+// shared memory.
+__device__ __noinline__ void fuse_finish(const ConfArgs& a, int64_t rows, int RPW, unsigned epoch,
+                                         float thr, unsigned* spre) {
+  const FuseTiles t = fuse_tiles(a.fz.tiles);
+  const unsigned* acc = t.acc + (epoch & 1u) * kFuseTiles;
+  const int tsh = fuse_tshift(rows, RPW);
+  const int64_t R = (int64_t(1) << tsh) * RPW;
+  const int NT = (int)((rows + R - 1) / R);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nthr = blockDim.x;
+  constexpr int PER = kFuseTiles / 256;            // tiles per thread (256-thread CTAs)
+  unsigned v[PER], sum = 0;
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    const int j = tid * PER + q;
+    v[q] = j < NT ? __ldcg(acc + j) : 0u;
+    sum += v[q];
   }
-}
-
-// End of claimed chunk c (`cdef` deferred rows): release-add to the tile
-// counter; the warp of the tile's first chunk becomes its owner (queued; the
-// warp waits only when kFusePend owned tiles are still unpublished).
-__device__ __noinline__ void fuse_chunk_end(const ConfArgs& a, FusePend* fp, int64_t c, unsigned cdef,
-                                            int64_t rows, int CR, float thr) {
-  const int lane = threadIdx.x & 31;
-  const int64_t sc = fuse_tile_chunks(rows, CR);
-  const int64_t c0 = c * CR;
-  const unsigned crow = (unsigned)(rows - c0 < CR ? rows - c0 : CR);
-  __syncwarp();                                    // both groups' row outputs before the release
-#ifdef HS_FZ_TRACE
-  if (lane == 0) atomicMax(&g_fz_trace[5], fz_now());
-#endif
-#ifdef HS_EXP_FZ_RELAXED
-  if (lane == 0) atomicAdd(&fuse_tiles(a.fz.tiles).acc[c / sc], ((unsigned long long)crow << 32) | cdef);
-#else
-  if (lane == 0)
-    red_add_release(&fuse_tiles(a.fz.tiles).acc[c / sc], ((unsigned long long)crow << 32) | cdef);
-#endif
-#ifdef HS_EXP_FZ_NOSCATTER
-  return;
-#endif
-  fuse_try_pending(a, fp, rows, CR, thr, false);
-  if (c % sc == 0) {
-    if (fp->count == kFusePend) {                  // rare: wait for the oldest
-      fuse_try_pending(a, fp, rows, CR, thr, true);
-    }
-    if (lane == 0) {
-      fp->tile[(fp->head + fp->count) % kFusePend] = (int)(c / sc);
-      fp->count += 1;
-    }
-    __syncwarp();
+  // block exclusive scan of the per-thread sums (warp scans + warp totals)
+  unsigned inc = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned y = __shfl_up_sync(0xFFFFFFFFu, inc, o);
+    if (lane >= o) inc += y;
+  }
+  unsigned* wtot = spre + kFuseTiles;
+  if (lane == 31) wtot[warp] = inc;
+  __syncthreads();
+  unsigned wbase = 0;
+  for (int w = 0; w < warp; ++w) wbase += wtot[w];
+  unsigned run = wbase + inc - sum;
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    spre[tid * PER + q] = run;
+    run += v[q];
+  }
+  __syncthreads();
+  const int64_t nwarps = ((int64_t)gridDim.x * nthr) >> 5;
+  const int64_t gw = ((int64_t)blockIdx.x * nthr + tid) >> 5;
+  for (int64_t j = gw; j < NT; j += nwarps) fuse_scatter_tile(a, j, R, rows, (long long)spre[j], thr);
+  if (blockIdx.x == 0 && tid == 0) {
+    unsigned total = 0;
+    for (int w = 0; w < nthr / 32; ++w) total += wtot[w];
+    a.fz.counts[0] = rows - (long long)total;
+    a.fz.counts[1] = (long long)total;
+    *(volatile unsigned*)t.epoch = epoch + 1u;     // every CTA read it before the barrier
   }
 }
 
@@ -1116,7 +958,7 @@ constexpr int async_smem_bytes() { return (kAsyncThreads / 32) * 2 * (32 / G) * 
 // epilogue (a.fz; requires DYN and no late wait).
 template <bool BF16, bool ENTROPY, int NV, int G, bool FULL, bool DYN, bool RIDX, bool FUSE>
 __global__ void __launch_bounds__(kAsyncThreads, 3) conf_async_kernel(const __grid_constant__ ConfArgs a) {
-  static_assert(!FUSE || DYN, "the fused compaction needs rows claimed in order");
+  static_assert(!(FUSE && DYN), "the fused compaction uses the static row assignment");
   if (a.late_wait) pdl_trigger(); else pdl_start();
   extern __shared__ __align__(16) unsigned char smem[];
   constexpr int RPW = 32 / G;
@@ -1147,8 +989,27 @@ __global__ void __launch_bounds__(kAsyncThreads, 3) conf_async_kernel(const __gr
   auto claim = [&]() {
     if (lane == 0) cpre = atomicAdd(a.ticket, (unsigned)kChunk);
   };
+  // fused: warps take blocks of 2^bsh consecutive row groups, strided (one
+  // tile-counter reduction per block; small batches use smaller blocks)
+  int bsh = 0;
+  if constexpr (FUSE) {
+    const int64_t lr = live_rows(a);
+    const int64_t per = ((lr + RPW - 1) / RPW) / (4 * nwarps);
+    bsh = per >= 8 ? 3 : per >= 4 ? 2 : per >= 2 ? 1 : 0;
+    const int ts = fuse_tshift(lr, RPW);    // a block never straddles two tiles
+    if (bsh > ts) bsh = ts;
+#ifndef HS_FZ_BLOCKS
+    bsh = 0;                                // A/B: blocks of consecutive groups were slower
+#endif
+  }
   auto next_group = [&](int64_t g) -> int64_t {
-    if (!dyn) return g + nwarps;
+    if (!dyn) {
+      if constexpr (FUSE) {
+        const int64_t B = int64_t(1) << bsh;
+        return ((g + 1) & (B - 1)) ? g + 1 : g + 1 + (nwarps - 1) * B;
+      }
+      return g + nwarps;
+    }
     if (cnext == cend) {
       cnext = (int64_t)__shfl_sync(0xFFFFFFFFu, cpre, 0);
       cend = cnext + kChunk;
@@ -1156,32 +1017,23 @@ __global__ void __launch_bounds__(kAsyncThreads, 3) conf_async_kernel(const __gr
     if (cnext == cend - 1) claim();
     return cnext++;
   };
-  // fused compaction: warp 0 of CTA 0 is the sequencer and claims no rows
-  const bool seq = FUSE && blockIdx.x == 0 && warp == 0;
-  if (dyn && !seq) claim();
-  const int64_t g0 = seq ? (int64_t(1) << 56) / RPW
-                         : dyn ? next_group(0) : ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (dyn) claim();
+  const int64_t g0 = dyn ? next_group(0) : (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) << bsh;
   const int64_t fA = fetch_index_t<RIDX>(a, g0 * RPW + grp < cap ? g0 * RPW + grp : 0);
   const int64_t rows = live_rows(a);
-  // fused compaction: the chunk's deferred rows (registers); the warp's pending
-  // tile in shared memory
-  constexpr int CR = kChunk * RPW;                    // rows per claimed chunk
+  // fused compaction: tiles of 2^tsh row groups, counters in bank epoch & 1
   float thr = 0.f;
-  unsigned cdef = 0;
-  __shared__ FusePend s_pend[FUSE ? kAsyncThreads / 32 : 1];
-  FusePend* fp = &s_pend[FUSE ? warp : 0];
+  int tsh = 0;
+  unsigned epoch = 0, cdef = 0;
+  unsigned* tacc = nullptr;
   if constexpr (FUSE) {
     thr = a.fz.d_threshold ? *a.fz.d_threshold : a.fz.threshold;
-    if (lane == 0) {
-      fp->head = 0;
-      fp->count = 0;
-      fp->epoch = *(volatile unsigned*)fuse_tiles(a.fz.tiles).epoch;
-#ifdef HS_FZ_TRACE
-      atomicMin(&g_fz_trace[0], fz_now());
-      atomicAdd(&g_fz_trace[4], 1ull);
-#endif
-    }
-    __syncwarp();
+    tsh = fuse_tshift(rows, RPW);
+    const FuseTiles t = fuse_tiles(a.fz.tiles);
+    epoch = *(volatile unsigned*)t.epoch;
+    tacc = t.acc + (epoch & 1u) * kFuseTiles;
+    if (blockIdx.x == 0)                       // the next launch's bank
+      for (int j = threadIdx.x; j < kFuseTiles; j += blockDim.x) t.acc[((epoch + 1u) & 1u) * kFuseTiles + j] = 0u;
   }
   if (g0 * RPW < rows) {
     // lane gl's vector k of stage st sits at base + st*STAGEB + grp*ROWB + k*G*16 + gl*16:
@@ -1232,10 +1084,11 @@ __global__ void __launch_bounds__(kAsyncThreads, 3) conf_async_kernel(const __gr
       if (a.tail) group_mask_tail<BF16, NV, G>(A, gl, nvec, a.tail);
       const float crA = group_reduce_row<BF16, ENTROPY, NV, G>(a, A, actA, rowA, gl, cA, pA, labA);
       if constexpr (FUSE) {
-        // D3 per row (accept iff c >= t, NaN defers; the last stage accepts all)
+        // D3 per row (accept iff c >= t, NaN defers; the last stage accepts
+        // all): the group's deferred rows go to its tile's counter
         cdef += (unsigned)__popc(__ballot_sync(0xFFFFFFFFu, actA && gl == 0 && !(a.fz.is_last || crA >= thr)));
-        if (((gA + 1) & (kChunk - 1)) == 0 || !anyB) {
-          fuse_chunk_end(a, fp, gA >> kShift, cdef, rows, CR, thr);
+        if ((((gA + 1) >> bsh) << bsh) == gA + 1 || !anyB) {     // end of the warp's block
+          if (lane == 0 && cdef) atomicAdd(tacc + (gA >> tsh), cdef);
           cdef = 0;
         }
       }
@@ -1250,13 +1103,13 @@ __global__ void __launch_bounds__(kAsyncThreads, 3) conf_async_kernel(const __gr
       fB = fC;
     }
     cp_async_wait<0>();
-#ifndef HS_EXP_FZ_NOSCATTER
-    if constexpr (FUSE) fuse_try_pending(a, fp, rows, CR, thr, true);
-#endif
   }
   if constexpr (FUSE) {
-#ifndef HS_EXP_FZ_NOSEQ
-    if (seq) fuse_sequencer(a, rows, CR, fp->epoch);
+#ifndef HS_EXP_FZ_NOSYNC
+    cooperative_groups::this_grid().sync();    // every row's confidence, argmax and count
+#ifndef HS_EXP_FZ_NOFINISH
+    fuse_finish(a, rows, RPW, epoch, thr, reinterpret_cast<unsigned*>(smem));
+#endif
 #endif
   }
   if (dyn) {
@@ -1881,6 +1734,25 @@ cudaError_t launch_async_d(const ConfArgs& a, int64_t rows, cudaStream_t s) {
   const int64_t want = (rows + RPB - 1) / RPB;
   const int64_t cap = (int64_t)num_sms() * occ;
   const int grid = (int)(want < cap ? (want > 0 ? want : 1) : cap);
+  if constexpr (FUSE) {
+    // cooperative (one grid barrier; every CTA resident) + programmatic
+    // dependent launch; the grid never exceeds one wave
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kAsyncThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_enabled() ? 2 : 1;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, k, a);
+    count_launch();
+    return e != cudaSuccess ? e : cudaGetLastError();
+  }
   return launch_pdl(k, dim3(grid), dim3(kAsyncThreads), smem, s, a);
 }
 
@@ -1892,11 +1764,11 @@ cudaError_t launch_async_l(const ConfArgs& a, int64_t rows, cudaStream_t s) {
   if (a.row_index)
 #endif
   {
-    if (a.fz.on) return launch_async_d<BF16, ENTROPY, NV, G, FULL, true, true, true>(a, rows, s);
+    if (a.fz.on) return launch_async_d<BF16, ENTROPY, NV, G, FULL, false, true, true>(a, rows, s);
     return a.ticket ? launch_async_d<BF16, ENTROPY, NV, G, FULL, true, true>(a, rows, s)
                     : launch_async_d<BF16, ENTROPY, NV, G, FULL, false, true>(a, rows, s);
   }
-  if (a.fz.on) return launch_async_d<BF16, ENTROPY, NV, G, FULL, true, false, true>(a, rows, s);
+  if (a.fz.on) return launch_async_d<BF16, ENTROPY, NV, G, FULL, false, false, true>(a, rows, s);
   return a.ticket ? launch_async_d<BF16, ENTROPY, NV, G, FULL, true, false>(a, rows, s)
                   : launch_async_d<BF16, ENTROPY, NV, G, FULL, false, false>(a, rows, s);
 }
@@ -2035,18 +1907,6 @@ cudaError_t dispatch(const ConfArgs& a, int64_t rows, cudaStream_t s) {
 }
 
 }  // namespace
-
-#ifdef HS_FZ_TRACE
-}  // namespace hs
-extern "C" int hs_fz_trace(unsigned long long* host8, int reset) {
-  unsigned long long z[8] = {~0ull, 0, 0, 0, 0, 0, 0, 0};
-  cudaDeviceSynchronize();
-  if (host8 && cudaMemcpyFromSymbol(host8, hs::g_fz_trace, sizeof(z)) != cudaSuccess) return 1;
-  if (reset && cudaMemcpyToSymbol(hs::g_fz_trace, z, sizeof(z)) != cudaSuccess) return 1;
-  return 0;
-}
-namespace hs {
-#endif
 
 bool confidence_fusable(const ConfArgs& a) {
   // the dispatch below: rows of <= 128 x 16 B take the cp.async kernel (K1a)

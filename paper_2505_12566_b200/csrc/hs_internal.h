@@ -39,12 +39,10 @@ cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t s
 
 // ---- K1 / K2 ---------------------------------------------------------------
 constexpr int kMaxBatch = 8;
-// K1 with the stage's threshold test and stable compaction (K3) fused into its
-// row epilogue (hs_cascade_step, single-token rows on the cp.async kernel).
-// Rows are cut into at most kFuseTiles contiguous tiles of whole claimed
-// chunks; the warp whose chunk completes a tile publishes the tile's deferred
-// count, looks back over the tile descriptors for its exclusive prefix and
-// scatters the tile's accepted / deferred lists.
+// K1 with the stage's threshold test and stable compaction (K3) fused into it
+// (hs_cascade_step with HS_FUSE=1, single-token rows on the cp.async kernel):
+// per-tile deferred counters while the rows stream, one grid barrier, then the
+// prefixes and the lists (conf.cu).
 constexpr int kFuseTiles = 1024;
 struct FuseArgs {
   int on;                         // 0: plain K1
@@ -58,9 +56,9 @@ struct FuseArgs {
   int64_t* def_ids;               // deferred: id (the next stage's batch), stable order
   int64_t* def_pos;               // deferred: row position (payload gather), or NULL
   int64_t* counts;                // {n_acc, n_def}
-  void* tiles;                    // fuse_ws_bytes(): header, descriptors, tile counters
+  void* tiles;                    // fuse_ws_bytes(): epoch, two banks of tile counters
 };
-constexpr size_t fuse_ws_bytes() { return 32 + (size_t)kFuseTiles * 16; }
+constexpr size_t fuse_ws_bytes() { return 32 + (size_t)kFuseTiles * 8; }
 struct ConfArgs {
   const void* logits;
   int64_t row_bytes;       // row_stride * element size (multiple of 16)

@@ -9,7 +9,8 @@ stage's batch), the payload gather and the counts -- must agree bit
 for bit, at tile edges (1, 15, 16, 17 rows; tiles of up to 1,024 chunks), with
 device-resident counts and thresholds, gathered rows, NaN rows, thresholds 0 /
 1 / +inf, the last stage, and over repeated launches on one workspace (the
-tile descriptors are epoch-tagged, the tile counters re-armed in-kernel)."""
+tile counters alternate between two banks by launch epoch; each launch zeroes
+the bank of the next)."""
 import numpy as np
 import pytest
 import torch
@@ -119,8 +120,7 @@ def test_fused_row_index_entropy(hs, monkeypatch):
 
 def test_fused_repeated_launches_one_workspace(hs, monkeypatch):
     """Many launches of different sizes and thresholds on one workspace (tile
-    descriptors epoch-tagged, tile counters re-armed by the completing warp),
-    eagerly and from a CUDA graph."""
+    counter banks alternating by epoch), eagerly and from a CUDA graph."""
     C, cap = 1000, 200000
     x = rand_logits(cap, C, "bf16", seed=11)
     ws = hs.workspace(hs.lib().hs_cascade_step_workspace(cap, 1), dev())

@@ -25,10 +25,8 @@ VARIANTS = {
     "topkm8": ["HS_TOPK_MERGE_AT=8"],
     "topkm4s40": ["HS_TOPK_MERGE_AT=4", "HS_TOPK_SLACK=40"],   # + 40 more buffered slots per lane
     "topkm8s40": ["HS_TOPK_MERGE_AT=8", "HS_TOPK_SLACK=40"],
-    "fztrace": ["HS_FZ_TRACE"],
-    "fznoscat": ["HS_EXP_FZ_NOSCATTER"],                  # fused step: no owner scatter (timing)
-    "fznoseq": ["HS_EXP_FZ_NOSCATTER", "HS_EXP_FZ_NOSEQ"],   # ... nor the sequencer
-    "fzrelax": ["HS_EXP_FZ_NOSCATTER", "HS_EXP_FZ_NOSEQ", "HS_EXP_FZ_RELAXED"],   # ... relaxed counter adds                           # fused step: globaltimer trace (tools/fz_trace.py)
+    "fznofin": ["HS_EXP_FZ_NOFINISH"],   # fused step timing bounds: grid barrier, no lists ...
+    "fznosync": ["HS_EXP_FZ_NOSYNC"],    # ... no barrier either (K1 + tile counters only)
 }
 
 if __name__ == "__main__":

@@ -10,9 +10,3 @@ for f in sorted(glob.glob(f"gpurun_out/{tag}_sc_*.txt")):
         print(f.split("_sc_")[1][:-4], {k: v for k, v in d.items() if k.startswith(("step", "k1", "full", "routing"))})
     except Exception as e:
         print(f, e)
-try:
-    t = json.load(open(f"gpurun_out/{tag}_fz_trace.txt"))
-    for k, v in t.items():
-        print(k, v)
-except Exception as e:
-    print("trace", e)
