@@ -960,6 +960,29 @@ static hs_status_t step_common_checks(int32_t stage, int32_t n_stages, int64_t n
   return HS_OK;
 }
 
+// The last stage's step without a compaction (HS_LAST_K3=1 restores it): it
+// accepts every row in order, so K1 writes the accepted lists itself.
+static bool last_direct_enabled() {
+  const char* e = getenv("HS_LAST_K3");
+  return !(e && e[0] == '1');
+}
+
+struct LastOut {                    // the last stage written by K1 (NULL: K1's own buffers)
+  float* conf;
+  int32_t* pred;
+  const int64_t* ids;
+  int64_t* ids_out;
+  int64_t* counts;
+};
+
+static hs_status_t cascade_confidence_impl(int32_t stage, int32_t n_stages, const void* logits, hs_dtype_t dtype,
+                                           int64_t n, int32_t seq_len, int64_t n_classes, int64_t row_stride,
+                                           const int64_t* row_index, const int64_t* d_n, float temperature,
+                                           hs_conf_kind_t kind, hs_seq_reduce_t reduce, float threshold,
+                                           const float* d_threshold, uint64_t* d_defer_count, void* ws,
+                                           size_t ws_bytes, uint32_t* d_status, int32_t top_k, uint32_t flags,
+                                           hs_stream_t stream, const LastOut* last);
+
 hs_status_t hs_cascade_confidence(int32_t stage, int32_t n_stages, const void* logits, hs_dtype_t dtype,
                                   int64_t n, int32_t seq_len, int64_t n_classes, int64_t row_stride,
                                   const int64_t* row_index, const int64_t* d_n, float temperature,
@@ -967,6 +990,18 @@ hs_status_t hs_cascade_confidence(int32_t stage, int32_t n_stages, const void* l
                                   const float* d_threshold, uint64_t* d_defer_count, void* ws,
                                   size_t ws_bytes, uint32_t* d_status, int32_t top_k, uint32_t flags,
                                   hs_stream_t stream) {
+  return cascade_confidence_impl(stage, n_stages, logits, dtype, n, seq_len, n_classes, row_stride, row_index, d_n,
+                                 temperature, kind, reduce, threshold, d_threshold, d_defer_count, ws, ws_bytes,
+                                 d_status, top_k, flags, stream, nullptr);
+}
+
+static hs_status_t cascade_confidence_impl(int32_t stage, int32_t n_stages, const void* logits, hs_dtype_t dtype,
+                                           int64_t n, int32_t seq_len, int64_t n_classes, int64_t row_stride,
+                                           const int64_t* row_index, const int64_t* d_n, float temperature,
+                                           hs_conf_kind_t kind, hs_seq_reduce_t reduce, float threshold,
+                                           const float* d_threshold, uint64_t* d_defer_count, void* ws,
+                                           size_t ws_bytes, uint32_t* d_status, int32_t top_k, uint32_t flags,
+                                           hs_stream_t stream, const LastOut* last) {
   if (flags & ~(uint32_t)HS_STEP_OVERLAP_PREVIOUS)
     return fail(HS_ERR_INVALID_ARGUMENT, "unknown flags 0x%x", flags);
   hs_status_t st = step_common_checks(stage, n_stages, n, threshold, d_threshold, top_k);
@@ -989,6 +1024,13 @@ hs_status_t hs_cascade_confidence(int32_t stage, int32_t n_stages, const void* l
     // CTAs that start late (SMs held by the previous kernel) take fewer rows
     a.ticket = reinterpret_cast<unsigned int*>(w + o_tick);
     a.late_wait = 1;
+  }
+  if (last) {
+    if (last->conf) conf = last->conf;
+    if (last->pred) am = last->pred;
+    a.last_ids = last->ids;
+    a.last_ids_out = last->ids_out;
+    a.last_counts = last->counts;
   }
   st = run_confidence_args(a, dtype, reduce, conf, am, nullptr, nullptr, w + o_cws, d_status, s);
   if (st != HS_OK || !d_defer_count) return st;
@@ -1040,6 +1082,16 @@ hs_status_t hs_cascade_step_ex(int32_t stage, int32_t n_stages, const void* logi
   if (next_payload && (!payload || payload_row_bytes <= 0 || (payload_row_bytes & 15) ||
                        !aligned16(payload) || !aligned16(next_payload)))
     return fail(HS_ERR_INVALID_ARGUMENT, "payload rows must be 16-byte aligned multiples of 16 bytes");
+  // the last stage accepts every row in order: K1 writes the accepted lists
+  // and the counts itself (one launch, no compaction)
+  if (stage == n_stages - 1 && seq_len == 1 && last_direct_enabled()) {
+    if (n == 0) return cuda_check(cudaMemsetAsync(d_counts, 0, 2 * sizeof(int64_t), (cudaStream_t)stream),
+                                  "memset counts");
+    const LastOut last{acc_conf, acc_pred, ids, acc_ids, d_counts};
+    return cascade_confidence_impl(stage, n_stages, logits, dtype, n, seq_len, n_classes, row_stride, row_index,
+                                   d_n, temperature, kind, reduce, threshold, d_threshold, nullptr, ws, ws_bytes,
+                                   d_status, top_k, flags, stream, &last);
+  }
   // HS_FUSE=1: one launch, K1 with the threshold test and the stable
   // compaction in its row epilogue, when the rows take the cp.async kernel
   if (!(flags & HS_STEP_OVERLAP_PREVIOUS) && fuse_enabled()) {

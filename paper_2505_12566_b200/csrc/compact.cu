@@ -257,53 +257,60 @@ __global__ void __launch_bounds__(T) route_compact_fast_kernel(const CompactArgs
   CompactWs* ws = reinterpret_cast<CompactWs*>(a.ws);
   unsigned long long* st = tile_status(a.ws);
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int64_t tile = draw_tile(ws);
-  const int64_t base = tile * TILE;
-  const int64_t i0 = base + (int64_t)tid * I;
   const bool pred1 = a.acc_pred && a.pred_len == 1;
   // The item loads are issued speculatively within the capacity a.n (the
   // buffers are capacity-sized) together with the device count and threshold,
   // so the tile's data and *d_n arrive after one memory latency, not two.
+  // They are issued for tile blockIdx.x while the ticket is drawn (the CTAs
+  // nearly always start, and so draw, in blockIdx order); a CTA that draws
+  // another tile reloads.
   const int64_t ncap = a.n;
   float cv[I];
   int64_t idv[I];
   int32_t pv[I];
-  if (vec && i0 + I <= ncap) {
-    const float4* c4 = reinterpret_cast<const float4*>(a.conf + i0);
-    const float4 x0 = __ldg(c4), x1 = __ldg(c4 + 1);
-    cv[0] = x0.x; cv[1] = x0.y; cv[2] = x0.z; cv[3] = x0.w;
-    cv[4] = x1.x; cv[5] = x1.y; cv[6] = x1.z; cv[7] = x1.w;
-    if (a.ids) {
-      const longlong2* q = reinterpret_cast<const longlong2*>(a.ids + i0);
+  auto load = [&](int64_t i0) {
+    if (vec && i0 + I <= ncap) {
+      const float4* c4 = reinterpret_cast<const float4*>(a.conf + i0);
+      const float4 x0 = __ldg(c4), x1 = __ldg(c4 + 1);
+      cv[0] = x0.x; cv[1] = x0.y; cv[2] = x0.z; cv[3] = x0.w;
+      cv[4] = x1.x; cv[5] = x1.y; cv[6] = x1.z; cv[7] = x1.w;
+      if (a.ids) {
+        const longlong2* q = reinterpret_cast<const longlong2*>(a.ids + i0);
 #pragma unroll
-      for (int j = 0; j < I / 2; ++j) {
-        const longlong2 y = __ldg(q + j);
-        idv[2 * j] = y.x;
-        idv[2 * j + 1] = y.y;
+        for (int j = 0; j < I / 2; ++j) {
+          const longlong2 y = __ldg(q + j);
+          idv[2 * j] = y.x;
+          idv[2 * j + 1] = y.y;
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < I; ++j) idv[j] = i0 + j;
+      }
+      if (pred1) {
+        const int4* q = reinterpret_cast<const int4*>(a.pred + i0);
+        const int4 p0 = __ldg(q), p1 = __ldg(q + 1);
+        pv[0] = p0.x; pv[1] = p0.y; pv[2] = p0.z; pv[3] = p0.w;
+        pv[4] = p1.x; pv[5] = p1.y; pv[6] = p1.z; pv[7] = p1.w;
+      } else {
+#pragma unroll
+        for (int j = 0; j < I; ++j) pv[j] = 0;
       }
     } else {
 #pragma unroll
-      for (int j = 0; j < I; ++j) idv[j] = i0 + j;
+      for (int j = 0; j < I; ++j) {
+        const int64_t i = i0 + j;
+        const bool in = i < ncap;
+        cv[j] = in ? __ldg(a.conf + i) : 0.f;
+        idv[j] = (in && a.ids) ? __ldg(a.ids + i) : i;
+        pv[j] = (in && pred1) ? __ldg(a.pred + i) : 0;
+      }
     }
-    if (pred1) {
-      const int4* q = reinterpret_cast<const int4*>(a.pred + i0);
-      const int4 p0 = __ldg(q), p1 = __ldg(q + 1);
-      pv[0] = p0.x; pv[1] = p0.y; pv[2] = p0.z; pv[3] = p0.w;
-      pv[4] = p1.x; pv[5] = p1.y; pv[6] = p1.z; pv[7] = p1.w;
-    } else {
-#pragma unroll
-      for (int j = 0; j < I; ++j) pv[j] = 0;
-    }
-  } else {
-#pragma unroll
-    for (int j = 0; j < I; ++j) {
-      const int64_t i = i0 + j;
-      const bool in = i < ncap;
-      cv[j] = in ? __ldg(a.conf + i) : 0.f;
-      idv[j] = (in && a.ids) ? __ldg(a.ids + i) : i;
-      pv[j] = (in && pred1) ? __ldg(a.pred + i) : 0;
-    }
-  }
+  };
+  load((int64_t)blockIdx.x * TILE + (int64_t)tid * I);
+  const int64_t tile = draw_tile(ws);
+  const int64_t base = tile * TILE;
+  const int64_t i0 = base + (int64_t)tid * I;
+  if (tile != (int64_t)blockIdx.x) load(i0);          // block-uniform, rare
   int64_t n = ncap;
   if (a.d_n) n = min(*a.d_n, ncap);
   const float thr = a.d_threshold ? *a.d_threshold : a.threshold;

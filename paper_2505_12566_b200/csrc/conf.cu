@@ -71,6 +71,7 @@ __device__ __forceinline__ float write_row(const ConfArgs& a, int64_t row, int32
   if (a.conf2) a.conf2[row] = bad ? __int_as_float(0x7FC00000) : exp2f(r.w / r.s - log2f(r.s));
   if (a.argmax) a.argmax[row] = am;
   if (a.ok) a.ok[row] = (uint8_t)(a.labels ? (!bad && lab == am) : 0);
+  if (a.last_ids_out) a.last_ids_out[row] = a.last_ids ? a.last_ids[row] : row;
   return c;
 }
 
@@ -82,6 +83,14 @@ __device__ __forceinline__ int64_t live_rows(const ConfArgs& a) {
     n = dn < n ? dn : n;
   }
   return n * a.L * (int64_t)a.nbatch;
+}
+
+// last stage (ConfArgs::last_counts): every live row is accepted
+__device__ __forceinline__ void write_last_counts(const ConfArgs& a) {
+  if (a.last_counts && blockIdx.x == 0 && threadIdx.x == 0) {
+    a.last_counts[0] = live_rows(a);
+    a.last_counts[1] = 0;
+  }
 }
 
 __device__ __forceinline__ uint32_t word(const uint4& v, int q) {
@@ -491,6 +500,7 @@ __device__ __forceinline__ void group_load_row(uint4 (&v)[NV], const uint4* p, i
 template <bool BF16, bool ENTROPY, int NV, int G, bool FULL>
 __global__ void __launch_bounds__(256, (NV <= 8 ? 2 : 1)) conf_warp_kernel(const ConfArgs a) {
   pdl_start();
+  write_last_counts(a);
   constexpr int RPW = 32 / G;      // rows per warp
   const int lane = threadIdx.x & 31, gl = lane % G, grp = lane / G;
   const int64_t stride = (((int64_t)gridDim.x * blockDim.x) >> 5) * RPW;
@@ -612,6 +622,7 @@ __device__ __noinline__ float topk_merge(float lst, float* col, int pn, int K, i
 template <bool BF16, bool ENTROPY>
 __global__ void __launch_bounds__(256, kTopkU <= 4 ? 3 : 2) conf_topk_kernel(const ConfArgs a) {
   pdl_start();
+  write_last_counts(a);
   constexpr int VE = BF16 ? 8 : 4, U = kTopkU;
   extern __shared__ __align__(16) float s_col[];          // [8 warps][kTopkPB][32 lanes]
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -960,6 +971,7 @@ template <bool BF16, bool ENTROPY, int NV, int G, bool FULL, bool DYN, bool RIDX
 __global__ void __launch_bounds__(kAsyncThreads, 3) conf_async_kernel(const __grid_constant__ ConfArgs a) {
   static_assert(!(FUSE && DYN), "the fused compaction uses the static row assignment");
   if (a.late_wait) pdl_trigger(); else pdl_start();
+  if (!a.late_wait) write_last_counts(a);
   extern __shared__ __align__(16) unsigned char smem[];
   constexpr int RPW = 32 / G;
   constexpr uint32_t ROWB = G * NV * 16;              // one group's row slot
@@ -1127,7 +1139,10 @@ __global__ void __launch_bounds__(kAsyncThreads, 3) conf_async_kernel(const __gr
       }
     }
   }
-  if (a.late_wait) pdl_wait();       // completes only after the previous kernel
+  if (a.late_wait) {
+    pdl_wait();                      // completes only after the previous kernel
+    write_last_counts(a);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -1148,6 +1163,7 @@ struct TmaRing {
 template <bool BF16, bool ENTROPY, int NV, int G, int NCW, int S, bool L1>
 __global__ void __launch_bounds__(32 * (NCW + 1), 1) conf_tma_kernel(const ConfArgs a, int dense) {
   pdl_start();
+  write_last_counts(a);
   extern __shared__ __align__(128) unsigned char smem[];
   constexpr int RPW = 32 / G;
   constexpr int RPS = NCW * RPW;          // rows per stage
@@ -1266,6 +1282,7 @@ __device__ __forceinline__ void cta_load_chunk(uint4 (&v)[NV], const uint4* p, i
 template <bool BF16, bool ENTROPY, int NT, int NV>
 __global__ void __launch_bounds__(NT) conf_cta_kernel(const ConfArgs a) {
   pdl_start();
+  write_last_counts(a);
   constexpr int NW = NT / 32;
   constexpr int VE = BF16 ? 8 : 4;
   constexpr int CH = NT * NV;                  // vectors per chunk
@@ -1405,6 +1422,7 @@ __global__ void __launch_bounds__(NT) conf_cta_kernel(const ConfArgs a) {
 template <bool BF16, bool ENTROPY, int NV>
 __global__ void __launch_bounds__(256, 2) conf_stream_kernel(const ConfArgs a) {
   pdl_start();
+  write_last_counts(a);
   constexpr int VE = BF16 ? 8 : 4;
   constexpr int CH = 32 * NV;                  // vectors per chunk
   const int lane = threadIdx.x & 31;
@@ -1555,6 +1573,7 @@ template <bool BF16, bool ENTROPY, int NV>
 __global__ void __launch_bounds__(256) conf_split_kernel(const ConfArgs a, int nseg, int segch,
                                                          SplitPart* parts, unsigned* arrive) {
   pdl_start();
+  write_last_counts(a);
   constexpr int VE = BF16 ? 8 : 4;
   constexpr int CH = 32 * NV;
   const int lane = threadIdx.x & 31;

@@ -101,6 +101,13 @@ struct ConfArgs {
   float* conf2;
   // K1+K3 fused (async kernel with a ticket, L = 1, nbatch = 1, no late wait)
   FuseArgs fz;
+  // the LAST stage of a cascade (it accepts every row, so its compaction is the
+  // identity): K1 writes conf / argmax straight into the accepted lists, copies
+  // the ids (NULL: the row) into last_ids_out and writes {live rows, 0} into
+  // last_counts -- no K3 launch (hs_cascade_step, L = 1)
+  const int64_t* last_ids;
+  int64_t* last_ids_out;
+  int64_t* last_counts;
 };
 // true when launch_confidence(a) takes the cp.async kernel, which is the one
 // that can run the fused threshold test + compaction

@@ -188,3 +188,49 @@ def test_fused_cascade_vs_oracle_production_shape(hs, monkeypatch):
         got = res[k]["ids"].numpy()
         want = lists[k][1]
         assert np.array_equal(got[~near[got]], want[~near[want]])
+
+
+# ---------------------------------------------------------------------------
+# The last stage without a compaction: it accepts every row in order, so K1
+# writes the accepted lists and the counts itself (HS_LAST_K3=1: K1 then K3)
+# ---------------------------------------------------------------------------
+def last_step(hs, monkeypatch, direct, x, *, n=None, ids=None, d_n=None, row_index=None, top_k=0, kind="maxprob"):
+    monkeypatch.setenv("HS_LAST_K3", "0" if direct else "1")
+    n = x.shape[0] if n is None else n
+    status = torch.zeros(1, dtype=torch.int32, device=dev())
+    out = hs.cascade_step(2, 3, x, 0.5, n=n, ids=ids, d_n=d_n, row_index=row_index, status=status,
+                          kind=kind, top_k=top_k, temperature=1.3)
+    torch.cuda.synchronize()
+    return out
+
+
+@pytest.mark.parametrize("C,dtype,n", [(1000, "bf16", 70001), (1000, "f32", 4097), (64, "bf16", 17),
+                                       (32128, "bf16", 300), (128256, "bf16", 40), (2000, "f32", 1)])
+def test_last_stage_direct_equals_compaction(hs, monkeypatch, C, dtype, n):
+    """Every K1 path (cp.async rows, register rows, warp per vocabulary row,
+    split rows for small batches): the same accepted lists and counts as K1
+    then K3, with ids given or the identity, a device count (also 0), gathered
+    rows, and the entropy kind."""
+    x = rand_logits(n, C, dtype, seed=C + n, nan_rows=2)
+    cap = n
+    g = torch.Generator().manual_seed(n)
+    ids = torch.randperm(5 * cap, generator=g)[:cap].to(torch.int64).to(dev())
+    for kw in ({}, {"ids": ids}, {"ids": ids, "row_index": torch.arange(n - 1, -1, -1, device=dev())},
+               {"kind": "entropy"}):
+        a = last_step(hs, monkeypatch, True, x, **kw)
+        b = last_step(hs, monkeypatch, False, x, **kw)
+        assert_same(a, b)
+        assert a["counts"].cpu().tolist() == [n, 0]
+    for live in (n // 2, 0):
+        d_n = torch.tensor([live], dtype=torch.int64, device=dev())
+        a = last_step(hs, monkeypatch, True, x, n=cap, ids=ids, d_n=d_n)
+        b = last_step(hs, monkeypatch, False, x, n=cap, ids=ids, d_n=d_n)
+        assert_same(a, b)
+        assert a["counts"].cpu().tolist() == [live, 0]
+
+
+def test_last_stage_direct_topk(hs, monkeypatch):
+    x = rand_logits(3000, 32128, "bf16", seed=5)
+    a = last_step(hs, monkeypatch, True, x, top_k=10)
+    b = last_step(hs, monkeypatch, False, x, top_k=10)
+    assert_same(a, b)
