@@ -316,7 +316,15 @@ def dense_stage_logits(fam, router, route, val, labels, payload, rank, dev, ids0
             ids = router.cascade.outs[k - 1]["next_ids"][:nk].clone()
             if ids0 is None:
                 ids += rank * fam.n
-        x = torch.empty(max(nk, 1) * fam.L, fam.C, dtype=tdt, device=dev)
+        # the live rows are a view of a capacity-sized buffer (what a graph-
+        # captured model stage writes into), so the confidence kernel may read
+        # dense rows before the live count is known (HS_STEP_LOGITS_CAPACITY);
+        # exact-sized when the capacity buffers would exceed 40 GB (c5s)
+        cap_rows = fam.n * fam.L
+        eb = 2 if fam.dtype == "bf16" else 4
+        full = peer is None and (fam.K - 1) * cap_rows * fam.C * eb <= (40 << 30)
+        buf = torch.empty(cap_rows if full else max(nk, 1) * fam.L, fam.C, dtype=tdt, device=dev)
+        x = buf[: max(nk, 1) * fam.L]
         if nk:
             workload.gpu_logits(x, fam, k, ids=ids, n=nk)
         out[k] = x

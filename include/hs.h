@@ -238,9 +238,16 @@ hs_status_t hs_cascade_step(int32_t stage, int32_t n_stages, const void* logits,
  *   row_index, d_n, ids, payload) nor reads or writes this step's workspace.
  *   Stream order is otherwise preserved: the step's kernels complete after the
  *   previous kernel, and the threshold test waits for it (d_threshold may be
- *   produced by it).  Unknown flag bits -> HS_ERR_INVALID_ARGUMENT.
+ *   produced by it).
+ *   HS_STEP_LOGITS_CAPACITY: `logits` holds all n*seq_len rows (the capacity)
+ *   even when d_n makes fewer of them live, so dense rows below the capacity may
+ *   be read before the live count is known (the first rows' loads then overlap
+ *   the previous libhs kernel's drain).  Without the flag and with d_n, only
+ *   live rows are ever read.  Results are identical either way.
+ *   Unknown flag bits -> HS_ERR_INVALID_ARGUMENT.
  * top_k: the stage's confidence over its top_k logits (hs_confidence_topk). */
 #define HS_STEP_OVERLAP_PREVIOUS 1u
+#define HS_STEP_LOGITS_CAPACITY 2u
 hs_status_t hs_cascade_step_ex(int32_t stage, int32_t n_stages, const void* logits, hs_dtype_t dtype,
                                int64_t n, int32_t seq_len, int64_t n_classes, int64_t row_stride,
                                const int64_t* row_index, const int64_t* d_n, float temperature,

@@ -22,7 +22,21 @@ from ._abi import HsError, lib
 
 MAXPROB, MAXPROB_SQ, ENTROPY = 0, 1, 2
 SEQ_NONE, SEQ_MIN, SEQ_MEAN = 0, 1, 2
-HS_STEP_OVERLAP_PREVIOUS = 1     # hs_cascade_step_ex flag (include/hs.h)
+HS_STEP_OVERLAP_PREVIOUS = 1     # hs_cascade_step_ex flags (include/hs.h)
+HS_STEP_LOGITS_CAPACITY = 2
+
+
+def _rows_capacity_flag(logits: torch.Tensor, rows: int, row_index) -> int:
+    """HS_STEP_LOGITS_CAPACITY when the memory from ``logits``' first row on
+    holds ``rows`` rows of its stride (e.g. a view of the live rows of a
+    capacity-sized buffer), so dense rows below the capacity may be read before
+    the live count is known."""
+    if row_index is not None or logits.dim() != 2:
+        return 0
+    eb = logits.element_size()
+    avail = logits.untyped_storage().nbytes() - logits.storage_offset() * eb
+    need = (rows - 1) * logits.stride(0) * eb + logits.shape[1] * eb if rows > 0 else 0
+    return HS_STEP_LOGITS_CAPACITY if avail >= need else 0
 _KINDS = {"maxprob": MAXPROB, "maxprob_sq": MAXPROB_SQ, "entropy": ENTROPY}
 _REDUCES = {"none": SEQ_NONE, "min": SEQ_MIN, "mean": SEQ_MEAN}
 STATUS_NONFINITE = 1
@@ -517,6 +531,7 @@ def cascade_step(stage: int, n_stages: int, logits: torch.Tensor, threshold, *, 
         ws = workspace(need, dev)
     d_thr = threshold if isinstance(threshold, torch.Tensor) else None
     thr = 0.0 if d_thr is not None else float(threshold)
+    flags = (HS_STEP_OVERLAP_PREVIOUS if overlap_previous else 0) | _rows_capacity_flag(logits, n * seq_len, row_index)
     if peer is not None:
         import ctypes
         dr, nd = _dest_array(next_ranks)
@@ -525,7 +540,7 @@ def cascade_step(stage: int, n_stages: int, logits: torch.Tensor, threshold, *, 
                   float(temperature), _kind(kind), _reduce(reduce), thr, _p(d_thr), _p(ids), _p(payload),
                   int(payload_row_bytes), _p(out["acc_ids"]), _p(out["acc_conf"]), _p(out["acc_pred"]),
                   _p(out["next_ids"]), _p(out.get("next_payload")), _p(out["counts"]), _p(ws),
-                  ws.numel(), _p(status), int(top_k), HS_STEP_OVERLAP_PREVIOUS if overlap_previous else 0,
+                  ws.numel(), _p(status), int(top_k), flags,
                   ctypes.byref(peer), int(peer_set), dr, nd, _p(recv_count), _stream(stream))
         return out
     _abi.call("hs_cascade_step_ex", int(stage), int(n_stages), _p(logits), _dtype_code(logits),
@@ -533,8 +548,7 @@ def cascade_step(stage: int, n_stages: int, logits: torch.Tensor, threshold, *, 
               float(temperature), _kind(kind), _reduce(reduce), thr, _p(d_thr), _p(ids), _p(payload),
               int(payload_row_bytes), _p(out["acc_ids"]), _p(out["acc_conf"]), _p(out["acc_pred"]),
               _p(out["next_ids"]), _p(out.get("next_payload")), _p(out["counts"]), _p(ws),
-              ws.numel(), _p(status), int(top_k), HS_STEP_OVERLAP_PREVIOUS if overlap_previous else 0,
-              _stream(stream))
+              ws.numel(), _p(status), int(top_k), flags, _stream(stream))
     return out
 
 

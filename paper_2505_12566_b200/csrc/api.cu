@@ -1002,7 +1002,7 @@ static hs_status_t cascade_confidence_impl(int32_t stage, int32_t n_stages, cons
                                            const float* d_threshold, uint64_t* d_defer_count, void* ws,
                                            size_t ws_bytes, uint32_t* d_status, int32_t top_k, uint32_t flags,
                                            hs_stream_t stream, const LastOut* last) {
-  if (flags & ~(uint32_t)HS_STEP_OVERLAP_PREVIOUS)
+  if (flags & ~(uint32_t)(HS_STEP_OVERLAP_PREVIOUS | HS_STEP_LOGITS_CAPACITY))
     return fail(HS_ERR_INVALID_ARGUMENT, "unknown flags 0x%x", flags);
   hs_status_t st = step_common_checks(stage, n_stages, n, threshold, d_threshold, top_k);
   if (st != HS_OK) return st;
@@ -1025,6 +1025,7 @@ static hs_status_t cascade_confidence_impl(int32_t stage, int32_t n_stages, cons
     a.ticket = reinterpret_cast<unsigned int*>(w + o_tick);
     a.late_wait = 1;
   }
+  a.rows_cap_valid = (flags & HS_STEP_LOGITS_CAPACITY) ? 1 : 0;
   if (last) {
     if (last->conf) conf = last->conf;
     if (last->pred) am = last->pred;
@@ -1076,6 +1077,8 @@ hs_status_t hs_cascade_step_ex(int32_t stage, int32_t n_stages, const void* logi
                                int64_t* d_counts, void* ws, size_t ws_bytes, uint32_t* d_status,
                                int32_t top_k, uint32_t flags, hs_stream_t stream) {
   // validate both halves before launching either
+  if (flags & ~(uint32_t)(HS_STEP_OVERLAP_PREVIOUS | HS_STEP_LOGITS_CAPACITY))
+    return fail(HS_ERR_INVALID_ARGUMENT, "unknown flags 0x%x", flags);
   hs_status_t st = step_common_checks(stage, n_stages, n, threshold, d_threshold, top_k);
   if (st != HS_OK) return st;
   if (!d_counts) return fail(HS_ERR_INVALID_ARGUMENT, "d_counts is required");
@@ -1104,6 +1107,7 @@ hs_status_t hs_cascade_step_ex(int32_t stage, int32_t n_stages, const void* logi
     hs::ConfArgs a = make_conf_args(logits, dtype, n, seq_len, n_classes, row_stride, row_index, d_n,
                                     temperature, kind);
     a.top_k = top_k;
+    a.rows_cap_valid = (flags & HS_STEP_LOGITS_CAPACITY) ? 1 : 0;
     if (hs::confidence_fusable(a)) {
       cudaStream_t s = (cudaStream_t)stream;
       if (n == 0) return cuda_check(cudaMemsetAsync(d_counts, 0, 2 * sizeof(int64_t), s), "memset counts");

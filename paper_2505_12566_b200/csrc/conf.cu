@@ -970,8 +970,18 @@ constexpr int async_smem_bytes() { return (kAsyncThreads / 32) * 2 * (32 / G) * 
 template <bool BF16, bool ENTROPY, int NV, int G, bool FULL, bool DYN, bool RIDX, bool FUSE>
 __global__ void __launch_bounds__(kAsyncThreads, 3) conf_async_kernel(const __grid_constant__ ConfArgs a) {
   static_assert(!(FUSE && DYN), "the fused compaction uses the static row assignment");
-  if (a.late_wait) pdl_trigger(); else pdl_start();
-  if (!a.late_wait) write_last_counts(a);
+  // EARLY: static rows of a dense batch -- the warp's first row is prefetched
+  // before waiting for the previous kernel (logits are never written by a libhs
+  // kernel; only the live count is, and it is read after the wait), so the
+  // first load's latency overlaps that kernel's drain
+#ifdef HS_AB_NO_EARLY
+  constexpr bool EARLY = false;
+#else
+  constexpr bool EARLY = !DYN && !RIDX;
+#endif
+  const bool early = EARLY && (a.rows_cap_valid || !a.d_n);
+  if (a.late_wait || early) pdl_trigger(); else pdl_start();
+  if (!a.late_wait && !early) write_last_counts(a);
   extern __shared__ __align__(16) unsigned char smem[];
   constexpr int RPW = 32 / G;
   constexpr uint32_t ROWB = G * NV * 16;              // one group's row slot
@@ -1032,6 +1042,32 @@ __global__ void __launch_bounds__(kAsyncThreads, 3) conf_async_kernel(const __gr
   if (dyn) claim();
   const int64_t g0 = dyn ? next_group(0) : (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) << bsh;
   const int64_t fA = fetch_index_t<RIDX>(a, g0 * RPW + grp < cap ? g0 * RPW + grp : 0);
+  // lane gl's vector k of stage st sits at base + st*STAGEB + grp*ROWB + k*G*16 + gl*16:
+  // a quarter-warp reads 128 contiguous bytes (conflict-free LDS.128)
+  const uint32_t sbase = smem_u32(smem) + (uint32_t)warp * 2u * STAGEB + (uint32_t)grp * ROWB +
+                         (uint32_t)gl * 16u;
+  BatchCur cur = cur_init(a);
+  const uint4* pA = nullptr;
+  float cA = 0.f;
+  int32_t labA = 0;
+  auto locate_A = [&](bool actA) {
+    const RowSrc r = locate_cur<RIDX>(a, cur, actA ? g0 * RPW + grp : 0,
+                                      actA ? fA : fetch_index_t<RIDX>(a, 0));
+    pA = reinterpret_cast<const uint4*>(r.base + r.src * a.row_bytes);
+    cA = r.c;
+    labA = fetch_label(a, r);
+  };
+  if constexpr (EARLY) {
+    if (early && !a.late_wait) {
+      if (g0 * RPW < cap) {                          // within the capacity: valid memory
+        locate_A(g0 * RPW + grp < cap);
+        group_prefetch_row<NV, G, FULL>(sbase, pA, gl, nvec);
+      }
+      cp_async_commit();
+      pdl_wait();
+      write_last_counts(a);
+    }
+  }
   const int64_t rows = live_rows(a);
   // fused compaction: tiles of 2^tsh row groups, counters in bank epoch & 1
   float thr = 0.f;
@@ -1048,26 +1084,17 @@ __global__ void __launch_bounds__(kAsyncThreads, 3) conf_async_kernel(const __gr
       for (int j = threadIdx.x; j < kFuseTiles; j += blockDim.x) t.acc[((epoch + 1u) & 1u) * kFuseTiles + j] = 0u;
   }
   if (g0 * RPW < rows) {
-    // lane gl's vector k of stage st sits at base + st*STAGEB + grp*ROWB + k*G*16 + gl*16:
-    // a quarter-warp reads 128 contiguous bytes (conflict-free LDS.128)
-    const uint32_t sbase = smem_u32(smem) + (uint32_t)warp * 2u * STAGEB + (uint32_t)grp * ROWB +
-                           (uint32_t)gl * 16u;
-    BatchCur cur = cur_init(a);
     // row A (being reduced) and row B (in flight) of this group: row pointer,
     // temperature factor, label; row C's gathered index is fetched one pass ahead
     int64_t rowA = g0 * RPW + grp;
     bool actA = rowA < rows;
-    const uint4* pA;
-    float cA;
-    int32_t labA;
-    {
-      const RowSrc r = locate_cur<RIDX>(a, cur, actA ? rowA : 0, actA ? fA : fetch_index_t<RIDX>(a, 0));
-      pA = reinterpret_cast<const uint4*>(r.base + r.src * a.row_bytes);
-      cA = r.c;
-      labA = fetch_label(a, r);
+    if (!(early && !a.late_wait)) {
+      locate_A(actA);
+      group_prefetch_row<NV, G, FULL>(sbase, pA, gl, nvec);
+      cp_async_commit();
+    } else if (!actA) {
+      locate_A(false);                 // the early prefetch assumed a live row: re-aim
     }
-    group_prefetch_row<NV, G, FULL>(sbase, pA, gl, nvec);
-    cp_async_commit();
     int64_t gA = g0;
     int64_t gB = next_group(g0);
     int64_t fB = fetch_index_t<RIDX>(a, gB * RPW + grp < cap ? gB * RPW + grp : 0);
@@ -1116,6 +1143,7 @@ __global__ void __launch_bounds__(kAsyncThreads, 3) conf_async_kernel(const __gr
     }
     cp_async_wait<0>();
   }
+  if constexpr (EARLY) cp_async_wait<0>();     // an early prefetch of a row beyond the live count
   if constexpr (FUSE) {
 #ifndef HS_EXP_FZ_NOSYNC
     cooperative_groups::this_grid().sync();    // every row's confidence, argmax and count

@@ -108,6 +108,10 @@ struct ConfArgs {
   const int64_t* last_ids;
   int64_t* last_ids_out;
   int64_t* last_counts;
+  // the logits hold all n * L * nbatch rows (true without d_n; with d_n the
+  // caller says so, HS_STEP_LOGITS_CAPACITY): dense rows may be read before the
+  // previous kernel's live count is visible
+  int rows_cap_valid;
 };
 // true when launch_confidence(a) takes the cp.async kernel, which is the one
 // that can run the fused threshold test + compaction

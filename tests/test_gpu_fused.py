@@ -234,3 +234,27 @@ def test_last_stage_direct_topk(hs, monkeypatch):
     a = last_step(hs, monkeypatch, True, x, top_k=10)
     b = last_step(hs, monkeypatch, False, x, top_k=10)
     assert_same(a, b)
+
+
+@pytest.mark.parametrize("C,dtype", [(1000, "bf16"), (200, "f32")])
+def test_logits_capacity_flag_early_rows(hs, monkeypatch, C, dtype):
+    """HS_STEP_LOGITS_CAPACITY (set by the binding when the logits memory covers
+    the capacity): dense rows are read before the device count is known; the
+    cascade step equals the one on an exact-sized copy of the live rows (flag
+    off), for several live counts, middle and last stage."""
+    monkeypatch.setenv("HS_FUSE", "0")
+    cap = 100003
+    x = rand_logits(cap, C, dtype, seed=C)
+    g = torch.Generator().manual_seed(3)
+    ids = torch.randperm(4 * cap, generator=g)[:cap].to(torch.int64).to(dev())
+    assert hs._rows_capacity_flag(x, cap, None) == hs.HS_STEP_LOGITS_CAPACITY
+    for live in (cap, 65537, 17, 1, 0):
+        d_n = torch.tensor([live], dtype=torch.int64, device=dev())
+        exact = x[: max(live, 1)].clone()
+        assert hs._rows_capacity_flag(exact, cap, None) == (hs.HS_STEP_LOGITS_CAPACITY if live >= cap else 0)
+        for stage in (1, 2):
+            a = hs.cascade_step(stage, 3, x, 0.4, n=cap, ids=ids, d_n=d_n)
+            b = hs.cascade_step(stage, 3, exact, 0.4, n=cap, ids=ids, d_n=d_n)
+            torch.cuda.synchronize()
+            assert_same(a, b)
+            assert sum(a["counts"].cpu().tolist()) == live
