@@ -49,6 +49,28 @@ __device__ __forceinline__ int64_t draw_tile(CompactWs* ws) {
   return (int64_t)s_t;
 }
 
+// Descriptor accesses: a descriptor is one self-contained 64-bit word (epoch,
+// flag and count together) and no other data is read on its strength -- the
+// lists are consumed by the next kernel -- so relaxed gpu-scope accesses
+// suffice (a release store costs a MEMBAR on the look-back's critical path;
+// HS_AB_K3_ACQREL restores acquire / release for A/B).
+__device__ __forceinline__ unsigned long long desc_ld(const unsigned long long* p) {
+#ifdef HS_AB_K3_ACQREL
+  return ld_acquire(p);
+#else
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+#endif
+}
+__device__ __forceinline__ void desc_st(unsigned long long* p, unsigned long long v) {
+#ifdef HS_AB_K3_ACQREL
+  st_release(p, v);
+#else
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+#endif
+}
+
 __device__ __forceinline__ unsigned desc_flag(unsigned long long d, unsigned epoch) {
   return (unsigned)(d >> 32) == epoch ? (unsigned)((d >> 30) & 3u) : 0u;   // 0 = not ready
 }
@@ -155,15 +177,15 @@ __global__ void __launch_bounds__(kCompactThreads) route_compact_kernel(const Co
       // ---- decoupled look-back for the deferred count before this tile
       long long excl = 0;
       if (tile == 0) {
-        if (lane == 0) st_release(&st[0], etag | kFlagP | (unsigned long long)agg);
+        if (lane == 0) desc_st(&st[0], etag | kFlagP | (unsigned long long)agg);
       } else {
-        if (lane == 0) st_release(&st[tile], etag | kFlagA | (unsigned long long)agg);
+        if (lane == 0) desc_st(&st[tile], etag | kFlagA | (unsigned long long)agg);
         int64_t pred = tile - 1;
         while (true) {
           const int64_t idx = pred - lane;
-          unsigned long long d = (idx >= 0) ? ld_acquire(&st[idx]) : (etag | kFlagP);
+          unsigned long long d = (idx >= 0) ? desc_ld(&st[idx]) : (etag | kFlagP);
           while (__any_sync(0xFFFFFFFFu, desc_flag(d, epoch) == 0)) {
-            if (desc_flag(d, epoch) == 0) d = ld_acquire(&st[idx]);
+            if (desc_flag(d, epoch) == 0) d = desc_ld(&st[idx]);
           }
           const unsigned pm = __ballot_sync(0xFFFFFFFFu, desc_flag(d, epoch) == 2);
           long long val = (long long)(d & kValMask);
@@ -175,7 +197,7 @@ __global__ void __launch_bounds__(kCompactThreads) route_compact_kernel(const Co
           excl += warp_sum(val);
           pred -= 32;
         }
-        if (lane == 0) st_release(&st[tile], etag | kFlagP | (unsigned long long)(excl + agg));
+        if (lane == 0) desc_st(&st[tile], etag | kFlagP | (unsigned long long)(excl + agg));
       }
       if (lane == 0 && tile == ntiles - 1) {
         // the last tile knows the totals; it also retires this launch's epoch
@@ -352,15 +374,15 @@ __global__ void __launch_bounds__(T) route_compact_fast_kernel(const CompactArgs
     const long long agg = __shfl_sync(0xFFFFFFFFu, wi, NW - 1);
     long long excl = 0;
     if (tile == 0) {
-      if (lane == 0) st_release(&st[0], etag | kFlagP | (unsigned long long)agg);
+      if (lane == 0) desc_st(&st[0], etag | kFlagP | (unsigned long long)agg);
     } else {
-      if (lane == 0) st_release(&st[tile], etag | kFlagA | (unsigned long long)agg);
+      if (lane == 0) desc_st(&st[tile], etag | kFlagA | (unsigned long long)agg);
       int64_t pred = tile - 1;
       while (true) {
         const int64_t idx = pred - lane;
-        unsigned long long d = (idx >= 0) ? ld_acquire(&st[idx]) : (etag | kFlagP);
+        unsigned long long d = (idx >= 0) ? desc_ld(&st[idx]) : (etag | kFlagP);
         while (__any_sync(0xFFFFFFFFu, desc_flag(d, epoch) == 0)) {
-          if (desc_flag(d, epoch) == 0) d = ld_acquire(&st[idx]);
+          if (desc_flag(d, epoch) == 0) d = desc_ld(&st[idx]);
         }
         const unsigned pm = __ballot_sync(0xFFFFFFFFu, desc_flag(d, epoch) == 2);
         const long long val = (long long)(d & kValMask);
@@ -372,7 +394,7 @@ __global__ void __launch_bounds__(T) route_compact_fast_kernel(const CompactArgs
         excl += warp_sum(val);
         pred -= 32;
       }
-      if (lane == 0) st_release(&st[tile], etag | kFlagP | (unsigned long long)(excl + agg));
+      if (lane == 0) desc_st(&st[tile], etag | kFlagP | (unsigned long long)(excl + agg));
     }
     if (lane == 0) {
       if (tile == ntiles - 1) {
