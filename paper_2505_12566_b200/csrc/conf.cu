@@ -1942,6 +1942,9 @@ cudaError_t dispatch(const ConfArgs& a, int64_t rows, cudaStream_t s) {
   if (nvec <= 16) return launch_warp<BF16, ENTROPY, 4, 4>(a, rows, s);
   if (nvec <= 32) return launch_warp<BF16, ENTROPY, 8, 4>(a, rows, s);
   if (nvec <= 64) return launch_warp<BF16, ENTROPY, 8, 8>(a, rows, s);
+#ifdef HS_AB_K1A_G32
+  if (nvec <= 128) return launch_warp<BF16, ENTROPY, 4, 32>(a, rows, s);   // A/B: one row per warp
+#endif
   if (nvec <= 128) return launch_warp<BF16, ENTROPY, 8, 16>(a, rows, s);
   if (nvec <= 256) return launch_warp<BF16, ENTROPY, 16, 16>(a, rows, s);
   if (nvec <= 512) return launch_warp<BF16, ENTROPY, 16, 32>(a, rows, s);

@@ -26,7 +26,8 @@ VARIANTS = {
     "topkm4s40": ["HS_TOPK_MERGE_AT=4", "HS_TOPK_SLACK=40"],   # + 40 more buffered slots per lane
     "topkm8s40": ["HS_TOPK_MERGE_AT=8", "HS_TOPK_SLACK=40"],
     "noearly": ["HS_AB_NO_EARLY"],
-    "k3acqrel": ["HS_AB_K3_ACQREL"],     # K3 look-back descriptors with acquire / release       # K1a: no first-row prefetch before the PDL wait
+    "k3acqrel": ["HS_AB_K3_ACQREL"],
+    "k1g32": ["HS_AB_K1A_G32"],          # K1a for C <= 1,024 bf16: one row per warp (32 lanes x 4 vectors)     # K3 look-back descriptors with acquire / release       # K1a: no first-row prefetch before the PDL wait
     "fznofin": ["HS_EXP_FZ_NOFINISH"],   # fused step timing bounds: grid barrier, no lists ...
     "fznosync": ["HS_EXP_FZ_NOSYNC"],    # ... no barrier either (K1 + tile counters only)
 }
