@@ -13,8 +13,8 @@
 // it, so the look-back makes progress whatever order the hardware dispatches
 // CTAs in and however many are resident (the CTA drawing the last ticket
 // re-arms the counter for the next launch).
-// Descriptors are 64-bit {epoch:32 | flag:2 | count:30}, written with
-// st.release and read with ld.acquire at gpu scope; the epoch (bumped by the
+// Descriptors are 64-bit {epoch:32 | flag:2 | count:30}, written and read
+// with relaxed gpu-scope accesses (self-contained words); the epoch (bumped by the
 // last tile of every launch) makes stale descriptors from earlier launches
 // read as "not ready", so there is no reset pass and no memset between calls.
 #include <cstdlib>
