@@ -214,3 +214,35 @@ def test_c_program_routes_a_cascade_on_the_gpu(libhs, tmp_path):
     import subprocess
     r = subprocess.run([_build_c_client(tmp_path), "--gpu"], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0 and "c client ok" in r.stdout, r.stdout + r.stderr
+
+
+def test_step_flags_validated_before_any_launch(libhs):
+    """hs_cascade_step_ex / hs_cascade_confidence reject unknown flag bits
+    synchronously (HS_STEP_OVERLAP_PREVIOUS = 1 and HS_STEP_LOGITS_CAPACITY = 2
+    are the only ones), before touching the device."""
+    lib = libhs.lib()
+    rc = lib.hs_cascade_step_ex(0, 3, 256, 1, 10, 1, 1000, 1000, None, None, 1.0, 0, 0, 0.5, None,
+                                None, None, 0, None, None, None, None, None, 512, 1024, 1 << 20,
+                                None, 0, 4, None)
+    assert rc == 1 and "flags" in lib.hs_last_error().decode()
+    rc = lib.hs_cascade_confidence(0, 3, 256, 1, 10, 1, 1000, 1000, None, None, 1.0, 0, 0, 0.5, None,
+                                   None, 1024, 1 << 20, None, 0, 8, None)
+    assert rc == 1 and "flags" in lib.hs_last_error().decode()
+
+
+def test_logits_capacity_flag_from_storage(libhs):
+    """The binding sets HS_STEP_LOGITS_CAPACITY exactly when the memory from the
+    logits' first row on covers the capacity (a view of the live rows of a
+    capacity-sized buffer), never for gathered rows."""
+    import torch
+    buf = torch.zeros(1000, 64, dtype=torch.bfloat16)
+    cap = libhs.HS_STEP_LOGITS_CAPACITY
+    assert libhs._rows_capacity_flag(buf, 1000, None) == cap
+    assert libhs._rows_capacity_flag(buf[:10], 1000, None) == cap       # view: storage covers 1,000 rows
+    assert libhs._rows_capacity_flag(buf[10:20], 1000, None) == 0       # starts 10 rows in
+    assert libhs._rows_capacity_flag(buf[:10].clone(), 1000, None) == 0  # exact-sized copy
+    assert libhs._rows_capacity_flag(buf[:10].clone(), 10, None) == cap
+    assert libhs._rows_capacity_flag(buf, 1000, torch.zeros(5, dtype=torch.int64)) == 0
+    padded = torch.zeros(100, 80, dtype=torch.float32)[:, :64]          # stride 80 > C
+    assert libhs._rows_capacity_flag(padded, 100, None) == cap
+    assert libhs._rows_capacity_flag(padded, 101, None) == 0
