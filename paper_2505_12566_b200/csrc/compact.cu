@@ -528,15 +528,31 @@ cudaError_t launch_route_compact(const CompactArgs& a, cudaStream_t s) {
   const bool fast = !a.sel_dest && !a.skip_dest && (!a.acc_pred || a.pred_len == 1);
   if (fast) {
     const int vec = aligned16(a.conf) && aligned16(a.ids) && (!a.acc_pred || aligned16(a.pred));
-    static const bool big_ok = [] {
-      return cudaFuncSetAttribute(route_compact_fast_kernel<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  1024 * kFastItems * 16) == cudaSuccess;
+    // tile size (A/B on one box, five-stage C2 step in a graph): 4,096 items
+    // (512 threads, 64 KB staging) 323.8 us; 8,192 items (1,024 threads, 128 KB)
+    // 338.4 us; 2,048 items (256 threads) 360.3 us.  The 128 KB CTAs hold SM
+    // slots the next stage's K1 needs while it launches early; the 2,048-item
+    // grid is 4x larger.  HS_COMPACT_TILES=8192 / 2048 select the others.
+    static const int tiles_env = [] {
+      const char* e = getenv("HS_COMPACT_TILES");
+      if (getenv("HS_COMPACT_SMALL_TILES") && getenv("HS_COMPACT_SMALL_TILES")[0] == '1') return 2048;
+      return e ? atoi(e) : 4096;
     }();
-    static const bool off = getenv("HS_COMPACT_SMALL_TILES") && getenv("HS_COMPACT_SMALL_TILES")[0] == '1';
-    if (big_ok && !off && a.n >= 4 * 1024 * kFastItems) {   // >= 4 big tiles
+    static const bool mid_ok = cudaFuncSetAttribute(route_compact_fast_kernel<512>,
+                                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                    512 * kFastItems * 16) == cudaSuccess;
+    static const bool big_ok = cudaFuncSetAttribute(route_compact_fast_kernel<1024>,
+                                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                    1024 * kFastItems * 16) == cudaSuccess;
+    if (tiles_env == 8192 && big_ok && a.n >= 4 * 1024 * kFastItems) {   // >= 4 tiles
       const int64_t bt = (a.n + 1024 * kFastItems - 1) / (1024 * kFastItems);
       return launch_pdl(route_compact_fast_kernel<1024>, dim3((unsigned)bt), dim3(1024),
                         (size_t)1024 * kFastItems * 16, s, a, vec);
+    }
+    if (tiles_env == 4096 && mid_ok && a.n >= 4 * 512 * kFastItems) {
+      const int64_t mt = (a.n + 512 * kFastItems - 1) / (512 * kFastItems);
+      return launch_pdl(route_compact_fast_kernel<512>, dim3((unsigned)mt), dim3(512),
+                        (size_t)512 * kFastItems * 16, s, a, vec);
     }
     return launch_pdl(route_compact_fast_kernel<256>, dim3(grid), dim3(256), (size_t)256 * kFastItems * 16, s,
                       a, vec);
