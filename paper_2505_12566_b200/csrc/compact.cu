@@ -264,10 +264,11 @@ static_assert(kFastItems * kCompactThreads == kCompactTile, "one tile per CTA");
 // (8,192-item tiles: 4x fewer tiles, so the look-back that decides the
 // kernel's latency crosses 4x fewer descriptors; the split is staged in
 // dynamic shared memory, 16 B per item).
-template <int T>
+template <int T, int I = kFastItems>
 __global__ void __launch_bounds__(T) route_compact_fast_kernel(const CompactArgs a, int vec) {
   pdl_start();
-  constexpr int I = kFastItems, NW = T / 32, TILE = T * kFastItems;
+  constexpr int NW = T / 32, TILE = T * I;
+  static_assert(I % 4 == 0 && I <= 32, "items per thread: 128-bit loads, one mask word");
   static_assert(NW <= 32, "one warp scans the warp offsets");
   extern __shared__ __align__(16) long long s_dyn[];
   long long* s_id = s_dyn;             // accepted ids [0, A_t), deferred ids [A_t, tn)
@@ -293,9 +294,11 @@ __global__ void __launch_bounds__(T) route_compact_fast_kernel(const CompactArgs
   auto load = [&](int64_t i0) {
     if (vec && i0 + I <= ncap) {
       const float4* c4 = reinterpret_cast<const float4*>(a.conf + i0);
-      const float4 x0 = __ldg(c4), x1 = __ldg(c4 + 1);
-      cv[0] = x0.x; cv[1] = x0.y; cv[2] = x0.z; cv[3] = x0.w;
-      cv[4] = x1.x; cv[5] = x1.y; cv[6] = x1.z; cv[7] = x1.w;
+#pragma unroll
+      for (int q = 0; q < I / 4; ++q) {
+        const float4 x = __ldg(c4 + q);
+        cv[4 * q] = x.x; cv[4 * q + 1] = x.y; cv[4 * q + 2] = x.z; cv[4 * q + 3] = x.w;
+      }
       if (a.ids) {
         const longlong2* q = reinterpret_cast<const longlong2*>(a.ids + i0);
 #pragma unroll
@@ -310,9 +313,11 @@ __global__ void __launch_bounds__(T) route_compact_fast_kernel(const CompactArgs
       }
       if (pred1) {
         const int4* q = reinterpret_cast<const int4*>(a.pred + i0);
-        const int4 p0 = __ldg(q), p1 = __ldg(q + 1);
-        pv[0] = p0.x; pv[1] = p0.y; pv[2] = p0.z; pv[3] = p0.w;
-        pv[4] = p1.x; pv[5] = p1.y; pv[6] = p1.z; pv[7] = p1.w;
+#pragma unroll
+        for (int k = 0; k < I / 4; ++k) {
+          const int4 x = __ldg(q + k);
+          pv[4 * k] = x.x; pv[4 * k + 1] = x.y; pv[4 * k + 2] = x.z; pv[4 * k + 3] = x.w;
+        }
       } else {
 #pragma unroll
         for (int j = 0; j < I; ++j) pv[j] = 0;
@@ -548,6 +553,17 @@ cudaError_t launch_route_compact(const CompactArgs& a, cudaStream_t s) {
       const int64_t bt = (a.n + 1024 * kFastItems - 1) / (1024 * kFastItems);
       return launch_pdl(route_compact_fast_kernel<1024>, dim3((unsigned)bt), dim3(1024),
                         (size_t)1024 * kFastItems * 16, s, a, vec);
+    }
+    static const bool t256 = [] {    // A/B: 4,096-item tiles from 256 threads x 16 items
+      const char* e = getenv("HS_COMPACT_T256");
+      return e && e[0] == '1' &&
+             cudaFuncSetAttribute(route_compact_fast_kernel<256, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  256 * 16 * 16) == cudaSuccess;
+    }();
+    if (t256 && a.n >= 4 * 4096) {
+      const int64_t mt = (a.n + 4095) / 4096;
+      return launch_pdl(route_compact_fast_kernel<256, 16>, dim3((unsigned)mt), dim3(256), (size_t)256 * 16 * 16,
+                        s, a, vec);
     }
     if (tiles_env == 4096 && mid_ok && a.n >= 4 * 512 * kFastItems) {
       const int64_t mt = (a.n + 512 * kFastItems - 1) / (512 * kFastItems);
